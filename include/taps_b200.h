@@ -197,11 +197,19 @@ tp_status tp_plan_upload(tp_plan* plan, void* stream);
  * detected by the kernels are reported by tp_plan_check_errors(). */
 tp_status tp_plan_execute(tp_plan* plan, const tp_build_opts* opts,
                           tp_cost_tensors* device_out);
+/* Run the kernels and copy the requested tensors back into HOST pointers
+ * (the one-shot call on an existing plan; synchronous). */
+tp_status tp_plan_execute_host(tp_plan* plan, const tp_build_opts* opts,
+                               tp_aux_index* index_out, tp_cost_tensors* host_out);
 /* Synchronise the plan's stream and turn a kernel-flagged error into a
  * status (and tp_last_error message). */
 tp_status tp_plan_check_errors(tp_plan* plan);
 /* Number of kernel launches the last execute issued. */
 int64_t tp_plan_last_launches(const tp_plan* plan);
+/* Optional cudaEvent_t pair recorded on the launch stream immediately before
+ * and after the fan-out kernel (K4) of every execute; NULL disables. Used by
+ * bench.py to time the dominant kernel live for the roofline. */
+tp_status tp_plan_set_profile_events(tp_plan* plan, void* start_event, void* stop_event);
 
 /* Strategy table of an operator with p axes on N devices, in the reference's
  * enumeration order (layout.hpp:270-328), produced on the device.

@@ -210,8 +210,12 @@ def load_engine() -> C.CDLL:
     lib.tp_plan_upload.restype = C.c_int
     lib.tp_plan_execute.argtypes = [C.c_void_p, P(tp_build_opts), P(tp_cost_tensors)]
     lib.tp_plan_execute.restype = C.c_int
+    lib.tp_plan_execute_host.argtypes = [C.c_void_p, P(tp_build_opts), P(tp_aux_index), P(tp_cost_tensors)]
+    lib.tp_plan_execute_host.restype = C.c_int
     lib.tp_plan_check_errors.argtypes = [C.c_void_p]
     lib.tp_plan_check_errors.restype = C.c_int
+    lib.tp_plan_set_profile_events.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.tp_plan_set_profile_events.restype = C.c_int
     lib.tp_plan_last_launches.argtypes = [C.c_void_p]
     lib.tp_plan_last_launches.restype = C.c_int64
     lib.tp_enumerate_strategies.argtypes = [C.c_int32, C.c_int64, P(C.c_int64), _p_i64, _p_i32,
@@ -232,8 +236,8 @@ def load_engine() -> C.CDLL:
 # Every symbol include/taps_b200.h declares (checked by the CPU test suite).
 EXPORTED_SYMBOLS = (
     "tp_build_cost_tensors", "tp_plan_create", "tp_plan_destroy", "tp_plan_sizes",
-    "tp_plan_index", "tp_plan_upload", "tp_plan_execute", "tp_plan_check_errors",
-    "tp_plan_last_launches", "tp_enumerate_strategies", "tp_redistribute_batch",
+    "tp_plan_index", "tp_plan_upload", "tp_plan_execute", "tp_plan_execute_host", "tp_plan_check_errors",
+    "tp_plan_last_launches", "tp_plan_set_profile_events", "tp_enumerate_strategies", "tp_redistribute_batch",
     "tp_last_error", "tp_last_error_kind", "tp_abi_version",
 )
 

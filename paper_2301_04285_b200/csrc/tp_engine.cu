@@ -1,0 +1,1400 @@
+// tp_engine.cu — B200 (sm_100a) cost-tensor engine behind include/taps_b200.h.
+//
+// Replaces topoplan::build_auxiliary_graph (aux_graph.hpp:211-315).
+// Pipeline of one build (all on one stream):
+//   K1 table_kernel   strategy tables, one thread per strategy (unranking)
+//   K2 node_kernel    one thread per aux node: divisibility, intra-operator
+//                     AllReduce cost/volume, memory (aux_graph.hpp:120-167)
+//   K3 pair_kernel    one thread per (edge class, su, sw): unify + sequence
+//                     inference + topology-aware pricing (tp_core.cuh)
+//   K4 expand_kernel  write-bound fan-out of the class tables to every aux
+//                     edge: cost = intra(w) + redist, 256-bit stores
+//   K5 rowmin_kernel  (optional) warp per (edge, su) row, lanes over sw,
+//                     shuffle min: the solver's cond_min (solver.hpp:239-253)
+//
+// Edges are grouped into *classes* on the host: two graph edges whose
+// (shape, producer slicing, consumer slicing, axis counts, tensor bytes)
+// agree have identical |Su| x |Sw| redistribution tables, so each class is
+// priced once (the reference's memo, aux_graph.hpp:257-271, made static).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/taps_b200.h"
+#include "tp_core.cuh"
+
+using tpk::DimT;
+using tpk::Env;
+using tpk::Lay;
+using tpk::Strat;
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+thread_local std::string g_err;
+thread_local int g_err_kind = 0;
+
+tp_status set_err(tp_status st, int kind, const std::string& msg) {
+  g_err = msg;
+  g_err_kind = kind;
+  return st;
+}
+
+tp_status status_of_kind(int kind) {
+  if (kind == tpk::kOk) return TP_OK;
+  if (kind == tpk::kEdgeTensorMissing) return TP_ERR_OUT_OF_RANGE;
+  if (kind == tpk::kCapacity) return TP_ERR_CAPACITY;
+  return TP_ERR_TOPOPLAN;
+}
+
+const char* kind_text(int kind) {
+  switch (kind) {
+    case tpk::kCycle: return "build_auxiliary_graph: graph has a cycle";
+    case tpk::kDangling: return "auxiliary graph: dangling edge";
+    case tpk::kNotPow2: return "enumerate_strategies: device count must be a power of two";
+    case tpk::kNoAxes: return "enumerate_strategies: operator has no axes";
+    case tpk::kUnknownSliceTensor: return "axis references unknown tensor";
+    case tpk::kIndivisible: return "extent is not divisible by the axis degree";
+    case tpk::kShapeMismatch: return "unify_layouts: layouts describe different tensor shapes";
+    case tpk::kNotUnifiable: return "device matrices are not unifiable";
+    case tpk::kFactorization: return "extent not divisible during device-matrix factorization";
+    case tpk::kRefine: return "tensor extent not divisible during shape unification";
+    case tpk::kDeviceSplit: return "tensor extent not divisible during device split";
+    case tpk::kNoConverge: return "unify_layouts failed to converge";
+    case tpk::kRefineMismatch: return "unify_layouts: internal refinement mismatch";
+    case tpk::kDeadlock: return "redistribution deadlock: no gatherable axis";
+    case tpk::kNoTerminate: return "redistribution failed to terminate";
+    case tpk::kEdgeTensorMissing: return "map::at (edge tensor absent from an endpoint)";
+    case tpk::kCapacity: return "input exceeds a fixed engine bound";
+    default: return "error";
+  }
+}
+
+#define CUDA_TRY(expr)                                                        \
+  do {                                                                        \
+    cudaError_t _e = (expr);                                                  \
+    if (_e != cudaSuccess)                                                    \
+      return set_err(TP_ERR_CUDA, 0, std::string(#expr ": ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+// Error keys: (order << 6) | kind; the smallest key is the error the
+// reference would throw first (its iteration order).
+constexpr uint64_t kEdgePhase = 1ull << 46;
+__host__ __device__ inline uint64_t ekey(uint64_t order, int kind) { return (order << 6) | (uint64_t)kind; }
+
+// ---------------------------------------------------------------------------
+// device descriptors
+// ---------------------------------------------------------------------------
+struct OpDesc {
+  int64_t node_base;
+  int32_t table;  // entry offset of the op's strategy table
+  int32_t p;
+  int32_t chk_begin, chk_end;
+  int32_t occ_begin, occ_end;
+  int32_t slot_begin;
+  int32_t pad;
+};
+
+struct SliceChk {
+  int16_t slot;  // -1: the slice names a tensor the op does not carry
+  int8_t axis;
+  int8_t v;      // 2-adic valuation of the sliced extent (capped at 63)
+};
+
+struct SlotDesc {
+  int64_t elements;
+  int32_t es;
+  int8_t R;
+  int8_t sa[tpk::kMaxR];
+  int8_t pad[3];
+};
+
+struct Occ {
+  int16_t slot;
+  uint8_t nonslicing;  // axes with no slice naming this tensor
+  uint8_t in_memory;   // output, or input not fed by an edge
+};
+
+struct SigDesc {
+  int64_t pair_begin;
+  int64_t first_aux;  // aux id of (su=0, sw=0) of the class's first edge
+  double bytes;
+  int32_t R, Su, Sw, tab_u, tab_w, has_override;
+  int8_t sa_u[tpk::kMaxR];
+  int8_t sa_w[tpk::kMaxR];
+  DimT dt[tpk::kMaxR];
+};
+
+struct EdgeDesc {
+  int64_t aux_base;  // aux id of the edge's (0, 0)
+  int64_t nb_u, nb_w;
+  double indeg_w;
+  int32_t sig, e;
+};
+
+struct Work {
+  int32_t sig;
+  int32_t ebeg, eend;  // into sig_edges
+  int32_t pad;
+  int64_t j0;          // first pair of the tile within the class block
+};
+
+struct TableDesc {
+  int64_t offset, count;
+  int32_t p, n;
+};
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void flag_error(unsigned long long* err, uint64_t key) {
+  atomicMin(err, (unsigned long long)key);
+}
+
+__global__ void table_kernel(const TableDesc* __restrict__ tabs, int ntabs, int64_t total,
+                             Strat* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  int t = 0;
+  while (t + 1 < ntabs && tabs[t + 1].offset <= i) ++t;
+  Strat s;
+  tpk::unrank_strategy(tabs[t].p, tabs[t].n, i - tabs[t].offset, s);
+  out[i] = s;
+}
+
+__global__ void __launch_bounds__(256) node_kernel(
+    const OpDesc* __restrict__ ops, int nops, int64_t total_nodes, int n_log2, Env env,
+    const Strat* __restrict__ tables, const SliceChk* __restrict__ chks,
+    const SlotDesc* __restrict__ slots, const Occ* __restrict__ occs, double* __restrict__ o_sec,
+    double* __restrict__ o_vol, double* __restrict__ o_mem, double* __restrict__ c_sec,
+    double* __restrict__ c_vol, double* __restrict__ c_mem, unsigned long long* err) {
+  const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= total_nodes) return;
+  int lo = 0, hi = nops - 1;  // last op with node_base <= node
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (ops[mid].node_base <= node) lo = mid; else hi = mid - 1;
+  }
+  const OpDesc od = ops[lo];
+  const Strat st = tables[od.table + (node - od.node_base)];
+  // layout.hpp:349-367: every slice in axis order must divide
+  for (int c = od.chk_begin; c < od.chk_end; ++c) {
+    const SliceChk k = chks[c];
+    int kind = 0;
+    if (k.slot < 0) kind = tpk::kUnknownSliceTensor;
+    else if (st.deg[k.axis] > k.v) kind = tpk::kIndivisible;
+    if (kind) {
+      flag_error(err, ekey(1 + (uint64_t)node * 2 + 1, kind));
+      o_sec[node] = o_vol[node] = o_mem[node] = 0;
+      return;
+    }
+  }
+  double sec = 0, vol = 0, mem = 0;
+  for (int q = od.occ_begin; q < od.occ_end; ++q) {
+    const Occ oc = occs[q];
+    const SlotDesc sd = slots[od.slot_begin + oc.slot];
+    int sdiv = 0;
+    for (int d = 0; d < sd.R; ++d)
+      if (sd.sa[d] >= 0) sdiv += st.deg[sd.sa[d]];
+    const int64_t shard_el = sdiv >= 63 ? 0 : (sd.elements >> sdiv);
+    const double sb = (double)shard_el * sd.es;  // layout.hpp:127-129
+    if (oc.in_memory) mem += sb;                 // aux_graph.hpp:151-167
+    int glog = 0;
+    for (int a = 0; a < od.p; ++a)
+      if ((oc.nonslicing >> a) & 1) glog += st.deg[a];
+    if (glog == 0) continue;  // group <= 1
+    // infer_ct_allreduce (cost_model.hpp:75-97)
+    const int64_t pd = sdiv > n_log2 ? 0 : ((int64_t)1 << (n_log2 - sdiv));
+    int64_t remain = env.local, dev_in = 1;
+    for (int k = 0; k < st.depth; ++k) {
+      bool contains = false;
+      for (int d = 0; d < sd.R; ++d)
+        contains |= sd.sa[d] >= 0 && st.dmap[sd.sa[d]] == k;
+      const int64_t ek = (int64_t)1 << st.mx[k];
+      if (!contains && remain > 1) dev_in *= remain > ek ? ek : remain;
+      remain /= ek;
+    }
+    const int64_t ct = dev_in >= pd ? 0 : (dev_in > 1 ? env.local / dev_in : env.local);
+    const double n = (double)((int64_t)1 << glog);
+    const double v = 2.0 * (n - 1) / n * sb;  // allreduce_volume, cost_model.hpp:39-43
+    vol += v;
+    sec += v / tpk::eff_bw(ct, env);
+  }
+  o_sec[node] = sec;
+  o_vol[node] = vol;
+  o_mem[node] = mem;
+  if (c_sec) c_sec[node] = sec;
+  if (c_vol) c_vol[node] = vol;
+  if (c_mem) c_mem[node] = mem;
+}
+
+__global__ void __launch_bounds__(128) pair_kernel(
+    const SigDesc* __restrict__ sigs, int nsigs, int64_t total_pairs, Env env,
+    const Strat* __restrict__ tables, const double* __restrict__ overrides,
+    double* __restrict__ r_sec, double* __restrict__ r_vol, unsigned long long* err) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total_pairs) return;
+  int lo = 0, hi = nsigs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (sigs[mid].pair_begin <= idx) lo = mid; else hi = mid - 1;
+  }
+  const SigDesc& sg = sigs[lo];
+  const int64_t local = idx - sg.pair_begin;
+  const int64_t su = local / sg.Sw, sw = local - su * sg.Sw;
+  const Strat a = tables[sg.tab_u + su];
+  const Strat b = tables[sg.tab_w + sw];
+  Lay F, T;
+  tpk::side_layout(a, sg.sa_u, sg.R, F);
+  tpk::side_layout(b, sg.sa_w, sg.R, T);
+  double sec = 0, vol = 0;
+  if (!tpk::same_layout(F, T, sg.R)) {
+    const double bytes = sg.has_override ? overrides[idx] : sg.bytes;
+    const int st = tpk::redist_cost_any(sg.R, F, T, sg.dt, bytes, env, sec, vol, nullptr);
+    if (st) {
+      flag_error(err, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
+      sec = vol = 0;
+    }
+  }
+  r_sec[idx] = sec;
+  r_vol[idx] = vol;
+}
+
+constexpr int kExpThreads = 256;
+constexpr int kExpTile = kExpThreads * 4;  // class pairs per CTA tile
+constexpr int kExpMaxSw = 1024;            // node rows staged in smem up to this width
+
+__device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kExpThreads) expand_kernel(
+    const Work* __restrict__ work, const SigDesc* __restrict__ sigs,
+    const int32_t* __restrict__ sig_edges, const EdgeDesc* __restrict__ edges,
+    const double* __restrict__ r_sec, const double* __restrict__ r_vol,
+    const double* __restrict__ n_sec, const double* __restrict__ n_vol,
+    const double* __restrict__ n_mem, int64_t out_offset, double* __restrict__ e_sec,
+    double* __restrict__ e_vol, double* __restrict__ e_mem, char* __restrict__ records) {
+  __shared__ double rs[kExpTile + 8], rv[kExpTile + 8];
+  __shared__ double is_[kExpMaxSw], iv_[kExpMaxSw], im_[kExpMaxSw];
+  const Work wk = work[blockIdx.x];
+  const SigDesc& sg = sigs[wk.sig];
+  const int64_t Sw = sg.Sw;
+  const int64_t P = (int64_t)sg.Su * Sw;
+  const int64_t j0 = wk.j0;
+  const int64_t j1 = min(j0 + (int64_t)kExpTile, P);
+  // class-table tile [j0-4, j1+4) into smem (reused for every edge of the chunk)
+  for (int64_t j = j0 - 4 + threadIdx.x; j < j1 + 4; j += kExpThreads) {
+    const bool ok = j >= 0 && j < P;
+    rs[j - (j0 - 4)] = ok ? r_sec[sg.pair_begin + j] : 0.0;
+    rv[j - (j0 - 4)] = ok ? r_vol[sg.pair_begin + j] : 0.0;
+  }
+  const bool staged = Sw <= kExpMaxSw;
+  for (int ei = wk.ebeg; ei < wk.eend; ++ei) {
+    const EdgeDesc ed = edges[sig_edges[ei]];
+    if (staged) {
+      for (int64_t s = threadIdx.x; s < Sw; s += kExpThreads) {
+        is_[s] = n_sec[ed.nb_w + s];
+        iv_[s] = n_vol[ed.nb_w + s];
+        im_[s] = n_mem[ed.nb_w + s] / ed.indeg_w;  // aux_graph.hpp:292
+      }
+    }
+    __syncthreads();
+    const int64_t ob = ed.aux_base - out_offset;  // output index of pair 0
+    const int64_t g0 = (ob + j0) & ~(int64_t)3;
+    for (int64_t a = g0 + 4 * (int64_t)threadIdx.x; a < ob + j1; a += 4 * kExpThreads) {
+      const int64_t jq = a - ob;
+      int64_t sw = jq % Sw;
+      if (sw < 0) sw += Sw;
+      double c[4], v[4], m[4];
+      bool ok[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t j = jq + q;
+        ok[q] = j >= j0 && j < j1;
+        double ws, wv, wm;
+        if (staged) {
+          ws = is_[sw];
+          wv = iv_[sw];
+          wm = im_[sw];
+        } else {
+          ws = n_sec[ed.nb_w + sw];
+          wv = n_vol[ed.nb_w + sw];
+          wm = n_mem[ed.nb_w + sw] / ed.indeg_w;
+        }
+        const int64_t t = (ok[q] ? j : j0) - (j0 - 4);
+        c[q] = ws + rs[t];  // aux_graph.hpp:290-291
+        v[q] = wv + rv[t];
+        m[q] = wm;
+        if (++sw == Sw) sw = 0;
+      }
+      if (ok[0] && ok[3]) {
+        if (e_sec) st_v4(e_sec + a, c[0], c[1], c[2], c[3]);
+        if (e_vol) st_v4(e_vol + a, v[0], v[1], v[2], v[3]);
+        if (e_mem) st_v4(e_mem + a, m[0], m[1], m[2], m[3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (!ok[q]) continue;
+          if (e_sec) e_sec[a + q] = c[q];
+          if (e_vol) e_vol[a + q] = v[q];
+          if (e_mem) e_mem[a + q] = m[q];
+        }
+      }
+      if (records) {  // topoplan::AuxEdge, 40 bytes (aux_graph.hpp:52-59)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (!ok[q]) continue;
+          const int64_t j = jq + q;
+          const int64_t su = j / Sw, swq = j - su * Sw;
+          char* rec = records + (a + q) * 40;
+          // 40*i is only 8-byte aligned: two 8-byte stores for the int header
+          *reinterpret_cast<int2*>(rec) = make_int2(ed.e, (int)(ed.nb_u + su));
+          *reinterpret_cast<int2*>(rec + 8) = make_int2((int)(ed.nb_w + swq), 0);
+          *reinterpret_cast<double*>(rec + 16) = c[q];
+          *reinterpret_cast<double*>(rec + 24) = v[q];
+          *reinterpret_cast<double*>(rec + 32) = m[q];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// cond_min (solver.hpp:239-253): warp per (edge, su) row, lanes over sw.
+__global__ void rowmin_kernel(const EdgeDesc* __restrict__ edges, const int64_t* __restrict__ row_base,
+                              int nedges, int64_t nrows, const SigDesc* __restrict__ sigs,
+                              const double* __restrict__ r_sec, const double* __restrict__ r_vol,
+                              const double* __restrict__ n_sec, const double* __restrict__ n_vol,
+                              double* __restrict__ out_c, double* __restrict__ out_v) {
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= nrows) return;
+  int lo = 0, hi = nedges - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (row_base[mid] <= row) lo = mid; else hi = mid - 1;
+  }
+  const EdgeDesc ed = edges[lo];
+  const SigDesc& sg = sigs[ed.sig];
+  const int64_t su = row - row_base[lo];
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  double mc = inf, mv = inf;
+  for (int64_t sw = lane; sw < sg.Sw; sw += 32) {
+    const int64_t j = sg.pair_begin + su * sg.Sw + sw;
+    const double c = n_sec[ed.nb_w + sw] + r_sec[j];
+    const double v = n_vol[ed.nb_w + sw] + r_vol[j];
+    mc = c < mc ? c : mc;
+    mv = v < mv ? v : mv;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double oc = __shfl_xor_sync(0xffffffffu, mc, off);
+    const double ov = __shfl_xor_sync(0xffffffffu, mv, off);
+    mc = oc < mc ? oc : mc;
+    mv = ov < mv ? ov : mv;
+  }
+  if (lane == 0) {
+    out_c[row] = mc;
+    out_v[row] = mv;
+  }
+}
+
+__global__ void query_kernel(const tpk::QueryPOD* __restrict__ q, int n, tp_redist_result* __restrict__ r) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  tp_redist_result res;
+  res.status = tpk::run_query(q[i], res);
+  r[i] = res;
+}
+
+// ---------------------------------------------------------------------------
+// device memory helper
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes < 256 ? 256 : bytes;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+template <typename T>
+cudaError_t upload(DevBuf& b, const std::vector<T>& v, cudaStream_t s) {
+  cudaError_t e = b.ensure(v.size() * sizeof(T) + 16);
+  if (e != cudaSuccess || v.empty()) return e;
+  return cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+}
+
+int log2_floor(int64_t v) {
+  int e = 0;
+  while (((int64_t)1 << (e + 1)) <= v) ++e;
+  return e;
+}
+
+int v2_capped(int64_t v) {
+  int t = 0;
+  while (t < 63 && !((v >> t) & 1)) ++t;
+  return t;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// the plan
+// ---------------------------------------------------------------------------
+// Device memory and stream of a plan. User-created plans own one; the
+// one-shot tp_build_cost_tensors reuses a per-thread, per-device arena so
+// repeated builds do not pay cudaMalloc/cudaStreamCreate.
+struct Arena {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  DevBuf d_tabs, d_tables, d_ops, d_chks, d_slots, d_occs, d_sigs, d_edges, d_sig_edges, d_work,
+      d_over, d_rsec, d_rvol, d_nsec, d_nvol, d_nmem, d_rowbase, d_err, d_edges_local;
+  DevBuf out[9];  // one-shot staging of the requested outputs
+  void release() {
+    for (DevBuf* b : {&d_tabs, &d_tables, &d_ops, &d_chks, &d_slots, &d_occs, &d_sigs, &d_edges,
+                      &d_sig_edges, &d_work, &d_over, &d_rsec, &d_rvol, &d_nsec, &d_nvol, &d_nmem,
+                      &d_rowbase, &d_err, &d_edges_local})
+      b->release();
+    for (auto& b : out) b.release();
+    if (stream) cudaStreamDestroy(stream);
+    stream = nullptr;
+  }
+};
+
+struct tp_plan {
+  int device = 0;
+  Arena* arena = nullptr;
+  bool owns_arena = true;
+  // sizes / index
+  int32_t num_ops = 0, num_edges = 0;
+  int64_t N = 1;
+  int n_log2 = 0;
+  Env env{};
+  std::vector<int64_t> node_base;  // [num_ops + 1]
+  std::vector<int64_t> edge_base;  // [num_edges + 1]
+  std::vector<int64_t> row_base;   // [num_edges + 1]
+  std::vector<int32_t> edge_from_op, edge_to_op, in_deg, out_deg, topo;
+  int64_t num_aux_nodes = 0, num_aux_edges = 0, num_rows = 0, num_virtual = 0;
+  int valid_ops = 0;    // ops whose nodes are built (before a host node-phase error)
+  int valid_edges = 0;  // edges processed before a host edge-phase error
+  uint64_t host_err = ~0ull;
+  // device descriptors (host copies)
+  std::vector<TableDesc> tabs;
+  int64_t table_total = 0;
+  std::vector<OpDesc> ops;
+  std::vector<SliceChk> chks;
+  std::vector<SlotDesc> slots;
+  std::vector<Occ> occs;
+  std::vector<SigDesc> sigs;
+  std::vector<EdgeDesc> edges;
+  std::vector<int32_t> sig_edges;    // edges grouped by class, edge order within
+  std::vector<int32_t> sig_edge_begin;
+  std::vector<double> overrides;     // per pair; empty if no class needs one
+  int64_t total_pairs = 0;
+  int64_t h2d_bytes = 0;
+  bool uploaded = false;
+  std::vector<Work> work;  // per execute (depends on the edge range)
+  int64_t last_launches = 0;
+  int32_t last_e0 = 0, last_e1 = 0;
+  cudaStream_t last_stream = nullptr;  // stream of the last execute
+  cudaEvent_t prof_start = nullptr, prof_stop = nullptr;  // recorded around K4
+};
+
+namespace {
+
+struct Builder {
+  const tp_graph_desc* g;
+  const tp_topology_desc* t;
+  tp_plan* P;
+
+  int num_tensors() const { return g->op_tensor_begin[g->num_ops]; }
+
+  tp_status check_desc() {
+    if (!g || !t) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null descriptor");
+    if (g->num_ops < 0 || g->num_edges < 0) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "negative counts");
+    if (g->num_ops > 0 && (!g->op_id || !g->op_tensor_begin || !g->op_num_inputs || !g->op_axis_begin))
+      return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null operator arrays");
+    if (g->num_edges > 0 && (!g->edge_from || !g->edge_to || !g->edge_tensor))
+      return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null edge arrays");
+    if (g->num_ops == 0) return TP_OK;
+    if (g->op_tensor_begin[0] != 0 || g->op_axis_begin[0] != 0)
+      return set_err(TP_ERR_INVALID_ARGUMENT, 0, "CSR offsets must start at 0");
+    for (int i = 0; i < g->num_ops; ++i) {
+      if (g->op_tensor_begin[i + 1] < g->op_tensor_begin[i] || g->op_axis_begin[i + 1] < g->op_axis_begin[i])
+        return set_err(TP_ERR_INVALID_ARGUMENT, 0, "CSR offsets must be non-decreasing");
+      const int nt = g->op_tensor_begin[i + 1] - g->op_tensor_begin[i];
+      if (g->op_num_inputs[i] < 0 || g->op_num_inputs[i] > nt)
+        return set_err(TP_ERR_INVALID_ARGUMENT, 0, "op_num_inputs out of range");
+    }
+    const int nt = num_tensors();
+    const int na = g->op_axis_begin[g->num_ops];
+    if (nt > 0 && (!g->tensor_name || !g->tensor_shape_begin || !g->tensor_element_size))
+      return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null tensor arrays");
+    if (na > 0 && !g->axis_slice_begin) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null axis arrays");
+    if (nt > 0) {
+      if (g->tensor_shape_begin[0] != 0) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "shape CSR must start at 0");
+      for (int k = 0; k < nt; ++k)
+        if (g->tensor_shape_begin[k + 1] < g->tensor_shape_begin[k])
+          return set_err(TP_ERR_INVALID_ARGUMENT, 0, "shape CSR must be non-decreasing");
+      if (g->tensor_shape_begin[nt] > 0 && !g->shape) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null shape");
+    }
+    if (na > 0) {
+      if (g->axis_slice_begin[0] != 0) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "slice CSR must start at 0");
+      for (int a = 0; a < na; ++a)
+        if (g->axis_slice_begin[a + 1] < g->axis_slice_begin[a])
+          return set_err(TP_ERR_INVALID_ARGUMENT, 0, "slice CSR must be non-decreasing");
+      if (g->axis_slice_begin[na] > 0 && (!g->slice_tensor || !g->slice_dim))
+        return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null slice arrays");
+    }
+    return TP_OK;
+  }
+
+  int rank_of(int tensor) const { return g->tensor_shape_begin[tensor + 1] - g->tensor_shape_begin[tensor]; }
+  const int64_t* shape_of(int tensor) const { return g->shape + g->tensor_shape_begin[tensor]; }
+
+  // per-op slot resolution: the reference keys layouts by tensor name, the
+  // last occurrence's spec winning (layout.hpp:339-347)
+  struct OpSlots {
+    std::vector<int32_t> name, spec;
+    int find(int nm) const {
+      for (size_t i = 0; i < name.size(); ++i)
+        if (name[i] == nm) return (int)i;
+      return -1;
+    }
+  };
+  std::vector<OpSlots> op_slots;
+  std::vector<std::vector<std::array<int8_t, tpk::kMaxR>>> slot_sa;  // per op, per slot
+
+  tp_status run() {
+    tp_status st = check_desc();
+    if (st) return st;
+    tp_plan& p = *P;
+    p.num_ops = g->num_ops;
+    p.num_edges = g->num_edges;
+    p.N = (int64_t)t->node_count * (int64_t)t->local_device_num;
+    p.env = Env{t->intra_bandwidth, t->inter_bandwidth, (int64_t)t->local_device_num};
+
+    // graph.hpp:135-140 find_op (first operator with the id), degrees by id
+    std::unordered_map<int32_t, int32_t> first_op;
+    std::unordered_map<int32_t, int32_t> to_count, from_count;
+    for (int i = 0; i < g->num_ops; ++i) first_op.emplace(g->op_id[i], i);
+    for (int e = 0; e < g->num_edges; ++e) {
+      to_count[g->edge_to[e]]++;
+      from_count[g->edge_from[e]]++;
+    }
+    p.in_deg.resize(g->num_ops);
+    p.out_deg.resize(g->num_ops);
+    for (int i = 0; i < g->num_ops; ++i) {
+      auto a = to_count.find(g->op_id[i]);
+      auto b = from_count.find(g->op_id[i]);
+      p.in_deg[i] = a == to_count.end() ? 0 : a->second;
+      p.out_deg[i] = b == from_count.end() ? 0 : b->second;
+    }
+    p.edge_from_op.resize(g->num_edges);
+    p.edge_to_op.resize(g->num_edges);
+    for (int e = 0; e < g->num_edges; ++e) {
+      auto a = first_op.find(g->edge_from[e]);
+      auto b = first_op.find(g->edge_to[e]);
+      p.edge_from_op[e] = a == first_op.end() ? -1 : a->second;
+      p.edge_to_op[e] = b == first_op.end() ? -1 : b->second;
+    }
+    // Kahn's algorithm (graph.hpp:158-183)
+    {
+      std::vector<int32_t> indeg(g->num_ops, 0);
+      std::vector<std::vector<int32_t>> succ(g->num_ops);
+      for (int e = 0; e < g->num_edges; ++e) {
+        const int u = p.edge_from_op[e], w = p.edge_to_op[e];
+        if (u < 0 || w < 0) continue;
+        succ[u].push_back(w);
+        ++indeg[w];
+      }
+      std::vector<int32_t> ready;
+      for (int i = 0; i < g->num_ops; ++i)
+        if (indeg[i] == 0) ready.push_back(i);
+      for (size_t h = 0; h < ready.size(); ++h) {
+        p.topo.push_back(ready[h]);
+        for (int w : succ[ready[h]])
+          if (--indeg[w] == 0) ready.push_back(w);
+      }
+      if ((int)p.topo.size() != g->num_ops) {
+        p.topo.assign(g->num_ops, 0);
+        p.host_err = ekey(0, tpk::kCycle);  // aux_graph.hpp:224-226
+        p.node_base.assign(g->num_ops + 1, 0);
+        p.edge_base.assign(g->num_edges + 1, 0);
+        p.row_base.assign(g->num_edges + 1, 0);
+        return TP_OK;
+      }
+    }
+
+    // ---------------- node phase (aux_graph.hpp:236-253) -----------------
+    const bool pow2 = p.N > 0 && (p.N & (p.N - 1)) == 0;
+    p.n_log2 = pow2 ? log2_floor(p.N) : 0;
+    if (pow2 && p.n_log2 > tpk::kMaxD) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "more than 2^16 devices");
+    p.node_base.assign(g->num_ops + 1, 0);
+    std::map<int, int64_t> table_of_p;  // p -> entry offset
+    op_slots.resize(g->num_ops);
+    slot_sa.resize(g->num_ops);
+    int64_t nodes = 0;
+    p.valid_ops = g->num_ops;
+    for (int i = 0; i < g->num_ops; ++i) {
+      p.node_base[i] = nodes;
+      const int np = g->op_axis_begin[i + 1] - g->op_axis_begin[i];
+      int ek = 0;
+      if (!pow2) ek = tpk::kNotPow2;
+      else if (np < 1) ek = tpk::kNoAxes;
+      if (ek) {
+        p.host_err = ekey(1 + (uint64_t)nodes * 2, ek);
+        p.valid_ops = i;
+        break;
+      }
+      if (np > tpk::kMaxAxes) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "operator with more than 8 axes");
+      const int64_t S = tpk::strategy_count(np, p.n_log2);
+      if (S > (1 << 20)) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "more than 2^20 strategies per operator");
+      if (!table_of_p.count(np)) {
+        table_of_p[np] = p.table_total;
+        p.tabs.push_back(TableDesc{p.table_total, S, np, p.n_log2});
+        p.table_total += S;
+      }
+      st = build_op(i, np, (int32_t)table_of_p[np], nodes);
+      if (st) return st;
+      nodes += S;
+    }
+    for (int i = p.valid_ops; i <= g->num_ops; ++i) p.node_base[i] = nodes;
+    p.num_aux_nodes = nodes;
+
+    // ---------------- edge phase (aux_graph.hpp:273-296) -----------------
+    p.edge_base.assign(g->num_edges + 1, 0);
+    p.row_base.assign(g->num_edges + 1, 0);
+    int64_t aux = 0, rows = 0;
+    p.valid_edges = 0;
+    std::map<std::vector<int64_t>, int32_t> sig_of_key;
+    std::vector<std::vector<int32_t>> edges_of_sig;
+    if (p.host_err == ~0ull) {
+      p.valid_edges = g->num_edges;
+      for (int e = 0; e < g->num_edges; ++e) {
+        p.edge_base[e] = aux;
+        p.row_base[e] = rows;
+        const int u = p.edge_from_op[e], w = p.edge_to_op[e];
+        if (u < 0 || w < 0) {
+          p.host_err = ekey(kEdgePhase + (uint64_t)aux * 2, tpk::kDangling);
+          p.valid_edges = e;
+          break;
+        }
+        const int ku = op_slots[u].find(g->edge_tensor[e]);
+        const int kw = op_slots[w].find(g->edge_tensor[e]);
+        if (ku < 0 || kw < 0) {
+          p.host_err = ekey(kEdgePhase + (uint64_t)aux * 2, tpk::kEdgeTensorMissing);
+          p.valid_edges = e;
+          break;
+        }
+        const int tu = op_slots[u].spec[ku], tw = op_slots[w].spec[kw];
+        const int R = rank_of(tu);
+        bool same_shape = R == rank_of(tw);
+        for (int d = 0; same_shape && d < R; ++d) same_shape = shape_of(tu)[d] == shape_of(tw)[d];
+        if (!same_shape) {
+          p.host_err = ekey(kEdgePhase + (uint64_t)aux * 2 + 1, tpk::kShapeMismatch);
+          p.valid_edges = e;
+          break;
+        }
+        const int pu = g->op_axis_begin[u + 1] - g->op_axis_begin[u];
+        const int pw = g->op_axis_begin[w + 1] - g->op_axis_begin[w];
+        const int64_t Su = p.node_base[u + 1] - p.node_base[u];
+        const int64_t Sw = p.node_base[w + 1] - p.node_base[w];
+        int64_t elements = 1;
+        for (int d = 0; d < R; ++d) elements *= shape_of(tu)[d];
+        const double bytes = (double)elements * g->tensor_element_size[tu];  // graph.hpp:52-54
+        // class key
+        std::vector<int64_t> key;
+        key.reserve(8 + 3 * R);
+        key.push_back(pu);
+        key.push_back(pw);
+        key.push_back(R);
+        int64_t bbits;
+        std::memcpy(&bbits, &bytes, 8);
+        key.push_back(bbits);
+        for (int d = 0; d < R; ++d) key.push_back(shape_of(tu)[d]);
+        for (int d = 0; d < R; ++d) key.push_back(slot_sa[u][ku][d]);
+        for (int d = 0; d < R; ++d) key.push_back(slot_sa[w][kw][d]);
+        auto it = sig_of_key.find(key);
+        int32_t sig;
+        if (it == sig_of_key.end()) {
+          sig = (int32_t)p.sigs.size();
+          sig_of_key.emplace(key, sig);
+          SigDesc sd{};
+          sd.pair_begin = p.total_pairs;
+          sd.first_aux = aux;
+          sd.bytes = bytes;
+          sd.R = R;
+          sd.Su = (int32_t)Su;
+          sd.Sw = (int32_t)Sw;
+          sd.tab_u = (int32_t)table_of_p[pu];
+          sd.tab_w = (int32_t)table_of_p[pw];
+          for (int d = 0; d < tpk::kMaxR; ++d) {
+            sd.sa_u[d] = d < R ? slot_sa[u][ku][d] : -1;
+            sd.sa_w[d] = d < R ? slot_sa[w][kw][d] : -1;
+            const int64_t E = d < R ? shape_of(tu)[d] : 1;
+            const int v = v2_capped(E);
+            sd.dt[d].t = (uint8_t)v;
+            sd.dt[d].odd = (E >> v) > 1;
+          }
+          p.sigs.push_back(sd);
+          edges_of_sig.emplace_back();
+          p.total_pairs += Su * Sw;
+        } else {
+          sig = it->second;
+        }
+        edges_of_sig[sig].push_back(e);
+        EdgeDesc ed{};
+        ed.aux_base = aux;
+        ed.nb_u = p.node_base[u];
+        ed.nb_w = p.node_base[w];
+        ed.indeg_w = (double)p.in_deg[w];
+        ed.sig = sig;
+        ed.e = e;
+        p.edges.push_back(ed);
+        aux += Su * Sw;
+        rows += Su;
+      }
+      for (int e = p.valid_edges; e <= g->num_edges; ++e) {
+        p.edge_base[e] = aux;
+        p.row_base[e] = rows;
+      }
+    }
+    p.num_aux_edges = aux;
+    p.num_rows = rows;
+    p.sig_edge_begin.push_back(0);
+    for (auto& v : edges_of_sig) {
+      for (int e : v) p.sig_edges.push_back(e);
+      p.sig_edge_begin.push_back((int32_t)p.sig_edges.size());
+    }
+    for (int i = 0; i < p.valid_ops; ++i)
+      if (p.in_deg[i] == 0) p.num_virtual += p.node_base[i + 1] - p.node_base[i];
+    return memo_aliasing();
+  }
+
+  tp_status build_op(int i, int np, int32_t table, int64_t nb) {
+    tp_plan& p = *P;
+    OpSlots& os = op_slots[i];
+    const int t0 = g->op_tensor_begin[i], t1 = g->op_tensor_begin[i + 1];
+    for (int t = t0; t < t1; ++t) {
+      int k = os.find(g->tensor_name[t]);
+      if (k < 0) {
+        k = (int)os.name.size();
+        os.name.push_back(g->tensor_name[t]);
+        os.spec.push_back(t);
+      }
+      os.spec[k] = t;
+      if (rank_of(t) > tpk::kMaxR) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "tensor rank above 8");
+      for (int d = 0; d < rank_of(t); ++d)
+        if (shape_of(t)[d] < 1) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "tensor extent < 1 is unsupported");
+    }
+    if (os.name.size() > 32000) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many tensors per op");
+    auto& sa = slot_sa[i];
+    sa.assign(os.name.size(), std::array<int8_t, tpk::kMaxR>{});
+    for (auto& a : sa) a.fill(-1);
+    OpDesc od{};
+    od.node_base = nb;
+    od.table = table;
+    od.p = np;
+    od.chk_begin = (int32_t)p.chks.size();
+    od.slot_begin = (int32_t)p.slots.size();
+    const int a0 = g->op_axis_begin[i];
+    for (int a = 0; a < np; ++a) {
+      for (int s = g->axis_slice_begin[a0 + a]; s < g->axis_slice_begin[a0 + a + 1]; ++s) {
+        const int k = os.find(g->slice_tensor[s]);
+        SliceChk c{};
+        c.axis = (int8_t)a;
+        c.slot = (int16_t)k;
+        c.v = 0;
+        if (k >= 0) {
+          const int dim = g->slice_dim[s];
+          const int tk = os.spec[k];
+          if (dim < 0 || dim >= rank_of(tk))
+            return set_err(TP_ERR_INVALID_ARGUMENT, 0, "slice dimension out of range");
+          c.v = (int8_t)v2_capped(shape_of(tk)[dim]);
+          sa[k][dim] = (int8_t)a;  // later slices overwrite (layout.hpp:366)
+        }
+        p.chks.push_back(c);
+      }
+    }
+    od.chk_end = (int32_t)p.chks.size();
+    for (size_t k = 0; k < os.name.size(); ++k) {
+      SlotDesc sd{};
+      const int tk = os.spec[k];
+      int64_t el = 1;
+      for (int d = 0; d < rank_of(tk); ++d) el *= shape_of(tk)[d];
+      sd.elements = el;
+      sd.es = g->tensor_element_size[tk];
+      sd.R = (int8_t)rank_of(tk);
+      for (int d = 0; d < tpk::kMaxR; ++d) sd.sa[d] = sa[k][d];
+      p.slots.push_back(sd);
+    }
+    od.occ_begin = (int32_t)p.occs.size();
+    const int nin = g->op_num_inputs[i];
+    for (int t = t0; t < t1; ++t) {
+      Occ oc{};
+      const int nm = g->tensor_name[t];
+      oc.slot = (int16_t)os.find(nm);
+      uint8_t mask = 0;
+      for (int a = 0; a < np; ++a) {
+        bool slices = false;
+        for (int s = g->axis_slice_begin[a0 + a]; s < g->axis_slice_begin[a0 + a + 1]; ++s)
+          slices |= g->slice_tensor[s] == nm;
+        if (!slices) mask |= (uint8_t)(1u << a);
+      }
+      oc.nonslicing = mask;
+      bool fed = false;
+      if (t - t0 < nin) {
+        for (int e = 0; e < g->num_edges && !fed; ++e)
+          fed = g->edge_to[e] == g->op_id[i] && g->edge_tensor[e] == nm;
+        oc.in_memory = !fed;
+      } else {
+        oc.in_memory = 1;
+      }
+      p.occs.push_back(oc);
+    }
+    od.occ_end = (int32_t)p.occs.size();
+    p.ops.push_back(od);
+    return TP_OK;
+  }
+
+  // The reference memo (aux_graph.hpp:257-271) keys on (shape, matrix, map)
+  // of both layouts but prices with the FIRST edge's tensor bytes. Only when
+  // same-shape classes carry different bytes can that be observed; then the
+  // first writer's bytes are resolved per pair here (host, rare path).
+  tp_status memo_aliasing() {
+    tp_plan& p = *P;
+    std::map<std::vector<int64_t>, std::vector<int32_t>> by_shape;
+    for (size_t s = 0; s < p.sigs.size(); ++s) {
+      std::vector<int64_t> sh;
+      const EdgeDesc& ed = p.edges[p.sig_edges[p.sig_edge_begin[s]]];
+      const int u = p.edge_from_op[ed.e];
+      const int ku = op_slots[u].find(g->edge_tensor[ed.e]);
+      const int tu = op_slots[u].spec[ku];
+      sh.assign(shape_of(tu), shape_of(tu) + rank_of(tu));
+      by_shape[sh].push_back((int32_t)s);
+    }
+    bool hazard = false;
+    for (auto& kv : by_shape) {
+      for (int32_t s : kv.second)
+        if (p.sigs[s].bytes != p.sigs[kv.second[0]].bytes) hazard = true;
+    }
+    if (!hazard) return TP_OK;
+    if (p.total_pairs > (int64_t)1 << 26) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "aliasing graph too large");
+    // host strategy tables
+    std::map<int, std::vector<Strat>> host_tab;
+    for (auto& td : p.tabs) {
+      auto& v = host_tab[td.p];
+      v.resize(td.count);
+      for (int64_t s = 0; s < td.count; ++s) tpk::unrank_strategy(td.p, td.n, s, v[s]);
+    }
+    auto strat_at = [&](int32_t tab_off, int64_t s) -> const Strat& {
+      for (auto& td : p.tabs)
+        if (td.offset == tab_off) return host_tab[td.p][s];
+      return host_tab.begin()->second[0];
+    };
+    p.overrides.assign(p.total_pairs, 0.0);
+    // classes in order of their first edge (first-writer order)
+    std::vector<int32_t> order(p.sigs.size());
+    for (size_t s = 0; s < order.size(); ++s) order[s] = (int32_t)s;
+    std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+      return p.sigs[a].first_aux < p.sigs[b].first_aux;
+    });
+    std::unordered_map<std::string, double> first;
+    for (int32_t s : order) {
+      SigDesc& sd = p.sigs[s];
+      sd.has_override = 1;
+      std::string shape_key;
+      const EdgeDesc& ed = p.edges[p.sig_edges[p.sig_edge_begin[s]]];
+      const int u = p.edge_from_op[ed.e];
+      const int tu = op_slots[u].spec[op_slots[u].find(g->edge_tensor[ed.e])];
+      shape_key.assign(reinterpret_cast<const char*>(shape_of(tu)), rank_of(tu) * sizeof(int64_t));
+      for (int64_t su = 0; su < sd.Su; ++su) {
+        Lay F;
+        tpk::side_layout(strat_at(sd.tab_u, su), sd.sa_u, sd.R, F);
+        for (int64_t sw = 0; sw < sd.Sw; ++sw) {
+          Lay T;
+          tpk::side_layout(strat_at(sd.tab_w, sw), sd.sa_w, sd.R, T);
+          const int64_t idx = sd.pair_begin + su * sd.Sw + sw;
+          p.overrides[idx] = sd.bytes;
+          if (tpk::same_layout(F, T, sd.R)) continue;
+          std::string key = shape_key;
+          key.push_back((char)F.depth);
+          key.append(reinterpret_cast<const char*>(F.mx), F.depth);
+          key.append(reinterpret_cast<const char*>(F.map), sd.R);
+          key.push_back((char)T.depth);
+          key.append(reinterpret_cast<const char*>(T.mx), T.depth);
+          key.append(reinterpret_cast<const char*>(T.map), sd.R);
+          auto it = first.find(key);
+          if (it == first.end()) first.emplace(key, sd.bytes);
+          else p.overrides[idx] = it->second;
+        }
+      }
+    }
+    return TP_OK;
+  }
+};
+
+tp_status ensure_stream(tp_plan* p) {
+  CUDA_TRY(cudaSetDevice(p->device));
+  if (!p->arena) {
+    p->arena = new Arena();
+    p->arena->device = p->device;
+    p->owns_arena = true;
+  }
+  if (!p->arena->stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->arena->stream, cudaStreamNonBlocking));
+  return TP_OK;
+}
+
+Arena* thread_arena(int device) {
+  static thread_local std::map<int, Arena*> arenas;
+  Arena*& a = arenas[device];
+  if (!a) {
+    a = new Arena();
+    a->device = device;
+  }
+  return a;
+}
+
+// Split class tiles x edge chunks into CTA work items for edges [e0, e1).
+void make_work(tp_plan* p, int32_t e0, int32_t e1, std::vector<Work>& out, std::vector<int32_t>& sig_edges_local,
+               std::vector<int32_t>& begin_local) {
+  out.clear();
+  sig_edges_local.clear();
+  begin_local.assign(1, 0);
+  int64_t total = 0;
+  for (size_t s = 0; s < p->sigs.size(); ++s) {
+    for (int i = p->sig_edge_begin[s]; i < p->sig_edge_begin[s + 1]; ++i) {
+      const int e = p->sig_edges[i];
+      if (e >= e0 && e < e1) {
+        sig_edges_local.push_back(e);
+        total += (int64_t)p->sigs[s].Su * p->sigs[s].Sw;
+      }
+    }
+    begin_local.push_back((int32_t)sig_edges_local.size());
+  }
+  // aim at >= 4 CTAs per SM while reusing each class tile across edges
+  const int64_t target = std::max<int64_t>(kExpTile * 4, total / (148 * 4) + 1);
+  for (size_t s = 0; s < p->sigs.size(); ++s) {
+    const int b = begin_local[s], en = begin_local[s + 1];
+    if (b == en) continue;
+    const int64_t P = (int64_t)p->sigs[s].Su * p->sigs[s].Sw;
+    const int64_t tile = std::min<int64_t>(P, kExpTile);
+    const int chunk = (int)std::max<int64_t>(1, target / std::max<int64_t>(tile, 1));
+    for (int64_t j0 = 0; j0 < P; j0 += kExpTile) {
+      for (int c = b; c < en; c += chunk) {
+        Work w{};
+        w.sig = (int32_t)s;
+        w.ebeg = c;
+        w.eend = std::min(en, c + chunk);
+        w.j0 = j0;
+        out.push_back(w);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int32_t tp_abi_version(void) { return TP_ABI_VERSION; }
+const char* tp_last_error(void) { return g_err.c_str(); }
+int32_t tp_last_error_kind(void) { return g_err_kind; }
+
+tp_status tp_plan_create(const tp_graph_desc* graph, const tp_topology_desc* topo, int32_t device,
+                         tp_plan** plan_out) {
+  if (!plan_out) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan_out");
+  *plan_out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(TP_ERR_CUDA, 0, "no CUDA device: the engine has no CPU path");
+  tp_plan* p = new tp_plan();
+  if (device < 0) cudaGetDevice(&p->device);
+  else p->device = device;
+  Builder b{graph, topo, p};
+  tp_status st = b.run();
+  if (st) {
+    delete p;
+    return st;
+  }
+  *plan_out = p;
+  g_err.clear();
+  g_err_kind = 0;
+  return TP_OK;
+}
+
+void tp_plan_destroy(tp_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  if (p->arena) {
+    if (p->arena->stream) cudaStreamSynchronize(p->arena->stream);
+    if (p->owns_arena) {
+      p->arena->release();
+      delete p->arena;
+    }
+  }
+  delete p;
+}
+
+tp_status tp_plan_sizes(const tp_plan* p, tp_plan_sizes_t* s) {
+  if (!p || !s) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null argument");
+  s->num_ops = p->num_ops;
+  s->num_edges = p->num_edges;
+  s->num_aux_nodes = p->num_aux_nodes;
+  s->num_aux_edges = p->num_aux_edges;
+  s->num_virtual_edges = p->num_virtual;
+  s->num_rows = p->num_rows;
+  s->num_signatures = (int64_t)p->sigs.size();
+  s->num_pair_evals = p->total_pairs;
+  s->h2d_bytes = p->h2d_bytes;
+  return TP_OK;
+}
+
+tp_status tp_plan_index(const tp_plan* p, tp_aux_index* x) {
+  if (!p || !x) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null argument");
+  if (x->node_base) std::memcpy(x->node_base, p->node_base.data(), sizeof(int64_t) * (p->num_ops + 1));
+  if (x->edge_base) std::memcpy(x->edge_base, p->edge_base.data(), sizeof(int64_t) * (p->num_edges + 1));
+  if (x->edge_from_op && p->num_edges) std::memcpy(x->edge_from_op, p->edge_from_op.data(), sizeof(int32_t) * p->num_edges);
+  if (x->edge_to_op && p->num_edges) std::memcpy(x->edge_to_op, p->edge_to_op.data(), sizeof(int32_t) * p->num_edges);
+  if (x->in_degree && p->num_ops) std::memcpy(x->in_degree, p->in_deg.data(), sizeof(int32_t) * p->num_ops);
+  if (x->out_degree && p->num_ops) std::memcpy(x->out_degree, p->out_deg.data(), sizeof(int32_t) * p->num_ops);
+  if (x->topo_order && p->num_ops) std::memcpy(x->topo_order, p->topo.data(), sizeof(int32_t) * p->num_ops);
+  return TP_OK;
+}
+
+tp_status tp_plan_upload(tp_plan* p, void* stream) {
+  if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
+  tp_status st = ensure_stream(p);
+  if (st) return st;
+  cudaStream_t s = stream ? (cudaStream_t)stream : p->arena->stream;
+  CUDA_TRY(upload(p->arena->d_tabs, p->tabs, s));
+  CUDA_TRY(p->arena->d_tables.ensure(sizeof(Strat) * (p->table_total + 1)));
+  CUDA_TRY(upload(p->arena->d_ops, p->ops, s));
+  CUDA_TRY(upload(p->arena->d_chks, p->chks, s));
+  CUDA_TRY(upload(p->arena->d_slots, p->slots, s));
+  CUDA_TRY(upload(p->arena->d_occs, p->occs, s));
+  CUDA_TRY(upload(p->arena->d_sigs, p->sigs, s));
+  CUDA_TRY(upload(p->arena->d_edges, p->edges, s));
+  CUDA_TRY(upload(p->arena->d_over, p->overrides, s));
+  CUDA_TRY(p->arena->d_rsec.ensure(sizeof(double) * (p->total_pairs + 1)));
+  CUDA_TRY(p->arena->d_rvol.ensure(sizeof(double) * (p->total_pairs + 1)));
+  CUDA_TRY(p->arena->d_nsec.ensure(sizeof(double) * (p->num_aux_nodes + 1)));
+  CUDA_TRY(p->arena->d_nvol.ensure(sizeof(double) * (p->num_aux_nodes + 1)));
+  CUDA_TRY(p->arena->d_nmem.ensure(sizeof(double) * (p->num_aux_nodes + 1)));
+  CUDA_TRY(p->arena->d_err.ensure(sizeof(unsigned long long)));
+  p->h2d_bytes = (int64_t)(p->tabs.size() * sizeof(TableDesc) + p->ops.size() * sizeof(OpDesc) +
+                           p->chks.size() * sizeof(SliceChk) + p->slots.size() * sizeof(SlotDesc) +
+                           p->occs.size() * sizeof(Occ) + p->sigs.size() * sizeof(SigDesc) +
+                           p->edges.size() * sizeof(EdgeDesc) + p->overrides.size() * sizeof(double));
+  p->uploaded = true;
+  p->last_e0 = p->last_e1 = -1;
+  return TP_OK;
+}
+
+tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors* out) {
+  if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
+  tp_status st = ensure_stream(p);
+  if (st) return st;
+  if (!p->uploaded) {
+    st = tp_plan_upload(p, opts ? opts->stream : nullptr);
+    if (st) return st;
+  }
+  cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : p->arena->stream;
+  p->last_stream = s;
+  int32_t e0 = opts ? opts->edge_begin : 0;
+  int32_t e1 = opts ? opts->edge_end : -1;
+  if (e1 < 0 || e1 > p->valid_edges) e1 = p->valid_edges;
+  if (e0 < 0) e0 = 0;
+  if (e0 > e1) e0 = e1;
+  const bool skip_nodes = opts && opts->skip_nodes;
+  tp_cost_tensors none{};
+  if (!out) out = &none;
+  int64_t launches = 0;
+  unsigned long long* err = (unsigned long long*)p->arena->d_err.p;
+  CUDA_TRY(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), s));
+  if (p->host_err != ~0ull && (p->host_err >> 6) == 0) {  // cycle: nothing to build
+    p->last_launches = 0;
+    return TP_OK;
+  }
+  // K1: strategy tables
+  if (p->table_total > 0) {
+    const int th = 128;
+    table_kernel<<<(unsigned)((p->table_total + th - 1) / th), th, 0, s>>>(
+        (const TableDesc*)p->arena->d_tabs.p, (int)p->tabs.size(), p->table_total, (Strat*)p->arena->d_tables.p);
+    ++launches;
+  }
+  // K2: per-node costs
+  const int64_t nodes = p->node_base[p->valid_ops];
+  if (nodes > 0) {
+    const int th = 256;
+    node_kernel<<<(unsigned)((nodes + th - 1) / th), th, 0, s>>>(
+        (const OpDesc*)p->arena->d_ops.p, (int)p->ops.size(), nodes, p->n_log2, p->env, (const Strat*)p->arena->d_tables.p,
+        (const SliceChk*)p->arena->d_chks.p, (const SlotDesc*)p->arena->d_slots.p, (const Occ*)p->arena->d_occs.p,
+        (double*)p->arena->d_nsec.p, (double*)p->arena->d_nvol.p, (double*)p->arena->d_nmem.p,
+        skip_nodes ? nullptr : out->node_intra_cost_s, skip_nodes ? nullptr : out->node_intra_volume_bytes,
+        skip_nodes ? nullptr : out->node_memory_bytes, err);
+    ++launches;
+  }
+  // K3: class tables (all classes; the tables are shared by every edge)
+  if (p->total_pairs > 0 && p->host_err >= ekey(kEdgePhase, 0)) {
+    const int th = 128;
+    pair_kernel<<<(unsigned)((p->total_pairs + th - 1) / th), th, 0, s>>>(
+        (const SigDesc*)p->arena->d_sigs.p, (int)p->sigs.size(), p->total_pairs, p->env, (const Strat*)p->arena->d_tables.p,
+        (const double*)p->arena->d_over.p, (double*)p->arena->d_rsec.p, (double*)p->arena->d_rvol.p, err);
+    ++launches;
+  }
+  // K4: fan-out to the aux edges of [e0, e1)
+  const int64_t out_offset = p->edge_base[e0];
+  if (p->edge_base[e1] > out_offset && p->host_err >= ekey(kEdgePhase, 0)) {
+    if (p->last_e0 != e0 || p->last_e1 != e1) {
+      std::vector<int32_t> sel, beg;
+      make_work(p, e0, e1, p->work, sel, beg);
+      CUDA_TRY(upload(p->arena->d_work, p->work, s));
+      CUDA_TRY(upload(p->arena->d_sig_edges, sel, s));  // Work ranges index this local list
+      p->last_e0 = e0;
+      p->last_e1 = e1;
+    }
+    if (!p->work.empty() && (out->edge_cost_s || out->edge_volume_bytes || out->edge_memory_bytes ||
+                             out->aux_edge_records)) {
+      if (p->prof_start) CUDA_TRY(cudaEventRecord(p->prof_start, s));
+      expand_kernel<<<(unsigned)p->work.size(), kExpThreads, 0, s>>>(
+          (const Work*)p->arena->d_work.p, (const SigDesc*)p->arena->d_sigs.p, (const int32_t*)p->arena->d_sig_edges.p,
+          (const EdgeDesc*)p->arena->d_edges.p, (const double*)p->arena->d_rsec.p, (const double*)p->arena->d_rvol.p,
+          (const double*)p->arena->d_nsec.p, (const double*)p->arena->d_nvol.p, (const double*)p->arena->d_nmem.p, out_offset,
+          out->edge_cost_s, out->edge_volume_bytes, out->edge_memory_bytes, (char*)out->aux_edge_records);
+      ++launches;
+      if (p->prof_stop) CUDA_TRY(cudaEventRecord(p->prof_stop, s));
+    }
+    if (out->row_min_cost_s && out->row_min_volume_bytes) {
+      const int64_t r0 = p->row_base[e0], r1 = p->row_base[e1];
+      std::vector<int64_t> rb(p->row_base.begin() + e0, p->row_base.begin() + e1 + 1);
+      for (auto& v : rb) v -= r0;
+      CUDA_TRY(upload(p->arena->d_rowbase, rb, s));
+      CUDA_TRY(p->arena->d_edges_local.ensure(sizeof(EdgeDesc) * (e1 - e0 + 1)));
+      CUDA_TRY(cudaMemcpyAsync(p->arena->d_edges_local.p, (const EdgeDesc*)p->arena->d_edges.p + e0,
+                               sizeof(EdgeDesc) * (e1 - e0), cudaMemcpyDeviceToDevice, s));
+      const int64_t rows = r1 - r0;
+      const int th = 256;
+      rowmin_kernel<<<(unsigned)((rows * 32 + th - 1) / th), th, 0, s>>>(
+          (const EdgeDesc*)p->arena->d_edges_local.p, (const int64_t*)p->arena->d_rowbase.p, e1 - e0, rows,
+          (const SigDesc*)p->arena->d_sigs.p, (const double*)p->arena->d_rsec.p, (const double*)p->arena->d_rvol.p,
+          (const double*)p->arena->d_nsec.p, (const double*)p->arena->d_nvol.p, out->row_min_cost_s, out->row_min_volume_bytes);
+      ++launches;
+    }
+  }
+  CUDA_TRY(cudaGetLastError());
+  p->last_launches = launches;
+  return TP_OK;
+}
+
+int64_t tp_plan_last_launches(const tp_plan* p) { return p ? p->last_launches : 0; }
+
+tp_status tp_plan_set_profile_events(tp_plan* p, void* start_event, void* stop_event) {
+  if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
+  p->prof_start = (cudaEvent_t)start_event;
+  p->prof_stop = (cudaEvent_t)stop_event;
+  return TP_OK;
+}
+
+tp_status tp_plan_check_errors(tp_plan* p) {
+  if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
+  CUDA_TRY(cudaSetDevice(p->device));
+  unsigned long long dev = ~0ull;
+  if (p->arena && p->arena->d_err.p && p->last_stream) {
+    CUDA_TRY(cudaMemcpyAsync(&dev, p->arena->d_err.p, sizeof(dev), cudaMemcpyDeviceToHost, p->last_stream));
+    CUDA_TRY(cudaStreamSynchronize(p->last_stream));
+  }
+  const uint64_t key = std::min<uint64_t>(dev, p->host_err);
+  if (key == ~0ull) return TP_OK;
+  const int kind = (int)(key & 63);
+  return set_err(status_of_kind(kind), kind, kind_text(kind));
+}
+
+tp_status tp_plan_execute_host(tp_plan* p, const tp_build_opts* opts, tp_aux_index* index_out,
+                               tp_cost_tensors* host_out) {
+  if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
+  tp_status st = ensure_stream(p);
+  if (st) return st;
+  if (!p->uploaded) {
+    st = tp_plan_upload(p, nullptr);
+    if (st) return st;
+  }
+  int32_t e0 = opts ? opts->edge_begin : 0;
+  int32_t e1 = opts ? opts->edge_end : -1;
+  if (e1 < 0 || e1 > p->valid_edges) e1 = p->valid_edges;
+  if (e0 < 0) e0 = 0;
+  if (e0 > e1) e0 = e1;
+  const int64_t ne = p->edge_base[e1] - p->edge_base[e0];
+  const int64_t nr = p->row_base[e1] - p->row_base[e0];
+  const int64_t nn = p->num_aux_nodes;
+  tp_cost_tensors h = host_out ? *host_out : tp_cost_tensors{};
+  DevBuf* b = p->arena->out;
+  tp_cost_tensors d{};
+  bool oom = false;
+  auto dev = [&](DevBuf& buf, void* host, int64_t n, size_t el) -> void* {
+    if (!host || n <= 0) return nullptr;
+    if (buf.ensure((size_t)n * el) != cudaSuccess) {
+      oom = true;
+      return nullptr;
+    }
+    return buf.p;
+  };
+  d.node_intra_cost_s = (double*)dev(b[0], h.node_intra_cost_s, nn, 8);
+  d.node_intra_volume_bytes = (double*)dev(b[1], h.node_intra_volume_bytes, nn, 8);
+  d.node_memory_bytes = (double*)dev(b[2], h.node_memory_bytes, nn, 8);
+  d.edge_cost_s = (double*)dev(b[3], h.edge_cost_s, ne, 8);
+  d.edge_volume_bytes = (double*)dev(b[4], h.edge_volume_bytes, ne, 8);
+  d.edge_memory_bytes = (double*)dev(b[5], h.edge_memory_bytes, ne, 8);
+  d.aux_edge_records = dev(b[6], h.aux_edge_records, ne, 40);
+  d.row_min_cost_s = (double*)dev(b[7], h.row_min_cost_s, nr, 8);
+  d.row_min_volume_bytes = (double*)dev(b[8], h.row_min_volume_bytes, nr, 8);
+  if (oom) return set_err(TP_ERR_CUDA, 0, "device allocation for the outputs failed");
+  tp_build_opts o = opts ? *opts : tp_build_opts{0, -1, 0, -1, nullptr};
+  o.stream = nullptr;
+  st = tp_plan_execute(p, &o, &d);
+  if (st) return st;
+  cudaStream_t s = p->arena->stream;
+  auto back = [&](void* hst, void* dv, int64_t n, size_t el) -> cudaError_t {
+    if (!hst || !dv || n <= 0) return cudaSuccess;
+    return cudaMemcpyAsync(hst, dv, (size_t)n * el, cudaMemcpyDeviceToHost, s);
+  };
+  cudaError_t ce = cudaSuccess;
+  if (!o.skip_nodes) {
+    ce = ce ? ce : back(h.node_intra_cost_s, d.node_intra_cost_s, nn, 8);
+    ce = ce ? ce : back(h.node_intra_volume_bytes, d.node_intra_volume_bytes, nn, 8);
+    ce = ce ? ce : back(h.node_memory_bytes, d.node_memory_bytes, nn, 8);
+  }
+  ce = ce ? ce : back(h.edge_cost_s, d.edge_cost_s, ne, 8);
+  ce = ce ? ce : back(h.edge_volume_bytes, d.edge_volume_bytes, ne, 8);
+  ce = ce ? ce : back(h.edge_memory_bytes, d.edge_memory_bytes, ne, 8);
+  ce = ce ? ce : back(h.aux_edge_records, d.aux_edge_records, ne, 40);
+  ce = ce ? ce : back(h.row_min_cost_s, d.row_min_cost_s, nr, 8);
+  ce = ce ? ce : back(h.row_min_volume_bytes, d.row_min_volume_bytes, nr, 8);
+  st = tp_plan_check_errors(p);  // synchronises the stream
+  if (ce != cudaSuccess) return set_err(TP_ERR_CUDA, 0, cudaGetErrorString(ce));
+  if (st) return st;
+  if (index_out) tp_plan_index(p, index_out);
+  return TP_OK;
+}
+
+tp_status tp_build_cost_tensors(const tp_graph_desc* graph, const tp_topology_desc* topo,
+                                const tp_build_opts* opts, tp_aux_index* index_out,
+                                tp_cost_tensors* host_out) {
+  tp_plan* p = nullptr;
+  tp_status st = tp_plan_create(graph, topo, opts ? opts->device : -1, &p);
+  if (st) return st;
+  p->arena = thread_arena(p->device);  // reused across one-shot calls
+  p->owns_arena = false;
+  st = tp_plan_execute_host(p, opts, index_out, host_out);
+  tp_plan_destroy(p);
+  return st;
+}
+
+tp_status tp_enumerate_strategies(int32_t p, int64_t total_devices, int64_t* count, int64_t* degrees,
+                                  int32_t* device_map, int64_t* matrix_dims, int32_t* matrix_depth) {
+  if (p < 1) return set_err(TP_ERR_TOPOPLAN, tpk::kNoAxes, "strategy_count: axis count must be >= 1");
+  if (total_devices <= 0 || (total_devices & (total_devices - 1)))
+    return set_err(TP_ERR_TOPOPLAN, tpk::kNotPow2, "device count is not a power of two");
+  if (p > tpk::kMaxAxes) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "more than 8 axes");
+  const int n = log2_floor(total_devices);
+  if (n > tpk::kMaxD) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "more than 2^16 devices");
+  const int64_t S = tpk::strategy_count(p, n);
+  if (count) *count = S;
+  if (!degrees && !device_map && !matrix_dims && !matrix_depth) return TP_OK;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(TP_ERR_CUDA, 0, "no CUDA device: the engine has no CPU path");
+  TableDesc td{0, S, p, n};
+  DevBuf dt, dout;
+  CUDA_TRY(dt.ensure(sizeof(td)));
+  CUDA_TRY(dout.ensure(sizeof(Strat) * S));
+  CUDA_TRY(cudaMemcpy(dt.p, &td, sizeof(td), cudaMemcpyHostToDevice));
+  table_kernel<<<(unsigned)((S + 127) / 128), 128>>>((const TableDesc*)dt.p, 1, S, (Strat*)dout.p);
+  std::vector<Strat> h(S);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpy(h.data(), dout.p, sizeof(Strat) * S, cudaMemcpyDeviceToHost));
+  dt.release();
+  dout.release();
+  for (int64_t i = 0; i < S; ++i) {
+    for (int a = 0; a < p; ++a) {
+      if (degrees) degrees[i * p + a] = (int64_t)1 << h[i].deg[a];
+      if (device_map) device_map[i * p + a] = h[i].dmap[a];
+      // DeviceMatrix::dims, outermost first: dims[j] = extent(depth-1-j)
+      if (matrix_dims) matrix_dims[i * p + a] = a < h[i].depth ? ((int64_t)1 << h[i].mx[h[i].depth - 1 - a]) : 0;
+    }
+    if (matrix_depth) matrix_depth[i] = h[i].depth;
+  }
+  return TP_OK;
+}
+
+tp_status tp_redistribute_batch(const tp_redist_query* q, int32_t n, tp_redist_result* r) {
+  if (n <= 0) return TP_OK;
+  if (!q || !r) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null argument");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(TP_ERR_CUDA, 0, "no CUDA device: the engine has no CPU path");
+  std::vector<tpk::QueryPOD> pod(n);
+  for (int i = 0; i < n; ++i) {
+    tpk::QueryPOD& x = pod[i];
+    std::memset(&x, 0, sizeof(x));
+    x.rank = q[i].rank;
+    x.fdepth = q[i].from_depth;
+    x.tdepth = q[i].to_depth;
+    x.local = q[i].local_device_num;
+    x.bytes = q[i].tensor_bytes;
+    x.intra = q[i].intra_bandwidth;
+    x.inter = q[i].inter_bandwidth;
+    if (x.rank > tpk::kMaxR || x.fdepth > tpk::kMaxD || x.tdepth > tpk::kMaxD || x.rank < 0) {
+      x.rank = tpk::kMaxR + 1;  // flagged as capacity by the kernel
+      continue;
+    }
+    for (int d = 0; d < x.rank; ++d) {
+      x.shape[d] = q[i].shape[d];
+      x.fmap[d] = q[i].from_map[d];
+      x.tmap[d] = q[i].to_map[d];
+    }
+    for (int k = 0; k < x.fdepth; ++k) x.fdims[k] = q[i].from_dims[k];
+    for (int k = 0; k < x.tdepth; ++k) x.tdims[k] = q[i].to_dims[k];
+  }
+  DevBuf dq, dr;
+  CUDA_TRY(dq.ensure(sizeof(tpk::QueryPOD) * n));
+  CUDA_TRY(dr.ensure(sizeof(tp_redist_result) * n));
+  CUDA_TRY(cudaMemcpy(dq.p, pod.data(), sizeof(tpk::QueryPOD) * n, cudaMemcpyHostToDevice));
+  query_kernel<<<(n + 63) / 64, 64>>>((const tpk::QueryPOD*)dq.p, n, (tp_redist_result*)dr.p);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpy(r, dr.p, sizeof(tp_redist_result) * n, cudaMemcpyDeviceToHost));
+  dq.release();
+  dr.release();
+  return TP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,253 @@
+"""Python face of the CUDA cost-tensor engine (include/taps_b200.h).
+
+`build_cost_tensors(graph, topo)` is the drop-in for the reference's
+`topoplan::build_auxiliary_graph(graph, topo, mode)`
+(/root/reference/proj/include/topoplan/aux_graph.hpp:211-315): it returns
+the same quantities (aux node/edge payloads in the reference's index order)
+as numpy arrays. `Plan` is the split API for device-resident, repeated or
+sharded builds (torch tensors as device memory; torch is plumbing only).
+There is no CPU path: without the CUDA library or a GPU every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Tuple, Union
+
+import numpy as np
+
+from . import abi
+from .graph import ClusterTopology, ComputationGraph, FlatGraph, flatten
+
+
+def _check(lib, status):
+    if status != abi.TP_OK:
+        abi.raise_for_status(status, lib.tp_last_error().decode(), lib.tp_last_error_kind())
+
+
+def _flat(graph) -> FlatGraph:
+    return graph if isinstance(graph, FlatGraph) else flatten(graph)
+
+
+@dataclass
+class CostTensors:
+    """Cost tensors of one build, reference index order (aux_graph.hpp:93-98)."""
+    node_base: np.ndarray
+    edge_base: np.ndarray
+    edge_from_op: np.ndarray
+    edge_to_op: np.ndarray
+    in_degree: np.ndarray
+    out_degree: np.ndarray
+    topo_order: np.ndarray
+    node_intra_cost_s: np.ndarray
+    node_intra_volume_bytes: np.ndarray
+    node_memory_bytes: np.ndarray
+    edge_cost_s: np.ndarray
+    edge_volume_bytes: np.ndarray
+    edge_memory_bytes: np.ndarray
+    records: Optional[np.ndarray] = None
+    row_min_cost_s: Optional[np.ndarray] = None
+    row_min_volume_bytes: Optional[np.ndarray] = None
+    sizes: dict = field(default_factory=dict)
+
+    def strategies_of(self, op: int) -> int:
+        return int(self.node_base[op + 1] - self.node_base[op])
+
+    def edge_id(self, e: int, su: int, sw: int) -> int:
+        """AuxiliaryGraph::edge_id (aux_graph.hpp:93-98)."""
+        return int(self.edge_base[e] + su * self.strategies_of(int(self.edge_to_op[e])) + sw)
+
+    def virtual_edges(self):
+        """(op, aux node) of every virtual source edge (aux_graph.hpp:298-312);
+        their payload is the node's own (intra cost, intra volume, memory)."""
+        out = []
+        for op in range(len(self.node_base) - 1):
+            if self.in_degree[op] == 0:
+                out.extend((op, n) for n in range(int(self.node_base[op]), int(self.node_base[op + 1])))
+        return out
+
+    def price_assignment(self, assignment, mode: str = "topology") -> Tuple[float, float]:
+        """price_assignment (aux_graph.hpp:326-348): topological order, a
+        source's virtual edge first, then its in-edges ascending."""
+        cost = 0.0
+        mem = 0.0
+        n_edges = len(self.edge_to_op)
+        in_edges = [[] for _ in range(len(self.node_base) - 1)]
+        for e in range(n_edges):
+            in_edges[int(self.edge_to_op[e])].append(e)
+        for op in self.topo_order:
+            op = int(op)
+            node = int(self.node_base[op]) + int(assignment[op])
+            if self.in_degree[op] == 0:
+                cost += float(self.node_intra_volume_bytes[node] if mode == "volume"
+                              else self.node_intra_cost_s[node])
+                mem += float(self.node_memory_bytes[node])
+            for e in in_edges[op]:
+                u = int(self.edge_from_op[e])
+                a = self.edge_id(e, int(assignment[u]), int(assignment[op]))
+                cost += float(self.edge_volume_bytes[a] if mode == "volume" else self.edge_cost_s[a])
+                mem += float(self.edge_memory_bytes[a])
+        return cost, mem
+
+
+class Plan:
+    """tp_plan: host analysis once, device execution many times."""
+
+    def __init__(self, graph: Union[ComputationGraph, FlatGraph], topo: ClusterTopology, device: int = -1):
+        self.lib = abi.load_engine()
+        self.flat = _flat(graph)
+        self.topo = topo
+        self._desc = self.flat.desc()
+        self._tdesc = topo.desc()
+        h = C.c_void_p()
+        _check(self.lib, self.lib.tp_plan_create(C.byref(self._desc), C.byref(self._tdesc), device, C.byref(h)))
+        self.handle = h
+        s = abi.tp_plan_sizes_t()
+        _check(self.lib, self.lib.tp_plan_sizes(self.handle, C.byref(s)))
+        self.sizes = {k: getattr(s, k) for k, _ in abi.tp_plan_sizes_t._fields_}
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            self.lib.tp_plan_destroy(h)
+            self.handle = None
+
+    def index(self) -> dict:
+        n_ops, n_e = self.flat.num_ops, self.flat.num_edges
+        ix = dict(node_base=np.zeros(n_ops + 1, np.int64), edge_base=np.zeros(n_e + 1, np.int64),
+                  edge_from_op=np.zeros(max(n_e, 1), np.int32), edge_to_op=np.zeros(max(n_e, 1), np.int32),
+                  in_degree=np.zeros(max(n_ops, 1), np.int32), out_degree=np.zeros(max(n_ops, 1), np.int32),
+                  topo_order=np.zeros(max(n_ops, 1), np.int32))
+        st = abi.tp_aux_index(*(abi.ptr(ix[k], C.c_int64 if ix[k].dtype == np.int64 else C.c_int32)
+                                for k, _ in abi.tp_aux_index._fields_))
+        _check(self.lib, self.lib.tp_plan_index(self.handle, C.byref(st)))
+        for k, n in (("edge_from_op", n_e), ("edge_to_op", n_e), ("in_degree", n_ops),
+                     ("out_degree", n_ops), ("topo_order", n_ops)):
+            ix[k] = ix[k][:n]
+        return ix
+
+    def upload(self, stream: int = 0):
+        _check(self.lib, self.lib.tp_plan_upload(self.handle, C.c_void_p(stream or None)))
+
+    def execute(self, out: abi.tp_cost_tensors, edge_range=(0, -1), skip_nodes=False, stream: int = 0):
+        """Asynchronous on `stream` into DEVICE pointers."""
+        o = abi.tp_build_opts(edge_range[0], edge_range[1], int(skip_nodes), -1, C.c_void_p(stream or None))
+        _check(self.lib, self.lib.tp_plan_execute(self.handle, C.byref(o), C.byref(out)))
+
+    def check_errors(self):
+        _check(self.lib, self.lib.tp_plan_check_errors(self.handle))
+
+    def set_profile_events(self, start, stop):
+        """torch.cuda.Event pair recorded around the fan-out kernel (K4)."""
+        _check(self.lib, self.lib.tp_plan_set_profile_events(
+            self.handle, C.c_void_p(start.cuda_event if start is not None else None),
+            C.c_void_p(stop.cuda_event if stop is not None else None)))
+
+    def last_launches(self) -> int:
+        return int(self.lib.tp_plan_last_launches(self.handle))
+
+    def execute_host(self, records=False, row_min=False, edge_range=(0, -1), skip_nodes=False,
+                     pinned=False) -> CostTensors:
+        """Synchronous build into HOST buffers (pinned if requested)."""
+        ix = self.index()
+        e0, e1 = edge_range
+        if e1 < 0:
+            e1 = self.flat.num_edges
+        eb = ix["edge_base"]
+        ne = int(eb[e1] - eb[e0])
+        nn = self.sizes["num_aux_nodes"]
+        rows = _row_counts(ix, e0, e1)
+        alloc = _pinned_empty if pinned else (lambda n, dt: np.zeros(n, dt))
+        ct = CostTensors(
+            node_intra_cost_s=alloc(max(nn, 1), np.float64), node_intra_volume_bytes=alloc(max(nn, 1), np.float64),
+            node_memory_bytes=alloc(max(nn, 1), np.float64), edge_cost_s=alloc(max(ne, 1), np.float64),
+            edge_volume_bytes=alloc(max(ne, 1), np.float64), edge_memory_bytes=alloc(max(ne, 1), np.float64),
+            records=alloc(max(ne, 1) * 40, np.uint8) if records else None,
+            row_min_cost_s=alloc(max(rows, 1), np.float64) if row_min else None,
+            row_min_volume_bytes=alloc(max(rows, 1), np.float64) if row_min else None,
+            sizes=dict(self.sizes), **ix)
+        out = cost_struct(ct)
+        o = abi.tp_build_opts(e0, e1, int(skip_nodes), -1, None)
+        _check(self.lib, self.lib.tp_plan_execute_host(self.handle, C.byref(o), None, C.byref(out)))
+        _trim(ct, nn, ne, rows)
+        return ct
+
+
+def _row_counts(ix, e0, e1):
+    nb = ix["node_base"]
+    return int(sum(int(nb[ix["edge_from_op"][e] + 1] - nb[ix["edge_from_op"][e]]) for e in range(e0, e1)))
+
+
+def _pinned_empty(n, dtype):
+    import torch
+    tdt = {np.float64: torch.float64, np.uint8: torch.uint8}[dtype]
+    return torch.empty(n, dtype=tdt, pin_memory=True).numpy()
+
+
+def _trim(ct: CostTensors, nn, ne, rows):
+    for k in ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes"):
+        setattr(ct, k, getattr(ct, k)[:nn])
+    for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes"):
+        setattr(ct, k, getattr(ct, k)[:ne])
+    if ct.records is not None:
+        ct.records = ct.records[: ne * 40]
+    if ct.row_min_cost_s is not None:
+        ct.row_min_cost_s = ct.row_min_cost_s[:rows]
+        ct.row_min_volume_bytes = ct.row_min_volume_bytes[:rows]
+
+
+def cost_struct(ct) -> abi.tp_cost_tensors:
+    f = lambda a: abi.ptr(a, C.c_double) if a is not None else None
+    return abi.tp_cost_tensors(
+        f(ct.node_intra_cost_s), f(ct.node_intra_volume_bytes), f(ct.node_memory_bytes),
+        f(ct.edge_cost_s), f(ct.edge_volume_bytes), f(ct.edge_memory_bytes),
+        ct.records.ctypes.data_as(C.c_void_p) if ct.records is not None else None,
+        f(ct.row_min_cost_s), f(ct.row_min_volume_bytes))
+
+
+def device_cost_struct(tensors: dict) -> abi.tp_cost_tensors:
+    """tp_cost_tensors of torch CUDA tensors (missing keys -> NULL)."""
+    def p(k, t=C.c_double):
+        x = tensors.get(k)
+        return C.cast(C.c_void_p(x.data_ptr()), C.POINTER(t)) if x is not None else None
+    rec = tensors.get("records")
+    return abi.tp_cost_tensors(p("node_intra_cost_s"), p("node_intra_volume_bytes"), p("node_memory_bytes"),
+                               p("edge_cost_s"), p("edge_volume_bytes"), p("edge_memory_bytes"),
+                               C.c_void_p(rec.data_ptr()) if rec is not None else None,
+                               p("row_min_cost_s"), p("row_min_volume_bytes"))
+
+
+def build_cost_tensors(graph, topo: ClusterTopology, records=False, row_min=False,
+                       edge_range=(0, -1), device=-1, pinned=False) -> CostTensors:
+    """The drop-in for build_auxiliary_graph: host graph in, host tensors out."""
+    return Plan(graph, topo, device).execute_host(records=records, row_min=row_min,
+                                                  edge_range=edge_range, pinned=pinned)
+
+
+def enumerate_strategies(p: int, total_devices: int):
+    """Strategy table (layout.hpp:270-328) computed by the device kernel:
+    (degrees[S,p], device_map[S,p], matrix_dims[S,p] outermost-first padded
+    with 0, matrix_depth[S])."""
+    lib = abi.load_engine()
+    n = C.c_int64()
+    _check(lib, lib.tp_enumerate_strategies(p, total_devices, C.byref(n), None, None, None, None))
+    S = n.value
+    deg = np.zeros(S * p, np.int64)
+    dm = np.zeros(S * p, np.int32)
+    md = np.zeros(S * p, np.int64)
+    dep = np.zeros(S, np.int32)
+    _check(lib, lib.tp_enumerate_strategies(p, total_devices, C.byref(n), abi.ptr(deg, C.c_int64),
+                                            abi.ptr(dm, C.c_int32), abi.ptr(md, C.c_int64),
+                                            abi.ptr(dep, C.c_int32)))
+    return deg.reshape(S, p), dm.reshape(S, p), md.reshape(S, p), dep
+
+
+def redistribute_batch(queries):
+    """Verification export: each tp_redist_query evaluated by the device
+    kernel's code path (unify + inference + pricing)."""
+    lib = abi.load_engine()
+    n = len(queries)
+    arr = (abi.tp_redist_query * n)(*queries)
+    res = (abi.tp_redist_result * n)()
+    _check(lib, lib.tp_redistribute_batch(arr, n, res))
+    return list(res)

@@ -1,0 +1,227 @@
+"""GPU parity: the CUDA engine (through its C-ABI) against the oracle and the
+reference's golden vectors. Bit-exact for every integer/index output and for
+the fp64 costs (the north star allows 1e-6 relative; the kernels keep the
+reference's operation order, so we hold them to identical bits)."""
+import random
+
+import numpy as np
+import pytest
+
+from golden_util import bits, golden, graph_of, topo_of, unhex
+from oracle import bindings as B
+from paper_2301_04285_b200 import abi, engine, fuzz, graph as G, models as M
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes",
+          "edge_cost_s", "edge_volume_bytes", "edge_memory_bytes")
+INDEX = ("node_base", "edge_base", "in_degree", "out_degree", "topo_order", "edge_from_op", "edge_to_op")
+
+
+def gpu_build(g, t, **kw):
+    return engine.build_cost_tensors(g, t, **kw)
+
+
+def assert_same(gpu, ref, rowmin=False, records=False):
+    for k in INDEX:
+        np.testing.assert_array_equal(getattr(gpu, k), getattr(ref, k), err_msg=k)
+    for k in FIELDS:
+        a, b = getattr(gpu, k), getattr(ref, k)
+        assert a.shape == b.shape, k
+        bad = np.flatnonzero(bits(a) != bits(b))
+        assert bad.size == 0, f"{k}: {bad.size} mismatches, first {bad[:5]} gpu={a[bad[:3]]} ref={b[bad[:3]]}"
+    if rowmin:
+        for k in ("row_min_cost_s", "row_min_volume_bytes"):
+            assert np.array_equal(bits(getattr(gpu, k)), bits(getattr(ref, k))), k
+    if records:
+        ra = gpu.records.reshape(-1, 40).copy()
+        rb = ref.records.reshape(-1, 40).copy()
+        ra[:, 12:16] = 0  # AuxEdge padding (uninitialised in the reference)
+        rb[:, 12:16] = 0
+        assert np.array_equal(ra, rb)
+
+
+def test_abi_version(engine):
+    assert engine.tp_abi_version() == 1
+
+
+@pytest.mark.parametrize("p,N", [(1, 1), (2, 8), (3, 4), (3, 8), (2, 128), (3, 128), (4, 64), (5, 32)])
+def test_strategy_tables_match_oracle(p, N):
+    got = engine.enumerate_strategies(p, N)
+    exp = B.enumerate_with(B.oracle().oracle_enumerate, p, N)
+    for a, b in zip(got, exp):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_strategy_tables_golden():
+    for tab in golden()["strategy_tables"]:
+        deg, dm, md, dep = engine.enumerate_strategies(tab["p"], tab["N"])
+        assert deg.tolist() == tab["degrees"]
+        assert dm.tolist() == tab["device_map"]
+        assert md.tolist() == tab["matrix"]
+        assert dep.tolist() == tab["depth"]
+
+
+def test_table3_rows():
+    """The nine MatMul strategies on four devices (test_layout.cpp:67-99)."""
+    deg, dm, md, dep = engine.enumerate_strategies(3, 4)
+    assert deg.tolist() == [[1, 1, 4], [1, 2, 2], [1, 2, 2], [1, 4, 1], [2, 1, 2], [2, 1, 2], [2, 2, 1],
+                            [2, 2, 1], [4, 1, 1]]
+    assert dm.tolist() == [[-1, -1, 0], [-1, 1, 0], [-1, 0, 1], [-1, 0, -1], [1, -1, 0], [0, -1, 1],
+                           [1, 0, -1], [0, 1, -1], [0, -1, -1]]
+
+
+def _query(c):
+    return B.make_query(c["shape"], c["from_dims"], c["from_map"], c["to_dims"], c["to_map"],
+                        tensor_bytes=c["tensor_bytes"], local=c["local"], intra=c["intra"], inter=c["inter"])
+
+
+def test_redistribution_goldens():
+    cases = golden()["redistributions"]
+    qs = [_query(c) for c in cases]
+    res = engine.redistribute_batch(qs)
+    for c, r in zip(cases, res):
+        if c["status"] != 0:
+            assert r.status != 0, c
+            continue
+        assert r.status == 0, (c, r.status)
+        dims, ushape, ufm, utm, ops, cts = r.plan()
+        assert list(dims) == c["dims"]
+        assert list(ushape) == c["ushape"]
+        assert list(ufm) == c["ufrom"] and list(utm) == c["uto"]
+        assert [list(o) for o in ops] == c["ops"]
+        assert list(cts) == c["ct"]
+        assert np.array_equal(bits(r.op_seconds[: r.num_ops]), bits(unhex(c["op_seconds"])))
+        assert bits([r.volume_bytes])[0] == bits([unhex(c["volume"])])[0]
+        assert bits([r.seconds])[0] == bits([unhex(c["seconds"])])[0]
+
+
+def test_redistribution_random_vs_oracle():
+    rng = random.Random(99)
+    qs = []
+    for i in range(4000):
+        dims, shape, fm, tm = fuzz.random_redist_case(rng)
+        if i % 2:
+            d2 = fuzz.random_matrix_with_total(rng, int(np.prod(dims)))
+            tm = fuzz.random_map_for(rng, shape, d2)
+        else:
+            d2 = dims
+        if i % 3 == 0:
+            shape = [s * rng.choice([1, 3, 5, 7]) for s in shape]
+        qs.append(B.make_query(shape, dims, fm, d2, tm, local=rng.choice([1, 2, 4, 8, 16]),
+                               inter=rng.choice([6e9, 60e9, 1.5e9])))
+    res = engine.redistribute_batch(qs)
+    for q, r in zip(qs, res):
+        o = B.oracle_redistribute(q)
+        assert r.status == o.status
+        if o.status == 0:
+            assert r.plan() == o.plan()
+            assert bits([r.seconds])[0] == bits([o.seconds])[0]
+            assert bits([r.volume_bytes])[0] == bits([o.volume_bytes])[0]
+
+
+@pytest.mark.parametrize("idx", range(8))
+def test_golden_builds(idx):
+    builds = golden()["builds"]
+    if idx >= len(builds):
+        pytest.skip("no such golden")
+    c = builds[idx]
+    g, t = graph_of(c["graph"]), topo_of(c["topo"])
+    got = gpu_build(g, t, row_min=True)
+    assert got.node_base.tolist() == c["node_base"]
+    assert got.edge_base.tolist() == c["edge_base"]
+    assert got.topo_order.tolist() == c["topo_order"]
+    for k in FIELDS + ("row_min_cost_s", "row_min_volume_bytes"):
+        exp = unhex(c[k])
+        assert np.array_equal(bits(getattr(got, k)), bits(exp)), (c["name"], k)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_configs_vs_oracle(name):
+    g, t = M.CONFIGS[name]()
+    f = G.flatten(g)
+    gpu = gpu_build(f, t, records=True, row_min=True)
+    ref = B.oracle_build(f, t)
+    assert ref.status == 0
+    assert_same(gpu, ref, rowmin=True, records=True)
+    if name == "cfg1":
+        assert len(gpu.node_intra_cost_s) == 48 and len(gpu.edge_cost_s) == 252
+
+
+@pytest.mark.parametrize("nodes,ratio", [(2, 1), (4, 10), (8, 100)])
+def test_cfg3_vs_oracle(nodes, ratio):
+    g, t = M.cfg3(nodes, ratio)
+    f = G.flatten(g)
+    gpu = gpu_build(f, t)
+    ref = B.oracle_build(f, t, records=False)
+    assert_same(gpu, ref)
+    assert len(gpu.edge_cost_s) == {2: 95936, 4: 190940, 8: 335088}[nodes]
+
+
+def test_random_graphs_vs_oracle():
+    rng = random.Random(1234)
+    ok = err = 0
+    for i in range(150):
+        g, t = fuzz.random_graph(rng, odd_extents=(i % 2 == 0), mixed_element_sizes=(i % 5 == 0))
+        f = G.flatten(g)
+        ref = B.oracle_build(f, t)
+        if ref.status != 0:
+            with pytest.raises((abi.TopoplanError, IndexError)):
+                gpu_build(f, t)
+            err += 1
+            continue
+        gpu = gpu_build(f, t, records=True, row_min=True)
+        assert_same(gpu, ref, rowmin=True, records=True)
+        ok += 1
+    assert ok > 20 and err > 10
+
+
+def test_planning_instances_vs_oracle():
+    rng = random.Random(17)
+    for _ in range(40):
+        g, t = fuzz.random_planning_instance(rng)
+        f = G.flatten(g)
+        assert_same(gpu_build(f, t, row_min=True), B.oracle_build(f, t), rowmin=True)
+
+
+def test_edge_range_shards_concatenate():
+    g, t = M.cfg2()
+    f = G.flatten(g)
+    full = gpu_build(f, t)
+    plan = engine.Plan(f, t)
+    cuts = [0, 4, 9, 15]
+    parts = [plan.execute_host(edge_range=(a, b)) for a, b in zip(cuts[:-1], cuts[1:])]
+    for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes"):
+        cat = np.concatenate([getattr(p, k) for p in parts])
+        assert np.array_equal(bits(cat), bits(getattr(full, k)))
+
+
+def test_errors_match_reference_class():
+    # indivisible extent (test_aux_graph.cpp:216-220)
+    g = G.ComputationGraph([M.dense_op("fc", "matmul", "x", 6, 6, 6, "y")], [])
+    with pytest.raises(abi.TopoplanError):
+        gpu_build(g, G.ClusterTopology(1, 4, 60e9, 60e9, 32e9))
+    # non power-of-two device count
+    with pytest.raises(abi.TopoplanError):
+        gpu_build(g, G.ClusterTopology(3, 1, 60e9, 60e9, 32e9))
+    # cycle
+    a = M.pointwise_op("a", "x", "y", 8, 8)
+    b = M.pointwise_op("b", "y", "x", 8, 8)
+    with pytest.raises(abi.TopoplanError):
+        gpu_build(G.ComputationGraph([a, b], [G.GraphEdge("a", "b", "y"), G.GraphEdge("b", "a", "x")]),
+                  G.ClusterTopology(1, 2, 60e9, 60e9, 32e9))
+    # edge tensor absent from the producer -> std::out_of_range
+    with pytest.raises(IndexError):
+        gpu_build(G.ComputationGraph([a, M.pointwise_op("c", "y", "z", 8, 8)], [G.GraphEdge("a", "c", "q")]),
+                  G.ClusterTopology(1, 2, 60e9, 60e9, 32e9))
+    # dangling edge
+    with pytest.raises(abi.TopoplanError):
+        gpu_build(G.ComputationGraph([a], [G.GraphEdge("a", "nope", "y")]), G.ClusterTopology(1, 2, 60e9, 60e9, 32e9))
+
+
+def test_single_device_and_empty():
+    g = G.ComputationGraph([M.dense_op("fc", "matmul", "x", 8, 8, 8, "y")], [])
+    r = gpu_build(g, G.ClusterTopology(1, 1, 60e9, 60e9, 32e9))
+    assert r.node_intra_cost_s.tolist() == [0.0] and r.node_intra_volume_bytes.tolist() == [0.0]
+    e = gpu_build(G.ComputationGraph([], []), G.ClusterTopology(1, 8, 60e9, 6e9, 32e9))
+    assert len(e.edge_cost_s) == 0 and len(e.node_intra_cost_s) == 0
