@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Benchmark of the TAPS cost-tensor build (the hot path of BASELINE.json).
+
+Metric: resharding-cost evaluations per second (= aux edges priced per second,
+one evaluation = one (edge, producer strategy, consumer strategy) triple of
+topoplan::build_auxiliary_graph, aux_graph.hpp:273-296), plus build ms.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4]
+  python bench.py --impl reference ...      # the reference's own CPU build
+
+A step is one complete cost-tensor build of the workload (strategy tables,
+per-node costs, class tables, fan-out of every aux edge). `value` is timed on
+the device with inputs resident in HBM; `e2e` goes through the C-ABI one-shot
+call tp_build_cost_tensors with pinned host buffers (host analysis, H2D,
+kernels, D2H of all tensors) and is wall-clock timed.
+
+Multi-GPU (torchrun, one process per GPU): weak scaling — every rank builds
+its own independent scenario (the workload graph under a rank-specific
+bandwidth ratio); no collective on the data path. Max over ranks of the
+device time; NCCL only carries that max.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+METRIC = "resharding-cost evals/sec"
+BYTES_PER_EVAL = 24  # fp64 cost_s, volume_bytes, memory_bytes per aux edge
+RATIOS = (10, 1, 2, 5, 20, 50, 100, 3)  # per-rank intra/inter bandwidth ratio
+
+
+def workload(name, rank=0, layers=None):
+    from paper_2301_04285_b200 import models as M
+    ratio = RATIOS[rank % len(RATIOS)]
+    if name == "cfg4":
+        L = layers or 96
+        g = M.build_gpt_chain(L, 12288, 8, 2048)
+        t = M.ClusterTopology(16, 8, 60e9, 60e9 / ratio, 80e9)
+        desc = f"GPT-{L} hidden 12288 batch 8 seq 2048 on 16x8 (128 devices), intra/inter {ratio}"
+    elif name == "cfg3":
+        L = layers or 24
+        g, t = M.cfg3(8, ratio)
+        if layers:
+            g = M.build_gpt_chain(L, 2048, 8, 512)
+        desc = f"GPT-{L} hidden 2048 on 8x8, intra/inter {ratio}"
+    elif name == "cfg2":
+        g, t = M.cfg2()
+        desc = "transformer layer hidden 4096 (32 heads as metadata) on 4x8"
+    elif name == "cfg1":
+        g, t = M.cfg1()
+        desc = "MatMul->ReLU->MatMul (data/sample_graph.json) on 2x4"
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    return g, t, desc
+
+
+class Clocks:
+    """nvidia-smi sampler for the measurement window (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={device}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    rows.append(dict(sm=float(parts[1]), smax=float(parts[2]), hw=parts[5], hwt=parts[6],
+                                     swt=parts[7], pcap=parts[8]))
+                except ValueError:
+                    continue
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        smax = max(r["smax"] for r in rows)
+        load = [r["sm"] for r in rows if r["sm"] > 0.5 * smax] or [r["sm"] for r in rows]
+        reasons = set()
+        for r in rows:
+            for k, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"),
+                            ("swt", "sw_thermal_slowdown"), ("pcap", "sw_power_cap")):
+                if r[k].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(rows), "samples_under_load": len(load)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the fan-out kernel from the committed ncu
+    capture (profiles/), or None."""
+    path = os.path.join(REPO, "profiles", "ncu_expand_latest.json")
+    try:
+        with open(path) as fh:
+            j = json.load(fh)
+        return j.get("dram_bytes_per_launch"), j.get("aux_edges")
+    except Exception:
+        return None, None
+
+
+def cpu_baseline(flat, topo, aux_edges, repeats=3):
+    from oracle import bindings as B
+    if not B.have_reference():
+        return None
+    best = float("inf")
+    for _ in range(repeats):
+        secs, n = B.reference_bench(flat, topo, iters=1, threads=1)
+        best = min(best, secs)
+    return {"value": aux_edges / best, "unit": "evals/s", "cores": 1, "kind": "reference",
+            "build_ms": best * 1e3,
+            "sample": f"{repeats} single-thread builds of the full workload by the reference's "
+                      f"build_auxiliary_graph (oracle/_ref, g++ -O2), best of {repeats}"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import bindings as B
+    from paper_2301_04285_b200 import graph as G
+    if not B.have_reference():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtopoplan_ref.so not built"}))
+        return 0
+    threads = max(1, min(os.cpu_count() or 1, 16))
+    # bounded sample: a prefix of the GPT chain sized so the run ends in ~3 min
+    budget_s, est_full_s = 150.0, 3.5
+    full_layers = {"cfg4": 96, "cfg3": 24}.get(args.workload)
+    layers = None
+    if full_layers:
+        layers = int(full_layers * budget_s / ((args.steps + args.warmup) * est_full_s))
+        layers = max(4, min(full_layers, layers))
+    g, t, desc = workload(args.workload, 0, layers)
+    f = G.flatten(g)
+    times, evals = [], 0
+    for i in range(args.warmup + args.steps):
+        secs, n = B.reference_bench(f, t, iters=1, threads=threads)
+        if i >= args.warmup:
+            times.append(secs)
+            evals = n
+    total = sum(times)
+    value = evals * len(times) / total
+    sample = (f"{threads} concurrent single-thread builds per step of {desc}"
+              + (f" (first {layers} of {full_layers} layers)" if layers and layers < full_layers else ""))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / len(times) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": args.workload, "desc": desc, "threads": threads},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_engine(args):
+    import torch
+    from paper_2301_04285_b200 import engine as E, graph as G
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    g, t, desc = workload(args.workload, rank)
+    flat = G.flatten(g)
+    plan = E.Plan(flat, t, device=local)
+    sizes = plan.sizes
+    ne, nn = sizes["num_aux_edges"], sizes["num_aux_nodes"]
+    stream = torch.cuda.Stream()
+    sp = stream.cuda_stream
+    plan.upload(sp)
+    dev = torch.device("cuda", local)
+    outs = {k: torch.empty(max(ne, 1), dtype=torch.float64, device=dev)
+            for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes")}
+    outs.update({k: torch.empty(max(nn, 1), dtype=torch.float64, device=dev)
+                 for k in ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes")})
+    cs = E.device_cost_struct(outs)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # 256 MiB > 126 MB L2
+
+    K, W = args.steps, args.warmup
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    with torch.cuda.stream(stream):
+        for a, b in ev + kev:  # materialise the cudaEvent_t handles
+            a.record(stream)
+            b.record(stream)
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    with torch.cuda.stream(stream):
+        for _ in range(W):
+            flush.zero_()
+            plan.set_profile_events(None, None)
+            plan.execute(cs, stream=sp)
+    plan.check_errors()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for i in range(K):
+            flush.zero_()  # write > L2 between timed steps
+            ev[i][0].record(stream)
+            plan.set_profile_events(kev[i][0], kev[i][1])
+            plan.execute(cs, stream=sp)
+            ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    plan.set_profile_events(None, None)
+    plan.check_errors()
+    launches = plan.last_launches()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    k4_ms = [a.elapsed_time(b) for a, b in kev]
+    total_ms = sum(step_ms)
+    t_max = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    evals = torch.tensor([float(ne) * K], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(evals, op=dist.ReduceOp.SUM)
+    total_ms = float(t_max.item())
+    value = float(evals.item()) / (total_ms / 1e3)
+
+    # ---- e2e: the C-ABI one-shot call with pinned host buffers ----
+    lib = plan.lib
+    host = {k: torch.empty(max(ne, 1), dtype=torch.float64, pin_memory=True).numpy()
+            for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes")}
+    host.update({k: torch.empty(max(nn, 1), dtype=torch.float64, pin_memory=True).numpy()
+                 for k in ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes")})
+
+    class _H:  # attribute view for cost_struct
+        pass
+    hv = _H()
+    for k, v in host.items():
+        setattr(hv, k, v)
+    hv.records = hv.row_min_cost_s = hv.row_min_volume_bytes = None
+    hs = E.cost_struct(hv)
+    gd, td = flat.desc(), t.desc()
+    opts = E.abi.tp_build_opts(0, -1, 0, local, None)
+    KE = max(3, min(K, args.e2e_steps))
+    for _ in range(2):
+        st = lib.tp_build_cost_tensors(C.byref(gd), C.byref(td), C.byref(opts), None, C.byref(hs))
+        assert st == 0, lib.tp_last_error()
+    if dist:
+        dist.barrier()
+    e2e_t = []
+    for _ in range(KE):
+        t0 = time.perf_counter()
+        st = lib.tp_build_cost_tensors(C.byref(gd), C.byref(td), C.byref(opts), None, C.byref(hs))
+        e2e_t.append(time.perf_counter() - t0)
+        assert st == 0, lib.tp_last_error()
+    e2e_total = torch.tensor([sum(e2e_t)], dtype=torch.float64, device=dev)
+    e2e_evals = torch.tensor([float(ne) * KE], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(e2e_total, op=dist.ReduceOp.MAX)
+        dist.all_reduce(e2e_evals, op=dist.ReduceOp.SUM)
+    e2e_value = float(e2e_evals.item()) / float(e2e_total.item())
+    # keep the GPU loaded until the clock sampler has seen >= 1 s of work
+    t_end = time.perf_counter() + 1.0
+    with torch.cuda.stream(stream):
+        while time.perf_counter() < t_end:
+            plan.execute(cs, stream=sp)
+            stream.synchronize()
+    clk = clocks.stop()
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+
+    k4_mean = sum(k4_ms) / len(k4_ms)
+    peak, peak_kind = measured_peak()
+    achieved = BYTES_PER_EVAL * ne / (k4_mean / 1e3) / 1e9
+    traffic, traffic_edges = ncu_traffic()
+    if traffic is not None and traffic_edges and traffic_edges != ne:
+        traffic = traffic * ne / traffic_edges
+    line = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "desc": desc, "aux_edges_per_rank": ne, "aux_nodes_per_rank": nn,
+                   "edge_classes": sizes["num_signatures"], "class_pairs": sizes["num_pair_evals"],
+                   "parallelism": f"scenario-sharded x{world}",
+                   "l2": "256 MiB buffer written between timed steps (flush)",
+                   "build_ms_device": total_ms / K, "build_ms_e2e": sum(e2e_t) / KE * 1e3},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": "expand_kernel (K4 fan-out)",
+                     "kernel_ms": k4_mean, "bytes_per_launch": BYTES_PER_EVAL * ne,
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                     "kernel_share_of_step": k4_mean / (total_ms / K)},
+        "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(sizes["h2d_bytes"]),
+                "d2h_bytes_per_step": int(BYTES_PER_EVAL * (ne + nn)),
+                "how": "tp_build_cost_tensors (host graph in, pinned host tensors out), wall clock"},
+        "gpu_launches": int(launches * K),
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(flat, t, ne)
+    else:
+        line["cpu_baseline"] = None
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--workload", default="cfg4", choices=("cfg1", "cfg2", "cfg3", "cfg4"))
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_engine(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -223,176 +223,188 @@ struct Trace {
   double sec[kMaxOps];
 };
 
-// Unification state of one side: parts of each tensor dim, outer first.
-template <int RM>
-struct Parts {
-  uint8_t n[RM];
-  uint8_t e[RM][kMaxPD];
-  int8_t m[RM][kMaxPD];
+// ---------------------------------------------------------------------------
+// Unification as a bitmask closure (redistribution.hpp:259-346).
+//
+// Exponent "positions": device position c (0..n) is the cumulative log2
+// extent from the innermost device dim; tensor position c (0..t_i) of dim i
+// is the cumulative log2 extent of its parts from the OUTERMOST side. A
+// layout mapping tensor dim i to an original device dim m of log2 extent x
+// whose lower device position is a places the outer x bits of dim i on that
+// dim, outermost first (reexpress_layout, :120-156): tensor position c in
+// (0, x) corresponds to device position a + x - c. The reference's restart
+// loop (refine_side :167-221 + split_device_dim :226-252) only ever adds
+// boundaries forced by
+//   R1  a tensor boundary strictly inside a mapped region -> the
+//       corresponding device boundary (device split),
+//   R2  a device boundary strictly inside a mapped region -> the
+//       corresponding tensor boundary (re-expression / part split),
+//   R3  both sides share the union of boundaries of each tensor dim,
+// and stops exactly when none applies, so its result is the least fixpoint
+// of R1-R3 from the step-1 device boundaries (both matrices' cumulative
+// products, :270-289). Device boundaries fit one uint32 (n <= 16) and every
+// tensor boundary lies inside some region (< n), so the closure is a few
+// bit-reversals per region; a part's map is the unified dim whose upper
+// device position mirrors the part's start, or -1 once the part starts past
+// the region (the "outer sub-part keeps the map" rule, :197-206). The
+// divisibility checks of expand_over_run (:92-115) reduce to x <= t_i; every
+// other check of the loop holds for power-of-two matrices, and the loop
+// needs at most n-1 device splits (< 64 rounds).
+// ---------------------------------------------------------------------------
+
+TP_HD uint32_t brev32(uint32_t v) {
+#ifdef __CUDA_ARCH__
+  return __brev(v);
+#else
+  v = ((v >> 1) & 0x55555555u) | ((v & 0x55555555u) << 1);
+  v = ((v >> 2) & 0x33333333u) | ((v & 0x33333333u) << 2);
+  v = ((v >> 4) & 0x0F0F0F0Fu) | ((v & 0x0F0F0F0Fu) << 4);
+  v = ((v >> 8) & 0x00FF00FFu) | ((v & 0x00FF00FFu) << 8);
+  return (v >> 16) | (v << 16);
+#endif
+}
+
+TP_HD int popc32(uint32_t v) {
+#ifdef __CUDA_ARCH__
+  return __popc(v);
+#else
+  return __builtin_popcount(v);
+#endif
+}
+
+TP_HD int ffs32(uint32_t v) {  // index of the lowest set bit, v != 0
+#ifdef __CUDA_ARCH__
+  return __ffs(v) - 1;
+#else
+  return __builtin_ctz(v);
+#endif
+}
+
+// bit j (1 <= j < x) of v  ->  bit x - j
+TP_HD uint32_t mirror(uint32_t v, int x) { return brev32(v) >> (31 - x); }
+
+TP_HD uint32_t low_bits(int x) { return x >= 32 ? 0xffffffffu : ((1u << x) - 1u); }
+
+struct Unified {
+  int next;          // unified depth
+  uint32_t D;        // device boundaries (positions 1..n-1)
+  int U;             // unified rank
+  int8_t from[kMaxU];
+  int8_t to[kMaxU];
+  uint8_t ext[kMaxD];
 };
 
-// redistribution.hpp:120-156 (re-expression over the step-1 unified matrix),
-// including expand_over_run (:92-115).
-template <int RM>
-TP_HD int reexpress(const Lay& L, const DimT* dt, const uint8_t* ext, int next, Parts<RM>& P, int R) {
-  uint8_t ocum[kMaxD + 1], ucum[kMaxD + 1];
+// Regions of one side: a[i], x[i] (x = 0: unmapped dim).
+struct Regions {
+  uint8_t a[kMaxR];
+  uint8_t x[kMaxR];
+};
+
+TP_HD void regions_of(const Lay& L, int R, Regions& g, uint32_t& D) {
+  uint8_t ocum[kMaxD + 1];
   ocum[0] = 0;
-  for (int k = 0; k < L.depth; ++k) ocum[k + 1] = (uint8_t)(ocum[k] + L.mx[k]);
-  ucum[0] = 0;
-  for (int u = 0; u < next; ++u) ucum[u + 1] = (uint8_t)(ucum[u] + ext[u]);
-  // every original dim of extent > 1 must be covered by unified dims (:140)
   for (int k = 0; k < L.depth; ++k) {
-    if (L.mx[k] == 0) continue;
-    bool any = false;
-    for (int u = next - 1; u >= 0; --u)
-      any |= ucum[u] >= ocum[k] && ucum[u + 1] <= ocum[k + 1] && ext[u] > 0;
-    if (!any) return kNotUnifiable;
+    ocum[k + 1] = (uint8_t)(ocum[k] + L.mx[k]);
+    D |= 1u << ocum[k + 1];
   }
   for (int i = 0; i < R; ++i) {
     const int m = L.map[i];
-    if (m < 0 || L.mx[m] == 0) {
-      P.n[i] = 1;
-      P.e[i][0] = dt[i].t;
-      P.m[i][0] = -1;
-      continue;
-    }
-    int rem = dt[i].t, np = 0, last = -1;
-    for (int u = next - 1; u >= 0; --u) {  // run_of[m], outer to inner
-      if (!(ucum[u] >= ocum[m] && ucum[u + 1] <= ocum[m + 1] && ext[u] > 0)) continue;
-      if (last >= 0) {  // the previous run member was not the last one
-        if (rem < ext[last]) return kFactorization;
-        P.e[i][np] = ext[last];
-        P.m[i][np] = (int8_t)last;
-        ++np;
-        rem -= ext[last];
-      }
-      last = u;
-    }
-    if (rem < ext[last]) return kFactorization;
-    P.e[i][np] = (uint8_t)rem;
-    P.m[i][np] = (int8_t)last;
-    P.n[i] = (uint8_t)(np + 1);
-  }
-  return kOk;
-}
-
-// redistribution.hpp:167-221 on one dim. Returns kOk (refined), -1 (device
-// split requested: *sk, *sy) or an error. Boundaries: bit c of `bmask` set
-// for every power-of-two boundary 2^c.
-template <int RM>
-TP_HD int refine_dim(Parts<RM>& P, int i, uint64_t bmask, const DimT& dt, const uint8_t* ext,
-                     int* sk, int* sy) {
-  uint8_t ne[kMaxPD];
-  int8_t nm[kMaxPD];
-  int nn = 0, pos = 0;
-  const int n = P.n[i];
-  for (int j = 0; j < n; ++j) {
-    const int e = P.e[i][j], m = P.m[i][j];
-    const int end = pos + e;
-    const int limit = (j == n - 1) ? end + (dt.odd ? 1 : 0) : end;  // cut c inside iff pos < c < limit
-    uint64_t cuts = 0;
-    if (limit > pos + 1) {
-      const uint64_t hi = limit >= 64 ? ~0ull : ((1ull << limit) - 1ull);
-      const uint64_t lo = (pos + 1) >= 64 ? ~0ull : ((1ull << (pos + 1)) - 1ull);
-      cuts = bmask & hi & ~lo;
-    }
-    if (cuts == 0) {
-      if (nn >= kMaxPD) return kCapacity;
-      ne[nn] = (uint8_t)e;
-      nm[nn] = (int8_t)m;
-      ++nn;
+    if (m >= 0 && L.mx[m] > 0) {
+      g.a[i] = ocum[m];
+      g.x[i] = L.mx[m];
     } else {
-      int c1 = 0;
-      while (!((cuts >> c1) & 1ull)) ++c1;
-      if (m >= 0 && c1 - pos < ext[m]) {  // d % f1 == 0 && f1 > 1: split
-        *sk = m;
-        *sy = c1 - pos;
-        return -1;
-      }
-      // replicated part, or mapped part whose outer piece keeps the map
-      int prev = pos;
-      bool first = true;
-      for (int c = c1; c < 64; ++c) {
-        if (!((cuts >> c) & 1ull)) continue;
-        if (nn >= kMaxPD) return kCapacity;
-        ne[nn] = (uint8_t)(c - prev);
-        nm[nn] = (int8_t)((first && m >= 0) ? m : -1);
-        ++nn;
-        prev = c;
-        first = false;
-      }
-      if (nn >= kMaxPD) return kCapacity;
-      ne[nn] = (uint8_t)(end - prev);
-      nm[nn] = -1;
-      ++nn;
+      g.a[i] = 0;
+      g.x[i] = 0;
     }
-    pos = end;
   }
-  P.n[i] = (uint8_t)nn;
-  for (int j = 0; j < nn; ++j) {
-    P.e[i][j] = ne[j];
-    P.m[i][j] = nm[j];
-  }
-  return kOk;
 }
 
-// redistribution.hpp:226-252
-template <int RM>
-TP_HD int split_device_dim(uint8_t* ext, int& next, int k, int y, Parts<RM>& A, Parts<RM>& B, int R) {
-  if (next + 1 > kMaxD) return kCapacity;
-  const int inner = ext[k] - y;
-  ext[k] = (uint8_t)inner;
-  for (int u = next; u > k + 1; --u) ext[u] = ext[u - 1];
-  ext[k + 1] = (uint8_t)y;
-  ++next;
-  Parts<RM>* sides[2] = {&A, &B};
-  for (int s = 0; s < 2; ++s) {
-    Parts<RM>& P = *sides[s];
-    for (int i = 0; i < R; ++i) {
-      uint8_t ne[kMaxPD];
-      int8_t nm[kMaxPD];
-      int nn = 0;
-      for (int j = 0; j < P.n[i]; ++j) {
-        const int e = P.e[i][j], m = P.m[i][j];
-        if (m == k) {
-          if (e < y || e - y < inner) return kDeviceSplit;
-          if (nn + 2 > kMaxPD) return kCapacity;
-          ne[nn] = (uint8_t)y;
-          nm[nn++] = (int8_t)(k + 1);
-          ne[nn] = (uint8_t)(e - y);
-          nm[nn++] = (int8_t)k;
-        } else {
-          if (nn >= kMaxPD) return kCapacity;
-          ne[nn] = (uint8_t)e;
-          nm[nn++] = (int8_t)(m > k ? m + 1 : m);
-        }
-      }
-      P.n[i] = (uint8_t)nn;
-      for (int j = 0; j < nn; ++j) {
-        P.e[i][j] = ne[j];
-        P.m[i][j] = nm[j];
+// Returns kOk or an error; fills u (and the trace's part structure).
+TP_HD int unify_bits(int R, const Lay& F, const Lay& T, const DimT* dt, Unified& u, Trace* tr) {
+  Regions gf, gt;
+  uint32_t D = 0;
+  regions_of(F, R, gf, D);
+  regions_of(T, R, gt, D);
+  int n = 0;
+  for (int k = 0; k < F.depth; ++k) n += F.mx[k];
+  int nt = 0;
+  for (int k = 0; k < T.depth; ++k) nt += T.mx[k];
+  if (n != nt) return kNotUnifiable;  // :264-268
+  if (n > kMaxD) return kCapacity;
+  // expand_over_run divisibility (:102-111): the region must fit in t_i
+  for (int i = 0; i < R; ++i)
+    if (gf.x[i] > dt[i].t) return kFactorization;
+  for (int i = 0; i < R; ++i)
+    if (gt.x[i] > dt[i].t) return kFactorization;
+  D &= ~1u & low_bits(n);  // interior device boundaries only
+  uint32_t P[kMaxR];
+  for (int i = 0; i < R; ++i) P[i] = 0;
+  for (bool changed = true; changed;) {
+    changed = false;
+    for (int s = 0; s < 2; ++s) {
+      const Regions& g = s ? gt : gf;
+      for (int i = 0; i < R; ++i) {
+        const int x = g.x[i], a = g.a[i];
+        if (x < 2) continue;
+        const uint32_t win = low_bits(x) & ~1u;
+        const uint32_t tb = mirror((D >> a) & win, x) & win;  // R2
+        const uint32_t db = (mirror(P[i] & win, x) & win) << a;  // R1
+        if ((tb & ~P[i]) | (db & ~D)) changed = true;
+        P[i] |= tb;
+        D |= db;
       }
     }
   }
+  // unified device dims: positions of D plus n
+  u.D = D;
+  u.next = 0;
+  if (n > 0) {
+    int prev = 0;
+    uint32_t rest = D | (1u << n);
+    while (rest) {
+      const int c = ffs32(rest);
+      rest &= rest - 1;
+      u.ext[u.next++] = (uint8_t)(c - prev);
+      prev = c;
+    }
+  }
+  // unified axes and maps (:330-345)
+  int U = 0;
+  for (int i = 0; i < R; ++i) {
+    uint32_t bnd = P[i];
+    int c = 0;
+    for (;;) {
+      if (U >= kMaxU) return kCapacity;
+      int8_t mf = -1, mt = -1;
+      if (c < gf.x[i]) mf = (int8_t)popc32(D & low_bits(gf.a[i] + gf.x[i] - c));
+      if (c < gt.x[i]) mt = (int8_t)popc32(D & low_bits(gt.a[i] + gt.x[i] - c));
+      u.from[U] = mf;
+      u.to[U] = mt;
+      const int next_c = bnd ? ffs32(bnd) : (int)dt[i].t;
+      if (tr) {
+        tr->pe[U] = (uint8_t)(next_c - c);
+        tr->plast[U] = bnd == 0;
+        tr->pdim[U] = (uint8_t)i;
+      }
+      ++U;
+      if (!bnd) break;
+      c = next_c;
+      bnd &= bnd - 1;
+    }
+  }
+  u.U = U;
+  if (tr) {
+    tr->depth = u.next;
+    for (int k = 0; k < u.next; ++k) tr->ext[k] = u.ext[k];
+    tr->urank = U;
+    for (int q = 0; q < U; ++q) {
+      tr->from_map[q] = u.from[q];
+      tr->to_map[q] = u.to[q];
+    }
+    tr->nops = 0;
+  }
   return kOk;
 }
-
-template <int RM>
-TP_HD uint64_t boundary_mask(const Parts<RM>& P, int i) {
-  uint64_t b = 0;
-  int c = 0;
-  for (int j = 0; j + 1 < P.n[i]; ++j) {  // the last cumulative product is E
-    c += P.e[i][j];
-    b |= 1ull << c;
-  }
-  return b;
-}
-
-// Shard-size bookkeeping and the per-op price (cost_model.hpp:176-263) for
-// the working map `w` (unified rank u) BEFORE the op.
-struct PriceState {
-  int s;  // sum of log2 extents of mapped entries of the working map
-};
 
 // infer_ct_allgather_dim (cost_model.hpp:108-135) with cnt[k] = number of
 // working-map entries equal to k.
@@ -417,8 +429,9 @@ TP_HD void ct_gather(const uint8_t* ext, const uint8_t* cnt, int g, int64_t L, i
   }
 }
 
-// One AllGather (a2a=false) or AllToAll on device dim g: returns seconds and
-// adds the plan volume (redistribution.hpp:521-553) to *vol.
+// One AllGather (a2a=false) or AllToAll on device dim g with s = log2 of
+// the working map's shard divisor: returns seconds and adds the plan volume
+// (redistribution.hpp:521-553) to *vol.
 TP_HD double price_op(bool a2a, int g, const uint8_t* ext, const uint8_t* cnt, int s,
                       double bytes, const Env& env, double* vol, int64_t* ct_out) {
   const double shard = bytes / exp2d(s);
@@ -447,113 +460,37 @@ TP_HD double price_op(bool a2a, int g, const uint8_t* ext, const uint8_t* cnt, i
   return scale * v / bw;
 }
 
-// unify (redistribution.hpp:259-346) + inference (:419-451, all2all on) +
-// pricing (:533-553, cost_model.hpp:233-263) of one (from, to) pair.
-// Inputs are layouts over power-of-two matrices with equal totals.
-template <int RM>
-TP_HD int redist_cost(int R, const Lay& F, const Lay& T, const DimT* dt, double bytes, const Env& env,
-                      double& sec_out, double& vol_out, Trace* tr) {
-  // ---- step 1: unified matrix = union of inner cumulative exponents ----
-  uint32_t cm = 0;
-  {
-    int c = 0;
-    for (int k = 0; k < F.depth; ++k) {
-      c += F.mx[k];
-      if (c > 0) cm |= 1u << c;
-    }
-    c = 0;
-    for (int k = 0; k < T.depth; ++k) {
-      c += T.mx[k];
-      if (c > 0) cm |= 1u << c;
-    }
-  }
-  uint8_t ext[kMaxD + 1];
-  int next = 0;
-  {
-    int prev = 0;
-    for (int c = 1; c < 32; ++c) {
-      if (!((cm >> c) & 1u)) continue;
-      if (next >= kMaxD) return kCapacity;
-      ext[next++] = (uint8_t)(c - prev);
-      prev = c;
-    }
-  }
-  Parts<RM> A, B;
-  int st = reexpress<RM>(F, dt, ext, next, A, R);
+// unify + inference (:419-451, all2all on) + pricing (:533-553,
+// cost_model.hpp:233-263) of one (from, to) pair of power-of-two layouts.
+TP_HD int redist_cost(int R, const Lay& F, const Lay& T, const DimT* dt, double bytes,
+                      const Env& env, double& sec_out, double& vol_out, Trace* tr) {
+  if (R < 0 || R > kMaxR) return kCapacity;
+  Unified u;
+  int st = unify_bits(R, F, T, dt, u, tr);
   if (st) return st;
-  st = reexpress<RM>(T, dt, ext, next, B, R);
-  if (st) return st;
-
-  // ---- step 2: refine the shape, splitting device dims on demand ----
-  for (int rounds = 1;; ++rounds) {
-    if (rounds > 64) return kNoConverge;
-    bool restarted = false;
-    for (int i = 0; i < R && !restarted; ++i) {
-      const uint64_t bm = boundary_mask<RM>(A, i) | boundary_mask<RM>(B, i);
-      int sk = -1, sy = 0;
-      int r = refine_dim<RM>(A, i, bm, dt[i], ext, &sk, &sy);
-      if (r == kOk) r = refine_dim<RM>(B, i, bm, dt[i], ext, &sk, &sy);
-      if (r == -1) {
-        st = split_device_dim<RM>(ext, next, sk, sy, A, B, R);
-        if (st) return st;
-        restarted = true;
-      } else if (r != kOk) {
-        return r;
-      }
-    }
-    if (!restarted) break;
-  }
-
-  // ---- read-off (:330-345) ----
-  int8_t w[kMaxU], to[kMaxU];
-  int U = 0;
-  for (int i = 0; i < R; ++i) {
-    if (A.n[i] != B.n[i]) return kRefineMismatch;
-    for (int j = 0; j < A.n[i]; ++j) {
-      if (A.e[i][j] != B.e[i][j]) return kRefineMismatch;
-      if (U >= kMaxU) return kCapacity;
-      if (tr) {
-        tr->pe[U] = A.e[i][j];
-        tr->plast[U] = j == A.n[i] - 1;
-        tr->pdim[U] = (uint8_t)i;
-      }
-      w[U] = A.m[i][j];
-      to[U] = B.m[i][j];
-      ++U;
-    }
-  }
-  if (tr) {
-    tr->depth = next;
-    for (int k = 0; k < next; ++k) tr->ext[k] = ext[k];
-    tr->urank = U;
-    for (int u = 0; u < U; ++u) {
-      tr->from_map[u] = w[u];
-      tr->to_map[u] = to[u];
-    }
-    tr->nops = 0;
-  }
-
-  // ---- inference with on-the-fly pricing ----
+  const int U = u.U;
+  int8_t* w = u.from;
+  const int8_t* to = u.to;
+  const uint8_t* ext = u.ext;
   uint8_t cnt[kMaxD];
   int8_t first_to[kMaxD];
   for (int k = 0; k < kMaxD; ++k) {
     cnt[k] = 0;
     first_to[k] = -1;
   }
-  int s = 0;
-  for (int u = 0; u < U; ++u) {
-    if (w[u] >= 0) {
-      cnt[w[u]]++;
-      s += ext[w[u]];
+  int s = 0, mism = 0;
+  for (int q = 0; q < U; ++q) {
+    if (w[q] >= 0) {
+      cnt[w[q]]++;
+      s += ext[w[q]];
     }
+    mism += w[q] != to[q];
   }
-  for (int u = U - 1; u >= 0; --u)
-    if (to[u] >= 0) first_to[to[u]] = (int8_t)u;
-  int mism = 0;
-  for (int u = 0; u < U; ++u) mism += w[u] != to[u];
+  for (int q = U - 1; q >= 0; --q)
+    if (to[q] >= 0) first_to[to[q]] = (int8_t)q;
 
   double sec = 0, vol = 0;
-  int guard = (next + 1) * (U + 1) * 4 + 16;
+  int guard = (u.next + 1) * (U + 1) * 4 + 16;
   auto record = [&](int kind, int k, int i, int j, int fb, int64_t ct, double sc) {
     if (!tr) return;
     if (tr->nops >= kMaxOps) {
@@ -583,7 +520,7 @@ TP_HD int redist_cost(int R, const Lay& F, const Lay& T, const DimT* dt, double 
           w[i] = (int8_t)k;
           cnt[k]++;
           s += ext[k];
-          mism -= 1;  // w[i] now equals to[i]
+          mism -= 1;
           progress = true;
         }
       }
@@ -600,9 +537,7 @@ TP_HD int redist_cost(int R, const Lay& F, const Lay& T, const DimT* dt, double 
             const double c = price_op(true, k, ext, cnt, s, bytes, env, &vol, tr ? &ct : nullptr);
             sec += c;
             record(2, k, i, j, 0, ct, c);
-            // w[i]: k -> -1 ; w[j]: -1 -> k (to[j] == k)
-            mism += (to[i] == -1) ? -1 : 0;
-            mism -= 1;
+            mism -= (to[i] == -1) ? 2 : 1;
             w[i] = -1;
             w[j] = (int8_t)k;
             a2a = true;
@@ -612,7 +547,7 @@ TP_HD int redist_cost(int R, const Lay& F, const Lay& T, const DimT* dt, double 
       }
     }
     if (!mism) break;
-    // InferAllGather (:387-401), else the fallback (:403-417)
+    // InferAllGather (:387-401), else the fallback gather (:403-417)
     int gi = -1, fb = 0;
     for (int i = 0; i < U; ++i) {
       if (w[i] >= 0 && to[i] == -1) {
@@ -638,24 +573,16 @@ TP_HD int redist_cost(int R, const Lay& F, const Lay& T, const DimT* dt, double 
     w[gi] = -1;
     cnt[k]--;
     s -= ext[k];
-    mism += (to[gi] == -1) ? -1 : 0;  // a regular gather fixes the entry
-    if (fb) mism += 0;                // a fallback gather leaves it mismatched
+    if (to[gi] == -1) mism -= 1;
   }
   sec_out = sec;
   vol_out = vol;
   return kOk;
 }
 
-// Dispatch on the tensor rank: rank <= 2 covers every model builder.
 TP_HD int redist_cost_any(int R, const Lay& F, const Lay& T, const DimT* dt, double bytes,
                           const Env& env, double& sec, double& vol, Trace* tr) {
-  if (R == 2) return redist_cost<2>(2, F, T, dt, bytes, env, sec, vol, tr);
-  if (R >= 1 && R <= 4) return redist_cost<4>(R, F, T, dt, bytes, env, sec, vol, tr);
-  if (R >= 5 && R <= kMaxR) return redist_cost<kMaxR>(R, F, T, dt, bytes, env, sec, vol, tr);
-  // rank 0: both maps empty, equal layouts; nothing to move
-  sec = 0;
-  vol = 0;
-  return R == 0 ? kOk : kCapacity;
+  return redist_cost(R, F, T, dt, bytes, env, sec, vol, tr);
 }
 
 // ---------------------------------------------------------------------------
@@ -696,7 +623,7 @@ TP_HD int run_query(const QueryPOD& q, Result& r) {
   r.num_ops = 0;
   r.volume_bytes = 0;
   r.seconds = 0;
-  if (q.rank < 0 || q.rank > kMaxR || q.fdepth > kMaxAxes || q.tdepth > kMaxAxes) return kCapacity;
+  if (q.rank < 0 || q.rank > kMaxR || q.fdepth > kMaxD || q.tdepth > kMaxD) return kCapacity;
   Lay F, T;
   F.depth = (uint8_t)q.fdepth;
   T.depth = (uint8_t)q.tdepth;

@@ -1,21 +1,27 @@
 // tp_engine.cu — B200 (sm_100a) cost-tensor engine behind include/taps_b200.h.
 //
 // Replaces topoplan::build_auxiliary_graph (aux_graph.hpp:211-315).
-// Pipeline of one build (all on one stream):
-//   K1 table_kernel   strategy tables, one thread per strategy (unranking)
-//   K2 node_kernel    one thread per aux node: divisibility, intra-operator
-//                     AllReduce cost/volume, memory (aux_graph.hpp:120-167)
-//   K3 pair_kernel    one thread per (edge class, su, sw): unify + sequence
-//                     inference + topology-aware pricing (tp_core.cuh)
-//   K4 expand_kernel  write-bound fan-out of the class tables to every aux
-//                     edge: cost = intra(w) + redist, 256-bit stores
-//   K5 rowmin_kernel  (optional) warp per (edge, su) row, lanes over sw,
-//                     shuffle min: the solver's cond_min (solver.hpp:239-253)
 //
-// Edges are grouped into *classes* on the host: two graph edges whose
-// (shape, producer slicing, consumer slicing, axis counts, tensor bytes)
-// agree have identical |Su| x |Sw| redistribution tables, so each class is
-// priced once (the reference's memo, aux_graph.hpp:257-271, made static).
+// Host analysis (tp_plan_create) groups the work into classes:
+//   * node classes — operators whose slicing, tensor shapes, element sizes,
+//     fed inputs and in-degree agree have identical per-strategy costs
+//     (aux_graph.hpp:120-167); each class is priced once per strategy;
+//   * edge classes — graph edges whose (shape, tensor bytes, producer and
+//     consumer slicing, axis counts) agree have identical |Su| x |Sw|
+//     redistribution tables; each class is priced once per pair (the
+//     reference's memo, aux_graph.hpp:257-271, made static).
+// Device pipeline of one build (one stream):
+//   build_kernel   one thread per (node class, strategy) and per
+//                  (edge class, su, sw): node costs, then unify + sequence
+//                  inference + topology-aware pricing (tp_core.cuh); the node
+//                  part also fans its row out to every member operator
+//   expand_kernel  the write-bound fan-out: every aux edge
+//                  cost = intra(w) + redist, volume likewise, memory =
+//                  mem(w) / in_degree(w), coalesced fp64 stores
+//   rowmin_kernel  (optional) warp per (edge, su) row, lanes over sw,
+//                  shuffle min: the solver's cond_min (solver.hpp:239-253)
+// The strategy tables (layout.hpp:270-328) are built once per plan by
+// table_kernel at upload and cached per device.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -23,7 +29,6 @@
 #include <cstdint>
 #include <cstring>
 #include <map>
-#include <mutex>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -80,31 +85,22 @@ const char* kind_text(int kind) {
   }
 }
 
-#define CUDA_TRY(expr)                                                        \
-  do {                                                                        \
-    cudaError_t _e = (expr);                                                  \
-    if (_e != cudaSuccess)                                                    \
-      return set_err(TP_ERR_CUDA, 0, std::string(#expr ": ") + cudaGetErrorString(_e)); \
+#define CUDA_TRY(expr)                                                                       \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      return set_err(TP_ERR_CUDA, 0, std::string(#expr ": ") + cudaGetErrorString(_e));      \
   } while (0)
 
 // Error keys: (order << 6) | kind; the smallest key is the error the
-// reference would throw first (its iteration order).
+// reference would throw first (its iteration order). Node phase orders are
+// 1 + 2*node (+1 for derivation errors), edge phase orders start at 2^46.
 constexpr uint64_t kEdgePhase = 1ull << 46;
 __host__ __device__ inline uint64_t ekey(uint64_t order, int kind) { return (order << 6) | (uint64_t)kind; }
 
 // ---------------------------------------------------------------------------
 // device descriptors
 // ---------------------------------------------------------------------------
-struct OpDesc {
-  int64_t node_base;
-  int32_t table;  // entry offset of the op's strategy table
-  int32_t p;
-  int32_t chk_begin, chk_end;
-  int32_t occ_begin, occ_end;
-  int32_t slot_begin;
-  int32_t pad;
-};
-
 struct SliceChk {
   int16_t slot;  // -1: the slice names a tensor the op does not carry
   int8_t axis;
@@ -125,9 +121,17 @@ struct Occ {
   uint8_t in_memory;   // output, or input not fed by an edge
 };
 
-struct SigDesc {
+struct ClassDesc {     // a node class
+  int64_t row_base;    // first row of the class in the class row tables
+  int64_t first_node;  // aux node id of strategy 0 of the class's first member
+  double indeg;        // in-degree shared by the members (memory / in_degree)
+  int32_t p, table;
+  int32_t chk_begin, chk_end, occ_begin, occ_end, slot_begin, mem_begin, mem_end, pad;
+};
+
+struct SigDesc {       // an edge class
   int64_t pair_begin;
-  int64_t first_aux;  // aux id of (su=0, sw=0) of the class's first edge
+  int64_t first_aux;   // aux id of (su=0, sw=0) of the class's first edge
   double bytes;
   int32_t R, Su, Sw, tab_u, tab_w, has_override;
   int8_t sa_u[tpk::kMaxR];
@@ -136,23 +140,27 @@ struct SigDesc {
 };
 
 struct EdgeDesc {
-  int64_t aux_base;  // aux id of the edge's (0, 0)
-  int64_t nb_u, nb_w;
-  double indeg_w;
+  int64_t aux_base;    // aux id of the edge's (0, 0)
+  int64_t nb_u, nb_w;  // first aux node of the producer / consumer
+  int64_t wrow;        // class row of the consumer's strategy 0
   int32_t sig, e;
 };
 
 struct Work {
   int32_t sig;
-  int32_t ebeg, eend;  // into sig_edges
-  int32_t pad;
-  int64_t j0;          // first pair of the tile within the class block
+  int32_t ebeg, eend;  // into the per-execute edge list
+  int32_t j0;          // first pair of the tile within the class block
 };
 
 struct TableDesc {
   int64_t offset, count;
   int32_t p, n;
 };
+
+constexpr int kBuildThreads = 64;
+constexpr int kExpThreads = 256;
+constexpr int kExpPer = 8;
+constexpr int kExpTile = kExpThreads * kExpPer;  // class pairs per CTA tile
 
 // ---------------------------------------------------------------------------
 // kernels
@@ -161,6 +169,7 @@ __device__ __forceinline__ void flag_error(unsigned long long* err, uint64_t key
   atomicMin(err, (unsigned long long)key);
 }
 
+// K0 (at upload): strategy tables by unranking (layout.hpp:270-328).
 __global__ void table_kernel(const TableDesc* __restrict__ tabs, int ntabs, int64_t total,
                              Strat* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -172,229 +181,222 @@ __global__ void table_kernel(const TableDesc* __restrict__ tabs, int ntabs, int6
   out[i] = s;
 }
 
-__global__ void __launch_bounds__(256) node_kernel(
-    const OpDesc* __restrict__ ops, int nops, int64_t total_nodes, int n_log2, Env env,
-    const Strat* __restrict__ tables, const SliceChk* __restrict__ chks,
-    const SlotDesc* __restrict__ slots, const Occ* __restrict__ occs, double* __restrict__ o_sec,
-    double* __restrict__ o_vol, double* __restrict__ o_mem, double* __restrict__ c_sec,
-    double* __restrict__ c_vol, double* __restrict__ c_mem, unsigned long long* err) {
-  const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (node >= total_nodes) return;
-  int lo = 0, hi = nops - 1;  // last op with node_base <= node
+struct BuildArgs {
+  // node classes
+  const ClassDesc* classes;
+  int ncls;
+  int64_t total_rows;
+  int64_t node_blocks;
+  const SliceChk* chks;
+  const SlotDesc* slots;
+  const Occ* occs;
+  const int64_t* member_nb;  // aux node id of strategy 0 of every class member
+  double* cls_sec;
+  double* cls_vol;
+  double* cls_memdiv;
+  double* node_sec;  // caller outputs (may be null)
+  double* node_vol;
+  double* node_mem;
+  // edge classes
+  const SigDesc* sigs;
+  int nsigs;
+  int64_t total_pairs;
+  const double* overrides;
+  double* r_sec;
+  double* r_vol;
+  // shared
+  const Strat* tables;
+  Env env;
+  int n_log2;
+  unsigned long long* err;
+};
+
+// One aux-node row of a node class (aux_graph.hpp:120-167).
+__device__ void node_row(const BuildArgs& a, int64_t row) {
+  int lo = 0, hi = a.ncls - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (ops[mid].node_base <= node) lo = mid; else hi = mid - 1;
+    if (a.classes[mid].row_base <= row) lo = mid; else hi = mid - 1;
   }
-  const OpDesc od = ops[lo];
-  const Strat st = tables[od.table + (node - od.node_base)];
-  // layout.hpp:349-367: every slice in axis order must divide
-  for (int c = od.chk_begin; c < od.chk_end; ++c) {
-    const SliceChk k = chks[c];
+  const ClassDesc cd = a.classes[lo];
+  const int64_t s = row - cd.row_base;
+  const Strat st = a.tables[cd.table + s];
+  // layout.hpp:349-367: every slice in axis order must divide its extent
+  for (int c = cd.chk_begin; c < cd.chk_end; ++c) {
+    const SliceChk k = a.chks[c];
     int kind = 0;
     if (k.slot < 0) kind = tpk::kUnknownSliceTensor;
     else if (st.deg[k.axis] > k.v) kind = tpk::kIndivisible;
     if (kind) {
-      flag_error(err, ekey(1 + (uint64_t)node * 2 + 1, kind));
-      o_sec[node] = o_vol[node] = o_mem[node] = 0;
+      flag_error(a.err, ekey(1 + (uint64_t)(cd.first_node + s) * 2 + 1, kind));
+      a.cls_sec[row] = a.cls_vol[row] = a.cls_memdiv[row] = 0;
       return;
     }
   }
   double sec = 0, vol = 0, mem = 0;
-  for (int q = od.occ_begin; q < od.occ_end; ++q) {
-    const Occ oc = occs[q];
-    const SlotDesc sd = slots[od.slot_begin + oc.slot];
+  for (int q = cd.occ_begin; q < cd.occ_end; ++q) {
+    const Occ oc = a.occs[q];
+    const SlotDesc sd = a.slots[cd.slot_begin + oc.slot];
     int sdiv = 0;
     for (int d = 0; d < sd.R; ++d)
       if (sd.sa[d] >= 0) sdiv += st.deg[sd.sa[d]];
     const int64_t shard_el = sdiv >= 63 ? 0 : (sd.elements >> sdiv);
-    const double sb = (double)shard_el * sd.es;  // layout.hpp:127-129
+    const double sb = (double)shard_el * sd.es;  // layout.hpp:125-129
     if (oc.in_memory) mem += sb;                 // aux_graph.hpp:151-167
     int glog = 0;
-    for (int a = 0; a < od.p; ++a)
-      if ((oc.nonslicing >> a) & 1) glog += st.deg[a];
+    for (int ax = 0; ax < cd.p; ++ax)
+      if ((oc.nonslicing >> ax) & 1) glog += st.deg[ax];
     if (glog == 0) continue;  // group <= 1
     // infer_ct_allreduce (cost_model.hpp:75-97)
-    const int64_t pd = sdiv > n_log2 ? 0 : ((int64_t)1 << (n_log2 - sdiv));
-    int64_t remain = env.local, dev_in = 1;
+    const int64_t pd = sdiv > a.n_log2 ? 0 : ((int64_t)1 << (a.n_log2 - sdiv));
+    int64_t remain = a.env.local, dev_in = 1;
     for (int k = 0; k < st.depth; ++k) {
       bool contains = false;
-      for (int d = 0; d < sd.R; ++d)
-        contains |= sd.sa[d] >= 0 && st.dmap[sd.sa[d]] == k;
+      for (int d = 0; d < sd.R; ++d) contains |= sd.sa[d] >= 0 && st.dmap[sd.sa[d]] == k;
       const int64_t ek = (int64_t)1 << st.mx[k];
       if (!contains && remain > 1) dev_in *= remain > ek ? ek : remain;
       remain /= ek;
     }
-    const int64_t ct = dev_in >= pd ? 0 : (dev_in > 1 ? env.local / dev_in : env.local);
+    const int64_t ct = dev_in >= pd ? 0 : (dev_in > 1 ? a.env.local / dev_in : a.env.local);
     const double n = (double)((int64_t)1 << glog);
     const double v = 2.0 * (n - 1) / n * sb;  // allreduce_volume, cost_model.hpp:39-43
     vol += v;
-    sec += v / tpk::eff_bw(ct, env);
+    sec += v / tpk::eff_bw(ct, a.env);
   }
-  o_sec[node] = sec;
-  o_vol[node] = vol;
-  o_mem[node] = mem;
-  if (c_sec) c_sec[node] = sec;
-  if (c_vol) c_vol[node] = vol;
-  if (c_mem) c_mem[node] = mem;
+  a.cls_sec[row] = sec;
+  a.cls_vol[row] = vol;
+  a.cls_memdiv[row] = mem / cd.indeg;  // aux_graph.hpp:292
+  if (a.node_sec) {
+    for (int m = cd.mem_begin; m < cd.mem_end; ++m) {
+      const int64_t node = a.member_nb[m] + s;
+      a.node_sec[node] = sec;
+      a.node_vol[node] = vol;
+      a.node_mem[node] = mem;
+    }
+  }
 }
 
-__global__ void __launch_bounds__(128) pair_kernel(
-    const SigDesc* __restrict__ sigs, int nsigs, int64_t total_pairs, Env env,
-    const Strat* __restrict__ tables, const double* __restrict__ overrides,
-    double* __restrict__ r_sec, double* __restrict__ r_vol, unsigned long long* err) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= total_pairs) return;
-  int lo = 0, hi = nsigs - 1;
+// One (edge class, su, sw) pair: redistribution seconds and volume.
+__device__ void pair_row(const BuildArgs& a, int64_t idx) {
+  int lo = 0, hi = a.nsigs - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (sigs[mid].pair_begin <= idx) lo = mid; else hi = mid - 1;
+    if (a.sigs[mid].pair_begin <= idx) lo = mid; else hi = mid - 1;
   }
-  const SigDesc& sg = sigs[lo];
-  const int64_t local = idx - sg.pair_begin;
-  const int64_t su = local / sg.Sw, sw = local - su * sg.Sw;
-  const Strat a = tables[sg.tab_u + su];
-  const Strat b = tables[sg.tab_w + sw];
+  const SigDesc& sg = a.sigs[lo];
+  const int32_t local = (int32_t)(idx - sg.pair_begin);
+  const int32_t su = local / sg.Sw, sw = local - su * sg.Sw;
+  const Strat su_s = a.tables[sg.tab_u + su];
+  const Strat sw_s = a.tables[sg.tab_w + sw];
   Lay F, T;
-  tpk::side_layout(a, sg.sa_u, sg.R, F);
-  tpk::side_layout(b, sg.sa_w, sg.R, T);
+  tpk::side_layout(su_s, sg.sa_u, sg.R, F);
+  tpk::side_layout(sw_s, sg.sa_w, sg.R, T);
   double sec = 0, vol = 0;
-  if (!tpk::same_layout(F, T, sg.R)) {
-    const double bytes = sg.has_override ? overrides[idx] : sg.bytes;
-    const int st = tpk::redist_cost_any(sg.R, F, T, sg.dt, bytes, env, sec, vol, nullptr);
+  if (!tpk::same_layout(F, T, sg.R)) {  // aux_graph.hpp:260
+    const double bytes = sg.has_override ? a.overrides[idx] : sg.bytes;
+    const int st = tpk::redist_cost(sg.R, F, T, sg.dt, bytes, a.env, sec, vol, nullptr);
     if (st) {
-      flag_error(err, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
+      flag_error(a.err, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
       sec = vol = 0;
     }
   }
-  r_sec[idx] = sec;
-  r_vol[idx] = vol;
+  a.r_sec[idx] = sec;
+  a.r_vol[idx] = vol;
 }
 
-constexpr int kExpThreads = 256;
-constexpr int kExpTile = kExpThreads * 4;  // class pairs per CTA tile
-constexpr int kExpMaxSw = 1024;            // node rows staged in smem up to this width
-
-__device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {
-  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
-               : "memory");
+// K1: node classes in blocks [0, node_blocks), edge-class pairs after.
+__global__ void __launch_bounds__(kBuildThreads) build_kernel(BuildArgs a) {
+  if ((int64_t)blockIdx.x < a.node_blocks) {
+    const int64_t row = (int64_t)blockIdx.x * kBuildThreads + threadIdx.x;
+    if (row < a.total_rows) node_row(a, row);
+  } else {
+    const int64_t idx = ((int64_t)blockIdx.x - a.node_blocks) * kBuildThreads + threadIdx.x;
+    if (idx < a.total_pairs) pair_row(a, idx);
+  }
 }
 
+// K2: fan-out of the class tables to every aux edge of the range. Each CTA
+// owns a tile of one edge class's pair block and a chunk of the class's
+// edges; a thread keeps its kExpPer pairs (class-table values and consumer
+// strategy) in registers and, for every edge, writes them at
+// aux_base(edge) + pair: lane-contiguous, so each warp store is 256 B.
 __global__ void __launch_bounds__(kExpThreads) expand_kernel(
     const Work* __restrict__ work, const SigDesc* __restrict__ sigs,
-    const int32_t* __restrict__ sig_edges, const EdgeDesc* __restrict__ edges,
+    const int32_t* __restrict__ edge_list, const EdgeDesc* __restrict__ edges,
     const double* __restrict__ r_sec, const double* __restrict__ r_vol,
-    const double* __restrict__ n_sec, const double* __restrict__ n_vol,
-    const double* __restrict__ n_mem, int64_t out_offset, double* __restrict__ e_sec,
+    const double* __restrict__ cls_sec, const double* __restrict__ cls_vol,
+    const double* __restrict__ cls_memdiv, int64_t out_offset, double* __restrict__ e_sec,
     double* __restrict__ e_vol, double* __restrict__ e_mem, char* __restrict__ records) {
-  __shared__ double rs[kExpTile + 8], rv[kExpTile + 8];
-  __shared__ double is_[kExpMaxSw], iv_[kExpMaxSw], im_[kExpMaxSw];
   const Work wk = work[blockIdx.x];
   const SigDesc& sg = sigs[wk.sig];
-  const int64_t Sw = sg.Sw;
-  const int64_t P = (int64_t)sg.Su * Sw;
-  const int64_t j0 = wk.j0;
-  const int64_t j1 = min(j0 + (int64_t)kExpTile, P);
-  // class-table tile [j0-4, j1+4) into smem (reused for every edge of the chunk)
-  for (int64_t j = j0 - 4 + threadIdx.x; j < j1 + 4; j += kExpThreads) {
-    const bool ok = j >= 0 && j < P;
-    rs[j - (j0 - 4)] = ok ? r_sec[sg.pair_begin + j] : 0.0;
-    rv[j - (j0 - 4)] = ok ? r_vol[sg.pair_begin + j] : 0.0;
+  const int32_t Sw = sg.Sw;
+  const int32_t P = sg.Su * Sw;
+  int32_t jj[kExpPer], sw[kExpPer];
+  double rs[kExpPer], rv[kExpPer];
+#pragma unroll
+  for (int k = 0; k < kExpPer; ++k) {
+    const int32_t j = wk.j0 + (int32_t)threadIdx.x + k * kExpThreads;
+    jj[k] = j < P ? j : -1;
+    const int32_t jc = j < P ? j : 0;
+    sw[k] = jc % Sw;
+    rs[k] = r_sec[sg.pair_begin + jc];
+    rv[k] = r_vol[sg.pair_begin + jc];
   }
-  const bool staged = Sw <= kExpMaxSw;
   for (int ei = wk.ebeg; ei < wk.eend; ++ei) {
-    const EdgeDesc ed = edges[sig_edges[ei]];
-    if (staged) {
-      for (int64_t s = threadIdx.x; s < Sw; s += kExpThreads) {
-        is_[s] = n_sec[ed.nb_w + s];
-        iv_[s] = n_vol[ed.nb_w + s];
-        im_[s] = n_mem[ed.nb_w + s] / ed.indeg_w;  // aux_graph.hpp:292
-      }
+    const EdgeDesc ed = edges[edge_list[ei]];
+    const int64_t base = ed.aux_base - out_offset;
+    double c[kExpPer], v[kExpPer], m[kExpPer];
+#pragma unroll
+    for (int k = 0; k < kExpPer; ++k) {  // loads first (memory-level parallelism)
+      c[k] = __ldg(cls_sec + ed.wrow + sw[k]);
+      v[k] = __ldg(cls_vol + ed.wrow + sw[k]);
+      m[k] = __ldg(cls_memdiv + ed.wrow + sw[k]);
     }
-    __syncthreads();
-    const int64_t ob = ed.aux_base - out_offset;  // output index of pair 0
-    const int64_t g0 = (ob + j0) & ~(int64_t)3;
-    for (int64_t a = g0 + 4 * (int64_t)threadIdx.x; a < ob + j1; a += 4 * kExpThreads) {
-      const int64_t jq = a - ob;
-      int64_t sw = jq % Sw;
-      if (sw < 0) sw += Sw;
-      double c[4], v[4], m[4];
-      bool ok[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t j = jq + q;
-        ok[q] = j >= j0 && j < j1;
-        double ws, wv, wm;
-        if (staged) {
-          ws = is_[sw];
-          wv = iv_[sw];
-          wm = im_[sw];
-        } else {
-          ws = n_sec[ed.nb_w + sw];
-          wv = n_vol[ed.nb_w + sw];
-          wm = n_mem[ed.nb_w + sw] / ed.indeg_w;
-        }
-        const int64_t t = (ok[q] ? j : j0) - (j0 - 4);
-        c[q] = ws + rs[t];  // aux_graph.hpp:290-291
-        v[q] = wv + rv[t];
-        m[q] = wm;
-        if (++sw == Sw) sw = 0;
-      }
-      if (ok[0] && ok[3]) {
-        if (e_sec) st_v4(e_sec + a, c[0], c[1], c[2], c[3]);
-        if (e_vol) st_v4(e_vol + a, v[0], v[1], v[2], v[3]);
-        if (e_mem) st_v4(e_mem + a, m[0], m[1], m[2], m[3]);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (!ok[q]) continue;
-          if (e_sec) e_sec[a + q] = c[q];
-          if (e_vol) e_vol[a + q] = v[q];
-          if (e_mem) e_mem[a + q] = m[q];
-        }
-      }
+    for (int k = 0; k < kExpPer; ++k) {
+      if (jj[k] < 0) continue;
+      const int64_t o = base + jj[k];
+      const double cs = c[k] + rs[k];  // aux_graph.hpp:290-291
+      const double vs = v[k] + rv[k];
+      if (e_sec) __stcs(e_sec + o, cs);  // streaming: written once, read by the host
+      if (e_vol) __stcs(e_vol + o, vs);
+      if (e_mem) __stcs(e_mem + o, m[k]);
       if (records) {  // topoplan::AuxEdge, 40 bytes (aux_graph.hpp:52-59)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (!ok[q]) continue;
-          const int64_t j = jq + q;
-          const int64_t su = j / Sw, swq = j - su * Sw;
-          char* rec = records + (a + q) * 40;
-          // 40*i is only 8-byte aligned: two 8-byte stores for the int header
-          *reinterpret_cast<int2*>(rec) = make_int2(ed.e, (int)(ed.nb_u + su));
-          *reinterpret_cast<int2*>(rec + 8) = make_int2((int)(ed.nb_w + swq), 0);
-          *reinterpret_cast<double*>(rec + 16) = c[q];
-          *reinterpret_cast<double*>(rec + 24) = v[q];
-          *reinterpret_cast<double*>(rec + 32) = m[q];
-        }
+        const int32_t su = jj[k] / Sw;
+        char* rec = records + o * 40;
+        *reinterpret_cast<int2*>(rec) = make_int2(ed.e, (int)(ed.nb_u + su));
+        *reinterpret_cast<int2*>(rec + 8) = make_int2((int)(ed.nb_w + sw[k]), 0);
+        *reinterpret_cast<double*>(rec + 16) = cs;
+        *reinterpret_cast<double*>(rec + 24) = vs;
+        *reinterpret_cast<double*>(rec + 32) = m[k];
       }
     }
-    __syncthreads();
   }
 }
 
-// cond_min (solver.hpp:239-253): warp per (edge, su) row, lanes over sw.
+// K3 (optional): cond_min (solver.hpp:239-253), warp per (edge, su) row.
 __global__ void rowmin_kernel(const EdgeDesc* __restrict__ edges, const int64_t* __restrict__ row_base,
-                              int nedges, int64_t nrows, const SigDesc* __restrict__ sigs,
+                              int e0, int nedges, int64_t nrows, const SigDesc* __restrict__ sigs,
                               const double* __restrict__ r_sec, const double* __restrict__ r_vol,
-                              const double* __restrict__ n_sec, const double* __restrict__ n_vol,
+                              const double* __restrict__ cls_sec, const double* __restrict__ cls_vol,
                               double* __restrict__ out_c, double* __restrict__ out_v) {
   const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= nrows) return;
-  int lo = 0, hi = nedges - 1;
+  int lo = 0, hi = nedges - 1;  // row_base is relative to edge e0
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (row_base[mid] <= row) lo = mid; else hi = mid - 1;
   }
-  const EdgeDesc ed = edges[lo];
+  const EdgeDesc ed = edges[e0 + lo];
   const SigDesc& sg = sigs[ed.sig];
   const int64_t su = row - row_base[lo];
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   double mc = inf, mv = inf;
   for (int64_t sw = lane; sw < sg.Sw; sw += 32) {
     const int64_t j = sg.pair_begin + su * sg.Sw + sw;
-    const double c = n_sec[ed.nb_w + sw] + r_sec[j];
-    const double v = n_vol[ed.nb_w + sw] + r_vol[j];
+    const double c = cls_sec[ed.wrow + sw] + r_sec[j];
+    const double v = cls_vol[ed.wrow + sw] + r_vol[j];
     mc = c < mc ? c : mc;
     mv = v < mv ? v : mv;
   }
@@ -420,7 +422,7 @@ __global__ void query_kernel(const tpk::QueryPOD* __restrict__ q, int n, tp_redi
 }
 
 // ---------------------------------------------------------------------------
-// device memory helper
+// host helpers
 // ---------------------------------------------------------------------------
 struct DevBuf {
   void* p = nullptr;
@@ -468,19 +470,21 @@ int v2_capped(int64_t v) {
 // ---------------------------------------------------------------------------
 // Device memory and stream of a plan. User-created plans own one; the
 // one-shot tp_build_cost_tensors reuses a per-thread, per-device arena so
-// repeated builds do not pay cudaMalloc/cudaStreamCreate.
+// repeated builds pay neither cudaMalloc nor the strategy-table kernel.
 struct Arena {
   int device = 0;
   cudaStream_t stream = nullptr;
-  DevBuf d_tabs, d_tables, d_ops, d_chks, d_slots, d_occs, d_sigs, d_edges, d_sig_edges, d_work,
-      d_over, d_rsec, d_rvol, d_nsec, d_nvol, d_nmem, d_rowbase, d_err, d_edges_local;
+  DevBuf d_tabs, d_tables, d_classes, d_chks, d_slots, d_occs, d_members, d_sigs, d_edges, d_list,
+      d_work, d_over, d_rsec, d_rvol, d_csec, d_cvol, d_cmem, d_rowbase, d_err;
   DevBuf out[9];  // one-shot staging of the requested outputs
+  std::vector<std::array<int64_t, 4>> table_key;  // (offset, count, p, n) of the resident tables
   void release() {
-    for (DevBuf* b : {&d_tabs, &d_tables, &d_ops, &d_chks, &d_slots, &d_occs, &d_sigs, &d_edges,
-                      &d_sig_edges, &d_work, &d_over, &d_rsec, &d_rvol, &d_nsec, &d_nvol, &d_nmem,
-                      &d_rowbase, &d_err, &d_edges_local})
+    for (DevBuf* b : {&d_tabs, &d_tables, &d_classes, &d_chks, &d_slots, &d_occs, &d_members, &d_sigs,
+                      &d_edges, &d_list, &d_work, &d_over, &d_rsec, &d_rvol, &d_csec, &d_cvol, &d_cmem,
+                      &d_rowbase, &d_err})
       b->release();
     for (auto& b : out) b.release();
+    table_key.clear();
     if (stream) cudaStreamDestroy(stream);
     stream = nullptr;
   }
@@ -490,7 +494,6 @@ struct tp_plan {
   int device = 0;
   Arena* arena = nullptr;
   bool owns_arena = true;
-  // sizes / index
   int32_t num_ops = 0, num_edges = 0;
   int64_t N = 1;
   int n_log2 = 0;
@@ -506,23 +509,25 @@ struct tp_plan {
   // device descriptors (host copies)
   std::vector<TableDesc> tabs;
   int64_t table_total = 0;
-  std::vector<OpDesc> ops;
+  std::vector<ClassDesc> classes;
+  std::vector<int64_t> members;  // member node bases, CSR by class
+  int64_t total_rows = 0;
   std::vector<SliceChk> chks;
   std::vector<SlotDesc> slots;
   std::vector<Occ> occs;
   std::vector<SigDesc> sigs;
   std::vector<EdgeDesc> edges;
-  std::vector<int32_t> sig_edges;    // edges grouped by class, edge order within
+  std::vector<int32_t> sig_edges;  // edges grouped by class, edge order within
   std::vector<int32_t> sig_edge_begin;
-  std::vector<double> overrides;     // per pair; empty if no class needs one
+  std::vector<double> overrides;   // per pair; empty if no class needs one
   int64_t total_pairs = 0;
   int64_t h2d_bytes = 0;
   bool uploaded = false;
-  std::vector<Work> work;  // per execute (depends on the edge range)
+  std::vector<Work> work;
   int64_t last_launches = 0;
-  int32_t last_e0 = 0, last_e1 = 0;
-  cudaStream_t last_stream = nullptr;  // stream of the last execute
-  cudaEvent_t prof_start = nullptr, prof_stop = nullptr;  // recorded around K4
+  int32_t last_e0 = -1, last_e1 = -1;
+  cudaStream_t last_stream = nullptr;
+  cudaEvent_t prof_start = nullptr, prof_stop = nullptr;  // recorded around K2
 };
 
 namespace {
@@ -533,6 +538,8 @@ struct Builder {
   tp_plan* P;
 
   int num_tensors() const { return g->op_tensor_begin[g->num_ops]; }
+  int rank_of(int tensor) const { return g->tensor_shape_begin[tensor + 1] - g->tensor_shape_begin[tensor]; }
+  const int64_t* shape_of(int tensor) const { return g->shape + g->tensor_shape_begin[tensor]; }
 
   tp_status check_desc() {
     if (!g || !t) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null descriptor");
@@ -574,11 +581,8 @@ struct Builder {
     return TP_OK;
   }
 
-  int rank_of(int tensor) const { return g->tensor_shape_begin[tensor + 1] - g->tensor_shape_begin[tensor]; }
-  const int64_t* shape_of(int tensor) const { return g->shape + g->tensor_shape_begin[tensor]; }
-
-  // per-op slot resolution: the reference keys layouts by tensor name, the
-  // last occurrence's spec winning (layout.hpp:339-347)
+  // Per-op slots: the reference keys an operator's layouts by tensor name,
+  // the last occurrence's spec winning (layout.hpp:339-347).
   struct OpSlots {
     std::vector<int32_t> name, spec;
     int find(int nm) const {
@@ -589,6 +593,11 @@ struct Builder {
   };
   std::vector<OpSlots> op_slots;
   std::vector<std::vector<std::array<int8_t, tpk::kMaxR>>> slot_sa;  // per op, per slot
+  std::map<int, int64_t> table_of_p;
+  std::map<std::vector<int64_t>, int32_t> class_of_key;
+  std::vector<std::vector<int64_t>> class_members;
+  std::unordered_map<int32_t, std::vector<int32_t>> fed_names;  // op id -> tensors fed by edges
+  std::vector<int64_t> wrow_of_op;
 
   tp_status run() {
     tp_status st = check_desc();
@@ -599,13 +608,13 @@ struct Builder {
     p.N = (int64_t)t->node_count * (int64_t)t->local_device_num;
     p.env = Env{t->intra_bandwidth, t->inter_bandwidth, (int64_t)t->local_device_num};
 
-    // graph.hpp:135-140 find_op (first operator with the id), degrees by id
-    std::unordered_map<int32_t, int32_t> first_op;
-    std::unordered_map<int32_t, int32_t> to_count, from_count;
+    // graph.hpp:135-154 find_op (first operator with the id), degrees by id
+    std::unordered_map<int32_t, int32_t> first_op, to_count, from_count;
     for (int i = 0; i < g->num_ops; ++i) first_op.emplace(g->op_id[i], i);
     for (int e = 0; e < g->num_edges; ++e) {
       to_count[g->edge_to[e]]++;
       from_count[g->edge_from[e]]++;
+      fed_names[g->edge_to[e]].push_back(g->edge_tensor[e]);
     }
     p.in_deg.resize(g->num_ops);
     p.out_deg.resize(g->num_ops);
@@ -623,6 +632,9 @@ struct Builder {
       p.edge_from_op[e] = a == first_op.end() ? -1 : a->second;
       p.edge_to_op[e] = b == first_op.end() ? -1 : b->second;
     }
+    p.node_base.assign(g->num_ops + 1, 0);
+    p.edge_base.assign(g->num_edges + 1, 0);
+    p.row_base.assign(g->num_edges + 1, 0);
     // Kahn's algorithm (graph.hpp:158-183)
     {
       std::vector<int32_t> indeg(g->num_ops, 0);
@@ -641,12 +653,10 @@ struct Builder {
         for (int w : succ[ready[h]])
           if (--indeg[w] == 0) ready.push_back(w);
       }
-      if ((int)p.topo.size() != g->num_ops) {
+      if ((int)p.topo.size() != g->num_ops) {  // aux_graph.hpp:224-226
         p.topo.assign(g->num_ops, 0);
-        p.host_err = ekey(0, tpk::kCycle);  // aux_graph.hpp:224-226
-        p.node_base.assign(g->num_ops + 1, 0);
-        p.edge_base.assign(g->num_edges + 1, 0);
-        p.row_base.assign(g->num_edges + 1, 0);
+        p.host_err = ekey(0, tpk::kCycle);
+        p.valid_ops = 0;
         return TP_OK;
       }
     }
@@ -655,10 +665,9 @@ struct Builder {
     const bool pow2 = p.N > 0 && (p.N & (p.N - 1)) == 0;
     p.n_log2 = pow2 ? log2_floor(p.N) : 0;
     if (pow2 && p.n_log2 > tpk::kMaxD) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "more than 2^16 devices");
-    p.node_base.assign(g->num_ops + 1, 0);
-    std::map<int, int64_t> table_of_p;  // p -> entry offset
     op_slots.resize(g->num_ops);
     slot_sa.resize(g->num_ops);
+    wrow_of_op.assign(g->num_ops, 0);
     int64_t nodes = 0;
     p.valid_ops = g->num_ops;
     for (int i = 0; i < g->num_ops; ++i) {
@@ -680,16 +689,19 @@ struct Builder {
         p.tabs.push_back(TableDesc{p.table_total, S, np, p.n_log2});
         p.table_total += S;
       }
-      st = build_op(i, np, (int32_t)table_of_p[np], nodes);
+      st = build_op(i, np, S, nodes);
       if (st) return st;
       nodes += S;
     }
     for (int i = p.valid_ops; i <= g->num_ops; ++i) p.node_base[i] = nodes;
     p.num_aux_nodes = nodes;
+    for (size_t c = 0; c < p.classes.size(); ++c) {  // class member CSR
+      p.classes[c].mem_begin = (int32_t)p.members.size();
+      for (int64_t nb : class_members[c]) p.members.push_back(nb);
+      p.classes[c].mem_end = (int32_t)p.members.size();
+    }
 
     // ---------------- edge phase (aux_graph.hpp:273-296) -----------------
-    p.edge_base.assign(g->num_edges + 1, 0);
-    p.row_base.assign(g->num_edges + 1, 0);
     int64_t aux = 0, rows = 0;
     p.valid_edges = 0;
     std::map<std::vector<int64_t>, int32_t> sig_of_key;
@@ -725,18 +737,16 @@ struct Builder {
         const int pw = g->op_axis_begin[w + 1] - g->op_axis_begin[w];
         const int64_t Su = p.node_base[u + 1] - p.node_base[u];
         const int64_t Sw = p.node_base[w + 1] - p.node_base[w];
+        if (Su * Sw >= ((int64_t)1 << 31) - kExpTile)
+          return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "more than 2^31 pairs on one edge");
         int64_t elements = 1;
         for (int d = 0; d < R; ++d) elements *= shape_of(tu)[d];
         const double bytes = (double)elements * g->tensor_element_size[tu];  // graph.hpp:52-54
-        // class key
         std::vector<int64_t> key;
         key.reserve(8 + 3 * R);
-        key.push_back(pu);
-        key.push_back(pw);
-        key.push_back(R);
         int64_t bbits;
         std::memcpy(&bbits, &bytes, 8);
-        key.push_back(bbits);
+        key.insert(key.end(), {(int64_t)pu, (int64_t)pw, (int64_t)R, bbits});
         for (int d = 0; d < R; ++d) key.push_back(shape_of(tu)[d]);
         for (int d = 0; d < R; ++d) key.push_back(slot_sa[u][ku][d]);
         for (int d = 0; d < R; ++d) key.push_back(slot_sa[w][kw][d]);
@@ -773,7 +783,7 @@ struct Builder {
         ed.aux_base = aux;
         ed.nb_u = p.node_base[u];
         ed.nb_w = p.node_base[w];
-        ed.indeg_w = (double)p.in_deg[w];
+        ed.wrow = wrow_of_op[w];
         ed.sig = sig;
         ed.e = e;
         p.edges.push_back(ed);
@@ -794,10 +804,17 @@ struct Builder {
     }
     for (int i = 0; i < p.valid_ops; ++i)
       if (p.in_deg[i] == 0) p.num_virtual += p.node_base[i + 1] - p.node_base[i];
-    return memo_aliasing();
+    st = memo_aliasing();
+    p.h2d_bytes = (int64_t)(p.tabs.size() * sizeof(TableDesc) + p.classes.size() * sizeof(ClassDesc) +
+                            p.members.size() * sizeof(int64_t) + p.chks.size() * sizeof(SliceChk) +
+                            p.slots.size() * sizeof(SlotDesc) + p.occs.size() * sizeof(Occ) +
+                            p.sigs.size() * sizeof(SigDesc) + p.edges.size() * sizeof(EdgeDesc) +
+                            p.overrides.size() * sizeof(double));
+    return st;
   }
 
-  tp_status build_op(int i, int np, int32_t table, int64_t nb) {
+  // Slots, slice checks, occurrences of one op; then its node class.
+  tp_status build_op(int i, int np, int64_t S, int64_t nb) {
     tp_plan& p = *P;
     OpSlots& os = op_slots[i];
     const int t0 = g->op_tensor_begin[i], t1 = g->op_tensor_begin[i + 1];
@@ -817,12 +834,7 @@ struct Builder {
     auto& sa = slot_sa[i];
     sa.assign(os.name.size(), std::array<int8_t, tpk::kMaxR>{});
     for (auto& a : sa) a.fill(-1);
-    OpDesc od{};
-    od.node_base = nb;
-    od.table = table;
-    od.p = np;
-    od.chk_begin = (int32_t)p.chks.size();
-    od.slot_begin = (int32_t)p.slots.size();
+    std::vector<SliceChk> chk;
     const int a0 = g->op_axis_begin[i];
     for (int a = 0; a < np; ++a) {
       for (int s = g->axis_slice_begin[a0 + a]; s < g->axis_slice_begin[a0 + a + 1]; ++s) {
@@ -839,10 +851,10 @@ struct Builder {
           c.v = (int8_t)v2_capped(shape_of(tk)[dim]);
           sa[k][dim] = (int8_t)a;  // later slices overwrite (layout.hpp:366)
         }
-        p.chks.push_back(c);
+        chk.push_back(c);
       }
     }
-    od.chk_end = (int32_t)p.chks.size();
+    std::vector<SlotDesc> slots;
     for (size_t k = 0; k < os.name.size(); ++k) {
       SlotDesc sd{};
       const int tk = os.spec[k];
@@ -852,10 +864,11 @@ struct Builder {
       sd.es = g->tensor_element_size[tk];
       sd.R = (int8_t)rank_of(tk);
       for (int d = 0; d < tpk::kMaxR; ++d) sd.sa[d] = sa[k][d];
-      p.slots.push_back(sd);
+      slots.push_back(sd);
     }
-    od.occ_begin = (int32_t)p.occs.size();
+    std::vector<Occ> occ;
     const int nin = g->op_num_inputs[i];
+    auto fit = fed_names.find(g->op_id[i]);
     for (int t = t0; t < t1; ++t) {
       Occ oc{};
       const int nm = g->tensor_name[t];
@@ -868,58 +881,83 @@ struct Builder {
         if (!slices) mask |= (uint8_t)(1u << a);
       }
       oc.nonslicing = mask;
-      bool fed = false;
       if (t - t0 < nin) {
-        for (int e = 0; e < g->num_edges && !fed; ++e)
-          fed = g->edge_to[e] == g->op_id[i] && g->edge_tensor[e] == nm;
+        bool fed = false;  // aux_graph.hpp:155-162
+        if (fit != fed_names.end())
+          for (int32_t x : fit->second) fed |= x == nm;
         oc.in_memory = !fed;
       } else {
         oc.in_memory = 1;
       }
-      p.occs.push_back(oc);
+      occ.push_back(oc);
     }
-    od.occ_end = (int32_t)p.occs.size();
-    p.ops.push_back(od);
+    // node class key: everything the per-node costs depend on
+    std::vector<int64_t> key{(int64_t)np, (int64_t)p.in_deg[i], (int64_t)chk.size(), (int64_t)slots.size(),
+                             (int64_t)occ.size()};
+    for (auto& c : chk) key.insert(key.end(), {(int64_t)c.slot, (int64_t)c.axis, (int64_t)c.v});
+    for (auto& s : slots) {
+      key.insert(key.end(), {s.elements, (int64_t)s.es, (int64_t)s.R});
+      for (int d = 0; d < tpk::kMaxR; ++d) key.push_back(s.sa[d]);
+    }
+    for (auto& o : occ) key.insert(key.end(), {(int64_t)o.slot, (int64_t)o.nonslicing, (int64_t)o.in_memory});
+    auto it = class_of_key.find(key);
+    int32_t cls;
+    if (it == class_of_key.end()) {
+      cls = (int32_t)p.classes.size();
+      class_of_key.emplace(key, cls);
+      ClassDesc cd{};
+      cd.row_base = p.total_rows;
+      cd.first_node = nb;
+      cd.indeg = (double)p.in_deg[i];
+      cd.p = np;
+      cd.table = (int32_t)table_of_p[np];
+      cd.chk_begin = (int32_t)p.chks.size();
+      p.chks.insert(p.chks.end(), chk.begin(), chk.end());
+      cd.chk_end = (int32_t)p.chks.size();
+      cd.slot_begin = (int32_t)p.slots.size();
+      p.slots.insert(p.slots.end(), slots.begin(), slots.end());
+      cd.occ_begin = (int32_t)p.occs.size();
+      p.occs.insert(p.occs.end(), occ.begin(), occ.end());
+      cd.occ_end = (int32_t)p.occs.size();
+      p.classes.push_back(cd);
+      class_members.emplace_back();
+      p.total_rows += S;
+    } else {
+      cls = it->second;
+    }
+    class_members[cls].push_back(nb);
+    wrow_of_op[i] = p.classes[cls].row_base;
     return TP_OK;
   }
 
   // The reference memo (aux_graph.hpp:257-271) keys on (shape, matrix, map)
   // of both layouts but prices with the FIRST edge's tensor bytes. Only when
-  // same-shape classes carry different bytes can that be observed; then the
-  // first writer's bytes are resolved per pair here (host, rare path).
+  // same-shape edge classes carry different bytes can that be observed; then
+  // the first writer's bytes are resolved per pair here (host, rare path).
   tp_status memo_aliasing() {
     tp_plan& p = *P;
     std::map<std::vector<int64_t>, std::vector<int32_t>> by_shape;
+    std::vector<std::vector<int64_t>> shape_of_sig(p.sigs.size());
     for (size_t s = 0; s < p.sigs.size(); ++s) {
-      std::vector<int64_t> sh;
       const EdgeDesc& ed = p.edges[p.sig_edges[p.sig_edge_begin[s]]];
       const int u = p.edge_from_op[ed.e];
-      const int ku = op_slots[u].find(g->edge_tensor[ed.e]);
-      const int tu = op_slots[u].spec[ku];
-      sh.assign(shape_of(tu), shape_of(tu) + rank_of(tu));
-      by_shape[sh].push_back((int32_t)s);
+      const int tu = op_slots[u].spec[op_slots[u].find(g->edge_tensor[ed.e])];
+      shape_of_sig[s].assign(shape_of(tu), shape_of(tu) + rank_of(tu));
+      by_shape[shape_of_sig[s]].push_back((int32_t)s);
     }
     bool hazard = false;
-    for (auto& kv : by_shape) {
+    for (auto& kv : by_shape)
       for (int32_t s : kv.second)
         if (p.sigs[s].bytes != p.sigs[kv.second[0]].bytes) hazard = true;
-    }
     if (!hazard) return TP_OK;
     if (p.total_pairs > (int64_t)1 << 26) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "aliasing graph too large");
-    // host strategy tables
-    std::map<int, std::vector<Strat>> host_tab;
+    std::map<int64_t, std::vector<Strat>> host_tab;  // by table offset
     for (auto& td : p.tabs) {
-      auto& v = host_tab[td.p];
+      auto& v = host_tab[td.offset];
       v.resize(td.count);
       for (int64_t s = 0; s < td.count; ++s) tpk::unrank_strategy(td.p, td.n, s, v[s]);
     }
-    auto strat_at = [&](int32_t tab_off, int64_t s) -> const Strat& {
-      for (auto& td : p.tabs)
-        if (td.offset == tab_off) return host_tab[td.p][s];
-      return host_tab.begin()->second[0];
-    };
     p.overrides.assign(p.total_pairs, 0.0);
-    // classes in order of their first edge (first-writer order)
     std::vector<int32_t> order(p.sigs.size());
     for (size_t s = 0; s < order.size(); ++s) order[s] = (int32_t)s;
     std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
@@ -929,17 +967,14 @@ struct Builder {
     for (int32_t s : order) {
       SigDesc& sd = p.sigs[s];
       sd.has_override = 1;
-      std::string shape_key;
-      const EdgeDesc& ed = p.edges[p.sig_edges[p.sig_edge_begin[s]]];
-      const int u = p.edge_from_op[ed.e];
-      const int tu = op_slots[u].spec[op_slots[u].find(g->edge_tensor[ed.e])];
-      shape_key.assign(reinterpret_cast<const char*>(shape_of(tu)), rank_of(tu) * sizeof(int64_t));
+      const std::string shape_key(reinterpret_cast<const char*>(shape_of_sig[s].data()),
+                                  shape_of_sig[s].size() * sizeof(int64_t));
       for (int64_t su = 0; su < sd.Su; ++su) {
         Lay F;
-        tpk::side_layout(strat_at(sd.tab_u, su), sd.sa_u, sd.R, F);
+        tpk::side_layout(host_tab[sd.tab_u][su], sd.sa_u, sd.R, F);
         for (int64_t sw = 0; sw < sd.Sw; ++sw) {
           Lay T;
-          tpk::side_layout(strat_at(sd.tab_w, sw), sd.sa_w, sd.R, T);
+          tpk::side_layout(host_tab[sd.tab_w][sw], sd.sa_w, sd.R, T);
           const int64_t idx = sd.pair_begin + su * sd.Sw + sw;
           p.overrides[idx] = sd.bytes;
           if (tpk::same_layout(F, T, sd.R)) continue;
@@ -981,27 +1016,26 @@ Arena* thread_arena(int device) {
   return a;
 }
 
-// Split class tiles x edge chunks into CTA work items for edges [e0, e1).
-void make_work(tp_plan* p, int32_t e0, int32_t e1, std::vector<Work>& out, std::vector<int32_t>& sig_edges_local,
-               std::vector<int32_t>& begin_local) {
+// CTA work items for edges [e0, e1): class tiles x edge chunks.
+void make_work(tp_plan* p, int32_t e0, int32_t e1, std::vector<Work>& out, std::vector<int32_t>& list) {
   out.clear();
-  sig_edges_local.clear();
-  begin_local.assign(1, 0);
+  list.clear();
+  std::vector<int32_t> begin(1, 0);
   int64_t total = 0;
   for (size_t s = 0; s < p->sigs.size(); ++s) {
     for (int i = p->sig_edge_begin[s]; i < p->sig_edge_begin[s + 1]; ++i) {
       const int e = p->sig_edges[i];
       if (e >= e0 && e < e1) {
-        sig_edges_local.push_back(e);
+        list.push_back(e);
         total += (int64_t)p->sigs[s].Su * p->sigs[s].Sw;
       }
     }
-    begin_local.push_back((int32_t)sig_edges_local.size());
+    begin.push_back((int32_t)list.size());
   }
-  // aim at >= 4 CTAs per SM while reusing each class tile across edges
-  const int64_t target = std::max<int64_t>(kExpTile * 4, total / (148 * 4) + 1);
+  // ~4 CTAs per SM; each CTA reuses its class tile across a chunk of edges
+  const int64_t target = std::max<int64_t>(kExpTile, total / (148 * 4) + 1);
   for (size_t s = 0; s < p->sigs.size(); ++s) {
-    const int b = begin_local[s], en = begin_local[s + 1];
+    const int b = begin[s], en = begin[s + 1];
     if (b == en) continue;
     const int64_t P = (int64_t)p->sigs[s].Su * p->sigs[s].Sw;
     const int64_t tile = std::min<int64_t>(P, kExpTile);
@@ -1012,7 +1046,7 @@ void make_work(tp_plan* p, int32_t e0, int32_t e1, std::vector<Work>& out, std::
         w.sig = (int32_t)s;
         w.ebeg = c;
         w.eend = std::min(en, c + chunk);
-        w.j0 = j0;
+        w.j0 = (int32_t)j0;
         out.push_back(w);
       }
     }
@@ -1083,7 +1117,8 @@ tp_status tp_plan_index(const tp_plan* p, tp_aux_index* x) {
   if (!p || !x) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null argument");
   if (x->node_base) std::memcpy(x->node_base, p->node_base.data(), sizeof(int64_t) * (p->num_ops + 1));
   if (x->edge_base) std::memcpy(x->edge_base, p->edge_base.data(), sizeof(int64_t) * (p->num_edges + 1));
-  if (x->edge_from_op && p->num_edges) std::memcpy(x->edge_from_op, p->edge_from_op.data(), sizeof(int32_t) * p->num_edges);
+  if (x->edge_from_op && p->num_edges)
+    std::memcpy(x->edge_from_op, p->edge_from_op.data(), sizeof(int32_t) * p->num_edges);
   if (x->edge_to_op && p->num_edges) std::memcpy(x->edge_to_op, p->edge_to_op.data(), sizeof(int32_t) * p->num_edges);
   if (x->in_degree && p->num_ops) std::memcpy(x->in_degree, p->in_deg.data(), sizeof(int32_t) * p->num_ops);
   if (x->out_degree && p->num_ops) std::memcpy(x->out_degree, p->out_deg.data(), sizeof(int32_t) * p->num_ops);
@@ -1095,26 +1130,33 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
   if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
   tp_status st = ensure_stream(p);
   if (st) return st;
-  cudaStream_t s = stream ? (cudaStream_t)stream : p->arena->stream;
-  CUDA_TRY(upload(p->arena->d_tabs, p->tabs, s));
-  CUDA_TRY(p->arena->d_tables.ensure(sizeof(Strat) * (p->table_total + 1)));
-  CUDA_TRY(upload(p->arena->d_ops, p->ops, s));
-  CUDA_TRY(upload(p->arena->d_chks, p->chks, s));
-  CUDA_TRY(upload(p->arena->d_slots, p->slots, s));
-  CUDA_TRY(upload(p->arena->d_occs, p->occs, s));
-  CUDA_TRY(upload(p->arena->d_sigs, p->sigs, s));
-  CUDA_TRY(upload(p->arena->d_edges, p->edges, s));
-  CUDA_TRY(upload(p->arena->d_over, p->overrides, s));
-  CUDA_TRY(p->arena->d_rsec.ensure(sizeof(double) * (p->total_pairs + 1)));
-  CUDA_TRY(p->arena->d_rvol.ensure(sizeof(double) * (p->total_pairs + 1)));
-  CUDA_TRY(p->arena->d_nsec.ensure(sizeof(double) * (p->num_aux_nodes + 1)));
-  CUDA_TRY(p->arena->d_nvol.ensure(sizeof(double) * (p->num_aux_nodes + 1)));
-  CUDA_TRY(p->arena->d_nmem.ensure(sizeof(double) * (p->num_aux_nodes + 1)));
-  CUDA_TRY(p->arena->d_err.ensure(sizeof(unsigned long long)));
-  p->h2d_bytes = (int64_t)(p->tabs.size() * sizeof(TableDesc) + p->ops.size() * sizeof(OpDesc) +
-                           p->chks.size() * sizeof(SliceChk) + p->slots.size() * sizeof(SlotDesc) +
-                           p->occs.size() * sizeof(Occ) + p->sigs.size() * sizeof(SigDesc) +
-                           p->edges.size() * sizeof(EdgeDesc) + p->overrides.size() * sizeof(double));
+  Arena& A = *p->arena;
+  cudaStream_t s = stream ? (cudaStream_t)stream : A.stream;
+  // strategy tables: a pure function of (p, N), cached on the arena
+  std::vector<std::array<int64_t, 4>> key;
+  for (auto& td : p->tabs) key.push_back({td.offset, td.count, td.p, td.n});
+  if (key != A.table_key && p->table_total > 0) {
+    CUDA_TRY(upload(A.d_tabs, p->tabs, s));
+    CUDA_TRY(A.d_tables.ensure(sizeof(Strat) * (p->table_total + 1)));
+    table_kernel<<<(unsigned)((p->table_total + 127) / 128), 128, 0, s>>>(
+        (const TableDesc*)A.d_tabs.p, (int)p->tabs.size(), p->table_total, (Strat*)A.d_tables.p);
+    CUDA_TRY(cudaGetLastError());
+    A.table_key = key;
+  }
+  CUDA_TRY(upload(A.d_classes, p->classes, s));
+  CUDA_TRY(upload(A.d_members, p->members, s));
+  CUDA_TRY(upload(A.d_chks, p->chks, s));
+  CUDA_TRY(upload(A.d_slots, p->slots, s));
+  CUDA_TRY(upload(A.d_occs, p->occs, s));
+  CUDA_TRY(upload(A.d_sigs, p->sigs, s));
+  CUDA_TRY(upload(A.d_edges, p->edges, s));
+  CUDA_TRY(upload(A.d_over, p->overrides, s));
+  CUDA_TRY(A.d_rsec.ensure(sizeof(double) * (p->total_pairs + 1)));
+  CUDA_TRY(A.d_rvol.ensure(sizeof(double) * (p->total_pairs + 1)));
+  CUDA_TRY(A.d_csec.ensure(sizeof(double) * (p->total_rows + 1)));
+  CUDA_TRY(A.d_cvol.ensure(sizeof(double) * (p->total_rows + 1)));
+  CUDA_TRY(A.d_cmem.ensure(sizeof(double) * (p->total_rows + 1)));
+  CUDA_TRY(A.d_err.ensure(sizeof(unsigned long long)));
   p->uploaded = true;
   p->last_e0 = p->last_e1 = -1;
   return TP_OK;
@@ -1128,7 +1170,8 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
     st = tp_plan_upload(p, opts ? opts->stream : nullptr);
     if (st) return st;
   }
-  cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : p->arena->stream;
+  Arena& A = *p->arena;
+  cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : A.stream;
   p->last_stream = s;
   int32_t e0 = opts ? opts->edge_begin : 0;
   int32_t e1 = opts ? opts->edge_end : -1;
@@ -1139,47 +1182,54 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   tp_cost_tensors none{};
   if (!out) out = &none;
   int64_t launches = 0;
-  unsigned long long* err = (unsigned long long*)p->arena->d_err.p;
+  unsigned long long* err = (unsigned long long*)A.d_err.p;
   CUDA_TRY(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), s));
   if (p->host_err != ~0ull && (p->host_err >> 6) == 0) {  // cycle: nothing to build
     p->last_launches = 0;
     return TP_OK;
   }
-  // K1: strategy tables
-  if (p->table_total > 0) {
-    const int th = 128;
-    table_kernel<<<(unsigned)((p->table_total + th - 1) / th), th, 0, s>>>(
-        (const TableDesc*)p->arena->d_tabs.p, (int)p->tabs.size(), p->table_total, (Strat*)p->arena->d_tables.p);
+  const bool edge_phase = p->host_err >= ekey(kEdgePhase, 0);
+  // K1: node classes + edge-class pairs in one launch
+  BuildArgs a{};
+  a.classes = (const ClassDesc*)A.d_classes.p;
+  a.ncls = (int)p->classes.size();
+  a.total_rows = p->total_rows;
+  a.node_blocks = (p->total_rows + kBuildThreads - 1) / kBuildThreads;
+  a.chks = (const SliceChk*)A.d_chks.p;
+  a.slots = (const SlotDesc*)A.d_slots.p;
+  a.occs = (const Occ*)A.d_occs.p;
+  a.member_nb = (const int64_t*)A.d_members.p;
+  a.cls_sec = (double*)A.d_csec.p;
+  a.cls_vol = (double*)A.d_cvol.p;
+  a.cls_memdiv = (double*)A.d_cmem.p;
+  const bool nodes_out = !skip_nodes && out->node_intra_cost_s && out->node_intra_volume_bytes &&
+                         out->node_memory_bytes;
+  a.node_sec = nodes_out ? out->node_intra_cost_s : nullptr;
+  a.node_vol = nodes_out ? out->node_intra_volume_bytes : nullptr;
+  a.node_mem = nodes_out ? out->node_memory_bytes : nullptr;
+  a.sigs = (const SigDesc*)A.d_sigs.p;
+  a.nsigs = (int)p->sigs.size();
+  a.total_pairs = edge_phase ? p->total_pairs : 0;
+  a.overrides = (const double*)A.d_over.p;
+  a.r_sec = (double*)A.d_rsec.p;
+  a.r_vol = (double*)A.d_rvol.p;
+  a.tables = (const Strat*)A.d_tables.p;
+  a.env = p->env;
+  a.n_log2 = p->n_log2;
+  a.err = err;
+  const int64_t blocks = a.node_blocks + (a.total_pairs + kBuildThreads - 1) / kBuildThreads;
+  if (blocks > 0) {
+    build_kernel<<<(unsigned)blocks, kBuildThreads, 0, s>>>(a);
     ++launches;
   }
-  // K2: per-node costs
-  const int64_t nodes = p->node_base[p->valid_ops];
-  if (nodes > 0) {
-    const int th = 256;
-    node_kernel<<<(unsigned)((nodes + th - 1) / th), th, 0, s>>>(
-        (const OpDesc*)p->arena->d_ops.p, (int)p->ops.size(), nodes, p->n_log2, p->env, (const Strat*)p->arena->d_tables.p,
-        (const SliceChk*)p->arena->d_chks.p, (const SlotDesc*)p->arena->d_slots.p, (const Occ*)p->arena->d_occs.p,
-        (double*)p->arena->d_nsec.p, (double*)p->arena->d_nvol.p, (double*)p->arena->d_nmem.p,
-        skip_nodes ? nullptr : out->node_intra_cost_s, skip_nodes ? nullptr : out->node_intra_volume_bytes,
-        skip_nodes ? nullptr : out->node_memory_bytes, err);
-    ++launches;
-  }
-  // K3: class tables (all classes; the tables are shared by every edge)
-  if (p->total_pairs > 0 && p->host_err >= ekey(kEdgePhase, 0)) {
-    const int th = 128;
-    pair_kernel<<<(unsigned)((p->total_pairs + th - 1) / th), th, 0, s>>>(
-        (const SigDesc*)p->arena->d_sigs.p, (int)p->sigs.size(), p->total_pairs, p->env, (const Strat*)p->arena->d_tables.p,
-        (const double*)p->arena->d_over.p, (double*)p->arena->d_rsec.p, (double*)p->arena->d_rvol.p, err);
-    ++launches;
-  }
-  // K4: fan-out to the aux edges of [e0, e1)
+  // K2: fan-out to the aux edges of [e0, e1)
   const int64_t out_offset = p->edge_base[e0];
-  if (p->edge_base[e1] > out_offset && p->host_err >= ekey(kEdgePhase, 0)) {
+  if (p->edge_base[e1] > out_offset && edge_phase) {
     if (p->last_e0 != e0 || p->last_e1 != e1) {
-      std::vector<int32_t> sel, beg;
-      make_work(p, e0, e1, p->work, sel, beg);
-      CUDA_TRY(upload(p->arena->d_work, p->work, s));
-      CUDA_TRY(upload(p->arena->d_sig_edges, sel, s));  // Work ranges index this local list
+      std::vector<int32_t> list;
+      make_work(p, e0, e1, p->work, list);
+      CUDA_TRY(upload(A.d_work, p->work, s));
+      CUDA_TRY(upload(A.d_list, list, s));
       p->last_e0 = e0;
       p->last_e1 = e1;
     }
@@ -1187,27 +1237,25 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
                              out->aux_edge_records)) {
       if (p->prof_start) CUDA_TRY(cudaEventRecord(p->prof_start, s));
       expand_kernel<<<(unsigned)p->work.size(), kExpThreads, 0, s>>>(
-          (const Work*)p->arena->d_work.p, (const SigDesc*)p->arena->d_sigs.p, (const int32_t*)p->arena->d_sig_edges.p,
-          (const EdgeDesc*)p->arena->d_edges.p, (const double*)p->arena->d_rsec.p, (const double*)p->arena->d_rvol.p,
-          (const double*)p->arena->d_nsec.p, (const double*)p->arena->d_nvol.p, (const double*)p->arena->d_nmem.p, out_offset,
+          (const Work*)A.d_work.p, (const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_list.p,
+          (const EdgeDesc*)A.d_edges.p, (const double*)A.d_rsec.p, (const double*)A.d_rvol.p,
+          (const double*)A.d_csec.p, (const double*)A.d_cvol.p, (const double*)A.d_cmem.p, out_offset,
           out->edge_cost_s, out->edge_volume_bytes, out->edge_memory_bytes, (char*)out->aux_edge_records);
       ++launches;
       if (p->prof_stop) CUDA_TRY(cudaEventRecord(p->prof_stop, s));
     }
+    // K3: row minima
     if (out->row_min_cost_s && out->row_min_volume_bytes) {
       const int64_t r0 = p->row_base[e0], r1 = p->row_base[e1];
       std::vector<int64_t> rb(p->row_base.begin() + e0, p->row_base.begin() + e1 + 1);
       for (auto& v : rb) v -= r0;
-      CUDA_TRY(upload(p->arena->d_rowbase, rb, s));
-      CUDA_TRY(p->arena->d_edges_local.ensure(sizeof(EdgeDesc) * (e1 - e0 + 1)));
-      CUDA_TRY(cudaMemcpyAsync(p->arena->d_edges_local.p, (const EdgeDesc*)p->arena->d_edges.p + e0,
-                               sizeof(EdgeDesc) * (e1 - e0), cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(upload(A.d_rowbase, rb, s));
       const int64_t rows = r1 - r0;
       const int th = 256;
       rowmin_kernel<<<(unsigned)((rows * 32 + th - 1) / th), th, 0, s>>>(
-          (const EdgeDesc*)p->arena->d_edges_local.p, (const int64_t*)p->arena->d_rowbase.p, e1 - e0, rows,
-          (const SigDesc*)p->arena->d_sigs.p, (const double*)p->arena->d_rsec.p, (const double*)p->arena->d_rvol.p,
-          (const double*)p->arena->d_nsec.p, (const double*)p->arena->d_nvol.p, out->row_min_cost_s, out->row_min_volume_bytes);
+          (const EdgeDesc*)A.d_edges.p, (const int64_t*)A.d_rowbase.p, e0, e1 - e0, rows,
+          (const SigDesc*)A.d_sigs.p, (const double*)A.d_rsec.p, (const double*)A.d_rvol.p,
+          (const double*)A.d_csec.p, (const double*)A.d_cvol.p, out->row_min_cost_s, out->row_min_volume_bytes);
       ++launches;
     }
   }
@@ -1349,7 +1397,8 @@ tp_status tp_enumerate_strategies(int32_t p, int64_t total_devices, int64_t* cou
       if (degrees) degrees[i * p + a] = (int64_t)1 << h[i].deg[a];
       if (device_map) device_map[i * p + a] = h[i].dmap[a];
       // DeviceMatrix::dims, outermost first: dims[j] = extent(depth-1-j)
-      if (matrix_dims) matrix_dims[i * p + a] = a < h[i].depth ? ((int64_t)1 << h[i].mx[h[i].depth - 1 - a]) : 0;
+      if (matrix_dims)
+        matrix_dims[i * p + a] = a < h[i].depth ? ((int64_t)1 << h[i].mx[h[i].depth - 1 - a]) : 0;
     }
     if (matrix_depth) matrix_depth[i] = h[i].depth;
   }
