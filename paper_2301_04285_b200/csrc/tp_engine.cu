@@ -35,6 +35,7 @@
 
 #include "../../include/taps_b200.h"
 #include "tp_core.cuh"
+#include "tp_warp.cuh"
 
 using tpk::DimT;
 using tpk::Env;
@@ -126,7 +127,7 @@ struct ClassDesc {     // a node class
   int64_t first_node;  // aux node id of strategy 0 of the class's first member
   double indeg;        // in-degree shared by the members (memory / in_degree)
   int32_t p, table;
-  int32_t chk_begin, chk_end, occ_begin, occ_end, slot_begin, mem_begin, mem_end, pad;
+  int32_t chk_begin, chk_end, occ_begin, occ_end, slot_begin, mem_begin, mem_end, S;
 };
 
 struct SigDesc {       // an edge class
@@ -152,12 +153,19 @@ struct Work {
   int32_t j0;          // first pair of the tile within the class block
 };
 
+struct NodeWork {      // fan-out of one node class's rows to a chunk of its members
+  int32_t cls;
+  int32_t mbeg, mend;
+  int32_t pad;
+};
+
 struct TableDesc {
   int64_t offset, count;
   int32_t p, n;
 };
 
-constexpr int kBuildThreads = 64;
+constexpr int kBuildThreads = 128;
+constexpr int kPairsPerBlock = kBuildThreads / 32;  // one warp per class pair
 constexpr int kExpThreads = 256;
 constexpr int kExpPer = 8;
 constexpr int kExpTile = kExpThreads * kExpPer;  // class pairs per CTA tile
@@ -190,13 +198,10 @@ struct BuildArgs {
   const SliceChk* chks;
   const SlotDesc* slots;
   const Occ* occs;
-  const int64_t* member_nb;  // aux node id of strategy 0 of every class member
   double* cls_sec;
   double* cls_vol;
+  double* cls_mem;
   double* cls_memdiv;
-  double* node_sec;  // caller outputs (may be null)
-  double* node_vol;
-  double* node_mem;
   // edge classes
   const SigDesc* sigs;
   int nsigs;
@@ -207,6 +212,7 @@ struct BuildArgs {
   // shared
   const Strat* tables;
   Env env;
+  int l_log2;
   int n_log2;
   unsigned long long* err;
 };
@@ -229,7 +235,7 @@ __device__ void node_row(const BuildArgs& a, int64_t row) {
     else if (st.deg[k.axis] > k.v) kind = tpk::kIndivisible;
     if (kind) {
       flag_error(a.err, ekey(1 + (uint64_t)(cd.first_node + s) * 2 + 1, kind));
-      a.cls_sec[row] = a.cls_vol[row] = a.cls_memdiv[row] = 0;
+      a.cls_sec[row] = a.cls_vol[row] = a.cls_mem[row] = a.cls_memdiv[row] = 0;
       return;
     }
   }
@@ -265,18 +271,11 @@ __device__ void node_row(const BuildArgs& a, int64_t row) {
   }
   a.cls_sec[row] = sec;
   a.cls_vol[row] = vol;
+  a.cls_mem[row] = mem;
   a.cls_memdiv[row] = mem / cd.indeg;  // aux_graph.hpp:292
-  if (a.node_sec) {
-    for (int m = cd.mem_begin; m < cd.mem_end; ++m) {
-      const int64_t node = a.member_nb[m] + s;
-      a.node_sec[node] = sec;
-      a.node_vol[node] = vol;
-      a.node_mem[node] = mem;
-    }
-  }
 }
 
-// One (edge class, su, sw) pair: redistribution seconds and volume.
+// One (edge class, su, sw) pair on one warp: redistribution seconds and volume.
 __device__ void pair_row(const BuildArgs& a, int64_t idx) {
   int lo = 0, hi = a.nsigs - 1;
   while (lo < hi) {
@@ -294,24 +293,31 @@ __device__ void pair_row(const BuildArgs& a, int64_t idx) {
   double sec = 0, vol = 0;
   if (!tpk::same_layout(F, T, sg.R)) {  // aux_graph.hpp:260
     const double bytes = sg.has_override ? a.overrides[idx] : sg.bytes;
-    const int st = tpk::redist_cost(sg.R, F, T, sg.dt, bytes, a.env, sec, vol, nullptr);
+    tpk::WarpEnv we;
+    we.env = a.env;
+    we.l_log2 = a.l_log2;
+    const int st = tpk::redist_cost_warp(sg.R, F, T, sg.dt, bytes, we, sec, vol, nullptr);
     if (st) {
-      flag_error(a.err, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
+      if ((threadIdx.x & 31) == 0)
+        flag_error(a.err, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
       sec = vol = 0;
     }
   }
-  a.r_sec[idx] = sec;
-  a.r_vol[idx] = vol;
+  if ((threadIdx.x & 31) == 0) {
+    a.r_sec[idx] = sec;
+    a.r_vol[idx] = vol;
+  }
 }
 
-// K1: node classes in blocks [0, node_blocks), edge-class pairs after.
+// K1: node-class rows (a thread each) in blocks [0, node_blocks), then
+// edge-class pairs (a warp each).
 __global__ void __launch_bounds__(kBuildThreads) build_kernel(BuildArgs a) {
   if ((int64_t)blockIdx.x < a.node_blocks) {
     const int64_t row = (int64_t)blockIdx.x * kBuildThreads + threadIdx.x;
     if (row < a.total_rows) node_row(a, row);
   } else {
-    const int64_t idx = ((int64_t)blockIdx.x - a.node_blocks) * kBuildThreads + threadIdx.x;
-    if (idx < a.total_pairs) pair_row(a, idx);
+    const int64_t idx = ((int64_t)blockIdx.x - a.node_blocks) * kPairsPerBlock + (threadIdx.x >> 5);
+    if (idx < a.total_pairs) pair_row(a, idx);  // warp-uniform
   }
 }
 
@@ -326,7 +332,25 @@ __global__ void __launch_bounds__(kExpThreads) expand_kernel(
     const double* __restrict__ r_sec, const double* __restrict__ r_vol,
     const double* __restrict__ cls_sec, const double* __restrict__ cls_vol,
     const double* __restrict__ cls_memdiv, int64_t out_offset, double* __restrict__ e_sec,
-    double* __restrict__ e_vol, double* __restrict__ e_mem, char* __restrict__ records) {
+    double* __restrict__ e_vol, double* __restrict__ e_mem, char* __restrict__ records, int num_edge_work,
+    const NodeWork* __restrict__ nwork, const ClassDesc* __restrict__ classes,
+    const int64_t* __restrict__ member_nb, const double* __restrict__ cls_mem, double* __restrict__ n_sec,
+    double* __restrict__ n_vol, double* __restrict__ n_mem) {
+  if ((int)blockIdx.x >= num_edge_work) {
+    // node tensors: every member operator of a node class gets the class rows
+    const NodeWork nw = nwork[blockIdx.x - num_edge_work];
+    const ClassDesc cd = classes[nw.cls];
+    const int64_t total = (int64_t)(nw.mend - nw.mbeg) * cd.S;
+    for (int64_t t = threadIdx.x; t < total; t += kExpThreads) {
+      const int64_t m = t / cd.S, sidx = t - m * cd.S;
+      const int64_t node = member_nb[nw.mbeg + m] + sidx;
+      const int64_t row = cd.row_base + sidx;
+      if (n_sec) __stcs(n_sec + node, cls_sec[row]);
+      if (n_vol) __stcs(n_vol + node, cls_vol[row]);
+      if (n_mem) __stcs(n_mem + node, cls_mem[row]);
+    }
+    return;
+  }
   const Work wk = work[blockIdx.x];
   const SigDesc& sg = sigs[wk.sig];
   const int32_t Sw = sg.Sw;
@@ -413,12 +437,13 @@ __global__ void rowmin_kernel(const EdgeDesc* __restrict__ edges, const int64_t*
   }
 }
 
-__global__ void query_kernel(const tpk::QueryPOD* __restrict__ q, int n, tp_redist_result* __restrict__ r) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+// Verification export: one warp per query, the kernels' own code path.
+__global__ void query_kernel(const tpk::QueryPOD* __restrict__ q, int n, tp_redist_result* __restrict__ r,
+                             tpk::Trace* __restrict__ traces) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= n) return;
-  tp_redist_result res;
-  res.status = tpk::run_query(q[i], res);
-  r[i] = res;
+  const int st = tpk::run_query_warp(q[i], r[i], traces[i]);
+  if ((threadIdx.x & 31) == 0) r[i].status = st;
 }
 
 // ---------------------------------------------------------------------------
@@ -475,13 +500,13 @@ struct Arena {
   int device = 0;
   cudaStream_t stream = nullptr;
   DevBuf d_tabs, d_tables, d_classes, d_chks, d_slots, d_occs, d_members, d_sigs, d_edges, d_list,
-      d_work, d_over, d_rsec, d_rvol, d_csec, d_cvol, d_cmem, d_rowbase, d_err;
+      d_work, d_over, d_rsec, d_rvol, d_csec, d_cvol, d_cmem, d_cmem0, d_nwork, d_rowbase, d_err;
   DevBuf out[9];  // one-shot staging of the requested outputs
   std::vector<std::array<int64_t, 4>> table_key;  // (offset, count, p, n) of the resident tables
   void release() {
     for (DevBuf* b : {&d_tabs, &d_tables, &d_classes, &d_chks, &d_slots, &d_occs, &d_members, &d_sigs,
                       &d_edges, &d_list, &d_work, &d_over, &d_rsec, &d_rvol, &d_csec, &d_cvol, &d_cmem,
-                      &d_rowbase, &d_err})
+                      &d_cmem0, &d_nwork, &d_rowbase, &d_err})
       b->release();
     for (auto& b : out) b.release();
     table_key.clear();
@@ -524,6 +549,7 @@ struct tp_plan {
   int64_t h2d_bytes = 0;
   bool uploaded = false;
   std::vector<Work> work;
+  std::vector<NodeWork> nwork;
   int64_t last_launches = 0;
   int32_t last_e0 = -1, last_e1 = -1;
   cudaStream_t last_stream = nullptr;
@@ -695,10 +721,13 @@ struct Builder {
     }
     for (int i = p.valid_ops; i <= g->num_ops; ++i) p.node_base[i] = nodes;
     p.num_aux_nodes = nodes;
-    for (size_t c = 0; c < p.classes.size(); ++c) {  // class member CSR
+    for (size_t c = 0; c < p.classes.size(); ++c) {  // class member CSR + fan-out work
       p.classes[c].mem_begin = (int32_t)p.members.size();
       for (int64_t nb : class_members[c]) p.members.push_back(nb);
       p.classes[c].mem_end = (int32_t)p.members.size();
+      const int per = std::max(1, 2048 / std::max(1, p.classes[c].S));
+      for (int m = p.classes[c].mem_begin; m < p.classes[c].mem_end; m += per)
+        p.nwork.push_back(NodeWork{(int32_t)c, m, std::min(p.classes[c].mem_end, m + per), 0});
     }
 
     // ---------------- edge phase (aux_graph.hpp:273-296) -----------------
@@ -909,6 +938,7 @@ struct Builder {
       cd.row_base = p.total_rows;
       cd.first_node = nb;
       cd.indeg = (double)p.in_deg[i];
+      cd.S = (int32_t)S;
       cd.p = np;
       cd.table = (int32_t)table_of_p[np];
       cd.chk_begin = (int32_t)p.chks.size();
@@ -1144,6 +1174,7 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
     A.table_key = key;
   }
   CUDA_TRY(upload(A.d_classes, p->classes, s));
+  CUDA_TRY(upload(A.d_nwork, p->nwork, s));
   CUDA_TRY(upload(A.d_members, p->members, s));
   CUDA_TRY(upload(A.d_chks, p->chks, s));
   CUDA_TRY(upload(A.d_slots, p->slots, s));
@@ -1156,6 +1187,7 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
   CUDA_TRY(A.d_csec.ensure(sizeof(double) * (p->total_rows + 1)));
   CUDA_TRY(A.d_cvol.ensure(sizeof(double) * (p->total_rows + 1)));
   CUDA_TRY(A.d_cmem.ensure(sizeof(double) * (p->total_rows + 1)));
+  CUDA_TRY(A.d_cmem0.ensure(sizeof(double) * (p->total_rows + 1)));
   CUDA_TRY(A.d_err.ensure(sizeof(unsigned long long)));
   p->uploaded = true;
   p->last_e0 = p->last_e1 = -1;
@@ -1198,15 +1230,12 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   a.chks = (const SliceChk*)A.d_chks.p;
   a.slots = (const SlotDesc*)A.d_slots.p;
   a.occs = (const Occ*)A.d_occs.p;
-  a.member_nb = (const int64_t*)A.d_members.p;
   a.cls_sec = (double*)A.d_csec.p;
   a.cls_vol = (double*)A.d_cvol.p;
+  a.cls_mem = (double*)A.d_cmem0.p;
   a.cls_memdiv = (double*)A.d_cmem.p;
-  const bool nodes_out = !skip_nodes && out->node_intra_cost_s && out->node_intra_volume_bytes &&
-                         out->node_memory_bytes;
-  a.node_sec = nodes_out ? out->node_intra_cost_s : nullptr;
-  a.node_vol = nodes_out ? out->node_intra_volume_bytes : nullptr;
-  a.node_mem = nodes_out ? out->node_memory_bytes : nullptr;
+  const bool nodes_out = !skip_nodes && (out->node_intra_cost_s || out->node_intra_volume_bytes ||
+                                         out->node_memory_bytes);
   a.sigs = (const SigDesc*)A.d_sigs.p;
   a.nsigs = (int)p->sigs.size();
   a.total_pairs = edge_phase ? p->total_pairs : 0;
@@ -1215,35 +1244,43 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   a.r_vol = (double*)A.d_rvol.p;
   a.tables = (const Strat*)A.d_tables.p;
   a.env = p->env;
+  a.l_log2 = (p->env.local > 0 && (p->env.local & (p->env.local - 1)) == 0) ? log2_floor(p->env.local) : -1;
   a.n_log2 = p->n_log2;
   a.err = err;
-  const int64_t blocks = a.node_blocks + (a.total_pairs + kBuildThreads - 1) / kBuildThreads;
+  const int64_t blocks = a.node_blocks + (a.total_pairs + kPairsPerBlock - 1) / kPairsPerBlock;
   if (blocks > 0) {
     build_kernel<<<(unsigned)blocks, kBuildThreads, 0, s>>>(a);
     ++launches;
   }
-  // K2: fan-out to the aux edges of [e0, e1)
+  // K2: fan-out to the aux edges of [e0, e1) (+ the node tensors)
   const int64_t out_offset = p->edge_base[e0];
+  const bool edges_out = p->edge_base[e1] > out_offset && edge_phase &&
+                         (out->edge_cost_s || out->edge_volume_bytes || out->edge_memory_bytes ||
+                          out->aux_edge_records);
+  if (edges_out && (p->last_e0 != e0 || p->last_e1 != e1)) {
+    std::vector<int32_t> list;
+    make_work(p, e0, e1, p->work, list);
+    CUDA_TRY(upload(A.d_work, p->work, s));
+    CUDA_TRY(upload(A.d_list, list, s));
+    p->last_e0 = e0;
+    p->last_e1 = e1;
+  }
+  const int n_edge_work = edges_out ? (int)p->work.size() : 0;
+  const int n_node_work = nodes_out ? (int)p->nwork.size() : 0;
+  if (n_edge_work + n_node_work > 0) {
+    if (p->prof_start) CUDA_TRY(cudaEventRecord(p->prof_start, s));
+    expand_kernel<<<(unsigned)(n_edge_work + n_node_work), kExpThreads, 0, s>>>(
+        (const Work*)A.d_work.p, (const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_list.p,
+        (const EdgeDesc*)A.d_edges.p, (const double*)A.d_rsec.p, (const double*)A.d_rvol.p,
+        (const double*)A.d_csec.p, (const double*)A.d_cvol.p, (const double*)A.d_cmem.p, out_offset,
+        out->edge_cost_s, out->edge_volume_bytes, out->edge_memory_bytes, (char*)out->aux_edge_records,
+        n_edge_work, (const NodeWork*)A.d_nwork.p, (const ClassDesc*)A.d_classes.p,
+        (const int64_t*)A.d_members.p, (const double*)A.d_cmem0.p, nodes_out ? out->node_intra_cost_s : nullptr,
+        nodes_out ? out->node_intra_volume_bytes : nullptr, nodes_out ? out->node_memory_bytes : nullptr);
+    ++launches;
+    if (p->prof_stop) CUDA_TRY(cudaEventRecord(p->prof_stop, s));
+  }
   if (p->edge_base[e1] > out_offset && edge_phase) {
-    if (p->last_e0 != e0 || p->last_e1 != e1) {
-      std::vector<int32_t> list;
-      make_work(p, e0, e1, p->work, list);
-      CUDA_TRY(upload(A.d_work, p->work, s));
-      CUDA_TRY(upload(A.d_list, list, s));
-      p->last_e0 = e0;
-      p->last_e1 = e1;
-    }
-    if (!p->work.empty() && (out->edge_cost_s || out->edge_volume_bytes || out->edge_memory_bytes ||
-                             out->aux_edge_records)) {
-      if (p->prof_start) CUDA_TRY(cudaEventRecord(p->prof_start, s));
-      expand_kernel<<<(unsigned)p->work.size(), kExpThreads, 0, s>>>(
-          (const Work*)A.d_work.p, (const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_list.p,
-          (const EdgeDesc*)A.d_edges.p, (const double*)A.d_rsec.p, (const double*)A.d_rvol.p,
-          (const double*)A.d_csec.p, (const double*)A.d_cvol.p, (const double*)A.d_cmem.p, out_offset,
-          out->edge_cost_s, out->edge_volume_bytes, out->edge_memory_bytes, (char*)out->aux_edge_records);
-      ++launches;
-      if (p->prof_stop) CUDA_TRY(cudaEventRecord(p->prof_stop, s));
-    }
     // K3: row minima
     if (out->row_min_cost_s && out->row_min_volume_bytes) {
       const int64_t r0 = p->row_base[e0], r1 = p->row_base[e1];
@@ -1434,15 +1471,18 @@ tp_status tp_redistribute_batch(const tp_redist_query* q, int32_t n, tp_redist_r
     for (int k = 0; k < x.fdepth; ++k) x.fdims[k] = q[i].from_dims[k];
     for (int k = 0; k < x.tdepth; ++k) x.tdims[k] = q[i].to_dims[k];
   }
-  DevBuf dq, dr;
+  DevBuf dq, dr, dtr;
   CUDA_TRY(dq.ensure(sizeof(tpk::QueryPOD) * n));
   CUDA_TRY(dr.ensure(sizeof(tp_redist_result) * n));
+  CUDA_TRY(dtr.ensure(sizeof(tpk::Trace) * n));
   CUDA_TRY(cudaMemcpy(dq.p, pod.data(), sizeof(tpk::QueryPOD) * n, cudaMemcpyHostToDevice));
-  query_kernel<<<(n + 63) / 64, 64>>>((const tpk::QueryPOD*)dq.p, n, (tp_redist_result*)dr.p);
+  query_kernel<<<(n + 3) / 4, 128>>>((const tpk::QueryPOD*)dq.p, n, (tp_redist_result*)dr.p,
+                                      (tpk::Trace*)dtr.p);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpy(r, dr.p, sizeof(tp_redist_result) * n, cudaMemcpyDeviceToHost));
   dq.release();
   dr.release();
+  dtr.release();
   return TP_OK;
 }
 
