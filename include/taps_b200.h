@@ -260,6 +260,12 @@ typedef struct tp_redist_result {
 
 tp_status tp_redistribute_batch(const tp_redist_query* queries, int32_t n,
                                 tp_redist_result* results);
+/* Same, choosing the kernel form of the pair path: 1 = warp per pair (used
+ * for small class tables), 2 = thread per pair (large ones). */
+tp_status tp_redistribute_batch_form(const tp_redist_query* queries, int32_t n,
+                                     tp_redist_result* results, int32_t form);
+/* Force the pair form of a plan: 0 = by size (default), 1 = warp, 2 = thread. */
+tp_status tp_plan_set_pair_form(tp_plan* plan, int32_t form);
 
 const char* tp_last_error(void);
 int32_t tp_last_error_kind(void);

@@ -223,6 +223,10 @@ def load_engine() -> C.CDLL:
     lib.tp_enumerate_strategies.restype = C.c_int
     lib.tp_redistribute_batch.argtypes = [P(tp_redist_query), C.c_int32, P(tp_redist_result)]
     lib.tp_redistribute_batch.restype = C.c_int
+    lib.tp_redistribute_batch_form.argtypes = [P(tp_redist_query), C.c_int32, P(tp_redist_result), C.c_int32]
+    lib.tp_redistribute_batch_form.restype = C.c_int
+    lib.tp_plan_set_pair_form.argtypes = [C.c_void_p, C.c_int32]
+    lib.tp_plan_set_pair_form.restype = C.c_int
     lib.tp_last_error.argtypes = []
     lib.tp_last_error.restype = C.c_char_p
     lib.tp_last_error_kind.argtypes = []
@@ -238,6 +242,7 @@ EXPORTED_SYMBOLS = (
     "tp_build_cost_tensors", "tp_plan_create", "tp_plan_destroy", "tp_plan_sizes",
     "tp_plan_index", "tp_plan_upload", "tp_plan_execute", "tp_plan_execute_host", "tp_plan_check_errors",
     "tp_plan_last_launches", "tp_plan_set_profile_events", "tp_enumerate_strategies", "tp_redistribute_batch",
+    "tp_redistribute_batch_form", "tp_plan_set_pair_form",
     "tp_last_error", "tp_last_error_kind", "tp_abi_version",
 )
 

@@ -8,7 +8,7 @@ import sys
 from .abi import ENGINE_SO, PKG_DIR, REPO_DIR
 
 SOURCES = [os.path.join(PKG_DIR, "csrc", "tp_engine.cu")]
-DEPS = SOURCES + [os.path.join(PKG_DIR, "csrc", "tp_core.cuh"),
+DEPS = SOURCES + [os.path.join(PKG_DIR, "csrc", "tp_core.cuh"), os.path.join(PKG_DIR, "csrc", "tp_fast.cuh"),
                   os.path.join(REPO_DIR, "include", "taps_b200.h")]
 
 NVCC_FLAGS = [
@@ -47,7 +47,7 @@ def build_devcheck() -> str:
     """Host compilation of tp_core.cuh for the CPU-side logic check."""
     src = os.path.join(REPO_DIR, "tests", "devcheck", "core_host.cpp")
     out = os.path.join(REPO_DIR, "tests", "devcheck", "libcore_host.so")
-    if _stale(out, [src, os.path.join(PKG_DIR, "csrc", "tp_core.cuh")]):
+    if _stale(out, [src, os.path.join(PKG_DIR, "csrc", "tp_core.cuh"), os.path.join(PKG_DIR, "csrc", "tp_fast.cuh")]):
         subprocess.run([os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-fPIC", "-shared",
                         "-ffp-contract=off", "-o", out, src], check=True)
     return out

@@ -35,6 +35,7 @@
 
 #include "../../include/taps_b200.h"
 #include "tp_core.cuh"
+#include "tp_fast.cuh"
 #include "tp_warp.cuh"
 
 using tpk::DimT;
@@ -164,8 +165,13 @@ struct TableDesc {
   int32_t p, n;
 };
 
-constexpr int kBuildThreads = 128;
-constexpr int kPairsPerBlock = kBuildThreads / 32;  // one warp per class pair
+constexpr int kBuildThreads = 64;       // thread-per-pair form
+constexpr int kBuildWarpThreads = 128;  // warp-per-pair form
+constexpr int kWarpPairsPerBlock = kBuildWarpThreads / 32;
+// Below this many class pairs the GPU cannot be filled with one thread per
+// pair (latency-bound), so a warp cooperates on each pair; above it the
+// register-resident thread form has ~6x fewer instructions per pair.
+constexpr int64_t kWarpPairLimit = 16384;
 constexpr int kExpThreads = 256;
 constexpr int kExpPer = 8;
 constexpr int kExpTile = kExpThreads * kExpPer;  // class pairs per CTA tile
@@ -275,8 +281,36 @@ __device__ void node_row(const BuildArgs& a, int64_t row) {
   a.cls_memdiv[row] = mem / cd.indeg;  // aux_graph.hpp:292
 }
 
-// One (edge class, su, sw) pair on one warp: redistribution seconds and volume.
+// One (edge class, su, sw) pair: redistribution seconds and volume.
 __device__ void pair_row(const BuildArgs& a, int64_t idx) {
+  int lo = 0, hi = a.nsigs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.sigs[mid].pair_begin <= idx) lo = mid; else hi = mid - 1;
+  }
+  const SigDesc& sg = a.sigs[lo];
+  const int32_t local = (int32_t)(idx - sg.pair_begin);
+  const int32_t su = local / sg.Sw, sw = local - su * sg.Sw;
+  const Strat su_s = a.tables[sg.tab_u + su];
+  const Strat sw_s = a.tables[sg.tab_w + sw];
+  Lay F, T;
+  tpk::side_layout(su_s, sg.sa_u, sg.R, F);
+  tpk::side_layout(sw_s, sg.sa_w, sg.R, T);
+  double sec = 0, vol = 0;
+  if (!tpk::same_layout(F, T, sg.R)) {  // aux_graph.hpp:260
+    const double bytes = sg.has_override ? a.overrides[idx] : sg.bytes;
+    const int st = tpk::pair_cost(sg.R, F, T, sg.dt, bytes, a.env, a.l_log2, sec, vol, nullptr);
+    if (st) {
+      flag_error(a.err, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
+      sec = vol = 0;
+    }
+  }
+  a.r_sec[idx] = sec;
+  a.r_vol[idx] = vol;
+}
+
+// One (edge class, su, sw) pair on one warp (tp_warp.cuh).
+__device__ void pair_row_warp(const BuildArgs& a, int64_t idx) {
   int lo = 0, hi = a.nsigs - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -309,15 +343,26 @@ __device__ void pair_row(const BuildArgs& a, int64_t idx) {
   }
 }
 
-// K1: node-class rows (a thread each) in blocks [0, node_blocks), then
-// edge-class pairs (a warp each).
+// K1 (warp form): node-class rows (a thread each), then pairs (a warp each).
+__global__ void __launch_bounds__(kBuildWarpThreads) build_kernel_warp(BuildArgs a) {
+  if ((int64_t)blockIdx.x < a.node_blocks) {
+    const int64_t row = (int64_t)blockIdx.x * kBuildWarpThreads + threadIdx.x;
+    if (row < a.total_rows) node_row(a, row);
+  } else {
+    const int64_t idx = ((int64_t)blockIdx.x - a.node_blocks) * kWarpPairsPerBlock + (threadIdx.x >> 5);
+    if (idx < a.total_pairs) pair_row_warp(a, idx);  // warp-uniform
+  }
+}
+
+// K1 (thread form): node-class rows in blocks [0, node_blocks), then
+// edge-class pairs; one thread each.
 __global__ void __launch_bounds__(kBuildThreads) build_kernel(BuildArgs a) {
   if ((int64_t)blockIdx.x < a.node_blocks) {
     const int64_t row = (int64_t)blockIdx.x * kBuildThreads + threadIdx.x;
     if (row < a.total_rows) node_row(a, row);
   } else {
-    const int64_t idx = ((int64_t)blockIdx.x - a.node_blocks) * kPairsPerBlock + (threadIdx.x >> 5);
-    if (idx < a.total_pairs) pair_row(a, idx);  // warp-uniform
+    const int64_t idx = ((int64_t)blockIdx.x - a.node_blocks) * kBuildThreads + threadIdx.x;
+    if (idx < a.total_pairs) pair_row(a, idx);
   }
 }
 
@@ -437,9 +482,18 @@ __global__ void rowmin_kernel(const EdgeDesc* __restrict__ edges, const int64_t*
   }
 }
 
-// Verification export: one warp per query, the kernels' own code path.
-__global__ void query_kernel(const tpk::QueryPOD* __restrict__ q, int n, tp_redist_result* __restrict__ r,
-                             tpk::Trace* __restrict__ traces) {
+// Verification export through the kernels' pair paths: thread form...
+__global__ void query_kernel(const tpk::QueryPOD* __restrict__ q, int n, tp_redist_result* __restrict__ r) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  tp_redist_result res;
+  res.status = tpk::run_query_fast(q[i], res);
+  r[i] = res;
+}
+
+// ... and warp form (one warp per query).
+__global__ void query_kernel_warp(const tpk::QueryPOD* __restrict__ q, int n, tp_redist_result* __restrict__ r,
+                                  tpk::Trace* __restrict__ traces) {
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= n) return;
   const int st = tpk::run_query_warp(q[i], r[i], traces[i]);
@@ -554,6 +608,7 @@ struct tp_plan {
   int32_t last_e0 = -1, last_e1 = -1;
   cudaStream_t last_stream = nullptr;
   cudaEvent_t prof_start = nullptr, prof_stop = nullptr;  // recorded around K2
+  int pair_form = 0;  // 0 = by size, 1 = warp per pair, 2 = thread per pair
 };
 
 namespace {
@@ -1247,10 +1302,20 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   a.l_log2 = (p->env.local > 0 && (p->env.local & (p->env.local - 1)) == 0) ? log2_floor(p->env.local) : -1;
   a.n_log2 = p->n_log2;
   a.err = err;
-  const int64_t blocks = a.node_blocks + (a.total_pairs + kPairsPerBlock - 1) / kPairsPerBlock;
-  if (blocks > 0) {
-    build_kernel<<<(unsigned)blocks, kBuildThreads, 0, s>>>(a);
-    ++launches;
+  const bool warp_form = p->pair_form == 1 || (p->pair_form == 0 && a.total_pairs <= kWarpPairLimit);
+  if (warp_form) {
+    a.node_blocks = (p->total_rows + kBuildWarpThreads - 1) / kBuildWarpThreads;
+    const int64_t blocks = a.node_blocks + (a.total_pairs + kWarpPairsPerBlock - 1) / kWarpPairsPerBlock;
+    if (blocks > 0) {
+      build_kernel_warp<<<(unsigned)blocks, kBuildWarpThreads, 0, s>>>(a);
+      ++launches;
+    }
+  } else {
+    const int64_t blocks = a.node_blocks + (a.total_pairs + kBuildThreads - 1) / kBuildThreads;
+    if (blocks > 0) {
+      build_kernel<<<(unsigned)blocks, kBuildThreads, 0, s>>>(a);
+      ++launches;
+    }
   }
   // K2: fan-out to the aux edges of [e0, e1) (+ the node tensors)
   const int64_t out_offset = p->edge_base[e0];
@@ -1302,6 +1367,12 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
 }
 
 int64_t tp_plan_last_launches(const tp_plan* p) { return p ? p->last_launches : 0; }
+
+tp_status tp_plan_set_pair_form(tp_plan* p, int32_t form) {
+  if (!p || form < 0 || form > 2) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "pair form must be 0, 1 or 2");
+  p->pair_form = form;
+  return TP_OK;
+}
 
 tp_status tp_plan_set_profile_events(tp_plan* p, void* start_event, void* stop_event) {
   if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
@@ -1443,6 +1514,10 @@ tp_status tp_enumerate_strategies(int32_t p, int64_t total_devices, int64_t* cou
 }
 
 tp_status tp_redistribute_batch(const tp_redist_query* q, int32_t n, tp_redist_result* r) {
+  return tp_redistribute_batch_form(q, n, r, 2);
+}
+
+tp_status tp_redistribute_batch_form(const tp_redist_query* q, int32_t n, tp_redist_result* r, int32_t form) {
   if (n <= 0) return TP_OK;
   if (!q || !r) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null argument");
   int ndev = 0;
@@ -1474,10 +1549,14 @@ tp_status tp_redistribute_batch(const tp_redist_query* q, int32_t n, tp_redist_r
   DevBuf dq, dr, dtr;
   CUDA_TRY(dq.ensure(sizeof(tpk::QueryPOD) * n));
   CUDA_TRY(dr.ensure(sizeof(tp_redist_result) * n));
-  CUDA_TRY(dtr.ensure(sizeof(tpk::Trace) * n));
   CUDA_TRY(cudaMemcpy(dq.p, pod.data(), sizeof(tpk::QueryPOD) * n, cudaMemcpyHostToDevice));
-  query_kernel<<<(n + 3) / 4, 128>>>((const tpk::QueryPOD*)dq.p, n, (tp_redist_result*)dr.p,
-                                      (tpk::Trace*)dtr.p);
+  if (form == 1) {
+    CUDA_TRY(dtr.ensure(sizeof(tpk::Trace) * n));
+    query_kernel_warp<<<(n + 3) / 4, 128>>>((const tpk::QueryPOD*)dq.p, n, (tp_redist_result*)dr.p,
+                                             (tpk::Trace*)dtr.p);
+  } else {
+    query_kernel<<<(n + 63) / 64, 64>>>((const tpk::QueryPOD*)dq.p, n, (tp_redist_result*)dr.p);
+  }
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpy(r, dr.p, sizeof(tp_redist_result) * n, cudaMemcpyDeviceToHost));
   dq.release();

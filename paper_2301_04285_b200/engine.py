@@ -143,6 +143,10 @@ class Plan:
             self.handle, C.c_void_p(start.cuda_event if start is not None else None),
             C.c_void_p(stop.cuda_event if stop is not None else None)))
 
+    def set_pair_form(self, form: int):
+        """0 = by size (default), 1 = warp per class pair, 2 = thread per pair."""
+        _check(self.lib, self.lib.tp_plan_set_pair_form(self.handle, form))
+
     def last_launches(self) -> int:
         return int(self.lib.tp_plan_last_launches(self.handle))
 
@@ -218,10 +222,12 @@ def device_cost_struct(tensors: dict) -> abi.tp_cost_tensors:
 
 
 def build_cost_tensors(graph, topo: ClusterTopology, records=False, row_min=False,
-                       edge_range=(0, -1), device=-1, pinned=False) -> CostTensors:
+                       edge_range=(0, -1), device=-1, pinned=False, pair_form: int = 0) -> CostTensors:
     """The drop-in for build_auxiliary_graph: host graph in, host tensors out."""
-    return Plan(graph, topo, device).execute_host(records=records, row_min=row_min,
-                                                  edge_range=edge_range, pinned=pinned)
+    plan = Plan(graph, topo, device)
+    if pair_form:
+        plan.set_pair_form(pair_form)
+    return plan.execute_host(records=records, row_min=row_min, edge_range=edge_range, pinned=pinned)
 
 
 def enumerate_strategies(p: int, total_devices: int):
@@ -242,12 +248,13 @@ def enumerate_strategies(p: int, total_devices: int):
     return deg.reshape(S, p), dm.reshape(S, p), md.reshape(S, p), dep
 
 
-def redistribute_batch(queries):
+def redistribute_batch(queries, form: int = 2):
     """Verification export: each tp_redist_query evaluated by the device
-    kernel's code path (unify + inference + pricing)."""
+    kernels' pair path (unify + inference + pricing); form 1 = warp per
+    pair, 2 = thread per pair."""
     lib = abi.load_engine()
     n = len(queries)
     arr = (abi.tp_redist_query * n)(*queries)
     res = (abi.tp_redist_result * n)()
-    _check(lib, lib.tp_redistribute_batch(arr, n, res))
+    _check(lib, lib.tp_redistribute_batch_form(arr, n, res, form))
     return list(res)

@@ -29,3 +29,22 @@ extern "C" int core_unrank(int p, int n, long long s, int* deg, int* dmap, int* 
   *depth = st.depth;
   return 0;
 }
+
+#include "../../paper_2301_04285_b200/csrc/tp_fast.cuh"
+
+// The register-resident pair path the kernels run (tp_fast.cuh).
+extern "C" int core_redistribute_fast(const tp_redist_query* q, tp_redist_result* r) {
+  std::memset(r, 0, sizeof(*r));
+  tpk::QueryPOD p{};
+  p.rank = q->rank;
+  p.fdepth = q->from_depth;
+  p.tdepth = q->to_depth;
+  p.local = q->local_device_num;
+  if (q->rank > tpk::kMaxR || q->from_depth > tpk::kMaxD || q->to_depth > tpk::kMaxD) return r->status = tpk::kCapacity;
+  for (int i = 0; i < q->rank; ++i) { p.shape[i] = q->shape[i]; p.fmap[i] = q->from_map[i]; p.tmap[i] = q->to_map[i]; }
+  for (int k = 0; k < q->from_depth; ++k) p.fdims[k] = q->from_dims[k];
+  for (int k = 0; k < q->to_depth; ++k) p.tdims[k] = q->to_dims[k];
+  p.bytes = q->tensor_bytes; p.intra = q->intra_bandwidth; p.inter = q->inter_bandwidth;
+  r->status = tpk::run_query_fast(p, *r);
+  return r->status;
+}

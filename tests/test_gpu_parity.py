@@ -22,6 +22,9 @@ def gpu_build(g, t, **kw):
     return engine.build_cost_tensors(g, t, **kw)
 
 
+FORMS = [1, 2]  # pair path: warp per pair, thread per pair
+
+
 def assert_same(gpu, ref, rowmin=False, records=False):
     for k in INDEX:
         np.testing.assert_array_equal(getattr(gpu, k), getattr(ref, k), err_msg=k)
@@ -76,10 +79,11 @@ def _query(c):
                         tensor_bytes=c["tensor_bytes"], local=c["local"], intra=c["intra"], inter=c["inter"])
 
 
-def test_redistribution_goldens():
+@pytest.mark.parametrize("form", FORMS)
+def test_redistribution_goldens(form):
     cases = golden()["redistributions"]
     qs = [_query(c) for c in cases]
-    res = engine.redistribute_batch(qs)
+    res = engine.redistribute_batch(qs, form=form)
     for c, r in zip(cases, res):
         if c["status"] != 0:
             assert r.status != 0, c
@@ -96,7 +100,8 @@ def test_redistribution_goldens():
         assert bits([r.seconds])[0] == bits([unhex(c["seconds"])])[0]
 
 
-def test_redistribution_random_vs_oracle():
+@pytest.mark.parametrize("form", FORMS)
+def test_redistribution_random_vs_oracle(form):
     rng = random.Random(99)
     qs = []
     for i in range(4000):
@@ -110,7 +115,7 @@ def test_redistribution_random_vs_oracle():
             shape = [s * rng.choice([1, 3, 5, 7]) for s in shape]
         qs.append(B.make_query(shape, dims, fm, d2, tm, local=rng.choice([1, 2, 4, 8, 16]),
                                inter=rng.choice([6e9, 60e9, 1.5e9])))
-    res = engine.redistribute_batch(qs)
+    res = engine.redistribute_batch(qs, form=form)
     for q, r in zip(qs, res):
         o = B.oracle_redistribute(q)
         assert r.status == o.status
@@ -120,14 +125,15 @@ def test_redistribution_random_vs_oracle():
             assert bits([r.volume_bytes])[0] == bits([o.volume_bytes])[0]
 
 
+@pytest.mark.parametrize("form", FORMS)
 @pytest.mark.parametrize("idx", range(8))
-def test_golden_builds(idx):
+def test_golden_builds(idx, form):
     builds = golden()["builds"]
     if idx >= len(builds):
         pytest.skip("no such golden")
     c = builds[idx]
     g, t = graph_of(c["graph"]), topo_of(c["topo"])
-    got = gpu_build(g, t, row_min=True)
+    got = gpu_build(g, t, row_min=True, pair_form=form)
     assert got.node_base.tolist() == c["node_base"]
     assert got.edge_base.tolist() == c["edge_base"]
     assert got.topo_order.tolist() == c["topo_order"]
@@ -136,11 +142,12 @@ def test_golden_builds(idx):
         assert np.array_equal(bits(getattr(got, k)), bits(exp)), (c["name"], k)
 
 
+@pytest.mark.parametrize("form", FORMS)
 @pytest.mark.parametrize("name", ["cfg1", "cfg2"])
-def test_configs_vs_oracle(name):
+def test_configs_vs_oracle(name, form):
     g, t = M.CONFIGS[name]()
     f = G.flatten(g)
-    gpu = gpu_build(f, t, records=True, row_min=True)
+    gpu = gpu_build(f, t, records=True, row_min=True, pair_form=form)
     ref = B.oracle_build(f, t)
     assert ref.status == 0
     assert_same(gpu, ref, rowmin=True, records=True)
@@ -148,17 +155,19 @@ def test_configs_vs_oracle(name):
         assert len(gpu.node_intra_cost_s) == 48 and len(gpu.edge_cost_s) == 252
 
 
+@pytest.mark.parametrize("form", FORMS)
 @pytest.mark.parametrize("nodes,ratio", [(2, 1), (4, 10), (8, 100)])
-def test_cfg3_vs_oracle(nodes, ratio):
+def test_cfg3_vs_oracle(nodes, ratio, form):
     g, t = M.cfg3(nodes, ratio)
     f = G.flatten(g)
-    gpu = gpu_build(f, t)
+    gpu = gpu_build(f, t, pair_form=form)
     ref = B.oracle_build(f, t, records=False)
     assert_same(gpu, ref)
     assert len(gpu.edge_cost_s) == {2: 95936, 4: 190940, 8: 335088}[nodes]
 
 
-def test_random_graphs_vs_oracle():
+@pytest.mark.parametrize("form", FORMS)
+def test_random_graphs_vs_oracle(form):
     rng = random.Random(1234)
     ok = err = 0
     for i in range(150):
@@ -167,21 +176,22 @@ def test_random_graphs_vs_oracle():
         ref = B.oracle_build(f, t)
         if ref.status != 0:
             with pytest.raises((abi.TopoplanError, IndexError)):
-                gpu_build(f, t)
+                gpu_build(f, t, pair_form=form)
             err += 1
             continue
-        gpu = gpu_build(f, t, records=True, row_min=True)
+        gpu = gpu_build(f, t, records=True, row_min=True, pair_form=form)
         assert_same(gpu, ref, rowmin=True, records=True)
         ok += 1
     assert ok > 20 and err > 10
 
 
-def test_planning_instances_vs_oracle():
+@pytest.mark.parametrize("form", FORMS)
+def test_planning_instances_vs_oracle(form):
     rng = random.Random(17)
     for _ in range(40):
         g, t = fuzz.random_planning_instance(rng)
         f = G.flatten(g)
-        assert_same(gpu_build(f, t, row_min=True), B.oracle_build(f, t), rowmin=True)
+        assert_same(gpu_build(f, t, row_min=True, pair_form=form), B.oracle_build(f, t), rowmin=True)
 
 
 def test_edge_range_shards_concatenate():
