@@ -1,0 +1,240 @@
+// adapter_parity.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// Runs the reference's build_auxiliary_graph (the UNMODIFIED headers from
+// /root/reference, included at build time) and the B200 drop-in
+// taps_b200::build_auxiliary_graph_b200 on the same inputs and checks that
+// every field of the two topoplan::AuxiliaryGraph objects is identical
+// (costs bit-for-bit), then that the reference's own ILP solver
+// (formulate + solve, solver.hpp:69-493) selects the same strategies with
+// the same objective on both, that price_assignment agrees and that
+// export_lp emits the same text. Built by oracle/Makefile into
+// oracle/_ref/adapter_parity; run on a GPU box by tests/test_gpu_adapter.py.
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+
+#include "topoplan/aux_graph.hpp"
+#include "topoplan/models.hpp"
+#include "topoplan/solver.hpp"
+#include "test_support.hpp"  // the reference's test oracles, -I$(REF_TESTS) (see Makefile)
+#include "taps_b200/aux_graph_b200.hpp"
+
+using namespace topoplan;
+
+namespace {
+
+int failures = 0;
+
+bool same_bits(double a, double b) { return std::memcmp(&a, &b, sizeof(double)) == 0; }
+
+std::string compare(const AuxiliaryGraph& r, const AuxiliaryGraph& g) {
+  if (r.nodes.size() != g.nodes.size()) return "node count";
+  if (r.edges.size() != g.edges.size()) return "edge count";
+  if (r.virtual_edges.size() != g.virtual_edges.size()) return "virtual edge count";
+  if (r.topo_order != g.topo_order) return "topo_order";
+  if (r.edge_base != g.edge_base) return "edge_base";
+  if (r.in_degree_of != g.in_degree_of || r.out_degree_of != g.out_degree_of) return "degrees";
+  if (r.nodes_of_op != g.nodes_of_op) return "nodes_of_op";
+  if (r.virtual_edge_of_node != g.virtual_edge_of_node) return "virtual_edge_of_node";
+  for (std::size_t i = 0; i < r.nodes.size(); ++i) {
+    const AuxNode &a = r.nodes[i], &b = g.nodes[i];
+    if (a.op_index != b.op_index || a.strategy_index != b.strategy_index) return "node index " + std::to_string(i);
+    if (!(a.strategy == b.strategy) || !(a.strategy.device_matrix == b.strategy.device_matrix) ||
+        a.strategy.op_id != b.strategy.op_id)
+      return "node strategy " + std::to_string(i);
+    if (!same_bits(a.intra_cost_s, b.intra_cost_s) || !same_bits(a.intra_volume_bytes, b.intra_volume_bytes) ||
+        !same_bits(a.memory_bytes, b.memory_bytes))
+      return "node payload " + std::to_string(i);
+  }
+  for (std::size_t e = 0; e < r.edges.size(); ++e) {
+    const AuxEdge &a = r.edges[e], &b = g.edges[e];
+    if (a.original_edge != b.original_edge || a.from_node != b.from_node || a.to_node != b.to_node)
+      return "edge index " + std::to_string(e);
+    if (!same_bits(a.cost_s, b.cost_s) || !same_bits(a.volume_bytes, b.volume_bytes) ||
+        !same_bits(a.memory_bytes, b.memory_bytes))
+      return "edge payload " + std::to_string(e);
+  }
+  for (std::size_t v = 0; v < r.virtual_edges.size(); ++v) {
+    const VirtualEdge &a = r.virtual_edges[v], &b = g.virtual_edges[v];
+    if (a.op_index != b.op_index || a.to_node != b.to_node || !same_bits(a.cost_s, b.cost_s) ||
+        !same_bits(a.volume_bytes, b.volume_bytes) || !same_bits(a.memory_bytes, b.memory_bytes))
+      return "virtual edge " + std::to_string(v);
+  }
+  return "";
+}
+
+void report(const std::string& name, const std::string& err, const std::string& extra = "") {
+  std::printf("[PARITY] %-34s %s%s%s\n", name.c_str(), err.empty() ? "PASS" : "FAIL", err.empty() ? "" : ": ",
+              err.empty() ? extra.c_str() : err.c_str());
+  std::fflush(stdout);
+  if (!err.empty()) ++failures;
+}
+
+struct SolveCfg {
+  bool solve = false;
+  int threads = 8;
+  std::int64_t max_nodes = 200'000'000;
+};
+
+void check_case(const std::string& name, const ComputationGraph& graph, const ClusterTopology& topo,
+                SolveCfg sc = {}) {
+  AuxiliaryGraph ref, gpu;
+  std::string ref_err, gpu_err;
+  try {
+    ref = build_auxiliary_graph(graph, topo);
+  } catch (const Error& e) {
+    ref_err = "Error";
+  } catch (const std::out_of_range& e) {
+    ref_err = "out_of_range";
+  }
+  try {
+    gpu = taps_b200::build_auxiliary_graph_b200(graph, topo, CostMode::kTopology, -1, true);
+  } catch (const Error& e) {
+    gpu_err = "Error";
+  } catch (const std::out_of_range& e) {
+    gpu_err = "out_of_range";
+  }
+  if (!ref_err.empty() || !gpu_err.empty()) {
+    report(name, ref_err == gpu_err ? "" : "reference threw '" + ref_err + "', b200 threw '" + gpu_err + "'",
+           "both throw " + ref_err);
+    return;
+  }
+  std::string err = compare(ref, gpu);
+  // edge_weight (aux_graph.hpp:184) through the adapter's layouts
+  if (err.empty() && !ref.edges.empty()) {
+    const EdgeWeight a = edge_weight(ref.graph, 0, ref.nodes[ref.edges[0].from_node],
+                                     ref.nodes[ref.edges[0].to_node], topo);
+    const EdgeWeight b = edge_weight(gpu.graph, 0, gpu.nodes[gpu.edges[0].from_node],
+                                     gpu.nodes[gpu.edges[0].to_node], topo);
+    if (!same_bits(a.cost_s, b.cost_s)) err = "edge_weight via layouts";
+  }
+  std::string extra = std::to_string(gpu.edges.size()) + " aux edges bit-identical";
+  if (err.empty() && sc.solve) {
+    for (CostMode mode : {CostMode::kTopology, CostMode::kVolume}) {
+      SolveOptions opts;
+      opts.threads = sc.threads;
+      opts.max_nodes = sc.max_nodes;
+      const PlanSolution a = solve(formulate(ref, mode, topo.device_memory), opts);
+      const PlanSolution b = solve(formulate(gpu, mode, topo.device_memory), opts);
+      if (a.feasible != b.feasible || a.strategy_per_op != b.strategy_per_op || !same_bits(a.objective, b.objective) ||
+          a.optimal != b.optimal) {
+        err = std::string("ILP differs (") + to_string(mode) + ")";
+        break;
+      }
+      if (export_lp(formulate(ref, mode, topo.device_memory)) != export_lp(formulate(gpu, mode, topo.device_memory))) {
+        err = std::string("export_lp differs (") + to_string(mode) + ")";
+        break;
+      }
+      char buf[160];
+      std::snprintf(buf, sizeof(buf), "; ILP %s obj %.6g %s", to_string(mode), a.objective,
+                    a.optimal ? "optimal" : "budget");
+      extra += buf;
+    }
+    std::mt19937 rng(7);
+    for (int t = 0; err.empty() && t < 50; ++t) {
+      std::vector<int> asg(graph.operators.size());
+      for (std::size_t i = 0; i < asg.size(); ++i) asg[i] = (int)(rng() % ref.strategies_of((int)i));
+      for (CostMode mode : {CostMode::kTopology, CostMode::kVolume}) {
+        const AssignmentPrice a = price_assignment(ref, asg, mode), b = price_assignment(gpu, asg, mode);
+        if (!same_bits(a.cost, b.cost) || !same_bits(a.memory_bytes, b.memory_bytes)) err = "price_assignment";
+      }
+    }
+  }
+  report(name, err, extra);
+}
+
+ComputationGraph gpt_chain(int layers, std::int64_t hidden, std::int64_t batch, std::int64_t seq) {
+  ModelConfig cfg;
+  cfg.family = ModelFamily::kTransformerLayer;
+  cfg.hidden = hidden;
+  cfg.batch = batch;
+  cfg.seq = seq;
+  const ComputationGraph layer = build_transformer_layer(cfg);
+  ComputationGraph g;
+  std::string x = "x";
+  for (int l = 0; l < layers; ++l) {
+    const std::string p = "L" + std::to_string(l) + ".";
+    auto ren = [&](const std::string& n) { return n == "x" ? x : p + n; };
+    for (OperatorNode op : layer.operators) {
+      op.id = p + op.id;
+      for (auto& t : op.inputs) t.name = ren(t.name);
+      for (auto& t : op.outputs) t.name = ren(t.name);
+      for (auto& a : op.axes)
+        for (auto& s : a.slices) s.tensor = ren(s.tensor);
+      g.operators.push_back(op);
+    }
+    if (l > 0) g.edges.push_back({"L" + std::to_string(l - 1) + ".add2", p + "ln1", x});
+    for (const GraphEdge& e : layer.edges) g.edges.push_back({p + e.from, p + e.to, ren(e.tensor)});
+    x = p + "add2_out";
+  }
+  return g;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  const bool big = argc > 1 && std::string(argv[1]) == "--big";
+  const ClusterTopology t2x4{2, 4, 60e9, 6e9, 32e9};
+  {  // cfg1: data/sample_graph.json on 2 x 4
+    ComputationGraph g;
+    g.operators.push_back(testing::matmul_op("fc1", 256, 1024, 4096, "x0", "x1"));
+    g.operators.push_back(testing::elementwise_op("relu", {"x1"}, "x2", 256, 4096));
+    g.operators.push_back(testing::matmul_op("fc2", 256, 4096, 1024, "x2", "x3"));
+    g.edges = {{"fc1", "relu", "x1"}, {"relu", "fc2", "x2"}};
+    check_case("cfg1 sample graph 2x4", g, t2x4, SolveCfg{true});
+  }
+  {
+    ComputationGraph chain;
+    chain.operators.push_back(testing::matmul_op("fc1", 16, 16, 16, "x0", "x1"));
+    chain.operators.push_back(testing::matmul_op("fc2", 16, 16, 16, "x1", "x2"));
+    chain.edges.push_back({"fc1", "fc2", "x1"});
+    check_case("two-matmul chain 1x4", chain, {1, 4, 60e9, 60e9, 32e9}, SolveCfg{true});
+    check_case("two-matmul chain 2x2", chain, {2, 2, 60e9, 6e9, 32e9}, SolveCfg{true});
+    ComputationGraph one;
+    one.operators.push_back(testing::matmul_op("fc", 8, 8, 8));
+    check_case("single op single device", one, {1, 1, 60e9, 60e9, 32e9}, SolveCfg{true});
+    ComputationGraph bad;
+    bad.operators.push_back(testing::matmul_op("fc", 6, 6, 6));
+    check_case("indivisible shapes throw", bad, {1, 4, 60e9, 60e9, 32e9});
+    ComputationGraph dangling = chain;
+    dangling.edges.push_back({"fc2", "nope", "x2"});
+    check_case("dangling edge throws", dangling, {1, 4, 60e9, 60e9, 32e9});
+    ComputationGraph missing = chain;
+    missing.edges.push_back({"fc1", "fc2", "nope"});
+    check_case("missing edge tensor throws", missing, {1, 4, 60e9, 60e9, 32e9});
+  }
+  {
+    ModelConfig tl;
+    tl.family = ModelFamily::kTransformerLayer;
+    tl.hidden = 256;
+    tl.seq = 64;
+    tl.batch = 4;
+    check_case("transformer-layer h256 2x4", build_graph(tl), {2, 4, 60e9, 6e9, 80e9}, SolveCfg{true});
+    check_case("alexnet-like 2x8", build_graph(parse_model_spec("alexnet-like")), {2, 8, 60e9, 6e9, 256e9},
+               SolveCfg{true});
+    check_case("mlp-chain 4x8", build_graph(parse_model_spec("mlp-chain")), {4, 8, 60e9, 6e9, 256e9},
+               SolveCfg{true});
+    ModelConfig c2;
+    c2.family = ModelFamily::kTransformerLayer;
+    c2.hidden = 4096;
+    c2.batch = 8;
+    c2.seq = 512;
+    check_case("cfg2 transformer h4096 4x8", build_graph(c2), {4, 8, 60e9, 6e9, 80e9}, SolveCfg{true, 16});
+  }
+  {
+    std::mt19937 rng(4096);
+    for (int i = 0; i < 40; ++i) {
+      const auto inst = testing::random_planning_instance(rng, 6, 2e5);
+      check_case("random planning instance " + std::to_string(i), inst.graph, inst.topo, SolveCfg{i % 4 == 0});
+    }
+  }
+  {  // cfg3 (24 layers) with a fixed node budget, threads=1 (deterministic truncated search)
+    SolveCfg sc{true, 1, 200000};
+    check_case("cfg3 GPT-24 h2048 2x8", gpt_chain(24, 2048, 8, 512), {2, 8, 60e9, 6e9, 80e9}, sc);
+    check_case("cfg3 GPT-24 h2048 8x8 r100", gpt_chain(24, 2048, 8, 512), {8, 8, 60e9, 0.6e9, 80e9}, SolveCfg{});
+    if (big) check_case("cfg4 GPT-96 h12288 16x8", gpt_chain(96, 12288, 8, 2048), {16, 8, 60e9, 6e9, 80e9}, SolveCfg{});
+  }
+  std::printf("[PARITY] %s (%d failures)\n", failures ? "FAILED" : "ALL PASS", failures);
+  return failures ? 1 : 0;
+}

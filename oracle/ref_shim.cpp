@@ -29,8 +29,14 @@ using namespace topoplan;
 
 namespace {
 
-thread_local int g_last_kind = 0;
-thread_local std::string g_last_msg;
+// POD thread-locals only: a non-trivial thread_local in a dlopen'ed library
+// crashed when numpy's runtime was loaded first.
+thread_local char g_last_msg[1024];
+
+void set_msg(const char* m) {
+  std::strncpy(g_last_msg, m, sizeof(g_last_msg) - 1);
+  g_last_msg[sizeof(g_last_msg) - 1] = 0;
+}
 
 std::string op_name(int id) { return "op" + std::to_string(id); }
 std::string t_name(int id) { return "t" + std::to_string(id); }
@@ -141,17 +147,16 @@ template <typename F>
 int guarded(F&& f) {
   try {
     f();
-    g_last_kind = 0;
-    g_last_msg.clear();
+    set_msg("");
     return TP_OK;
   } catch (const Error& e) {
-    g_last_msg = e.what();
+    set_msg(e.what());
     return TP_ERR_TOPOPLAN;
   } catch (const std::out_of_range& e) {
-    g_last_msg = e.what();
+    set_msg(e.what());
     return TP_ERR_OUT_OF_RANGE;
   } catch (const std::exception& e) {
-    g_last_msg = e.what();
+    set_msg(e.what());
     return TP_ERR_INVALID_ARGUMENT;
   }
 }
@@ -200,7 +205,7 @@ void dump_graph(std::ostringstream& o, const ComputationGraph& g) {
 
 extern "C" {
 
-const char* ref_last_error() { return g_last_msg.c_str(); }
+const char* ref_last_error() { return g_last_msg; }
 
 // build_auxiliary_graph (aux_graph.hpp:211) -> SoA / AoS export.
 int ref_build(const tp_graph_desc* g, const tp_topology_desc* t,

@@ -48,11 +48,14 @@ namespace {
 // ---------------------------------------------------------------------------
 // error plumbing
 // ---------------------------------------------------------------------------
-thread_local std::string g_err;
+// POD thread-locals only (a non-trivial thread_local in a dlopen'ed library
+// is fragile when other runtimes were loaded first).
+thread_local char g_err[512];
 thread_local int g_err_kind = 0;
 
 tp_status set_err(tp_status st, int kind, const std::string& msg) {
-  g_err = msg;
+  std::strncpy(g_err, msg.c_str(), sizeof(g_err) - 1);
+  g_err[sizeof(g_err) - 1] = 0;
   g_err_kind = kind;
   return st;
 }
@@ -150,8 +153,15 @@ struct EdgeDesc {
 
 struct Work {
   int32_t sig;
-  int32_t ebeg, eend;  // into the per-execute edge list
+  int32_t ebeg, eend;  // into the per-execute FanEdge list
   int32_t j0;          // first pair of the tile within the class block
+};
+
+struct FanEdge {       // one graph edge of an execute's range
+  int64_t out_base;    // output index of its pair (0, 0)
+  int64_t wrow;        // class row of the consumer's strategy 0
+  int64_t nb_u, nb_w;  // first aux node of producer / consumer (records)
+  int32_t e, pad;
 };
 
 struct NodeWork {      // fan-out of one node class's rows to a chunk of its members
@@ -173,8 +183,9 @@ constexpr int kWarpPairsPerBlock = kBuildWarpThreads / 32;
 // register-resident thread form has ~6x fewer instructions per pair.
 constexpr int64_t kWarpPairLimit = 16384;
 constexpr int kExpThreads = 256;
-constexpr int kExpPer = 8;
+constexpr int kExpPer = 4;
 constexpr int kExpTile = kExpThreads * kExpPer;  // class pairs per CTA tile
+constexpr int kMaxChunk = 64;                    // edges per CTA
 
 // ---------------------------------------------------------------------------
 // kernels
@@ -366,18 +377,18 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(BuildArgs a) {
   }
 }
 
-// K2: fan-out of the class tables to every aux edge of the range. Each CTA
+// K2: fan-out of the class tables to every aux edge of the range. A CTA
 // owns a tile of one edge class's pair block and a chunk of the class's
-// edges; a thread keeps its kExpPer pairs (class-table values and consumer
-// strategy) in registers and, for every edge, writes them at
-// aux_base(edge) + pair: lane-contiguous, so each warp store is 256 B.
+// edges (their descriptors staged in shared memory once). A thread keeps
+// kExpPer pairs of the tile — class-table values and consumer strategy — in
+// registers and, for every edge, writes them at out_base(edge) + pair:
+// lane-contiguous, so each warp store instruction writes 256 B.
 __global__ void __launch_bounds__(kExpThreads) expand_kernel(
-    const Work* __restrict__ work, const SigDesc* __restrict__ sigs,
-    const int32_t* __restrict__ edge_list, const EdgeDesc* __restrict__ edges,
+    const Work* __restrict__ work, const SigDesc* __restrict__ sigs, const FanEdge* __restrict__ fan,
     const double* __restrict__ r_sec, const double* __restrict__ r_vol,
     const double* __restrict__ cls_sec, const double* __restrict__ cls_vol,
-    const double* __restrict__ cls_memdiv, int64_t out_offset, double* __restrict__ e_sec,
-    double* __restrict__ e_vol, double* __restrict__ e_mem, char* __restrict__ records, int num_edge_work,
+    const double* __restrict__ cls_memdiv, double* __restrict__ e_sec, double* __restrict__ e_vol,
+    double* __restrict__ e_mem, char* __restrict__ records, int num_edge_work,
     const NodeWork* __restrict__ nwork, const ClassDesc* __restrict__ classes,
     const int64_t* __restrict__ member_nb, const double* __restrict__ cls_mem, double* __restrict__ n_sec,
     double* __restrict__ n_vol, double* __restrict__ n_mem) {
@@ -396,30 +407,40 @@ __global__ void __launch_bounds__(kExpThreads) expand_kernel(
     }
     return;
   }
+  __shared__ FanEdge sedge[kMaxChunk];
   const Work wk = work[blockIdx.x];
+  const int nE = wk.eend - wk.ebeg;
+  for (int t = threadIdx.x; t < nE; t += kExpThreads) sedge[t] = fan[wk.ebeg + t];
   const SigDesc& sg = sigs[wk.sig];
   const int32_t Sw = sg.Sw;
   const int32_t P = sg.Su * Sw;
+  const int64_t pb = sg.pair_begin;
+  const int32_t step = kExpThreads % Sw;
   int32_t jj[kExpPer], sw[kExpPer];
   double rs[kExpPer], rv[kExpPer];
+  int32_t cur = (wk.j0 + (int32_t)threadIdx.x) % Sw;
 #pragma unroll
   for (int k = 0; k < kExpPer; ++k) {
     const int32_t j = wk.j0 + (int32_t)threadIdx.x + k * kExpThreads;
     jj[k] = j < P ? j : -1;
-    const int32_t jc = j < P ? j : 0;
-    sw[k] = jc % Sw;
-    rs[k] = r_sec[sg.pair_begin + jc];
-    rv[k] = r_vol[sg.pair_begin + jc];
+    sw[k] = cur;
+    cur += step;
+    if (cur >= Sw) cur -= Sw;
+    const int64_t jc = j < P ? j : 0;
+    rs[k] = __ldg(r_sec + pb + jc);
+    rv[k] = __ldg(r_vol + pb + jc);
   }
-  for (int ei = wk.ebeg; ei < wk.eend; ++ei) {
-    const EdgeDesc ed = edges[edge_list[ei]];
-    const int64_t base = ed.aux_base - out_offset;
+  __syncthreads();
+#pragma unroll 2
+  for (int ei = 0; ei < nE; ++ei) {
+    const int64_t base = sedge[ei].out_base;
+    const int64_t wrow = sedge[ei].wrow;
     double c[kExpPer], v[kExpPer], m[kExpPer];
 #pragma unroll
     for (int k = 0; k < kExpPer; ++k) {  // loads first (memory-level parallelism)
-      c[k] = __ldg(cls_sec + ed.wrow + sw[k]);
-      v[k] = __ldg(cls_vol + ed.wrow + sw[k]);
-      m[k] = __ldg(cls_memdiv + ed.wrow + sw[k]);
+      c[k] = __ldg(cls_sec + wrow + sw[k]);
+      v[k] = __ldg(cls_vol + wrow + sw[k]);
+      m[k] = __ldg(cls_memdiv + wrow + sw[k]);
     }
 #pragma unroll
     for (int k = 0; k < kExpPer; ++k) {
@@ -433,8 +454,8 @@ __global__ void __launch_bounds__(kExpThreads) expand_kernel(
       if (records) {  // topoplan::AuxEdge, 40 bytes (aux_graph.hpp:52-59)
         const int32_t su = jj[k] / Sw;
         char* rec = records + o * 40;
-        *reinterpret_cast<int2*>(rec) = make_int2(ed.e, (int)(ed.nb_u + su));
-        *reinterpret_cast<int2*>(rec + 8) = make_int2((int)(ed.nb_w + sw[k]), 0);
+        *reinterpret_cast<int2*>(rec) = make_int2(sedge[ei].e, (int)(sedge[ei].nb_u + su));
+        *reinterpret_cast<int2*>(rec + 8) = make_int2((int)(sedge[ei].nb_w + sw[k]), 0);
         *reinterpret_cast<double*>(rec + 16) = cs;
         *reinterpret_cast<double*>(rec + 24) = vs;
         *reinterpret_cast<double*>(rec + 32) = m[k];
@@ -1092,7 +1113,8 @@ tp_status ensure_stream(tp_plan* p) {
 }
 
 Arena* thread_arena(int device) {
-  static thread_local std::map<int, Arena*> arenas;
+  static thread_local Arena* arenas[64];  // one per device ordinal; POD
+  if (device < 0 || device >= 64) return nullptr;
   Arena*& a = arenas[device];
   if (!a) {
     a = new Arena();
@@ -1102,16 +1124,18 @@ Arena* thread_arena(int device) {
 }
 
 // CTA work items for edges [e0, e1): class tiles x edge chunks.
-void make_work(tp_plan* p, int32_t e0, int32_t e1, std::vector<Work>& out, std::vector<int32_t>& list) {
+void make_work(tp_plan* p, int32_t e0, int32_t e1, std::vector<Work>& out, std::vector<FanEdge>& list) {
   out.clear();
   list.clear();
   std::vector<int32_t> begin(1, 0);
   int64_t total = 0;
+  const int64_t out_offset = p->edge_base[e0];
   for (size_t s = 0; s < p->sigs.size(); ++s) {
     for (int i = p->sig_edge_begin[s]; i < p->sig_edge_begin[s + 1]; ++i) {
       const int e = p->sig_edges[i];
       if (e >= e0 && e < e1) {
-        list.push_back(e);
+        const EdgeDesc& ed = p->edges[e];
+        list.push_back(FanEdge{ed.aux_base - out_offset, ed.wrow, ed.nb_u, ed.nb_w, ed.e, 0});
         total += (int64_t)p->sigs[s].Su * p->sigs[s].Sw;
       }
     }
@@ -1124,7 +1148,7 @@ void make_work(tp_plan* p, int32_t e0, int32_t e1, std::vector<Work>& out, std::
     if (b == en) continue;
     const int64_t P = (int64_t)p->sigs[s].Su * p->sigs[s].Sw;
     const int64_t tile = std::min<int64_t>(P, kExpTile);
-    const int chunk = (int)std::max<int64_t>(1, target / std::max<int64_t>(tile, 1));
+    const int chunk = (int)std::min<int64_t>(kMaxChunk, std::max<int64_t>(1, target / std::max<int64_t>(tile, 1)));
     for (int64_t j0 = 0; j0 < P; j0 += kExpTile) {
       for (int c = b; c < en; c += chunk) {
         Work w{};
@@ -1146,7 +1170,7 @@ void make_work(tp_plan* p, int32_t e0, int32_t e1, std::vector<Work>& out, std::
 extern "C" {
 
 int32_t tp_abi_version(void) { return TP_ABI_VERSION; }
-const char* tp_last_error(void) { return g_err.c_str(); }
+const char* tp_last_error(void) { return g_err; }
 int32_t tp_last_error_kind(void) { return g_err_kind; }
 
 tp_status tp_plan_create(const tp_graph_desc* graph, const tp_topology_desc* topo, int32_t device,
@@ -1166,7 +1190,7 @@ tp_status tp_plan_create(const tp_graph_desc* graph, const tp_topology_desc* top
     return st;
   }
   *plan_out = p;
-  g_err.clear();
+  g_err[0] = 0;
   g_err_kind = 0;
   return TP_OK;
 }
@@ -1323,7 +1347,7 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
                          (out->edge_cost_s || out->edge_volume_bytes || out->edge_memory_bytes ||
                           out->aux_edge_records);
   if (edges_out && (p->last_e0 != e0 || p->last_e1 != e1)) {
-    std::vector<int32_t> list;
+    std::vector<FanEdge> list;
     make_work(p, e0, e1, p->work, list);
     CUDA_TRY(upload(A.d_work, p->work, s));
     CUDA_TRY(upload(A.d_list, list, s));
@@ -1335,9 +1359,9 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   if (n_edge_work + n_node_work > 0) {
     if (p->prof_start) CUDA_TRY(cudaEventRecord(p->prof_start, s));
     expand_kernel<<<(unsigned)(n_edge_work + n_node_work), kExpThreads, 0, s>>>(
-        (const Work*)A.d_work.p, (const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_list.p,
-        (const EdgeDesc*)A.d_edges.p, (const double*)A.d_rsec.p, (const double*)A.d_rvol.p,
-        (const double*)A.d_csec.p, (const double*)A.d_cvol.p, (const double*)A.d_cmem.p, out_offset,
+        (const Work*)A.d_work.p, (const SigDesc*)A.d_sigs.p, (const FanEdge*)A.d_list.p,
+        (const double*)A.d_rsec.p, (const double*)A.d_rvol.p,
+        (const double*)A.d_csec.p, (const double*)A.d_cvol.p, (const double*)A.d_cmem.p,
         out->edge_cost_s, out->edge_volume_bytes, out->edge_memory_bytes, (char*)out->aux_edge_records,
         n_edge_work, (const NodeWork*)A.d_nwork.p, (const ClassDesc*)A.d_classes.p,
         (const int64_t*)A.d_members.p, (const double*)A.d_cmem0.p, nodes_out ? out->node_intra_cost_s : nullptr,
@@ -1469,7 +1493,7 @@ tp_status tp_build_cost_tensors(const tp_graph_desc* graph, const tp_topology_de
   tp_status st = tp_plan_create(graph, topo, opts ? opts->device : -1, &p);
   if (st) return st;
   p->arena = thread_arena(p->device);  // reused across one-shot calls
-  p->owns_arena = false;
+  p->owns_arena = p->arena == nullptr;
   st = tp_plan_execute_host(p, opts, index_out, host_out);
   tp_plan_destroy(p);
   return st;

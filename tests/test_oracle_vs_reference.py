@@ -1,0 +1,107 @@
+"""The C restatement against the reference compiled from /root/reference
+(oracle/_ref): seeded random graphs and redistributions, bit for bit."""
+import random
+
+import numpy as np
+import pytest
+
+from oracle import bindings as B
+from paper_2301_04285_b200 import fuzz, graph as G, models as M
+
+pytestmark = pytest.mark.skipif(not B.have_reference(), reason="oracle/_ref not built")
+
+FIELDS = ("node_base", "edge_base", "in_degree", "out_degree", "topo_order", "edge_from_op", "edge_to_op",
+          "node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes", "edge_cost_s",
+          "edge_volume_bytes", "edge_memory_bytes", "row_min_cost_s", "row_min_volume_bytes")
+
+
+def same(o, r):
+    if o.status != r.status:
+        return f"status {o.status} vs {r.status}"
+    if o.status:
+        return None
+    for k in FIELDS:
+        if getattr(o, k).tobytes() != getattr(r, k).tobytes():
+            return k
+    a, b = o.records.reshape(-1, 40).copy(), r.records.reshape(-1, 40).copy()
+    a[:, 12:16] = 0
+    b[:, 12:16] = 0
+    return None if np.array_equal(a, b) else "records"
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_graphs(seed):
+    rng = random.Random(seed)
+    for i in range(60):
+        g, t = fuzz.random_graph(rng, odd_extents=i % 2 == 0, mixed_element_sizes=i % 3 == 0)
+        f = G.flatten(g)
+        assert same(B.oracle_build(f, t), B.reference_build(f, t)) is None
+
+
+def test_planning_instances():
+    rng = random.Random(29)
+    for _ in range(60):
+        g, t = fuzz.random_planning_instance(rng)
+        f = G.flatten(g)
+        assert same(B.oracle_build(f, t), B.reference_build(f, t)) is None
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_configs(name):
+    g, t = M.CONFIGS[name]()
+    f = G.flatten(g)
+    assert same(B.oracle_build(f, t), B.reference_build(f, t)) is None
+
+
+def test_cfg3_two_nodes():
+    g, t = M.cfg3(2, 10)
+    f = G.flatten(g)
+    o, r = B.oracle_build(f, t, records=False), B.reference_build(f, t, records=False)
+    for k in FIELDS:
+        assert getattr(o, k).tobytes() == getattr(r, k).tobytes(), k
+
+
+def test_unmemoized_equals_edge_weight():
+    rng = random.Random(3)
+    for i in range(20):
+        g, t = fuzz.random_graph(rng, odd_extents=False, mixed_element_sizes=True)
+        f = G.flatten(g)
+        o, r = B.oracle_build(f, t, memoize=False), B.reference_build_unmemoized(f, t)
+        if o.status == 0 and r.status == 0:
+            for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes"):
+                assert getattr(o, k).tobytes() == getattr(r, k).tobytes(), k
+
+
+def test_redistributions():
+    rng = random.Random(41)
+    for i in range(3000):
+        total = 1 << rng.randrange(0, 7)
+        d1 = fuzz.random_matrix_with_total(rng, total)
+        d2 = fuzz.random_matrix_with_total(rng, total)
+        rank = rng.randint(1, 3)
+        shape = [rng.choice([1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64, 5, 10, 7, 128]) for _ in range(rank)]
+
+        def rm(dims):
+            m = [-1] * rank
+            for a in range(rank):
+                if dims and rng.randrange(3):
+                    m[a] = rng.randrange(len(dims))
+            return m
+        qq = B.make_query(shape, d1, rm(d1), d2, rm(d2), local=rng.choice([1, 2, 4, 8]),
+                          inter=rng.choice([6e9, 60e9]))
+        a, b = B.oracle_redistribute(qq), B.reference_redistribute(qq)
+        assert (a.status == 0) == (b.status == 0)
+        if a.status == 0:
+            assert a.plan() == b.plan() and a.seconds == b.seconds and a.volume_bytes == b.volume_bytes
+
+
+def test_ilp_on_oracle_tensors_matches_reference():
+    """The reference's solver (formulate + solve) on oracle-built tensors
+    selects exactly what it selects on its own (cfg1, both modes)."""
+    g, t = M.cfg1()
+    f = G.flatten(g)
+    o = B.oracle_build(f, t)
+    for vol in (False, True):
+        a = B.reference_solve(f, t, mode_volume=vol, threads=4)
+        b = B.reference_solve(f, t, mode_volume=vol, threads=4, given=o)
+        assert a == b
