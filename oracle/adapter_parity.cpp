@@ -65,7 +65,7 @@ std::string compare(const AuxiliaryGraph& r, const AuxiliaryGraph& g) {
 }
 
 void report(const std::string& name, const std::string& err, const std::string& extra = "") {
-  std::printf("[PARITY] %-34s %s%s%s\n", name.c_str(), err.empty() ? "PASS" : "FAIL", err.empty() ? "" : ": ",
+  std::printf("[PARITY] %-34s %s%s%s\n", name.c_str(), err.empty() ? "PASS  " : "FAIL: ", "",
               err.empty() ? extra.c_str() : err.c_str());
   std::fflush(stdout);
   if (!err.empty()) ++failures;
