@@ -319,6 +319,58 @@ TP_HD void regions_of(const Lay& L, int R, Regions& g, uint32_t& D) {
   }
 }
 
+// A layout in the form the pair kernels consume, precomputed once per
+// (edge class, side, strategy): the cumulative device boundaries of its
+// matrix and the device region of every tensor dim. For canonical strategy
+// matrices (no size-1 dims) equality of descriptors is equality of
+// layouts (TensorLayout::operator==, layout.hpp:169-171, minus the spec,
+// which is shared by construction).
+struct alignas(8) SideDesc {
+  uint32_t D;        // bit c set at every cumulative log2 extent c (1..n)
+  uint8_t n;         // log2 of the total device count
+  uint8_t pad[3];
+  uint8_t a[kMaxR];  // lower device position of dim i's region
+  uint8_t x[kMaxR];  // log2 extent of the region, 0 = replicated dim
+};
+
+TP_HD void side_of(const Lay& L, int R, SideDesc& s) {
+  Regions g;
+  uint32_t D = 0;
+  regions_of(L, R, g, D);
+  int n = 0;
+  for (int k = 0; k < L.depth; ++k) n += L.mx[k];
+  s.D = D;
+  s.n = (uint8_t)n;
+  s.pad[0] = s.pad[1] = s.pad[2] = 0;
+  for (int i = 0; i < kMaxR; ++i) {
+    s.a[i] = i < R ? g.a[i] : 0;
+    s.x[i] = i < R ? g.x[i] : 0;
+  }
+}
+
+// Inverse for canonical matrices (used by the array-form fallback).
+TP_HD void lay_of(const SideDesc& s, int R, Lay& L) {
+  L.depth = 0;
+  for (int k = 0; k < kMaxD; ++k) L.mx[k] = 0;
+  int prev = 0;
+  uint32_t rest = s.D;
+  while (rest) {
+    const int c = ffs32(rest);
+    rest &= rest - 1;
+    L.mx[L.depth++] = (uint8_t)(c - prev);
+    prev = c;
+  }
+  for (int i = 0; i < R; ++i)
+    L.map[i] = s.x[i] ? (int8_t)popc32(s.D & low_bits(s.a[i] + 1)) : (int8_t)-1;
+}
+
+TP_HD bool same_side(const SideDesc& f, const SideDesc& t, int R) {
+  if (f.D != t.D || f.n != t.n) return false;
+  for (int i = 0; i < R; ++i)
+    if (f.a[i] != t.a[i] || f.x[i] != t.x[i]) return false;
+  return true;
+}
+
 // Returns kOk or an error; fills u (and the trace's part structure).
 TP_HD int unify_bits(int R, const Lay& F, const Lay& T, const DimT* dt, Unified& u, Trace* tr) {
   Regions gf, gt;

@@ -139,6 +139,7 @@ struct SigDesc {       // an edge class
   int64_t first_aux;   // aux id of (su=0, sw=0) of the class's first edge
   double bytes;
   int32_t R, Su, Sw, tab_u, tab_w, has_override;
+  int32_t side_u, side_w;  // first producer / consumer SideDesc of the class
   int8_t sa_u[tpk::kMaxR];
   int8_t sa_w[tpk::kMaxR];
   DimT dt[tpk::kMaxR];
@@ -175,6 +176,13 @@ struct TableDesc {
   int32_t p, n;
 };
 
+struct SideJob {       // the SideDescs of one (edge class, side)
+  int64_t out;         // first SideDesc
+  int32_t tab, count;  // strategy table offset, strategies
+  int8_t sa[tpk::kMaxR];
+  int32_t R, pad;
+};
+
 constexpr int kBuildThreads = 64;       // thread-per-pair form
 constexpr int kBuildWarpThreads = 128;  // warp-per-pair form
 constexpr int kWarpPairsPerBlock = kBuildWarpThreads / 32;
@@ -206,6 +214,24 @@ __global__ void table_kernel(const TableDesc* __restrict__ tabs, int ntabs, int6
   out[i] = s;
 }
 
+// K0b (at upload): layout descriptors of every (edge class, side, strategy).
+__global__ void side_kernel(const SideJob* __restrict__ jobs, int njobs, int64_t total,
+                            const Strat* __restrict__ tables, tpk::SideDesc* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  int lo = 0, hi = njobs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (jobs[mid].out <= i) lo = mid; else hi = mid - 1;
+  }
+  const SideJob j = jobs[lo];
+  Lay L;
+  tpk::side_layout(tables[j.tab + (i - j.out)], j.sa, j.R, L);
+  tpk::SideDesc d;
+  tpk::side_of(L, j.R, d);
+  out[i] = d;
+}
+
 struct BuildArgs {
   // node classes
   const ClassDesc* classes;
@@ -224,6 +250,7 @@ struct BuildArgs {
   int nsigs;
   int64_t total_pairs;
   const double* overrides;
+  const tpk::SideDesc* sides;
   double* r_sec;
   double* r_vol;
   // shared
@@ -302,15 +329,13 @@ __device__ void pair_row(const BuildArgs& a, int64_t idx) {
   const SigDesc& sg = a.sigs[lo];
   const int32_t local = (int32_t)(idx - sg.pair_begin);
   const int32_t su = local / sg.Sw, sw = local - su * sg.Sw;
-  const Strat su_s = a.tables[sg.tab_u + su];
-  const Strat sw_s = a.tables[sg.tab_w + sw];
-  Lay F, T;
-  tpk::side_layout(su_s, sg.sa_u, sg.R, F);
-  tpk::side_layout(sw_s, sg.sa_w, sg.R, T);
+  const tpk::SideDesc F = a.sides[sg.side_u + su];
+  const tpk::SideDesc T = a.sides[sg.side_w + sw];
   double sec = 0, vol = 0;
-  if (!tpk::same_layout(F, T, sg.R)) {  // aux_graph.hpp:260
+  if (!tpk::same_side(F, T, sg.R)) {  // aux_graph.hpp:260
     const double bytes = sg.has_override ? a.overrides[idx] : sg.bytes;
-    const int st = tpk::pair_cost(sg.R, F, T, sg.dt, bytes, a.env, a.l_log2, sec, vol, nullptr);
+    const int st = tpk::pair_cost_sd(sg.R, F, T, nullptr, nullptr, sg.dt, bytes, a.env, a.l_log2, sec, vol,
+                                     nullptr);
     if (st) {
       flag_error(a.err, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
       sec = vol = 0;
@@ -330,13 +355,10 @@ __device__ void pair_row_warp(const BuildArgs& a, int64_t idx) {
   const SigDesc& sg = a.sigs[lo];
   const int32_t local = (int32_t)(idx - sg.pair_begin);
   const int32_t su = local / sg.Sw, sw = local - su * sg.Sw;
-  const Strat su_s = a.tables[sg.tab_u + su];
-  const Strat sw_s = a.tables[sg.tab_w + sw];
-  Lay F, T;
-  tpk::side_layout(su_s, sg.sa_u, sg.R, F);
-  tpk::side_layout(sw_s, sg.sa_w, sg.R, T);
+  const tpk::SideDesc F = a.sides[sg.side_u + su];
+  const tpk::SideDesc T = a.sides[sg.side_w + sw];
   double sec = 0, vol = 0;
-  if (!tpk::same_layout(F, T, sg.R)) {  // aux_graph.hpp:260
+  if (!tpk::same_side(F, T, sg.R)) {  // aux_graph.hpp:260
     const double bytes = sg.has_override ? a.overrides[idx] : sg.bytes;
     tpk::WarpEnv we;
     we.env = a.env;
@@ -383,7 +405,7 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(BuildArgs a) {
 // kExpPer pairs of the tile — class-table values and consumer strategy — in
 // registers and, for every edge, writes them at out_base(edge) + pair:
 // lane-contiguous, so each warp store instruction writes 256 B.
-__global__ void __launch_bounds__(kExpThreads) expand_kernel(
+__global__ void __launch_bounds__(kExpThreads, 4) expand_kernel(
     const Work* __restrict__ work, const SigDesc* __restrict__ sigs, const FanEdge* __restrict__ fan,
     const double* __restrict__ r_sec, const double* __restrict__ r_vol,
     const double* __restrict__ cls_sec, const double* __restrict__ cls_vol,
@@ -575,13 +597,14 @@ struct Arena {
   int device = 0;
   cudaStream_t stream = nullptr;
   DevBuf d_tabs, d_tables, d_classes, d_chks, d_slots, d_occs, d_members, d_sigs, d_edges, d_list,
-      d_work, d_over, d_rsec, d_rvol, d_csec, d_cvol, d_cmem, d_cmem0, d_nwork, d_rowbase, d_err;
+      d_work, d_over, d_rsec, d_rvol, d_csec, d_cvol, d_cmem, d_cmem0, d_nwork, d_rowbase, d_err, d_sidejobs,
+      d_sides;
   DevBuf out[9];  // one-shot staging of the requested outputs
   std::vector<std::array<int64_t, 4>> table_key;  // (offset, count, p, n) of the resident tables
   void release() {
     for (DevBuf* b : {&d_tabs, &d_tables, &d_classes, &d_chks, &d_slots, &d_occs, &d_members, &d_sigs,
                       &d_edges, &d_list, &d_work, &d_over, &d_rsec, &d_rvol, &d_csec, &d_cvol, &d_cmem,
-                      &d_cmem0, &d_nwork, &d_rowbase, &d_err})
+                      &d_cmem0, &d_nwork, &d_rowbase, &d_err, &d_sidejobs, &d_sides})
       b->release();
     for (auto& b : out) b.release();
     table_key.clear();
@@ -625,6 +648,8 @@ struct tp_plan {
   bool uploaded = false;
   std::vector<Work> work;
   std::vector<NodeWork> nwork;
+  std::vector<SideJob> side_jobs;
+  int64_t side_total = 0;
   int64_t last_launches = 0;
   int32_t last_e0 = -1, last_e1 = -1;
   cudaStream_t last_stream = nullptr;
@@ -869,6 +894,17 @@ struct Builder {
           sd.Sw = (int32_t)Sw;
           sd.tab_u = (int32_t)table_of_p[pu];
           sd.tab_w = (int32_t)table_of_p[pw];
+          for (int side = 0; side < 2; ++side) {
+            SideJob j{};
+            j.out = p.side_total;
+            j.tab = side ? sd.tab_w : sd.tab_u;
+            j.count = (int32_t)(side ? Sw : Su);
+            j.R = R;
+            for (int d = 0; d < tpk::kMaxR; ++d) j.sa[d] = d < R ? (side ? slot_sa[w][kw][d] : slot_sa[u][ku][d]) : -1;
+            (side ? sd.side_w : sd.side_u) = (int32_t)p.side_total;
+            p.side_jobs.push_back(j);
+            p.side_total += j.count;
+          }
           for (int d = 0; d < tpk::kMaxR; ++d) {
             sd.sa_u[d] = d < R ? slot_sa[u][ku][d] : -1;
             sd.sa_w[d] = d < R ? slot_sa[w][kw][d] : -1;
@@ -914,6 +950,7 @@ struct Builder {
                             p.members.size() * sizeof(int64_t) + p.chks.size() * sizeof(SliceChk) +
                             p.slots.size() * sizeof(SlotDesc) + p.occs.size() * sizeof(Occ) +
                             p.sigs.size() * sizeof(SigDesc) + p.edges.size() * sizeof(EdgeDesc) +
+                            p.side_jobs.size() * sizeof(SideJob) +
                             p.overrides.size() * sizeof(double));
     return st;
   }
@@ -1252,6 +1289,15 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
     CUDA_TRY(cudaGetLastError());
     A.table_key = key;
   }
+  // layout descriptors of every (edge class, side, strategy)
+  CUDA_TRY(upload(A.d_sidejobs, p->side_jobs, s));
+  CUDA_TRY(A.d_sides.ensure(sizeof(tpk::SideDesc) * (p->side_total + 1)));
+  if (p->side_total > 0) {
+    side_kernel<<<(unsigned)((p->side_total + 127) / 128), 128, 0, s>>>(
+        (const SideJob*)A.d_sidejobs.p, (int)p->side_jobs.size(), p->side_total, (const Strat*)A.d_tables.p,
+        (tpk::SideDesc*)A.d_sides.p);
+    CUDA_TRY(cudaGetLastError());
+  }
   CUDA_TRY(upload(A.d_classes, p->classes, s));
   CUDA_TRY(upload(A.d_nwork, p->nwork, s));
   CUDA_TRY(upload(A.d_members, p->members, s));
@@ -1319,6 +1365,7 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   a.nsigs = (int)p->sigs.size();
   a.total_pairs = edge_phase ? p->total_pairs : 0;
   a.overrides = (const double*)A.d_over.p;
+  a.sides = (const tpk::SideDesc*)A.d_sides.p;
   a.r_sec = (double*)A.d_rsec.p;
   a.r_vol = (double*)A.d_rvol.p;
   a.tables = (const Strat*)A.d_tables.p;

@@ -123,17 +123,12 @@ TP_HD double price_fast(bool a2a, int te, int rexp, int ek, int s, double bytes,
 
 // Returns the tp_error_kind, or -1 when the pair needs the array form
 // (a device dim held twice by the working map).
-TP_HD int redist_cost_fast(int R, const Lay& F, const Lay& T, const DimT* dt, double bytes, const Env& env,
-                           int l_log2, double& sec_out, double& vol_out, Trace* tr) {
+TP_HD int redist_cost_fast(int R, const SideDesc& gf, const SideDesc& gt, const DimT* dt, double bytes,
+                           const Env& env, int l_log2, double& sec_out, double& vol_out, Trace* tr) {
   if (R < 0 || R > kMaxR) return kCapacity;
   // ---- unify: bitmask closure (see tp_core.cuh) ----
-  Regions gf, gt;
-  uint32_t D = 0;
-  regions_of(F, R, gf, D);
-  regions_of(T, R, gt, D);
-  int n = 0, nt = 0;
-  for (int k = 0; k < F.depth; ++k) n += F.mx[k];
-  for (int k = 0; k < T.depth; ++k) nt += T.mx[k];
+  uint32_t D = gf.D | gt.D;
+  const int n = gf.n, nt = gt.n;
   if (n != nt) return kNotUnifiable;  // redistribution.hpp:264-268
   if (n > kMaxD) return kCapacity;
   for (int i = 0; i < R; ++i)
@@ -146,7 +141,7 @@ TP_HD int redist_cost_fast(int R, const Lay& F, const Lay& T, const DimT* dt, do
   for (bool changed = true; changed;) {
     changed = false;
     for (int sd = 0; sd < 2; ++sd) {
-      const Regions& g = sd ? gt : gf;
+      const SideDesc& g = sd ? gt : gf;
       for (int i = 0; i < R; ++i) {
         const int x = g.x[i], a = g.a[i];
         if (x < 2) continue;
@@ -326,12 +321,23 @@ TP_HD int redist_cost_fast(int R, const Lay& F, const Lay& T, const DimT* dt, do
 }
 
 // The kernels' entry: the register form, or the array form for working maps
-// that hold a device dim twice.
-TP_HD int pair_cost(int R, const Lay& F, const Lay& T, const DimT* dt, double bytes, const Env& env, int l_log2,
-                    double& sec, double& vol, Trace* tr) {
+// that hold a device dim twice (Fl/Tl: the original layouts when known).
+TP_HD int pair_cost_sd(int R, const SideDesc& F, const SideDesc& T, const Lay* Fl, const Lay* Tl, const DimT* dt,
+                       double bytes, const Env& env, int l_log2, double& sec, double& vol, Trace* tr) {
   const int st = redist_cost_fast(R, F, T, dt, bytes, env, l_log2, sec, vol, tr);
   if (st != -1) return st;
-  return redist_cost(R, F, T, dt, bytes, env, sec, vol, tr);
+  Lay a, b;
+  if (Fl) a = *Fl; else lay_of(F, R, a);
+  if (Tl) b = *Tl; else lay_of(T, R, b);
+  return redist_cost(R, a, b, dt, bytes, env, sec, vol, tr);
+}
+
+TP_HD int pair_cost(int R, const Lay& F, const Lay& T, const DimT* dt, double bytes, const Env& env, int l_log2,
+                    double& sec, double& vol, Trace* tr) {
+  SideDesc f, t;
+  side_of(F, R, f);
+  side_of(T, R, t);
+  return pair_cost_sd(R, f, t, &F, &T, dt, bytes, env, l_log2, sec, vol, tr);
 }
 
 // Verification export: one query through pair_cost (the kernels' path).

@@ -95,19 +95,14 @@ __device__ __forceinline__ double price_op_warp(bool a2a, int te, int rexp, int 
 // All 32 lanes call this with identical arguments. Returns the
 // tp_error_kind; sec/vol are valid on every lane. `tr` (verification
 // export only) is written by lane 0.
-__device__ int redist_cost_warp(int R, const Lay& F, const Lay& T, const DimT* dt, double bytes,
+__device__ int redist_cost_warp(int R, const SideDesc& gf, const SideDesc& gt, const DimT* dt, double bytes,
                                 const WarpEnv& we, double& sec_out, double& vol_out, Trace* tr) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   if (R < 0 || R > kMaxR) return kCapacity;
   // ---- unify: the bitmask closure of tp_core.cuh (warp-uniform) ----
-  Regions gf, gt;
-  uint32_t D = 0;
-  regions_of(F, R, gf, D);
-  regions_of(T, R, gt, D);
-  int n = 0, nt = 0;
-  for (int k = 0; k < F.depth; ++k) n += F.mx[k];
-  for (int k = 0; k < T.depth; ++k) nt += T.mx[k];
+  uint32_t D = gf.D | gt.D;
+  const int n = gf.n, nt = gt.n;
   if (n != nt) return kNotUnifiable;  // redistribution.hpp:264-268
   if (n > kMaxD) return kCapacity;
   for (int i = 0; i < R; ++i)
@@ -120,7 +115,7 @@ __device__ int redist_cost_warp(int R, const Lay& F, const Lay& T, const DimT* d
   for (bool changed = true; changed;) {
     changed = false;
     for (int sd = 0; sd < 2; ++sd) {
-      const Regions& g = sd ? gt : gf;
+      const SideDesc& g = sd ? gt : gf;
       for (int i = 0; i < R; ++i) {
         const int x = g.x[i], a = g.a[i];
         if (x < 2) continue;
@@ -337,7 +332,10 @@ __device__ int run_query_warp(const QueryPOD& q, Result& r, Trace& tr) {
   we.env = Env{q.intra, q.inter, (int64_t)q.local};
   we.l_log2 = ilog2_exact((int64_t)q.local);
   double sec = 0, vol = 0;
-  const int st = redist_cost_warp(q.rank, F, T, dt, q.bytes, we, sec, vol, &tr);
+  SideDesc fs, ts;
+  side_of(F, q.rank, fs);
+  side_of(T, q.rank, ts);
+  const int st = redist_cost_warp(q.rank, fs, ts, dt, q.bytes, we, sec, vol, &tr);
   if (st) return st;
   __syncwarp();
   if (lane == 0) {
