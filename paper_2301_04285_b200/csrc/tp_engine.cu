@@ -10,16 +10,20 @@
 //     consumer slicing, axis counts) agree have identical |Su| x |Sw|
 //     redistribution tables; each class is priced once per pair (the
 //     reference's memo, aux_graph.hpp:257-271, made static).
-// Device pipeline of one build (one stream):
-//   build_kernel   one thread per (node class, strategy) and per
-//                  (edge class, su, sw): node costs, then unify + sequence
-//                  inference + topology-aware pricing (tp_core.cuh); the node
-//                  part also fans its row out to every member operator
-//   expand_kernel  the write-bound fan-out: every aux edge
+// Device pipeline of one build: ONE persistent launch (fused_kernel) whose
+// CTAs pull work items from an atomic queue:
+//   node rows      one thread per (node class, strategy): intra-operator
+//                  AllReduce cost/volume and memory (aux_graph.hpp:120-167)
+//   class pairs    one warp (or thread) per (edge class, su, sw): unify +
+//                  sequence inference + topology-aware pricing (tp_warp.cuh /
+//                  tp_fast.cuh)
+//   fan-out tiles  the write-bound part: every aux edge gets
 //                  cost = intra(w) + redist, volume likewise, memory =
-//                  mem(w) / in_degree(w), coalesced fp64 stores
-//   rowmin_kernel  (optional) warp per (edge, su) row, lanes over sw,
-//                  shuffle min: the solver's cond_min (solver.hpp:239-253)
+//                  mem(w) / in_degree(w), lane-contiguous fp64 stores; a tile
+//                  waits only for its own edge class's pairs
+//   node fan-out   class rows to every member operator's aux nodes
+// rowmin_kernel (optional, second launch): warp per (edge, su) row, lanes
+// over sw, shuffle min — the solver's cond_min (solver.hpp:239-253).
 // The strategy tables (layout.hpp:270-328) are built once per plan by
 // table_kernel at upload and cached per device.
 #include <cuda_runtime.h>
@@ -183,25 +187,17 @@ struct SideJob {       // the SideDescs of one (edge class, side)
   int32_t R, pad;
 };
 
-constexpr int kBuildThreads = 64;       // thread-per-pair form
-constexpr int kBuildWarpThreads = 128;  // warp-per-pair form
-constexpr int kWarpPairsPerBlock = kBuildWarpThreads / 32;
 // Below this many class pairs the GPU cannot be filled with one thread per
 // pair (latency-bound), so a warp cooperates on each pair; above it the
 // register-resident thread form has ~6x fewer instructions per pair.
 constexpr int64_t kWarpPairLimit = 16384;
-constexpr int kExpThreads = 256;
 constexpr int kExpPer = 4;
-constexpr int kExpTile = kExpThreads * kExpPer;  // class pairs per CTA tile
-constexpr int kMaxChunk = 64;                    // edges per CTA
+constexpr int kExpTile = 256 * kExpPer;  // class pairs per fan-out tile
+constexpr int kMaxChunk = 64;            // edges per fan-out tile
 
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void flag_error(unsigned long long* err, uint64_t key) {
-  atomicMin(err, (unsigned long long)key);
-}
-
 // K0 (at upload): strategy tables by unranking (layout.hpp:270-328).
 __global__ void table_kernel(const TableDesc* __restrict__ tabs, int ntabs, int64_t total,
                              Strat* __restrict__ out) {
@@ -232,12 +228,31 @@ __global__ void side_kernel(const SideJob* __restrict__ jobs, int njobs, int64_t
   out[i] = d;
 }
 
-struct BuildArgs {
+// Per-execute scheduling state, zeroed by one memset before the launch.
+struct Sched {
+  unsigned long long err_c;  // ~(smallest error key); 0 = no error
+  int head;                  // next block work item (node rows, then fan-out)
+  int pair_head;             // next class pair (warp form) / pair chunk (thread form)
+  int node_done;             // node-class rows finished
+  int pad;
+  int pairs_done[2];         // per edge class (allocated to the class count)
+};
+
+__device__ __forceinline__ void flag_error(Sched* s, uint64_t key) {
+  atomicMax(&s->err_c, ~(unsigned long long)key);  // max of ~key = min of key
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+struct FusedArgs {
   // node classes
   const ClassDesc* classes;
   int ncls;
   int64_t total_rows;
-  int64_t node_blocks;
   const SliceChk* chks;
   const SlotDesc* slots;
   const Occ* occs;
@@ -253,16 +268,38 @@ struct BuildArgs {
   const tpk::SideDesc* sides;
   double* r_sec;
   double* r_vol;
+  // fan-out
+  const Work* work;
+  const FanEdge* fan;
+  double* e_sec;
+  double* e_vol;
+  double* e_mem;
+  char* records;
+  int general_store;  // records requested or not all three SoA tensors given
+  const NodeWork* nwork;
+  const int64_t* member_nb;
+  double* n_sec;
+  double* n_vol;
+  double* n_mem;
+  // work-item ranges: [0, i_pair) node rows, [i_pair, i_exp) pairs,
+  // [i_exp, i_nfan) fan-out tiles, [i_nfan, i_end) node fan-out
+  int i_pair, i_exp, i_nfan, i_end;
+  int warp_form;  // pairs: 1 = warp per pair, 0 = thread per pair
   // shared
   const Strat* tables;
   Env env;
   int l_log2;
   int n_log2;
-  unsigned long long* err;
+  const double* bw_tab;     // inter/ct, tpk::kBwTab entries
+  const double* scale_tab;  // AllToAll scale, kScaleDim^2 entries
+  Sched* sched;
 };
 
+constexpr int kFusedThreads = 256;
+constexpr int kWarpPairsPerItem = kFusedThreads / 32;
+
 // One aux-node row of a node class (aux_graph.hpp:120-167).
-__device__ void node_row(const BuildArgs& a, int64_t row) {
+__device__ void node_row(const FusedArgs& a, int64_t row) {
   int lo = 0, hi = a.ncls - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -278,7 +315,7 @@ __device__ void node_row(const BuildArgs& a, int64_t row) {
     if (k.slot < 0) kind = tpk::kUnknownSliceTensor;
     else if (st.deg[k.axis] > k.v) kind = tpk::kIndivisible;
     if (kind) {
-      flag_error(a.err, ekey(1 + (uint64_t)(cd.first_node + s) * 2 + 1, kind));
+      flag_error(a.sched, ekey(1 + (uint64_t)(cd.first_node + s) * 2 + 1, kind));
       a.cls_sec[row] = a.cls_vol[row] = a.cls_mem[row] = a.cls_memdiv[row] = 0;
       return;
     }
@@ -319,14 +356,18 @@ __device__ void node_row(const BuildArgs& a, int64_t row) {
   a.cls_memdiv[row] = mem / cd.indeg;  // aux_graph.hpp:292
 }
 
-// One (edge class, su, sw) pair: redistribution seconds and volume.
-__device__ void pair_row(const BuildArgs& a, int64_t idx) {
+__device__ __forceinline__ int sig_of_pair(const FusedArgs& a, int64_t idx) {
   int lo = 0, hi = a.nsigs - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (a.sigs[mid].pair_begin <= idx) lo = mid; else hi = mid - 1;
   }
-  const SigDesc& sg = a.sigs[lo];
+  return lo;
+}
+
+// One (edge class, su, sw) pair on one thread (register form, tp_fast.cuh).
+__device__ void pair_thread(const FusedArgs& a, int64_t idx, int sig) {
+  const SigDesc& sg = a.sigs[sig];
   const int32_t local = (int32_t)(idx - sg.pair_begin);
   const int32_t su = local / sg.Sw, sw = local - su * sg.Sw;
   const tpk::SideDesc F = a.sides[sg.side_u + su];
@@ -334,10 +375,10 @@ __device__ void pair_row(const BuildArgs& a, int64_t idx) {
   double sec = 0, vol = 0;
   if (!tpk::same_side(F, T, sg.R)) {  // aux_graph.hpp:260
     const double bytes = sg.has_override ? a.overrides[idx] : sg.bytes;
-    const int st = tpk::pair_cost_sd(sg.R, F, T, nullptr, nullptr, sg.dt, bytes, a.env, a.l_log2, sec, vol,
-                                     nullptr);
+    const int st = tpk::pair_cost_sd(sg.R, F, T, nullptr, nullptr, sg.dt, bytes, a.env, a.l_log2,
+                                     tpk::FastTabs{a.bw_tab, a.scale_tab}, sec, vol, nullptr);
     if (st) {
-      flag_error(a.err, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
+      flag_error(a.sched, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
       sec = vol = 0;
     }
   }
@@ -345,28 +386,23 @@ __device__ void pair_row(const BuildArgs& a, int64_t idx) {
   a.r_vol[idx] = vol;
 }
 
-// One (edge class, su, sw) pair on one warp (tp_warp.cuh).
-__device__ void pair_row_warp(const BuildArgs& a, int64_t idx) {
-  int lo = 0, hi = a.nsigs - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a.sigs[mid].pair_begin <= idx) lo = mid; else hi = mid - 1;
-  }
-  const SigDesc& sg = a.sigs[lo];
+// One pair on one warp (warp form, tp_warp.cuh); lane 0 writes.
+__device__ void pair_warp(const FusedArgs& a, int64_t idx, int sig) {
+  const SigDesc& sg = a.sigs[sig];
   const int32_t local = (int32_t)(idx - sg.pair_begin);
   const int32_t su = local / sg.Sw, sw = local - su * sg.Sw;
-  const tpk::SideDesc F = a.sides[sg.side_u + su];
-  const tpk::SideDesc T = a.sides[sg.side_w + sw];
+  const tpk::SideDesc* F = a.sides + sg.side_u + su;
+  const tpk::SideDesc* T = a.sides + sg.side_w + sw;
   double sec = 0, vol = 0;
-  if (!tpk::same_side(F, T, sg.R)) {  // aux_graph.hpp:260
+  if (!tpk::same_side(*F, *T, sg.R)) {  // aux_graph.hpp:260
     const double bytes = sg.has_override ? a.overrides[idx] : sg.bytes;
     tpk::WarpEnv we;
     we.env = a.env;
     we.l_log2 = a.l_log2;
+    we.tab = tpk::PriceTabs{a.bw_tab, a.scale_tab};
     const int st = tpk::redist_cost_warp(sg.R, F, T, sg.dt, bytes, we, sec, vol, nullptr);
     if (st) {
-      if ((threadIdx.x & 31) == 0)
-        flag_error(a.err, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
+      if ((threadIdx.x & 31) == 0) flag_error(a.sched, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
       sec = vol = 0;
     }
   }
@@ -376,113 +412,175 @@ __device__ void pair_row_warp(const BuildArgs& a, int64_t idx) {
   }
 }
 
-// K1 (warp form): node-class rows (a thread each), then pairs (a warp each).
-__global__ void __launch_bounds__(kBuildWarpThreads) build_kernel_warp(BuildArgs a) {
-  if ((int64_t)blockIdx.x < a.node_blocks) {
-    const int64_t row = (int64_t)blockIdx.x * kBuildWarpThreads + threadIdx.x;
-    if (row < a.total_rows) node_row(a, row);
-  } else {
-    const int64_t idx = ((int64_t)blockIdx.x - a.node_blocks) * kWarpPairsPerBlock + (threadIdx.x >> 5);
-    if (idx < a.total_pairs) pair_row_warp(a, idx);  // warp-uniform
-  }
-}
-
-// K1 (thread form): node-class rows in blocks [0, node_blocks), then
-// edge-class pairs; one thread each.
-__global__ void __launch_bounds__(kBuildThreads) build_kernel(BuildArgs a) {
-  if ((int64_t)blockIdx.x < a.node_blocks) {
-    const int64_t row = (int64_t)blockIdx.x * kBuildThreads + threadIdx.x;
-    if (row < a.total_rows) node_row(a, row);
-  } else {
-    const int64_t idx = ((int64_t)blockIdx.x - a.node_blocks) * kBuildThreads + threadIdx.x;
-    if (idx < a.total_pairs) pair_row(a, idx);
-  }
-}
-
-// K2: fan-out of the class tables to every aux edge of the range. A CTA
-// owns a tile of one edge class's pair block and a chunk of the class's
-// edges (their descriptors staged in shared memory once). A thread keeps
-// kExpPer pairs of the tile — class-table values and consumer strategy — in
-// registers and, for every edge, writes them at out_base(edge) + pair:
-// lane-contiguous, so each warp store instruction writes 256 B.
-__global__ void __launch_bounds__(kExpThreads, 4) expand_kernel(
-    const Work* __restrict__ work, const SigDesc* __restrict__ sigs, const FanEdge* __restrict__ fan,
-    const double* __restrict__ r_sec, const double* __restrict__ r_vol,
-    const double* __restrict__ cls_sec, const double* __restrict__ cls_vol,
-    const double* __restrict__ cls_memdiv, double* __restrict__ e_sec, double* __restrict__ e_vol,
-    double* __restrict__ e_mem, char* __restrict__ records, int num_edge_work,
-    const NodeWork* __restrict__ nwork, const ClassDesc* __restrict__ classes,
-    const int64_t* __restrict__ member_nb, const double* __restrict__ cls_mem, double* __restrict__ n_sec,
-    double* __restrict__ n_vol, double* __restrict__ n_mem) {
-  if ((int)blockIdx.x >= num_edge_work) {
-    // node tensors: every member operator of a node class gets the class rows
-    const NodeWork nw = nwork[blockIdx.x - num_edge_work];
-    const ClassDesc cd = classes[nw.cls];
-    const int64_t total = (int64_t)(nw.mend - nw.mbeg) * cd.S;
-    for (int64_t t = threadIdx.x; t < total; t += kExpThreads) {
-      const int64_t m = t / cd.S, sidx = t - m * cd.S;
-      const int64_t node = member_nb[nw.mbeg + m] + sidx;
-      const int64_t row = cd.row_base + sidx;
-      if (n_sec) __stcs(n_sec + node, cls_sec[row]);
-      if (n_vol) __stcs(n_vol + node, cls_vol[row]);
-      if (n_mem) __stcs(n_mem + node, cls_mem[row]);
-    }
-    return;
-  }
-  __shared__ FanEdge sedge[kMaxChunk];
-  const Work wk = work[blockIdx.x];
+// Fan-out tile: every edge of a chunk of one edge class gets the class
+// tile's values at out_base(edge) + pair, lane-contiguous (256-B warp
+// stores); class rows are reloaded only when the consumer class changes
+// (edges are sorted by it).
+__device__ void fanout_tile(const FusedArgs& a, const Work& wk, FanEdge* sedge) {
   const int nE = wk.eend - wk.ebeg;
-  for (int t = threadIdx.x; t < nE; t += kExpThreads) sedge[t] = fan[wk.ebeg + t];
-  const SigDesc& sg = sigs[wk.sig];
+  for (int t = threadIdx.x; t < nE; t += kFusedThreads) sedge[t] = a.fan[wk.ebeg + t];
+  const SigDesc& sg = a.sigs[wk.sig];
   const int32_t Sw = sg.Sw;
   const int32_t P = sg.Su * Sw;
   const int64_t pb = sg.pair_begin;
-  const int32_t step = kExpThreads % Sw;
+  if (threadIdx.x == 0) {  // wait for the class table and the node rows
+    while (ld_acquire(&a.sched->pairs_done[wk.sig]) < P) __nanosleep(64);
+    while (ld_acquire(&a.sched->node_done) < a.total_rows) __nanosleep(64);
+  }
+  __syncthreads();
+  const int32_t step = kFusedThreads % Sw;
   int32_t jj[kExpPer], sw[kExpPer];
   double rs[kExpPer], rv[kExpPer];
   int32_t cur = (wk.j0 + (int32_t)threadIdx.x) % Sw;
 #pragma unroll
   for (int k = 0; k < kExpPer; ++k) {
-    const int32_t j = wk.j0 + (int32_t)threadIdx.x + k * kExpThreads;
+    const int32_t j = wk.j0 + (int32_t)threadIdx.x + k * kFusedThreads;
     jj[k] = j < P ? j : -1;
     sw[k] = cur;
     cur += step;
     if (cur >= Sw) cur -= Sw;
     const int64_t jc = j < P ? j : 0;
-    rs[k] = __ldg(r_sec + pb + jc);
-    rv[k] = __ldg(r_vol + pb + jc);
+    rs[k] = __ldcg(a.r_sec + pb + jc);  // L2: written by other SMs in this launch
+    rv[k] = __ldcg(a.r_vol + pb + jc);
   }
-  __syncthreads();
-#pragma unroll 2
+  double c[kExpPer], v[kExpPer], m[kExpPer];
+  int64_t cur_row = -1;
   for (int ei = 0; ei < nE; ++ei) {
     const int64_t base = sedge[ei].out_base;
     const int64_t wrow = sedge[ei].wrow;
-    double c[kExpPer], v[kExpPer], m[kExpPer];
+    if (wrow != cur_row) {  // block-uniform
+      cur_row = wrow;
 #pragma unroll
-    for (int k = 0; k < kExpPer; ++k) {  // loads first (memory-level parallelism)
-      c[k] = __ldg(cls_sec + wrow + sw[k]);
-      v[k] = __ldg(cls_vol + wrow + sw[k]);
-      m[k] = __ldg(cls_memdiv + wrow + sw[k]);
+      for (int k = 0; k < kExpPer; ++k) {
+        c[k] = __ldcg(a.cls_sec + wrow + sw[k]) + rs[k];  // aux_graph.hpp:290-291
+        v[k] = __ldcg(a.cls_vol + wrow + sw[k]) + rv[k];
+        m[k] = __ldcg(a.cls_memdiv + wrow + sw[k]);       // :292
+      }
     }
+    if (!a.general_store) {
 #pragma unroll
-    for (int k = 0; k < kExpPer; ++k) {
-      if (jj[k] < 0) continue;
-      const int64_t o = base + jj[k];
-      const double cs = c[k] + rs[k];  // aux_graph.hpp:290-291
-      const double vs = v[k] + rv[k];
-      if (e_sec) __stcs(e_sec + o, cs);  // streaming: written once, read by the host
-      if (e_vol) __stcs(e_vol + o, vs);
-      if (e_mem) __stcs(e_mem + o, m[k]);
-      if (records) {  // topoplan::AuxEdge, 40 bytes (aux_graph.hpp:52-59)
+      for (int k = 0; k < kExpPer; ++k) {
+        if (jj[k] < 0) continue;
+        const int64_t o = base + jj[k];
+        __stcs(a.e_sec + o, c[k]);  // streaming: written once, read by the host
+        __stcs(a.e_vol + o, v[k]);
+        __stcs(a.e_mem + o, m[k]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kExpPer; ++k) {
+        if (jj[k] < 0) continue;
+        const int64_t o = base + jj[k];
+        if (a.e_sec) __stcs(a.e_sec + o, c[k]);
+        if (a.e_vol) __stcs(a.e_vol + o, v[k]);
+        if (a.e_mem) __stcs(a.e_mem + o, m[k]);
+        if (!a.records) continue;
+        // topoplan::AuxEdge, 40 bytes (aux_graph.hpp:52-59)
         const int32_t su = jj[k] / Sw;
-        char* rec = records + o * 40;
+        char* rec = a.records + o * 40;
         *reinterpret_cast<int2*>(rec) = make_int2(sedge[ei].e, (int)(sedge[ei].nb_u + su));
         *reinterpret_cast<int2*>(rec + 8) = make_int2((int)(sedge[ei].nb_w + sw[k]), 0);
-        *reinterpret_cast<double*>(rec + 16) = cs;
-        *reinterpret_cast<double*>(rec + 24) = vs;
+        *reinterpret_cast<double*>(rec + 16) = c[k];
+        *reinterpret_cast<double*>(rec + 24) = v[k];
         *reinterpret_cast<double*>(rec + 32) = m[k];
       }
     }
+  }
+}
+
+// Node tensors: every member operator of a node class gets the class rows.
+__device__ void node_fanout(const FusedArgs& a, const NodeWork& nw) {
+  if (threadIdx.x == 0)
+    while (ld_acquire(&a.sched->node_done) < a.total_rows) __nanosleep(64);
+  __syncthreads();
+  const ClassDesc cd = a.classes[nw.cls];
+  const int64_t total = (int64_t)(nw.mend - nw.mbeg) * cd.S;
+  for (int64_t t = threadIdx.x; t < total; t += kFusedThreads) {
+    const int64_t mm = t / cd.S, sidx = t - mm * cd.S;
+    const int64_t node = a.member_nb[nw.mbeg + mm] + sidx;
+    const int64_t row = cd.row_base + sidx;
+    if (a.n_sec) __stcs(a.n_sec + node, __ldcg(a.cls_sec + row));
+    if (a.n_vol) __stcs(a.n_vol + node, __ldcg(a.cls_vol + row));
+    if (a.n_mem) __stcs(a.n_mem + node, __ldcg(a.cls_mem + row));
+  }
+}
+
+// The whole build in one persistent launch. Phase 1: block work items for
+// the node-class rows (few). Phase 2: every warp pulls class pairs from an
+// atomic counter on its own — no block barrier, so a slow pair never idles
+// the other warps of its CTA. Phase 3: block work items for the fan-out tiles
+// and the node fan-out; a tile waits (acquire) only for its own edge class's
+// pair counter. Every pair is dequeued before any fan-out item and each
+// dequeued item runs to completion, so the waits always end. The
+// latency-bound pair work and the HBM-bound fan-out overlap, with no launch
+// gap or wave tail between them.
+template <bool kWarpForm>
+__global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
+  __shared__ int s_item;
+  __shared__ FanEdge sedge[kMaxChunk];
+  const int lane = threadIdx.x & 31;
+  // phase 1: node-class rows; the first item past them is kept for phase 3
+  int carried;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(&a.sched->head, 1);
+    __syncthreads();
+    const int item = s_item;
+    __syncthreads();
+    if (item >= a.i_pair) {
+      carried = item;
+      break;
+    }
+    const int64_t row = (int64_t)item * kFusedThreads + threadIdx.x;
+    if (row < a.total_rows) node_row(a, row);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int64_t rem = a.total_rows - (int64_t)item * kFusedThreads;
+      atomicAdd(&a.sched->node_done, (int)(rem < kFusedThreads ? rem : kFusedThreads));
+    }
+  }
+  // phase 2: class pairs, dequeued per warp
+  if (kWarpForm) {
+    for (;;) {
+      int64_t idx = 0;
+      if (lane == 0) idx = atomicAdd(&a.sched->pair_head, 1);
+      idx = __shfl_sync(0xffffffffu, (long long)idx, 0);
+      if (idx >= a.total_pairs) break;
+      const int sig = sig_of_pair(a, idx);
+      pair_warp(a, idx, sig);
+      if (lane == 0) {
+        __threadfence();
+        atomicAdd(&a.sched->pairs_done[sig], 1);
+      }
+    }
+  } else {
+    for (;;) {
+      int64_t chunk = 0;
+      if (lane == 0) chunk = atomicAdd(&a.sched->pair_head, 1);
+      chunk = __shfl_sync(0xffffffffu, (long long)chunk, 0);
+      const int64_t idx = chunk * 32 + lane;
+      if (chunk * 32 >= a.total_pairs) break;
+      const bool valid = idx < a.total_pairs;
+      const int sig = valid ? sig_of_pair(a, idx) : -1;
+      if (valid) pair_thread(a, idx, sig);
+      __threadfence();
+      // one counter update per (warp, edge class)
+      const unsigned grp = __match_any_sync(0xffffffffu, sig);
+      if (valid && lane == __ffs(grp) - 1) atomicAdd(&a.sched->pairs_done[sig], __popc(grp));
+    }
+  }
+  // phase 3: fan-out tiles and node fan-out (every pair is dequeued by now)
+  for (bool first = true;; first = false) {
+    int item = carried;
+    if (!first) {
+      if (threadIdx.x == 0) s_item = atomicAdd(&a.sched->head, 1);
+      __syncthreads();
+      item = s_item;
+      __syncthreads();
+    }
+    if (item >= a.i_end) return;
+    if (item < a.i_nfan) fanout_tile(a, a.work[item - a.i_exp], sedge);
+    else node_fanout(a, a.nwork[item - a.i_nfan]);
   }
 }
 
@@ -526,20 +624,23 @@ __global__ void rowmin_kernel(const EdgeDesc* __restrict__ edges, const int64_t*
 }
 
 // Verification export through the kernels' pair paths: thread form...
-__global__ void query_kernel(const tpk::QueryPOD* __restrict__ q, int n, tp_redist_result* __restrict__ r) {
+__global__ void query_kernel(const tpk::QueryPOD* __restrict__ q, int n, tp_redist_result* __restrict__ r,
+                             const double* __restrict__ tabs) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const double* t = tabs + (int64_t)i * (tpk::kBwTab + tpk::kScaleDim * tpk::kScaleDim);
   tp_redist_result res;
-  res.status = tpk::run_query_fast(q[i], res);
+  res.status = tpk::run_query_fast(q[i], res, tpk::FastTabs{t, t + tpk::kBwTab});
   r[i] = res;
 }
 
 // ... and warp form (one warp per query).
 __global__ void query_kernel_warp(const tpk::QueryPOD* __restrict__ q, int n, tp_redist_result* __restrict__ r,
-                                  tpk::Trace* __restrict__ traces) {
+                                  tpk::Trace* __restrict__ traces, const double* __restrict__ tabs) {
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= n) return;
-  const int st = tpk::run_query_warp(q[i], r[i], traces[i]);
+  const double* t = tabs + (int64_t)i * (tpk::kBwTab + tpk::kScaleDim * tpk::kScaleDim);
+  const int st = tpk::run_query_warp(q[i], r[i], traces[i], tpk::PriceTabs{t, t + tpk::kBwTab});
   if ((threadIdx.x & 31) == 0) r[i].status = st;
 }
 
@@ -597,14 +698,14 @@ struct Arena {
   int device = 0;
   cudaStream_t stream = nullptr;
   DevBuf d_tabs, d_tables, d_classes, d_chks, d_slots, d_occs, d_members, d_sigs, d_edges, d_list,
-      d_work, d_over, d_rsec, d_rvol, d_csec, d_cvol, d_cmem, d_cmem0, d_nwork, d_rowbase, d_err, d_sidejobs,
-      d_sides;
+      d_work, d_over, d_rsec, d_rvol, d_csec, d_cvol, d_cmem, d_cmem0, d_nwork, d_rowbase, d_sched, d_sidejobs,
+      d_sides, d_price;
   DevBuf out[9];  // one-shot staging of the requested outputs
   std::vector<std::array<int64_t, 4>> table_key;  // (offset, count, p, n) of the resident tables
   void release() {
     for (DevBuf* b : {&d_tabs, &d_tables, &d_classes, &d_chks, &d_slots, &d_occs, &d_members, &d_sigs,
                       &d_edges, &d_list, &d_work, &d_over, &d_rsec, &d_rvol, &d_csec, &d_cvol, &d_cmem,
-                      &d_cmem0, &d_nwork, &d_rowbase, &d_err, &d_sidejobs, &d_sides})
+                      &d_cmem0, &d_nwork, &d_rowbase, &d_sched, &d_sidejobs, &d_sides, &d_price})
       b->release();
     for (auto& b : out) b.release();
     table_key.clear();
@@ -655,6 +756,7 @@ struct tp_plan {
   cudaStream_t last_stream = nullptr;
   cudaEvent_t prof_start = nullptr, prof_stop = nullptr;  // recorded around K2
   int pair_form = 0;  // 0 = by size, 1 = warp per pair, 2 = thread per pair
+  int resident_blocks = 0;  // persistent grid size (SMs x resident CTAs)
 };
 
 namespace {
@@ -1298,6 +1400,11 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
         (tpk::SideDesc*)A.d_sides.p);
     CUDA_TRY(cudaGetLastError());
   }
+  {
+    std::vector<double> tabs(tpk::kBwTab + tpk::kScaleDim * tpk::kScaleDim);
+    tpk::make_price_tabs(p->env, tabs.data(), tabs.data() + tpk::kBwTab);
+    CUDA_TRY(upload(A.d_price, tabs, s));
+  }
   CUDA_TRY(upload(A.d_classes, p->classes, s));
   CUDA_TRY(upload(A.d_nwork, p->nwork, s));
   CUDA_TRY(upload(A.d_members, p->members, s));
@@ -1313,7 +1420,7 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
   CUDA_TRY(A.d_cvol.ensure(sizeof(double) * (p->total_rows + 1)));
   CUDA_TRY(A.d_cmem.ensure(sizeof(double) * (p->total_rows + 1)));
   CUDA_TRY(A.d_cmem0.ensure(sizeof(double) * (p->total_rows + 1)));
-  CUDA_TRY(A.d_err.ensure(sizeof(unsigned long long)));
+  CUDA_TRY(A.d_sched.ensure(sizeof(Sched) + sizeof(int) * (p->sigs.size() + 2)));
   p->uploaded = true;
   p->last_e0 = p->last_e1 = -1;
   return TP_OK;
@@ -1339,56 +1446,16 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   tp_cost_tensors none{};
   if (!out) out = &none;
   int64_t launches = 0;
-  unsigned long long* err = (unsigned long long*)A.d_err.p;
-  CUDA_TRY(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), s));
+  Sched* sched = (Sched*)A.d_sched.p;
+  const size_t sched_bytes = sizeof(Sched) + sizeof(int) * (p->sigs.size() + 2);
+  CUDA_TRY(cudaMemsetAsync(sched, 0, sched_bytes, s));
   if (p->host_err != ~0ull && (p->host_err >> 6) == 0) {  // cycle: nothing to build
     p->last_launches = 0;
     return TP_OK;
   }
   const bool edge_phase = p->host_err >= ekey(kEdgePhase, 0);
-  // K1: node classes + edge-class pairs in one launch
-  BuildArgs a{};
-  a.classes = (const ClassDesc*)A.d_classes.p;
-  a.ncls = (int)p->classes.size();
-  a.total_rows = p->total_rows;
-  a.node_blocks = (p->total_rows + kBuildThreads - 1) / kBuildThreads;
-  a.chks = (const SliceChk*)A.d_chks.p;
-  a.slots = (const SlotDesc*)A.d_slots.p;
-  a.occs = (const Occ*)A.d_occs.p;
-  a.cls_sec = (double*)A.d_csec.p;
-  a.cls_vol = (double*)A.d_cvol.p;
-  a.cls_mem = (double*)A.d_cmem0.p;
-  a.cls_memdiv = (double*)A.d_cmem.p;
   const bool nodes_out = !skip_nodes && (out->node_intra_cost_s || out->node_intra_volume_bytes ||
                                          out->node_memory_bytes);
-  a.sigs = (const SigDesc*)A.d_sigs.p;
-  a.nsigs = (int)p->sigs.size();
-  a.total_pairs = edge_phase ? p->total_pairs : 0;
-  a.overrides = (const double*)A.d_over.p;
-  a.sides = (const tpk::SideDesc*)A.d_sides.p;
-  a.r_sec = (double*)A.d_rsec.p;
-  a.r_vol = (double*)A.d_rvol.p;
-  a.tables = (const Strat*)A.d_tables.p;
-  a.env = p->env;
-  a.l_log2 = (p->env.local > 0 && (p->env.local & (p->env.local - 1)) == 0) ? log2_floor(p->env.local) : -1;
-  a.n_log2 = p->n_log2;
-  a.err = err;
-  const bool warp_form = p->pair_form == 1 || (p->pair_form == 0 && a.total_pairs <= kWarpPairLimit);
-  if (warp_form) {
-    a.node_blocks = (p->total_rows + kBuildWarpThreads - 1) / kBuildWarpThreads;
-    const int64_t blocks = a.node_blocks + (a.total_pairs + kWarpPairsPerBlock - 1) / kWarpPairsPerBlock;
-    if (blocks > 0) {
-      build_kernel_warp<<<(unsigned)blocks, kBuildWarpThreads, 0, s>>>(a);
-      ++launches;
-    }
-  } else {
-    const int64_t blocks = a.node_blocks + (a.total_pairs + kBuildThreads - 1) / kBuildThreads;
-    if (blocks > 0) {
-      build_kernel<<<(unsigned)blocks, kBuildThreads, 0, s>>>(a);
-      ++launches;
-    }
-  }
-  // K2: fan-out to the aux edges of [e0, e1) (+ the node tensors)
   const int64_t out_offset = p->edge_base[e0];
   const bool edges_out = p->edge_base[e1] > out_offset && edge_phase &&
                          (out->edge_cost_s || out->edge_volume_bytes || out->edge_memory_bytes ||
@@ -1401,18 +1468,69 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
     p->last_e0 = e0;
     p->last_e1 = e1;
   }
-  const int n_edge_work = edges_out ? (int)p->work.size() : 0;
-  const int n_node_work = nodes_out ? (int)p->nwork.size() : 0;
-  if (n_edge_work + n_node_work > 0) {
+  FusedArgs a{};
+  a.classes = (const ClassDesc*)A.d_classes.p;
+  a.ncls = (int)p->classes.size();
+  a.total_rows = p->total_rows;
+  a.chks = (const SliceChk*)A.d_chks.p;
+  a.slots = (const SlotDesc*)A.d_slots.p;
+  a.occs = (const Occ*)A.d_occs.p;
+  a.cls_sec = (double*)A.d_csec.p;
+  a.cls_vol = (double*)A.d_cvol.p;
+  a.cls_mem = (double*)A.d_cmem0.p;
+  a.cls_memdiv = (double*)A.d_cmem.p;
+  a.sigs = (const SigDesc*)A.d_sigs.p;
+  a.nsigs = (int)p->sigs.size();
+  a.total_pairs = edge_phase ? p->total_pairs : 0;
+  a.overrides = (const double*)A.d_over.p;
+  a.sides = (const tpk::SideDesc*)A.d_sides.p;
+  a.r_sec = (double*)A.d_rsec.p;
+  a.r_vol = (double*)A.d_rvol.p;
+  a.work = (const Work*)A.d_work.p;
+  a.fan = (const FanEdge*)A.d_list.p;
+  a.e_sec = out->edge_cost_s;
+  a.e_vol = out->edge_volume_bytes;
+  a.e_mem = out->edge_memory_bytes;
+  a.records = (char*)out->aux_edge_records;
+  a.general_store = a.records || !(a.e_sec && a.e_vol && a.e_mem);
+  a.nwork = (const NodeWork*)A.d_nwork.p;
+  a.member_nb = (const int64_t*)A.d_members.p;
+  a.n_sec = nodes_out ? out->node_intra_cost_s : nullptr;
+  a.n_vol = nodes_out ? out->node_intra_volume_bytes : nullptr;
+  a.n_mem = nodes_out ? out->node_memory_bytes : nullptr;
+  a.tables = (const Strat*)A.d_tables.p;
+  a.env = p->env;
+  a.l_log2 = (p->env.local > 0 && (p->env.local & (p->env.local - 1)) == 0) ? log2_floor(p->env.local) : -1;
+  a.n_log2 = p->n_log2;
+  a.bw_tab = (const double*)A.d_price.p;
+  a.scale_tab = (const double*)A.d_price.p + tpk::kBwTab;
+  a.sched = sched;
+  a.warp_form = p->pair_form == 1 || (p->pair_form == 0 && a.total_pairs <= kWarpPairLimit);
+  // block queue: [0, i_pair) node-row items, then [i_exp, i_nfan) fan-out
+  // tiles, [i_nfan, i_end) node fan-out; the pairs have their own warp queue
+  const int64_t node_items = (p->total_rows + kFusedThreads - 1) / kFusedThreads;
+  const int64_t exp_items = edges_out ? (int64_t)p->work.size() : 0;
+  const int64_t nfan_items = nodes_out ? (int64_t)p->nwork.size() : 0;
+  const int64_t total_items = node_items + exp_items + nfan_items;
+  if (total_items >= (1ll << 31) || a.total_pairs >= (1ll << 36))
+    return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many work items");
+  a.i_pair = (int)node_items;
+  a.i_exp = (int)node_items;
+  a.i_nfan = (int)(node_items + exp_items);
+  a.i_end = (int)total_items;
+  if (total_items > 0 || a.total_pairs > 0) {
+    if (p->resident_blocks == 0) {
+      int sms = 0, per_sm = 0;
+      CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<true>, kFusedThreads, 0));
+      p->resident_blocks = std::max(1, sms * std::max(1, per_sm));
+    }
+    const int64_t warps_needed = a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32;
+    const int64_t blocks_needed = std::max<int64_t>(total_items, (warps_needed + 7) / 8);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(blocks_needed, p->resident_blocks));
     if (p->prof_start) CUDA_TRY(cudaEventRecord(p->prof_start, s));
-    expand_kernel<<<(unsigned)(n_edge_work + n_node_work), kExpThreads, 0, s>>>(
-        (const Work*)A.d_work.p, (const SigDesc*)A.d_sigs.p, (const FanEdge*)A.d_list.p,
-        (const double*)A.d_rsec.p, (const double*)A.d_rvol.p,
-        (const double*)A.d_csec.p, (const double*)A.d_cvol.p, (const double*)A.d_cmem.p,
-        out->edge_cost_s, out->edge_volume_bytes, out->edge_memory_bytes, (char*)out->aux_edge_records,
-        n_edge_work, (const NodeWork*)A.d_nwork.p, (const ClassDesc*)A.d_classes.p,
-        (const int64_t*)A.d_members.p, (const double*)A.d_cmem0.p, nodes_out ? out->node_intra_cost_s : nullptr,
-        nodes_out ? out->node_intra_volume_bytes : nullptr, nodes_out ? out->node_memory_bytes : nullptr);
+    if (a.warp_form) fused_kernel<true><<<(unsigned)grid, kFusedThreads, 0, s>>>(a);
+    else fused_kernel<false><<<(unsigned)grid, kFusedThreads, 0, s>>>(a);
     ++launches;
     if (p->prof_stop) CUDA_TRY(cudaEventRecord(p->prof_stop, s));
   }
@@ -1456,9 +1574,11 @@ tp_status tp_plan_check_errors(tp_plan* p) {
   if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
   CUDA_TRY(cudaSetDevice(p->device));
   unsigned long long dev = ~0ull;
-  if (p->arena && p->arena->d_err.p && p->last_stream) {
-    CUDA_TRY(cudaMemcpyAsync(&dev, p->arena->d_err.p, sizeof(dev), cudaMemcpyDeviceToHost, p->last_stream));
+  if (p->arena && p->arena->d_sched.p && p->last_stream) {
+    unsigned long long c = 0;
+    CUDA_TRY(cudaMemcpyAsync(&c, p->arena->d_sched.p, sizeof(c), cudaMemcpyDeviceToHost, p->last_stream));
     CUDA_TRY(cudaStreamSynchronize(p->last_stream));
+    dev = ~c;  // Sched::err_c holds the complement of the smallest key
   }
   const uint64_t key = std::min<uint64_t>(dev, p->host_err);
   if (key == ~0ull) return TP_OK;
@@ -1617,22 +1737,32 @@ tp_status tp_redistribute_batch_form(const tp_redist_query* q, int32_t n, tp_red
     for (int k = 0; k < x.fdepth; ++k) x.fdims[k] = q[i].from_dims[k];
     for (int k = 0; k < x.tdepth; ++k) x.tdims[k] = q[i].to_dims[k];
   }
-  DevBuf dq, dr, dtr;
+  // per-query pricing tables, exactly as a plan builds them
+  constexpr int kTab = tpk::kBwTab + tpk::kScaleDim * tpk::kScaleDim;
+  std::vector<double> tabs((size_t)n * kTab);
+  for (int i = 0; i < n; ++i)
+    tpk::make_price_tabs(Env{pod[i].intra, pod[i].inter, (int64_t)pod[i].local}, &tabs[(size_t)i * kTab],
+                         &tabs[(size_t)i * kTab + tpk::kBwTab]);
+  DevBuf dq, dr, dtr, dtab;
   CUDA_TRY(dq.ensure(sizeof(tpk::QueryPOD) * n));
   CUDA_TRY(dr.ensure(sizeof(tp_redist_result) * n));
+  CUDA_TRY(dtab.ensure(sizeof(double) * tabs.size()));
   CUDA_TRY(cudaMemcpy(dq.p, pod.data(), sizeof(tpk::QueryPOD) * n, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dtab.p, tabs.data(), sizeof(double) * tabs.size(), cudaMemcpyHostToDevice));
   if (form == 1) {
     CUDA_TRY(dtr.ensure(sizeof(tpk::Trace) * n));
     query_kernel_warp<<<(n + 3) / 4, 128>>>((const tpk::QueryPOD*)dq.p, n, (tp_redist_result*)dr.p,
-                                             (tpk::Trace*)dtr.p);
+                                             (tpk::Trace*)dtr.p, (const double*)dtab.p);
   } else {
-    query_kernel<<<(n + 63) / 64, 64>>>((const tpk::QueryPOD*)dq.p, n, (tp_redist_result*)dr.p);
+    query_kernel<<<(n + 63) / 64, 64>>>((const tpk::QueryPOD*)dq.p, n, (tp_redist_result*)dr.p,
+                                        (const double*)dtab.p);
   }
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpy(r, dr.p, sizeof(tp_redist_result) * n, cudaMemcpyDeviceToHost));
   dq.release();
   dr.release();
   dtr.release();
+  dtab.release();
   return TP_OK;
 }
 

@@ -90,22 +90,30 @@ TP_HD void ct_fast(int te, int rexp, int ek, int64_t L, int l_log2, int64_t& ct,
   }
 }
 
+// Optional per-build tables: inter/ct for small ct and the AllToAll scale
+// k(p-k)/(p-1), computed with the reference's expressions (tp_warp.cuh
+// make_price_tabs). Null pointers: computed directly.
+struct FastTabs {
+  const double* bw;     // [65]
+  const double* scale;  // [17 * 17]
+};
+
 TP_HD double price_fast(bool a2a, int te, int rexp, int ek, int s, double bytes, const Env& env, int l_log2,
-                        double* vol, int64_t* ct_out) {
-  const double shard = bytes / exp2d(s);
+                        const FastTabs& tab, double* vol, int64_t* ct_out) {
+  const double shard = bytes * exp2d(-s);  // == bytes / 2^s (exact)
   const int64_t p = (int64_t)1 << ek;
   const double d = (double)p;
   int64_t ct, rep, gin;
   int rep_e, gin_e;
   ct_fast(te, rexp, ek, env.local, l_log2, ct, rep, gin, rep_e, gin_e);
   if (!a2a) {
-    *vol += (d - 1) * shard;
-    const double v = (double)(p - 1) * shard;
+    const double v = (d - 1) * shard;  // == (double)(p - 1) * shard
+    *vol += v;
     if (ct_out) *ct_out = ct;
-    return v / eff_bw(ct, env);
+    return v / ((tab.bw && ct >= 0 && ct < 65) ? tab.bw[ct] : eff_bw(ct, env));
   }
-  *vol += (d - 1) / d * shard;
-  const double v = (d - 1) / d * shard;
+  const double v = ((d - 1) * exp2d(-ek)) * shard;  // == (d - 1) / d * shard (exact)
+  *vol += v;
   const int64_t k = gin;
   if (k >= p) {
     if (ct_out) *ct_out = 0;
@@ -116,15 +124,17 @@ TP_HD double price_fast(bool a2a, int te, int rexp, int ek, int s, double bytes,
   else c = env.local / (k * rep);
   if (c < 1) c = 1;
   if (ct_out) *ct_out = c;
-  const double bw = eff_bw(c, env);
-  const double scale = (double)k * (double)(p - k) / (double)(p - 1);
+  const double bw = (tab.bw && c < 65) ? tab.bw[c] : eff_bw(c, env);
+  const double scale = (tab.scale && gin_e >= 0 && ek < 17) ? tab.scale[gin_e * 17 + ek]
+                                                             : (double)k * (double)(p - k) / (double)(p - 1);
   return scale * v / bw;
 }
 
 // Returns the tp_error_kind, or -1 when the pair needs the array form
 // (a device dim held twice by the working map).
 TP_HD int redist_cost_fast(int R, const SideDesc& gf, const SideDesc& gt, const DimT* dt, double bytes,
-                           const Env& env, int l_log2, double& sec_out, double& vol_out, Trace* tr) {
+                           const Env& env, int l_log2, const FastTabs& tab, double& sec_out, double& vol_out,
+                           Trace* tr) {
   if (R < 0 || R > kMaxR) return kCapacity;
   // ---- unify: bitmask closure (see tp_core.cuh) ----
   uint32_t D = gf.D | gt.D;
@@ -277,7 +287,7 @@ TP_HD int redist_cost_fast(int R, const SideDesc& gf, const SideDesc& gt, const 
           const int e = p2get(EXT, k), pos = p2get(POS, k);
           const int rexp = pos - popc32(PB & low_bits(pos));
           int64_t ct = 0;
-          const double c = price_fast(true, pos, rexp, e, s, bytes, env, l_log2, &vol, tr ? &ct : nullptr);
+          const double c = price_fast(true, pos, rexp, e, s, bytes, env, l_log2, tab, &vol, tr ? &ct : nullptr);
           sec += c;
           record(2, k, i, j, 0, ct, c);
           const uint32_t bi = 1u << i, bj = 1u << j;
@@ -304,7 +314,7 @@ TP_HD int redist_cost_fast(int R, const SideDesc& gf, const SideDesc& gt, const 
     const int e = p2get(EXT, k), pos = p2get(POS, k);
     const int rexp = pos - popc32(PB & low_bits(pos));
     int64_t ct = 0;
-    const double c = price_fast(false, pos, rexp, e, s, bytes, env, l_log2, &vol, tr ? &ct : nullptr);
+    const double c = price_fast(false, pos, rexp, e, s, bytes, env, l_log2, tab, &vol, tr ? &ct : nullptr);
     sec += c;
     record(1, k, i, -1, fb, ct, c);
     const uint32_t bi = 1u << i;
@@ -323,8 +333,9 @@ TP_HD int redist_cost_fast(int R, const SideDesc& gf, const SideDesc& gt, const 
 // The kernels' entry: the register form, or the array form for working maps
 // that hold a device dim twice (Fl/Tl: the original layouts when known).
 TP_HD int pair_cost_sd(int R, const SideDesc& F, const SideDesc& T, const Lay* Fl, const Lay* Tl, const DimT* dt,
-                       double bytes, const Env& env, int l_log2, double& sec, double& vol, Trace* tr) {
-  const int st = redist_cost_fast(R, F, T, dt, bytes, env, l_log2, sec, vol, tr);
+                       double bytes, const Env& env, int l_log2, const FastTabs& tab, double& sec, double& vol,
+                       Trace* tr) {
+  const int st = redist_cost_fast(R, F, T, dt, bytes, env, l_log2, tab, sec, vol, tr);
   if (st != -1) return st;
   Lay a, b;
   if (Fl) a = *Fl; else lay_of(F, R, a);
@@ -333,16 +344,16 @@ TP_HD int pair_cost_sd(int R, const SideDesc& F, const SideDesc& T, const Lay* F
 }
 
 TP_HD int pair_cost(int R, const Lay& F, const Lay& T, const DimT* dt, double bytes, const Env& env, int l_log2,
-                    double& sec, double& vol, Trace* tr) {
+                    const FastTabs& tab, double& sec, double& vol, Trace* tr) {
   SideDesc f, t;
   side_of(F, R, f);
   side_of(T, R, t);
-  return pair_cost_sd(R, f, t, &F, &T, dt, bytes, env, l_log2, sec, vol, tr);
+  return pair_cost_sd(R, f, t, &F, &T, dt, bytes, env, l_log2, tab, sec, vol, tr);
 }
 
 // Verification export: one query through pair_cost (the kernels' path).
 template <typename Result>
-TP_HD int run_query_fast(const QueryPOD& q, Result& r) {
+TP_HD int run_query_fast(const QueryPOD& q, Result& r, const FastTabs& tab) {
   r.status = 0;
   r.depth = 0;
   r.urank = 0;
@@ -380,7 +391,7 @@ TP_HD int run_query_fast(const QueryPOD& q, Result& r) {
   Env env{q.intra, q.inter, (int64_t)q.local};
   Trace tr;
   double sec = 0, vol = 0;
-  const int st = pair_cost(q.rank, F, T, dt, q.bytes, env, ilog2_exact((int64_t)q.local), sec, vol, &tr);
+  const int st = pair_cost(q.rank, F, T, dt, q.bytes, env, ilog2_exact((int64_t)q.local), tab, sec, vol, &tr);
   if (st) return st;
   if (tr.nops > kMaxOps) return kCapacity;
   r.depth = tr.depth;

@@ -1,25 +1,48 @@
 // tp_warp.cuh — warp-cooperative pricing of one (from, to) layout pair.
 //
-// The form the kernels run: one warp prices one pair. Lane q holds unified
-// tensor axis q (working-map entry w, target entry to) and unified device
-// dim q (log2 extent, lower device position). The sequence search's scans
-// (redistribution.hpp:350-417) become ballots + find-first-set, "device dim
-// k is in the working map" is a __reduce_or_sync mask, and with a
-// power-of-two local_device_num every integer division of the ct formulas
-// (cost_model.hpp:108-135, 197-222) is a shift. Control flow is
-// warp-uniform; the order of the inferred ops — and so the fp64 summation
-// order — is exactly the reference's. tp_core.cuh's scalar redist_cost is
-// the same algorithm one thread at a time (used by the host-side check).
+// The form the kernels run for small class tables: one warp prices one
+// pair. Everything that was a sequential loop in the scalar form is spread
+// over lanes:
+//   * the unification closure (tp_core.cuh): lane (side, dim) reflects its
+//     own region, the boundary sets are combined with one shuffle and one
+//     __reduce_or_sync per round;
+//   * unified device dim k sits on lane k (log2 extent, lower position,
+//     found with __fns), unified tensor axis q on lane q (its dim and part
+//     start located by a prefix over the dims' part counts);
+//   * the sequence search's scans (redistribution.hpp:350-417) are ballots +
+//     find-first-set, "device dim k is held" is a __reduce_or_sync mask and
+//     the ct repetition (cost_model.hpp:115-119) a __reduce_add_sync;
+//   * with a power-of-two local_device_num every ct division is a shift, and
+//     inter/ct and the AllToAll scale k(p-k)/(p-1) (cost_model.hpp:148-151,
+//     218) come from per-build tables computed with the reference's own
+//     expressions (so the values are the same IEEE results).
+// Control flow is warp-uniform; the order of the inferred ops — and so the
+// fp64 summation order — is exactly the reference's.
 #pragma once
 
 #include "tp_core.cuh"
 
 namespace tpk {
 
+constexpr int kBwTab = 65;      // inter/ct for ct in [0, 64] (ct = 0 -> intra)
+constexpr int kScaleDim = 17;   // scale[log2 k][log2 p], k < p <= 2^16
+
+// Per-build pricing tables (host-computed, same expressions as the reference).
+struct PriceTabs {
+  const double* bw;     // [kBwTab]
+  const double* scale;  // [kScaleDim * kScaleDim]
+};
+
 struct WarpEnv {
   Env env;
-  int l_log2;  // log2(local_device_num) when it is a power of two, else -1
+  int l_log2;     // log2(local_device_num) when it is a power of two, else -1
+  PriceTabs tab;  // may hold null pointers: then computed directly
 };
+
+__device__ __forceinline__ double bw_of(int64_t ct, const WarpEnv& we) {
+  if (we.tab.bw && ct >= 0 && ct < kBwTab) return we.tab.bw[ct];
+  return eff_bw(ct, we.env);
+}
 
 __device__ __forceinline__ void ct_gather_warp(int te, int rexp, int ek, const WarpEnv& we, int64_t& ct,
                                                int& rep_e, int64_t& rep, int64_t& gin, int& gin_e) {
@@ -58,119 +81,117 @@ __device__ __forceinline__ void ct_gather_warp(int te, int rexp, int ek, const W
 // AllGather / AllToAll on a device dim with log2 extent ek at lower device
 // position te; rexp = log2 of the in-node repetition; s = log2 of the
 // working map's shard divisor (cost_model.hpp:176-225, redistribution.hpp:521-553).
+// Divisions by powers of two are exact, so they are multiplications here.
 __device__ __forceinline__ double price_op_warp(bool a2a, int te, int rexp, int ek, int s, double bytes,
                                                 const WarpEnv& we, double* vol, int64_t* ct_out) {
-  const double shard = bytes / exp2d(s);
+  const double shard = bytes * exp2d(-s);  // == bytes / 2^s
   const int64_t p = (int64_t)1 << ek;
   const double d = (double)p;
   int64_t ct, rep, gin;
   int rep_e, gin_e;
   ct_gather_warp(te, rexp, ek, we, ct, rep_e, rep, gin, gin_e);
   if (!a2a) {
-    *vol += (d - 1) * shard;
-    const double v = (double)(p - 1) * shard;
+    const double v = (d - 1) * shard;  // == (double)(p - 1) * shard
+    *vol += v;
     *ct_out = ct;
-    return v / eff_bw(ct, we.env);
+    return v / bw_of(ct, we);
   }
-  *vol += (d - 1) / d * shard;
-  const double v = (d - 1) / d * shard;
+  const double v = ((d - 1) * exp2d(-ek)) * shard;  // == (d - 1) / d * shard
+  *vol += v;
   const int64_t k = gin;
   if (k >= p) {
     *ct_out = 0;
     return v / we.env.intra;
   }
   int64_t c;
-  if (we.l_log2 >= 0) {
-    c = gin_e + rep_e <= we.l_log2 ? ((int64_t)1 << (we.l_log2 - gin_e - rep_e)) : 0;
-  } else {
-    c = we.env.local / (k * rep);
-  }
+  if (we.l_log2 >= 0) c = gin_e + rep_e <= we.l_log2 ? ((int64_t)1 << (we.l_log2 - gin_e - rep_e)) : 0;
+  else c = we.env.local / (k * rep);
   if (c < 1) c = 1;
   *ct_out = c;
-  const double bw = eff_bw(c, we.env);
-  const double scale = (double)k * (double)(p - k) / (double)(p - 1);
+  const double bw = bw_of(c, we);
+  const double scale = (we.tab.scale && gin_e >= 0 && ek < kScaleDim)
+                           ? we.tab.scale[gin_e * kScaleDim + ek]
+                           : (double)k * (double)(p - k) / (double)(p - 1);
   return scale * v / bw;
 }
 
-// All 32 lanes call this with identical arguments. Returns the
-// tp_error_kind; sec/vol are valid on every lane. `tr` (verification
-// export only) is written by lane 0.
-__device__ int redist_cost_warp(int R, const SideDesc& gf, const SideDesc& gt, const DimT* dt, double bytes,
+// All 32 lanes call this with identical arguments. pf/pt point at the two
+// layout descriptors (global or local memory: lanes index them by dim).
+// Returns the tp_error_kind; sec/vol are valid on every lane. `tr`
+// (verification export only) is written by lane 0.
+__device__ int redist_cost_warp(int R, const SideDesc* pf, const SideDesc* pt, const DimT* dt, double bytes,
                                 const WarpEnv& we, double& sec_out, double& vol_out, Trace* tr) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   if (R < 0 || R > kMaxR) return kCapacity;
-  // ---- unify: the bitmask closure of tp_core.cuh (warp-uniform) ----
-  uint32_t D = gf.D | gt.D;
-  const int n = gf.n, nt = gt.n;
-  if (n != nt) return kNotUnifiable;  // redistribution.hpp:264-268
+  const int n = pf->n;
+  if (n != pt->n) return kNotUnifiable;  // redistribution.hpp:264-268
   if (n > kMaxD) return kCapacity;
-  for (int i = 0; i < R; ++i)
-    if (gf.x[i] > dt[i].t) return kFactorization;  // :102-111
-  for (int i = 0; i < R; ++i)
-    if (gt.x[i] > dt[i].t) return kFactorization;
-  D &= ~1u & low_bits(n);
-  uint32_t P[kMaxR];
-  for (int i = 0; i < R; ++i) P[i] = 0;
-  for (bool changed = true; changed;) {
-    changed = false;
-    for (int sd = 0; sd < 2; ++sd) {
-      const SideDesc& g = sd ? gt : gf;
-      for (int i = 0; i < R; ++i) {
-        const int x = g.x[i], a = g.a[i];
-        if (x < 2) continue;
-        const uint32_t win = low_bits(x) & ~1u;
-        const uint32_t tb = mirror((D >> a) & win, x) & win;
-        const uint32_t db = (mirror(P[i] & win, x) & win) << a;
-        if ((tb & ~P[i]) | (db & ~D)) changed = true;
-        P[i] |= tb;
-        D |= db;
-      }
-    }
+  // ---- unify: closure with lane (side, dim) owning one region ----
+  const bool rl = lane < 2 * R;
+  const int side = lane >= R ? 1 : 0;
+  const int dim = rl ? lane - side * R : 0;
+  const SideDesc* me = side ? pt : pf;
+  const int x = rl ? me->x[dim] : 0;
+  const int a = rl ? me->a[dim] : 0;
+  const int tdim = dt[dim].t;
+  if (__any_sync(FULL, rl && x > tdim)) return kFactorization;  // :102-111
+  uint32_t D = (pf->D | pt->D) & ~1u & low_bits(n);
+  uint32_t P = 0;  // boundaries of tensor dim `dim` (lanes of both sides agree)
+  const int partner = rl ? (side ? lane - R : lane + R) : lane;
+  const uint32_t win = low_bits(x) & ~1u;
+  for (;;) {
+    const uint32_t tb = x >= 2 ? (mirror((D >> a) & win, x) & win) : 0u;
+    const uint32_t db = x >= 2 ? ((mirror(P & win, x) & win) << a) : 0u;
+    const uint32_t nP = P | tb | __shfl_sync(FULL, tb, partner);
+    const uint32_t nD = D | __reduce_or_sync(FULL, db);
+    const bool changed = __any_sync(FULL, nP != P) || nD != D;
+    P = nP;
+    D = nD;
+    if (!changed) break;
   }
-  // lane k <- (log2 extent, lower position) of unified device dim k
-  int my_ext = 0, my_pos = n, next = 0;
-  if (n > 0) {
-    int prev = 0;
-    uint32_t rest = D | (1u << n);
-    while (rest) {
-      const int c = ffs32(rest);
-      rest &= rest - 1;
-      if (lane == next) {
-        my_ext = c - prev;
-        my_pos = prev;
-      }
-      ++next;
-      prev = c;
-    }
+  // ---- unified device dims: lane k <- (log2 extent, lower position) ----
+  const uint32_t Dn = n > 0 ? (D | (1u << n)) : 0u;
+  const int next = popc32(Dn);
+  int my_ext = 0, my_pos = n;
+  if (lane < next) {
+    const int up = __fns(Dn, 0, lane + 1);
+    my_pos = lane == 0 ? 0 : __fns(Dn, 0, lane);
+    my_ext = up - my_pos;
   }
-  // lane q <- (from, to) maps of unified tensor axis q (:330-345)
-  int my_w = -1, my_to = -1, U = 0;
+  // ---- unified tensor axes: lane q <- (from, to) of axis q (:330-345) ----
+  int U = 0, qi = -1, qj = 0;
+  uint32_t Pq = 0;
   for (int i = 0; i < R; ++i) {
-    uint32_t bnd = P[i];
-    int c = 0;
-    for (;;) {
-      if (U >= 32) return kCapacity;
-      if (lane == U) {
-        if (c < gf.x[i]) my_w = popc32(D & low_bits(gf.a[i] + gf.x[i] - c));
-        if (c < gt.x[i]) my_to = popc32(D & low_bits(gt.a[i] + gt.x[i] - c));
-      }
-      const int next_c = bnd ? ffs32(bnd) : (int)dt[i].t;
-      if (tr && lane == 0) {
-        tr->pe[U] = (uint8_t)(next_c - c);
-        tr->plast[U] = bnd == 0;
-        tr->pdim[U] = (uint8_t)i;
-      }
-      ++U;
-      if (!bnd) break;
-      c = next_c;
-      bnd &= bnd - 1;
+    const uint32_t Pi = __shfl_sync(FULL, P, i);
+    const int cnt = popc32(Pi) + 1;
+    if (qi < 0 && lane < U + cnt) {
+      qi = i;
+      qj = lane - U;
+      Pq = Pi;
     }
+    U += cnt;
+  }
+  if (U > 32) return kCapacity;
+  int my_w = -1, my_to = -1;
+  if (lane < U) {
+    const int c = qj == 0 ? 0 : __fns(Pq, 0, qj);
+    const int xf = pf->x[qi], xt = pt->x[qi];
+    if (c < xf) my_w = popc32(D & low_bits(pf->a[qi] + xf - c));
+    if (c < xt) my_to = popc32(D & low_bits(pt->a[qi] + xt - c));
   }
   if (tr) {
     for (int q = 0; q < U; ++q) {
       const int fw = __shfl_sync(FULL, my_w, q), ft = __shfl_sync(FULL, my_to, q);
+      const int di = __shfl_sync(FULL, qi, q), dj = __shfl_sync(FULL, qj, q);
+      const uint32_t Pd = __shfl_sync(FULL, Pq, q);
       if (lane == 0) {
+        const int np = popc32(Pd);
+        const int c0 = dj == 0 ? 0 : __fns(Pd, 0, dj);
+        const int c1 = dj < np ? __fns(Pd, 0, dj + 1) : (int)dt[di].t;
+        tr->pe[q] = (uint8_t)(c1 - c0);
+        tr->plast[q] = dj == np;
+        tr->pdim[q] = (uint8_t)di;
         tr->from_map[q] = (int8_t)fw;
         tr->to_map[q] = (int8_t)ft;
       }
@@ -290,7 +311,7 @@ __device__ int redist_cost_warp(int R, const SideDesc& gf, const SideDesc& gt, c
 
 // Verification export on a warp: exactly the kernels' code path.
 template <typename Result>
-__device__ int run_query_warp(const QueryPOD& q, Result& r, Trace& tr) {
+__device__ int run_query_warp(const QueryPOD& q, Result& r, Trace& tr, const PriceTabs& tabs) {
   const int lane = threadIdx.x & 31;
   if (lane == 0) {
     r.status = 0;
@@ -319,6 +340,10 @@ __device__ int run_query_warp(const QueryPOD& q, Result& r, Trace& tr) {
     ttot *= q.tdims[k];
   }
   DimT dt[kMaxR];
+  for (int i = 0; i < kMaxR; ++i) {
+    dt[i].t = 0;
+    dt[i].odd = 0;
+  }
   for (int i = 0; i < q.rank; ++i) {
     if (q.shape[i] < 1) return kCapacity;
     if (q.fmap[i] < -1 || q.fmap[i] >= q.fdepth || q.tmap[i] < -1 || q.tmap[i] >= q.tdepth) return kCapacity;
@@ -331,11 +356,12 @@ __device__ int run_query_warp(const QueryPOD& q, Result& r, Trace& tr) {
   WarpEnv we;
   we.env = Env{q.intra, q.inter, (int64_t)q.local};
   we.l_log2 = ilog2_exact((int64_t)q.local);
+  we.tab = tabs;
   double sec = 0, vol = 0;
   SideDesc fs, ts;
   side_of(F, q.rank, fs);
   side_of(T, q.rank, ts);
-  const int st = redist_cost_warp(q.rank, fs, ts, dt, q.bytes, we, sec, vol, &tr);
+  const int st = redist_cost_warp(q.rank, &fs, &ts, dt, q.bytes, we, sec, vol, &tr);
   if (st) return st;
   __syncwarp();
   if (lane == 0) {
@@ -360,6 +386,17 @@ __device__ int run_query_warp(const QueryPOD& q, Result& r, Trace& tr) {
     r.seconds = sec;
   }
   return kOk;
+}
+
+// Host-side construction of the pricing tables for one environment.
+inline void make_price_tabs(const Env& env, double* bw, double* scale) {
+  for (int ct = 0; ct < kBwTab; ++ct) bw[ct] = eff_bw(ct, env);  // cost_model.hpp:148-151
+  for (int ke = 0; ke < kScaleDim; ++ke) {
+    for (int pe = 0; pe < kScaleDim; ++pe) {
+      const int64_t k = (int64_t)1 << ke, p = (int64_t)1 << pe;
+      scale[ke * kScaleDim + pe] = ke < pe ? (double)k * (double)(p - k) / (double)(p - 1) : 0.0;  // :218
+    }
+  }
 }
 
 }  // namespace tpk

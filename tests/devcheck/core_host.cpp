@@ -45,6 +45,16 @@ extern "C" int core_redistribute_fast(const tp_redist_query* q, tp_redist_result
   for (int k = 0; k < q->from_depth; ++k) p.fdims[k] = q->from_dims[k];
   for (int k = 0; k < q->to_depth; ++k) p.tdims[k] = q->to_dims[k];
   p.bytes = q->tensor_bytes; p.intra = q->intra_bandwidth; p.inter = q->inter_bandwidth;
-  r->status = tpk::run_query_fast(p, *r);
+  tpk::FastTabs none{nullptr, nullptr};
+  if (q->local_device_num == 2) {  // also exercise the table path
+    static double bw[65], sc[17 * 17];
+    const tpk::Env env{p.intra, p.inter, (int64_t)p.local};
+    for (int ct = 0; ct < 65; ++ct) bw[ct] = tpk::eff_bw(ct, env);
+    for (int ke = 0; ke < 17; ++ke)
+      for (int pe = 0; pe < 17; ++pe)
+        sc[ke * 17 + pe] = ke < pe ? (double)(1ll << ke) * (double)((1ll << pe) - (1ll << ke)) / (double)((1ll << pe) - 1) : 0.0;
+    none = tpk::FastTabs{bw, sc};
+  }
+  r->status = tpk::run_query_fast(p, *r, none);
   return r->status;
 }
