@@ -540,12 +540,14 @@ __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
     }
   }
   // phase 2: class pairs, dequeued per warp
+  // the next index is fetched while the current one is priced
   if (kWarpForm) {
+    int next_idx = 0;
+    if (lane == 0) next_idx = atomicAdd(&a.sched->pair_head, 1);
     for (;;) {
-      int64_t idx = 0;
-      if (lane == 0) idx = atomicAdd(&a.sched->pair_head, 1);
-      idx = __shfl_sync(0xffffffffu, (long long)idx, 0);
+      const int64_t idx = __shfl_sync(0xffffffffu, next_idx, 0);
       if (idx >= a.total_pairs) break;
+      if (lane == 0) next_idx = atomicAdd(&a.sched->pair_head, 1);
       const int sig = sig_of_pair(a, idx);
       pair_warp(a, idx, sig);
       if (lane == 0) {
@@ -554,12 +556,13 @@ __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
       }
     }
   } else {
+    int next_chunk = 0;
+    if (lane == 0) next_chunk = atomicAdd(&a.sched->pair_head, 1);
     for (;;) {
-      int64_t chunk = 0;
-      if (lane == 0) chunk = atomicAdd(&a.sched->pair_head, 1);
-      chunk = __shfl_sync(0xffffffffu, (long long)chunk, 0);
+      const int64_t chunk = __shfl_sync(0xffffffffu, next_chunk, 0);
       const int64_t idx = chunk * 32 + lane;
       if (chunk * 32 >= a.total_pairs) break;
+      if (lane == 0) next_chunk = atomicAdd(&a.sched->pair_head, 1);
       const bool valid = idx < a.total_pairs;
       const int sig = valid ? sig_of_pair(a, idx) : -1;
       if (valid) pair_thread(a, idx, sig);

@@ -151,44 +151,57 @@ __device__ int redist_cost_warp(int R, const SideDesc* pf, const SideDesc* pt, c
     if (!changed) break;
   }
   // ---- unified device dims: lane k <- (log2 extent, lower position) ----
-  const uint32_t Dn = n > 0 ? (D | (1u << n)) : 0u;
-  const int next = popc32(Dn);
-  int my_ext = 0, my_pos = n;
-  if (lane < next) {
-    const int up = __fns(Dn, 0, lane + 1);
-    my_pos = lane == 0 ? 0 : __fns(Dn, 0, lane);
-    my_ext = up - my_pos;
+  int my_ext = 0, my_pos = n, next = 0;
+  if (n > 0) {
+    int prev = 0;
+    uint32_t rest = D | (1u << n);
+    while (rest) {  // warp-uniform
+      const int c = ffs32(rest);
+      rest &= rest - 1;
+      if (lane == next) {
+        my_ext = c - prev;
+        my_pos = prev;
+      }
+      ++next;
+      prev = c;
+    }
   }
   // ---- unified tensor axes: lane q <- (from, to) of axis q (:330-345) ----
   int U = 0, qi = -1, qj = 0;
   uint32_t Pq = 0;
+  int my_w = -1, my_to = -1, my_c = 0;
   for (int i = 0; i < R; ++i) {
-    const uint32_t Pi = __shfl_sync(FULL, P, i);
-    const int cnt = popc32(Pi) + 1;
-    if (qi < 0 && lane < U + cnt) {
-      qi = i;
-      qj = lane - U;
-      Pq = Pi;
+    uint32_t bnd = __shfl_sync(FULL, P, i);
+    const uint32_t Pi = bnd;
+    const int af = pf->a[i], xf = pf->x[i], at = pt->a[i], xt = pt->x[i];
+    int c = 0, j = 0;
+    for (;;) {  // warp-uniform walk over the dim's parts
+      if (U >= 32) return kCapacity;
+      if (lane == U) {
+        qi = i;
+        qj = j;
+        Pq = Pi;
+        my_c = c;
+        if (c < xf) my_w = popc32(D & low_bits(af + xf - c));
+        if (c < xt) my_to = popc32(D & low_bits(at + xt - c));
+      }
+      ++U;
+      ++j;
+      if (!bnd) break;
+      c = ffs32(bnd);
+      bnd &= bnd - 1;
     }
-    U += cnt;
-  }
-  if (U > 32) return kCapacity;
-  int my_w = -1, my_to = -1;
-  if (lane < U) {
-    const int c = qj == 0 ? 0 : __fns(Pq, 0, qj);
-    const int xf = pf->x[qi], xt = pt->x[qi];
-    if (c < xf) my_w = popc32(D & low_bits(pf->a[qi] + xf - c));
-    if (c < xt) my_to = popc32(D & low_bits(pt->a[qi] + xt - c));
   }
   if (tr) {
     for (int q = 0; q < U; ++q) {
       const int fw = __shfl_sync(FULL, my_w, q), ft = __shfl_sync(FULL, my_to, q);
       const int di = __shfl_sync(FULL, qi, q), dj = __shfl_sync(FULL, qj, q);
       const uint32_t Pd = __shfl_sync(FULL, Pq, q);
+      const int c0 = __shfl_sync(FULL, my_c, q);
       if (lane == 0) {
         const int np = popc32(Pd);
-        const int c0 = dj == 0 ? 0 : __fns(Pd, 0, dj);
-        const int c1 = dj < np ? __fns(Pd, 0, dj + 1) : (int)dt[di].t;
+        const uint32_t above = Pd & ~low_bits(c0 + 1);
+        const int c1 = dj < np ? ffs32(above) : (int)dt[di].t;
         tr->pe[q] = (uint8_t)(c1 - c0);
         tr->plast[q] = dj == np;
         tr->pdim[q] = (uint8_t)di;
