@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <array>
 #include <cstdint>
 #include <cstring>
@@ -139,11 +140,14 @@ struct ClassDesc {     // a node class
 };
 
 struct SigDesc {       // an edge class
-  int64_t pair_begin;
+  int64_t pair_begin;  // its table (a derived class: the base class's table)
   int64_t first_aux;   // aux id of (su=0, sw=0) of the class's first edge
   double bytes;
+  double scale;        // derived class: exact power-of-two factor on the base table
   int32_t R, Su, Sw, tab_u, tab_w, has_override;
   int32_t side_u, side_w;  // first producer / consumer SideDesc of the class
+  int32_t base;        // class whose pairs are computed (itself unless derived)
+  int32_t pad;
   int8_t sa_u[tpk::kMaxR];
   int8_t sa_w[tpk::kMaxR];
   DimT dt[tpk::kMaxR];
@@ -263,6 +267,8 @@ struct FusedArgs {
   // edge classes
   const SigDesc* sigs;
   int nsigs;
+  const int32_t* pair_sigs;
+  int npair_sigs;
   int64_t total_pairs;
   const double* overrides;
   const tpk::SideDesc* sides;
@@ -357,12 +363,12 @@ __device__ void node_row(const FusedArgs& a, int64_t row) {
 }
 
 __device__ __forceinline__ int sig_of_pair(const FusedArgs& a, int64_t idx) {
-  int lo = 0, hi = a.nsigs - 1;
+  int lo = 0, hi = a.npair_sigs - 1;  // classes that own a table, by pair_begin
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (a.sigs[mid].pair_begin <= idx) lo = mid; else hi = mid - 1;
+    if (a.sigs[a.pair_sigs[mid]].pair_begin <= idx) lo = mid; else hi = mid - 1;
   }
-  return lo;
+  return a.pair_sigs[lo];
 }
 
 // One (edge class, su, sw) pair on one thread (register form, tp_fast.cuh).
@@ -423,8 +429,9 @@ __device__ void fanout_tile(const FusedArgs& a, const Work& wk, FanEdge* sedge) 
   const int32_t Sw = sg.Sw;
   const int32_t P = sg.Su * Sw;
   const int64_t pb = sg.pair_begin;
+  const double f = sg.scale;  // 1, or the exact factor of a derived class
   if (threadIdx.x == 0) {  // wait for the class table and the node rows
-    while (ld_acquire(&a.sched->pairs_done[wk.sig]) < P) __nanosleep(64);
+    while (ld_acquire(&a.sched->pairs_done[sg.base]) < P) __nanosleep(64);
     while (ld_acquire(&a.sched->node_done) < a.total_rows) __nanosleep(64);
   }
   __syncthreads();
@@ -440,8 +447,8 @@ __device__ void fanout_tile(const FusedArgs& a, const Work& wk, FanEdge* sedge) 
     cur += step;
     if (cur >= Sw) cur -= Sw;
     const int64_t jc = j < P ? j : 0;
-    rs[k] = __ldcg(a.r_sec + pb + jc);  // L2: written by other SMs in this launch
-    rv[k] = __ldcg(a.r_vol + pb + jc);
+    rs[k] = __ldcg(a.r_sec + pb + jc) * f;  // L2: written by other SMs in this launch
+    rv[k] = __ldcg(a.r_vol + pb + jc) * f;
   }
   double c[kExpPer], v[kExpPer], m[kExpPer];
   int64_t cur_row = -1;
@@ -608,8 +615,8 @@ __global__ void rowmin_kernel(const EdgeDesc* __restrict__ edges, const int64_t*
   double mc = inf, mv = inf;
   for (int64_t sw = lane; sw < sg.Sw; sw += 32) {
     const int64_t j = sg.pair_begin + su * sg.Sw + sw;
-    const double c = cls_sec[ed.wrow + sw] + r_sec[j];
-    const double v = cls_vol[ed.wrow + sw] + r_vol[j];
+    const double c = cls_sec[ed.wrow + sw] + r_sec[j] * sg.scale;
+    const double v = cls_vol[ed.wrow + sw] + r_vol[j] * sg.scale;
     mc = c < mc ? c : mc;
     mv = v < mv ? v : mv;
   }
@@ -702,13 +709,13 @@ struct Arena {
   cudaStream_t stream = nullptr;
   DevBuf d_tabs, d_tables, d_classes, d_chks, d_slots, d_occs, d_members, d_sigs, d_edges, d_list,
       d_work, d_over, d_rsec, d_rvol, d_csec, d_cvol, d_cmem, d_cmem0, d_nwork, d_rowbase, d_sched, d_sidejobs,
-      d_sides, d_price;
+      d_sides, d_price, d_pairsigs;
   DevBuf out[9];  // one-shot staging of the requested outputs
   std::vector<std::array<int64_t, 4>> table_key;  // (offset, count, p, n) of the resident tables
   void release() {
     for (DevBuf* b : {&d_tabs, &d_tables, &d_classes, &d_chks, &d_slots, &d_occs, &d_members, &d_sigs,
                       &d_edges, &d_list, &d_work, &d_over, &d_rsec, &d_rvol, &d_csec, &d_cvol, &d_cmem,
-                      &d_cmem0, &d_nwork, &d_rowbase, &d_sched, &d_sidejobs, &d_sides, &d_price})
+                      &d_cmem0, &d_nwork, &d_rowbase, &d_sched, &d_sidejobs, &d_sides, &d_price, &d_pairsigs})
       b->release();
     for (auto& b : out) b.release();
     table_key.clear();
@@ -747,6 +754,7 @@ struct tp_plan {
   std::vector<int32_t> sig_edges;  // edges grouped by class, edge order within
   std::vector<int32_t> sig_edge_begin;
   std::vector<double> overrides;   // per pair; empty if no class needs one
+  std::vector<int32_t> pair_sigs;  // classes whose tables are computed, by pair_begin
   int64_t total_pairs = 0;
   int64_t h2d_bytes = 0;
   bool uploaded = false;
@@ -1050,7 +1058,16 @@ struct Builder {
     }
     for (int i = 0; i < p.valid_ops; ++i)
       if (p.in_deg[i] == 0) p.num_virtual += p.node_base[i + 1] - p.node_base[i];
+    for (auto& sd : p.sigs) {
+      sd.base = (int32_t)(&sd - p.sigs.data());
+      sd.scale = 1.0;
+    }
     st = memo_aliasing();
+    if (st) return st;
+    if (p.overrides.empty() && p.N > 0 && (p.N & (p.N - 1)) == 0) derive_classes();
+    p.pair_sigs.clear();
+    for (size_t c = 0; c < p.sigs.size(); ++c)
+      if (p.sigs[c].base == (int32_t)c) p.pair_sigs.push_back((int32_t)c);
     p.h2d_bytes = (int64_t)(p.tabs.size() * sizeof(TableDesc) + p.classes.size() * sizeof(ClassDesc) +
                             p.members.size() * sizeof(int64_t) + p.chks.size() * sizeof(SliceChk) +
                             p.slots.size() * sizeof(SlotDesc) + p.occs.size() * sizeof(Occ) +
@@ -1176,6 +1193,47 @@ struct Builder {
     class_members[cls].push_back(nb);
     wrow_of_op[i] = p.classes[cls].row_base;
     return TP_OK;
+  }
+
+  // Two edge classes with the same axis counts and slicings see the same
+  // layout pairs. When every tensor dim of both has 2-adic valuation >= log2
+  // N, no strategy can fail a divisibility check (a region spans at most
+  // log2 N bits), so their plans are identical and every priced quantity is
+  // linear in the tensor bytes; with a power-of-two byte ratio the later
+  // class's table is the earlier one's times that ratio, exactly (scaling by
+  // 2^k commutes with IEEE rounding). Such a class reuses the base table.
+  void derive_classes() {
+    tp_plan& p = *P;
+    std::map<std::vector<int64_t>, int32_t> base_of;
+    int64_t pairs = 0;
+    for (size_t c = 0; c < p.sigs.size(); ++c) {
+      SigDesc& sd = p.sigs[c];
+      bool safe = true;
+      for (int d = 0; d < sd.R; ++d) safe &= sd.dt[d].t >= p.n_log2;
+      std::vector<int64_t> key{sd.tab_u, sd.tab_w, sd.R};
+      for (int d = 0; d < sd.R; ++d) key.insert(key.end(), {(int64_t)sd.sa_u[d], (int64_t)sd.sa_w[d]});
+      if (safe) {
+        auto it = base_of.find(key);
+        if (it != base_of.end()) {
+          const SigDesc& b = p.sigs[it->second];
+          int ex = 0;
+          const double m = std::frexp(sd.bytes / b.bytes, &ex);
+          if (m == 0.5 && sd.bytes == std::ldexp(b.bytes, ex - 1) && ex > -900 && ex < 900) {
+            sd.base = it->second;
+            sd.scale = std::ldexp(1.0, ex - 1);
+            sd.pair_begin = b.pair_begin;
+            continue;
+          }
+        } else {
+          base_of.emplace(key, (int32_t)c);
+        }
+      }
+      sd.pair_begin = pairs;  // compact the computed tables
+      pairs += (int64_t)sd.Su * sd.Sw;
+    }
+    for (auto& sd : p.sigs)
+      if (sd.base != (int32_t)(&sd - p.sigs.data())) sd.pair_begin = p.sigs[sd.base].pair_begin;
+    p.total_pairs = pairs;
   }
 
   // The reference memo (aux_graph.hpp:257-271) keys on (shape, matrix, map)
@@ -1415,6 +1473,7 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
   CUDA_TRY(upload(A.d_slots, p->slots, s));
   CUDA_TRY(upload(A.d_occs, p->occs, s));
   CUDA_TRY(upload(A.d_sigs, p->sigs, s));
+  CUDA_TRY(upload(A.d_pairsigs, p->pair_sigs, s));
   CUDA_TRY(upload(A.d_edges, p->edges, s));
   CUDA_TRY(upload(A.d_over, p->overrides, s));
   CUDA_TRY(A.d_rsec.ensure(sizeof(double) * (p->total_pairs + 1)));
@@ -1484,6 +1543,8 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   a.cls_memdiv = (double*)A.d_cmem.p;
   a.sigs = (const SigDesc*)A.d_sigs.p;
   a.nsigs = (int)p->sigs.size();
+  a.pair_sigs = (const int32_t*)A.d_pairsigs.p;
+  a.npair_sigs = (int)p->pair_sigs.size();
   a.total_pairs = edge_phase ? p->total_pairs : 0;
   a.overrides = (const double*)A.d_over.p;
   a.sides = (const tpk::SideDesc*)A.d_sides.p;

@@ -18,14 +18,14 @@ flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)
 s = torch.cuda.Stream()
 plan.upload(s.cuda_stream)
 
-def timeit(cs, n=20):
+def timeit(cs, n=20, **kw):
     ts = []
     with torch.cuda.stream(s):
         for i in range(n + 3):
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(s)
-            plan.execute(cs, stream=s.cuda_stream)
+            plan.execute(cs, stream=s.cuda_stream, **kw)
             b.record(s)
             if i >= 3:
                 ts.append((a, b))
@@ -36,4 +36,6 @@ def timeit(cs, n=20):
 
 for form in (1, 2):
     plan.set_pair_form(form)
-    print(f"form {form}: nodes+pairs only {timeit(nodes_only):.1f} us, full build {timeit(full):.1f} us")
+    print(f"form {form}: nodes+pairs only {timeit(nodes_only):.1f} us, full build {timeit(full):.1f} us, "
+          f"nodes only {timeit(full, edge_range=(0, 0)):.1f} us, pairs only {timeit(nodes_only, skip_nodes=True):.1f} us, "
+          f"empty {timeit(nodes_only, edge_range=(0, 0), skip_nodes=True):.1f} us")

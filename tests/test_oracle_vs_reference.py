@@ -104,4 +104,6 @@ def test_ilp_on_oracle_tensors_matches_reference():
     for vol in (False, True):
         a = B.reference_solve(f, t, mode_volume=vol, threads=4)
         b = B.reference_solve(f, t, mode_volume=vol, threads=4, given=o)
+        # the explored-node count depends on how the 4 solver threads interleave
+        a.pop("nodes"), b.pop("nodes")
         assert a == b
