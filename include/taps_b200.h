@@ -171,6 +171,7 @@ typedef struct tp_plan_sizes_t {
   int64_t num_signatures;    /* distinct edge classes priced */
   int64_t num_pair_evals;    /* (signature, su, sw) pairs priced on device */
   int64_t h2d_bytes;         /* descriptor bytes copied to the device */
+  int64_t num_class_rows;    /* node-class strategy rows priced on device */
 } tp_plan_sizes_t;
 
 /* --- one-shot call: the drop-in for build_auxiliary_graph ---------------- */
@@ -210,6 +211,18 @@ int64_t tp_plan_last_launches(const tp_plan* plan);
  * and after the fan-out kernel (K4) of every execute; NULL disables. Used by
  * bench.py to time the dominant kernel live for the roofline. */
 tp_status tp_plan_set_profile_events(tp_plan* plan, void* start_event, void* stop_event);
+/* Diagnostics: when on, execute records device timestamps of its phases.
+ * tp_plan_timeline (synchronous) returns, in ns after the kernel's first block
+ * started: node rows done, first class pair done, all pairs done, first
+ * fan-out tile past its wait, kernel end (-1 where a phase did not run). */
+tp_status tp_plan_set_timeline(tp_plan* plan, int32_t on);
+tp_status tp_plan_timeline(tp_plan* plan, int64_t ns_out[5]);
+/* Per-item trace of the last execute with the timeline on. section 0: class
+ * pairs (start, duration); 1: node-class rows (start, duration);
+ * 2: fan-out tiles (start, wait for inputs, duration); ns, uint32, start
+ * after kernel start. out == NULL returns the entry count in *count; else
+ * *count must equal it and out holds 2 or 3 values per entry. */
+tp_status tp_plan_timeline_detail(tp_plan* plan, int32_t section, uint32_t* out, int64_t* count);
 
 /* Strategy table of an operator with p axes on N devices, in the reference's
  * enumeration order (layout.hpp:270-328), produced on the device.

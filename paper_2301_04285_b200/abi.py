@@ -114,6 +114,7 @@ class tp_plan_sizes_t(C.Structure):
         ("num_signatures", C.c_int64),
         ("num_pair_evals", C.c_int64),
         ("h2d_bytes", C.c_int64),
+        ("num_class_rows", C.c_int64),
     ]
 
 
@@ -216,6 +217,13 @@ def load_engine() -> C.CDLL:
     lib.tp_plan_check_errors.restype = C.c_int
     lib.tp_plan_set_profile_events.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     lib.tp_plan_set_profile_events.restype = C.c_int
+    lib.tp_plan_set_timeline.argtypes = [C.c_void_p, C.c_int32]
+    lib.tp_plan_set_timeline.restype = C.c_int
+    lib.tp_plan_timeline.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+    lib.tp_plan_timeline.restype = C.c_int
+    lib.tp_plan_timeline_detail.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_uint32),
+                                            C.POINTER(C.c_int64)]
+    lib.tp_plan_timeline_detail.restype = C.c_int
     lib.tp_plan_last_launches.argtypes = [C.c_void_p]
     lib.tp_plan_last_launches.restype = C.c_int64
     lib.tp_enumerate_strategies.argtypes = [C.c_int32, C.c_int64, P(C.c_int64), _p_i64, _p_i32,
@@ -241,7 +249,7 @@ def load_engine() -> C.CDLL:
 EXPORTED_SYMBOLS = (
     "tp_build_cost_tensors", "tp_plan_create", "tp_plan_destroy", "tp_plan_sizes",
     "tp_plan_index", "tp_plan_upload", "tp_plan_execute", "tp_plan_execute_host", "tp_plan_check_errors",
-    "tp_plan_last_launches", "tp_plan_set_profile_events", "tp_enumerate_strategies", "tp_redistribute_batch",
+    "tp_plan_last_launches", "tp_plan_set_profile_events", "tp_plan_set_timeline", "tp_plan_timeline", "tp_plan_timeline_detail", "tp_enumerate_strategies", "tp_redistribute_batch",
     "tp_redistribute_batch_form", "tp_plan_set_pair_form",
     "tp_last_error", "tp_last_error_kind", "tp_abi_version",
 )

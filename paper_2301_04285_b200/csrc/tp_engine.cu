@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <array>
 #include <cstdint>
@@ -147,7 +148,12 @@ struct SigDesc {       // an edge class
   int32_t R, Su, Sw, tab_u, tab_w, has_override;
   int32_t side_u, side_w;  // first producer / consumer SideDesc of the class
   int32_t base;        // class whose pairs are computed (itself unless derived)
-  int32_t pad;
+  // distinct producer / consumer layouts: the class table is Un x Wn; maps
+  // (offsets into FusedArgs::maps) take a strategy to its distinct layout
+  // (uid_*, [S*]) and a distinct layout to its first strategy (rep_*, [*n])
+  int32_t Un, Wn, uid_u, uid_w, rep_u, rep_w;
+  int32_t ident;       // the maps are identities (every strategy a distinct layout)
+  int32_t pad2;
   int8_t sa_u[tpk::kMaxR];
   int8_t sa_w[tpk::kMaxR];
   DimT dt[tpk::kMaxR];
@@ -160,24 +166,7 @@ struct EdgeDesc {
   int32_t sig, e;
 };
 
-struct Work {
-  int32_t sig;
-  int32_t ebeg, eend;  // into the per-execute FanEdge list
-  int32_t j0;          // first pair of the tile within the class block
-};
 
-struct FanEdge {       // one graph edge of an execute's range
-  int64_t out_base;    // output index of its pair (0, 0)
-  int64_t wrow;        // class row of the consumer's strategy 0
-  int64_t nb_u, nb_w;  // first aux node of producer / consumer (records)
-  int32_t e, pad;
-};
-
-struct NodeWork {      // fan-out of one node class's rows to a chunk of its members
-  int32_t cls;
-  int32_t mbeg, mend;
-  int32_t pad;
-};
 
 struct TableDesc {
   int64_t offset, count;
@@ -195,9 +184,7 @@ struct SideJob {       // the SideDescs of one (edge class, side)
 // pair (latency-bound), so a warp cooperates on each pair; above it the
 // register-resident thread form has ~6x fewer instructions per pair.
 constexpr int64_t kWarpPairLimit = 16384;
-constexpr int kExpPer = 4;
-constexpr int kExpTile = 256 * kExpPer;  // class pairs per fan-out tile
-constexpr int kMaxChunk = 64;            // edges per fan-out tile
+constexpr int kFanPer = 4;  // output positions a fan-out thread has in flight
 
 // ---------------------------------------------------------------------------
 // kernels
@@ -232,24 +219,65 @@ __global__ void side_kernel(const SideJob* __restrict__ jobs, int njobs, int64_t
   out[i] = d;
 }
 
-// Per-execute scheduling state, zeroed by one memset before the launch.
+// Scheduling state of a launch. Zeroed once (memset) when the arena is set
+// up; afterwards the last CTA of every launch zeroes the counters it used, so
+// a build is one kernel node with no memset in front. Errors alternate
+// between two slots by launch parity: a launch writes err_c[parity] and
+// clears the other slot for the next one.
 struct Sched {
-  unsigned long long err_c;  // ~(smallest error key); 0 = no error
-  int head;                  // next block work item (node rows, then fan-out)
-  int pair_head;             // next class pair (warp form) / pair chunk (thread form)
+  unsigned long long err_c[2];  // ~(smallest error key); 0 = no error
+  int head;                  // next phase-2 block item
+  int unit_head;             // next phase-1 unit: node row, then class pair (chunk)
   int node_done;             // node-class rows finished
+  int exit_count;            // CTAs done (the last one resets)
+  int timeline;              // record the timestamps below
   int pad;
+  // %globaltimer ns (min fields stored as complements): kernel start (min),
+  // node rows done, first pair done (min), pairs done, first fan-out tile
+  // past its wait (min), kernel end
+  unsigned long long t[6];
   int pairs_done[2];         // per edge class (allocated to the class count)
 };
 
-__device__ __forceinline__ void flag_error(Sched* s, uint64_t key) {
-  atomicMax(&s->err_c, ~(unsigned long long)key);  // max of ~key = min of key
+__device__ __forceinline__ void flag_error(unsigned long long* err, uint64_t key) {
+  atomicMax(err, ~(unsigned long long)key);  // max of ~key = min of key
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// timeline slot k: max of the timestamp, or min for the complemented slots
+__device__ __forceinline__ void stamp(Sched* s, int k, bool is_min) {
+  if (!s->timeline) return;
+  const unsigned long long t = gtimer();
+  atomicMax(&s->t[k], is_min ? ~t : t);
+}
+
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// counter bump that publishes this thread's earlier stores (pairs with ld_acquire)
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" : : "l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+// Spin (relaxed: an acquire load also invalidates the SM's L1, which the
+// other CTAs there are reading through) until *p >= v, then acquire once.
+__device__ __forceinline__ void wait_at_least(const int* p, int v) {
+  while (ld_relaxed(p) < v) __nanosleep(64);
+  (void)ld_acquire(p);
 }
 
 struct FusedArgs {
@@ -265,31 +293,41 @@ struct FusedArgs {
   double* cls_mem;
   double* cls_memdiv;
   // edge classes
+  unsigned* pair_ns;  // timeline: per class pair / node-row item duration
+  unsigned* item_ns;
+  unsigned* fan_ns;
   const SigDesc* sigs;
   int nsigs;
-  const int32_t* pair_sigs;
-  int npair_sigs;
+  const int32_t* pair_sig;  // edge class of every table entry
+  const int32_t* row_cls;   // node class of every class row
+  const int32_t* maps;
+
   int64_t total_pairs;
   const double* overrides;
   const tpk::SideDesc* sides;
   double* r_sec;
   double* r_vol;
   // fan-out
-  const Work* work;
-  const FanEdge* fan;
+  const EdgeDesc* edges;  // graph edges, by id
+  int e0, e1;             // the execute's edge range
+  int64_t A0, A1;         // its aux ids
+  int64_t range_len;      // aux edges per fan-out item
   double* e_sec;
   double* e_vol;
   double* e_mem;
   char* records;
   int general_store;  // records requested or not all three SoA tensors given
-  const NodeWork* nwork;
-  const int64_t* member_nb;
+  const int64_t* op_node;  // node_base per operator [num_ops + 1]
+  const int64_t* op_row;   // class row of strategy 0 per operator
+  int nops;
+  int64_t num_nodes;
+  int64_t node_range_len;  // aux nodes per node range
   double* n_sec;
   double* n_vol;
   double* n_mem;
-  // work-item ranges: [0, i_pair) node rows, [i_pair, i_exp) pairs,
-  // [i_exp, i_nfan) fan-out tiles, [i_nfan, i_end) node fan-out
-  int i_pair, i_exp, i_nfan, i_end;
+  // phase-2 block items: [0, i_exp) node ranges (need only the node rows,
+  // which finish long before the class tables), [i_exp, i_end) edge ranges
+  int i_exp, i_end;
   int warp_form;  // pairs: 1 = warp per pair, 0 = thread per pair
   // shared
   const Strat* tables;
@@ -299,92 +337,117 @@ struct FusedArgs {
   const double* bw_tab;     // inter/ct, tpk::kBwTab entries
   const double* scale_tab;  // AllToAll scale, kScaleDim^2 entries
   Sched* sched;
+  unsigned long long* err;  // this launch's error slot
+  int parity;               // of the launch (error slot)
+  int nsigs_reset;          // pairs_done counters the last CTA zeroes
+  int dbg;
 };
 
 constexpr int kFusedThreads = 256;
-constexpr int kWarpPairsPerItem = kFusedThreads / 32;
 
-// One aux-node row of a node class (aux_graph.hpp:120-167).
+// One aux-node row of a node class (aux_graph.hpp:120-167) on one warp:
+// lanes take the slice checks and the tensor occurrences in parallel (their
+// descriptor loads overlap), lane 0 then accumulates the terms in occurrence
+// order, so the sums round exactly as the reference's sequential loop.
 __device__ void node_row(const FusedArgs& a, int64_t row) {
-  int lo = 0, hi = a.ncls - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a.classes[mid].row_base <= row) lo = mid; else hi = mid - 1;
-  }
-  const ClassDesc cd = a.classes[lo];
+  const int lane = threadIdx.x & 31;
+  const ClassDesc cd = a.classes[a.row_cls[row]];
   const int64_t s = row - cd.row_base;
   const Strat st = a.tables[cd.table + s];
-  // layout.hpp:349-367: every slice in axis order must divide its extent
-  for (int c = cd.chk_begin; c < cd.chk_end; ++c) {
-    const SliceChk k = a.chks[c];
+  // layout.hpp:349-367: every slice in axis order must divide its extent;
+  // the first failing one (in order) names the error
+  for (int c0 = cd.chk_begin; c0 < cd.chk_end; c0 += 32) {
+    const int c = c0 + lane;
     int kind = 0;
-    if (k.slot < 0) kind = tpk::kUnknownSliceTensor;
-    else if (st.deg[k.axis] > k.v) kind = tpk::kIndivisible;
-    if (kind) {
-      flag_error(a.sched, ekey(1 + (uint64_t)(cd.first_node + s) * 2 + 1, kind));
-      a.cls_sec[row] = a.cls_vol[row] = a.cls_mem[row] = a.cls_memdiv[row] = 0;
+    if (c < cd.chk_end) {
+      const SliceChk k = a.chks[c];
+      if (k.slot < 0) kind = tpk::kUnknownSliceTensor;
+      else if (st.deg[k.axis] > k.v) kind = tpk::kIndivisible;
+    }
+    const unsigned bad = __ballot_sync(0xffffffffu, kind != 0);
+    if (bad) {
+      if (lane == __ffs(bad) - 1) {
+        flag_error(a.err, ekey(1 + (uint64_t)(cd.first_node + s) * 2 + 1, kind));
+        a.cls_sec[row] = a.cls_vol[row] = a.cls_mem[row] = a.cls_memdiv[row] = 0;
+      }
       return;
     }
   }
   double sec = 0, vol = 0, mem = 0;
-  for (int q = cd.occ_begin; q < cd.occ_end; ++q) {
-    const Occ oc = a.occs[q];
-    const SlotDesc sd = a.slots[cd.slot_begin + oc.slot];
-    int sdiv = 0;
-    for (int d = 0; d < sd.R; ++d)
-      if (sd.sa[d] >= 0) sdiv += st.deg[sd.sa[d]];
-    const int64_t shard_el = sdiv >= 63 ? 0 : (sd.elements >> sdiv);
-    const double sb = (double)shard_el * sd.es;  // layout.hpp:125-129
-    if (oc.in_memory) mem += sb;                 // aux_graph.hpp:151-167
-    int glog = 0;
-    for (int ax = 0; ax < cd.p; ++ax)
-      if ((oc.nonslicing >> ax) & 1) glog += st.deg[ax];
-    if (glog == 0) continue;  // group <= 1
-    // infer_ct_allreduce (cost_model.hpp:75-97)
-    const int64_t pd = sdiv > a.n_log2 ? 0 : ((int64_t)1 << (a.n_log2 - sdiv));
-    int64_t remain = a.env.local, dev_in = 1;
-    for (int k = 0; k < st.depth; ++k) {
-      bool contains = false;
-      for (int d = 0; d < sd.R; ++d) contains |= sd.sa[d] >= 0 && st.dmap[sd.sa[d]] == k;
-      const int64_t ek = (int64_t)1 << st.mx[k];
-      if (!contains && remain > 1) dev_in *= remain > ek ? ek : remain;
-      remain /= ek;
+  for (int q0 = cd.occ_begin; q0 < cd.occ_end; q0 += 32) {
+    const int q = q0 + lane;
+    double tv = 0, tc = 0, tm = 0;  // this occurrence's terms
+    bool has_v = false, has_m = false;
+    if (q < cd.occ_end) {
+      const Occ oc = a.occs[q];
+      const SlotDesc sd = a.slots[cd.slot_begin + oc.slot];
+      int sdiv = 0;
+      for (int d = 0; d < sd.R; ++d)
+        if (sd.sa[d] >= 0) sdiv += st.deg[sd.sa[d]];
+      const int64_t shard_el = sdiv >= 63 ? 0 : (sd.elements >> sdiv);
+      const double sb = (double)shard_el * sd.es;  // layout.hpp:125-129
+      has_m = oc.in_memory;                        // aux_graph.hpp:151-167
+      tm = sb;
+      int glog = 0;
+      for (int ax = 0; ax < cd.p; ++ax)
+        if ((oc.nonslicing >> ax) & 1) glog += st.deg[ax];
+      if (glog > 0) {  // group > 1
+        // infer_ct_allreduce (cost_model.hpp:75-97)
+        const int64_t pd = sdiv > a.n_log2 ? 0 : ((int64_t)1 << (a.n_log2 - sdiv));
+        int64_t remain = a.env.local, dev_in = 1;
+        for (int k = 0; k < st.depth; ++k) {
+          bool contains = false;
+          for (int d = 0; d < sd.R; ++d) contains |= sd.sa[d] >= 0 && st.dmap[sd.sa[d]] == k;
+          const int64_t ek = (int64_t)1 << st.mx[k];
+          if (!contains && remain > 1) dev_in *= remain > ek ? ek : remain;
+          remain /= ek;
+        }
+        const int64_t ct = dev_in >= pd ? 0 : (dev_in > 1 ? a.env.local / dev_in : a.env.local);
+        const double n = (double)((int64_t)1 << glog);
+        tv = 2.0 * (n - 1) / n * sb;  // allreduce_volume, cost_model.hpp:39-43
+        tc = tv / tpk::eff_bw(ct, a.env);
+        has_v = true;
+      }
     }
-    const int64_t ct = dev_in >= pd ? 0 : (dev_in > 1 ? a.env.local / dev_in : a.env.local);
-    const double n = (double)((int64_t)1 << glog);
-    const double v = 2.0 * (n - 1) / n * sb;  // allreduce_volume, cost_model.hpp:39-43
-    vol += v;
-    sec += v / tpk::eff_bw(ct, a.env);
+    const int cnt = min(32, cd.occ_end - q0);
+    for (int i = 0; i < cnt; ++i) {  // in occurrence order
+      const double v = __shfl_sync(0xffffffffu, tv, i);
+      const double c = __shfl_sync(0xffffffffu, tc, i);
+      const double m = __shfl_sync(0xffffffffu, tm, i);
+      const unsigned flags = __shfl_sync(0xffffffffu, (has_v ? 1u : 0u) | (has_m ? 2u : 0u), i);
+      if (flags & 2u) mem += m;
+      if (flags & 1u) {
+        vol += v;
+        sec += c;
+      }
+    }
   }
-  a.cls_sec[row] = sec;
-  a.cls_vol[row] = vol;
-  a.cls_mem[row] = mem;
-  a.cls_memdiv[row] = mem / cd.indeg;  // aux_graph.hpp:292
+  if (lane == 0) {
+    a.cls_sec[row] = sec;
+    a.cls_vol[row] = vol;
+    a.cls_mem[row] = mem;
+    a.cls_memdiv[row] = mem / cd.indeg;  // aux_graph.hpp:292
+  }
 }
 
-__device__ __forceinline__ int sig_of_pair(const FusedArgs& a, int64_t idx) {
-  int lo = 0, hi = a.npair_sigs - 1;  // classes that own a table, by pair_begin
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a.sigs[a.pair_sigs[mid]].pair_begin <= idx) lo = mid; else hi = mid - 1;
-  }
-  return a.pair_sigs[lo];
-}
+__device__ __forceinline__ int sig_of_pair(const FusedArgs& a, int64_t idx) { return a.pair_sig[idx]; }
 
 // One (edge class, su, sw) pair on one thread (register form, tp_fast.cuh).
-__device__ void pair_thread(const FusedArgs& a, int64_t idx, int sig) {
+__device__ void pair_thread(const FusedArgs& a, int64_t idx, int sig, const double* price) {
   const SigDesc& sg = a.sigs[sig];
-  const int32_t local = (int32_t)(idx - sg.pair_begin);
-  const int32_t su = local / sg.Sw, sw = local - su * sg.Sw;
+  const int32_t t = (int32_t)(idx - sg.pair_begin);
+  const int32_t ui = t / sg.Wn, wi = t - ui * sg.Wn;
+  const int32_t su = a.maps[sg.rep_u + ui], sw = a.maps[sg.rep_w + wi];
+  const int32_t local = su * sg.Sw + sw;  // first (su, sw) with these layouts
   const tpk::SideDesc F = a.sides[sg.side_u + su];
   const tpk::SideDesc T = a.sides[sg.side_w + sw];
   double sec = 0, vol = 0;
   if (!tpk::same_side(F, T, sg.R)) {  // aux_graph.hpp:260
     const double bytes = sg.has_override ? a.overrides[idx] : sg.bytes;
     const int st = tpk::pair_cost_sd(sg.R, F, T, nullptr, nullptr, sg.dt, bytes, a.env, a.l_log2,
-                                     tpk::FastTabs{a.bw_tab, a.scale_tab}, sec, vol, nullptr);
+                                     tpk::FastTabs{price, price + tpk::kBwTab}, sec, vol, nullptr);
     if (st) {
-      flag_error(a.sched, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
+      flag_error(a.err, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
       sec = vol = 0;
     }
   }
@@ -393,10 +456,13 @@ __device__ void pair_thread(const FusedArgs& a, int64_t idx, int sig) {
 }
 
 // One pair on one warp (warp form, tp_warp.cuh); lane 0 writes.
-__device__ void pair_warp(const FusedArgs& a, int64_t idx, int sig) {
+__device__ void pair_warp(const FusedArgs& a, int64_t idx, int sig, const double* price) {
+  const int lane = threadIdx.x & 31;
   const SigDesc& sg = a.sigs[sig];
-  const int32_t local = (int32_t)(idx - sg.pair_begin);
-  const int32_t su = local / sg.Sw, sw = local - su * sg.Sw;
+  const int32_t t = (int32_t)(idx - sg.pair_begin);
+  const int32_t ui = t / sg.Wn, wi = t - ui * sg.Wn;
+  const int32_t su = a.maps[sg.rep_u + ui], sw = a.maps[sg.rep_w + wi];
+  const int32_t local = su * sg.Sw + sw;  // first (su, sw) with these layouts
   const tpk::SideDesc* F = a.sides + sg.side_u + su;
   const tpk::SideDesc* T = a.sides + sg.side_w + sw;
   double sec = 0, vol = 0;
@@ -405,198 +471,344 @@ __device__ void pair_warp(const FusedArgs& a, int64_t idx, int sig) {
     tpk::WarpEnv we;
     we.env = a.env;
     we.l_log2 = a.l_log2;
-    we.tab = tpk::PriceTabs{a.bw_tab, a.scale_tab};
+    we.tab = tpk::PriceTabs{price, price + tpk::kBwTab};
     const int st = tpk::redist_cost_warp(sg.R, F, T, sg.dt, bytes, we, sec, vol, nullptr);
     if (st) {
-      if ((threadIdx.x & 31) == 0) flag_error(a.sched, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
+      if (lane == 0) flag_error(a.err, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
       sec = vol = 0;
     }
   }
-  if ((threadIdx.x & 31) == 0) {
+  if (lane == 0) {
     a.r_sec[idx] = sec;
     a.r_vol[idx] = vol;
   }
 }
 
-// Fan-out tile: every edge of a chunk of one edge class gets the class
-// tile's values at out_base(edge) + pair, lane-contiguous (256-B warp
-// stores); class rows are reloaded only when the consumer class changes
-// (edges are sorted by it).
-__device__ void fanout_tile(const FusedArgs& a, const Work& wk, FanEdge* sedge) {
-  const int nE = wk.eend - wk.ebeg;
-  for (int t = threadIdx.x; t < nE; t += kFusedThreads) sedge[t] = a.fan[wk.ebeg + t];
-  const SigDesc& sg = a.sigs[wk.sig];
-  const int32_t Sw = sg.Sw;
-  const int32_t P = sg.Su * Sw;
-  const int64_t pb = sg.pair_begin;
-  const double f = sg.scale;  // 1, or the exact factor of a derived class
-  if (threadIdx.x == 0) {  // wait for the class table and the node rows
-    while (ld_acquire(&a.sched->pairs_done[sg.base]) < P) __nanosleep(64);
-    while (ld_acquire(&a.sched->node_done) < a.total_rows) __nanosleep(64);
+// Fan-out range: the aux edges [start, end) of the execute's edge range,
+// contiguous in the reference's id order (edge, su, sw) and so in every
+// output array; all ranges have the same length, one wave of CTAs. Thread 0
+// stages the range's edges (up to kSegs at a time) in shared memory and waits
+// (acquire) for the node rows and the tables of their classes. Each thread
+// then walks its ids: aux id -> edge segment -> (su, sw) -> consumer class
+// row + table entry (aux_graph.hpp:286-295). Consecutive lanes write
+// consecutive ids, so every warp store is one 256-B segment per array.
+constexpr int kSegs = 32;  // one per lane of warp 0
+struct FanSeg {
+  int64_t begin, end;  // aux ids of the edge
+  int64_t pb, wrow;    // its class table, consumer class row of sw = 0
+  int64_t nb_u, nb_w;  // records only
+  double f;            // exact factor of a derived class
+  int32_t e, Sw, Wn, uid_u, uid_w, ident;
+  int32_t st_q, st_r;  // a thread's stride (kFusedThreads ids) in (su, sw)
+};
+
+__device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n, int* s_edge) {
+  const unsigned long long t0 = a.fan_ns ? gtimer() : 0;
+  const int64_t start = a.A0 + (int64_t)item * a.range_len;
+  const int64_t end = min(start + a.range_len, a.A1);
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {  // last edge with aux_base <= start: 32-ary search
+    int lo = a.e0, hi = a.e1 - 1;
+    while (lo < hi) {
+      const int step = (hi - lo + 32) / 32;
+      const int idx = lo + lane * step;
+      const unsigned ok = __ballot_sync(0xffffffffu, idx <= hi && a.edges[idx].aux_base <= start);
+      lo += (31 - __clz(ok)) * step;  // lane 0 always holds (invariant)
+      hi = min(hi, lo + step - 1);
+    }
+    if (lane == 0) *s_edge = lo;
   }
-  __syncthreads();
-  const int32_t step = kFusedThreads % Sw;
-  int32_t jj[kExpPer], sw[kExpPer];
-  double rs[kExpPer], rv[kExpPer];
-  int32_t cur = (wk.j0 + (int32_t)threadIdx.x) % Sw;
-#pragma unroll
-  for (int k = 0; k < kExpPer; ++k) {
-    const int32_t j = wk.j0 + (int32_t)threadIdx.x + k * kFusedThreads;
-    jj[k] = j < P ? j : -1;
-    sw[k] = cur;
-    cur += step;
-    if (cur >= Sw) cur -= Sw;
-    const int64_t jc = j < P ? j : 0;
-    rs[k] = __ldcg(a.r_sec + pb + jc) * f;  // L2: written by other SMs in this launch
-    rv[k] = __ldcg(a.r_vol + pb + jc) * f;
-  }
-  double c[kExpPer], v[kExpPer], m[kExpPer];
-  int64_t cur_row = -1;
-  for (int ei = 0; ei < nE; ++ei) {
-    const int64_t base = sedge[ei].out_base;
-    const int64_t wrow = sedge[ei].wrow;
-    if (wrow != cur_row) {  // block-uniform
-      cur_row = wrow;
-#pragma unroll
-      for (int k = 0; k < kExpPer; ++k) {
-        c[k] = __ldcg(a.cls_sec + wrow + sw[k]) + rs[k];  // aux_graph.hpp:290-291
-        v[k] = __ldcg(a.cls_vol + wrow + sw[k]) + rv[k];
-        m[k] = __ldcg(a.cls_memdiv + wrow + sw[k]);       // :292
+  int64_t pos = start;
+  bool first = true;
+  while (pos < end) {
+    __syncthreads();
+    if (threadIdx.x < 32) {  // warp 0 stages the next kSegs edges, lane per edge
+      const int e = *s_edge + lane;
+      const bool in = e < a.e1 && a.edges[e].aux_base < end;
+      if (in) {
+        const EdgeDesc ed = a.edges[e];
+        const int64_t eend = e + 1 < a.e1 ? a.edges[e + 1].aux_base : a.A1;
+        const SigDesc& sg = a.sigs[ed.sig];
+        wait_at_least(&a.sched->pairs_done[sg.base], sg.Un * sg.Wn);
+        seg[lane] = FanSeg{ed.aux_base, eend, sg.pair_begin, ed.wrow, ed.nb_u, ed.nb_w, sg.scale,
+                           ed.e, sg.Sw, sg.Wn, sg.uid_u, sg.uid_w, sg.ident,
+                           kFusedThreads / sg.Sw, kFusedThreads % sg.Sw};
+      }
+      if (a.dbg == 2 && first)
+        for (int c = lane; c < a.nsigs; c += 32)
+          if (a.sigs[c].base == c) wait_at_least(&a.sched->pairs_done[c], a.sigs[c].Un * a.sigs[c].Wn);
+      const int n = __popc(__ballot_sync(0xffffffffu, in));  // a prefix of the lanes
+      if (first) {
+        if (lane == 0) wait_at_least(&a.sched->node_done, (int)a.total_rows);
+        __syncwarp();
+      }
+      if (lane == 0) {
+        *s_n = n;
+        *s_edge += n;
+        if (first) {
+          stamp(a.sched, 4, true);
+          if (a.fan_ns) {
+            a.fan_ns[3 * item] = (unsigned)t0;
+            a.fan_ns[3 * item + 1] = (unsigned)(gtimer() - t0);
+          }
+        }
       }
     }
-    if (!a.general_store) {
+    first = false;
+    __syncthreads();
+    const int n = *s_n;
+    const int64_t span_end = min(end, seg[n - 1].end);
+    // (su, sw) of a thread's ids advance by a fixed stride within an edge;
+    // a division only where the thread enters an edge
+    int si = -1;
+    int32_t su = 0, sw = 0;
+    for (int64_t o0 = pos + threadIdx.x; o0 < span_end; o0 += kFusedThreads * kFanPer) {
+      double cs[kFanPer], vs[kFanPer], ms[kFanPer];
+      int64_t q[kFanPer];
 #pragma unroll
-      for (int k = 0; k < kExpPer; ++k) {
-        if (jj[k] < 0) continue;
-        const int64_t o = base + jj[k];
-        __stcs(a.e_sec + o, c[k]);  // streaming: written once, read by the host
-        __stcs(a.e_vol + o, v[k]);
-        __stcs(a.e_mem + o, m[k]);
+      for (int k = 0; k < kFanPer; ++k) {
+        const int64_t o = o0 + (int64_t)k * kFusedThreads;
+        q[k] = -1;
+        if (o >= span_end) continue;
+        if (si >= 0 && o < seg[si].end) {
+          su += seg[si].st_q;
+          sw += seg[si].st_r;
+          if (sw >= seg[si].Sw) {
+            sw -= seg[si].Sw;
+            ++su;
+          }
+        } else {
+          if (si < 0) si = 0;
+          while (o >= seg[si].end) ++si;
+          const int32_t j = (int32_t)(o - seg[si].begin);
+          su = j / seg[si].Sw;
+          sw = j - su * seg[si].Sw;
+        }
+        const FanSeg& g = seg[si];
+        const int32_t j = su * g.Sw + sw;
+        const int64_t r = g.ident ? g.pb + j : g.pb + (int64_t)a.maps[g.uid_u + su] * g.Wn + a.maps[g.uid_w + sw];
+        // class rows and tables: written before the acquire above, reused
+        // across the range's ids (L1)
+        if (a.dbg == 1) {
+          cs[k] = (double)r; vs[k] = (double)sw; ms[k] = g.f;
+        } else {
+        cs[k] = a.cls_sec[g.wrow + sw] + a.r_sec[r] * g.f;  // aux_graph.hpp:290-291
+        vs[k] = a.cls_vol[g.wrow + sw] + a.r_vol[r] * g.f;
+        ms[k] = a.cls_memdiv[g.wrow + sw];                 // :292
+        }
+        q[k] = o - a.A0;
+        if (a.records) {  // topoplan::AuxEdge, 40 bytes (aux_graph.hpp:52-59)
+          char* rec = a.records + q[k] * 40;
+          *reinterpret_cast<int2*>(rec) = make_int2(g.e, (int)(g.nb_u + su));
+          *reinterpret_cast<int2*>(rec + 8) = make_int2((int)(g.nb_w + sw), 0);
+        }
       }
-    } else {
 #pragma unroll
-      for (int k = 0; k < kExpPer; ++k) {
-        if (jj[k] < 0) continue;
-        const int64_t o = base + jj[k];
-        if (a.e_sec) __stcs(a.e_sec + o, c[k]);
-        if (a.e_vol) __stcs(a.e_vol + o, v[k]);
-        if (a.e_mem) __stcs(a.e_mem + o, m[k]);
-        if (!a.records) continue;
-        // topoplan::AuxEdge, 40 bytes (aux_graph.hpp:52-59)
-        const int32_t su = jj[k] / Sw;
-        char* rec = a.records + o * 40;
-        *reinterpret_cast<int2*>(rec) = make_int2(sedge[ei].e, (int)(sedge[ei].nb_u + su));
-        *reinterpret_cast<int2*>(rec + 8) = make_int2((int)(sedge[ei].nb_w + sw[k]), 0);
-        *reinterpret_cast<double*>(rec + 16) = c[k];
-        *reinterpret_cast<double*>(rec + 24) = v[k];
-        *reinterpret_cast<double*>(rec + 32) = m[k];
+      for (int k = 0; k < kFanPer; ++k) {
+        if (q[k] < 0) continue;
+        if (!a.general_store) {
+          __stcs(a.e_sec + q[k], cs[k]);  // streaming: written once, read by the host
+          __stcs(a.e_vol + q[k], vs[k]);
+          __stcs(a.e_mem + q[k], ms[k]);
+        } else {
+          if (a.e_sec) __stcs(a.e_sec + q[k], cs[k]);
+          if (a.e_vol) __stcs(a.e_vol + q[k], vs[k]);
+          if (a.e_mem) __stcs(a.e_mem + q[k], ms[k]);
+          if (a.records) {
+            char* rec = a.records + q[k] * 40;
+            *reinterpret_cast<double*>(rec + 16) = cs[k];
+            *reinterpret_cast<double*>(rec + 24) = vs[k];
+            *reinterpret_cast<double*>(rec + 32) = ms[k];
+          }
+        }
       }
     }
+    pos = span_end;
+  }
+  if (a.fan_ns) {
+    __syncthreads();
+    if (threadIdx.x == 0) a.fan_ns[3 * item + 2] = (unsigned)(gtimer() - t0);
   }
 }
 
 // Node tensors: every member operator of a node class gets the class rows.
-__device__ void node_fanout(const FusedArgs& a, const NodeWork& nw) {
-  if (threadIdx.x == 0)
-    while (ld_acquire(&a.sched->node_done) < a.total_rows) __nanosleep(64);
-  __syncthreads();
-  const ClassDesc cd = a.classes[nw.cls];
-  const int64_t total = (int64_t)(nw.mend - nw.mbeg) * cd.S;
-  for (int64_t t = threadIdx.x; t < total; t += kFusedThreads) {
-    const int64_t mm = t / cd.S, sidx = t - mm * cd.S;
-    const int64_t node = a.member_nb[nw.mbeg + mm] + sidx;
-    const int64_t row = cd.row_base + sidx;
-    if (a.n_sec) __stcs(a.n_sec + node, __ldcg(a.cls_sec + row));
-    if (a.n_vol) __stcs(a.n_vol + node, __ldcg(a.cls_vol + row));
-    if (a.n_mem) __stcs(a.n_mem + node, __ldcg(a.cls_mem + row));
+// Node range: the aux nodes [start, end) get their node class's rows
+// (aux_graph.hpp:120-167 values, one copy per member operator). Same walk as
+// the fan-out: warp 0 finds and stages the operators (lane per operator),
+// each thread copies its ids with kFanPer loads in flight.
+struct NodeSeg {
+  int64_t begin, end, row;
+};
+
+__device__ void node_range(const FusedArgs& a, int item, NodeSeg* seg, int* s_n, int* s_op) {
+  const int64_t start = (int64_t)item * a.node_range_len;
+  const int64_t end = min(start + a.node_range_len, a.num_nodes);
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {  // last operator with node_base <= start
+    int lo = 0, hi = a.nops - 1;
+    while (lo < hi) {
+      const int step = (hi - lo + 32) / 32;
+      const int idx = lo + lane * step;
+      const unsigned ok = __ballot_sync(0xffffffffu, idx <= hi && a.op_node[idx] <= start);
+      lo += (31 - __clz(ok)) * step;
+      hi = min(hi, lo + step - 1);
+    }
+    if (lane == 0) {
+      *s_op = lo;
+      wait_at_least(&a.sched->node_done, (int)a.total_rows);
+    }
+  }
+  int64_t pos = start;
+  while (pos < end) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int op = *s_op + lane;
+      const bool in = op < a.nops && a.op_node[op] < end;
+      if (in) seg[lane] = NodeSeg{a.op_node[op], a.op_node[op + 1], a.op_row[op]};
+      const int n = __popc(__ballot_sync(0xffffffffu, in));
+      if (lane == 0) {
+        *s_n = n;
+        *s_op += n;
+      }
+    }
+    __syncthreads();
+    const int64_t span_end = min(end, seg[*s_n - 1].end);
+    int si = 0;
+    for (int64_t o0 = pos + threadIdx.x; o0 < span_end; o0 += kFusedThreads * kFanPer) {
+      double cs[kFanPer], vs[kFanPer], ms[kFanPer];
+      int64_t q[kFanPer];
+#pragma unroll
+      for (int k = 0; k < kFanPer; ++k) {
+        const int64_t o = o0 + (int64_t)k * kFusedThreads;
+        q[k] = -1;
+        if (o >= span_end) continue;
+        while (o >= seg[si].end) ++si;
+        const int64_t row = seg[si].row + (o - seg[si].begin);
+        cs[k] = a.cls_sec[row];
+        vs[k] = a.cls_vol[row];
+        ms[k] = a.cls_mem[row];
+        q[k] = o;
+      }
+#pragma unroll
+      for (int k = 0; k < kFanPer; ++k) {
+        if (q[k] < 0) continue;
+        if (a.n_sec) __stcs(a.n_sec + q[k], cs[k]);
+        if (a.n_vol) __stcs(a.n_vol + q[k], vs[k]);
+        if (a.n_mem) __stcs(a.n_mem + q[k], ms[k]);
+      }
+    }
+    pos = span_end;
   }
 }
 
-// The whole build in one persistent launch. Phase 1: block work items for
-// the node-class rows (few). Phase 2: every warp pulls class pairs from an
-// atomic counter on its own — no block barrier, so a slow pair never idles
-// the other warps of its CTA. Phase 3: block work items for the fan-out tiles
-// and the node fan-out; a tile waits (acquire) only for its own edge class's
-// pair counter. Every pair is dequeued before any fan-out item and each
-// dequeued item runs to completion, so the waits always end. The
-// latency-bound pair work and the HBM-bound fan-out overlap, with no launch
-// gap or wave tail between them.
+// The whole build in one persistent launch. Phase 1: warps take units --
+// node-class rows first (every fan-out needs them), then class pairs (one per
+// warp, or 32 per warp in the thread form). A CTA claims its first 8 units
+// with one atomic and a warp claims further units alone, skipping the atomic
+// once the queue is drained, so the start-up burst does not serialise on the
+// counter and a slow pair never idles the other warps of its CTA. Each
+// finished unit bumps its counter with a release add. Phase 2: block work
+// items for the fan-out tiles and the node fan-out; a tile waits (acquire)
+// only for its own edge class's table and the node rows. A CTA reaches phase
+// 2 only after its warps drained the unit queue, and every claimed unit runs
+// to completion, so the waits always end. The latency-bound pricing and the
+// write-bound fan-out overlap, with no launch gap or wave tail between them.
 template <bool kWarpForm>
 __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
-  __shared__ int s_item;
-  __shared__ FanEdge sedge[kMaxChunk];
+  __shared__ int s_item, s_unit, s_edge, s_nseg;
+  __shared__ union {
+    FanSeg f[kSegs];
+    NodeSeg n[kSegs];
+  } s_seg;
+  __shared__ double s_price[tpk::kBwTab + tpk::kScaleDim * tpk::kScaleDim];  // the pricing tables
   const int lane = threadIdx.x & 31;
-  // phase 1: node-class rows; the first item past them is kept for phase 3
-  int carried;
-  for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(&a.sched->head, 1);
-    __syncthreads();
-    const int item = s_item;
-    __syncthreads();
-    if (item >= a.i_pair) {
-      carried = item;
-      break;
-    }
-    const int64_t row = (int64_t)item * kFusedThreads + threadIdx.x;
-    if (row < a.total_rows) node_row(a, row);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int64_t rem = a.total_rows - (int64_t)item * kFusedThreads;
-      atomicAdd(&a.sched->node_done, (int)(rem < kFusedThreads ? rem : kFusedThreads));
-    }
+  const int64_t pair_units = kWarpForm ? a.total_pairs : (a.total_pairs + 31) / 32;
+  const int64_t units = a.total_rows + pair_units;
+  if (threadIdx.x == 0) {
+    stamp(a.sched, 0, true);
+    s_unit = atomicAdd(&a.sched->unit_head, kFusedThreads / 32);
   }
-  // phase 2: class pairs, dequeued per warp
-  // the next index is fetched while the current one is priced
-  if (kWarpForm) {
-    int next_idx = 0;
-    if (lane == 0) next_idx = atomicAdd(&a.sched->pair_head, 1);
-    for (;;) {
-      const int64_t idx = __shfl_sync(0xffffffffu, next_idx, 0);
-      if (idx >= a.total_pairs) break;
-      if (lane == 0) next_idx = atomicAdd(&a.sched->pair_head, 1);
-      const int sig = sig_of_pair(a, idx);
-      pair_warp(a, idx, sig);
+  if (a.total_pairs > 0)
+    for (int i = threadIdx.x; i < tpk::kBwTab + tpk::kScaleDim * tpk::kScaleDim; i += kFusedThreads)
+      s_price[i] = a.bw_tab[i];  // bw_tab and scale_tab are one array
+  __syncthreads();
+  // phase 1: node-class rows, then class pairs
+  int64_t u = (int64_t)s_unit + (threadIdx.x >> 5);
+  while (u < units) {
+    const unsigned long long t0 = (a.pair_ns || a.item_ns) ? gtimer() : 0;
+    if (u < a.total_rows) {
+      node_row(a, u);
       if (lane == 0) {
-        __threadfence();
-        atomicAdd(&a.sched->pairs_done[sig], 1);
+        if (a.item_ns) {
+          a.item_ns[2 * u] = (unsigned)t0;
+          a.item_ns[2 * u + 1] = (unsigned)(gtimer() - t0);
+        }
+        red_release_add(&a.sched->node_done, 1);
       }
-    }
-  } else {
-    int next_chunk = 0;
-    if (lane == 0) next_chunk = atomicAdd(&a.sched->pair_head, 1);
-    for (;;) {
-      const int64_t chunk = __shfl_sync(0xffffffffu, next_chunk, 0);
-      const int64_t idx = chunk * 32 + lane;
-      if (chunk * 32 >= a.total_pairs) break;
-      if (lane == 0) next_chunk = atomicAdd(&a.sched->pair_head, 1);
+    } else if (kWarpForm) {
+      const int64_t idx = u - a.total_rows;
+      const int sig = sig_of_pair(a, idx);
+      pair_warp(a, idx, sig, s_price);
+      if (lane == 0) {
+        if (a.pair_ns) {
+          a.pair_ns[2 * idx] = (unsigned)t0;
+          a.pair_ns[2 * idx + 1] = (unsigned)(gtimer() - t0);
+        }
+        if (a.dbg == 3) atomicAdd(&a.sched->pairs_done[sig], 1);
+        else red_release_add(&a.sched->pairs_done[sig], 1);  // lane 0 wrote the entry
+      }
+    } else {
+      const int64_t idx = (u - a.total_rows) * 32 + lane;
       const bool valid = idx < a.total_pairs;
       const int sig = valid ? sig_of_pair(a, idx) : -1;
-      if (valid) pair_thread(a, idx, sig);
+      if (valid) pair_thread(a, idx, sig, s_price);
+      if (a.pair_ns && valid) {
+        a.pair_ns[2 * idx] = (unsigned)t0;
+        a.pair_ns[2 * idx + 1] = (unsigned)(gtimer() - t0);
+      }
       __threadfence();
       // one counter update per (warp, edge class)
       const unsigned grp = __match_any_sync(0xffffffffu, sig);
       if (valid && lane == __ffs(grp) - 1) atomicAdd(&a.sched->pairs_done[sig], __popc(grp));
     }
+    int next = 0;
+    if (lane == 0)
+      next = ld_relaxed(&a.sched->unit_head) >= units ? INT_MAX : atomicAdd(&a.sched->unit_head, 1);
+    u = __shfl_sync(0xffffffffu, next, 0);
   }
-  // phase 3: fan-out tiles and node fan-out (every pair is dequeued by now)
-  for (bool first = true;; first = false) {
-    int item = carried;
-    if (!first) {
-      if (threadIdx.x == 0) s_item = atomicAdd(&a.sched->head, 1);
-      __syncthreads();
-      item = s_item;
-      __syncthreads();
+  // phase 2: fan-out tiles and node fan-out
+  for (;;) {
+    __syncthreads();  // s_item / s_seg reuse
+    if (threadIdx.x == 0) s_item = atomicAdd(&a.sched->head, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= a.i_end) {
+      if (threadIdx.x == 0) {
+        stamp(a.sched, 5, false);
+        __threadfence();
+        if (atomicAdd(&a.sched->exit_count, 1) == (int)gridDim.x - 1) {
+          // every other CTA has finished: reset for the next launch
+          Sched* sc = a.sched;
+          sc->head = 0;
+          sc->unit_head = 0;
+          sc->node_done = 0;
+          for (int i = 0; i < a.nsigs_reset; ++i) sc->pairs_done[i] = 0;
+          sc->err_c[a.parity ^ 1] = 0;
+          sc->exit_count = 0;
+          __threadfence();
+        }
+      }
+      return;
     }
-    if (item >= a.i_end) return;
-    if (item < a.i_nfan) fanout_tile(a, a.work[item - a.i_exp], sedge);
-    else node_fanout(a, a.nwork[item - a.i_nfan]);
+    if (item < a.i_exp) node_range(a, item, s_seg.n, &s_nseg, &s_edge);
+    else fanout_range(a, item - a.i_exp, s_seg.f, &s_nseg, &s_edge);
   }
 }
 
 // K3 (optional): cond_min (solver.hpp:239-253), warp per (edge, su) row.
 __global__ void rowmin_kernel(const EdgeDesc* __restrict__ edges, const int64_t* __restrict__ row_base,
                               int e0, int nedges, int64_t nrows, const SigDesc* __restrict__ sigs,
+                              const int32_t* __restrict__ maps,
                               const double* __restrict__ r_sec, const double* __restrict__ r_vol,
                               const double* __restrict__ cls_sec, const double* __restrict__ cls_vol,
                               double* __restrict__ out_c, double* __restrict__ out_v) {
@@ -613,8 +825,9 @@ __global__ void rowmin_kernel(const EdgeDesc* __restrict__ edges, const int64_t*
   const int64_t su = row - row_base[lo];
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   double mc = inf, mv = inf;
+  const int64_t rbase = sg.pair_begin + (int64_t)maps[sg.uid_u + su] * sg.Wn;
   for (int64_t sw = lane; sw < sg.Sw; sw += 32) {
-    const int64_t j = sg.pair_begin + su * sg.Sw + sw;
+    const int64_t j = rbase + maps[sg.uid_w + sw];
     const double c = cls_sec[ed.wrow + sw] + r_sec[j] * sg.scale;
     const double v = cls_vol[ed.wrow + sw] + r_vol[j] * sg.scale;
     mc = c < mc ? c : mc;
@@ -707,15 +920,18 @@ int v2_capped(int64_t v) {
 struct Arena {
   int device = 0;
   cudaStream_t stream = nullptr;
-  DevBuf d_tabs, d_tables, d_classes, d_chks, d_slots, d_occs, d_members, d_sigs, d_edges, d_list,
-      d_work, d_over, d_rsec, d_rvol, d_csec, d_cvol, d_cmem, d_cmem0, d_nwork, d_rowbase, d_sched, d_sidejobs,
-      d_sides, d_price, d_pairsigs;
+  DevBuf d_tabs, d_tables, d_classes, d_chks, d_slots, d_occs, d_members, d_sigs, d_edges,
+      d_over, d_rsec, d_rvol, d_csec, d_cvol, d_cmem, d_cmem0, d_opnode, d_oprow, d_rowbase, d_sched, d_sidejobs,
+      d_sides, d_price, d_pairsigs, d_trace, d_maps, d_rowcls;
   DevBuf out[9];  // one-shot staging of the requested outputs
+  bool sched_clean = false;  // Sched zero (set up, or left so by the last launch)
+  bool timeline_set = false;
+  int parity = 0;
   std::vector<std::array<int64_t, 4>> table_key;  // (offset, count, p, n) of the resident tables
   void release() {
     for (DevBuf* b : {&d_tabs, &d_tables, &d_classes, &d_chks, &d_slots, &d_occs, &d_members, &d_sigs,
-                      &d_edges, &d_list, &d_work, &d_over, &d_rsec, &d_rvol, &d_csec, &d_cvol, &d_cmem,
-                      &d_cmem0, &d_nwork, &d_rowbase, &d_sched, &d_sidejobs, &d_sides, &d_price, &d_pairsigs})
+                      &d_edges, &d_over, &d_rsec, &d_rvol, &d_csec, &d_cvol, &d_cmem,
+                      &d_cmem0, &d_opnode, &d_oprow, &d_rowbase, &d_sched, &d_sidejobs, &d_sides, &d_price, &d_pairsigs, &d_trace, &d_maps, &d_rowcls})
       b->release();
     for (auto& b : out) b.release();
     table_key.clear();
@@ -754,18 +970,21 @@ struct tp_plan {
   std::vector<int32_t> sig_edges;  // edges grouped by class, edge order within
   std::vector<int32_t> sig_edge_begin;
   std::vector<double> overrides;   // per pair; empty if no class needs one
-  std::vector<int32_t> pair_sigs;  // classes whose tables are computed, by pair_begin
+  std::vector<int32_t> pair_sig;   // edge class of every table entry
+  std::vector<int32_t> row_cls;    // node class of every class row
+  std::vector<int32_t> maps;       // SigDesc uid_* / rep_* / mb_* / ml_* arrays
   int64_t total_pairs = 0;
   int64_t h2d_bytes = 0;
   bool uploaded = false;
-  std::vector<Work> work;
-  std::vector<NodeWork> nwork;
+  std::vector<int64_t> op_row;  // class row of strategy 0 per operator
   std::vector<SideJob> side_jobs;
   int64_t side_total = 0;
   int64_t last_launches = 0;
-  int32_t last_e0 = -1, last_e1 = -1;
   cudaStream_t last_stream = nullptr;
   cudaEvent_t prof_start = nullptr, prof_stop = nullptr;  // recorded around K2
+  bool timeline = false;
+  int last_parity = -1;  // error slot of the last launch (-1: none)
+  int64_t trace_n[3] = {0, 0, 0};  // pairs, node-row items, fan-out items traced
   int pair_form = 0;  // 0 = by size, 1 = warp per pair, 2 = thread per pair
   int resident_blocks = 0;  // persistent grid size (SMs x resident CTAs)
 };
@@ -908,6 +1127,7 @@ struct Builder {
     op_slots.resize(g->num_ops);
     slot_sa.resize(g->num_ops);
     wrow_of_op.assign(g->num_ops, 0);
+    p.op_row.assign(g->num_ops, 0);
     int64_t nodes = 0;
     p.valid_ops = g->num_ops;
     for (int i = 0; i < g->num_ops; ++i) {
@@ -939,9 +1159,6 @@ struct Builder {
       p.classes[c].mem_begin = (int32_t)p.members.size();
       for (int64_t nb : class_members[c]) p.members.push_back(nb);
       p.classes[c].mem_end = (int32_t)p.members.size();
-      const int per = std::max(1, 2048 / std::max(1, p.classes[c].S));
-      for (int m = p.classes[c].mem_begin; m < p.classes[c].mem_end; m += per)
-        p.nwork.push_back(NodeWork{(int32_t)c, m, std::min(p.classes[c].mem_end, m + per), 0});
     }
 
     // ---------------- edge phase (aux_graph.hpp:273-296) -----------------
@@ -980,7 +1197,7 @@ struct Builder {
         const int pw = g->op_axis_begin[w + 1] - g->op_axis_begin[w];
         const int64_t Su = p.node_base[u + 1] - p.node_base[u];
         const int64_t Sw = p.node_base[w + 1] - p.node_base[w];
-        if (Su * Sw >= ((int64_t)1 << 31) - kExpTile)
+        if (Su * Sw >= ((int64_t)1 << 31) - 4096)
           return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "more than 2^31 pairs on one edge");
         int64_t elements = 1;
         for (int d = 0; d < R; ++d) elements *= shape_of(tu)[d];
@@ -1064,16 +1281,23 @@ struct Builder {
     }
     st = memo_aliasing();
     if (st) return st;
-    if (p.overrides.empty() && p.N > 0 && (p.N & (p.N - 1)) == 0) derive_classes();
-    p.pair_sigs.clear();
+    layout_tables(p.overrides.empty());
+    p.pair_sig.assign(p.total_pairs, 0);
     for (size_t c = 0; c < p.sigs.size(); ++c)
-      if (p.sigs[c].base == (int32_t)c) p.pair_sigs.push_back((int32_t)c);
+      if (p.sigs[c].base == (int32_t)c)
+        std::fill(p.pair_sig.begin() + p.sigs[c].pair_begin,
+                  p.pair_sig.begin() + p.sigs[c].pair_begin + (int64_t)p.sigs[c].Un * p.sigs[c].Wn, (int32_t)c);
+    p.row_cls.assign(p.total_rows, 0);
+    for (size_t c = 0; c < p.classes.size(); ++c)
+      std::fill(p.row_cls.begin() + p.classes[c].row_base, p.row_cls.begin() + p.classes[c].row_base + p.classes[c].S,
+                (int32_t)c);
     p.h2d_bytes = (int64_t)(p.tabs.size() * sizeof(TableDesc) + p.classes.size() * sizeof(ClassDesc) +
                             p.members.size() * sizeof(int64_t) + p.chks.size() * sizeof(SliceChk) +
                             p.slots.size() * sizeof(SlotDesc) + p.occs.size() * sizeof(Occ) +
                             p.sigs.size() * sizeof(SigDesc) + p.edges.size() * sizeof(EdgeDesc) +
                             p.side_jobs.size() * sizeof(SideJob) +
-                            p.overrides.size() * sizeof(double));
+                            p.overrides.size() * sizeof(double) + p.maps.size() * sizeof(int32_t) +
+                            (p.pair_sig.size() + p.row_cls.size()) * sizeof(int32_t));
     return st;
   }
 
@@ -1192,23 +1416,78 @@ struct Builder {
     }
     class_members[cls].push_back(nb);
     wrow_of_op[i] = p.classes[cls].row_base;
+    p.op_row[i] = p.classes[cls].row_base;
     return TP_OK;
   }
 
+  // Class tables over distinct layouts. A pair's price is a function of the
+  // two layout descriptors (and the class's dims and bytes) only, so a class
+  // computes one entry per (distinct producer layout, distinct consumer
+  // layout) -- the reference's own memo key (aux_graph.hpp:257-271) -- and the
+  // fan-out reads it through the strategy -> layout maps. An entry's error
+  // is attributed to its first (su, sw), which is the smallest aux id any
+  // strategy pair with those layouts has.
+  //
   // Two edge classes with the same axis counts and slicings see the same
-  // layout pairs. When every tensor dim of both has 2-adic valuation >= log2
-  // N, no strategy can fail a divisibility check (a region spans at most
-  // log2 N bits), so their plans are identical and every priced quantity is
-  // linear in the tensor bytes; with a power-of-two byte ratio the later
-  // class's table is the earlier one's times that ratio, exactly (scaling by
-  // 2^k commutes with IEEE rounding). Such a class reuses the base table.
-  void derive_classes() {
+  // layouts. When every tensor dim of both has 2-adic valuation >= log2 N, no
+  // layout can fail a divisibility check (a region spans at most log2 N
+  // bits), so their plans are identical and every priced quantity is linear
+  // in the tensor bytes; with a power-of-two byte ratio the later class's
+  // table is the earlier one's times that ratio, exactly (scaling by 2^k
+  // commutes with IEEE rounding). Such a class reuses the base table.
+  //
+  // With per-pair byte overrides (memo_aliasing) the tables stay per
+  // strategy pair (identity maps).
+  void layout_tables(bool dedup) {
     tp_plan& p = *P;
+    p.maps.clear();
+    std::map<std::vector<int64_t>, std::array<int32_t, 3>> side_cache;  // -> uid, rep, count
+    auto side_maps = [&](int32_t tab, const int8_t* sa, int R, int32_t S) {
+      std::vector<int64_t> key{tab, R};
+      for (int d = 0; d < R; ++d) key.push_back(sa[d]);
+      auto it = side_cache.find(key);
+      if (it != side_cache.end()) return it->second;
+      std::array<int32_t, 3> r{(int32_t)p.maps.size(), 0, 0};
+      std::vector<int32_t> uid(S), reps;
+      if (dedup) {
+        const TableDesc* td = nullptr;
+        for (const auto& t : p.tabs)
+          if (t.offset == tab) td = &t;
+        std::map<std::vector<uint8_t>, int32_t> ids;
+        for (int32_t s = 0; s < S; ++s) {
+          Strat st;
+          tpk::unrank_strategy((int)td->p, (int)td->n, s, st);
+          Lay L;
+          tpk::side_layout(st, sa, R, L);
+          tpk::SideDesc d;
+          std::memset(&d, 0, sizeof(d));
+          tpk::side_of(L, R, d);
+          std::vector<uint8_t> k((const uint8_t*)&d, (const uint8_t*)&d + sizeof(d));
+          auto ins = ids.emplace(k, (int32_t)reps.size());
+          if (ins.second) reps.push_back(s);
+          uid[s] = ins.first->second;
+        }
+      } else {
+        for (int32_t s = 0; s < S; ++s) uid[s] = s, reps.push_back(s);
+      }
+      p.maps.insert(p.maps.end(), uid.begin(), uid.end());
+      r[1] = (int32_t)p.maps.size();
+      r[2] = (int32_t)reps.size();
+      p.maps.insert(p.maps.end(), reps.begin(), reps.end());
+      side_cache.emplace(key, r);
+      return r;
+    };
+    const bool derive = dedup && p.N > 0 && (p.N & (p.N - 1)) == 0;
     std::map<std::vector<int64_t>, int32_t> base_of;
     int64_t pairs = 0;
     for (size_t c = 0; c < p.sigs.size(); ++c) {
       SigDesc& sd = p.sigs[c];
-      bool safe = true;
+      const auto mu = side_maps(sd.tab_u, sd.sa_u, sd.R, sd.Su);
+      const auto mw = side_maps(sd.tab_w, sd.sa_w, sd.R, sd.Sw);
+      sd.uid_u = mu[0], sd.rep_u = mu[1], sd.Un = mu[2];
+      sd.uid_w = mw[0], sd.rep_w = mw[1], sd.Wn = mw[2];
+      sd.ident = sd.Un == sd.Su && sd.Wn == sd.Sw;  // ids are assigned in first-seen order
+      bool safe = derive;
       for (int d = 0; d < sd.R; ++d) safe &= sd.dt[d].t >= p.n_log2;
       std::vector<int64_t> key{sd.tab_u, sd.tab_w, sd.R};
       for (int d = 0; d < sd.R; ++d) key.insert(key.end(), {(int64_t)sd.sa_u[d], (int64_t)sd.sa_w[d]});
@@ -1229,10 +1508,8 @@ struct Builder {
         }
       }
       sd.pair_begin = pairs;  // compact the computed tables
-      pairs += (int64_t)sd.Su * sd.Sw;
+      pairs += (int64_t)sd.Un * sd.Wn;
     }
-    for (auto& sd : p.sigs)
-      if (sd.base != (int32_t)(&sd - p.sigs.data())) sd.pair_begin = p.sigs[sd.base].pair_begin;
     p.total_pairs = pairs;
   }
 
@@ -1324,44 +1601,6 @@ Arena* thread_arena(int device) {
 }
 
 // CTA work items for edges [e0, e1): class tiles x edge chunks.
-void make_work(tp_plan* p, int32_t e0, int32_t e1, std::vector<Work>& out, std::vector<FanEdge>& list) {
-  out.clear();
-  list.clear();
-  std::vector<int32_t> begin(1, 0);
-  int64_t total = 0;
-  const int64_t out_offset = p->edge_base[e0];
-  for (size_t s = 0; s < p->sigs.size(); ++s) {
-    for (int i = p->sig_edge_begin[s]; i < p->sig_edge_begin[s + 1]; ++i) {
-      const int e = p->sig_edges[i];
-      if (e >= e0 && e < e1) {
-        const EdgeDesc& ed = p->edges[e];
-        list.push_back(FanEdge{ed.aux_base - out_offset, ed.wrow, ed.nb_u, ed.nb_w, ed.e, 0});
-        total += (int64_t)p->sigs[s].Su * p->sigs[s].Sw;
-      }
-    }
-    begin.push_back((int32_t)list.size());
-  }
-  // ~4 CTAs per SM; each CTA reuses its class tile across a chunk of edges
-  const int64_t target = std::max<int64_t>(kExpTile, total / (148 * 4) + 1);
-  for (size_t s = 0; s < p->sigs.size(); ++s) {
-    const int b = begin[s], en = begin[s + 1];
-    if (b == en) continue;
-    const int64_t P = (int64_t)p->sigs[s].Su * p->sigs[s].Sw;
-    const int64_t tile = std::min<int64_t>(P, kExpTile);
-    const int chunk = (int)std::min<int64_t>(kMaxChunk, std::max<int64_t>(1, target / std::max<int64_t>(tile, 1)));
-    for (int64_t j0 = 0; j0 < P; j0 += kExpTile) {
-      for (int c = b; c < en; c += chunk) {
-        Work w{};
-        w.sig = (int32_t)s;
-        w.ebeg = c;
-        w.eend = std::min(en, c + chunk);
-        w.j0 = (int32_t)j0;
-        out.push_back(w);
-      }
-    }
-  }
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1419,6 +1658,7 @@ tp_status tp_plan_sizes(const tp_plan* p, tp_plan_sizes_t* s) {
   s->num_signatures = (int64_t)p->sigs.size();
   s->num_pair_evals = p->total_pairs;
   s->h2d_bytes = p->h2d_bytes;
+  s->num_class_rows = p->total_rows;
   return TP_OK;
 }
 
@@ -1467,13 +1707,16 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
     CUDA_TRY(upload(A.d_price, tabs, s));
   }
   CUDA_TRY(upload(A.d_classes, p->classes, s));
-  CUDA_TRY(upload(A.d_nwork, p->nwork, s));
+  CUDA_TRY(upload(A.d_opnode, p->node_base, s));
+  CUDA_TRY(upload(A.d_oprow, p->op_row, s));
   CUDA_TRY(upload(A.d_members, p->members, s));
   CUDA_TRY(upload(A.d_chks, p->chks, s));
   CUDA_TRY(upload(A.d_slots, p->slots, s));
   CUDA_TRY(upload(A.d_occs, p->occs, s));
   CUDA_TRY(upload(A.d_sigs, p->sigs, s));
-  CUDA_TRY(upload(A.d_pairsigs, p->pair_sigs, s));
+  CUDA_TRY(upload(A.d_pairsigs, p->pair_sig, s));
+  CUDA_TRY(upload(A.d_rowcls, p->row_cls, s));
+  CUDA_TRY(upload(A.d_maps, p->maps, s));
   CUDA_TRY(upload(A.d_edges, p->edges, s));
   CUDA_TRY(upload(A.d_over, p->overrides, s));
   CUDA_TRY(A.d_rsec.ensure(sizeof(double) * (p->total_pairs + 1)));
@@ -1483,8 +1726,8 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
   CUDA_TRY(A.d_cmem.ensure(sizeof(double) * (p->total_rows + 1)));
   CUDA_TRY(A.d_cmem0.ensure(sizeof(double) * (p->total_rows + 1)));
   CUDA_TRY(A.d_sched.ensure(sizeof(Sched) + sizeof(int) * (p->sigs.size() + 2)));
+  A.sched_clean = false;
   p->uploaded = true;
-  p->last_e0 = p->last_e1 = -1;
   return TP_OK;
 }
 
@@ -1509,8 +1752,17 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   if (!out) out = &none;
   int64_t launches = 0;
   Sched* sched = (Sched*)A.d_sched.p;
-  const size_t sched_bytes = sizeof(Sched) + sizeof(int) * (p->sigs.size() + 2);
-  CUDA_TRY(cudaMemsetAsync(sched, 0, sched_bytes, s));
+  if (!A.sched_clean) {
+    CUDA_TRY(cudaMemsetAsync(sched, 0, sizeof(Sched) + sizeof(int) * (p->sigs.size() + 2), s));
+    A.sched_clean = true;
+    A.parity = 0;
+  }
+  p->last_parity = -1;
+  if (p->timeline || A.timeline_set) {
+    CUDA_TRY(cudaMemsetAsync(&sched->timeline, 0, sizeof(int) * 2 + sizeof(sched->t), s));
+    if (p->timeline) CUDA_TRY(cudaMemsetAsync(&sched->timeline, 0x01, 1, s));
+    A.timeline_set = p->timeline;
+  }
   if (p->host_err != ~0ull && (p->host_err >> 6) == 0) {  // cycle: nothing to build
     p->last_launches = 0;
     return TP_OK;
@@ -1522,14 +1774,22 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   const bool edges_out = p->edge_base[e1] > out_offset && edge_phase &&
                          (out->edge_cost_s || out->edge_volume_bytes || out->edge_memory_bytes ||
                           out->aux_edge_records);
-  if (edges_out && (p->last_e0 != e0 || p->last_e1 != e1)) {
-    std::vector<FanEdge> list;
-    make_work(p, e0, e1, p->work, list);
-    CUDA_TRY(upload(A.d_work, p->work, s));
-    CUDA_TRY(upload(A.d_list, list, s));
-    p->last_e0 = e0;
-    p->last_e1 = e1;
+  if (p->resident_blocks == 0) {
+    int sms = 0, per_sm = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<true>, kFusedThreads, 0));
+    p->resident_blocks = std::max(1, sms * std::max(1, per_sm));
   }
+  // fan-out: equal ranges of the edge range's aux ids, one per resident CTA
+  // phase 2: the aux nodes and the edge range's aux edges cut into equal
+  // ranges, one per resident CTA
+  const int64_t total_out = edges_out ? p->edge_base[e1] - out_offset : 0;
+  const int64_t total_nodes = nodes_out ? p->num_aux_nodes : 0;
+  const int64_t nranges = std::max(1, p->resident_blocks - 2);  // the two ceilings below add at most 2
+  const int64_t range_len =
+      std::max<int64_t>(kFusedThreads * kFanPer, (total_out + total_nodes + nranges - 1) / nranges);
+  const int64_t exp_items = (total_out + range_len - 1) / range_len;
+  const int64_t nfan_items = (total_nodes + range_len - 1) / range_len;
   FusedArgs a{};
   a.classes = (const ClassDesc*)A.d_classes.p;
   a.ncls = (int)p->classes.size();
@@ -1543,22 +1803,31 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   a.cls_memdiv = (double*)A.d_cmem.p;
   a.sigs = (const SigDesc*)A.d_sigs.p;
   a.nsigs = (int)p->sigs.size();
-  a.pair_sigs = (const int32_t*)A.d_pairsigs.p;
-  a.npair_sigs = (int)p->pair_sigs.size();
+  a.pair_sig = (const int32_t*)A.d_pairsigs.p;
+  a.row_cls = (const int32_t*)A.d_rowcls.p;
+  a.maps = (const int32_t*)A.d_maps.p;
+
   a.total_pairs = edge_phase ? p->total_pairs : 0;
   a.overrides = (const double*)A.d_over.p;
   a.sides = (const tpk::SideDesc*)A.d_sides.p;
   a.r_sec = (double*)A.d_rsec.p;
   a.r_vol = (double*)A.d_rvol.p;
-  a.work = (const Work*)A.d_work.p;
-  a.fan = (const FanEdge*)A.d_list.p;
+  a.edges = (const EdgeDesc*)A.d_edges.p;
+  a.e0 = e0;
+  a.e1 = e1;
+  a.A0 = out_offset;
+  a.A1 = p->edge_base[e1];
+  a.range_len = range_len;
   a.e_sec = out->edge_cost_s;
   a.e_vol = out->edge_volume_bytes;
   a.e_mem = out->edge_memory_bytes;
   a.records = (char*)out->aux_edge_records;
   a.general_store = a.records || !(a.e_sec && a.e_vol && a.e_mem);
-  a.nwork = (const NodeWork*)A.d_nwork.p;
-  a.member_nb = (const int64_t*)A.d_members.p;
+  a.op_node = (const int64_t*)A.d_opnode.p;
+  a.op_row = (const int64_t*)A.d_oprow.p;
+  a.nops = p->num_ops;
+  a.num_nodes = p->num_aux_nodes;
+  a.node_range_len = range_len;
   a.n_sec = nodes_out ? out->node_intra_cost_s : nullptr;
   a.n_vol = nodes_out ? out->node_intra_volume_bytes : nullptr;
   a.n_mem = nodes_out ? out->node_memory_bytes : nullptr;
@@ -1569,32 +1838,39 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   a.bw_tab = (const double*)A.d_price.p;
   a.scale_tab = (const double*)A.d_price.p + tpk::kBwTab;
   a.sched = sched;
+  a.parity = A.parity;
+  a.err = &sched->err_c[A.parity];
+  a.nsigs_reset = (int)p->sigs.size();
+  { static const int d = getenv("TP_DBG") ? atoi(getenv("TP_DBG")) : 0; a.dbg = d; }
+  if (p->timeline) {
+    p->trace_n[0] = p->total_pairs;
+    p->trace_n[1] = p->total_rows;
+    p->trace_n[2] = exp_items;
+    const int64_t n = 2 * p->trace_n[0] + 2 * p->trace_n[1] + 3 * p->trace_n[2] + 1;
+    CUDA_TRY(A.d_trace.ensure(sizeof(unsigned) * n));
+    CUDA_TRY(cudaMemsetAsync(A.d_trace.p, 0, sizeof(unsigned) * n, s));
+    a.pair_ns = (unsigned*)A.d_trace.p;
+    a.item_ns = a.pair_ns + 2 * p->trace_n[0];
+    a.fan_ns = a.item_ns + 2 * p->trace_n[1];
+  }
   a.warp_form = p->pair_form == 1 || (p->pair_form == 0 && a.total_pairs <= kWarpPairLimit);
-  // block queue: [0, i_pair) node-row items, then [i_exp, i_nfan) fan-out
-  // tiles, [i_nfan, i_end) node fan-out; the pairs have their own warp queue
-  const int64_t node_items = (p->total_rows + kFusedThreads - 1) / kFusedThreads;
-  const int64_t exp_items = edges_out ? (int64_t)p->work.size() : 0;
-  const int64_t nfan_items = nodes_out ? (int64_t)p->nwork.size() : 0;
-  const int64_t total_items = node_items + exp_items + nfan_items;
-  if (total_items >= (1ll << 31) || a.total_pairs >= (1ll << 36))
+  // phase-1 units: node rows, then class pairs (warp form) or 32-pair chunks;
+  // phase-2 block items: [0, i_exp) node fan-out, [i_exp, i_end) fan-out ranges
+  const int64_t units = p->total_rows + (a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32);
+  const int64_t total_items = exp_items + nfan_items;
+  if (total_items >= (1ll << 30) || units >= (1ll << 30))
     return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many work items");
-  a.i_pair = (int)node_items;
-  a.i_exp = (int)node_items;
-  a.i_nfan = (int)(node_items + exp_items);
+  a.i_exp = (int)nfan_items;
   a.i_end = (int)total_items;
-  if (total_items > 0 || a.total_pairs > 0) {
-    if (p->resident_blocks == 0) {
-      int sms = 0, per_sm = 0;
-      CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<true>, kFusedThreads, 0));
-      p->resident_blocks = std::max(1, sms * std::max(1, per_sm));
-    }
-    const int64_t warps_needed = a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32;
-    const int64_t blocks_needed = std::max<int64_t>(total_items, (warps_needed + 7) / 8);
+  if (total_items > 0 || units > 0) {
+    const int64_t blocks_needed = std::max<int64_t>(total_items, (units + 7) / 8);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(blocks_needed, p->resident_blocks));
     if (p->prof_start) CUDA_TRY(cudaEventRecord(p->prof_start, s));
     if (a.warp_form) fused_kernel<true><<<(unsigned)grid, kFusedThreads, 0, s>>>(a);
     else fused_kernel<false><<<(unsigned)grid, kFusedThreads, 0, s>>>(a);
+    if (cudaPeekAtLastError() != cudaSuccess) A.sched_clean = false;
+    p->last_parity = A.parity;
+    A.parity ^= 1;
     ++launches;
     if (p->prof_stop) CUDA_TRY(cudaEventRecord(p->prof_stop, s));
   }
@@ -1609,7 +1885,7 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
       const int th = 256;
       rowmin_kernel<<<(unsigned)((rows * 32 + th - 1) / th), th, 0, s>>>(
           (const EdgeDesc*)A.d_edges.p, (const int64_t*)A.d_rowbase.p, e0, e1 - e0, rows,
-          (const SigDesc*)A.d_sigs.p, (const double*)A.d_rsec.p, (const double*)A.d_rvol.p,
+          (const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_maps.p, (const double*)A.d_rsec.p, (const double*)A.d_rvol.p,
           (const double*)A.d_csec.p, (const double*)A.d_cvol.p, out->row_min_cost_s, out->row_min_volume_bytes);
       ++launches;
     }
@@ -1634,13 +1910,68 @@ tp_status tp_plan_set_profile_events(tp_plan* p, void* start_event, void* stop_e
   return TP_OK;
 }
 
+tp_status tp_plan_set_timeline(tp_plan* p, int32_t on) {
+  if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
+  p->timeline = on != 0;
+  return TP_OK;
+}
+
+tp_status tp_plan_timeline(tp_plan* p, int64_t* ns_out) {
+  if (!p || !ns_out) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan or output");
+  if (!p->arena || !p->arena->d_sched.p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "plan not executed");
+  CUDA_TRY(cudaSetDevice(p->device));
+  CUDA_TRY(cudaStreamSynchronize(p->last_stream));
+  unsigned long long t[6];
+  CUDA_TRY(cudaMemcpy(t, ((Sched*)p->arena->d_sched.p)->t, sizeof(t), cudaMemcpyDeviceToHost));
+  const unsigned long long t0 = ~t[0];
+  for (int k = 1; k < 6; ++k) {
+    const bool is_min = k == 2 || k == 4;
+    const unsigned long long v = is_min ? ~t[k] : t[k];
+    ns_out[k - 1] = (t[k] == 0 || v < t0) ? -1 : (int64_t)(v - t0);
+  }
+  return TP_OK;
+}
+
+tp_status tp_plan_timeline_detail(tp_plan* p, int32_t section, uint32_t* out, int64_t* count) {
+  if (!p || !count || section < 0 || section > 2) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "bad argument");
+  if (!p->timeline || !p->arena || !p->arena->d_trace.p)
+    return set_err(TP_ERR_INVALID_ARGUMENT, 0, "timeline not recorded");
+  const int64_t n[3] = {p->trace_n[0], p->trace_n[1], p->trace_n[2]};
+  const int width[3] = {2, 2, 3};
+  if (!out) {
+    *count = n[section];
+    return TP_OK;
+  }
+  if (*count != n[section]) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "timeline count differs from the plan's");
+  CUDA_TRY(cudaSetDevice(p->device));
+  CUDA_TRY(cudaStreamSynchronize(p->last_stream));
+  unsigned long long t0 = 0;
+  CUDA_TRY(cudaMemcpy(&t0, &((Sched*)p->arena->d_sched.p)->t[0], sizeof(t0), cudaMemcpyDeviceToHost));
+  t0 = ~t0;
+  int64_t off = 0;
+  for (int k = 0; k < section; ++k) off += width[k] * n[k];
+  const int w = width[section];
+  std::vector<unsigned> h(w * n[section]);
+  if (!h.empty())
+    CUDA_TRY(cudaMemcpy(h.data(), (const unsigned*)p->arena->d_trace.p + off, sizeof(unsigned) * h.size(),
+                        cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < n[section]; ++i) {  // start after kernel start, then durations
+    out[w * i] = (uint32_t)(h[w * i] - (unsigned)t0);
+    for (int k = 1; k < w; ++k) out[w * i + k] = h[w * i + k];
+  }
+  return TP_OK;
+}
+
 tp_status tp_plan_check_errors(tp_plan* p) {
   if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
   CUDA_TRY(cudaSetDevice(p->device));
   unsigned long long dev = ~0ull;
   if (p->arena && p->arena->d_sched.p && p->last_stream) {
     unsigned long long c = 0;
-    CUDA_TRY(cudaMemcpyAsync(&c, p->arena->d_sched.p, sizeof(c), cudaMemcpyDeviceToHost, p->last_stream));
+    if (p->last_parity >= 0) {
+      CUDA_TRY(cudaMemcpyAsync(&c, &((Sched*)p->arena->d_sched.p)->err_c[p->last_parity], sizeof(c),
+                               cudaMemcpyDeviceToHost, p->last_stream));
+    }
     CUDA_TRY(cudaStreamSynchronize(p->last_stream));
     dev = ~c;  // Sched::err_c holds the complement of the smallest key
   }

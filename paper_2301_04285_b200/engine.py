@@ -143,6 +143,31 @@ class Plan:
             self.handle, C.c_void_p(start.cuda_event if start is not None else None),
             C.c_void_p(stop.cuda_event if stop is not None else None)))
 
+    def set_timeline(self, on: bool = True):
+        """Record device timestamps of the build phases (diagnostics)."""
+        _check(self.lib, self.lib.tp_plan_set_timeline(self.handle, int(on)))
+
+    def timeline(self) -> dict:
+        """ns after kernel start of the last execute (synchronises): node rows
+        done, first pair done, pairs done, first fan-out tile, kernel end."""
+        v = (C.c_int64 * 5)()
+        _check(self.lib, self.lib.tp_plan_timeline(self.handle, v))
+        return dict(zip(("rows", "first_pair", "pairs", "first_fanout", "end"), list(v)))
+
+    def timeline_detail(self):
+        """Per-item traces of the last execute: pairs and node-row items as
+        [start, duration], fan-out tiles as [start, wait, duration] (ns)."""
+        import numpy as np
+        res = []
+        for sec, w in ((0, 2), (1, 2), (2, 3)):
+            n = C.c_int64(0)
+            _check(self.lib, self.lib.tp_plan_timeline_detail(self.handle, sec, None, C.byref(n)))
+            v = np.zeros((n.value, w), np.uint32)
+            _check(self.lib, self.lib.tp_plan_timeline_detail(
+                self.handle, sec, v.ctypes.data_as(C.POINTER(C.c_uint32)), C.byref(n)))
+            res.append(v)
+        return tuple(res)
+
     def set_pair_form(self, form: int):
         """0 = by size (default), 1 = warp per class pair, 2 = thread per pair."""
         _check(self.lib, self.lib.tp_plan_set_pair_form(self.handle, form))

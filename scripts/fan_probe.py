@@ -1,0 +1,44 @@
+"""Full cfg4 build time (device, write-flush) and fan-out trace summary."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_2301_04285_b200 import engine as E, graph as G, models as M
+
+g, t = M.cfg4()
+plan = E.Plan(G.flatten(g), t, device=0)
+ne, nn = plan.sizes["num_aux_edges"], plan.sizes["num_aux_nodes"]
+dev = torch.device("cuda", 0)
+outs = {k: torch.empty(ne, dtype=torch.float64, device=dev) for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes")}
+outs.update({k: torch.empty(nn, dtype=torch.float64, device=dev) for k in ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes")})
+full = E.device_cost_struct(outs)
+flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)
+s = torch.cuda.Stream()
+plan.upload(s.cuda_stream)
+ts = []
+with torch.cuda.stream(s):
+    for i in range(23):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        plan.execute(full, stream=s.cuda_stream)
+        b.record(s)
+        if i >= 3:
+            ts.append((a, b))
+torch.cuda.synchronize()
+v = sorted(x.elapsed_time(y) * 1e3 for x, y in ts)
+plan.set_timeline(True)
+with torch.cuda.stream(s):
+    for i in range(4):
+        flush.zero_()
+        plan.execute(full, stream=s.cuda_stream)
+pr, it, fo = plan.timeline_detail()
+q = lambda x: [round(float(np.percentile(x, p)) / 1e3, 1) for p in (0, 50, 90, 100)]
+print(f"dbg={os.environ.get("TP_DBG", "0")} build {v[len(v)//2]:.1f} us | pairs end {q(pr[:,0]+pr[:,1])} "
+      f"rows end {q(it[:,0]+it[:,1])} | fan n={len(fo)} ready {q(fo[:,0]+fo[:,1])} work {q(fo[:,2]-fo[:,1])} end {q(fo[:,0]+fo[:,2])}")
+order = np.argsort(fo[:, 0] + fo[:, 1])[-8:]
+for i in order:
+    print(f"  late range {i}: start {fo[i,0]/1e3:.1f} wait {fo[i,1]/1e3:.1f} dur {fo[i,2]/1e3:.1f}")
+order = np.argsort(fo[:, 0])[:5]
+for i in order:
+    print(f"  early range {i}: start {fo[i,0]/1e3:.1f} wait {fo[i,1]/1e3:.1f} dur {fo[i,2]/1e3:.1f}")
