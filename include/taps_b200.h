@@ -218,10 +218,10 @@ tp_status tp_plan_set_profile_events(tp_plan* plan, void* start_event, void* sto
 tp_status tp_plan_set_timeline(tp_plan* plan, int32_t on);
 tp_status tp_plan_timeline(tp_plan* plan, int64_t ns_out[5]);
 /* Per-item trace of the last execute with the timeline on. section 0: class
- * pairs (start, duration); 1: node-class rows (start, duration);
+ * pairs (start, duration, edge class); 1: node-class rows (start, duration);
  * 2: fan-out tiles (start, wait for inputs, duration); ns, uint32, start
  * after kernel start. out == NULL returns the entry count in *count; else
- * *count must equal it and out holds 2 or 3 values per entry. */
+ * *count must equal it and out holds 3, 2 or 3 values per entry. */
 tp_status tp_plan_timeline_detail(tp_plan* plan, int32_t section, uint32_t* out, int64_t* count);
 
 /* Strategy table of an operator with p axes on N devices, in the reference's

@@ -219,6 +219,39 @@ __global__ void side_kernel(const SideJob* __restrict__ jobs, int njobs, int64_t
   out[i] = d;
 }
 
+// Everything one class-table entry's pricing reads, gathered at upload so a
+// pair warp starts from one dependent load (not pair -> class -> maps ->
+// layouts).
+struct alignas(16) PairRec {
+  tpk::SideDesc F, T;  // producer / consumer layouts (first strategies with them)
+  double bytes;        // tensor bytes (after the memo's first-writer rule)
+  int32_t sig, local;  // edge class; su * Sw + sw of the first such strategy pair
+  int32_t R, pad;
+  DimT dt[tpk::kMaxR];
+};
+
+__global__ void pair_rec_kernel(const SigDesc* __restrict__ sigs, const int32_t* __restrict__ pair_sig,
+                                const int32_t* __restrict__ maps, const tpk::SideDesc* __restrict__ sides,
+                                const double* __restrict__ overrides, int64_t total, PairRec* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int sig = pair_sig[idx];
+  const SigDesc& sg = sigs[sig];
+  const int32_t t = (int32_t)(idx - sg.pair_begin);
+  const int32_t ui = t / sg.Wn, wi = t - ui * sg.Wn;
+  const int32_t su = maps[sg.rep_u + ui], sw = maps[sg.rep_w + wi];
+  PairRec r;
+  r.F = sides[sg.side_u + su];
+  r.T = sides[sg.side_w + sw];
+  r.bytes = sg.has_override ? overrides[idx] : sg.bytes;
+  r.sig = sig;
+  r.local = su * sg.Sw + sw;
+  r.R = sg.R;
+  r.pad = 0;
+  for (int d = 0; d < tpk::kMaxR; ++d) r.dt[d] = sg.dt[d];
+  out[idx] = r;
+}
+
 // Scheduling state of a launch. Zeroed once (memset) when the arena is set
 // up; afterwards the last CTA of every launch zeroes the counters it used, so
 // a build is one kernel node with no memset in front. Errors alternate
@@ -299,6 +332,7 @@ struct FusedArgs {
   const SigDesc* sigs;
   int nsigs;
   const int32_t* pair_sig;  // edge class of every table entry
+  const PairRec* pairs;     // per table entry
   const int32_t* row_cls;   // node class of every class row
   const int32_t* maps;
 
@@ -432,22 +466,17 @@ __device__ void node_row(const FusedArgs& a, int64_t row) {
 
 __device__ __forceinline__ int sig_of_pair(const FusedArgs& a, int64_t idx) { return a.pair_sig[idx]; }
 
-// One (edge class, su, sw) pair on one thread (register form, tp_fast.cuh).
-__device__ void pair_thread(const FusedArgs& a, int64_t idx, int sig, const double* price) {
-  const SigDesc& sg = a.sigs[sig];
-  const int32_t t = (int32_t)(idx - sg.pair_begin);
-  const int32_t ui = t / sg.Wn, wi = t - ui * sg.Wn;
-  const int32_t su = a.maps[sg.rep_u + ui], sw = a.maps[sg.rep_w + wi];
-  const int32_t local = su * sg.Sw + sw;  // first (su, sw) with these layouts
-  const tpk::SideDesc F = a.sides[sg.side_u + su];
-  const tpk::SideDesc T = a.sides[sg.side_w + sw];
+// One class-table entry on one thread (register form, tp_fast.cuh).
+__device__ void pair_thread(const FusedArgs& a, int64_t idx, const double* price) {
+  const PairRec& pr = a.pairs[idx];
+  const tpk::SideDesc F = pr.F, T = pr.T;
+  const int R = pr.R;
   double sec = 0, vol = 0;
-  if (!tpk::same_side(F, T, sg.R)) {  // aux_graph.hpp:260
-    const double bytes = sg.has_override ? a.overrides[idx] : sg.bytes;
-    const int st = tpk::pair_cost_sd(sg.R, F, T, nullptr, nullptr, sg.dt, bytes, a.env, a.l_log2,
+  if (!tpk::same_side(F, T, R)) {  // aux_graph.hpp:260
+    const int st = tpk::pair_cost_sd(R, F, T, nullptr, nullptr, pr.dt, pr.bytes, a.env, a.l_log2,
                                      tpk::FastTabs{price, price + tpk::kBwTab}, sec, vol, nullptr);
     if (st) {
-      flag_error(a.err, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
+      flag_error(a.err, ekey(kEdgePhase + (uint64_t)(a.sigs[pr.sig].first_aux + pr.local) * 2 + 1, st));
       sec = vol = 0;
     }
   }
@@ -455,26 +484,21 @@ __device__ void pair_thread(const FusedArgs& a, int64_t idx, int sig, const doub
   a.r_vol[idx] = vol;
 }
 
-// One pair on one warp (warp form, tp_warp.cuh); lane 0 writes.
-__device__ void pair_warp(const FusedArgs& a, int64_t idx, int sig, const double* price) {
+// One class-table entry on one warp (warp form, tp_warp.cuh); lane 0 writes.
+__device__ void pair_warp(const FusedArgs& a, int64_t idx, const double* price) {
   const int lane = threadIdx.x & 31;
-  const SigDesc& sg = a.sigs[sig];
-  const int32_t t = (int32_t)(idx - sg.pair_begin);
-  const int32_t ui = t / sg.Wn, wi = t - ui * sg.Wn;
-  const int32_t su = a.maps[sg.rep_u + ui], sw = a.maps[sg.rep_w + wi];
-  const int32_t local = su * sg.Sw + sw;  // first (su, sw) with these layouts
-  const tpk::SideDesc* F = a.sides + sg.side_u + su;
-  const tpk::SideDesc* T = a.sides + sg.side_w + sw;
+  const PairRec* pr = a.pairs + idx;
   double sec = 0, vol = 0;
-  if (!tpk::same_side(*F, *T, sg.R)) {  // aux_graph.hpp:260
-    const double bytes = sg.has_override ? a.overrides[idx] : sg.bytes;
+  const int R = pr->R;
+  if (!tpk::same_side(pr->F, pr->T, R)) {  // aux_graph.hpp:260
     tpk::WarpEnv we;
     we.env = a.env;
     we.l_log2 = a.l_log2;
     we.tab = tpk::PriceTabs{price, price + tpk::kBwTab};
-    const int st = tpk::redist_cost_warp(sg.R, F, T, sg.dt, bytes, we, sec, vol, nullptr);
+    const int st = tpk::redist_cost_warp(R, &pr->F, &pr->T, pr->dt, pr->bytes, we, sec, vol, nullptr);
     if (st) {
-      if (lane == 0) flag_error(a.err, ekey(kEdgePhase + (uint64_t)(sg.first_aux + local) * 2 + 1, st));
+      if (lane == 0)
+        flag_error(a.err, ekey(kEdgePhase + (uint64_t)(a.sigs[pr->sig].first_aux + pr->local) * 2 + 1, st));
       sec = vol = 0;
     }
   }
@@ -747,8 +771,8 @@ __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
       }
     } else if (kWarpForm) {
       const int64_t idx = u - a.total_rows;
-      const int sig = sig_of_pair(a, idx);
-      pair_warp(a, idx, sig, s_price);
+      pair_warp(a, idx, s_price);
+      const int sig = a.pairs[idx].sig;
       if (lane == 0) {
         if (a.pair_ns) {
           a.pair_ns[2 * idx] = (unsigned)t0;
@@ -761,7 +785,7 @@ __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
       const int64_t idx = (u - a.total_rows) * 32 + lane;
       const bool valid = idx < a.total_pairs;
       const int sig = valid ? sig_of_pair(a, idx) : -1;
-      if (valid) pair_thread(a, idx, sig, s_price);
+      if (valid) pair_thread(a, idx, s_price);
       if (a.pair_ns && valid) {
         a.pair_ns[2 * idx] = (unsigned)t0;
         a.pair_ns[2 * idx + 1] = (unsigned)(gtimer() - t0);
@@ -922,7 +946,7 @@ struct Arena {
   cudaStream_t stream = nullptr;
   DevBuf d_tabs, d_tables, d_classes, d_chks, d_slots, d_occs, d_members, d_sigs, d_edges,
       d_over, d_rsec, d_rvol, d_csec, d_cvol, d_cmem, d_cmem0, d_opnode, d_oprow, d_rowbase, d_sched, d_sidejobs,
-      d_sides, d_price, d_pairsigs, d_trace, d_maps, d_rowcls;
+      d_sides, d_price, d_pairsigs, d_trace, d_maps, d_rowcls, d_pairrec;
   DevBuf out[9];  // one-shot staging of the requested outputs
   bool sched_clean = false;  // Sched zero (set up, or left so by the last launch)
   bool timeline_set = false;
@@ -931,7 +955,7 @@ struct Arena {
   void release() {
     for (DevBuf* b : {&d_tabs, &d_tables, &d_classes, &d_chks, &d_slots, &d_occs, &d_members, &d_sigs,
                       &d_edges, &d_over, &d_rsec, &d_rvol, &d_csec, &d_cvol, &d_cmem,
-                      &d_cmem0, &d_opnode, &d_oprow, &d_rowbase, &d_sched, &d_sidejobs, &d_sides, &d_price, &d_pairsigs, &d_trace, &d_maps, &d_rowcls})
+                      &d_cmem0, &d_opnode, &d_oprow, &d_rowbase, &d_sched, &d_sidejobs, &d_sides, &d_price, &d_pairsigs, &d_trace, &d_maps, &d_rowcls, &d_pairrec})
       b->release();
     for (auto& b : out) b.release();
     table_key.clear();
@@ -1719,6 +1743,13 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
   CUDA_TRY(upload(A.d_maps, p->maps, s));
   CUDA_TRY(upload(A.d_edges, p->edges, s));
   CUDA_TRY(upload(A.d_over, p->overrides, s));
+  CUDA_TRY(A.d_pairrec.ensure(sizeof(PairRec) * (p->total_pairs + 1)));
+  if (p->total_pairs > 0) {
+    pair_rec_kernel<<<(unsigned)((p->total_pairs + 127) / 128), 128, 0, s>>>(
+        (const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_pairsigs.p, (const int32_t*)A.d_maps.p,
+        (const tpk::SideDesc*)A.d_sides.p, (const double*)A.d_over.p, p->total_pairs, (PairRec*)A.d_pairrec.p);
+    CUDA_TRY(cudaGetLastError());
+  }
   CUDA_TRY(A.d_rsec.ensure(sizeof(double) * (p->total_pairs + 1)));
   CUDA_TRY(A.d_rvol.ensure(sizeof(double) * (p->total_pairs + 1)));
   CUDA_TRY(A.d_csec.ensure(sizeof(double) * (p->total_rows + 1)));
@@ -1804,6 +1835,7 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   a.sigs = (const SigDesc*)A.d_sigs.p;
   a.nsigs = (int)p->sigs.size();
   a.pair_sig = (const int32_t*)A.d_pairsigs.p;
+  a.pairs = (const PairRec*)A.d_pairrec.p;
   a.row_cls = (const int32_t*)A.d_rowcls.p;
   a.maps = (const int32_t*)A.d_maps.p;
 
@@ -1938,6 +1970,7 @@ tp_status tp_plan_timeline_detail(tp_plan* p, int32_t section, uint32_t* out, in
     return set_err(TP_ERR_INVALID_ARGUMENT, 0, "timeline not recorded");
   const int64_t n[3] = {p->trace_n[0], p->trace_n[1], p->trace_n[2]};
   const int width[3] = {2, 2, 3};
+  const int out_width[3] = {3, 2, 3};  // pairs also get their edge class
   if (!out) {
     *count = n[section];
     return TP_OK;
@@ -1955,9 +1988,11 @@ tp_status tp_plan_timeline_detail(tp_plan* p, int32_t section, uint32_t* out, in
   if (!h.empty())
     CUDA_TRY(cudaMemcpy(h.data(), (const unsigned*)p->arena->d_trace.p + off, sizeof(unsigned) * h.size(),
                         cudaMemcpyDeviceToHost));
+  const int ow = out_width[section];
   for (int64_t i = 0; i < n[section]; ++i) {  // start after kernel start, then durations
-    out[w * i] = (uint32_t)(h[w * i] - (unsigned)t0);
-    for (int k = 1; k < w; ++k) out[w * i + k] = h[w * i + k];
+    out[ow * i] = (uint32_t)(h[w * i] - (unsigned)t0);
+    for (int k = 1; k < w; ++k) out[ow * i + k] = h[w * i + k];
+    if (section == 0) out[ow * i + 2] = (uint32_t)p->pair_sig[i];
   }
   return TP_OK;
 }

@@ -155,11 +155,12 @@ class Plan:
         return dict(zip(("rows", "first_pair", "pairs", "first_fanout", "end"), list(v)))
 
     def timeline_detail(self):
-        """Per-item traces of the last execute: pairs and node-row items as
-        [start, duration], fan-out tiles as [start, wait, duration] (ns)."""
+        """Per-item traces of the last execute (ns): pairs as [start, duration,
+        edge class], node rows as [start, duration], fan-out ranges as
+        [start, wait, duration]."""
         import numpy as np
         res = []
-        for sec, w in ((0, 2), (1, 2), (2, 3)):
+        for sec, w in ((0, 3), (1, 2), (2, 3)):
             n = C.c_int64(0)
             _check(self.lib, self.lib.tp_plan_timeline_detail(self.handle, sec, None, C.byref(n)))
             v = np.zeros((n.value, w), np.uint32)

@@ -42,3 +42,6 @@ for i in order:
 order = np.argsort(fo[:, 0])[:5]
 for i in order:
     print(f"  early range {i}: start {fo[i,0]/1e3:.1f} wait {fo[i,1]/1e3:.1f} dur {fo[i,2]/1e3:.1f}")
+for c in np.unique(pr[:, 2]):
+    m = pr[:, 2] == c
+    print(f"  class {c}: pairs {m.sum()}, dur us {q(pr[m, 1])}")
