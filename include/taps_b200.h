@@ -208,8 +208,7 @@ tp_status tp_plan_check_errors(tp_plan* plan);
 /* Number of kernel launches the last execute issued. */
 int64_t tp_plan_last_launches(const tp_plan* plan);
 /* Optional cudaEvent_t pair recorded on the launch stream immediately before
- * and after the fan-out kernel (K4) of every execute; NULL disables. Used by
- * bench.py to time the dominant kernel live for the roofline. */
+ * and after the fused kernel of every execute; NULL disables. */
 tp_status tp_plan_set_profile_events(tp_plan* plan, void* start_event, void* stop_event);
 /* Diagnostics: when on, execute records device timestamps of its phases.
  * tp_plan_timeline (synchronous) returns, in ns after the kernel's first block
@@ -217,11 +216,15 @@ tp_status tp_plan_set_profile_events(tp_plan* plan, void* start_event, void* sto
  * fan-out tile past its wait, kernel end (-1 where a phase did not run). */
 tp_status tp_plan_set_timeline(tp_plan* plan, int32_t on);
 tp_status tp_plan_timeline(tp_plan* plan, int64_t ns_out[5]);
-/* Per-item trace of the last execute with the timeline on. section 0: class
- * pairs (start, duration, edge class); 1: node-class rows (start, duration);
- * 2: fan-out tiles (start, wait for inputs, duration); ns, uint32, start
- * after kernel start. out == NULL returns the entry count in *count; else
- * *count must equal it and out holds 3, 2 or 3 values per entry. */
+/* Per-item trace of the last execute with the timeline on (uint32 values).
+ * section 0: class pairs (start, duration, edge class); 1: node-class rows
+ * (start, duration); 2: fan-out ranges (start, wait for inputs, duration) --
+ * times in ns, starts after the kernel's first CTA started; 3: per class
+ * pair (warp form), SM clocks of the pricing sections (closure, axes,
+ * inference), inferred ops, unified axes, unified device dims, closure
+ * rounds, 0; 4: per warp of the launch, when it left the pricing phase (ns).
+ * out == NULL returns the entry count in *count; else *count must equal it
+ * and out holds 3, 2, 3, 8 or 1 values per entry. */
 tp_status tp_plan_timeline_detail(tp_plan* plan, int32_t section, uint32_t* out, int64_t* count);
 
 /* Strategy table of an operator with p axes on N devices, in the reference's

@@ -1,6 +1,7 @@
 """Build recipe: the CUDA engine (sm_100a) in-tree, plus the test oracles."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -8,8 +9,8 @@ import sys
 from .abi import ENGINE_SO, PKG_DIR, REPO_DIR
 
 SOURCES = [os.path.join(PKG_DIR, "csrc", "tp_engine.cu")]
-DEPS = SOURCES + [os.path.join(PKG_DIR, "csrc", "tp_core.cuh"), os.path.join(PKG_DIR, "csrc", "tp_fast.cuh"),
-                  os.path.join(REPO_DIR, "include", "taps_b200.h")]
+DEPS = SOURCES + sorted(glob.glob(os.path.join(PKG_DIR, "csrc", "*.cuh"))) + \
+    [os.path.join(REPO_DIR, "include", "taps_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

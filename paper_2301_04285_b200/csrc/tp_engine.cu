@@ -159,6 +159,18 @@ struct SigDesc {       // an edge class
   DimT dt[tpk::kMaxR];
 };
 
+// Everything the fan-out reads about one graph edge (host-built at plan
+// creation, one load per lane when a range stages its edges).
+struct FanSeg {
+  int64_t begin, end;  // aux ids of the edge
+  int64_t pb, wrow;    // its class table, consumer class row of sw = 0
+  int64_t nb_u, nb_w;  // records only
+  double f;            // exact factor of a derived class
+  int32_t e, Sw, Wn, uid_u, uid_w, ident;
+  int32_t st_q, st_r;  // a thread's stride (kFusedThreads ids) in (su, sw)
+  int32_t base, need;  // table owner and its entry count (pairs_done target)
+};
+
 struct EdgeDesc {
   int64_t aux_base;    // aux id of the edge's (0, 0)
   int64_t nb_u, nb_w;  // first aux node of the producer / consumer
@@ -257,11 +269,17 @@ __global__ void pair_rec_kernel(const SigDesc* __restrict__ sigs, const int32_t*
 // a build is one kernel node with no memset in front. Errors alternate
 // between two slots by launch parity: a launch writes err_c[parity] and
 // clears the other slot for the next one.
+// A counter alone on its 128-B line: the waiting CTAs poll these while the
+// warps bump them, and lines shared with other counters would queue all of
+// that traffic on one L2 slice.
+struct alignas(128) Line {
+  int v;
+  int pad[31];
+};
+
 struct Sched {
   unsigned long long err_c[2];  // ~(smallest error key); 0 = no error
-  int head;                  // next phase-2 block item
-  int unit_head;             // next phase-1 unit: node row, then class pair (chunk)
-  int node_done;             // node-class rows finished
+  int head;                  // unused
   int exit_count;            // CTAs done (the last one resets)
   int timeline;              // record the timestamps below
   int pad;
@@ -269,7 +287,9 @@ struct Sched {
   // node rows done, first pair done (min), pairs done, first fan-out tile
   // past its wait (min), kernel end
   unsigned long long t[6];
-  int pairs_done[2];         // per edge class (allocated to the class count)
+  Line unit_head;            // next phase-1 unit: node row, then class pair (chunk)
+  Line node_done;            // node-class rows finished
+  Line pairs_done[1];        // per edge class (allocated to the class count)
 };
 
 __device__ __forceinline__ void flag_error(unsigned long long* err, uint64_t key) {
@@ -309,8 +329,52 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // Spin (relaxed: an acquire load also invalidates the SM's L1, which the
 // other CTAs there are reading through) until *p >= v, then acquire once.
 __device__ __forceinline__ void wait_at_least(const int* p, int v) {
-  while (ld_relaxed(p) < v) __nanosleep(64);
+  for (unsigned ns = 64; ld_relaxed(p) < v; ns = ns < 512 ? 2 * ns : ns) __nanosleep(ns);
   (void)ld_acquire(p);
+}
+
+// Class-table entries are published without fences: a pair warp stores its
+// entry and bumps the class counter with a relaxed add; a fan-out range
+// waits for the counters of the classes it reads (node rows use a release). The counter may become visible before an entry's store, so entries
+// start as kUnset (a signalling NaN no arithmetic produces) and a reader that
+// finds kUnset retries until the store lands. (A CTA reaches phase 2 only
+// after the unit queue is drained, so every entry it may wait for belongs to
+// a running warp.) Two parity blocks of tables alternate between launches;
+// a launch refills the other one.
+constexpr unsigned long long kUnset = 0xfff4000000000badull;
+
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ double ld_acquire_f64(const double* p) {
+  double v;
+  asm volatile("ld.acquire.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// The retry is an acquire load: it also drops the SM's L1 lines, so the
+// stale copy that returned kUnset does not fail the next reads of its line.
+__device__ __forceinline__ double table_load(const double* p) {
+  double v = *p;
+  if (__double_as_longlong(v) != (long long)kUnset) return v;
+  v = ld_acquire_f64(p);
+  for (unsigned ns = 64; __double_as_longlong(v) == (long long)kUnset; ns = ns < 512 ? 2 * ns : ns) {
+    __nanosleep(ns);
+    v = ld_acquire_f64(p);
+  }
+  return v;
+}
+
+__global__ void fill_kernel(double* __restrict__ p, int64_t n, unsigned long long bits) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = __longlong_as_double((long long)bits);
+}
+
+__device__ __forceinline__ void red_relaxed_add(int* p, int v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" : : "l"(p), "r"(v) : "memory");
 }
 
 struct FusedArgs {
@@ -333,16 +397,23 @@ struct FusedArgs {
   int nsigs;
   const int32_t* pair_sig;  // edge class of every table entry
   const PairRec* pairs;     // per table entry
+  unsigned* pair_prof;      // timeline: per entry clocks of the pricing sections
+  unsigned* warp_exit;      // timeline: globaltimer (low bits) when each warp leaves phase 1
   const int32_t* row_cls;   // node class of every class row
   const int32_t* maps;
 
   int64_t total_pairs;
   const double* overrides;
   const tpk::SideDesc* sides;
-  double* r_sec;
+  double* r_sec;       // this launch's class tables (parity buffer), kUnset-filled
+  double* next_tables; // the other parity's block (all tables), refilled during this launch
+  int64_t tables_len;  // doubles per parity block
   double* r_vol;
   // fan-out
   const EdgeDesc* edges;  // graph edges, by id
+  const FanSeg* fsegs;    // per graph edge
+  const int32_t* range_first;   // first edge of every edge range
+  const int32_t* nrange_first;  // first operator of every node range
   int e0, e1;             // the execute's edge range
   int64_t A0, A1;         // its aux ids
   int64_t range_len;      // aux edges per fan-out item
@@ -359,8 +430,7 @@ struct FusedArgs {
   double* n_sec;
   double* n_vol;
   double* n_mem;
-  // phase-2 block items: [0, i_exp) node ranges (need only the node rows,
-  // which finish long before the class tables), [i_exp, i_end) edge ranges
+  // phase-2 items: [0, i_exp) node ranges, [i_exp, i_end) edge ranges
   int i_exp, i_end;
   int warp_form;  // pairs: 1 = warp per pair, 0 = thread per pair
   // shared
@@ -374,7 +444,6 @@ struct FusedArgs {
   unsigned long long* err;  // this launch's error slot
   int parity;               // of the launch (error slot)
   int nsigs_reset;          // pairs_done counters the last CTA zeroes
-  int dbg;
 };
 
 constexpr int kFusedThreads = 256;
@@ -495,7 +564,8 @@ __device__ void pair_warp(const FusedArgs& a, int64_t idx, const double* price) 
     we.env = a.env;
     we.l_log2 = a.l_log2;
     we.tab = tpk::PriceTabs{price, price + tpk::kBwTab};
-    const int st = tpk::redist_cost_warp(R, &pr->F, &pr->T, pr->dt, pr->bytes, we, sec, vol, nullptr);
+    const int st = tpk::redist_cost_warp(R, &pr->F, &pr->T, pr->dt, pr->bytes, we, sec, vol, nullptr,
+                                         a.pair_prof ? a.pair_prof + 8 * idx : nullptr);
     if (st) {
       if (lane == 0)
         flag_error(a.err, ekey(kEdgePhase + (uint64_t)(a.sigs[pr->sig].first_aux + pr->local) * 2 + 1, st));
@@ -517,53 +587,32 @@ __device__ void pair_warp(const FusedArgs& a, int64_t idx, const double* price) 
 // row + table entry (aux_graph.hpp:286-295). Consecutive lanes write
 // consecutive ids, so every warp store is one 256-B segment per array.
 constexpr int kSegs = 32;  // one per lane of warp 0
-struct FanSeg {
-  int64_t begin, end;  // aux ids of the edge
-  int64_t pb, wrow;    // its class table, consumer class row of sw = 0
-  int64_t nb_u, nb_w;  // records only
-  double f;            // exact factor of a derived class
-  int32_t e, Sw, Wn, uid_u, uid_w, ident;
-  int32_t st_q, st_r;  // a thread's stride (kFusedThreads ids) in (su, sw)
-};
 
 __device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n, int* s_edge) {
   const unsigned long long t0 = a.fan_ns ? gtimer() : 0;
   const int64_t start = a.A0 + (int64_t)item * a.range_len;
   const int64_t end = min(start + a.range_len, a.A1);
   const int lane = threadIdx.x & 31;
-  if (threadIdx.x < 32) {  // last edge with aux_base <= start: 32-ary search
-    int lo = a.e0, hi = a.e1 - 1;
-    while (lo < hi) {
-      const int step = (hi - lo + 32) / 32;
-      const int idx = lo + lane * step;
-      const unsigned ok = __ballot_sync(0xffffffffu, idx <= hi && a.edges[idx].aux_base <= start);
-      lo += (31 - __clz(ok)) * step;  // lane 0 always holds (invariant)
-      hi = min(hi, lo + step - 1);
-    }
-    if (lane == 0) *s_edge = lo;
-  }
+  if (threadIdx.x == 0) *s_edge = a.range_first[item];  // host-computed
   int64_t pos = start;
   bool first = true;
   while (pos < end) {
     __syncthreads();
     if (threadIdx.x < 32) {  // warp 0 stages the next kSegs edges, lane per edge
       const int e = *s_edge + lane;
-      const bool in = e < a.e1 && a.edges[e].aux_base < end;
-      if (in) {
-        const EdgeDesc ed = a.edges[e];
-        const int64_t eend = e + 1 < a.e1 ? a.edges[e + 1].aux_base : a.A1;
-        const SigDesc& sg = a.sigs[ed.sig];
-        wait_at_least(&a.sched->pairs_done[sg.base], sg.Un * sg.Wn);
-        seg[lane] = FanSeg{ed.aux_base, eend, sg.pair_begin, ed.wrow, ed.nb_u, ed.nb_w, sg.scale,
-                           ed.e, sg.Sw, sg.Wn, sg.uid_u, sg.uid_w, sg.ident,
-                           kFusedThreads / sg.Sw, kFusedThreads % sg.Sw};
+      FanSeg g;
+      bool in = false;
+      if (e < a.e1) {
+        g = a.fsegs[e];
+        in = g.begin < end;
       }
-      if (a.dbg == 2 && first)
-        for (int c = lane; c < a.nsigs; c += 32)
-          if (a.sigs[c].base == c) wait_at_least(&a.sched->pairs_done[c], a.sigs[c].Un * a.sigs[c].Wn);
+      if (in) {
+        wait_at_least(&a.sched->pairs_done[g.base].v, g.need);
+        seg[lane] = g;
+      }
       const int n = __popc(__ballot_sync(0xffffffffu, in));  // a prefix of the lanes
       if (first) {
-        if (lane == 0) wait_at_least(&a.sched->node_done, (int)a.total_rows);
+        if (lane == 0) wait_at_least(&a.sched->node_done.v, (int)a.total_rows);
         __syncwarp();
       }
       if (lane == 0) {
@@ -613,13 +662,12 @@ __device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n
         const int64_t r = g.ident ? g.pb + j : g.pb + (int64_t)a.maps[g.uid_u + su] * g.Wn + a.maps[g.uid_w + sw];
         // class rows and tables: written before the acquire above, reused
         // across the range's ids (L1)
-        if (a.dbg == 1) {
-          cs[k] = (double)r; vs[k] = (double)sw; ms[k] = g.f;
-        } else {
-        cs[k] = a.cls_sec[g.wrow + sw] + a.r_sec[r] * g.f;  // aux_graph.hpp:290-291
-        vs[k] = a.cls_vol[g.wrow + sw] + a.r_vol[r] * g.f;
-        ms[k] = a.cls_memdiv[g.wrow + sw];                 // :292
-        }
+        // class rows (released, acquired above) and tables: reused across
+        // the range's ids, through L1
+        const int64_t row = g.wrow + sw;
+        cs[k] = a.cls_sec[row] + table_load(a.r_sec + r) * g.f;  // aux_graph.hpp:290-291
+        vs[k] = a.cls_vol[row] + table_load(a.r_vol + r) * g.f;
+        ms[k] = a.cls_memdiv[row];                               // :292
         q[k] = o - a.A0;
         if (a.records) {  // topoplan::AuxEdge, 40 bytes (aux_graph.hpp:52-59)
           char* rec = a.records + q[k] * 40;
@@ -668,19 +716,9 @@ __device__ void node_range(const FusedArgs& a, int item, NodeSeg* seg, int* s_n,
   const int64_t start = (int64_t)item * a.node_range_len;
   const int64_t end = min(start + a.node_range_len, a.num_nodes);
   const int lane = threadIdx.x & 31;
-  if (threadIdx.x < 32) {  // last operator with node_base <= start
-    int lo = 0, hi = a.nops - 1;
-    while (lo < hi) {
-      const int step = (hi - lo + 32) / 32;
-      const int idx = lo + lane * step;
-      const unsigned ok = __ballot_sync(0xffffffffu, idx <= hi && a.op_node[idx] <= start);
-      lo += (31 - __clz(ok)) * step;
-      hi = min(hi, lo + step - 1);
-    }
-    if (lane == 0) {
-      *s_op = lo;
-      wait_at_least(&a.sched->node_done, (int)a.total_rows);
-    }
+  if (threadIdx.x == 0) {
+    *s_op = a.nrange_first[item];  // host-computed
+    wait_at_least(&a.sched->node_done.v, (int)a.total_rows);
   }
   int64_t pos = start;
   while (pos < end) {
@@ -750,7 +788,7 @@ __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
   const int64_t units = a.total_rows + pair_units;
   if (threadIdx.x == 0) {
     stamp(a.sched, 0, true);
-    s_unit = atomicAdd(&a.sched->unit_head, kFusedThreads / 32);
+    s_unit = atomicAdd(&a.sched->unit_head.v, kFusedThreads / 32);
   }
   if (a.total_pairs > 0)
     for (int i = threadIdx.x; i < tpk::kBwTab + tpk::kScaleDim * tpk::kScaleDim; i += kFusedThreads)
@@ -763,11 +801,11 @@ __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
     if (u < a.total_rows) {
       node_row(a, u);
       if (lane == 0) {
+        red_release_add(&a.sched->node_done.v, 1);  // rows: off the critical path, released
         if (a.item_ns) {
           a.item_ns[2 * u] = (unsigned)t0;
           a.item_ns[2 * u + 1] = (unsigned)(gtimer() - t0);
         }
-        red_release_add(&a.sched->node_done, 1);
       }
     } else if (kWarpForm) {
       const int64_t idx = u - a.total_rows;
@@ -778,8 +816,7 @@ __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
           a.pair_ns[2 * idx] = (unsigned)t0;
           a.pair_ns[2 * idx + 1] = (unsigned)(gtimer() - t0);
         }
-        if (a.dbg == 3) atomicAdd(&a.sched->pairs_done[sig], 1);
-        else red_release_add(&a.sched->pairs_done[sig], 1);  // lane 0 wrote the entry
+        red_relaxed_add(&a.sched->pairs_done[sig].v, 1);  // no fence: see table_load
       }
     } else {
       const int64_t idx = (u - a.total_rows) * 32 + lane;
@@ -790,22 +827,26 @@ __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
         a.pair_ns[2 * idx] = (unsigned)t0;
         a.pair_ns[2 * idx + 1] = (unsigned)(gtimer() - t0);
       }
-      __threadfence();
-      // one counter update per (warp, edge class)
+      // one counter update per (warp, edge class); no fence: see table_load
       const unsigned grp = __match_any_sync(0xffffffffu, sig);
-      if (valid && lane == __ffs(grp) - 1) atomicAdd(&a.sched->pairs_done[sig], __popc(grp));
+      if (valid && lane == __ffs(grp) - 1) red_relaxed_add(&a.sched->pairs_done[sig].v, __popc(grp));
     }
     int next = 0;
     if (lane == 0)
-      next = ld_relaxed(&a.sched->unit_head) >= units ? INT_MAX : atomicAdd(&a.sched->unit_head, 1);
+      next = ld_relaxed(&a.sched->unit_head.v) >= units ? INT_MAX : atomicAdd(&a.sched->unit_head.v, 1);
     u = __shfl_sync(0xffffffffu, next, 0);
   }
-  // phase 2: fan-out tiles and node fan-out
-  for (;;) {
-    __syncthreads();  // s_item / s_seg reuse
-    if (threadIdx.x == 0) s_item = atomicAdd(&a.sched->head, 1);
-    __syncthreads();
-    const int item = s_item;
+  if (a.warp_exit && lane == 0) a.warp_exit[blockIdx.x * (kFusedThreads / 32) + (threadIdx.x >> 5)] = (unsigned)gtimer();
+  // the next launch's tables start unset: every CTA refills a slice
+  {
+    const int64_t per = (a.tables_len + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = (int64_t)blockIdx.x * per, b1 = min(b0 + per, a.tables_len);
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += kFusedThreads)
+      a.next_tables[i] = __longlong_as_double((long long)kUnset);
+  }
+  // phase 2: node ranges, then edge ranges; CTA b takes items b, b + grid, ...
+  for (int item = blockIdx.x;; item += gridDim.x) {
+    __syncthreads();  // s_seg reuse
     if (item >= a.i_end) {
       if (threadIdx.x == 0) {
         stamp(a.sched, 5, false);
@@ -814,9 +855,9 @@ __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
           // every other CTA has finished: reset for the next launch
           Sched* sc = a.sched;
           sc->head = 0;
-          sc->unit_head = 0;
-          sc->node_done = 0;
-          for (int i = 0; i < a.nsigs_reset; ++i) sc->pairs_done[i] = 0;
+          sc->unit_head.v = 0;
+          sc->node_done.v = 0;
+          for (int i = 0; i < a.nsigs_reset; ++i) sc->pairs_done[i].v = 0;
           sc->err_c[a.parity ^ 1] = 0;
           sc->exit_count = 0;
           __threadfence();
@@ -945,8 +986,8 @@ struct Arena {
   int device = 0;
   cudaStream_t stream = nullptr;
   DevBuf d_tabs, d_tables, d_classes, d_chks, d_slots, d_occs, d_members, d_sigs, d_edges,
-      d_over, d_rsec, d_rvol, d_csec, d_cvol, d_cmem, d_cmem0, d_opnode, d_oprow, d_rowbase, d_sched, d_sidejobs,
-      d_sides, d_price, d_pairsigs, d_trace, d_maps, d_rowcls, d_pairrec;
+      d_over, d_tables2, d_opnode, d_oprow, d_rowbase, d_sched, d_sidejobs,
+      d_sides, d_price, d_pairsigs, d_trace, d_maps, d_rowcls, d_pairrec, d_prof, d_fsegs, d_rfirst;
   DevBuf out[9];  // one-shot staging of the requested outputs
   bool sched_clean = false;  // Sched zero (set up, or left so by the last launch)
   bool timeline_set = false;
@@ -954,8 +995,7 @@ struct Arena {
   std::vector<std::array<int64_t, 4>> table_key;  // (offset, count, p, n) of the resident tables
   void release() {
     for (DevBuf* b : {&d_tabs, &d_tables, &d_classes, &d_chks, &d_slots, &d_occs, &d_members, &d_sigs,
-                      &d_edges, &d_over, &d_rsec, &d_rvol, &d_csec, &d_cvol, &d_cmem,
-                      &d_cmem0, &d_opnode, &d_oprow, &d_rowbase, &d_sched, &d_sidejobs, &d_sides, &d_price, &d_pairsigs, &d_trace, &d_maps, &d_rowcls, &d_pairrec})
+                      &d_edges, &d_over, &d_tables2, &d_opnode, &d_oprow, &d_rowbase, &d_sched, &d_sidejobs, &d_sides, &d_price, &d_pairsigs, &d_trace, &d_maps, &d_rowcls, &d_pairrec, &d_prof, &d_fsegs, &d_rfirst})
       b->release();
     for (auto& b : out) b.release();
     table_key.clear();
@@ -996,7 +1036,10 @@ struct tp_plan {
   std::vector<double> overrides;   // per pair; empty if no class needs one
   std::vector<int32_t> pair_sig;   // edge class of every table entry
   std::vector<int32_t> row_cls;    // node class of every class row
-  std::vector<int32_t> maps;       // SigDesc uid_* / rep_* / mb_* / ml_* arrays
+  std::vector<int32_t> maps;       // SigDesc uid_* / rep_* arrays
+  std::vector<FanSeg> fsegs;       // per valid graph edge
+  std::vector<int32_t> range_first;   // per execute: first edge of every edge range,
+  std::array<int64_t, 4> range_key{{-1, -1, -1, -1}};  // then first op of every node range
   int64_t total_pairs = 0;
   int64_t h2d_bytes = 0;
   bool uploaded = false;
@@ -1008,6 +1051,7 @@ struct tp_plan {
   cudaEvent_t prof_start = nullptr, prof_stop = nullptr;  // recorded around K2
   bool timeline = false;
   int last_parity = -1;  // error slot of the last launch (-1: none)
+  int64_t last_grid = 0;
   int64_t trace_n[3] = {0, 0, 0};  // pairs, node-row items, fan-out items traced
   int pair_form = 0;  // 0 = by size, 1 = warp per pair, 2 = thread per pair
   int resident_blocks = 0;  // persistent grid size (SMs x resident CTAs)
@@ -1306,6 +1350,31 @@ struct Builder {
     st = memo_aliasing();
     if (st) return st;
     layout_tables(p.overrides.empty());
+    p.fsegs.clear();
+    for (size_t e = 0; e < p.edges.size(); ++e) {
+      const EdgeDesc& ed = p.edges[e];
+      const SigDesc& sg = p.sigs[ed.sig];
+      const SigDesc& bs = p.sigs[sg.base];
+      FanSeg f{};
+      f.begin = ed.aux_base;
+      f.end = p.edge_base[e + 1];
+      f.pb = sg.pair_begin;
+      f.wrow = ed.wrow;
+      f.nb_u = ed.nb_u;
+      f.nb_w = ed.nb_w;
+      f.f = sg.scale;
+      f.e = ed.e;
+      f.Sw = sg.Sw;
+      f.Wn = sg.Wn;
+      f.uid_u = sg.uid_u;
+      f.uid_w = sg.uid_w;
+      f.ident = sg.ident;
+      f.st_q = kFusedThreads / sg.Sw;
+      f.st_r = kFusedThreads % sg.Sw;
+      f.base = sg.base;
+      f.need = bs.Un * bs.Wn;
+      p.fsegs.push_back(f);
+    }
     p.pair_sig.assign(p.total_pairs, 0);
     for (size_t c = 0; c < p.sigs.size(); ++c)
       if (p.sigs[c].base == (int32_t)c)
@@ -1699,6 +1768,9 @@ tp_status tp_plan_index(const tp_plan* p, tp_aux_index* x) {
   return TP_OK;
 }
 
+// doubles per parity block of the published tables
+static int64_t tables_len(const tp_plan* p) { return 2 * (p->total_pairs + 1) + 4 * (p->total_rows + 1); }
+
 tp_status tp_plan_upload(tp_plan* p, void* stream) {
   if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
   tp_status st = ensure_stream(p);
@@ -1742,6 +1814,8 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
   CUDA_TRY(upload(A.d_rowcls, p->row_cls, s));
   CUDA_TRY(upload(A.d_maps, p->maps, s));
   CUDA_TRY(upload(A.d_edges, p->edges, s));
+  CUDA_TRY(upload(A.d_fsegs, p->fsegs, s));
+  p->range_key = {{-1, -1, -1, -1}};
   CUDA_TRY(upload(A.d_over, p->overrides, s));
   CUDA_TRY(A.d_pairrec.ensure(sizeof(PairRec) * (p->total_pairs + 1)));
   if (p->total_pairs > 0) {
@@ -1750,13 +1824,9 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
         (const tpk::SideDesc*)A.d_sides.p, (const double*)A.d_over.p, p->total_pairs, (PairRec*)A.d_pairrec.p);
     CUDA_TRY(cudaGetLastError());
   }
-  CUDA_TRY(A.d_rsec.ensure(sizeof(double) * (p->total_pairs + 1)));
-  CUDA_TRY(A.d_rvol.ensure(sizeof(double) * (p->total_pairs + 1)));
-  CUDA_TRY(A.d_csec.ensure(sizeof(double) * (p->total_rows + 1)));
-  CUDA_TRY(A.d_cvol.ensure(sizeof(double) * (p->total_rows + 1)));
-  CUDA_TRY(A.d_cmem.ensure(sizeof(double) * (p->total_rows + 1)));
-  CUDA_TRY(A.d_cmem0.ensure(sizeof(double) * (p->total_rows + 1)));
-  CUDA_TRY(A.d_sched.ensure(sizeof(Sched) + sizeof(int) * (p->sigs.size() + 2)));
+  // per parity: r_sec, r_vol [total_pairs]; cls_sec, cls_vol, cls_mem, cls_memdiv [total_rows]
+  CUDA_TRY(A.d_tables2.ensure(sizeof(double) * 2 * tables_len(p)));
+  CUDA_TRY(A.d_sched.ensure(sizeof(Sched) + sizeof(Line) * (p->sigs.size() + 1)));
   A.sched_clean = false;
   p->uploaded = true;
   return TP_OK;
@@ -1784,7 +1854,9 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   int64_t launches = 0;
   Sched* sched = (Sched*)A.d_sched.p;
   if (!A.sched_clean) {
-    CUDA_TRY(cudaMemsetAsync(sched, 0, sizeof(Sched) + sizeof(int) * (p->sigs.size() + 2), s));
+    CUDA_TRY(cudaMemsetAsync(sched, 0, sizeof(Sched) + sizeof(Line) * (p->sigs.size() + 1), s));
+    fill_kernel<<<64, 256, 0, s>>>((double*)A.d_tables2.p, 2 * tables_len(p), kUnset);  // both parities
+    CUDA_TRY(cudaGetLastError());
     A.sched_clean = true;
     A.parity = 0;
   }
@@ -1821,6 +1893,22 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
       std::max<int64_t>(kFusedThreads * kFanPer, (total_out + total_nodes + nranges - 1) / nranges);
   const int64_t exp_items = (total_out + range_len - 1) / range_len;
   const int64_t nfan_items = (total_nodes + range_len - 1) / range_len;
+  const std::array<int64_t, 4> rkey{{e0, e1, range_len, nfan_items}};
+  if (p->range_key != rkey) {  // first edge / operator of every range (cached)
+    p->range_first.assign(exp_items + nfan_items, 0);
+    for (int64_t r = 0; r < exp_items; ++r) {
+      const int64_t start = out_offset + r * range_len;
+      auto it = std::upper_bound(p->edge_base.begin() + e0, p->edge_base.begin() + e1, start);
+      p->range_first[r] = (int32_t)(it - p->edge_base.begin()) - 1;
+    }
+    for (int64_t r = 0; r < nfan_items; ++r) {
+      const int64_t start = r * range_len;
+      auto it = std::upper_bound(p->node_base.begin(), p->node_base.begin() + p->num_ops, start);
+      p->range_first[exp_items + r] = (int32_t)(it - p->node_base.begin()) - 1;
+    }
+    CUDA_TRY(upload(A.d_rfirst, p->range_first, s));
+    p->range_key = rkey;
+  }
   FusedArgs a{};
   a.classes = (const ClassDesc*)A.d_classes.p;
   a.ncls = (int)p->classes.size();
@@ -1828,10 +1916,18 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   a.chks = (const SliceChk*)A.d_chks.p;
   a.slots = (const SlotDesc*)A.d_slots.p;
   a.occs = (const Occ*)A.d_occs.p;
-  a.cls_sec = (double*)A.d_csec.p;
-  a.cls_vol = (double*)A.d_cvol.p;
-  a.cls_mem = (double*)A.d_cmem0.p;
-  a.cls_memdiv = (double*)A.d_cmem.p;
+  {
+    const int64_t L = tables_len(p), P = p->total_pairs + 1, R = p->total_rows + 1;
+    double* t = (double*)A.d_tables2.p + A.parity * L;
+    a.r_sec = t;
+    a.r_vol = t + P;
+    a.cls_sec = t + 2 * P;
+    a.cls_vol = t + 2 * P + R;
+    a.cls_mem = t + 2 * P + 2 * R;
+    a.cls_memdiv = t + 2 * P + 3 * R;
+    a.next_tables = (double*)A.d_tables2.p + (A.parity ^ 1) * L;
+    a.tables_len = L;
+  }
   a.sigs = (const SigDesc*)A.d_sigs.p;
   a.nsigs = (int)p->sigs.size();
   a.pair_sig = (const int32_t*)A.d_pairsigs.p;
@@ -1842,9 +1938,11 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   a.total_pairs = edge_phase ? p->total_pairs : 0;
   a.overrides = (const double*)A.d_over.p;
   a.sides = (const tpk::SideDesc*)A.d_sides.p;
-  a.r_sec = (double*)A.d_rsec.p;
-  a.r_vol = (double*)A.d_rvol.p;
+
   a.edges = (const EdgeDesc*)A.d_edges.p;
+  a.fsegs = (const FanSeg*)A.d_fsegs.p;
+  a.range_first = (const int32_t*)A.d_rfirst.p;
+  a.nrange_first = a.range_first + exp_items;
   a.e0 = e0;
   a.e1 = e1;
   a.A0 = out_offset;
@@ -1873,7 +1971,6 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   a.parity = A.parity;
   a.err = &sched->err_c[A.parity];
   a.nsigs_reset = (int)p->sigs.size();
-  { static const int d = getenv("TP_DBG") ? atoi(getenv("TP_DBG")) : 0; a.dbg = d; }
   if (p->timeline) {
     p->trace_n[0] = p->total_pairs;
     p->trace_n[1] = p->total_rows;
@@ -1884,10 +1981,15 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
     a.pair_ns = (unsigned*)A.d_trace.p;
     a.item_ns = a.pair_ns + 2 * p->trace_n[0];
     a.fan_ns = a.item_ns + 2 * p->trace_n[1];
+    const size_t nprof = 8 * (p->total_pairs + 1) + 8 * 4096;
+    CUDA_TRY(A.d_prof.ensure(sizeof(unsigned) * nprof));
+    CUDA_TRY(cudaMemsetAsync(A.d_prof.p, 0, sizeof(unsigned) * nprof, s));
+    a.pair_prof = (unsigned*)A.d_prof.p;
+    a.warp_exit = a.pair_prof + 8 * (p->total_pairs + 1);
   }
   a.warp_form = p->pair_form == 1 || (p->pair_form == 0 && a.total_pairs <= kWarpPairLimit);
   // phase-1 units: node rows, then class pairs (warp form) or 32-pair chunks;
-  // phase-2 block items: [0, i_exp) node fan-out, [i_exp, i_end) fan-out ranges
+  // phase-2 items: node ranges, then edge ranges
   const int64_t units = p->total_rows + (a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32);
   const int64_t total_items = exp_items + nfan_items;
   if (total_items >= (1ll << 30) || units >= (1ll << 30))
@@ -1902,6 +2004,7 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
     else fused_kernel<false><<<(unsigned)grid, kFusedThreads, 0, s>>>(a);
     if (cudaPeekAtLastError() != cudaSuccess) A.sched_clean = false;
     p->last_parity = A.parity;
+    p->last_grid = grid;
     A.parity ^= 1;
     ++launches;
     if (p->prof_stop) CUDA_TRY(cudaEventRecord(p->prof_stop, s));
@@ -1917,8 +2020,8 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
       const int th = 256;
       rowmin_kernel<<<(unsigned)((rows * 32 + th - 1) / th), th, 0, s>>>(
           (const EdgeDesc*)A.d_edges.p, (const int64_t*)A.d_rowbase.p, e0, e1 - e0, rows,
-          (const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_maps.p, (const double*)A.d_rsec.p, (const double*)A.d_rvol.p,
-          (const double*)A.d_csec.p, (const double*)A.d_cvol.p, out->row_min_cost_s, out->row_min_volume_bytes);
+          (const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_maps.p, a.r_sec, a.r_vol,
+          a.cls_sec, a.cls_vol, out->row_min_cost_s, out->row_min_volume_bytes);
       ++launches;
     }
   }
@@ -1965,7 +2068,36 @@ tp_status tp_plan_timeline(tp_plan* p, int64_t* ns_out) {
 }
 
 tp_status tp_plan_timeline_detail(tp_plan* p, int32_t section, uint32_t* out, int64_t* count) {
-  if (!p || !count || section < 0 || section > 2) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "bad argument");
+  if (!p || !count || section < 0 || section > 4) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "bad argument");
+  if (section == 4) {  // phase-1 exit of every warp of the last launch (ns after kernel start)
+    if (!p->timeline || !p->arena || !p->arena->d_prof.p)
+      return set_err(TP_ERR_INVALID_ARGUMENT, 0, "timeline not recorded");
+    if (!out) {
+      *count = p->last_grid * (kFusedThreads / 32);
+      return TP_OK;
+    }
+    CUDA_TRY(cudaSetDevice(p->device));
+    CUDA_TRY(cudaStreamSynchronize(p->last_stream));
+    unsigned long long t0 = 0;
+    CUDA_TRY(cudaMemcpy(&t0, &((Sched*)p->arena->d_sched.p)->t[0], sizeof(t0), cudaMemcpyDeviceToHost));
+    t0 = ~t0;
+    CUDA_TRY(cudaMemcpy(out, (const unsigned*)p->arena->d_prof.p + 8 * (p->total_pairs + 1),
+                        sizeof(unsigned) * *count, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < *count; ++i) out[i] -= (unsigned)t0;
+    return TP_OK;
+  }
+  if (section == 3) {  // pricing-section clocks per class pair (warp form), 8 values each
+    if (!p->timeline || !p->arena || !p->arena->d_prof.p)
+      return set_err(TP_ERR_INVALID_ARGUMENT, 0, "timeline not recorded");
+    if (!out) {
+      *count = p->total_pairs;
+      return TP_OK;
+    }
+    CUDA_TRY(cudaSetDevice(p->device));
+    CUDA_TRY(cudaStreamSynchronize(p->last_stream));
+    if (*count) CUDA_TRY(cudaMemcpy(out, p->arena->d_prof.p, sizeof(unsigned) * 8 * *count, cudaMemcpyDeviceToHost));
+    return TP_OK;
+  }
   if (!p->timeline || !p->arena || !p->arena->d_trace.p)
     return set_err(TP_ERR_INVALID_ARGUMENT, 0, "timeline not recorded");
   const int64_t n[3] = {p->trace_n[0], p->trace_n[1], p->trace_n[2]};

@@ -120,9 +120,12 @@ __device__ __forceinline__ double price_op_warp(bool a2a, int te, int rexp, int 
 // Returns the tp_error_kind; sec/vol are valid on every lane. `tr`
 // (verification export only) is written by lane 0.
 __device__ int redist_cost_warp(int R, const SideDesc* pf, const SideDesc* pt, const DimT* dt, double bytes,
-                                const WarpEnv& we, double& sec_out, double& vol_out, Trace* tr) {
+                                const WarpEnv& we, double& sec_out, double& vol_out, Trace* tr,
+                                unsigned* prof = nullptr) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+  const long long c_start = prof ? clock64() : 0;
+  int rounds = 0;
   if (R < 0 || R > kMaxR) return kCapacity;
   const int n = pf->n;
   if (n != pt->n) return kNotUnifiable;  // redistribution.hpp:264-268
@@ -148,8 +151,10 @@ __device__ int redist_cost_warp(int R, const SideDesc* pf, const SideDesc* pt, c
     const bool changed = __any_sync(FULL, nP != P) || nD != D;
     P = nP;
     D = nD;
+    ++rounds;
     if (!changed) break;
   }
+  const long long c_closure = prof ? clock64() : 0;
   // ---- unified device dims: lane k <- (log2 extent, lower position) ----
   int my_ext = 0, my_pos = n, next = 0;
   if (n > 0) {
@@ -219,6 +224,7 @@ __device__ int redist_cost_warp(int R, const SideDesc* pf, const SideDesc* pt, c
       tr->nops = 0;
     }
   }
+  const long long c_axes = prof ? clock64() : 0;
   // ---- sequence inference with on-the-fly pricing (:419-451) ----
   uint32_t PM = __reduce_or_sync(FULL, my_w >= 0 ? (1u << my_w) : 0u);
   const int ext_w = __shfl_sync(FULL, my_ext, my_w >= 0 ? my_w : 0);
@@ -249,47 +255,90 @@ __device__ int redist_cost_warp(int R, const SideDesc* pf, const SideDesc* pt, c
     const int held = (int)__reduce_add_sync(FULL, (unsigned)((lane < k && ((PM >> lane) & 1u)) ? my_ext : 0));
     return te - held;
   };
+  // Priced ops. With a trace they are priced on the spot. Otherwise op t is
+  // parked on lane t and a batch is priced by all lanes at once -- the fp64
+  // chains of up to 32 ops overlap -- then summed in op order, the same
+  // additions as pricing each op in turn (the search never reads sec/vol).
+  int nb = 0;
+  int b_te = 0, b_rexp = 0, b_ek = 0, b_s = 0;
+  bool b_a2a = false;
+  auto flush = [&]() {
+    double c = 0, v = 0;
+    if (lane < nb) {
+      int64_t ct = 0;
+      c = price_op_warp(b_a2a, b_te, b_rexp, b_ek, b_s, bytes, we, &v, &ct);  // v = 0 + op volume
+    }
+    for (int t = 0; t < nb; ++t) {
+      vol += __shfl_sync(FULL, v, t);
+      sec += __shfl_sync(FULL, c, t);
+    }
+    nb = 0;
+  };
+  auto op = [&](bool a2a_op, int te, int rexp, int ek, int k, int i, int j, int fb) {
+    if (tr) {
+      int64_t ct = 0;
+      const double c = price_op_warp(a2a_op, te, rexp, ek, s, bytes, we, &vol, &ct);
+      sec += c;
+      record(a2a_op ? 2 : 1, k, i, j, fb, ct, c);
+      return;
+    }
+    if (lane == nb) {
+      b_te = te;
+      b_rexp = rexp;
+      b_ek = ek;
+      b_s = s;
+      b_a2a = a2a_op;
+    }
+    ++nops;
+    if (++nb == 32) flush();
+  };
   while (mism) {
     if (--guard < 0) return kNoTerminate;
     bool progress = true;
     while (progress) {
-      // InferSlice (:350-365), positions ascending
+      // InferSlice (:350-365). The to-map's device dims are distinct, so
+      // the slices of one pass never conflict and commute (a slice prices
+      // nothing): they are applied together; the trace lists them in
+      // position order like the reference.
       progress = false;
-      uint32_t cand = __ballot_sync(FULL, my_w == -1 && my_to >= 0 && !((PM >> (my_to & 31)) & 1u));
-      while (cand) {
-        const int i = ffs32(cand);
-        cand &= cand - 1;
-        const int k = __shfl_sync(FULL, my_to, i);
-        if ((PM >> k) & 1u) continue;  // an earlier slice of this pass took k
-        record(0, k, i, -1, 0, 0, 0.0);
-        if (lane == i) my_w = k;
-        PM |= 1u << k;
-        s += __shfl_sync(FULL, my_ext, k);
+      const uint32_t cand = __ballot_sync(FULL, my_w == -1 && my_to >= 0 && !((PM >> (my_to & 31)) & 1u));
+      if (cand) {
+        if (tr) {
+          for (uint32_t c = cand; c; c &= c - 1) {
+            const int i = ffs32(c);
+            record(0, __shfl_sync(FULL, my_to, i), i, -1, 0, 0, 0.0);
+          }
+        } else {
+          nops += __popc(cand);
+        }
+        const bool me = (cand >> lane) & 1u;
+        const int ext_to = __shfl_sync(FULL, my_ext, my_to >= 0 ? my_to : 0);
+        PM |= __reduce_or_sync(FULL, me ? (1u << my_to) : 0u);
+        s += (int)__reduce_add_sync(FULL, me ? (unsigned)ext_to : 0u);
+        if (me) my_w = my_to;
         progress = true;
       }
-      // InferAll2All until none applies (:367-385); each candidate is
-      // re-checked against the state the earlier moves of the pass left
+      // InferAll2All until none applies (:367-385): a pass takes positions
+      // in ascending order, each checked against the state the earlier moves
+      // of the pass left. Lane i qualifies when it holds a dim k it must not
+      // keep and the position whose to-map is k holds nothing (free_to).
       bool a2a = true;
       while (a2a) {
         a2a = false;
-        uint32_t ca = __ballot_sync(FULL, my_w >= 0 && my_w != my_to);
-        while (ca) {
-          const int i = ffs32(ca);
-          ca &= ca - 1;
+        int cursor = -1;
+        for (;;) {
+          const uint32_t free_to = __reduce_or_sync(FULL, (my_to >= 0 && my_w == -1) ? (1u << my_to) : 0u);
+          const uint32_t ok = __ballot_sync(FULL, lane > cursor && my_w >= 0 && my_w != my_to &&
+                                                      ((free_to >> (my_w & 31)) & 1u));
+          if (!ok) break;
+          const int i = ffs32(ok);
           const int k = __shfl_sync(FULL, my_w, i);
-          const int ti = __shfl_sync(FULL, my_to, i);
-          if (k < 0 || ti == k) continue;
-          const uint32_t tk = __ballot_sync(FULL, my_to == k);
-          if (!tk) continue;
-          const int j = ffs32(tk);  // to.axis_of(k)
-          if (j == i || __shfl_sync(FULL, my_w, j) != -1) continue;
+          const int j = ffs32(__ballot_sync(FULL, my_to == k));  // to.axis_of(k)
           const int te = __shfl_sync(FULL, my_pos, k), ek = __shfl_sync(FULL, my_ext, k);
-          int64_t ct = 0;
-          const double c = price_op_warp(true, te, rexp_below(k, te), ek, s, bytes, we, &vol, &ct);
-          sec += c;
-          record(2, k, i, j, 0, ct, c);
+          op(true, te, rexp_below(k, te), ek, k, i, j, 0);
           if (lane == i) my_w = -1;
           if (lane == j) my_w = k;
+          cursor = i;
           a2a = true;
         }
         progress |= a2a;
@@ -308,17 +357,26 @@ __device__ int redist_cost_warp(int R, const SideDesc* pf, const SideDesc* pt, c
     const int i = ffs32(gm);
     const int k = __shfl_sync(FULL, my_w, i);
     const int te = __shfl_sync(FULL, my_pos, k), ek = __shfl_sync(FULL, my_ext, k);
-    int64_t ct = 0;
-    const double c = price_op_warp(false, te, rexp_below(k, te), ek, s, bytes, we, &vol, &ct);
-    sec += c;
-    record(1, k, i, -1, fb, ct, c);
+    op(false, te, rexp_below(k, te), ek, k, i, -1, fb);
     if (lane == i) my_w = -1;
     PM = __reduce_or_sync(FULL, my_w >= 0 ? (1u << my_w) : 0u);
     s -= ek;
     mism = __ballot_sync(FULL, my_w != my_to);
   }
+  flush();
   sec_out = sec;
   vol_out = vol;
+  if (prof && lane == 0) {
+    const long long c_end = clock64();
+    prof[0] = (unsigned)(c_closure - c_start);
+    prof[1] = (unsigned)(c_axes - c_closure);
+    prof[2] = (unsigned)(c_end - c_axes);
+    prof[3] = (unsigned)nops;
+    prof[4] = (unsigned)U;
+    prof[5] = (unsigned)next;
+    prof[6] = (unsigned)rounds;
+    prof[7] = 0;
+  }
   return kOk;
 }
 

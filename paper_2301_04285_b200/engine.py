@@ -160,7 +160,7 @@ class Plan:
         [start, wait, duration]."""
         import numpy as np
         res = []
-        for sec, w in ((0, 3), (1, 2), (2, 3)):
+        for sec, w in ((0, 3), (1, 2), (2, 3), (3, 8), (4, 1)):
             n = C.c_int64(0)
             _check(self.lib, self.lib.tp_plan_timeline_detail(self.handle, sec, None, C.byref(n)))
             v = np.zeros((n.value, w), np.uint32)

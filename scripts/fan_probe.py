@@ -32,9 +32,9 @@ with torch.cuda.stream(s):
     for i in range(4):
         flush.zero_()
         plan.execute(full, stream=s.cuda_stream)
-pr, it, fo = plan.timeline_detail()
+pr, it, fo, _, wx = plan.timeline_detail()
 q = lambda x: [round(float(np.percentile(x, p)) / 1e3, 1) for p in (0, 50, 90, 100)]
-print(f"dbg={os.environ.get("TP_DBG", "0")} build {v[len(v)//2]:.1f} us | pairs end {q(pr[:,0]+pr[:,1])} "
+print(f"build {v[len(v)//2]:.1f} us | pairs end {q(pr[:,0]+pr[:,1])} "
       f"rows end {q(it[:,0]+it[:,1])} | fan n={len(fo)} ready {q(fo[:,0]+fo[:,1])} work {q(fo[:,2]-fo[:,1])} end {q(fo[:,0]+fo[:,2])}")
 order = np.argsort(fo[:, 0] + fo[:, 1])[-8:]
 for i in order:
@@ -45,3 +45,16 @@ for i in order:
 for c in np.unique(pr[:, 2]):
     m = pr[:, 2] == c
     print(f"  class {c}: pairs {m.sum()}, dur us {q(pr[m, 1])}")
+pf = plan.timeline_detail()[3]
+print("pricing clocks per pair (closure, axes, inference) pct(0,50,90,100):")
+for c in np.unique(pr[:, 2]):
+    m = pr[:, 2] == c
+    print(f"  class {c}: closure {q(pf[m,0])} axes {q(pf[m,1])} infer {q(pf[m,2])} (k-clocks); ops {q(pf[m,3]*1000)} U {q(pf[m,4]*1000)} depth {q(pf[m,5]*1000)} rounds {q(pf[m,6]*1000)}")
+slow = np.argsort(pr[:, 1])[-5:]
+for i in slow:
+    print(f"  slow pair {i} class {pr[i,2]} dur {pr[i,1]/1e3:.1f}us clocks {list(pf[i,:3])} price {pf[i,7]} ops {pf[i,3]} U {pf[i,4]} depth {pf[i,5]} rounds {pf[i,6]}")
+wx = wx[:, 0]
+print("warp phase-1 exit us pct:", q(wx))
+order = np.argsort(fo[:, 0] + fo[:, 2])[-6:]
+for i in order:
+    print(f"  slowest-ending range {i}: start {fo[i,0]/1e3:.1f} wait {fo[i,1]/1e3:.1f} dur {fo[i,2]/1e3:.1f}")

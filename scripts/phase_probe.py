@@ -64,7 +64,7 @@ for form in (1, 2):
         for i in range(4):
             flush.zero_()
             plan.execute(full, stream=s.cuda_stream)
-    pr, it, fo = plan.timeline_detail()
+    pr, it, fo, _, _ = plan.timeline_detail()
     q = lambda v: [round(float(np.percentile(v, x)) / 1e3, 2) for x in (0, 10, 50, 90, 99, 100)] if len(v) else []
     print(f"form {form} pair dur us pct(0,10,50,90,99,100):", q(pr[:, 1]), "sum ms", pr[:, 1].sum() / 1e6)
     print(f"form {form} pair start us pct:", q(pr[:, 0]), " end:", q(pr[:, 0] + pr[:, 1]))
