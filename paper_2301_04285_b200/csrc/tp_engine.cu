@@ -328,8 +328,12 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 
 // Spin (relaxed: an acquire load also invalidates the SM's L1, which the
 // other CTAs there are reading through) until *p >= v, then acquire once.
-__device__ __forceinline__ void wait_at_least(const int* p, int v) {
+__device__ __forceinline__ void wait_relaxed(const int* p, int v) {
   for (unsigned ns = 64; ld_relaxed(p) < v; ns = ns < 512 ? 2 * ns : ns) __nanosleep(ns);
+}
+
+__device__ __forceinline__ void wait_at_least(const int* p, int v) {
+  wait_relaxed(p, v);
   (void)ld_acquire(p);
 }
 
@@ -357,6 +361,18 @@ __device__ __forceinline__ double ld_acquire_f64(const double* p) {
 
 // The retry is an acquire load: it also drops the SM's L1 lines, so the
 // stale copy that returned kUnset does not fail the next reads of its line.
+__device__ __forceinline__ double table_load(const double* p);
+
+// A (cost, volume) entry, written by one 16-B store.
+__device__ __forceinline__ double2 table_load2(const double2* p) {
+  double2 v = *p;
+  if (__double_as_longlong(v.x) == (long long)kUnset || __double_as_longlong(v.y) == (long long)kUnset) {
+    v.x = table_load(&p->x);
+    v.y = table_load(&p->y);
+  }
+  return v;
+}
+
 __device__ __forceinline__ double table_load(const double* p) {
   double v = *p;
   if (__double_as_longlong(v) != (long long)kUnset) return v;
@@ -385,8 +401,7 @@ struct FusedArgs {
   const SliceChk* chks;
   const SlotDesc* slots;
   const Occ* occs;
-  double* cls_sec;
-  double* cls_vol;
+  double2* cls_sv;     // node-class rows: (intra cost, intra volume)
   double* cls_mem;
   double* cls_memdiv;
   // edge classes
@@ -405,10 +420,9 @@ struct FusedArgs {
   int64_t total_pairs;
   const double* overrides;
   const tpk::SideDesc* sides;
-  double* r_sec;       // this launch's class tables (parity buffer), kUnset-filled
+  double2* r_tab;      // this launch's class tables (cost, volume) (parity buffer), kUnset-filled
   double* next_tables; // the other parity's block (all tables), refilled during this launch
   int64_t tables_len;  // doubles per parity block
-  double* r_vol;
   // fan-out
   const EdgeDesc* edges;  // graph edges, by id
   const FanSeg* fsegs;    // per graph edge
@@ -471,7 +485,8 @@ __device__ void node_row(const FusedArgs& a, int64_t row) {
     if (bad) {
       if (lane == __ffs(bad) - 1) {
         flag_error(a.err, ekey(1 + (uint64_t)(cd.first_node + s) * 2 + 1, kind));
-        a.cls_sec[row] = a.cls_vol[row] = a.cls_mem[row] = a.cls_memdiv[row] = 0;
+        a.cls_sv[row] = make_double2(0.0, 0.0);
+        a.cls_mem[row] = a.cls_memdiv[row] = 0;
       }
       return;
     }
@@ -526,8 +541,7 @@ __device__ void node_row(const FusedArgs& a, int64_t row) {
     }
   }
   if (lane == 0) {
-    a.cls_sec[row] = sec;
-    a.cls_vol[row] = vol;
+    a.cls_sv[row] = make_double2(sec, vol);
     a.cls_mem[row] = mem;
     a.cls_memdiv[row] = mem / cd.indeg;  // aux_graph.hpp:292
   }
@@ -549,8 +563,7 @@ __device__ void pair_thread(const FusedArgs& a, int64_t idx, const double* price
       sec = vol = 0;
     }
   }
-  a.r_sec[idx] = sec;
-  a.r_vol[idx] = vol;
+  a.r_tab[idx] = make_double2(sec, vol);
 }
 
 // One class-table entry on one warp (warp form, tp_warp.cuh); lane 0 writes.
@@ -573,8 +586,7 @@ __device__ void pair_warp(const FusedArgs& a, int64_t idx, const double* price) 
     }
   }
   if (lane == 0) {
-    a.r_sec[idx] = sec;
-    a.r_vol[idx] = vol;
+    a.r_tab[idx] = make_double2(sec, vol);  // one 16-B store
   }
 }
 
@@ -607,7 +619,9 @@ __device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n
         in = g.begin < end;
       }
       if (in) {
-        wait_at_least(&a.sched->pairs_done[g.base].v, g.need);
+        // relaxed: the entries are unset-checked; an acquire here would also
+        // drop the L1 lines the SM's other CTAs are reading
+        wait_relaxed(&a.sched->pairs_done[g.base].v, g.need);
         seg[lane] = g;
       }
       const int n = __popc(__ballot_sync(0xffffffffu, in));  // a prefix of the lanes
@@ -665,8 +679,10 @@ __device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n
         // class rows (released, acquired above) and tables: reused across
         // the range's ids, through L1
         const int64_t row = g.wrow + sw;
-        cs[k] = a.cls_sec[row] + table_load(a.r_sec + r) * g.f;  // aux_graph.hpp:290-291
-        vs[k] = a.cls_vol[row] + table_load(a.r_vol + r) * g.f;
+        const double2 cv = a.cls_sv[row];
+        const double2 rv = table_load2(a.r_tab + r);
+        cs[k] = cv.x + rv.x * g.f;  // aux_graph.hpp:290-291
+        vs[k] = cv.y + rv.y * g.f;
         ms[k] = a.cls_memdiv[row];                               // :292
         q[k] = o - a.A0;
         if (a.records) {  // topoplan::AuxEdge, 40 bytes (aux_graph.hpp:52-59)
@@ -746,8 +762,9 @@ __device__ void node_range(const FusedArgs& a, int item, NodeSeg* seg, int* s_n,
         if (o >= span_end) continue;
         while (o >= seg[si].end) ++si;
         const int64_t row = seg[si].row + (o - seg[si].begin);
-        cs[k] = a.cls_sec[row];
-        vs[k] = a.cls_vol[row];
+        const double2 cv = a.cls_sv[row];
+        cs[k] = cv.x;
+        vs[k] = cv.y;
         ms[k] = a.cls_mem[row];
         q[k] = o;
       }
@@ -874,8 +891,7 @@ __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
 __global__ void rowmin_kernel(const EdgeDesc* __restrict__ edges, const int64_t* __restrict__ row_base,
                               int e0, int nedges, int64_t nrows, const SigDesc* __restrict__ sigs,
                               const int32_t* __restrict__ maps,
-                              const double* __restrict__ r_sec, const double* __restrict__ r_vol,
-                              const double* __restrict__ cls_sec, const double* __restrict__ cls_vol,
+                              const double2* __restrict__ r_tab, const double2* __restrict__ cls_sv,
                               double* __restrict__ out_c, double* __restrict__ out_v) {
   const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -893,8 +909,9 @@ __global__ void rowmin_kernel(const EdgeDesc* __restrict__ edges, const int64_t*
   const int64_t rbase = sg.pair_begin + (int64_t)maps[sg.uid_u + su] * sg.Wn;
   for (int64_t sw = lane; sw < sg.Sw; sw += 32) {
     const int64_t j = rbase + maps[sg.uid_w + sw];
-    const double c = cls_sec[ed.wrow + sw] + r_sec[j] * sg.scale;
-    const double v = cls_vol[ed.wrow + sw] + r_vol[j] * sg.scale;
+    const double2 cv = cls_sv[ed.wrow + sw], rv = r_tab[j];
+    const double c = cv.x + rv.x * sg.scale;
+    const double v = cv.y + rv.y * sg.scale;
     mc = c < mc ? c : mc;
     mv = v < mv ? v : mv;
   }
@@ -1824,7 +1841,7 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
         (const tpk::SideDesc*)A.d_sides.p, (const double*)A.d_over.p, p->total_pairs, (PairRec*)A.d_pairrec.p);
     CUDA_TRY(cudaGetLastError());
   }
-  // per parity: r_sec, r_vol [total_pairs]; cls_sec, cls_vol, cls_mem, cls_memdiv [total_rows]
+  // per parity: (cost, volume) [total_pairs + 1]; (cost, volume), mem, mem / indeg [total_rows + 1]
   CUDA_TRY(A.d_tables2.ensure(sizeof(double) * 2 * tables_len(p)));
   CUDA_TRY(A.d_sched.ensure(sizeof(Sched) + sizeof(Line) * (p->sigs.size() + 1)));
   A.sched_clean = false;
@@ -1919,10 +1936,8 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   {
     const int64_t L = tables_len(p), P = p->total_pairs + 1, R = p->total_rows + 1;
     double* t = (double*)A.d_tables2.p + A.parity * L;
-    a.r_sec = t;
-    a.r_vol = t + P;
-    a.cls_sec = t + 2 * P;
-    a.cls_vol = t + 2 * P + R;
+    a.r_tab = reinterpret_cast<double2*>(t);  // 16-B aligned: L and P, R offsets are even
+    a.cls_sv = reinterpret_cast<double2*>(t + 2 * P);
     a.cls_mem = t + 2 * P + 2 * R;
     a.cls_memdiv = t + 2 * P + 3 * R;
     a.next_tables = (double*)A.d_tables2.p + (A.parity ^ 1) * L;
@@ -2020,8 +2035,8 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
       const int th = 256;
       rowmin_kernel<<<(unsigned)((rows * 32 + th - 1) / th), th, 0, s>>>(
           (const EdgeDesc*)A.d_edges.p, (const int64_t*)A.d_rowbase.p, e0, e1 - e0, rows,
-          (const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_maps.p, a.r_sec, a.r_vol,
-          a.cls_sec, a.cls_vol, out->row_min_cost_s, out->row_min_volume_bytes);
+          (const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_maps.p, a.r_tab, a.cls_sv,
+          out->row_min_cost_s, out->row_min_volume_bytes);
       ++launches;
     }
   }
