@@ -172,6 +172,8 @@ typedef struct tp_plan_sizes_t {
   int64_t num_pair_evals;    /* (signature, su, sw) pairs priced on device */
   int64_t h2d_bytes;         /* descriptor bytes copied to the device */
   int64_t num_class_rows;    /* node-class strategy rows priced on device */
+  int64_t num_pair_slots;    /* strategy pairs of the distinct edge classes; num_pair_evals is
+                                smaller where classes share layouts or derive from another */
 } tp_plan_sizes_t;
 
 /* --- one-shot call: the drop-in for build_auxiliary_graph ---------------- */

@@ -115,6 +115,7 @@ class tp_plan_sizes_t(C.Structure):
         ("num_pair_evals", C.c_int64),
         ("h2d_bytes", C.c_int64),
         ("num_class_rows", C.c_int64),
+        ("num_pair_slots", C.c_int64),
     ]
 
 

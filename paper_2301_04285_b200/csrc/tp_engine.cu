@@ -1769,6 +1769,8 @@ tp_status tp_plan_sizes(const tp_plan* p, tp_plan_sizes_t* s) {
   s->num_pair_evals = p->total_pairs;
   s->h2d_bytes = p->h2d_bytes;
   s->num_class_rows = p->total_rows;
+  s->num_pair_slots = 0;
+  for (const auto& sd : p->sigs) s->num_pair_slots += (int64_t)sd.Su * sd.Sw;
   return TP_OK;
 }
 

@@ -235,3 +235,55 @@ def test_single_device_and_empty():
     assert r.node_intra_cost_s.tolist() == [0.0] and r.node_intra_volume_bytes.tolist() == [0.0]
     e = gpu_build(G.ComputationGraph([], []), G.ClusterTopology(1, 8, 60e9, 6e9, 32e9))
     assert len(e.edge_cost_s) == 0 and len(e.node_intra_cost_s) == 0
+
+
+def test_shared_layouts_and_derived_classes():
+    """Class tables over distinct layouts (and classes derived by an exact
+    power-of-two byte ratio) are bit-exact, and they do shrink the pair work:
+    some random graphs price fewer entries than their classes' strategy pairs."""
+    rng = random.Random(99)
+    shrunk = 0
+    for i in range(60):
+        g, t = fuzz.random_graph(rng, odd_extents=False, mixed_element_sizes=(i % 3 == 0))
+        f = G.flatten(g)
+        ref = B.oracle_build(f, t)
+        if ref.status != 0:
+            continue
+        plan = engine.Plan(f, t, device=0)
+        sz = plan.sizes
+        assert sz["num_pair_evals"] <= sz["num_pair_slots"]
+        shrunk += sz["num_pair_evals"] < sz["num_pair_slots"]
+        del plan
+        assert_same(gpu_build(f, t, row_min=True), ref, rowmin=True)
+    g, t = M.cfg4()
+    sz = engine.Plan(G.flatten(g), t, device=0).sizes
+    assert sz["num_pair_evals"] < sz["num_pair_slots"] * 0.55  # GPT: the 4h-wide classes derive from the h-wide ones
+    assert shrunk > 0
+
+
+def test_timeline_diagnostics():
+    import torch
+    g, t = M.cfg2()
+    f = G.flatten(g)
+    plan = engine.Plan(f, t, device=0)
+    sz = plan.sizes
+    dev = torch.device("cuda", 0)
+    outs = {k: torch.empty(sz["num_aux_edges"], dtype=torch.float64, device=dev)
+            for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes")}
+    outs.update({k: torch.empty(sz["num_aux_nodes"], dtype=torch.float64, device=dev)
+                 for k in ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes")})
+    plan.set_timeline(True)
+    plan.execute(engine.device_cost_struct(outs))
+    tl = plan.timeline()
+    assert tl["end"] > 0 and tl["first_fanout"] > 0
+    pairs, rows, ranges, clocks, exits = plan.timeline_detail()
+    assert pairs.shape == (sz["num_pair_evals"], 3) and (pairs[:, 1] > 0).all()
+    assert rows.shape == (sz["num_class_rows"], 2) and (rows[:, 1] > 0).all()
+    assert ranges.shape[1] == 3 and (ranges[:, 2] > 0).all()
+    assert clocks.shape == (sz["num_pair_evals"], 8)
+    assert exits.shape[1] == 1 and exits.shape[0] % 8 == 0
+    plan.set_timeline(False)
+    plan.execute(engine.device_cost_struct(outs))
+    plan.check_errors()
+    ref = B.oracle_build(f, t)
+    np.testing.assert_array_equal(bits(outs["edge_cost_s"].cpu().numpy()), bits(ref.edge_cost_s))
