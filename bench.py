@@ -179,7 +179,8 @@ def run_reference(args):
     sample = (f"{threads} concurrent single-thread builds per step of {desc}"
               + (f" (first {layers} of {full_layers} layers)" if layers and layers < full_layers else ""))
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": 0,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "device": "host CPU (rank 0 only)",
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / len(times) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": args.workload, "desc": desc, "threads": threads},
