@@ -470,7 +470,7 @@ __device__ void node_row(const FusedArgs& a, int64_t row) {
   const int lane = threadIdx.x & 31;
   const ClassDesc cd = a.classes[a.row_cls[row]];
   const int64_t s = row - cd.row_base;
-  const Strat st = a.tables[cd.table + s];
+  const Strat& st = a.tables[cd.table + s];  // indexed by axis: read in place (L1), not copied to local memory
   // layout.hpp:349-367: every slice in axis order must divide its extent;
   // the first failing one (in order) names the error
   for (int c0 = cd.chk_begin; c0 < cd.chk_end; c0 += 32) {
@@ -498,7 +498,7 @@ __device__ void node_row(const FusedArgs& a, int64_t row) {
     bool has_v = false, has_m = false;
     if (q < cd.occ_end) {
       const Occ oc = a.occs[q];
-      const SlotDesc sd = a.slots[cd.slot_begin + oc.slot];
+      const SlotDesc& sd = a.slots[cd.slot_begin + oc.slot];
       int sdiv = 0;
       for (int d = 0; d < sd.R; ++d)
         if (sd.sa[d] >= 0) sdiv += st.deg[sd.sa[d]];
@@ -518,7 +518,7 @@ __device__ void node_row(const FusedArgs& a, int64_t row) {
           for (int d = 0; d < sd.R; ++d) contains |= sd.sa[d] >= 0 && st.dmap[sd.sa[d]] == k;
           const int64_t ek = (int64_t)1 << st.mx[k];
           if (!contains && remain > 1) dev_in *= remain > ek ? ek : remain;
-          remain /= ek;
+          remain >>= st.mx[k];  // remain / ek, ek a power of two, remain >= 0
         }
         const int64_t ct = dev_in >= pd ? 0 : (dev_in > 1 ? a.env.local / dev_in : a.env.local);
         const double n = (double)((int64_t)1 << glog);
