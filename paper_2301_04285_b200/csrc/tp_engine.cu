@@ -29,6 +29,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <climits>
 #include <cmath>
 #include <array>
@@ -986,9 +988,7 @@ int log2_floor(int64_t v) {
 }
 
 int v2_capped(int64_t v) {
-  int t = 0;
-  while (t < 63 && !((v >> t) & 1)) ++t;
-  return t;
+  return v == 0 ? 63 : std::min(63, __builtin_ctzll((unsigned long long)v));
 }
 
 }  // namespace
@@ -1076,6 +1076,15 @@ struct tp_plan {
 
 namespace {
 
+// FNV-style hash of an interned key (class dedup on the host)
+struct KeyHash {
+  size_t operator()(const std::vector<int64_t>& v) const {
+    uint64_t h = 1469598103934665603ull ^ v.size();
+    for (int64_t x : v) h = (h ^ (uint64_t)x) * 1099511628211ull;
+    return (size_t)(h ^ (h >> 29));
+  }
+};
+
 struct Builder {
   const tp_graph_desc* g;
   const tp_topology_desc* t;
@@ -1127,24 +1136,35 @@ struct Builder {
 
   // Per-op slots: the reference keys an operator's layouts by tensor name,
   // the last occurrence's spec winning (layout.hpp:339-347).
-  struct OpSlots {
-    std::vector<int32_t> name, spec;
-    int find(int nm) const {
-      for (size_t i = 0; i < name.size(); ++i)
-        if (name[i] == nm) return (int)i;
-      return -1;
-    }
-  };
-  std::vector<OpSlots> op_slots;
-  std::vector<std::vector<std::array<int8_t, tpk::kMaxR>>> slot_sa;  // per op, per slot
+  // Flat over all operators: op i owns slots [slot_begin[i], slot_begin[i + 1]).
+  std::vector<int32_t> slot_begin, slot_name, slot_spec;
+  std::vector<std::array<int8_t, tpk::kMaxR>> slot_sa;  // tensor dim -> slicing axis, per slot
+  int find_slot(int op, int nm) const {  // local slot index of tensor name nm, or -1
+    const int b = slot_begin[op], e = slot_begin[op + 1];
+    for (int i = b; i < e; ++i)
+      if (slot_name[i] == nm) return i - b;
+    return -1;
+  }
+  int spec_of(int op, int k) const { return slot_spec[slot_begin[op] + k]; }
+  const std::array<int8_t, tpk::kMaxR>& sa_of(int op, int k) const { return slot_sa[slot_begin[op] + k]; }
   std::map<int, int64_t> table_of_p;
-  std::map<std::vector<int64_t>, int32_t> class_of_key;
+  std::unordered_map<std::vector<int64_t>, int32_t, KeyHash> class_of_key;
+  // per-operator scratch, reused
+  std::vector<SliceChk> chk;
+  std::vector<SlotDesc> slots;
+  std::vector<Occ> occ;
+  std::vector<int64_t> key;
   std::vector<std::vector<int64_t>> class_members;
-  std::unordered_map<int32_t, std::vector<int32_t>> fed_names;  // op id -> tensors fed by edges
+  // tensors fed by edges, CSR by dense op id (op_key[i] = dense id of op i)
+  std::vector<int32_t> fed_begin, fed_list, op_key;
   std::vector<int64_t> wrow_of_op;
 
   tp_status run() {
+    static const bool prof = getenv("TP_PROFILE_HOST") != nullptr;
+    auto clk = [] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    double tc0 = prof ? clk() : 0;
     tp_status st = check_desc();
+    double tc1 = prof ? clk() : 0;
     if (st) return st;
     tp_plan& p = *P;
     p.num_ops = g->num_ops;
@@ -1152,29 +1172,57 @@ struct Builder {
     p.N = (int64_t)t->node_count * (int64_t)t->local_device_num;
     p.env = Env{t->intra_bandwidth, t->inter_bandwidth, (int64_t)t->local_device_num};
 
-    // graph.hpp:135-154 find_op (first operator with the id), degrees by id
-    std::unordered_map<int32_t, int32_t> first_op, to_count, from_count;
-    for (int i = 0; i < g->num_ops; ++i) first_op.emplace(g->op_id[i], i);
-    for (int e = 0; e < g->num_edges; ++e) {
-      to_count[g->edge_to[e]]++;
-      from_count[g->edge_from[e]]++;
-      fed_names[g->edge_to[e]].push_back(g->edge_tensor[e]);
-    }
-    p.in_deg.resize(g->num_ops);
-    p.out_deg.resize(g->num_ops);
-    for (int i = 0; i < g->num_ops; ++i) {
-      auto a = to_count.find(g->op_id[i]);
-      auto b = from_count.find(g->op_id[i]);
-      p.in_deg[i] = a == to_count.end() ? 0 : a->second;
-      p.out_deg[i] = b == from_count.end() ? 0 : b->second;
-    }
-    p.edge_from_op.resize(g->num_edges);
-    p.edge_to_op.resize(g->num_edges);
-    for (int e = 0; e < g->num_edges; ++e) {
-      auto a = first_op.find(g->edge_from[e]);
-      auto b = first_op.find(g->edge_to[e]);
-      p.edge_from_op[e] = a == first_op.end() ? -1 : a->second;
-      p.edge_to_op[e] = b == first_op.end() ? -1 : b->second;
+    // graph.hpp:135-154 find_op (first operator with the id), degrees by id.
+    // Ids are made dense first: a direct table when they span a small range
+    // (the usual case), a hash map otherwise.
+    {
+      int32_t lo = INT32_MAX, hi = INT32_MIN;
+      auto span = [&](int32_t v) { lo = std::min(lo, v); hi = std::max(hi, v); };
+      for (int i = 0; i < g->num_ops; ++i) span(g->op_id[i]);
+      for (int e = 0; e < g->num_edges; ++e) span(g->edge_from[e]), span(g->edge_to[e]);
+      const int64_t range = g->num_ops + g->num_edges == 0 ? 0 : (int64_t)hi - lo + 1;
+      std::vector<int32_t> direct;
+      std::unordered_map<int32_t, int32_t> hashed;
+      const bool use_direct = range <= 4 * (int64_t)(g->num_ops + g->num_edges) + 1024;
+      if (use_direct) direct.assign(range, -1);
+      int32_t ndense = 0;
+      auto dense = [&](int32_t id) -> int32_t {  // id -> dense index, allocated on first use
+        if (use_direct) {
+          int32_t& d = direct[id - lo];
+          if (d < 0) d = ndense++;
+          return d;
+        }
+        auto ins = hashed.emplace(id, ndense);
+        if (ins.second) ++ndense;
+        return ins.first->second;
+      };
+      std::vector<int32_t> op_dense(g->num_ops), from_dense(g->num_edges), to_dense(g->num_edges);
+      for (int i = 0; i < g->num_ops; ++i) op_dense[i] = dense(g->op_id[i]);
+      for (int e = 0; e < g->num_edges; ++e) from_dense[e] = dense(g->edge_from[e]), to_dense[e] = dense(g->edge_to[e]);
+      std::vector<int32_t> first_op(ndense, -1), to_count(ndense, 0), from_count(ndense, 0);
+      for (int i = g->num_ops - 1; i >= 0; --i) first_op[op_dense[i]] = i;
+      fed_begin.assign(ndense + 1, 0);
+      for (int e = 0; e < g->num_edges; ++e) {
+        to_count[to_dense[e]]++;
+        from_count[from_dense[e]]++;
+      }
+      for (int d = 0; d < ndense; ++d) fed_begin[d + 1] = fed_begin[d] + to_count[d];
+      fed_list.assign(g->num_edges, 0);
+      std::vector<int32_t> fill(fed_begin.begin(), fed_begin.end() - 1);
+      for (int e = 0; e < g->num_edges; ++e) fed_list[fill[to_dense[e]]++] = g->edge_tensor[e];
+      op_key.assign(op_dense.begin(), op_dense.end());
+      p.in_deg.resize(g->num_ops);
+      p.out_deg.resize(g->num_ops);
+      for (int i = 0; i < g->num_ops; ++i) {
+        p.in_deg[i] = to_count[op_dense[i]];
+        p.out_deg[i] = from_count[op_dense[i]];
+      }
+      p.edge_from_op.resize(g->num_edges);
+      p.edge_to_op.resize(g->num_edges);
+      for (int e = 0; e < g->num_edges; ++e) {
+        p.edge_from_op[e] = first_op[from_dense[e]];
+        p.edge_to_op[e] = first_op[to_dense[e]];
+      }
     }
     p.node_base.assign(g->num_ops + 1, 0);
     p.edge_base.assign(g->num_edges + 1, 0);
@@ -1205,12 +1253,15 @@ struct Builder {
       }
     }
 
+    double tc2 = prof ? clk() : 0;
     // ---------------- node phase (aux_graph.hpp:236-253) -----------------
     const bool pow2 = p.N > 0 && (p.N & (p.N - 1)) == 0;
     p.n_log2 = pow2 ? log2_floor(p.N) : 0;
     if (pow2 && p.n_log2 > tpk::kMaxD) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "more than 2^16 devices");
-    op_slots.resize(g->num_ops);
-    slot_sa.resize(g->num_ops);
+    slot_begin.assign(g->num_ops + 1, 0);
+    slot_name.clear();
+    slot_spec.clear();
+    slot_sa.clear();
     wrow_of_op.assign(g->num_ops, 0);
     p.op_row.assign(g->num_ops, 0);
     int64_t nodes = 0;
@@ -1239,6 +1290,7 @@ struct Builder {
       nodes += S;
     }
     for (int i = p.valid_ops; i <= g->num_ops; ++i) p.node_base[i] = nodes;
+    for (int i = p.valid_ops; i <= g->num_ops; ++i) slot_begin[i] = (int32_t)slot_name.size();  // unbuilt: no slots
     p.num_aux_nodes = nodes;
     for (size_t c = 0; c < p.classes.size(); ++c) {  // class member CSR + fan-out work
       p.classes[c].mem_begin = (int32_t)p.members.size();
@@ -1246,10 +1298,11 @@ struct Builder {
       p.classes[c].mem_end = (int32_t)p.members.size();
     }
 
+    double tc3 = prof ? clk() : 0;
     // ---------------- edge phase (aux_graph.hpp:273-296) -----------------
     int64_t aux = 0, rows = 0;
     p.valid_edges = 0;
-    std::map<std::vector<int64_t>, int32_t> sig_of_key;
+    std::unordered_map<std::vector<int64_t>, int32_t, KeyHash> sig_of_key;
     std::vector<std::vector<int32_t>> edges_of_sig;
     if (p.host_err == ~0ull) {
       p.valid_edges = g->num_edges;
@@ -1262,14 +1315,14 @@ struct Builder {
           p.valid_edges = e;
           break;
         }
-        const int ku = op_slots[u].find(g->edge_tensor[e]);
-        const int kw = op_slots[w].find(g->edge_tensor[e]);
+        const int ku = find_slot(u, g->edge_tensor[e]);
+        const int kw = find_slot(w, g->edge_tensor[e]);
         if (ku < 0 || kw < 0) {
           p.host_err = ekey(kEdgePhase + (uint64_t)aux * 2, tpk::kEdgeTensorMissing);
           p.valid_edges = e;
           break;
         }
-        const int tu = op_slots[u].spec[ku], tw = op_slots[w].spec[kw];
+        const int tu = spec_of(u, ku), tw = spec_of(w, kw);
         const int R = rank_of(tu);
         bool same_shape = R == rank_of(tw);
         for (int d = 0; same_shape && d < R; ++d) same_shape = shape_of(tu)[d] == shape_of(tw)[d];
@@ -1293,8 +1346,8 @@ struct Builder {
         std::memcpy(&bbits, &bytes, 8);
         key.insert(key.end(), {(int64_t)pu, (int64_t)pw, (int64_t)R, bbits});
         for (int d = 0; d < R; ++d) key.push_back(shape_of(tu)[d]);
-        for (int d = 0; d < R; ++d) key.push_back(slot_sa[u][ku][d]);
-        for (int d = 0; d < R; ++d) key.push_back(slot_sa[w][kw][d]);
+        for (int d = 0; d < R; ++d) key.push_back(sa_of(u, ku)[d]);
+        for (int d = 0; d < R; ++d) key.push_back(sa_of(w, kw)[d]);
         auto it = sig_of_key.find(key);
         int32_t sig;
         if (it == sig_of_key.end()) {
@@ -1315,14 +1368,14 @@ struct Builder {
             j.tab = side ? sd.tab_w : sd.tab_u;
             j.count = (int32_t)(side ? Sw : Su);
             j.R = R;
-            for (int d = 0; d < tpk::kMaxR; ++d) j.sa[d] = d < R ? (side ? slot_sa[w][kw][d] : slot_sa[u][ku][d]) : -1;
+            for (int d = 0; d < tpk::kMaxR; ++d) j.sa[d] = d < R ? (side ? sa_of(w, kw)[d] : sa_of(u, ku)[d]) : -1;
             (side ? sd.side_w : sd.side_u) = (int32_t)p.side_total;
             p.side_jobs.push_back(j);
             p.side_total += j.count;
           }
           for (int d = 0; d < tpk::kMaxR; ++d) {
-            sd.sa_u[d] = d < R ? slot_sa[u][ku][d] : -1;
-            sd.sa_w[d] = d < R ? slot_sa[w][kw][d] : -1;
+            sd.sa_u[d] = d < R ? sa_of(u, ku)[d] : -1;
+            sd.sa_w[d] = d < R ? sa_of(w, kw)[d] : -1;
             const int64_t E = d < R ? shape_of(tu)[d] : 1;
             const int v = v2_capped(E);
             sd.dt[d].t = (uint8_t)v;
@@ -1364,9 +1417,12 @@ struct Builder {
       sd.base = (int32_t)(&sd - p.sigs.data());
       sd.scale = 1.0;
     }
+    double tc4 = prof ? clk() : 0;
     st = memo_aliasing();
+    double tc5 = prof ? clk() : 0;
     if (st) return st;
     layout_tables(p.overrides.empty());
+    double tc6 = prof ? clk() : 0;
     p.fsegs.clear();
     for (size_t e = 0; e < p.edges.size(); ++e) {
       const EdgeDesc& ed = p.edges[e];
@@ -1401,6 +1457,9 @@ struct Builder {
     for (size_t c = 0; c < p.classes.size(); ++c)
       std::fill(p.row_cls.begin() + p.classes[c].row_base, p.row_cls.begin() + p.classes[c].row_base + p.classes[c].S,
                 (int32_t)c);
+    if (prof)
+      fprintf(stderr, "[tp host] check %.0f us, graph %.0f, node phase %.0f, edge phase %.0f, memo %.0f, tables %.0f, rest %.0f\n",
+              tc1 - tc0, tc2 - tc1, tc3 - tc2, tc4 - tc3, tc5 - tc4, tc6 - tc5, clk() - tc6);
     p.h2d_bytes = (int64_t)(p.tabs.size() * sizeof(TableDesc) + p.classes.size() * sizeof(ClassDesc) +
                             p.members.size() * sizeof(int64_t) + p.chks.size() * sizeof(SliceChk) +
                             p.slots.size() * sizeof(SlotDesc) + p.occs.size() * sizeof(Occ) +
@@ -1414,36 +1473,42 @@ struct Builder {
   // Slots, slice checks, occurrences of one op; then its node class.
   tp_status build_op(int i, int np, int64_t S, int64_t nb) {
     tp_plan& p = *P;
-    OpSlots& os = op_slots[i];
     const int t0 = g->op_tensor_begin[i], t1 = g->op_tensor_begin[i + 1];
+    const int sb = (int)slot_name.size();
+    slot_begin[i] = sb;
     for (int t = t0; t < t1; ++t) {
-      int k = os.find(g->tensor_name[t]);
+      int k = -1;
+      for (int x = sb; x < (int)slot_name.size(); ++x)
+        if (slot_name[x] == g->tensor_name[t]) k = x - sb;
       if (k < 0) {
-        k = (int)os.name.size();
-        os.name.push_back(g->tensor_name[t]);
-        os.spec.push_back(t);
+        k = (int)slot_name.size() - sb;
+        slot_name.push_back(g->tensor_name[t]);
+        slot_spec.push_back(t);
       }
-      os.spec[k] = t;
+      slot_spec[sb + k] = t;
       if (rank_of(t) > tpk::kMaxR) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "tensor rank above 8");
       for (int d = 0; d < rank_of(t); ++d)
         if (shape_of(t)[d] < 1) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "tensor extent < 1 is unsupported");
     }
-    if (os.name.size() > 32000) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many tensors per op");
-    auto& sa = slot_sa[i];
-    sa.assign(os.name.size(), std::array<int8_t, tpk::kMaxR>{});
-    for (auto& a : sa) a.fill(-1);
-    std::vector<SliceChk> chk;
+    const int nslot = (int)slot_name.size() - sb;
+    slot_begin[i + 1] = sb + nslot;
+    if (nslot > 32000) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many tensors per op");
+    std::array<int8_t, tpk::kMaxR> none;
+    none.fill(-1);
+    slot_sa.resize(sb + nslot, none);
+    std::array<int8_t, tpk::kMaxR>* sa = slot_sa.data() + sb;
+    chk.clear();
     const int a0 = g->op_axis_begin[i];
     for (int a = 0; a < np; ++a) {
       for (int s = g->axis_slice_begin[a0 + a]; s < g->axis_slice_begin[a0 + a + 1]; ++s) {
-        const int k = os.find(g->slice_tensor[s]);
+        const int k = find_slot(i, g->slice_tensor[s]);
         SliceChk c{};
         c.axis = (int8_t)a;
         c.slot = (int16_t)k;
         c.v = 0;
         if (k >= 0) {
           const int dim = g->slice_dim[s];
-          const int tk = os.spec[k];
+          const int tk = spec_of(i, k);
           if (dim < 0 || dim >= rank_of(tk))
             return set_err(TP_ERR_INVALID_ARGUMENT, 0, "slice dimension out of range");
           c.v = (int8_t)v2_capped(shape_of(tk)[dim]);
@@ -1452,10 +1517,10 @@ struct Builder {
         chk.push_back(c);
       }
     }
-    std::vector<SlotDesc> slots;
-    for (size_t k = 0; k < os.name.size(); ++k) {
+    slots.clear();
+    for (int k = 0; k < nslot; ++k) {
       SlotDesc sd{};
-      const int tk = os.spec[k];
+      const int tk = spec_of(i, k);
       int64_t el = 1;
       for (int d = 0; d < rank_of(tk); ++d) el *= shape_of(tk)[d];
       sd.elements = el;
@@ -1464,13 +1529,14 @@ struct Builder {
       for (int d = 0; d < tpk::kMaxR; ++d) sd.sa[d] = sa[k][d];
       slots.push_back(sd);
     }
-    std::vector<Occ> occ;
+    occ.clear();
     const int nin = g->op_num_inputs[i];
-    auto fit = fed_names.find(g->op_id[i]);
+    const int32_t* fed0 = fed_list.data() + fed_begin[op_key[i]];
+    const int32_t* fed1 = fed_list.data() + fed_begin[op_key[i] + 1];
     for (int t = t0; t < t1; ++t) {
       Occ oc{};
       const int nm = g->tensor_name[t];
-      oc.slot = (int16_t)os.find(nm);
+      oc.slot = (int16_t)find_slot(i, nm);
       uint8_t mask = 0;
       for (int a = 0; a < np; ++a) {
         bool slices = false;
@@ -1481,8 +1547,7 @@ struct Builder {
       oc.nonslicing = mask;
       if (t - t0 < nin) {
         bool fed = false;  // aux_graph.hpp:155-162
-        if (fit != fed_names.end())
-          for (int32_t x : fit->second) fed |= x == nm;
+        for (const int32_t* x = fed0; x < fed1; ++x) fed |= *x == nm;
         oc.in_memory = !fed;
       } else {
         oc.in_memory = 1;
@@ -1490,8 +1555,8 @@ struct Builder {
       occ.push_back(oc);
     }
     // node class key: everything the per-node costs depend on
-    std::vector<int64_t> key{(int64_t)np, (int64_t)p.in_deg[i], (int64_t)chk.size(), (int64_t)slots.size(),
-                             (int64_t)occ.size()};
+    key.assign({(int64_t)np, (int64_t)p.in_deg[i], (int64_t)chk.size(), (int64_t)slots.size(),
+                (int64_t)occ.size()});
     for (auto& c : chk) key.insert(key.end(), {(int64_t)c.slot, (int64_t)c.axis, (int64_t)c.v});
     for (auto& s : slots) {
       key.insert(key.end(), {s.elements, (int64_t)s.es, (int64_t)s.R});
@@ -1634,7 +1699,7 @@ struct Builder {
     for (size_t s = 0; s < p.sigs.size(); ++s) {
       const EdgeDesc& ed = p.edges[p.sig_edges[p.sig_edge_begin[s]]];
       const int u = p.edge_from_op[ed.e];
-      const int tu = op_slots[u].spec[op_slots[u].find(g->edge_tensor[ed.e])];
+      const int tu = spec_of(u, find_slot(u, g->edge_tensor[ed.e]));
       shape_of_sig[s].assign(shape_of(tu), shape_of(tu) + rank_of(tu));
       by_shape[shape_of_sig[s]].push_back((int32_t)s);
     }
