@@ -957,20 +957,48 @@ __global__ void query_kernel_warp(const tpk::QueryPOD* __restrict__ q, int n, tp
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  bool view = false;  // points into another buffer (the descriptor pack)
+  void set_view(void* at, size_t bytes) {
+    release();
+    p = at;
+    cap = bytes;
+    view = true;
+  }
   cudaError_t ensure(size_t bytes) {
     if (bytes <= cap) return cudaSuccess;
-    if (p) cudaFree(p);
+    if (p && !view) cudaFree(p);
     p = nullptr;
     cap = 0;
+    view = false;
     size_t want = bytes < 256 ? 256 : bytes;
     cudaError_t e = cudaMalloc(&p, want);
     if (e == cudaSuccess) cap = want;
     return e;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p && !view) cudaFree(p);
     p = nullptr;
     cap = 0;
+    view = false;
+  }
+};
+
+// The plan's descriptor arrays go up in ONE copy: packed (256-B aligned) into
+// pinned staging memory, copied into one device buffer, each DevBuf a view.
+struct DescPack {
+  struct Piece {
+    DevBuf* buf;
+    const void* src;
+    size_t bytes;
+  };
+  std::vector<Piece> pieces;
+  template <typename T>
+  void add(DevBuf& b, const std::vector<T>& v) { pieces.push_back({&b, v.data(), v.size() * sizeof(T)}); }
+  static size_t pad(size_t n) { return (n + 16 + 255) & ~(size_t)255; }
+  size_t total() const {
+    size_t t = 0;
+    for (auto& x : pieces) t += pad(x.bytes);
+    return t;
   }
 };
 
@@ -1006,6 +1034,10 @@ struct Arena {
       d_over, d_tables2, d_opnode, d_oprow, d_rowbase, d_sched, d_sidejobs,
       d_sides, d_price, d_pairsigs, d_trace, d_maps, d_rowcls, d_pairrec, d_prof, d_fsegs, d_rfirst;
   DevBuf out[9];  // one-shot staging of the requested outputs
+  DevBuf d_desc;  // the descriptor pack
+  void* h_stage = nullptr;  // pinned staging of the pack
+  size_t h_stage_cap = 0;
+  cudaEvent_t stage_done = nullptr;  // the last pack copy out of h_stage
   bool sched_clean = false;  // Sched zero (set up, or left so by the last launch)
   bool timeline_set = false;
   int parity = 0;
@@ -1015,6 +1047,12 @@ struct Arena {
                       &d_edges, &d_over, &d_tables2, &d_opnode, &d_oprow, &d_rowbase, &d_sched, &d_sidejobs, &d_sides, &d_price, &d_pairsigs, &d_trace, &d_maps, &d_rowcls, &d_pairrec, &d_prof, &d_fsegs, &d_rfirst})
       b->release();
     for (auto& b : out) b.release();
+    d_desc.release();
+    if (h_stage) cudaFreeHost(h_stage);
+    h_stage = nullptr;
+    h_stage_cap = 0;
+    if (stage_done) cudaEventDestroy(stage_done);
+    stage_done = nullptr;
     table_key.clear();
     if (stream) cudaStreamDestroy(stream);
     stream = nullptr;
@@ -1864,8 +1902,51 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
   // strategy tables: a pure function of (p, N), cached on the arena
   std::vector<std::array<int64_t, 4>> key;
   for (auto& td : p->tabs) key.push_back({td.offset, td.count, td.p, td.n});
-  if (key != A.table_key && p->table_total > 0) {
-    CUDA_TRY(upload(A.d_tabs, p->tabs, s));
+  const bool new_tables = key != A.table_key && p->table_total > 0;
+  std::vector<double> price(tpk::kBwTab + tpk::kScaleDim * tpk::kScaleDim);
+  tpk::make_price_tabs(p->env, price.data(), price.data() + tpk::kBwTab);
+  {
+    DescPack pk;
+    if (new_tables) pk.add(A.d_tabs, p->tabs);
+    pk.add(A.d_sidejobs, p->side_jobs);
+    pk.add(A.d_price, price);
+    pk.add(A.d_classes, p->classes);
+    pk.add(A.d_opnode, p->node_base);
+    pk.add(A.d_oprow, p->op_row);
+    pk.add(A.d_members, p->members);
+    pk.add(A.d_chks, p->chks);
+    pk.add(A.d_slots, p->slots);
+    pk.add(A.d_occs, p->occs);
+    pk.add(A.d_sigs, p->sigs);
+    pk.add(A.d_pairsigs, p->pair_sig);
+    pk.add(A.d_rowcls, p->row_cls);
+    pk.add(A.d_maps, p->maps);
+    pk.add(A.d_edges, p->edges);
+    pk.add(A.d_fsegs, p->fsegs);
+    pk.add(A.d_over, p->overrides);
+    const size_t total = pk.total();
+    if (A.stage_done) CUDA_TRY(cudaEventSynchronize(A.stage_done));  // h_stage free again
+    if (A.h_stage_cap < total) {
+      if (A.h_stage) cudaFreeHost(A.h_stage);
+      A.h_stage = nullptr;
+      A.h_stage_cap = 0;
+      CUDA_TRY(cudaMallocHost(&A.h_stage, total));
+      A.h_stage_cap = total;
+    }
+    // views first (d_desc may be reallocated, which frees nothing the views own)
+    for (auto& x : pk.pieces) x.buf->release();
+    CUDA_TRY(A.d_desc.ensure(total));
+    size_t off = 0;
+    for (auto& x : pk.pieces) {
+      if (x.bytes) std::memcpy((char*)A.h_stage + off, x.src, x.bytes);
+      x.buf->set_view((char*)A.d_desc.p + off, DescPack::pad(x.bytes));
+      off += DescPack::pad(x.bytes);
+    }
+    CUDA_TRY(cudaMemcpyAsync(A.d_desc.p, A.h_stage, total, cudaMemcpyHostToDevice, s));
+    if (!A.stage_done) CUDA_TRY(cudaEventCreateWithFlags(&A.stage_done, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(A.stage_done, s));
+  }
+  if (new_tables) {
     CUDA_TRY(A.d_tables.ensure(sizeof(Strat) * (p->table_total + 1)));
     table_kernel<<<(unsigned)((p->table_total + 127) / 128), 128, 0, s>>>(
         (const TableDesc*)A.d_tabs.p, (int)p->tabs.size(), p->table_total, (Strat*)A.d_tables.p);
@@ -1873,7 +1954,6 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
     A.table_key = key;
   }
   // layout descriptors of every (edge class, side, strategy)
-  CUDA_TRY(upload(A.d_sidejobs, p->side_jobs, s));
   CUDA_TRY(A.d_sides.ensure(sizeof(tpk::SideDesc) * (p->side_total + 1)));
   if (p->side_total > 0) {
     side_kernel<<<(unsigned)((p->side_total + 127) / 128), 128, 0, s>>>(
@@ -1881,26 +1961,7 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
         (tpk::SideDesc*)A.d_sides.p);
     CUDA_TRY(cudaGetLastError());
   }
-  {
-    std::vector<double> tabs(tpk::kBwTab + tpk::kScaleDim * tpk::kScaleDim);
-    tpk::make_price_tabs(p->env, tabs.data(), tabs.data() + tpk::kBwTab);
-    CUDA_TRY(upload(A.d_price, tabs, s));
-  }
-  CUDA_TRY(upload(A.d_classes, p->classes, s));
-  CUDA_TRY(upload(A.d_opnode, p->node_base, s));
-  CUDA_TRY(upload(A.d_oprow, p->op_row, s));
-  CUDA_TRY(upload(A.d_members, p->members, s));
-  CUDA_TRY(upload(A.d_chks, p->chks, s));
-  CUDA_TRY(upload(A.d_slots, p->slots, s));
-  CUDA_TRY(upload(A.d_occs, p->occs, s));
-  CUDA_TRY(upload(A.d_sigs, p->sigs, s));
-  CUDA_TRY(upload(A.d_pairsigs, p->pair_sig, s));
-  CUDA_TRY(upload(A.d_rowcls, p->row_cls, s));
-  CUDA_TRY(upload(A.d_maps, p->maps, s));
-  CUDA_TRY(upload(A.d_edges, p->edges, s));
-  CUDA_TRY(upload(A.d_fsegs, p->fsegs, s));
   p->range_key = {{-1, -1, -1, -1}};
-  CUDA_TRY(upload(A.d_over, p->overrides, s));
   CUDA_TRY(A.d_pairrec.ensure(sizeof(PairRec) * (p->total_pairs + 1)));
   if (p->total_pairs > 0) {
     pair_rec_kernel<<<(unsigned)((p->total_pairs + 127) / 128), 128, 0, s>>>(
