@@ -229,6 +229,33 @@ tp_status tp_plan_timeline(tp_plan* plan, int64_t ns_out[5]);
  * and out holds 3, 2, 3, 8 or 1 values per entry. */
 tp_status tp_plan_timeline_detail(tp_plan* plan, int32_t section, uint32_t* out, int64_t* count);
 
+/* --- batches of independent scenarios (cfg5 sweeps) ------------------------
+ * A sweep of (model, mesh, bandwidth-ratio) scenarios is a set of independent
+ * build_auxiliary_graph calls (aux_graph.hpp:211; the reference's CLI/tests
+ * loop over them one at a time, pipeline.hpp:152-168 per scenario). The
+ * batch entry points run the host analysis of many scenarios on a pool of
+ * host threads and keep the device busy with one stream per worker, so the
+ * per-build latencies (analysis, descriptor copy, launch, D2H) overlap.
+ *
+ * tp_plan_create_batch: plans_out[i] / status_out[i] for scenario i (a failed
+ * analysis leaves plans_out[i] = NULL and its tp_status in status_out[i]).
+ * host_threads <= 0 picks the hardware concurrency (capped at 32).
+ * Returns TP_OK when every scenario succeeded, else the status of the first
+ * failing one (its message in tp_last_error). */
+tp_status tp_plan_create_batch(const tp_graph_desc* const* graphs,
+                               const tp_topology_desc* const* topos, int32_t n,
+                               int32_t device, int32_t host_threads,
+                               tp_plan** plans_out, int32_t* status_out);
+/* Execute plans[i] into HOST pointers host_outs[i] (like tp_plan_execute_host,
+ * whole graphs, nodes included). index_outs may be NULL. Plans with their own
+ * uploaded arena (tp_plan_upload called) keep it; the others borrow a pooled
+ * per-worker arena for the duration of the call. NULL plans are skipped with
+ * status TP_ERR_INVALID_ARGUMENT. */
+tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n,
+                                     tp_aux_index* index_outs,
+                                     tp_cost_tensors* host_outs,
+                                     int32_t host_threads, int32_t* status_out);
+
 /* Strategy table of an operator with p axes on N devices, in the reference's
  * enumeration order (layout.hpp:270-328), produced on the device.
  * degrees[S*p], device_map[S*p], matrix_dims[S*p] (outermost first, padded

@@ -295,3 +295,18 @@ def reference_bench(flat, topo, iters=1, threads=1):
     if st != 0:
         raise RuntimeError(reference().ref_last_error().decode())
     return secs.value, edges.value
+
+
+def reference_bench_sweep(pairs, threads=1):
+    """(seconds, aux edges) of building every (flat, topo) scenario with the
+    reference on a pool of `threads` host threads."""
+    n = len(pairs)
+    ds = [f.desc() for f, _ in pairs]
+    ts = [t.desc() for _, t in pairs]
+    gp = (C.POINTER(abi.tp_graph_desc) * max(n, 1))(*[C.pointer(d) for d in ds])
+    tp = (C.POINTER(abi.tp_topology_desc) * max(n, 1))(*[C.pointer(d) for d in ts])
+    secs, edges = C.c_double(), C.c_int64()
+    st = reference().ref_bench_sweep(gp, tp, n, threads, C.byref(secs), C.byref(edges))
+    if st != 0:
+        raise RuntimeError(reference().ref_last_error().decode())
+    return secs.value, edges.value

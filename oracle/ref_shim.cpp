@@ -11,6 +11,7 @@
 // No reference source is copied here; the headers are included from their
 // read-only location at build time only.
 
+#include <atomic>
 #include <chrono>
 #include <cstring>
 #include <sstream>
@@ -253,6 +254,39 @@ int ref_bench_build(const tp_graph_desc* g, const tp_topology_desc* t,
       pool.emplace_back([&, th] {
         for (int i = 0; i < iters; ++i) {
           const AuxiliaryGraph aux = build_auxiliary_graph(graph, topo);
+          counts[th] += static_cast<std::int64_t>(aux.edges.size());
+        }
+      });
+    }
+    for (auto& th : pool) th.join();
+    auto t1 = std::chrono::steady_clock::now();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
+    std::int64_t total = 0;
+    for (auto c : counts) total += c;
+    *aux_edges = total;
+  });
+}
+
+// A sweep of independent scenarios on a pool of `threads` host threads, each
+// scenario one unmodified build_auxiliary_graph call (the reference has no
+// intra-build parallelism; scenarios are pure functions).
+int ref_bench_sweep(const tp_graph_desc* const* g, const tp_topology_desc* const* t, int n, int threads,
+                    double* seconds, int64_t* aux_edges) {
+  return guarded([&] {
+    std::vector<ComputationGraph> graphs;
+    std::vector<ClusterTopology> topos;
+    for (int i = 0; i < n; ++i) {
+      graphs.push_back(to_graph(g[i]));
+      topos.push_back(to_topo(t[i]));
+    }
+    std::vector<std::int64_t> counts(threads, 0);
+    std::atomic<int> next{0};
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int th = 0; th < threads; ++th) {
+      pool.emplace_back([&, th] {
+        for (int i = next.fetch_add(1); i < n; i = next.fetch_add(1)) {
+          const AuxiliaryGraph aux = build_auxiliary_graph(graphs[i], topos[i]);
           counts[th] += static_cast<std::int64_t>(aux.edges.size());
         }
       });

@@ -236,6 +236,12 @@ def load_engine() -> C.CDLL:
     lib.tp_redistribute_batch_form.restype = C.c_int
     lib.tp_plan_set_pair_form.argtypes = [C.c_void_p, C.c_int32]
     lib.tp_plan_set_pair_form.restype = C.c_int
+    lib.tp_plan_create_batch.argtypes = [P(P(tp_graph_desc)), P(P(tp_topology_desc)), C.c_int32, C.c_int32,
+                                         C.c_int32, P(C.c_void_p), _p_i32]
+    lib.tp_plan_create_batch.restype = C.c_int
+    lib.tp_plan_execute_host_batch.argtypes = [P(C.c_void_p), C.c_int32, P(tp_aux_index), P(tp_cost_tensors),
+                                               C.c_int32, _p_i32]
+    lib.tp_plan_execute_host_batch.restype = C.c_int
     lib.tp_last_error.argtypes = []
     lib.tp_last_error.restype = C.c_char_p
     lib.tp_last_error_kind.argtypes = []
@@ -251,7 +257,7 @@ EXPORTED_SYMBOLS = (
     "tp_build_cost_tensors", "tp_plan_create", "tp_plan_destroy", "tp_plan_sizes",
     "tp_plan_index", "tp_plan_upload", "tp_plan_execute", "tp_plan_execute_host", "tp_plan_check_errors",
     "tp_plan_last_launches", "tp_plan_set_profile_events", "tp_plan_set_timeline", "tp_plan_timeline", "tp_plan_timeline_detail", "tp_enumerate_strategies", "tp_redistribute_batch",
-    "tp_redistribute_batch_form", "tp_plan_set_pair_form",
+    "tp_redistribute_batch_form", "tp_plan_set_pair_form", "tp_plan_create_batch", "tp_plan_execute_host_batch",
     "tp_last_error", "tp_last_error_kind", "tp_abi_version",
 )
 

@@ -40,6 +40,9 @@
 #include <string>
 #include <unordered_map>
 #include <vector>
+#include <atomic>
+#include <mutex>
+#include <thread>
 
 #include "../../include/taps_b200.h"
 #include "tp_core.cuh"
@@ -1813,7 +1816,78 @@ Arena* thread_arena(int device) {
   return a;
 }
 
-// CTA work items for edges [e0, e1): class tiles x edge chunks.
+// --- batches: a host worker pool and pooled per-device arenas ---------------
+// Arenas outlive a batch call so later batches pay neither cudaMalloc nor the
+// strategy-table kernel; a worker holds one for the whole call.
+std::mutex g_pool_mu;
+std::vector<Arena*> g_pool[64];
+
+Arena* arena_pool_get(int device) {
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto& v = g_pool[device & 63];
+    if (!v.empty()) {
+      Arena* a = v.back();
+      v.pop_back();
+      return a;
+    }
+  }
+  Arena* a = new Arena();
+  a->device = device;
+  return a;
+}
+
+void arena_pool_put(Arena* a) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  g_pool[a->device & 63].push_back(a);
+}
+
+int pool_size(int n, int host_threads) {
+  int t = host_threads > 0 ? host_threads : (int)std::min(32u, std::max(1u, std::thread::hardware_concurrency()));
+  return std::max(1, std::min(t, n));
+}
+
+// fn(item, worker) over items [0, n), items claimed one at a time
+template <typename F>
+void run_pool(int n, int workers, F&& fn) {
+  workers = pool_size(n, workers);
+  std::atomic<int> next{0};
+  auto body = [&](int w) {
+    for (int i = next.fetch_add(1); i < n; i = next.fetch_add(1)) fn(i, w);
+  };
+  std::vector<std::thread> th;
+  for (int w = 1; w < workers; ++w) th.emplace_back(body, w);
+  body(0);
+  for (auto& x : th) x.join();
+}
+
+// a worker's status and message (tp_last_error is per thread)
+struct BatchErr {
+  tp_status st = TP_OK;
+  int kind = 0;
+  std::string msg;
+  void take(tp_status s) {
+    st = s;
+    if (s) {
+      kind = g_err_kind;
+      msg = g_err;
+    }
+  }
+};
+
+tp_status batch_status(const std::vector<BatchErr>& errs, int32_t* status_out) {
+  const BatchErr* first = nullptr;
+  for (size_t i = 0; i < errs.size(); ++i) {
+    if (status_out) status_out[i] = errs[i].st;
+    if (errs[i].st && !first) first = &errs[i];
+  }
+  if (!first) {
+    g_err[0] = 0;
+    g_err_kind = 0;
+    return TP_OK;
+  }
+  return set_err(first->st, first->kind, first->msg);
+}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -2369,6 +2443,64 @@ tp_status tp_build_cost_tensors(const tp_graph_desc* graph, const tp_topology_de
   st = tp_plan_execute_host(p, opts, index_out, host_out);
   tp_plan_destroy(p);
   return st;
+}
+
+tp_status tp_plan_create_batch(const tp_graph_desc* const* graphs, const tp_topology_desc* const* topos, int32_t n,
+                               int32_t device, int32_t host_threads, tp_plan** plans_out, int32_t* status_out) {
+  if (n < 0 || (n > 0 && (!graphs || !topos || !plans_out)))
+    return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null batch arrays");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(TP_ERR_CUDA, 0, "no CUDA device: the engine has no CPU path");
+  if (device < 0) CUDA_TRY(cudaGetDevice(&device));
+  std::vector<BatchErr> errs(n);
+  run_pool(n, host_threads, [&](int i, int) {
+    tp_plan* p = nullptr;
+    const tp_status st = tp_plan_create(graphs[i], topos[i], device, &p);
+    plans_out[i] = p;
+    errs[i].take(st);
+  });
+  return batch_status(errs, status_out);
+}
+
+tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_index* index_outs,
+                                     tp_cost_tensors* host_outs, int32_t host_threads, int32_t* status_out) {
+  if (n < 0 || (n > 0 && (!plans || !host_outs))) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null batch arrays");
+  std::vector<BatchErr> errs(n);
+  const int workers = pool_size(n, host_threads);
+  std::vector<Arena*> borrowed(workers, nullptr);
+  std::vector<int> borrowed_dev(workers, -1);
+  run_pool(n, workers, [&](int i, int w) {
+    tp_plan* p = plans[i];
+    if (!p) {
+      errs[i].take(set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan"));
+      return;
+    }
+    const bool borrow = p->arena == nullptr;
+    if (borrow) {
+      if (borrowed[w] && borrowed_dev[w] != p->device) {
+        arena_pool_put(borrowed[w]);
+        borrowed[w] = nullptr;
+      }
+      if (!borrowed[w]) {
+        borrowed[w] = arena_pool_get(p->device);
+        borrowed_dev[w] = p->device;
+      }
+      p->arena = borrowed[w];
+      p->owns_arena = false;
+      p->uploaded = false;
+    }
+    errs[i].take(tp_plan_execute_host(p, nullptr, index_outs ? &index_outs[i] : nullptr, &host_outs[i]));
+    if (borrow) {  // the arena's descriptors belong to the next plan now
+      p->arena = nullptr;
+      p->owns_arena = true;
+      p->uploaded = false;
+      p->range_key = {{-1, -1, -1, -1}};
+    }
+  });
+  for (Arena* a : borrowed)
+    if (a) arena_pool_put(a);
+  return batch_status(errs, status_out);
 }
 
 tp_status tp_enumerate_strategies(int32_t p, int64_t total_devices, int64_t* count, int64_t* degrees,

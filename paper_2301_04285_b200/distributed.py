@@ -14,6 +14,7 @@ tests), used when the caller wants the full tensors on one device.
 from __future__ import annotations
 
 import heapq
+import math
 from typing import Callable, List, Sequence, Tuple
 
 
@@ -44,6 +45,22 @@ def partition_edges(pair_counts: Sequence[int], world: int) -> List[Tuple[int, i
         bounds.append(max(e, bounds[-1]))
     bounds.append(n)
     return [(bounds[r], bounds[r + 1]) for r in range(world)]
+
+
+def strategy_count(p: int, total_devices: int) -> int:
+    """layout.hpp:222-244 closed form: sum_i i! C(p,i) C(n-1,i-1)."""
+    n = total_devices.bit_length() - 1
+    if n == 0:
+        return 1
+    return sum(math.factorial(i) * math.comb(p, i) * math.comb(n - 1, i - 1) for i in range(1, min(p, n) + 1))
+
+
+def estimated_aux_edges(graph, topo) -> int:
+    """|E_A| of a scenario (sum over edges of S(from) * S(to)), the LPT weight
+    of a sweep scenario; graph is a ComputationGraph."""
+    N = topo.total_devices()
+    S = [strategy_count(op.axis_count(), N) for op in graph.operators]
+    return sum(S[graph.find_op(e.from_)] * S[graph.find_op(e.to)] for e in graph.edges)
 
 
 def partition_scenarios(costs: Sequence[float], world: int) -> List[List[int]]:

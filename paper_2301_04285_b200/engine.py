@@ -284,3 +284,127 @@ def redistribute_batch(queries, form: int = 2):
     res = (abi.tp_redist_result * n)()
     _check(lib, lib.tp_redistribute_batch_form(arr, n, res, form))
     return list(res)
+
+
+_OUT_KEYS = ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes",
+             "edge_cost_s", "edge_volume_bytes", "edge_memory_bytes")
+
+
+class Sweep:
+    """A batch of independent (graph, topology) scenarios — cfg5's sweep of
+    (model, mesh, bandwidth-ratio) triples — built with the batch entry
+    points (tp_plan_create_batch / tp_plan_execute_host_batch): the host
+    analysis runs on a pool of host threads and every worker keeps its own
+    stream busy, so per-build latencies overlap. Each scenario's result is a
+    CostTensors in the reference's index order, exactly what
+    build_auxiliary_graph returns for that scenario alone (aux_graph.hpp:211).
+
+    Outputs live in one (optionally pinned) host allocation per tensor kind,
+    sliced per scenario, allocated once by `allocate()` and reused by every
+    `execute()`."""
+
+    def __init__(self, scenarios, device: int = -1, host_threads: int = 0):
+        self.lib = abi.load_engine()
+        self.flats = [_flat(g) for g, _ in scenarios]
+        self.topos = [t for _, t in scenarios]
+        self.device = device
+        self.host_threads = host_threads
+        n = len(self.flats)
+        self._descs = [f.desc() for f in self.flats]
+        self._tdescs = [t.desc() for t in self.topos]
+        self._gp = (C.POINTER(abi.tp_graph_desc) * max(n, 1))(*[C.pointer(d) for d in self._descs])
+        self._tp = (C.POINTER(abi.tp_topology_desc) * max(n, 1))(*[C.pointer(d) for d in self._tdescs])
+        self.handles = (C.c_void_p * max(n, 1))()
+        self.status = np.zeros(max(n, 1), np.int32)
+        self.results = None
+        self._outs = None
+
+    def __len__(self):
+        return len(self.flats)
+
+    def create(self, raise_errors: bool = True):
+        """Host analysis of every scenario (tp_plan_create_batch)."""
+        self.destroy()
+        st = self.lib.tp_plan_create_batch(self._gp, self._tp, len(self), self.device, self.host_threads,
+                                           self.handles, abi.ptr(self.status, C.c_int32))
+        if raise_errors:
+            _check(self.lib, st)
+        return st
+
+    def destroy(self):
+        for i in range(len(self)):
+            if self.handles[i]:
+                self.lib.tp_plan_destroy(self.handles[i])
+                self.handles[i] = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    def sizes(self, i: int) -> dict:
+        s = abi.tp_plan_sizes_t()
+        _check(self.lib, self.lib.tp_plan_sizes(self.handles[i], C.byref(s)))
+        return {k: getattr(s, k) for k, _ in abi.tp_plan_sizes_t._fields_}
+
+    def allocate(self, pinned: bool = True):
+        """Caller-owned outputs of every scenario (plans must exist)."""
+        n = len(self)
+        nn = [self.sizes(i)["num_aux_nodes"] if self.handles[i] else 0 for i in range(n)]
+        ne = [self.sizes(i)["num_aux_edges"] if self.handles[i] else 0 for i in range(n)]
+        alloc = _pinned_empty if pinned else (lambda k, dt: np.zeros(k, dt))
+        node_off = np.concatenate([[0], np.cumsum(nn)]).astype(np.int64)
+        edge_off = np.concatenate([[0], np.cumsum(ne)]).astype(np.int64)
+        big = {k: alloc(max(int((node_off if k.startswith("node") else edge_off)[-1]), 1), np.float64)
+               for k in _OUT_KEYS}
+        self._outs = (big, node_off, edge_off)
+        self.results = []
+        self._cs = (abi.tp_cost_tensors * max(n, 1))()
+        self._ix = (abi.tp_aux_index * max(n, 1))()
+        self._keep = []
+        for i in range(n):
+            f = self.flats[i]
+            n_ops, n_e = f.num_ops, f.num_edges
+            ix = dict(node_base=np.zeros(n_ops + 1, np.int64), edge_base=np.zeros(n_e + 1, np.int64),
+                      edge_from_op=np.zeros(max(n_e, 1), np.int32), edge_to_op=np.zeros(max(n_e, 1), np.int32),
+                      in_degree=np.zeros(max(n_ops, 1), np.int32), out_degree=np.zeros(max(n_ops, 1), np.int32),
+                      topo_order=np.zeros(max(n_ops, 1), np.int32))
+            views = {k: big[k][(node_off if k.startswith("node") else edge_off)[i]:
+                               (node_off if k.startswith("node") else edge_off)[i + 1]] for k in _OUT_KEYS}
+            ct = CostTensors(sizes=self.sizes(i) if self.handles[i] else {}, **ix, **views)
+            self.results.append(ct)
+            self._cs[i] = cost_struct(ct) if ne[i] + nn[i] > 0 else abi.tp_cost_tensors()
+            self._ix[i] = abi.tp_aux_index(*(abi.ptr(ix[k], C.c_int64 if ix[k].dtype == np.int64 else C.c_int32)
+                                             for k, _ in abi.tp_aux_index._fields_))
+            self._keep.append(ix)
+        return self
+
+    def execute(self, raise_errors: bool = True):
+        """Build every scenario into its host slices (tp_plan_execute_host_batch)."""
+        st = self.lib.tp_plan_execute_host_batch(self.handles, len(self), self._ix, self._cs, self.host_threads,
+                                                 abi.ptr(self.status, C.c_int32))
+        if raise_errors:
+            _check(self.lib, st)
+        for i, ct in enumerate(self.results):
+            f = self.flats[i]
+            for k, n in (("edge_from_op", f.num_edges), ("edge_to_op", f.num_edges), ("in_degree", f.num_ops),
+                         ("out_degree", f.num_ops), ("topo_order", f.num_ops)):
+                setattr(ct, k, self._keep[i][k][:n])
+        return st
+
+    @property
+    def num_aux_edges(self) -> int:
+        return int(self._outs[2][-1]) if self._outs else 0
+
+
+def build_sweep(scenarios, device: int = -1, host_threads: int = 0, pinned: bool = False):
+    """Cost tensors of every (graph, topology) scenario: a list of CostTensors,
+    element i equal to build_cost_tensors(*scenarios[i])."""
+    sw = Sweep(scenarios, device, host_threads)
+    sw.create()
+    sw.allocate(pinned=pinned)
+    sw.execute()
+    res = sw.results
+    sw.destroy()
+    return res
