@@ -156,7 +156,7 @@ def run_reference(args):
     from oracle import bindings as B
     from paper_2301_04285_b200 import graph as G
     if not B.have_reference():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtopoplan_ref.so not built"}))
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtopoplan_ref.so not built"}), flush=True)
         return 0
     threads = max(1, min(os.cpu_count() or 1, 16))
     if args.workload == "cfg5":
@@ -169,7 +169,8 @@ def run_reference(args):
             "config": {"workload": "cfg5", "desc": desc, "threads": threads},
             "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "reference",
                              "sample": sample},
-            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+            flush=True)
         return 0
     # bounded sample: a prefix of the GPT chain sized so the run ends in ~3 min
     budget_s, est_full_s = 150.0, 3.5
@@ -200,7 +201,7 @@ def run_reference(args):
                          "sample": sample},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -250,6 +251,8 @@ def run_sweep(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
+        if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+            os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     pairs, total_evals = sweep_scenarios(rank, world)
     dev = torch.device("cuda", local)
@@ -371,7 +374,7 @@ def run_sweep(args):
             secs, n = B.reference_bench_sweep(sample, threads=1)
             line["cpu_baseline"] = {"value": n / secs, "unit": "evals/s", "cores": 1, "kind": "reference",
                                     "sample": f"every 10th scenario ({len(sample)}, {n} aux edges), one thread"}
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     sw.destroy()
     if dist:
         dist.destroy_process_group()
@@ -389,6 +392,8 @@ def run_engine(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
+        if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+            os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     g, t, desc = workload(args.workload, rank)
@@ -527,7 +532,7 @@ def run_engine(args):
         line["cpu_baseline"] = cpu_baseline(flat, t, ne)
     else:
         line["cpu_baseline"] = None
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
     return 0

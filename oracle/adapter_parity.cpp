@@ -9,6 +9,7 @@
 // the same objective on both, that price_assignment agrees and that
 // export_lp emits the same text. Built by oracle/Makefile into
 // oracle/_ref/adapter_parity; run on a GPU box by tests/test_gpu_adapter.py.
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <random>
@@ -171,6 +172,81 @@ ComputationGraph gpt_chain(int layers, std::int64_t hidden, std::int64_t batch, 
   return g;
 }
 
+// cfg5: the seeded scenario sweep (SURVEY.md §8d draw order). For every
+// sampled scenario both builds go through the reference's own ILP in both
+// cost modes and run_compare's TAPS-vs-volume ratio (pipeline.hpp:152-168:
+// both winners priced in topology mode) must be bit-identical.
+void check_sweep(int count, int every) {
+  std::mt19937_64 rng(0x230104285ull);
+  int checked = 0;
+  for (int i = 0; i < count; ++i) {
+    const std::uint64_t fam = rng() % 4;
+    const int nodes = 1 << (rng() % 4);
+    const double ratio = std::pow(10.0, static_cast<double>(rng() % 1001) / 500.0);
+    ComputationGraph g;
+    std::string name;
+    if (fam == 0) {
+      ModelConfig c;
+      c.family = ModelFamily::kMlpChain;
+      c.layers = 2 + static_cast<std::int64_t>(rng() % 7);
+      c.hidden = static_cast<std::int64_t>(256) << (rng() % 5);
+      c.batch = 256;
+      g = build_graph(c);
+      name = "mlp-chain L" + std::to_string(c.layers) + " h" + std::to_string(c.hidden);
+    } else if (fam == 1) {
+      ModelConfig c;
+      c.family = ModelFamily::kTransformerLayer;
+      c.hidden = static_cast<std::int64_t>(1024) << (rng() % 3);
+      c.batch = 8;
+      c.seq = 512;
+      g = build_graph(c);
+      name = "transformer h" + std::to_string(c.hidden);
+    } else if (fam == 2) {
+      ModelConfig c;
+      c.family = ModelFamily::kAlexnetLike;
+      c.batch = 64;
+      g = build_graph(c);
+      name = "alexnet-like";
+    } else {
+      const int L = 2 + static_cast<int>(rng() % 3);
+      g = gpt_chain(L, 2048, 8, 512);
+      name = "gpt-chain L" + std::to_string(L);
+    }
+    if (i % every != 0) continue;
+    const ClusterTopology topo{nodes, 8, 60e9, 60e9 / ratio, 80e9};
+    const AuxiliaryGraph ref = build_auxiliary_graph(g, topo);
+    const AuxiliaryGraph gpu = taps_b200::build_auxiliary_graph_b200(g, topo, CostMode::kTopology, -1, true);
+    std::string err = compare(ref, gpu);
+    double ratios[2] = {0, 0};
+    const AuxiliaryGraph* both[2] = {&ref, &gpu};
+    for (int k = 0; err.empty() && k < 2; ++k) {
+      SolveOptions opts;
+      opts.threads = 1;
+      opts.max_nodes = 20000;  // fixed budget, one thread: a deterministic search
+      const PlanSolution v = solve(formulate(*both[k], CostMode::kVolume, topo.device_memory), opts);
+      const PlanSolution t = solve(formulate(*both[k], CostMode::kTopology, topo.device_memory), opts);
+      const double den = price_assignment(*both[k], v.strategy_per_op, CostMode::kTopology).cost;
+      const double num = price_assignment(*both[k], t.strategy_per_op, CostMode::kTopology).cost;
+      ratios[k] = den == 0 ? 1.0 : num / den;
+      static PlanSolution keep_v, keep_t;
+      if (k == 0) {
+        keep_v = v;
+        keep_t = t;
+      } else if (keep_v.strategy_per_op != v.strategy_per_op || keep_t.strategy_per_op != t.strategy_per_op ||
+                 !same_bits(keep_v.objective, v.objective) || !same_bits(keep_t.objective, t.objective)) {
+        err = "ILP selection differs";
+      }
+    }
+    if (err.empty() && !same_bits(ratios[0], ratios[1])) err = "TAPS/volume ratio differs";
+    char buf[200];
+    std::snprintf(buf, sizeof(buf), "%zu aux edges, %dx8, ratio bw %.3g: TAPS/volume %.4f", gpu.edges.size(), nodes,
+                  ratio, ratios[0]);
+    report("cfg5 #" + std::to_string(i) + " " + name, err, buf);
+    ++checked;
+  }
+  std::printf("[PARITY] cfg5 sweep: %d scenarios checked\n", checked);
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -235,6 +311,7 @@ int main(int argc, char** argv) {
     check_case("cfg3 GPT-24 h2048 8x8 r100", gpt_chain(24, 2048, 8, 512), {8, 8, 60e9, 0.6e9, 80e9}, SolveCfg{});
     if (big) check_case("cfg4 GPT-96 h12288 16x8", gpt_chain(96, 12288, 8, 2048), {16, 8, 60e9, 6e9, 80e9}, SolveCfg{});
   }
+  check_sweep(1000, big ? 10 : 40);
   std::printf("[PARITY] %s (%d failures)\n", failures ? "FAILED" : "ALL PASS", failures);
   return failures ? 1 : 0;
 }

@@ -119,3 +119,36 @@ def sharded_build(dist, flat, topo, compute: Callable, gather: bool = True):
     eb = index["edge_base"]
     total = int(eb[len(counts)])
     return ranges, tuple(gather_to_rank0(dist, x, ranges, eb, total) for x in (c, v, m))
+
+
+def engine_compute(device: int):
+    """The `compute` of sharded_build on a GPU rank: the CUDA engine builds the
+    rank's edge range straight into device tensors (tp_plan_execute with
+    tp_build_opts.edge_begin/end), ready for the NCCL gather."""
+    import torch
+
+    from . import engine as E
+
+    cache = {}
+
+    def compute(flat, topo, rng):
+        key = (id(flat), id(topo))
+        if key not in cache:
+            cache.clear()
+            cache[key] = E.Plan(flat, topo, device=device)
+        plan = cache[key]
+        ix = plan.index()
+        e0, e1 = rng
+        eb = ix["edge_base"]
+        n = int(eb[e1] - eb[e0])
+        dev = torch.device("cuda", device)
+        outs = {k: torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+                for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes")}
+        stream = torch.cuda.current_stream(dev)
+        if n > 0:
+            plan.execute(E.device_cost_struct(outs), edge_range=(e0, e1), skip_nodes=True,
+                         stream=stream.cuda_stream)
+            plan.check_errors()
+        return ix, outs["edge_cost_s"][:n], outs["edge_volume_bytes"][:n], outs["edge_memory_bytes"][:n]
+
+    return compute

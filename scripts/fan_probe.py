@@ -58,3 +58,31 @@ print("warp phase-1 exit us pct:", q(wx))
 order = np.argsort(fo[:, 0] + fo[:, 2])[-6:]
 for i in order:
     print(f"  slowest-ending range {i}: start {fo[i,0]/1e3:.1f} wait {fo[i,1]/1e3:.1f} dur {fo[i,2]/1e3:.1f}")
+# node-row and pair start/duration distributions, and the same build without the L2 flush
+print("node rows start us", q(it[:, 0]), "dur", q(it[:, 1]))
+print("pairs start us", q(pr[:, 0]), "dur", q(pr[:, 1]))
+ts2 = []
+with torch.cuda.stream(s):
+    for i in range(23):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        plan.execute(full, stream=s.cuda_stream)
+        b.record(s)
+        if i >= 3:
+            ts2.append((a, b))
+torch.cuda.synchronize()
+v2 = sorted(x.elapsed_time(y) * 1e3 for x, y in ts2)
+print(f"build without flush (timeline on) {v2[len(v2)//2]:.1f} us")
+plan.set_timeline(False)
+ts3 = []
+with torch.cuda.stream(s):
+    for i in range(23):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        plan.execute(full, stream=s.cuda_stream)
+        b.record(s)
+        if i >= 3:
+            ts3.append((a, b))
+torch.cuda.synchronize()
+v3 = sorted(x.elapsed_time(y) * 1e3 for x, y in ts3)
+print(f"build without flush {v3[len(v3)//2]:.1f} us (with flush {v[len(v)//2]:.1f})")
