@@ -238,8 +238,8 @@ def run_reference_sweep(args, threads):
 
 def run_sweep(args):
     """cfg5 through the batch entry points. value: device-resident (plans
-    analysed and uploaded, every scenario's kernels on 8 streams, CUDA events
-    around the batch); e2e: host graphs in -> tp_plan_create_batch +
+    analysed and uploaded, all scenarios rebuilt by one batched persistent
+    launch, CUDA events around it); e2e: host graphs in -> tp_plan_create_batch +
     tp_plan_execute_host_batch -> pinned host tensors out, wall clock."""
     import torch
     from paper_2301_04285_b200 import engine as E
@@ -257,68 +257,38 @@ def run_sweep(args):
     pairs, total_evals = sweep_scenarios(rank, world)
     dev = torch.device("cuda", local)
 
-    # ---- device-resident: own plan + arena per scenario ----
-    plans = [E.Plan(f, t, device=local) for f, t in pairs]
-    nstreams = 8
-    streams = [torch.cuda.Stream() for _ in range(nstreams)]
-    main = torch.cuda.Stream()
-    ne = [p.sizes["num_aux_edges"] for p in plans]
-    nn = [p.sizes["num_aux_nodes"] for p in plans]
-    eoff = np.concatenate([[0], np.cumsum(ne)]).astype(np.int64)
-    noff = np.concatenate([[0], np.cumsum(nn)]).astype(np.int64)
-    big = {k: torch.empty(max(int(eoff[-1]), 1), dtype=torch.float64, device=dev)
-           for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes")}
-    big.update({k: torch.empty(max(int(noff[-1]), 1), dtype=torch.float64, device=dev)
-                for k in ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes")})
-    structs = []
-    for i, p in enumerate(plans):
-        p.upload(streams[i % nstreams].cuda_stream)
-        sl = {k: (v[eoff[i]:eoff[i + 1]] if k.startswith("edge") else v[noff[i]:noff[i + 1]])
-              for k, v in big.items()}
-        structs.append(E.device_cost_struct({k: v for k, v in sl.items() if v.numel()}))
+    # ---- device-resident: own plan + arena per scenario, one batched launch per step ----
+    ds = E.DeviceSweep(pairs, device=local)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
-    torch.cuda.synchronize()
-
-    def batch():
-        fork = torch.cuda.Event()
-        fork.record(main)
-        for s in streams:
-            s.wait_event(fork)
-        for i, p in enumerate(plans):
-            p.execute(structs[i], stream=streams[i % nstreams].cuda_stream)
-        for s in streams:
-            j = torch.cuda.Event()
-            j.record(s)
-            main.wait_event(j)
-
     K, W = args.steps, args.warmup
     clocks = Clocks(local)
     for _ in range(W):
-        batch()
+        with torch.cuda.stream(ds.main):
+            flush.zero_()
+        ds.run()
     torch.cuda.synchronize()
-    for p in plans:
-        p.check_errors()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     for i in range(K):
-        with torch.cuda.stream(main):
+        with torch.cuda.stream(ds.main):
             flush.zero_()
-        ev[i][0].record(main)
-        batch()
-        ev[i][1].record(main)
+        ev[i][0].record(ds.main)
+        ds.run()
+        ev[i][1].record(ds.main)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    launches = sum(p.last_launches() for p in plans)
+    launches = ds.launches_per_run()
     dev_ms = sum(a.elapsed_time(b) for a, b in ev)
     t_max = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     dev_ms = float(t_max.item())
     value = total_evals * K / (dev_ms / 1e3)
-    del plans, structs
+    eoff, noff = ds.edge_off, ds.node_off
+    del ds
 
     # ---- e2e: host graphs in, pinned host tensors out ----
     sw = E.Sweep(pairs, device=local, host_threads=0)
@@ -355,11 +325,11 @@ def run_sweep(args):
         "config": {"workload": "cfg5", "desc": "1,000 seeded (model, mesh, bandwidth-ratio) scenarios, "
                    "LPT-sharded over ranks (SURVEY §8d)", "scenarios_rank0": len(pairs),
                    "aux_edges_total": total_evals, "parallelism": f"scenario-sharded x{world}",
-                   "streams": nstreams, "l2": "256 MiB buffer written between timed steps (flush)",
+                   "l2": "256 MiB buffer written between timed steps (flush)",
                    "build_ms_e2e": sum(e2e_t) / KE * 1e3},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "fused_kernel (one launch per scenario, 8 streams)",
-                     "bytes_per_launch": out_bytes / max(len(pairs), 1),
+                     "traffic": None, "kernel": "fused_batch_kernel (all scenarios of the rank in one persistent launch)",
+                     "bytes_per_launch": out_bytes,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
         "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": out_bytes,

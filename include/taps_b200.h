@@ -256,6 +256,17 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n,
                                      tp_cost_tensors* host_outs,
                                      int32_t host_threads, int32_t* status_out);
 
+/* Build every plan into DEVICE pointers device_outs[i] with ONE persistent
+ * launch on `stream` (NULL = plans[0]'s stream): the units and output ranges
+ * of all plans form one work queue, so the latency-bound pricing of many small
+ * scenarios overlaps instead of paying one launch each. Every plan's results
+ * equal tp_plan_execute's (whole graphs). Plans must live on one device;
+ * a plan not yet uploaded is uploaded on `stream` (a plan uploaded on another
+ * stream must have completed that upload). Errors are per plan:
+ * tp_plan_check_errors(plans[i]). */
+tp_status tp_plan_execute_batch(tp_plan* const* plans, int32_t n,
+                                tp_cost_tensors* device_outs, void* stream);
+
 /* Strategy table of an operator with p axes on N devices, in the reference's
  * enumeration order (layout.hpp:270-328), produced on the device.
  * degrees[S*p], device_map[S*p], matrix_dims[S*p] (outermost first, padded

@@ -797,17 +797,84 @@ __device__ void node_range(const FusedArgs& a, int item, NodeSeg* seg, int* s_n,
 // 2 only after its warps drained the unit queue, and every claimed unit runs
 // to completion, so the waits always end. The latency-bound pricing and the
 // write-bound fan-out overlap, with no launch gap or wave tail between them.
+// One phase-1 unit u of a plan: a node-class row, or a class pair (warp
+// form) / 32 class pairs (thread form).
+template <bool kWarpForm>
+__device__ __forceinline__ void run_unit(const FusedArgs& a, int64_t u, const double* price) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long t0 = (a.pair_ns || a.item_ns) ? gtimer() : 0;
+  if (u < a.total_rows) {
+    node_row(a, u);
+    if (lane == 0) {
+      red_release_add(&a.sched->node_done.v, 1);  // rows: off the critical path, released
+      if (a.item_ns) {
+        a.item_ns[2 * u] = (unsigned)t0;
+        a.item_ns[2 * u + 1] = (unsigned)(gtimer() - t0);
+      }
+    }
+  } else if (kWarpForm) {
+    const int64_t idx = u - a.total_rows;
+    pair_warp(a, idx, price);
+    const int sig = a.pairs[idx].sig;
+    if (lane == 0) {
+      if (a.pair_ns) {
+        a.pair_ns[2 * idx] = (unsigned)t0;
+        a.pair_ns[2 * idx + 1] = (unsigned)(gtimer() - t0);
+      }
+      red_relaxed_add(&a.sched->pairs_done[sig].v, 1);  // no fence: see table_load
+    }
+  } else {
+    const int64_t idx = (u - a.total_rows) * 32 + lane;
+    const bool valid = idx < a.total_pairs;
+    const int sig = valid ? sig_of_pair(a, idx) : -1;
+    if (valid) pair_thread(a, idx, price);
+    if (a.pair_ns && valid) {
+      a.pair_ns[2 * idx] = (unsigned)t0;
+      a.pair_ns[2 * idx + 1] = (unsigned)(gtimer() - t0);
+    }
+    // one counter update per (warp, edge class); no fence: see table_load
+    const unsigned grp = __match_any_sync(0xffffffffu, sig);
+    if (valid && lane == __ffs(grp) - 1) red_relaxed_add(&a.sched->pairs_done[sig].v, __popc(grp));
+  }
+}
+
+__device__ __forceinline__ int64_t plan_units(const FusedArgs& a) {
+  return a.total_rows + (a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32);
+}
+
+// The plan's per-launch reset, done by the last CTA to leave (one thread).
+__device__ __forceinline__ void reset_plan(const FusedArgs& a) {
+  Sched* sc = a.sched;
+  sc->head = 0;
+  sc->unit_head.v = 0;
+  sc->node_done.v = 0;
+  for (int i = 0; i < a.nsigs_reset; ++i) sc->pairs_done[i].v = 0;
+  sc->err_c[a.parity ^ 1] = 0;
+  sc->exit_count = 0;
+}
+
+// The whole build in one persistent launch. Phase 1: warps take units --
+// node-class rows first (every fan-out needs them), then class pairs (one per
+// warp, or 32 per warp in the thread form). A CTA claims its first 8 units
+// with one atomic and a warp claims further units alone, skipping the atomic
+// once the queue is drained, so the start-up burst does not serialise on the
+// counter and a slow pair never idles the other warps of its CTA. Each
+// finished unit bumps its counter with a release add. Phase 2: block work
+// items for the fan-out tiles and the node fan-out; a tile waits (acquire)
+// only for its own edge class's table and the node rows. A CTA reaches phase
+// 2 only after its warps drained the unit queue, and every claimed unit runs
+// to completion, so the waits always end. The latency-bound pricing and the
+// write-bound fan-out overlap, with no launch gap or wave tail between them.
 template <bool kWarpForm>
 __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
-  __shared__ int s_item, s_unit, s_edge, s_nseg;
+  __shared__ int s_unit, s_edge, s_nseg;
   __shared__ union {
     FanSeg f[kSegs];
     NodeSeg n[kSegs];
   } s_seg;
   __shared__ double s_price[tpk::kBwTab + tpk::kScaleDim * tpk::kScaleDim];  // the pricing tables
   const int lane = threadIdx.x & 31;
-  const int64_t pair_units = kWarpForm ? a.total_pairs : (a.total_pairs + 31) / 32;
-  const int64_t units = a.total_rows + pair_units;
+  const int64_t units = plan_units(a);
   if (threadIdx.x == 0) {
     stamp(a.sched, 0, true);
     s_unit = atomicAdd(&a.sched->unit_head.v, kFusedThreads / 32);
@@ -819,40 +886,7 @@ __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
   // phase 1: node-class rows, then class pairs
   int64_t u = (int64_t)s_unit + (threadIdx.x >> 5);
   while (u < units) {
-    const unsigned long long t0 = (a.pair_ns || a.item_ns) ? gtimer() : 0;
-    if (u < a.total_rows) {
-      node_row(a, u);
-      if (lane == 0) {
-        red_release_add(&a.sched->node_done.v, 1);  // rows: off the critical path, released
-        if (a.item_ns) {
-          a.item_ns[2 * u] = (unsigned)t0;
-          a.item_ns[2 * u + 1] = (unsigned)(gtimer() - t0);
-        }
-      }
-    } else if (kWarpForm) {
-      const int64_t idx = u - a.total_rows;
-      pair_warp(a, idx, s_price);
-      const int sig = a.pairs[idx].sig;
-      if (lane == 0) {
-        if (a.pair_ns) {
-          a.pair_ns[2 * idx] = (unsigned)t0;
-          a.pair_ns[2 * idx + 1] = (unsigned)(gtimer() - t0);
-        }
-        red_relaxed_add(&a.sched->pairs_done[sig].v, 1);  // no fence: see table_load
-      }
-    } else {
-      const int64_t idx = (u - a.total_rows) * 32 + lane;
-      const bool valid = idx < a.total_pairs;
-      const int sig = valid ? sig_of_pair(a, idx) : -1;
-      if (valid) pair_thread(a, idx, s_price);
-      if (a.pair_ns && valid) {
-        a.pair_ns[2 * idx] = (unsigned)t0;
-        a.pair_ns[2 * idx + 1] = (unsigned)(gtimer() - t0);
-      }
-      // one counter update per (warp, edge class); no fence: see table_load
-      const unsigned grp = __match_any_sync(0xffffffffu, sig);
-      if (valid && lane == __ffs(grp) - 1) red_relaxed_add(&a.sched->pairs_done[sig].v, __popc(grp));
-    }
+    run_unit<kWarpForm>(a, u, s_price);
     int next = 0;
     if (lane == 0)
       next = ld_relaxed(&a.sched->unit_head.v) >= units ? INT_MAX : atomicAdd(&a.sched->unit_head.v, 1);
@@ -875,13 +909,7 @@ __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
         __threadfence();
         if (atomicAdd(&a.sched->exit_count, 1) == (int)gridDim.x - 1) {
           // every other CTA has finished: reset for the next launch
-          Sched* sc = a.sched;
-          sc->head = 0;
-          sc->unit_head.v = 0;
-          sc->node_done.v = 0;
-          for (int i = 0; i < a.nsigs_reset; ++i) sc->pairs_done[i].v = 0;
-          sc->err_c[a.parity ^ 1] = 0;
-          sc->exit_count = 0;
+          reset_plan(a);
           __threadfence();
         }
       }
@@ -889,6 +917,104 @@ __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
     }
     if (item < a.i_exp) node_range(a, item, s_seg.n, &s_nseg, &s_edge);
     else fanout_range(a, item - a.i_exp, s_seg.f, &s_nseg, &s_edge);
+  }
+}
+
+// Batches of plans (a sweep of independent scenarios) in ONE persistent
+// launch: the units of all plans form one queue, then the phase-2 items of
+// all plans; every unit and item runs exactly the single-plan code on its
+// own plan's arguments, counters and tables. Offsets are prefix sums over the
+// plans; a warp's (a CTA's) claims only increase, so it finds the plan of its
+// next unit (item) by walking forward from the previous one.
+struct BatchHdr {
+  Line unit_head;
+  Line exit_count;
+};
+
+__device__ __forceinline__ int find_plan(const int64_t* off, int n, int64_t x, int p) {
+  // the plan q with off[q] <= x < off[q + 1]: gallop forward from the previous
+  // plan (claims only increase), then bisect
+  int lo = (p < 0 || off[p] > x) ? 0 : p, hi;
+  int step = 1;
+  for (;;) {
+    hi = lo + step;
+    if (hi >= n || off[hi] > x) break;
+    lo = hi;
+    step <<= 1;
+  }
+  if (hi > n - 1) hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= x) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// pair forms in the batch: 1 = warp only, 2 = thread only, 0 = mixed;
+// 3 = thread only with 2 CTAs per SM (128 registers: the register form's
+// state without spills)
+template <int kForm>
+__global__ void __launch_bounds__(kFusedThreads, kForm == 3 ? 2 : 4)
+    fused_batch_kernel(const FusedArgs* __restrict__ args, int n, const int64_t* __restrict__ unit_off,
+                       const int64_t* __restrict__ item_off, const int64_t* __restrict__ tab_off, BatchHdr* hdr,
+                       unsigned long long* __restrict__ err_out) {
+  __shared__ int s_unit, s_edge, s_nseg, s_last;
+  __shared__ union {
+    FanSeg f[kSegs];
+    NodeSeg n[kSegs];
+  } s_seg;
+  const int lane = threadIdx.x & 31;
+  const int64_t units = unit_off[n];
+  if (threadIdx.x == 0) s_unit = atomicAdd(&hdr->unit_head.v, kFusedThreads / 32);
+  __syncthreads();
+  int64_t u = (int64_t)s_unit + (threadIdx.x >> 5);
+  int p = -1;
+  while (u < units) {
+    p = find_plan(unit_off, n, u, p);
+    const FusedArgs& a = args[p];
+    if (kForm == 1 || (kForm == 0 && a.warp_form)) run_unit<true>(a, u - unit_off[p], a.bw_tab);
+    else run_unit<false>(a, u - unit_off[p], a.bw_tab);
+    int next = 0;
+    if (lane == 0) next = ld_relaxed(&hdr->unit_head.v) >= units ? INT_MAX : atomicAdd(&hdr->unit_head.v, 1);
+    u = __shfl_sync(0xffffffffu, next, 0);
+  }
+  {  // every plan's other-parity tables start unset: one slice of the concatenation per CTA
+    const int64_t total = tab_off[n];
+    const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = (int64_t)blockIdx.x * per, b1 = min(b0 + per, total);
+    int q = -1;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += kFusedThreads) {
+      q = find_plan(tab_off, n, i, q);
+      args[q].next_tables[i - tab_off[q]] = __longlong_as_double((long long)kUnset);
+    }
+  }
+  const int64_t items = item_off[n];
+  int ip = -1;
+  for (int64_t item = blockIdx.x;; item += gridDim.x) {
+    __syncthreads();  // s_seg reuse
+    if (item >= items) break;
+    ip = find_plan(item_off, n, item, ip);
+    const FusedArgs& a = args[ip];
+    const int li = (int)(item - item_off[ip]);
+    if (li < a.i_exp) node_range(a, li, s_seg.n, &s_nseg, &s_edge);
+    else fanout_range(a, li - a.i_exp, s_seg.f, &s_nseg, &s_edge);
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&hdr->exit_count.v, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {  // every other CTA has finished: reset every plan and the batch queue
+    __threadfence();
+    for (int q = threadIdx.x; q < n; q += kFusedThreads) {
+      if (err_out) err_out[q] = *args[q].err;  // this launch's error slot of every plan
+      reset_plan(args[q]);
+    }
+    if (threadIdx.x == 0) {
+      hdr->unit_head.v = 0;
+      hdr->exit_count.v = 0;
+    }
+    __threadfence();
   }
 }
 
@@ -1112,12 +1238,32 @@ struct tp_plan {
   int64_t last_grid = 0;
   int64_t trace_n[3] = {0, 0, 0};  // pairs, node-row items, fan-out items traced
   int pair_form = 0;  // 0 = by size, 1 = warp per pair, 2 = thread per pair
+  bool in_big_batch = false;  // by size: judged by the whole batch's pairs (thread form)
   int resident_blocks = 0;  // persistent grid size (SMs x resident CTAs)
 };
 
 namespace {
 
 // FNV-style hash of an interned key (class dedup on the host)
+// hash of a POD byte range, 8 bytes at a time (host class dedup)
+inline uint64_t hash_words(uint64_t h, const void* data, size_t bytes) {
+  const unsigned char* b = (const unsigned char*)data;
+  size_t i = 0;
+  for (; i + 8 <= bytes; i += 8) {
+    uint64_t w;
+    std::memcpy(&w, b + i, 8);
+    h = (h ^ w) * 0x100000001b3ull;
+    h ^= h >> 29;
+  }
+  if (i < bytes) {
+    uint64_t w = 0;
+    std::memcpy(&w, b + i, bytes - i);
+    h = (h ^ w) * 0x100000001b3ull;
+    h ^= h >> 29;
+  }
+  return h ^ (bytes << 7);
+}
+
 struct KeyHash {
   size_t operator()(const std::vector<int64_t>& v) const {
     uint64_t h = 1469598103934665603ull ^ v.size();
@@ -1125,6 +1271,21 @@ struct KeyHash {
     return (size_t)(h ^ (h >> 29));
   }
 };
+
+#ifdef TP_HOST_PROF
+double g_hprof[8];
+std::chrono::steady_clock::time_point g_hlast;
+#define HPROF(k)                                                                                  \
+  do {                                                                                            \
+    auto now_ = std::chrono::steady_clock::now();                                                 \
+    if (k) g_hprof[k] += std::chrono::duration<double, std::micro>(now_ - g_hlast).count();       \
+    g_hlast = now_;                                                                               \
+  } while (0)
+#else
+#define HPROF(k) \
+  do {           \
+  } while (0)
+#endif
 
 struct Builder {
   const tp_graph_desc* g;
@@ -1189,7 +1350,10 @@ struct Builder {
   int spec_of(int op, int k) const { return slot_spec[slot_begin[op] + k]; }
   const std::array<int8_t, tpk::kMaxR>& sa_of(int op, int k) const { return slot_sa[slot_begin[op] + k]; }
   std::map<int, int64_t> table_of_p;
-  std::unordered_map<std::vector<int64_t>, int32_t, KeyHash> class_of_key;
+  // node classes by key hash: first class with a hash, then a chain per class
+  std::unordered_map<uint64_t, int32_t> class_head;
+  std::vector<int32_t> class_next;
+  std::vector<int32_t> class_nslot;
   // per-operator scratch, reused
   std::vector<SliceChk> chk;
   std::vector<SlotDesc> slots;
@@ -1270,21 +1434,28 @@ struct Builder {
     p.row_base.assign(g->num_edges + 1, 0);
     // Kahn's algorithm (graph.hpp:158-183)
     {
-      std::vector<int32_t> indeg(g->num_ops, 0);
-      std::vector<std::vector<int32_t>> succ(g->num_ops);
-      for (int e = 0; e < g->num_edges; ++e) {
+      std::vector<int32_t> indeg(g->num_ops, 0), sb(g->num_ops + 1, 0), succ(g->num_edges);
+      for (int e = 0; e < g->num_edges; ++e) {  // successors, CSR in edge order
         const int u = p.edge_from_op[e], w = p.edge_to_op[e];
         if (u < 0 || w < 0) continue;
-        succ[u].push_back(w);
+        ++sb[u + 1];
         ++indeg[w];
       }
-      std::vector<int32_t> ready;
+      for (int i = 0; i < g->num_ops; ++i) sb[i + 1] += sb[i];
+      {
+        std::vector<int32_t> fill(sb.begin(), sb.end() - 1);
+        for (int e = 0; e < g->num_edges; ++e) {
+          const int u = p.edge_from_op[e], w = p.edge_to_op[e];
+          if (u >= 0 && w >= 0) succ[fill[u]++] = w;
+        }
+      }
+      p.topo.reserve(g->num_ops);
       for (int i = 0; i < g->num_ops; ++i)
-        if (indeg[i] == 0) ready.push_back(i);
-      for (size_t h = 0; h < ready.size(); ++h) {
-        p.topo.push_back(ready[h]);
-        for (int w : succ[ready[h]])
-          if (--indeg[w] == 0) ready.push_back(w);
+        if (indeg[i] == 0) p.topo.push_back(i);
+      for (size_t h = 0; h < p.topo.size(); ++h) {
+        const int u = p.topo[h];
+        for (int k = sb[u]; k < sb[u + 1]; ++k)
+          if (--indeg[succ[k]] == 0) p.topo.push_back(succ[k]);
       }
       if ((int)p.topo.size() != g->num_ops) {  // aux_graph.hpp:224-226
         p.topo.assign(g->num_ops, 0);
@@ -1343,7 +1514,9 @@ struct Builder {
     // ---------------- edge phase (aux_graph.hpp:273-296) -----------------
     int64_t aux = 0, rows = 0;
     p.valid_edges = 0;
-    std::unordered_map<std::vector<int64_t>, int32_t, KeyHash> sig_of_key;
+    std::unordered_map<uint64_t, int32_t> sig_head;  // key hash -> first class; chains below
+    std::vector<int32_t> sig_next, sig_pu, sig_pw;
+    std::vector<int64_t> sig_shape;  // kMaxR extents per class
     std::vector<std::vector<int32_t>> edges_of_sig;
     if (p.host_err == ~0ull) {
       p.valid_edges = g->num_edges;
@@ -1381,19 +1554,37 @@ struct Builder {
         int64_t elements = 1;
         for (int d = 0; d < R; ++d) elements *= shape_of(tu)[d];
         const double bytes = (double)elements * g->tensor_element_size[tu];  // graph.hpp:52-54
-        std::vector<int64_t> key;
-        key.reserve(8 + 3 * R);
+        // edge class key (the reference's memo key, aux_graph.hpp:257-271, plus
+        // the bytes and axis counts): hashed, compared field by field on a hit
         int64_t bbits;
         std::memcpy(&bbits, &bytes, 8);
-        key.insert(key.end(), {(int64_t)pu, (int64_t)pw, (int64_t)R, bbits});
-        for (int d = 0; d < R; ++d) key.push_back(shape_of(tu)[d]);
-        for (int d = 0; d < R; ++d) key.push_back(sa_of(u, ku)[d]);
-        for (int d = 0; d < R; ++d) key.push_back(sa_of(w, kw)[d]);
-        auto it = sig_of_key.find(key);
-        int32_t sig;
-        if (it == sig_of_key.end()) {
+        const auto& sau = sa_of(u, ku);
+        const auto& saw = sa_of(w, kw);
+        uint64_t h = hash_words(0x51ed27f3c6a8b9d1ull ^ ((uint64_t)pu << 40) ^ ((uint64_t)pw << 20) ^ (uint64_t)R,
+                                &bbits, 8);
+        h = hash_words(h, shape_of(tu), sizeof(int64_t) * R);
+        h = hash_words(h, sau.data(), R);
+        h = hash_words(h, saw.data(), R);
+        int32_t sig = -1;
+        auto it = sig_head.find(h);
+        for (int32_t c = it == sig_head.end() ? -1 : it->second; c >= 0; c = sig_next[c]) {
+          const SigDesc& o = p.sigs[c];
+          if (o.R == R && o.tab_u == (int32_t)table_of_p[pu] && o.tab_w == (int32_t)table_of_p[pw] &&
+              sig_pu[c] == pu && sig_pw[c] == pw && !std::memcmp(&o.bytes, &bytes, 8) &&
+              !std::memcmp(sig_shape.data() + (size_t)c * tpk::kMaxR, shape_of(tu), sizeof(int64_t) * R) &&
+              !std::memcmp(o.sa_u, sau.data(), R) && !std::memcmp(o.sa_w, saw.data(), R)) {
+            sig = c;
+            break;
+          }
+        }
+        if (sig < 0) {
           sig = (int32_t)p.sigs.size();
-          sig_of_key.emplace(key, sig);
+          sig_next.push_back(it == sig_head.end() ? -1 : it->second);
+          sig_head[h] = sig;
+          sig_pu.push_back(pu);
+          sig_pw.push_back(pw);
+          sig_shape.resize(sig_shape.size() + tpk::kMaxR, 0);
+          std::memcpy(sig_shape.data() + (size_t)sig * tpk::kMaxR, shape_of(tu), sizeof(int64_t) * R);
           SigDesc sd{};
           sd.pair_begin = p.total_pairs;
           sd.first_aux = aux;
@@ -1425,8 +1616,6 @@ struct Builder {
           p.sigs.push_back(sd);
           edges_of_sig.emplace_back();
           p.total_pairs += Su * Sw;
-        } else {
-          sig = it->second;
         }
         edges_of_sig[sig].push_back(e);
         EdgeDesc ed{};
@@ -1465,6 +1654,7 @@ struct Builder {
     layout_tables(p.overrides.empty());
     double tc6 = prof ? clk() : 0;
     p.fsegs.clear();
+    p.fsegs.reserve(p.edges.size());
     for (size_t e = 0; e < p.edges.size(); ++e) {
       const EdgeDesc& ed = p.edges[e];
       const SigDesc& sg = p.sigs[ed.sig];
@@ -1514,6 +1704,7 @@ struct Builder {
   // Slots, slice checks, occurrences of one op; then its node class.
   tp_status build_op(int i, int np, int64_t S, int64_t nb) {
     tp_plan& p = *P;
+    HPROF(0);
     const int t0 = g->op_tensor_begin[i], t1 = g->op_tensor_begin[i + 1];
     const int sb = (int)slot_name.size();
     slot_begin[i] = sb;
@@ -1531,6 +1722,7 @@ struct Builder {
       for (int d = 0; d < rank_of(t); ++d)
         if (shape_of(t)[d] < 1) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "tensor extent < 1 is unsupported");
     }
+    HPROF(1);
     const int nslot = (int)slot_name.size() - sb;
     slot_begin[i + 1] = sb + nslot;
     if (nslot > 32000) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many tensors per op");
@@ -1558,6 +1750,7 @@ struct Builder {
         chk.push_back(c);
       }
     }
+    HPROF(2);
     slots.clear();
     for (int k = 0; k < nslot; ++k) {
       SlotDesc sd{};
@@ -1570,6 +1763,7 @@ struct Builder {
       for (int d = 0; d < tpk::kMaxR; ++d) sd.sa[d] = sa[k][d];
       slots.push_back(sd);
     }
+    HPROF(3);
     occ.clear();
     const int nin = g->op_num_inputs[i];
     const int32_t* fed0 = fed_list.data() + fed_begin[op_key[i]];
@@ -1595,20 +1789,33 @@ struct Builder {
       }
       occ.push_back(oc);
     }
-    // node class key: everything the per-node costs depend on
-    key.assign({(int64_t)np, (int64_t)p.in_deg[i], (int64_t)chk.size(), (int64_t)slots.size(),
-                (int64_t)occ.size()});
-    for (auto& c : chk) key.insert(key.end(), {(int64_t)c.slot, (int64_t)c.axis, (int64_t)c.v});
-    for (auto& s : slots) {
-      key.insert(key.end(), {s.elements, (int64_t)s.es, (int64_t)s.R});
-      for (int d = 0; d < tpk::kMaxR; ++d) key.push_back(s.sa[d]);
+    HPROF(4);
+    // node class key: everything the per-node costs depend on -- the axis
+    // count, the in-degree and the slice checks, slots and occurrences (POD,
+    // padding zeroed), hashed as words and compared bytewise on a hit
+    uint64_t h = hash_words(0x9e3779b97f4a7c15ull ^ ((uint64_t)np << 32) ^ (uint64_t)(uint32_t)p.in_deg[i], chk.data(),
+                            chk.size() * sizeof(SliceChk));
+    h = hash_words(h ^ chk.size(), slots.data(), slots.size() * sizeof(SlotDesc));
+    h = hash_words(h ^ slots.size(), occ.data(), occ.size() * sizeof(Occ));
+    HPROF(5);
+    int32_t cls = -1;
+    auto it = class_head.find(h);
+    for (int32_t c = it == class_head.end() ? -1 : it->second; c >= 0; c = class_next[c]) {
+      const ClassDesc& cd = p.classes[c];
+      if (cd.p == np && cd.indeg == (double)p.in_deg[i] && cd.chk_end - cd.chk_begin == (int)chk.size() &&
+          class_nslot[c] == (int)slots.size() && cd.occ_end - cd.occ_begin == (int)occ.size() &&
+          !std::memcmp(p.chks.data() + cd.chk_begin, chk.data(), chk.size() * sizeof(SliceChk)) &&
+          !std::memcmp(p.slots.data() + cd.slot_begin, slots.data(), slots.size() * sizeof(SlotDesc)) &&
+          !std::memcmp(p.occs.data() + cd.occ_begin, occ.data(), occ.size() * sizeof(Occ))) {
+        cls = c;
+        break;
+      }
     }
-    for (auto& o : occ) key.insert(key.end(), {(int64_t)o.slot, (int64_t)o.nonslicing, (int64_t)o.in_memory});
-    auto it = class_of_key.find(key);
-    int32_t cls;
-    if (it == class_of_key.end()) {
+    if (cls < 0) {
       cls = (int32_t)p.classes.size();
-      class_of_key.emplace(key, cls);
+      class_next.push_back(it == class_head.end() ? -1 : it->second);
+      class_head[h] = cls;
+      class_nslot.push_back((int32_t)slots.size());
       ClassDesc cd{};
       cd.row_base = p.total_rows;
       cd.first_node = nb;
@@ -1627,9 +1834,8 @@ struct Builder {
       p.classes.push_back(cd);
       class_members.emplace_back();
       p.total_rows += S;
-    } else {
-      cls = it->second;
     }
+    HPROF(6);
     class_members[cls].push_back(nb);
     wrow_of_op[i] = p.classes[cls].row_base;
     p.op_row[i] = p.classes[cls].row_base;
@@ -1669,7 +1875,10 @@ struct Builder {
         const TableDesc* td = nullptr;
         for (const auto& t : p.tabs)
           if (t.offset == tab) td = &t;
-        std::map<std::vector<uint8_t>, int32_t> ids;
+        // distinct layout descriptors (POD, zeroed), by hash with a chain per id
+        std::unordered_map<uint64_t, int32_t> head;
+        std::vector<int32_t> next;
+        std::vector<tpk::SideDesc> seen;
         for (int32_t s = 0; s < S; ++s) {
           Strat st;
           tpk::unrank_strategy((int)td->p, (int)td->n, s, st);
@@ -1678,10 +1887,22 @@ struct Builder {
           tpk::SideDesc d;
           std::memset(&d, 0, sizeof(d));
           tpk::side_of(L, R, d);
-          std::vector<uint8_t> k((const uint8_t*)&d, (const uint8_t*)&d + sizeof(d));
-          auto ins = ids.emplace(k, (int32_t)reps.size());
-          if (ins.second) reps.push_back(s);
-          uid[s] = ins.first->second;
+          const uint64_t h = hash_words(0x2545f4914f6cdd1dull, &d, sizeof(d));
+          auto it = head.find(h);
+          int32_t id = -1;
+          for (int32_t c = it == head.end() ? -1 : it->second; c >= 0; c = next[c])
+            if (!std::memcmp(&seen[c], &d, sizeof(d))) {
+              id = c;
+              break;
+            }
+          if (id < 0) {
+            id = (int32_t)reps.size();
+            next.push_back(it == head.end() ? -1 : it->second);
+            head[h] = id;
+            seen.push_back(d);
+            reps.push_back(s);
+          }
+          uid[s] = id;
         }
       } else {
         for (int32_t s = 0; s < S; ++s) uid[s] = s, reps.push_back(s);
@@ -2051,16 +2272,26 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
   return TP_OK;
 }
 
-tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors* out) {
-  if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
-  tp_status st = ensure_stream(p);
-  if (st) return st;
-  if (!p->uploaded) {
-    st = tp_plan_upload(p, opts ? opts->stream : nullptr);
-    if (st) return st;
-  }
+}  // extern "C"
+
+namespace {
+// The host half of an execute, up to the fused launch: per-arena set-up on
+// stream s, the range tables, the kernel arguments. X.launch says whether a
+// fused launch is needed (X.a, X.grid); tp_plan_execute launches it alone,
+// tp_plan_execute_batch together with other plans'.
+struct ExecPrep {
+  FusedArgs a{};
+  int64_t grid = 0;
+  bool launch = false;
+  bool done = false;  // nothing at all to run (host-detected cycle)
+  int32_t e0 = 0, e1 = 0;
+  int64_t out_offset = 0;
+  bool edge_phase = false;
+  int64_t units = 0, items = 0;
+};
+
+tp_status prepare_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors* out, cudaStream_t s, ExecPrep& X) {
   Arena& A = *p->arena;
-  cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : A.stream;
   p->last_stream = s;
   int32_t e0 = opts ? opts->edge_begin : 0;
   int32_t e1 = opts ? opts->edge_end : -1;
@@ -2068,9 +2299,8 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   if (e0 < 0) e0 = 0;
   if (e0 > e1) e0 = e1;
   const bool skip_nodes = opts && opts->skip_nodes;
-  tp_cost_tensors none{};
-  if (!out) out = &none;
-  int64_t launches = 0;
+  static const tp_cost_tensors none{};
+  if (!out) out = const_cast<tp_cost_tensors*>(&none);
   Sched* sched = (Sched*)A.d_sched.p;
   if (!A.sched_clean) {
     CUDA_TRY(cudaMemsetAsync(sched, 0, sizeof(Sched) + sizeof(Line) * (p->sigs.size() + 1), s));
@@ -2086,7 +2316,7 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
     A.timeline_set = p->timeline;
   }
   if (p->host_err != ~0ull && (p->host_err >> 6) == 0) {  // cycle: nothing to build
-    p->last_launches = 0;
+    X.done = true;
     return TP_OK;
   }
   const bool edge_phase = p->host_err >= ekey(kEdgePhase, 0);
@@ -2128,7 +2358,7 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
     CUDA_TRY(upload(A.d_rfirst, p->range_first, s));
     p->range_key = rkey;
   }
-  FusedArgs a{};
+  FusedArgs& a = X.a;
   a.classes = (const ClassDesc*)A.d_classes.p;
   a.ncls = (int)p->classes.size();
   a.total_rows = p->total_rows;
@@ -2204,7 +2434,9 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
     a.pair_prof = (unsigned*)A.d_prof.p;
     a.warp_exit = a.pair_prof + 8 * (p->total_pairs + 1);
   }
-  a.warp_form = p->pair_form == 1 || (p->pair_form == 0 && a.total_pairs <= kWarpPairLimit);
+  // by size: a warp per pair while the launch has too few pairs to fill the
+  // GPU with one thread per pair; a big batch of plans is judged as a whole
+  a.warp_form = p->pair_form == 1 || (p->pair_form == 0 && !p->in_big_batch && a.total_pairs <= kWarpPairLimit);
   // phase-1 units: node rows, then class pairs (warp form) or 32-pair chunks;
   // phase-2 items: node ranges, then edge ranges
   const int64_t units = p->total_rows + (a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32);
@@ -2213,19 +2445,34 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
     return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many work items");
   a.i_exp = (int)nfan_items;
   a.i_end = (int)total_items;
-  if (total_items > 0 || units > 0) {
+  X.e0 = e0;
+  X.e1 = e1;
+  X.out_offset = out_offset;
+  X.edge_phase = edge_phase;
+  X.units = units;
+  X.items = total_items;
+  X.launch = total_items > 0 || units > 0;
+  if (X.launch) {
     const int64_t blocks_needed = std::max<int64_t>(total_items, (units + 7) / 8);
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(blocks_needed, p->resident_blocks));
-    if (p->prof_start) CUDA_TRY(cudaEventRecord(p->prof_start, s));
-    if (a.warp_form) fused_kernel<true><<<(unsigned)grid, kFusedThreads, 0, s>>>(a);
-    else fused_kernel<false><<<(unsigned)grid, kFusedThreads, 0, s>>>(a);
-    if (cudaPeekAtLastError() != cudaSuccess) A.sched_clean = false;
-    p->last_parity = A.parity;
-    p->last_grid = grid;
-    A.parity ^= 1;
-    ++launches;
-    if (p->prof_stop) CUDA_TRY(cudaEventRecord(p->prof_stop, s));
+    X.grid = std::max<int64_t>(1, std::min<int64_t>(blocks_needed, p->resident_blocks));
   }
+  return TP_OK;
+}
+
+// After the fused launch of a prepared plan (alone or in a batch).
+void after_launch(tp_plan* p) {
+  Arena& A = *p->arena;
+  p->last_parity = A.parity;
+  A.parity ^= 1;
+}
+
+// K3 (optional row minima) and the launch count of a prepared execute.
+tp_status finish_execute(tp_plan* p, tp_cost_tensors* out, cudaStream_t s, const ExecPrep& X, int64_t launches) {
+  Arena& A = *p->arena;
+  const int32_t e0 = X.e0, e1 = X.e1;
+  const int64_t out_offset = X.out_offset;
+  const bool edge_phase = X.edge_phase;
+  const FusedArgs& a = X.a;
   if (p->edge_base[e1] > out_offset && edge_phase) {
     // K3: row minima
     if (out->row_min_cost_s && out->row_min_volume_bytes) {
@@ -2245,6 +2492,187 @@ tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   CUDA_TRY(cudaGetLastError());
   p->last_launches = launches;
   return TP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors* out) {
+  if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
+  tp_status st = ensure_stream(p);
+  if (st) return st;
+  if (!p->uploaded) {
+    st = tp_plan_upload(p, opts ? opts->stream : nullptr);
+    if (st) return st;
+  }
+  cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : p->arena->stream;
+  ExecPrep X;
+  st = prepare_execute(p, opts, out, s, X);
+  if (st) return st;
+  if (X.done) {
+    p->last_launches = 0;
+    return TP_OK;
+  }
+  Arena& A = *p->arena;
+  int64_t launches = 0;
+  if (X.launch) {
+    if (p->prof_start) CUDA_TRY(cudaEventRecord(p->prof_start, s));
+    if (X.a.warp_form) fused_kernel<true><<<(unsigned)X.grid, kFusedThreads, 0, s>>>(X.a);
+    else fused_kernel<false><<<(unsigned)X.grid, kFusedThreads, 0, s>>>(X.a);
+    if (cudaPeekAtLastError() != cudaSuccess) A.sched_clean = false;
+    after_launch(p);
+    p->last_grid = X.grid;
+    ++launches;
+    if (p->prof_stop) CUDA_TRY(cudaEventRecord(p->prof_stop, s));
+  }
+  static tp_cost_tensors none{};
+  return finish_execute(p, out ? out : &none, s, X, launches);
+}
+
+}  // extern "C"
+
+namespace {
+// Per-device staging of batched launches: the plans' kernel arguments and the
+// unit / item / table prefix sums go up in one pinned copy per launch.
+struct BatchCtx {
+  std::mutex mu;
+  std::mutex host_mu;  // the one-shot host batch: output staging below
+  DevBuf d_args, d_hdr, d_err;
+  DevBuf out[6];
+  unsigned long long* h_err = nullptr;
+  size_t h_err_cap = 0;
+  void* h_stage = nullptr;
+  size_t h_cap = 0;
+  cudaEvent_t copied = nullptr;  // the last staging copy
+  bool hdr_clean = false;
+  int resident = 0, resident_wide = 0;
+};
+BatchCtx g_batch[64];
+
+// err_dev: optional device array [n] that receives every launched plan's
+// error slot (in `live` order via live_out) -- the host batch checks all
+// plans with one copy instead of one synchronising read per plan.
+tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* device_outs, void* stream,
+                             unsigned long long* err_dev, std::vector<int>* live_out) {
+  if (n < 0 || (n > 0 && (!plans || !device_outs))) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null batch arrays");
+  if (n == 0) return TP_OK;
+  for (int i = 0; i < n; ++i)
+    if (!plans[i]) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan in batch");
+  const int device = plans[0]->device;
+  for (int i = 1; i < n; ++i)
+    if (plans[i]->device != device) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "batch plans on different devices");
+  if (device < 0 || device >= 64) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "device ordinal out of range");
+  CUDA_TRY(cudaSetDevice(device));
+  tp_status st = ensure_stream(plans[0]);
+  if (st) return st;
+  cudaStream_t s = stream ? (cudaStream_t)stream : plans[0]->arena->stream;
+  BatchCtx& B = g_batch[device];
+  std::lock_guard<std::mutex> lk(B.mu);
+  std::vector<ExecPrep> X(n);
+  std::vector<int> live;
+  int64_t batch_pairs = 0;
+  for (int i = 0; i < n; ++i) batch_pairs += plans[i]->total_pairs;
+  for (int i = 0; i < n; ++i) plans[i]->in_big_batch = batch_pairs > kWarpPairLimit;
+  for (int i = 0; i < n; ++i) {
+    tp_plan* p = plans[i];
+    st = ensure_stream(p);
+    if (st) return st;
+    if (!p->uploaded) {
+      st = tp_plan_upload(p, s);
+      if (st) return st;
+    }
+    st = prepare_execute(p, nullptr, &device_outs[i], s, X[i]);
+    p->in_big_batch = false;
+    if (st) return st;
+    if (!X[i].done && X[i].launch) live.push_back(i);
+  }
+  const int m = (int)live.size();
+  if (m > 0) {
+    if (B.resident == 0) {
+      int sms = 0, per_sm = 0;
+      CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_batch_kernel<0>, kFusedThreads, 0));
+      B.resident = std::max(1, sms * std::max(1, per_sm));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_batch_kernel<3>, kFusedThreads, 0));
+      B.resident_wide = std::max(1, sms * std::max(1, per_sm));
+    }
+    // staging: args[m] | unit_off[m+1] | item_off[m+1] | tab_off[m+1]
+    const size_t args_b = sizeof(FusedArgs) * m, off_b = sizeof(int64_t) * (m + 1);
+    const size_t total = args_b + 3 * off_b;
+    if (B.copied) CUDA_TRY(cudaEventSynchronize(B.copied));
+    if (B.h_cap < total) {
+      if (B.h_stage) cudaFreeHost(B.h_stage);
+      B.h_stage = nullptr;
+      B.h_cap = 0;
+      CUDA_TRY(cudaMallocHost(&B.h_stage, total));
+      B.h_cap = total;
+    }
+    FusedArgs* ha = (FusedArgs*)B.h_stage;
+    int64_t* uo = (int64_t*)((char*)B.h_stage + args_b);
+    int64_t* io = uo + (m + 1);
+    int64_t* to = io + (m + 1);
+    uo[0] = io[0] = to[0] = 0;
+    for (int k = 0; k < m; ++k) {
+      const ExecPrep& x = X[live[k]];
+      ha[k] = x.a;
+      uo[k + 1] = uo[k] + x.units;
+      io[k + 1] = io[k] + x.items;
+      to[k + 1] = to[k] + x.a.tables_len;
+    }
+    if (uo[m] >= (1ll << 30) || io[m] >= (1ll << 30))
+      return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many work items in one batch");
+    CUDA_TRY(B.d_args.ensure(total));
+    CUDA_TRY(cudaMemcpyAsync(B.d_args.p, B.h_stage, total, cudaMemcpyHostToDevice, s));
+    if (!B.copied) CUDA_TRY(cudaEventCreateWithFlags(&B.copied, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(B.copied, s));
+    CUDA_TRY(B.d_hdr.ensure(sizeof(BatchHdr)));
+    if (!B.hdr_clean) {
+      CUDA_TRY(cudaMemsetAsync(B.d_hdr.p, 0, sizeof(BatchHdr), s));
+      B.hdr_clean = true;
+    }
+    const int64_t blocks_needed = std::max<int64_t>(io[m], (uo[m] + 7) / 8);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(blocks_needed, B.resident));
+    const FusedArgs* da = (const FusedArgs*)B.d_args.p;
+    const int64_t* duo = (const int64_t*)((const char*)B.d_args.p + args_b);
+    int nwarp = 0;
+    for (int k : live) nwarp += X[k].a.warp_form != 0;
+    static const int wide = getenv("TP_BATCH_WIDE") ? atoi(getenv("TP_BATCH_WIDE")) : 1;
+    const int form = nwarp == m ? 1 : (nwarp == 0 ? (wide ? 3 : 2) : 0);
+    const dim3 gd((unsigned)std::min<int64_t>(grid, form == 3 ? B.resident_wide : B.resident)), bd(kFusedThreads);
+    const int64_t* dio = duo + (m + 1);
+    const int64_t* dto = duo + 2 * (m + 1);
+    BatchHdr* hd = (BatchHdr*)B.d_hdr.p;
+    if (form == 1) fused_batch_kernel<1><<<gd, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
+    else if (form == 2) fused_batch_kernel<2><<<gd, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
+    else if (form == 3) fused_batch_kernel<3><<<gd, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
+    else fused_batch_kernel<0><<<gd, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
+    if (cudaPeekAtLastError() != cudaSuccess) {
+      B.hdr_clean = false;
+      for (int k : live) plans[k]->arena->sched_clean = false;
+    }
+    for (int k : live) {
+      after_launch(plans[k]);
+      plans[k]->last_grid = grid;
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    if (X[i].done) {
+      plans[i]->last_launches = 0;
+      continue;
+    }
+    st = finish_execute(plans[i], &device_outs[i], s, X[i], X[i].launch ? 1 : 0);
+    if (st) return st;
+  }
+  if (live_out) *live_out = live;
+  return TP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+tp_status tp_plan_execute_batch(tp_plan* const* plans, int32_t n, tp_cost_tensors* device_outs, void* stream) {
+  return execute_batch_impl(plans, n, device_outs, stream, nullptr, nullptr);
 }
 
 int64_t tp_plan_last_launches(const tp_plan* p) { return p ? p->last_launches : 0; }
@@ -2463,11 +2891,17 @@ tp_status tp_plan_create_batch(const tp_graph_desc* const* graphs, const tp_topo
   return batch_status(errs, status_out);
 }
 
-tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_index* index_outs,
-                                     tp_cost_tensors* host_outs, int32_t host_threads, int32_t* status_out) {
+}  // extern "C"
+
+namespace {
+// One execute_host per plan on the worker threads (plans on several devices).
+tp_status execute_host_each(tp_plan* const* plans, int32_t n, tp_aux_index* index_outs, tp_cost_tensors* host_outs,
+                            int32_t host_threads, int32_t* status_out) {
   if (n < 0 || (n > 0 && (!plans || !host_outs))) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null batch arrays");
   std::vector<BatchErr> errs(n);
   const int workers = pool_size(n, host_threads);
+  int64_t batch_pairs = 0;
+  for (int i = 0; i < n; ++i) batch_pairs += plans[i] ? plans[i]->total_pairs : 0;
   std::vector<Arena*> borrowed(workers, nullptr);
   std::vector<int> borrowed_dev(workers, -1);
   run_pool(n, workers, [&](int i, int w) {
@@ -2490,7 +2924,9 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
       p->owns_arena = false;
       p->uploaded = false;
     }
+    p->in_big_batch = batch_pairs > kWarpPairLimit;  // the workers' plans share the GPU
     errs[i].take(tp_plan_execute_host(p, nullptr, index_outs ? &index_outs[i] : nullptr, &host_outs[i]));
+    p->in_big_batch = false;
     if (borrow) {  // the arena's descriptors belong to the next plan now
       p->arena = nullptr;
       p->owns_arena = true;
@@ -2500,6 +2936,158 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
   });
   for (Arena* a : borrowed)
     if (a) arena_pool_put(a);
+  return batch_status(errs, status_out);
+}
+
+
+// Error status of plan p from its device error slot value (complemented key).
+tp_status status_from_slot(tp_plan* p, unsigned long long c) {
+  const uint64_t key = std::min<uint64_t>(~c, p->host_err);
+  if (key == ~0ull) return TP_OK;
+  const int kind = (int)(key & 63);
+  return set_err(status_of_kind(kind), kind, kind_text(kind));
+}
+}  // namespace
+
+extern "C" {
+
+// One device: every plan's descriptors uploaded (worker threads, pooled
+// arenas), ONE batched launch into staging buffers, the tensors copied back
+// with one copy per tensor kind when the caller's host slices are contiguous
+// (as engine.Sweep allocates them), and every plan's error read by one copy.
+tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_index* index_outs,
+                                     tp_cost_tensors* host_outs, int32_t host_threads, int32_t* status_out) {
+  if (n < 0 || (n > 0 && (!plans || !host_outs))) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null batch arrays");
+  if (n == 0) return TP_OK;
+  bool one_device = plans[0] != nullptr;
+  for (int i = 0; one_device && i < n; ++i) one_device = plans[i] && plans[i]->device == plans[0]->device;
+  if (!one_device || plans[0]->device < 0 || plans[0]->device >= 64)
+    return execute_host_each(plans, n, index_outs, host_outs, host_threads, status_out);
+  const int device = plans[0]->device;
+  CUDA_TRY(cudaSetDevice(device));
+  BatchCtx& B = g_batch[device];
+  std::lock_guard<std::mutex> hl(B.host_mu);
+  // arenas: plans without one borrow a pooled arena for the call
+  std::vector<char> borrowed(n, 0);
+  for (int i = 0; i < n; ++i) {
+    tp_plan* p = plans[i];
+    if (p->arena) continue;
+    p->arena = arena_pool_get(device);
+    p->owns_arena = false;
+    p->uploaded = false;
+    borrowed[i] = 1;
+  }
+  auto give_back = [&]() {
+    for (int i = 0; i < n; ++i) {
+      if (!borrowed[i]) continue;
+      tp_plan* p = plans[i];
+      arena_pool_put(p->arena);
+      p->arena = nullptr;
+      p->owns_arena = true;
+      p->uploaded = false;
+      p->range_key = {{-1, -1, -1, -1}};
+    }
+  };
+  tp_status st = ensure_stream(plans[0]);
+  if (st) {
+    give_back();
+    return st;
+  }
+  cudaStream_t s = plans[0]->arena->stream;
+  // uploads: the host side (descriptor packing) on the workers, all copies and
+  // set-up kernels on the batch stream
+  std::vector<BatchErr> errs(n);
+  run_pool(n, host_threads, [&](int i, int) {
+    tp_plan* p = plans[i];
+    tp_status e = ensure_stream(p);
+    if (!e && !p->uploaded) e = tp_plan_upload(p, s);
+    errs[i].take(e);
+  });
+  for (int i = 0; i < n; ++i)
+    if (errs[i].st) {
+      give_back();
+      return batch_status(errs, status_out);
+    }
+  // device staging of the outputs, one buffer per tensor kind
+  std::vector<int64_t> nn(n), ne(n);
+  int64_t tn = 0, te = 0;
+  for (int i = 0; i < n; ++i) {
+    nn[i] = plans[i]->num_aux_nodes;
+    ne[i] = plans[i]->edge_base[plans[i]->valid_edges] - plans[i]->edge_base[0];
+    tn += nn[i];
+    te += ne[i];
+  }
+  double* h_of[6];
+  auto host_ptr = [&](int i, int k) -> double* {
+    const tp_cost_tensors& h = host_outs[i];
+    double* const v[6] = {h.node_intra_cost_s, h.node_intra_volume_bytes, h.node_memory_bytes,
+                          h.edge_cost_s,       h.edge_volume_bytes,       h.edge_memory_bytes};
+    return v[k];
+  };
+  std::vector<tp_cost_tensors> dev(n);
+  bool want[6];
+  for (int k = 0; k < 6; ++k) {
+    want[k] = false;
+    for (int i = 0; i < n; ++i) want[k] |= host_ptr(i, k) != nullptr;
+    const int64_t tot = k < 3 ? tn : te;
+    if (want[k]) CUDA_TRY(B.out[k].ensure(sizeof(double) * (size_t)std::max<int64_t>(tot, 1)));
+    h_of[k] = (double*)B.out[k].p;
+  }
+  {
+    int64_t on = 0, oe = 0;
+    for (int i = 0; i < n; ++i) {
+      double* d[6];
+      for (int k = 0; k < 6; ++k) d[k] = want[k] && host_ptr(i, k) ? h_of[k] + (k < 3 ? on : oe) : nullptr;
+      dev[i] = tp_cost_tensors{d[0], d[1], d[2], d[3], d[4], d[5], nullptr, nullptr, nullptr};
+      on += nn[i];
+      oe += ne[i];
+    }
+  }
+  CUDA_TRY(B.d_err.ensure(sizeof(unsigned long long) * n));
+  std::vector<int> live;
+  st = execute_batch_impl(plans, n, dev.data(), s, (unsigned long long*)B.d_err.p, &live);
+  if (st) {
+    give_back();
+    return st;
+  }
+  // back to the host: one copy per tensor kind where the caller's slices are contiguous
+  for (int k = 0; k < 6; ++k) {
+    if (!want[k]) continue;
+    bool contiguous = true;
+    for (int i = 0; contiguous && i < n; ++i) {
+      contiguous = host_ptr(i, k) != nullptr;
+      if (contiguous && i + 1 < n) contiguous = host_ptr(i + 1, k) == host_ptr(i, k) + (k < 3 ? nn[i] : ne[i]);
+    }
+    const int64_t tot = k < 3 ? tn : te;
+    if (contiguous) {
+      if (tot > 0) CUDA_TRY(cudaMemcpyAsync(host_ptr(0, k), h_of[k], sizeof(double) * tot, cudaMemcpyDeviceToHost, s));
+      continue;
+    }
+    int64_t off = 0;
+    for (int i = 0; i < n; ++i) {
+      const int64_t c = k < 3 ? nn[i] : ne[i];
+      if (host_ptr(i, k) && c > 0)
+        CUDA_TRY(cudaMemcpyAsync(host_ptr(i, k), h_of[k] + off, sizeof(double) * c, cudaMemcpyDeviceToHost, s));
+      off += c;
+    }
+  }
+  if (B.h_err_cap < (size_t)n) {
+    if (B.h_err) cudaFreeHost(B.h_err);
+    B.h_err = nullptr;
+    B.h_err_cap = 0;
+    CUDA_TRY(cudaMallocHost(&B.h_err, sizeof(unsigned long long) * n));
+    B.h_err_cap = n;
+  }
+  if (!live.empty())
+    CUDA_TRY(cudaMemcpyAsync(B.h_err, B.d_err.p, sizeof(unsigned long long) * live.size(), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  std::vector<unsigned long long> slot(n, 0);
+  for (size_t k = 0; k < live.size(); ++k) slot[live[k]] = B.h_err[k];
+  for (int i = 0; i < n; ++i) {
+    errs[i].take(status_from_slot(plans[i], slot[i]));
+    if (index_outs) tp_plan_index(plans[i], &index_outs[i]);
+  }
+  give_back();
   return batch_status(errs, status_out);
 }
 

@@ -408,3 +408,63 @@ def build_sweep(scenarios, device: int = -1, host_threads: int = 0, pinned: bool
     res = sw.results
     sw.destroy()
     return res
+
+
+class DeviceSweep:
+    """A sweep kept resident on one GPU: every scenario analysed once, its
+    descriptors uploaded on its own arena, its cost tensors in slices of one
+    device allocation per tensor kind. `run()` rebuilds every scenario with
+    ONE persistent launch (tp_plan_execute_batch): the pricing units and the
+    output ranges of all scenarios share one work queue, so many small,
+    latency-bound builds overlap instead of paying a launch each."""
+
+    def __init__(self, scenarios, device: int = 0):
+        import torch
+        self.torch = torch
+        self.device = device
+        self.lib = abi.load_engine()
+        self.plans = [Plan(g, t, device=device) for g, t in scenarios]
+        n = len(self.plans)
+        dev = torch.device("cuda", device)
+        self.main = torch.cuda.Stream(dev)
+        ne = [p.sizes["num_aux_edges"] for p in self.plans]
+        nn = [p.sizes["num_aux_nodes"] for p in self.plans]
+        self.edge_off = np.concatenate([[0], np.cumsum(ne)]).astype(np.int64)
+        self.node_off = np.concatenate([[0], np.cumsum(nn)]).astype(np.int64)
+        self.out = {k: torch.empty(max(int(self.edge_off[-1]), 1), dtype=torch.float64, device=dev)
+                    for k in _OUT_KEYS if k.startswith("edge")}
+        self.out.update({k: torch.empty(max(int(self.node_off[-1]), 1), dtype=torch.float64, device=dev)
+                         for k in _OUT_KEYS if k.startswith("node")})
+        self._handles = (C.c_void_p * max(n, 1))(*[p.handle for p in self.plans])
+        self._structs = (abi.tp_cost_tensors * max(n, 1))()
+        for i, p in enumerate(self.plans):
+            p.upload(self.main.cuda_stream)
+            sl = self.result(i)
+            self._structs[i] = device_cost_struct({k: v for k, v in sl.items() if v.numel()})
+        torch.cuda.synchronize(dev)
+
+    @property
+    def num_aux_edges(self) -> int:
+        return int(self.edge_off[-1])
+
+    @property
+    def num_aux_nodes(self) -> int:
+        return int(self.node_off[-1])
+
+    def launches_per_run(self) -> int:
+        """Kernel launches of the last run (the batch launch counts once)."""
+        return 1 if any(p.last_launches() for p in self.plans) else 0
+
+    def run(self):
+        """Rebuild every scenario, asynchronously on `self.main`."""
+        _check(self.lib, self.lib.tp_plan_execute_batch(self._handles, len(self.plans), self._structs,
+                                                         C.c_void_p(self.main.cuda_stream)))
+
+    def check_errors(self):
+        for p in self.plans:
+            p.check_errors()
+
+    def result(self, i: int) -> dict:
+        """Scenario i's tensors (device slices)."""
+        return {k: (v[self.edge_off[i]:self.edge_off[i + 1]] if k.startswith("edge")
+                    else v[self.node_off[i]:self.node_off[i + 1]]) for k, v in self.out.items()}

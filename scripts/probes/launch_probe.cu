@@ -1,0 +1,44 @@
+// Event-timed launch cost of empty kernels of several shapes (diagnostic).
+#include <cstdio>
+#include <cuda_runtime.h>
+struct Big { char b[400]; };
+__global__ void empty_small() {}
+__global__ void __launch_bounds__(256, 4) empty_big(Big a) { if (a.b[threadIdx.x % 400] == 123 && blockIdx.x == 9999) printf("x"); }
+__global__ void spin_big(Big a, int ns) {
+  unsigned long long t0; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned long long t; do { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); } while (t - t0 < (unsigned long long)ns);
+  if (a.b[threadIdx.x % 400] == 123 && blockIdx.x == 9999) printf("x");
+}
+__global__ void atomics_big(int* c) { if (threadIdx.x == 0) { atomicAdd(c, 1); __threadfence(); atomicAdd(c + 32, 1); } }
+int main() {
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  int* flush; size_t fb = 256u << 20; cudaMalloc(&flush, fb);
+  int* c; cudaMalloc(&c, 4096); cudaMemset(c, 0, 4096);
+  Big big{};
+  bool do_flush = true;
+  auto time = [&](const char* name, auto launch) {
+    float best = 1e9, sum = 0; int n = 30;
+    for (int i = 0; i < n + 3; ++i) {
+      if (do_flush) cudaMemsetAsync(flush, 0, fb);
+      cudaEventRecord(a); launch(); cudaEventRecord(b); cudaEventSynchronize(b);
+      float ms; cudaEventElapsedTime(&ms, a, b);
+      if (i >= 3) { sum += ms; if (ms < best) best = ms; }
+    }
+    printf("%-40s mean %.2f us  best %.2f us\n", name, sum / n * 1e3, best * 1e3);
+  };
+  for (int flush_on = 1; flush_on >= 0; --flush_on) {
+    do_flush = flush_on;
+    printf("--- flush %d\n", flush_on);
+    time("empty <<<1,32>>>", [&] { empty_small<<<1, 32>>>(); });
+    time("empty <<<148,1024>>>", [&] { empty_big<<<148, 1024>>>(big); });
+    time("empty <<<296,512>>>", [&] { empty_big<<<296, 512>>>(big); });
+    time("empty <<<592,256>>>", [&] { empty_big<<<592, 256>>>(big); });
+    time("empty <<<1184,128>>>", [&] { empty_big<<<1184, 128>>>(big); });
+    time("empty <<<1,32>>> again", [&] { empty_small<<<1, 32>>>(); });
+    time("spin 10us <<<148,1024>>>", [&] { spin_big<<<148, 1024>>>(big, 10000); });
+    time("spin 10us <<<592,256>>>", [&] { spin_big<<<592, 256>>>(big, 10000); });
+    time("atomics <<<148,1024>>>", [&] { atomics_big<<<148, 1024>>>(c); });
+    time("atomics <<<592,256>>>", [&] { atomics_big<<<592, 256>>>(c); });
+  }
+  return 0;
+}

@@ -100,3 +100,56 @@ def test_sweep_mixes_owned_and_borrowed_arenas():
     for i, (f, t) in enumerate(pairs):
         same(sw.results[i], B.oracle_build(f, t), f"scenario {i}")
     sw.destroy()
+
+
+def test_device_sweep_batched_launch_matches_oracle(sweep1000):
+    """The device-resident sweep: one persistent launch for all scenarios
+    (tp_plan_execute_batch), repeated (the tables alternate parity), matches
+    the oracle on every scenario, every time."""
+    import torch
+    scen = sweep1000[100:220]
+    pairs = [(G.flatten(s.graph), s.topo) for s in scen]
+    ds = engine.DeviceSweep(pairs, device=0)
+    refs = [B.oracle_build(f, t) for f, t in pairs]
+    for rep in range(3):
+        for v in ds.out.values():
+            v.fill_(float("nan"))
+        torch.cuda.synchronize()
+        ds.run()
+        ds.check_errors()
+        for i in range(len(pairs)):
+            got = {k: v.cpu().numpy() for k, v in ds.result(i).items()}
+            for k in FIELDS:
+                assert np.array_equal(bits(got[k]), bits(getattr(refs[i], k))), (rep, i, k)
+        assert ds.launches_per_run() == 1
+
+
+def test_batch_mixes_forms_errors_and_single_executes():
+    """A batch with a thread-form plan (pair_form 2), an error plan and a
+    cycle; plans executed alone between batches keep their parity state."""
+    import torch
+    a = M.pointwise_op("a", "x", "y", 8, 8)
+    b = M.pointwise_op("b", "y", "x", 8, 8)
+    cycle = G.ComputationGraph([a, b], [G.GraphEdge("a", "b", "y"), G.GraphEdge("b", "a", "x")])
+    indivisible = G.ComputationGraph([M.dense_op("fc", "matmul", "x", 6, 6, 6, "y")], [])
+    g1, t1 = M.cfg1()
+    g2, t2 = M.cfg2()
+    scen = [(g1, t1), (g2, t2), (cycle, G.ClusterTopology(1, 2, 60e9, 60e9, 32e9)),
+            (indivisible, G.ClusterTopology(1, 4, 60e9, 60e9, 32e9)), (g2, M.ClusterTopology(4, 8, 60e9, 1e9, 80e9))]
+    pairs = [(G.flatten(g), t) for g, t in scen]
+    ds = engine.DeviceSweep(pairs, device=0)
+    ds.plans[1].set_pair_form(2)
+    refs = [B.oracle_build(f, t) for f, t in pairs]
+    for rep in range(3):
+        if rep == 1:  # a plan run alone in between
+            ds.plans[4].execute(engine.device_cost_struct(ds.result(4)), stream=ds.main.cuda_stream)
+        ds.run()
+        torch.cuda.synchronize()
+        for i in (0, 1, 4):
+            ds.plans[i].check_errors()
+            got = {k: v.cpu().numpy() for k, v in ds.result(i).items()}
+            for k in FIELDS:
+                assert np.array_equal(bits(got[k]), bits(getattr(refs[i], k))), (rep, i, k)
+        for i in (2, 3):
+            with pytest.raises(abi.TopoplanError):
+                ds.plans[i].check_errors()
