@@ -236,32 +236,48 @@ def run_reference_sweep(args, threads):
         f"host threads, one build_auxiliary_graph per scenario")
 
 
-def run_sweep(args):
-    """cfg5 through the batch entry points. value: device-resident (plans
-    analysed and uploaded, all scenarios rebuilt by one batched persistent
-    launch, CUDA events around it); e2e: host graphs in -> tp_plan_create_batch +
-    tp_plan_execute_host_batch -> pinned host tensors out, wall clock."""
+def init_dist(local, world):
     import torch
-    from paper_2301_04285_b200 import engine as E
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+    if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+        os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return dist
 
+
+def run_sweep(args):
+    import torch
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
-            os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = init_dist(local, world)
+    line = measure_sweep(args, rank, world, local, dist, args.steps, args.warmup, with_clocks=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_sweep(args, rank, world, local, dist, K, W, with_clocks=False):
+    """cfg5 through the batch entry points. value: device-resident (plans
+    analysed and uploaded, all scenarios rebuilt by one batched persistent
+    launch, CUDA events around it); e2e: host graphs in -> tp_plan_create_batch +
+    tp_plan_execute_host_batch -> pinned host tensors out, wall clock.
+    Returns rank 0's JSON line (None on the other ranks)."""
+    import torch
+    from paper_2301_04285_b200 import engine as E
     pairs, total_evals = sweep_scenarios(rank, world)
     dev = torch.device("cuda", local)
 
     # ---- device-resident: own plan + arena per scenario, one batched launch per step ----
     ds = E.DeviceSweep(pairs, device=local)
+    pair_evals = sum(int(p.sizes["num_pair_evals"]) for p in ds.plans)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
-    K, W = args.steps, args.warmup
-    clocks = Clocks(local)
+    clocks = Clocks(local) if with_clocks else None
     for _ in range(W):
         with torch.cuda.stream(ds.main):
             flush.zero_()
@@ -309,12 +325,10 @@ def run_sweep(args):
         dist.all_reduce(e2e_total, op=dist.ReduceOp.MAX)
     e2e_value = total_evals * KE / float(e2e_total.item())
     h2d = sum(int(sw.sizes(i)["h2d_bytes"]) for i in range(len(sw)))
-    clk = clocks.stop()
+    clk = clocks.stop() if clocks else None
     if rank != 0:
         sw.destroy()
-        if dist:
-            dist.destroy_process_group()
-        return 0
+        return None
     peak, peak_kind = measured_peak()
     out_bytes = BYTES_PER_EVAL * (int(eoff[-1]) + int(noff[-1]))
     achieved = out_bytes / (dev_ms / K / 1e3) / 1e9
@@ -324,7 +338,8 @@ def run_sweep(args):
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": "cfg5", "desc": "1,000 seeded (model, mesh, bandwidth-ratio) scenarios, "
                    "LPT-sharded over ranks (SURVEY §8d)", "scenarios_rank0": len(pairs),
-                   "aux_edges_total": total_evals, "parallelism": f"scenario-sharded x{world}",
+                   "aux_edges_total": total_evals, "class_pairs_rank0": pair_evals,
+                   "parallelism": f"scenario-sharded x{world}",
                    "l2": "256 MiB buffer written between timed steps (flush)",
                    "build_ms_e2e": sum(e2e_t) / KE * 1e3},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -344,11 +359,8 @@ def run_sweep(args):
             secs, n = B.reference_bench_sweep(sample, threads=1)
             line["cpu_baseline"] = {"value": n / secs, "unit": "evals/s", "cores": 1, "kind": "reference",
                                     "sample": f"every 10th scenario ({len(sample)}, {n} aux edges), one thread"}
-    print(json.dumps(line), flush=True)
     sw.destroy()
-    if dist:
-        dist.destroy_process_group()
-    return 0
+    return line
 
 
 def run_engine(args):
@@ -359,12 +371,7 @@ def run_engine(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
-            os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = init_dist(local, world)
 
     g, t, desc = workload(args.workload, rank)
     flat = G.flatten(g)
@@ -465,6 +472,18 @@ def run_engine(args):
             stream.synchronize()
     clk = clocks.stop()
 
+    # the cfg5 sweep alongside (BASELINE config 5): all ranks take part
+    sweep = None
+    if not args.no_sweep:
+        try:
+            sl = measure_sweep(args, rank, world, local, dist, min(K, 10), W)
+            if sl is not None:
+                sweep = {k: sl[k] for k in ("value", "unit", "ms_per_step", "scaling")}
+                sweep.update(config=sl["config"], e2e=sl["e2e"], roofline=sl["roofline"],
+                             gpu_launches=sl["gpu_launches"])
+        except Exception as ex:  # the headline line must still be printed
+            sweep = {"error": f"{type(ex).__name__}: {ex}"}
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -497,6 +516,7 @@ def run_engine(args):
                 "how": "tp_build_cost_tensors (host graph in, pinned host tensors out), wall clock"},
         "gpu_launches": int(launches * K),
         "clocks": clk,
+        "cfg5_sweep": sweep,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(flat, t, ne)
@@ -517,6 +537,7 @@ def main():
     ap.add_argument("--workload", default="cfg4", choices=("cfg1", "cfg2", "cfg3", "cfg4", "cfg5"))
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the cfg5 sweep block of the cfg4 line")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

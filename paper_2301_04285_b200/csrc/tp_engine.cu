@@ -1168,6 +1168,8 @@ struct Arena {
   size_t h_stage_cap = 0;
   cudaEvent_t stage_done = nullptr;  // the last pack copy out of h_stage
   bool sched_clean = false;  // Sched zero (set up, or left so by the last launch)
+  int64_t tables_L = -1;     // table layout (doubles per parity) the clean state is for
+  size_t sched_bytes = 0;
   bool timeline_set = false;
   int parity = 0;
   std::vector<std::array<int64_t, 4>> table_key;  // (offset, count, p, n) of the resident tables
@@ -2185,6 +2187,48 @@ tp_status tp_plan_index(const tp_plan* p, tp_aux_index* x) {
   return TP_OK;
 }
 
+namespace {
+// Persistent grid of the fused kernel on the plan's device (cached per device).
+int g_resident[64];
+tp_status resident_of(tp_plan* p) {
+  int& r = g_resident[p->device & 63];
+  if (r == 0) {
+    int sms = 0, per_sm = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<true>, kFusedThreads, 0));
+    r = std::max(1, sms * std::max(1, per_sm));
+  }
+  p->resident_blocks = r;
+  return TP_OK;
+}
+
+// Phase 2: the aux nodes and the edge range's aux edges cut into equal
+// ranges, one per resident CTA.
+void range_layout(const tp_plan* p, int64_t total_out, int64_t total_nodes, int64_t& range_len, int64_t& exp_items,
+                  int64_t& nfan_items) {
+  const int64_t nranges = std::max(1, p->resident_blocks - 2);  // the two ceilings below add at most 2
+  range_len = std::max<int64_t>(kFusedThreads * kFanPer, (total_out + total_nodes + nranges - 1) / nranges);
+  exp_items = (total_out + range_len - 1) / range_len;
+  nfan_items = (total_nodes + range_len - 1) / range_len;
+}
+
+// First edge / operator of every range.
+void fill_range_first(tp_plan* p, int32_t e0, int32_t e1, int64_t range_len, int64_t exp_items, int64_t nfan_items) {
+  const int64_t out_offset = p->edge_base[e0];
+  p->range_first.assign(exp_items + nfan_items, 0);
+  for (int64_t r = 0; r < exp_items; ++r) {
+    const int64_t start = out_offset + r * range_len;
+    auto it = std::upper_bound(p->edge_base.begin() + e0, p->edge_base.begin() + e1, start);
+    p->range_first[r] = (int32_t)(it - p->edge_base.begin()) - 1;
+  }
+  for (int64_t r = 0; r < nfan_items; ++r) {
+    const int64_t start = r * range_len;
+    auto it = std::upper_bound(p->node_base.begin(), p->node_base.begin() + p->num_ops, start);
+    p->range_first[exp_items + r] = (int32_t)(it - p->node_base.begin()) - 1;
+  }
+}
+}  // namespace
+
 // doubles per parity block of the published tables
 static int64_t tables_len(const tp_plan* p) { return 2 * (p->total_pairs + 1) + 4 * (p->total_rows + 1); }
 
@@ -2200,6 +2244,8 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
   const bool new_tables = key != A.table_key && p->table_total > 0;
   std::vector<double> price(tpk::kBwTab + tpk::kScaleDim * tpk::kScaleDim);
   tpk::make_price_tabs(p->env, price.data(), price.data() + tpk::kBwTab);
+  bool packed_ranges = false;
+  std::array<int64_t, 4> def_key{{-1, -1, -1, -1}};
   {
     DescPack pk;
     if (new_tables) pk.add(A.d_tabs, p->tabs);
@@ -2219,6 +2265,21 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
     pk.add(A.d_edges, p->edges);
     pk.add(A.d_fsegs, p->fsegs);
     pk.add(A.d_over, p->overrides);
+    // the range table of the default execute (whole graph, every tensor) goes
+    // up with the pack; another edge range or output set re-uploads its own
+    if (!(p->host_err != ~0ull && (p->host_err >> 6) == 0)) {
+      tp_status rs = resident_of(p);
+      if (rs) return rs;
+      const bool edge_phase = p->host_err >= ekey(kEdgePhase, 0);
+      const int32_t e1 = p->valid_edges;
+      const int64_t total_out = (edge_phase && p->edge_base[e1] > p->edge_base[0]) ? p->edge_base[e1] - p->edge_base[0] : 0;
+      int64_t rl, ei, ni;
+      range_layout(p, total_out, p->num_aux_nodes, rl, ei, ni);
+      fill_range_first(p, 0, e1, rl, ei, ni);
+      def_key = {{0, e1, rl, ni}};
+      pk.add(A.d_rfirst, p->range_first);
+      packed_ranges = true;
+    }
     const size_t total = pk.total();
     if (A.stage_done) CUDA_TRY(cudaEventSynchronize(A.stage_done));  // h_stage free again
     if (A.h_stage_cap < total) {
@@ -2256,7 +2317,7 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
         (tpk::SideDesc*)A.d_sides.p);
     CUDA_TRY(cudaGetLastError());
   }
-  p->range_key = {{-1, -1, -1, -1}};
+  p->range_key = packed_ranges ? def_key : std::array<int64_t, 4>{{-1, -1, -1, -1}};
   CUDA_TRY(A.d_pairrec.ensure(sizeof(PairRec) * (p->total_pairs + 1)));
   if (p->total_pairs > 0) {
     pair_rec_kernel<<<(unsigned)((p->total_pairs + 127) / 128), 128, 0, s>>>(
@@ -2265,9 +2326,18 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
     CUDA_TRY(cudaGetLastError());
   }
   // per parity: (cost, volume) [total_pairs + 1]; (cost, volume), mem, mem / indeg [total_rows + 1]
-  CUDA_TRY(A.d_tables2.ensure(sizeof(double) * 2 * tables_len(p)));
-  CUDA_TRY(A.d_sched.ensure(sizeof(Sched) + sizeof(Line) * (p->sigs.size() + 1)));
-  A.sched_clean = false;
+  // A finished launch leaves the counters zero and the next parity's tables
+  // unset, so an arena whose table layout and counter block are unchanged
+  // stays clean for the next plan; anything else is reset before its launch.
+  const int64_t L = tables_len(p);
+  const size_t sched_bytes = sizeof(Sched) + sizeof(Line) * (p->sigs.size() + 1);
+  const bool same_layout = A.d_tables2.p && A.d_tables2.cap >= sizeof(double) * 2 * L && A.d_sched.p &&
+                           A.d_sched.cap >= sched_bytes && A.tables_L == L && A.sched_bytes == sched_bytes;
+  CUDA_TRY(A.d_tables2.ensure(sizeof(double) * 2 * L));
+  CUDA_TRY(A.d_sched.ensure(sched_bytes));
+  if (!same_layout) A.sched_clean = false;
+  A.tables_L = L;
+  A.sched_bytes = sched_bytes;
   p->uploaded = true;
   return TP_OK;
 }
@@ -2327,34 +2397,16 @@ tp_status prepare_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
                          (out->edge_cost_s || out->edge_volume_bytes || out->edge_memory_bytes ||
                           out->aux_edge_records);
   if (p->resident_blocks == 0) {
-    int sms = 0, per_sm = 0;
-    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<true>, kFusedThreads, 0));
-    p->resident_blocks = std::max(1, sms * std::max(1, per_sm));
+    tp_status rs = resident_of(p);
+    if (rs) return rs;
   }
-  // fan-out: equal ranges of the edge range's aux ids, one per resident CTA
-  // phase 2: the aux nodes and the edge range's aux edges cut into equal
-  // ranges, one per resident CTA
   const int64_t total_out = edges_out ? p->edge_base[e1] - out_offset : 0;
   const int64_t total_nodes = nodes_out ? p->num_aux_nodes : 0;
-  const int64_t nranges = std::max(1, p->resident_blocks - 2);  // the two ceilings below add at most 2
-  const int64_t range_len =
-      std::max<int64_t>(kFusedThreads * kFanPer, (total_out + total_nodes + nranges - 1) / nranges);
-  const int64_t exp_items = (total_out + range_len - 1) / range_len;
-  const int64_t nfan_items = (total_nodes + range_len - 1) / range_len;
+  int64_t range_len, exp_items, nfan_items;
+  range_layout(p, total_out, total_nodes, range_len, exp_items, nfan_items);
   const std::array<int64_t, 4> rkey{{e0, e1, range_len, nfan_items}};
   if (p->range_key != rkey) {  // first edge / operator of every range (cached)
-    p->range_first.assign(exp_items + nfan_items, 0);
-    for (int64_t r = 0; r < exp_items; ++r) {
-      const int64_t start = out_offset + r * range_len;
-      auto it = std::upper_bound(p->edge_base.begin() + e0, p->edge_base.begin() + e1, start);
-      p->range_first[r] = (int32_t)(it - p->edge_base.begin()) - 1;
-    }
-    for (int64_t r = 0; r < nfan_items; ++r) {
-      const int64_t start = r * range_len;
-      auto it = std::upper_bound(p->node_base.begin(), p->node_base.begin() + p->num_ops, start);
-      p->range_first[exp_items + r] = (int32_t)(it - p->node_base.begin()) - 1;
-    }
+    fill_range_first(p, e0, e1, range_len, exp_items, nfan_items);
     CUDA_TRY(upload(A.d_rfirst, p->range_first, s));
     p->range_key = rkey;
   }
@@ -2547,6 +2599,10 @@ struct BatchCtx {
   cudaEvent_t copied = nullptr;  // the last staging copy
   bool hdr_clean = false;
   int resident = 0, resident_wide = 0;
+  // arenas of the one-shot host batch, by position: scenario i of a batch
+  // always gets arena i, so a repeated sweep finds its buffers sized (no
+  // cudaMalloc / cudaFree, which would synchronise the device)
+  std::vector<Arena*> host_arenas;
 };
 BatchCtx g_batch[64];
 
@@ -2637,7 +2693,7 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     const int64_t* duo = (const int64_t*)((const char*)B.d_args.p + args_b);
     int nwarp = 0;
     for (int k : live) nwarp += X[k].a.warp_form != 0;
-    static const int wide = getenv("TP_BATCH_WIDE") ? atoi(getenv("TP_BATCH_WIDE")) : 1;
+    static const int wide = getenv("TP_BATCH_WIDE") ? atoi(getenv("TP_BATCH_WIDE")) : 0;  // measured: 4 CTAs/SM with spills beats 2 without
     const int form = nwarp == m ? 1 : (nwarp == 0 ? (wide ? 3 : 2) : 0);
     const dim3 gd((unsigned)std::min<int64_t>(grid, form == 3 ? B.resident_wide : B.resident)), bd(kFusedThreads);
     const int64_t* dio = duo + (m + 1);
@@ -2882,12 +2938,18 @@ tp_status tp_plan_create_batch(const tp_graph_desc* const* graphs, const tp_topo
     return set_err(TP_ERR_CUDA, 0, "no CUDA device: the engine has no CPU path");
   if (device < 0) CUDA_TRY(cudaGetDevice(&device));
   std::vector<BatchErr> errs(n);
+  static const bool prof = getenv("TP_PROFILE_HOST") != nullptr;
+  const auto c0 = std::chrono::steady_clock::now();
   run_pool(n, host_threads, [&](int i, int) {
     tp_plan* p = nullptr;
     const tp_status st = tp_plan_create(graphs[i], topos[i], device, &p);
     plans_out[i] = p;
     errs[i].take(st);
   });
+  if (prof)
+    fprintf(stderr, "[tp batch] %d plans created in %.0f us on %d threads\n", n,
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - c0).count(),
+            pool_size(n, host_threads));
   return batch_status(errs, status_out);
 }
 
@@ -2967,12 +3029,20 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
   CUDA_TRY(cudaSetDevice(device));
   BatchCtx& B = g_batch[device];
   std::lock_guard<std::mutex> hl(B.host_mu);
-  // arenas: plans without one borrow a pooled arena for the call
+  static const bool prof = getenv("TP_PROFILE_HOST") != nullptr;
+  auto clk = [] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double hb0 = prof ? clk() : 0;
+  // arenas: plans without one borrow the batch's arena of their position
   std::vector<char> borrowed(n, 0);
+  while ((int)B.host_arenas.size() < n) {
+    Arena* a = new Arena();
+    a->device = device;
+    B.host_arenas.push_back(a);
+  }
   for (int i = 0; i < n; ++i) {
     tp_plan* p = plans[i];
     if (p->arena) continue;
-    p->arena = arena_pool_get(device);
+    p->arena = B.host_arenas[i];
     p->owns_arena = false;
     p->uploaded = false;
     borrowed[i] = 1;
@@ -2981,7 +3051,6 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
     for (int i = 0; i < n; ++i) {
       if (!borrowed[i]) continue;
       tp_plan* p = plans[i];
-      arena_pool_put(p->arena);
       p->arena = nullptr;
       p->owns_arena = true;
       p->uploaded = false;
@@ -3008,6 +3077,7 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
       give_back();
       return batch_status(errs, status_out);
     }
+  const double hb1 = prof ? clk() : 0;
   // device staging of the outputs, one buffer per tensor kind
   std::vector<int64_t> nn(n), ne(n);
   int64_t tn = 0, te = 0;
@@ -3050,6 +3120,7 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
     give_back();
     return st;
   }
+  const double hb2 = prof ? clk() : 0;
   // back to the host: one copy per tensor kind where the caller's slices are contiguous
   for (int k = 0; k < 6; ++k) {
     if (!want[k]) continue;
@@ -3080,7 +3151,11 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
   }
   if (!live.empty())
     CUDA_TRY(cudaMemcpyAsync(B.h_err, B.d_err.p, sizeof(unsigned long long) * live.size(), cudaMemcpyDeviceToHost, s));
+  const double hb3 = prof ? clk() : 0;
   CUDA_TRY(cudaStreamSynchronize(s));
+  if (prof)
+    fprintf(stderr, "[tp batch] %d plans: uploads %.0f us, launch prep %.0f, copies enqueued %.0f, wait %.0f\n", n,
+            hb1 - hb0, hb2 - hb1, hb3 - hb2, clk() - hb3);
   std::vector<unsigned long long> slot(n, 0);
   for (size_t k = 0; k < live.size(); ++k) slot[live[k]] = B.h_err[k];
   for (int i = 0; i < n; ++i) {
