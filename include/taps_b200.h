@@ -267,6 +267,19 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n,
 tp_status tp_plan_execute_batch(tp_plan* const* plans, int32_t n,
                                 tp_cost_tensors* device_outs, void* stream);
 
+/* price_assignment (aux_graph.hpp:326-348) of k strategy assignments on the
+ * device, both cost modes at once: assignments [k * num_ops] (the strategy
+ * index of every operator, DEVICE memory), t = the plan's six DEVICE cost
+ * tensors from tp_plan_execute; out (DEVICE, [k], any may be NULL): the
+ * topology-mode cost (sum of cost_s), the volume-mode cost (sum of
+ * volume_bytes) and the memory sum, each accumulated in the reference's
+ * order. Asynchronous on `stream`. Used for the TAPS-vs-volume ratio of a
+ * sweep (pipeline.hpp:152-168: both winners priced in topology mode). */
+tp_status tp_plan_price_assignments(tp_plan* plan, const tp_cost_tensors* t,
+                                    const int32_t* assignments, int32_t k,
+                                    double* cost_s, double* volume_bytes,
+                                    double* memory_bytes, void* stream);
+
 /* Strategy table of an operator with p axes on N devices, in the reference's
  * enumeration order (layout.hpp:270-328), produced on the device.
  * degrees[S*p], device_map[S*p], matrix_dims[S*p] (outermost first, padded

@@ -219,10 +219,8 @@ __global__ void table_kernel(const TableDesc* __restrict__ tabs, int ntabs, int6
 }
 
 // K0b (at upload): layout descriptors of every (edge class, side, strategy).
-__global__ void side_kernel(const SideJob* __restrict__ jobs, int njobs, int64_t total,
-                            const Strat* __restrict__ tables, tpk::SideDesc* __restrict__ out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
+__device__ __forceinline__ void side_one(const SideJob* __restrict__ jobs, int njobs, int64_t i,
+                                         const Strat* __restrict__ tables, tpk::SideDesc* __restrict__ out) {
   int lo = 0, hi = njobs - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -236,6 +234,13 @@ __global__ void side_kernel(const SideJob* __restrict__ jobs, int njobs, int64_t
   out[i] = d;
 }
 
+__global__ void side_kernel(const SideJob* __restrict__ jobs, int njobs, int64_t total,
+                            const Strat* __restrict__ tables, tpk::SideDesc* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  side_one(jobs, njobs, i, tables, out);
+}
+
 // Everything one class-table entry's pricing reads, gathered at upload so a
 // pair warp starts from one dependent load (not pair -> class -> maps ->
 // layouts).
@@ -247,11 +252,10 @@ struct alignas(16) PairRec {
   DimT dt[tpk::kMaxR];
 };
 
-__global__ void pair_rec_kernel(const SigDesc* __restrict__ sigs, const int32_t* __restrict__ pair_sig,
-                                const int32_t* __restrict__ maps, const tpk::SideDesc* __restrict__ sides,
-                                const double* __restrict__ overrides, int64_t total, PairRec* __restrict__ out) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= total) return;
+__device__ __forceinline__ void pair_rec_one(const SigDesc* __restrict__ sigs, const int32_t* __restrict__ pair_sig,
+                                             const int32_t* __restrict__ maps, const tpk::SideDesc* __restrict__ sides,
+                                             const double* __restrict__ overrides, int64_t idx,
+                                             PairRec* __restrict__ out) {
   const int sig = pair_sig[idx];
   const SigDesc& sg = sigs[sig];
   const int32_t t = (int32_t)(idx - sg.pair_begin);
@@ -267,6 +271,53 @@ __global__ void pair_rec_kernel(const SigDesc* __restrict__ sigs, const int32_t*
   r.pad = 0;
   for (int d = 0; d < tpk::kMaxR; ++d) r.dt[d] = sg.dt[d];
   out[idx] = r;
+}
+
+__global__ void pair_rec_kernel(const SigDesc* __restrict__ sigs, const int32_t* __restrict__ pair_sig,
+                                const int32_t* __restrict__ maps, const tpk::SideDesc* __restrict__ sides,
+                                const double* __restrict__ overrides, int64_t total, PairRec* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  pair_rec_one(sigs, pair_sig, maps, sides, overrides, idx, out);
+}
+
+// The set-up kernels of many plans in one launch each (batched uploads):
+// thread i finds its plan by bisection over the prefix sums.
+struct UpJob {
+  const SideJob* jobs;
+  const Strat* tables;
+  tpk::SideDesc* sides;
+  const SigDesc* sigs;
+  const int32_t* pair_sig;
+  const int32_t* maps;
+  const double* overrides;
+  PairRec* recs;
+  int32_t njobs, pad;
+};
+
+__device__ __forceinline__ int bisect_off(const int64_t* off, int n, int64_t x) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= x) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void batch_side_kernel(const UpJob* __restrict__ up, int n, const int64_t* __restrict__ off) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= off[n]) return;
+  const int q = bisect_off(off, n, i);
+  const UpJob& u = up[q];
+  side_one(u.jobs, u.njobs, i - off[q], u.tables, u.sides);
+}
+
+__global__ void batch_pair_rec_kernel(const UpJob* __restrict__ up, int n, const int64_t* __restrict__ off) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= off[n]) return;
+  const int q = bisect_off(off, n, i);
+  const UpJob& u = up[q];
+  pair_rec_one(u.sigs, u.pair_sig, u.maps, u.sides, u.overrides, i - off[q], u.recs);
 }
 
 // Scheduling state of a launch. Zeroed once (memset) when the arena is set
@@ -1018,6 +1069,66 @@ __global__ void __launch_bounds__(kFusedThreads, kForm == 3 ? 2 : 4)
   }
 }
 
+// price_assignment (aux_graph.hpp:326-348) of K strategy assignments, one
+// warp per assignment: lanes gather a chunk of 32 summation terms (node or
+// edge payloads at the assignment's aux ids) into shared memory, lane 0 adds
+// them in the reference's order (topological order; a source's virtual edge,
+// then its in-edges ascending), so both cost modes and the memory sum are the
+// reference's own roundings.
+constexpr int kPriceWarps = 4;
+__global__ void __launch_bounds__(32 * kPriceWarps) price_kernel(
+    const int4* __restrict__ terms, int nterms, const int64_t* __restrict__ node_base,
+    const int64_t* __restrict__ edge_base, const int32_t* __restrict__ edge_to_op, const int32_t* __restrict__ asg,
+    int nops, int k, const double* __restrict__ n_sec, const double* __restrict__ n_vol,
+    const double* __restrict__ n_mem, const double* __restrict__ e_sec, const double* __restrict__ e_vol,
+    const double* __restrict__ e_mem, double* __restrict__ o_sec, double* __restrict__ o_vol,
+    double* __restrict__ o_mem) {
+  __shared__ double sv[kPriceWarps][3][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int a = blockIdx.x * kPriceWarps + w;
+  if (a >= k) return;
+  const int32_t* as = asg + (int64_t)a * nops;
+  double c = 0, v = 0, m = 0;
+  for (int t0 = 0; t0 < nterms; t0 += 32) {
+    const int t = t0 + lane;
+    if (t < nterms) {
+      const int4 tm = terms[t];
+      double x, y, z;
+      if (tm.x == 0) {
+        const int64_t id = node_base[tm.w] + as[tm.w];
+        x = n_sec[id];
+        y = n_vol[id];
+        z = n_mem[id];
+      } else {
+        const int wo = edge_to_op[tm.y];
+        const int64_t id =
+            edge_base[tm.y] + (int64_t)as[tm.z] * (node_base[wo + 1] - node_base[wo]) + as[tm.w];
+        x = e_sec[id];
+        y = e_vol[id];
+        z = e_mem[id];
+      }
+      sv[w][0][lane] = x;
+      sv[w][1][lane] = y;
+      sv[w][2][lane] = z;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const int cnt = min(32, nterms - t0);
+      for (int i = 0; i < cnt; ++i) {
+        c += sv[w][0][i];
+        v += sv[w][1][i];
+        m += sv[w][2][i];
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (o_sec) o_sec[a] = c;
+    if (o_vol) o_vol[a] = v;
+    if (o_mem) o_mem[a] = m;
+  }
+}
+
 // K3 (optional): cond_min (solver.hpp:239-253), warp per (edge, su) row.
 __global__ void rowmin_kernel(const EdgeDesc* __restrict__ edges, const int64_t* __restrict__ row_base,
                               int e0, int nedges, int64_t nrows, const SigDesc* __restrict__ sigs,
@@ -1202,6 +1313,13 @@ struct tp_plan {
   std::vector<int64_t> edge_base;  // [num_edges + 1]
   std::vector<int64_t> row_base;   // [num_edges + 1]
   std::vector<int32_t> edge_from_op, edge_to_op, in_deg, out_deg, topo;
+  // price_assignment's summation terms (aux_graph.hpp:326-348), host-built on
+  // first use: per op in topological order a source's virtual edge, then the
+  // edges whose `to` id equals the op's id, ascending
+  std::vector<int32_t> op_dense_id, edge_to_dense;
+  std::vector<int4> price_terms;  // (kind 0 node / 1 edge, e, u, op)
+  DevBuf* d_terms = nullptr;      // their device copy (owned)
+  int64_t terms_bytes = 0;
   int64_t num_aux_nodes = 0, num_aux_edges = 0, num_rows = 0, num_virtual = 0;
   int valid_ops = 0;    // ops whose nodes are built (before a host node-phase error)
   int valid_edges = 0;  // edges processed before a host edge-phase error
@@ -1418,6 +1536,8 @@ struct Builder {
       std::vector<int32_t> fill(fed_begin.begin(), fed_begin.end() - 1);
       for (int e = 0; e < g->num_edges; ++e) fed_list[fill[to_dense[e]]++] = g->edge_tensor[e];
       op_key.assign(op_dense.begin(), op_dense.end());
+      p.op_dense_id = op_dense;
+      p.edge_to_dense = to_dense;
       p.in_deg.resize(g->num_ops);
       p.out_deg.resize(g->num_ops);
       for (int i = 0; i < g->num_ops; ++i) {
@@ -2147,6 +2267,10 @@ tp_status tp_plan_create(const tp_graph_desc* graph, const tp_topology_desc* top
 void tp_plan_destroy(tp_plan* p) {
   if (!p) return;
   cudaSetDevice(p->device);
+  if (p->d_terms) {
+    p->d_terms->release();
+    delete p->d_terms;
+  }
   if (p->arena) {
     if (p->arena->stream) cudaStreamSynchronize(p->arena->stream);
     if (p->owns_arena) {
@@ -2232,99 +2356,85 @@ void fill_range_first(tp_plan* p, int32_t e0, int32_t e1, int64_t range_len, int
 // doubles per parity block of the published tables
 static int64_t tables_len(const tp_plan* p) { return 2 * (p->total_pairs + 1) + 4 * (p->total_rows + 1); }
 
-tp_status tp_plan_upload(tp_plan* p, void* stream) {
-  if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
-  tp_status st = ensure_stream(p);
-  if (st) return st;
-  Arena& A = *p->arena;
-  cudaStream_t s = stream ? (cudaStream_t)stream : A.stream;
-  // strategy tables: a pure function of (p, N), cached on the arena
+}  // extern "C"
+
+namespace {
+// An upload in pieces (tp_plan_upload runs them back to back; the host batch
+// packs every plan's descriptors into one copy and runs the set-up kernels
+// of all plans as two launches).
+struct UploadPrep {
+  DescPack pk;
+  bool new_tables = false;
   std::vector<std::array<int64_t, 4>> key;
-  for (auto& td : p->tabs) key.push_back({td.offset, td.count, td.p, td.n});
-  const bool new_tables = key != A.table_key && p->table_total > 0;
-  std::vector<double> price(tpk::kBwTab + tpk::kScaleDim * tpk::kScaleDim);
-  tpk::make_price_tabs(p->env, price.data(), price.data() + tpk::kBwTab);
+  std::vector<double> price;
   bool packed_ranges = false;
   std::array<int64_t, 4> def_key{{-1, -1, -1, -1}};
-  {
-    DescPack pk;
-    if (new_tables) pk.add(A.d_tabs, p->tabs);
-    pk.add(A.d_sidejobs, p->side_jobs);
-    pk.add(A.d_price, price);
-    pk.add(A.d_classes, p->classes);
-    pk.add(A.d_opnode, p->node_base);
-    pk.add(A.d_oprow, p->op_row);
-    pk.add(A.d_members, p->members);
-    pk.add(A.d_chks, p->chks);
-    pk.add(A.d_slots, p->slots);
-    pk.add(A.d_occs, p->occs);
-    pk.add(A.d_sigs, p->sigs);
-    pk.add(A.d_pairsigs, p->pair_sig);
-    pk.add(A.d_rowcls, p->row_cls);
-    pk.add(A.d_maps, p->maps);
-    pk.add(A.d_edges, p->edges);
-    pk.add(A.d_fsegs, p->fsegs);
-    pk.add(A.d_over, p->overrides);
-    // the range table of the default execute (whole graph, every tensor) goes
-    // up with the pack; another edge range or output set re-uploads its own
-    if (!(p->host_err != ~0ull && (p->host_err >> 6) == 0)) {
-      tp_status rs = resident_of(p);
-      if (rs) return rs;
-      const bool edge_phase = p->host_err >= ekey(kEdgePhase, 0);
-      const int32_t e1 = p->valid_edges;
-      const int64_t total_out = (edge_phase && p->edge_base[e1] > p->edge_base[0]) ? p->edge_base[e1] - p->edge_base[0] : 0;
-      int64_t rl, ei, ni;
-      range_layout(p, total_out, p->num_aux_nodes, rl, ei, ni);
-      fill_range_first(p, 0, e1, rl, ei, ni);
-      def_key = {{0, e1, rl, ni}};
-      pk.add(A.d_rfirst, p->range_first);
-      packed_ranges = true;
-    }
-    const size_t total = pk.total();
-    if (A.stage_done) CUDA_TRY(cudaEventSynchronize(A.stage_done));  // h_stage free again
-    if (A.h_stage_cap < total) {
-      if (A.h_stage) cudaFreeHost(A.h_stage);
-      A.h_stage = nullptr;
-      A.h_stage_cap = 0;
-      CUDA_TRY(cudaMallocHost(&A.h_stage, total));
-      A.h_stage_cap = total;
-    }
-    // views first (d_desc may be reallocated, which frees nothing the views own)
-    for (auto& x : pk.pieces) x.buf->release();
-    CUDA_TRY(A.d_desc.ensure(total));
-    size_t off = 0;
-    for (auto& x : pk.pieces) {
-      if (x.bytes) std::memcpy((char*)A.h_stage + off, x.src, x.bytes);
-      x.buf->set_view((char*)A.d_desc.p + off, DescPack::pad(x.bytes));
-      off += DescPack::pad(x.bytes);
-    }
-    CUDA_TRY(cudaMemcpyAsync(A.d_desc.p, A.h_stage, total, cudaMemcpyHostToDevice, s));
-    if (!A.stage_done) CUDA_TRY(cudaEventCreateWithFlags(&A.stage_done, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventRecord(A.stage_done, s));
+};
+
+// Host only: the descriptor pieces of the plan (and its default range table).
+tp_status upload_prepare(tp_plan* p, UploadPrep& U) {
+  Arena& A = *p->arena;
+  // strategy tables: a pure function of (p, N), cached on the arena
+  for (auto& td : p->tabs) U.key.push_back({td.offset, td.count, td.p, td.n});
+  U.new_tables = U.key != A.table_key && p->table_total > 0;
+  U.price.resize(tpk::kBwTab + tpk::kScaleDim * tpk::kScaleDim);
+  tpk::make_price_tabs(p->env, U.price.data(), U.price.data() + tpk::kBwTab);
+  DescPack& pk = U.pk;
+  if (U.new_tables) pk.add(A.d_tabs, p->tabs);
+  pk.add(A.d_sidejobs, p->side_jobs);
+  pk.add(A.d_price, U.price);
+  pk.add(A.d_classes, p->classes);
+  pk.add(A.d_opnode, p->node_base);
+  pk.add(A.d_oprow, p->op_row);
+  pk.add(A.d_members, p->members);
+  pk.add(A.d_chks, p->chks);
+  pk.add(A.d_slots, p->slots);
+  pk.add(A.d_occs, p->occs);
+  pk.add(A.d_sigs, p->sigs);
+  pk.add(A.d_pairsigs, p->pair_sig);
+  pk.add(A.d_rowcls, p->row_cls);
+  pk.add(A.d_maps, p->maps);
+  pk.add(A.d_edges, p->edges);
+  pk.add(A.d_fsegs, p->fsegs);
+  pk.add(A.d_over, p->overrides);
+  // the range table of the default execute (whole graph, every tensor) goes
+  // up with the pack; another edge range or output set re-uploads its own
+  if (!(p->host_err != ~0ull && (p->host_err >> 6) == 0)) {
+    tp_status rs = resident_of(p);
+    if (rs) return rs;
+    const bool edge_phase = p->host_err >= ekey(kEdgePhase, 0);
+    const int32_t e1 = p->valid_edges;
+    const int64_t total_out =
+        (edge_phase && p->edge_base[e1] > p->edge_base[0]) ? p->edge_base[e1] - p->edge_base[0] : 0;
+    int64_t rl, ei, ni;
+    range_layout(p, total_out, p->num_aux_nodes, rl, ei, ni);
+    fill_range_first(p, 0, e1, rl, ei, ni);
+    U.def_key = {{0, e1, rl, ni}};
+    pk.add(A.d_rfirst, p->range_first);
+    U.packed_ranges = true;
   }
-  if (new_tables) {
-    CUDA_TRY(A.d_tables.ensure(sizeof(Strat) * (p->table_total + 1)));
-    table_kernel<<<(unsigned)((p->table_total + 127) / 128), 128, 0, s>>>(
-        (const TableDesc*)A.d_tabs.p, (int)p->tabs.size(), p->table_total, (Strat*)A.d_tables.p);
-    CUDA_TRY(cudaGetLastError());
-    A.table_key = key;
+  return TP_OK;
+}
+
+// Copy the pieces into pinned staging at `host` and point the plan's views
+// at `dev` (same offsets); the caller copies host -> dev.
+void upload_stage(UploadPrep& U, char* host, char* dev) {
+  for (auto& x : U.pk.pieces) x.buf->release();
+  size_t off = 0;
+  for (auto& x : U.pk.pieces) {
+    if (x.bytes) std::memcpy(host + off, x.src, x.bytes);
+    x.buf->set_view(dev + off, DescPack::pad(x.bytes));
+    off += DescPack::pad(x.bytes);
   }
-  // layout descriptors of every (edge class, side, strategy)
+}
+
+// Device buffers the set-up kernels and the launches write (cudaMalloc only
+// when an arena grows), the clean state, the plan's flags.
+tp_status upload_finish(tp_plan* p, UploadPrep& U) {
+  Arena& A = *p->arena;
   CUDA_TRY(A.d_sides.ensure(sizeof(tpk::SideDesc) * (p->side_total + 1)));
-  if (p->side_total > 0) {
-    side_kernel<<<(unsigned)((p->side_total + 127) / 128), 128, 0, s>>>(
-        (const SideJob*)A.d_sidejobs.p, (int)p->side_jobs.size(), p->side_total, (const Strat*)A.d_tables.p,
-        (tpk::SideDesc*)A.d_sides.p);
-    CUDA_TRY(cudaGetLastError());
-  }
-  p->range_key = packed_ranges ? def_key : std::array<int64_t, 4>{{-1, -1, -1, -1}};
   CUDA_TRY(A.d_pairrec.ensure(sizeof(PairRec) * (p->total_pairs + 1)));
-  if (p->total_pairs > 0) {
-    pair_rec_kernel<<<(unsigned)((p->total_pairs + 127) / 128), 128, 0, s>>>(
-        (const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_pairsigs.p, (const int32_t*)A.d_maps.p,
-        (const tpk::SideDesc*)A.d_sides.p, (const double*)A.d_over.p, p->total_pairs, (PairRec*)A.d_pairrec.p);
-    CUDA_TRY(cudaGetLastError());
-  }
+  if (U.new_tables) CUDA_TRY(A.d_tables.ensure(sizeof(Strat) * (p->table_total + 1)));
   // per parity: (cost, volume) [total_pairs + 1]; (cost, volume), mem, mem / indeg [total_rows + 1]
   // A finished launch leaves the counters zero and the next parity's tables
   // unset, so an arena whose table layout and counter block are unchanged
@@ -2338,7 +2448,66 @@ tp_status tp_plan_upload(tp_plan* p, void* stream) {
   if (!same_layout) A.sched_clean = false;
   A.tables_L = L;
   A.sched_bytes = sched_bytes;
+  p->range_key = U.packed_ranges ? U.def_key : std::array<int64_t, 4>{{-1, -1, -1, -1}};
   p->uploaded = true;
+  return TP_OK;
+}
+
+tp_status upload_tables(tp_plan* p, UploadPrep& U, cudaStream_t s) {
+  Arena& A = *p->arena;
+  if (!U.new_tables) return TP_OK;
+  table_kernel<<<(unsigned)((p->table_total + 127) / 128), 128, 0, s>>>(
+      (const TableDesc*)A.d_tabs.p, (int)p->tabs.size(), p->table_total, (Strat*)A.d_tables.p);
+  CUDA_TRY(cudaGetLastError());
+  A.table_key = U.key;
+  return TP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+tp_status tp_plan_upload(tp_plan* p, void* stream) {
+  if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
+  tp_status st = ensure_stream(p);
+  if (st) return st;
+  Arena& A = *p->arena;
+  cudaStream_t s = stream ? (cudaStream_t)stream : A.stream;
+  UploadPrep U;
+  st = upload_prepare(p, U);
+  if (st) return st;
+  const size_t total = U.pk.total();
+  if (A.stage_done) CUDA_TRY(cudaEventSynchronize(A.stage_done));  // h_stage free again
+  if (A.h_stage_cap < total) {
+    if (A.h_stage) cudaFreeHost(A.h_stage);
+    A.h_stage = nullptr;
+    A.h_stage_cap = 0;
+    CUDA_TRY(cudaMallocHost(&A.h_stage, total));
+    A.h_stage_cap = total;
+  }
+  // views first (d_desc may be reallocated, which frees nothing the views own)
+  for (auto& x : U.pk.pieces) x.buf->release();
+  CUDA_TRY(A.d_desc.ensure(total));
+  upload_stage(U, (char*)A.h_stage, (char*)A.d_desc.p);
+  CUDA_TRY(cudaMemcpyAsync(A.d_desc.p, A.h_stage, total, cudaMemcpyHostToDevice, s));
+  if (!A.stage_done) CUDA_TRY(cudaEventCreateWithFlags(&A.stage_done, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(A.stage_done, s));
+  st = upload_finish(p, U);
+  if (st) return st;
+  st = upload_tables(p, U, s);
+  if (st) return st;
+  // layout descriptors of every (edge class, side, strategy)
+  if (p->side_total > 0) {
+    side_kernel<<<(unsigned)((p->side_total + 127) / 128), 128, 0, s>>>(
+        (const SideJob*)A.d_sidejobs.p, (int)p->side_jobs.size(), p->side_total, (const Strat*)A.d_tables.p,
+        (tpk::SideDesc*)A.d_sides.p);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (p->total_pairs > 0) {
+    pair_rec_kernel<<<(unsigned)((p->total_pairs + 127) / 128), 128, 0, s>>>(
+        (const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_pairsigs.p, (const int32_t*)A.d_maps.p,
+        (const tpk::SideDesc*)A.d_sides.p, (const double*)A.d_over.p, p->total_pairs, (PairRec*)A.d_pairrec.p);
+    CUDA_TRY(cudaGetLastError());
+  }
   return TP_OK;
 }
 
@@ -2603,6 +2772,10 @@ struct BatchCtx {
   // always gets arena i, so a repeated sweep finds its buffers sized (no
   // cudaMalloc / cudaFree, which would synchronise the device)
   std::vector<Arena*> host_arenas;
+  // batched uploads: every plan's descriptor pack + the set-up jobs, one copy
+  void* h_pack = nullptr;
+  size_t h_pack_cap = 0;
+  DevBuf d_pack;
 };
 BatchCtx g_batch[64];
 
@@ -3063,20 +3236,74 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
     return st;
   }
   cudaStream_t s = plans[0]->arena->stream;
-  // uploads: the host side (descriptor packing) on the workers, all copies and
-  // set-up kernels on the batch stream
+  // uploads: plans on their own arenas the usual way; the borrowed ones in
+  // ONE packed copy (descriptors packed by the workers) and two set-up launches
   std::vector<BatchErr> errs(n);
-  run_pool(n, host_threads, [&](int i, int) {
-    tp_plan* p = plans[i];
-    tp_status e = ensure_stream(p);
-    if (!e && !p->uploaded) e = tp_plan_upload(p, s);
-    errs[i].take(e);
-  });
+  for (int i = 0; i < n; ++i)
+    if (!borrowed[i] && !plans[i]->uploaded) errs[i].take(tp_plan_upload(plans[i], s));
+  std::vector<int> todo;
+  for (int i = 0; i < n; ++i)
+    if (borrowed[i]) todo.push_back(i);
+  std::vector<UploadPrep> U(todo.size());
+  run_pool((int)todo.size(), host_threads, [&](int j, int) { errs[todo[j]].take(upload_prepare(plans[todo[j]], U[j])); });
   for (int i = 0; i < n; ++i)
     if (errs[i].st) {
       give_back();
       return batch_status(errs, status_out);
     }
+  if (!todo.empty()) {
+    const int m = (int)todo.size();
+    std::vector<size_t> off(m + 1, 0);
+    for (int j = 0; j < m; ++j) off[j + 1] = off[j] + U[j].pk.total();
+    const size_t jobs_at = (off[m] + 255) & ~(size_t)255;
+    const size_t total = jobs_at + sizeof(UpJob) * m + 2 * sizeof(int64_t) * (m + 1);
+    if (B.h_pack_cap < total) {
+      if (B.h_pack) cudaFreeHost(B.h_pack);
+      B.h_pack = nullptr;
+      B.h_pack_cap = 0;
+      CUDA_TRY(cudaMallocHost(&B.h_pack, total));
+      B.h_pack_cap = total;
+    }
+    CUDA_TRY(B.d_pack.ensure(total));
+    char* hp = (char*)B.h_pack;
+    char* dp = (char*)B.d_pack.p;
+    run_pool(m, host_threads, [&](int j, int) {
+      tp_plan* p = plans[todo[j]];
+      upload_stage(U[j], hp + off[j], dp + off[j]);
+      errs[todo[j]].take(upload_finish(p, U[j]));
+    });
+    for (int i = 0; i < n; ++i)
+      if (errs[i].st) {
+        give_back();
+        return batch_status(errs, status_out);
+      }
+    UpJob* jobs = (UpJob*)(hp + jobs_at);
+    int64_t* so = (int64_t*)(hp + jobs_at + sizeof(UpJob) * m);
+    int64_t* po = so + (m + 1);
+    so[0] = po[0] = 0;
+    for (int j = 0; j < m; ++j) {
+      tp_plan* p = plans[todo[j]];
+      Arena& A = *p->arena;
+      jobs[j] = UpJob{(const SideJob*)A.d_sidejobs.p, (const Strat*)A.d_tables.p, (tpk::SideDesc*)A.d_sides.p,
+                      (const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_pairsigs.p, (const int32_t*)A.d_maps.p,
+                      (const double*)A.d_over.p, (PairRec*)A.d_pairrec.p, (int32_t)p->side_jobs.size(), 0};
+      so[j + 1] = so[j] + p->side_total;
+      po[j + 1] = po[j] + p->total_pairs;
+    }
+    CUDA_TRY(cudaMemcpyAsync(dp, hp, total, cudaMemcpyHostToDevice, s));
+    for (int j = 0; j < m; ++j) {
+      st = upload_tables(plans[todo[j]], U[j], s);
+      if (st) {
+        give_back();
+        return st;
+      }
+    }
+    const UpJob* dj = (const UpJob*)(dp + jobs_at);
+    const int64_t* dso = (const int64_t*)(dp + jobs_at + sizeof(UpJob) * m);
+    if (so[m] > 0) batch_side_kernel<<<(unsigned)((so[m] + 127) / 128), 128, 0, s>>>(dj, m, dso);
+    if (po[m] > 0) batch_pair_rec_kernel<<<(unsigned)((po[m] + 127) / 128), 128, 0, s>>>(dj, m, dso + (m + 1));
+    CUDA_TRY(cudaGetLastError());
+  }
   const double hb1 = prof ? clk() : 0;
   // device staging of the outputs, one buffer per tensor kind
   std::vector<int64_t> nn(n), ne(n);
@@ -3164,6 +3391,71 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
   }
   give_back();
   return batch_status(errs, status_out);
+}
+
+tp_status tp_plan_price_assignments(tp_plan* p, const tp_cost_tensors* t, const int32_t* assignments, int32_t k,
+                                    double* cost_s, double* volume_bytes, double* memory_bytes, void* stream) {
+  if (!p || !t || (k > 0 && !assignments)) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null argument");
+  if (k < 0) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "negative assignment count");
+  if (p->host_err != ~0ull) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "the plan's build has an error");
+  if (!t->node_intra_cost_s || !t->node_intra_volume_bytes || !t->node_memory_bytes || !t->edge_cost_s ||
+      !t->edge_volume_bytes || !t->edge_memory_bytes)
+    return set_err(TP_ERR_INVALID_ARGUMENT, 0, "all six cost tensors are needed");
+  if (k == 0 || p->num_ops == 0) return TP_OK;
+  tp_status st = ensure_stream(p);
+  if (st) return st;
+  cudaStream_t s = stream ? (cudaStream_t)stream : p->arena->stream;
+  if (!p->d_terms) {  // the summation terms and the index arrays they read, once per plan
+    p->price_terms.clear();
+    // edges by the dense id of their `to`, ascending edge order
+    int32_t nd = 0;
+    for (int v : p->op_dense_id) nd = std::max(nd, v + 1);
+    for (int v : p->edge_to_dense) nd = std::max(nd, v + 1);
+    std::vector<int32_t> db(nd + 1, 0), de(p->num_edges);
+    for (int e = 0; e < p->num_edges; ++e) ++db[p->edge_to_dense[e] + 1];
+    for (int d = 0; d < nd; ++d) db[d + 1] += db[d];
+    {
+      std::vector<int32_t> f(db.begin(), db.end() - 1);
+      for (int e = 0; e < p->num_edges; ++e) de[f[p->edge_to_dense[e]]++] = e;
+    }
+    for (int op : p->topo) {
+      if (p->in_deg[op] == 0) p->price_terms.push_back(make_int4(0, -1, -1, op));
+      const int d = p->op_dense_id[op];
+      for (int q = db[d]; q < db[d + 1]; ++q) {
+        const int e = de[q];
+        p->price_terms.push_back(make_int4(1, e, p->edge_from_op[e], op));
+      }
+    }
+    std::vector<int64_t> idx64;
+    idx64.insert(idx64.end(), p->node_base.begin(), p->node_base.end());
+    idx64.insert(idx64.end(), p->edge_base.begin(), p->edge_base.end());
+    const size_t b_terms = sizeof(int4) * std::max<size_t>(p->price_terms.size(), 1);
+    const size_t b_idx = sizeof(int64_t) * idx64.size();
+    const size_t b_to = sizeof(int32_t) * std::max<int>(p->num_edges, 1);
+    p->d_terms = new DevBuf();
+    CUDA_TRY(p->d_terms->ensure(b_terms + b_idx + b_to));
+    char* base = (char*)p->d_terms->p;
+    CUDA_TRY(cudaMemcpyAsync(base, p->price_terms.data(), sizeof(int4) * p->price_terms.size(),
+                             cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(base + b_terms, idx64.data(), b_idx, cudaMemcpyHostToDevice, s));
+    if (p->num_edges)
+      CUDA_TRY(cudaMemcpyAsync(base + b_terms + b_idx, p->edge_to_op.data(), sizeof(int32_t) * p->num_edges,
+                               cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaStreamSynchronize(s));  // the host vectors above are pageable and temporary
+    p->terms_bytes = (int64_t)b_terms;
+  }
+  const char* base = (const char*)p->d_terms->p;
+  const int4* terms = (const int4*)base;
+  const int64_t* nb = (const int64_t*)(base + p->terms_bytes);
+  const int64_t* eb = nb + (p->num_ops + 1);
+  const int32_t* to = (const int32_t*)(eb + (p->num_edges + 1));
+  const int blocks = (k + kPriceWarps - 1) / kPriceWarps;
+  price_kernel<<<blocks, 32 * kPriceWarps, 0, s>>>(terms, (int)p->price_terms.size(), nb, eb, to, assignments,
+                                                   p->num_ops, k, t->node_intra_cost_s, t->node_intra_volume_bytes,
+                                                   t->node_memory_bytes, t->edge_cost_s, t->edge_volume_bytes,
+                                                   t->edge_memory_bytes, cost_s, volume_bytes, memory_bytes);
+  CUDA_TRY(cudaGetLastError());
+  return TP_OK;
 }
 
 tp_status tp_enumerate_strategies(int32_t p, int64_t total_devices, int64_t* count, int64_t* degrees,

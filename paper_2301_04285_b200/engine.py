@@ -176,6 +176,22 @@ class Plan:
     def last_launches(self) -> int:
         return int(self.lib.tp_plan_last_launches(self.handle))
 
+    def price_assignments(self, tensors: dict, assignments, stream: int = 0):
+        """price_assignment (aux_graph.hpp:326-348) of every row of
+        `assignments` (a CUDA int32 tensor [k, num_ops]) against this plan's
+        device cost tensors (dict of the six tensors, as executed): returns
+        CUDA float64 tensors (topology-mode cost, volume-mode cost, memory)."""
+        import torch
+        a = assignments.to(torch.int32).contiguous()
+        k = int(a.shape[0]) if a.dim() == 2 else 0
+        outs = [torch.empty(max(k, 1), dtype=torch.float64, device=a.device) for _ in range(3)]
+        ptr = lambda x: C.cast(C.c_void_p(x.data_ptr()), C.POINTER(C.c_double))
+        ts = device_cost_struct(tensors)
+        _check(self.lib, self.lib.tp_plan_price_assignments(
+            self.handle, C.byref(ts), C.cast(C.c_void_p(a.data_ptr()), C.POINTER(C.c_int32)), k,
+            ptr(outs[0]), ptr(outs[1]), ptr(outs[2]), C.c_void_p(stream or None)))
+        return tuple(o[:k] for o in outs)
+
     def execute_host(self, records=False, row_min=False, edge_range=(0, -1), skip_nodes=False,
                      pinned=False) -> CostTensors:
         """Synchronous build into HOST buffers (pinned if requested)."""
