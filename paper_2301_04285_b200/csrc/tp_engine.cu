@@ -503,6 +503,13 @@ struct FusedArgs {
   // phase-2 items: [0, i_exp) node ranges, [i_exp, i_end) edge ranges
   int i_exp, i_end;
   int warp_form;  // pairs: 1 = warp per pair, 0 = thread per pair
+  // batches (thread form): plans equal but for their bandwidths share their
+  // class pairs -- the leader infers every pair once and prices it for each
+  // member (group: member indices into the batch's args, the leader first);
+  // a member's pairs are not units of its own
+  const int32_t* group;
+  int group_n;
+  int priced_by_leader;
   // shared
   const Strat* tables;
   Env env;
@@ -605,21 +612,39 @@ __device__ void node_row(const FusedArgs& a, int64_t row) {
 
 __device__ __forceinline__ int sig_of_pair(const FusedArgs& a, int64_t idx) { return a.pair_sig[idx]; }
 
-// One class-table entry on one thread (register form, tp_fast.cuh).
-__device__ void pair_thread(const FusedArgs& a, int64_t idx, const double* price) {
+// One class-table entry on one thread (register form, tp_fast.cuh); with a
+// bandwidth group (batches) the entry of every member, inferred once. One
+// call site of the register form keeps the kernels' code (and the
+// instruction-cache footprint) single.
+__device__ void pair_thread(const FusedArgs& a, int64_t idx, const double* price,
+                            const FusedArgs* __restrict__ all = nullptr) {
   const PairRec& pr = a.pairs[idx];
   const tpk::SideDesc F = pr.F, T = pr.T;
   const int R = pr.R;
+  const int g = (all && a.group_n > 1) ? a.group_n : 1;
+  tpk::MultiSec ms;
+  ms.g = g;
+  for (int q = 1; q < g; ++q) {
+    const FusedArgs& b = all[a.group[q]];
+    ms.env[q] = b.env;
+    ms.tab[q] = tpk::FastTabs{b.bw_tab, b.bw_tab + tpk::kBwTab};
+    ms.sec[q] = 0;
+  }
   double sec = 0, vol = 0;
   if (!tpk::same_side(F, T, R)) {  // aux_graph.hpp:260
     const int st = tpk::pair_cost_sd(R, F, T, nullptr, nullptr, pr.dt, pr.bytes, a.env, a.l_log2,
-                                     tpk::FastTabs{price, price + tpk::kBwTab}, sec, vol, nullptr);
+                                     tpk::FastTabs{price, price + tpk::kBwTab}, sec, vol, nullptr,
+                                     g > 1 ? &ms : nullptr);
     if (st) {
-      flag_error(a.err, ekey(kEdgePhase + (uint64_t)(a.sigs[pr.sig].first_aux + pr.local) * 2 + 1, st));
+      const uint64_t key = ekey(kEdgePhase + (uint64_t)(a.sigs[pr.sig].first_aux + pr.local) * 2 + 1, st);
+      flag_error(a.err, key);
+      for (int q = 1; q < g; ++q) flag_error(all[a.group[q]].err, key);
       sec = vol = 0;
+      for (int q = 1; q < g; ++q) ms.sec[q] = 0;
     }
   }
   a.r_tab[idx] = make_double2(sec, vol);
+  for (int q = 1; q < g; ++q) all[a.group[q]].r_tab[idx] = make_double2(ms.sec[q], vol);
 }
 
 // One class-table entry on one warp (warp form, tp_warp.cuh); lane 0 writes.
@@ -851,7 +876,8 @@ __device__ void node_range(const FusedArgs& a, int item, NodeSeg* seg, int* s_n,
 // One phase-1 unit u of a plan: a node-class row, or a class pair (warp
 // form) / 32 class pairs (thread form).
 template <bool kWarpForm>
-__device__ __forceinline__ void run_unit(const FusedArgs& a, int64_t u, const double* price) {
+__device__ __forceinline__ void run_unit(const FusedArgs& a, int64_t u, const double* price,
+                                         const FusedArgs* all = nullptr) {
   const int lane = threadIdx.x & 31;
   const unsigned long long t0 = (a.pair_ns || a.item_ns) ? gtimer() : 0;
   if (u < a.total_rows) {
@@ -878,18 +904,25 @@ __device__ __forceinline__ void run_unit(const FusedArgs& a, int64_t u, const do
     const int64_t idx = (u - a.total_rows) * 32 + lane;
     const bool valid = idx < a.total_pairs;
     const int sig = valid ? sig_of_pair(a, idx) : -1;
-    if (valid) pair_thread(a, idx, price);
+    const bool grouped = all && a.group_n > 1;
+    if (valid) pair_thread(a, idx, price, all);
     if (a.pair_ns && valid) {
       a.pair_ns[2 * idx] = (unsigned)t0;
       a.pair_ns[2 * idx + 1] = (unsigned)(gtimer() - t0);
     }
     // one counter update per (warp, edge class); no fence: see table_load
     const unsigned grp = __match_any_sync(0xffffffffu, sig);
-    if (valid && lane == __ffs(grp) - 1) red_relaxed_add(&a.sched->pairs_done[sig].v, __popc(grp));
+    if (valid && lane == __ffs(grp) - 1) {
+      if (grouped)
+        for (int q = 0; q < a.group_n; ++q) red_relaxed_add(&all[a.group[q]].sched->pairs_done[sig].v, __popc(grp));
+      else
+        red_relaxed_add(&a.sched->pairs_done[sig].v, __popc(grp));
+    }
   }
 }
 
 __device__ __forceinline__ int64_t plan_units(const FusedArgs& a) {
+  if (a.priced_by_leader) return a.total_rows;
   return a.total_rows + (a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32);
 }
 
@@ -985,6 +1018,7 @@ struct BatchHdr {
 __device__ __forceinline__ int find_plan(const int64_t* off, int n, int64_t x, int p) {
   // the plan q with off[q] <= x < off[q + 1]: gallop forward from the previous
   // plan (claims only increase), then bisect
+  if (p >= 0 && off[p] <= x && (p + 1 >= n || off[p + 1] > x)) return p;
   int lo = (p < 0 || off[p] > x) ? 0 : p, hi;
   int step = 1;
   for (;;) {
@@ -1024,7 +1058,7 @@ __global__ void __launch_bounds__(kFusedThreads, kForm == 3 ? 2 : 4)
     p = find_plan(unit_off, n, u, p);
     const FusedArgs& a = args[p];
     if (kForm == 1 || (kForm == 0 && a.warp_form)) run_unit<true>(a, u - unit_off[p], a.bw_tab);
-    else run_unit<false>(a, u - unit_off[p], a.bw_tab);
+    else run_unit<false>(a, u - unit_off[p], a.bw_tab, args);
     int next = 0;
     if (lane == 0) next = ld_relaxed(&hdr->unit_head.v) >= units ? INT_MAX : atomicAdd(&hdr->unit_head.v, 1);
     u = __shfl_sync(0xffffffffu, next, 0);
@@ -1359,6 +1393,8 @@ struct tp_plan {
   int64_t trace_n[3] = {0, 0, 0};  // pairs, node-row items, fan-out items traced
   int pair_form = 0;  // 0 = by size, 1 = warp per pair, 2 = thread per pair
   bool in_big_batch = false;  // by size: judged by the whole batch's pairs (thread form)
+  uint64_t shash = 0;         // struct_hash, cached (a plan's structure never changes)
+  bool shash_ok = false;
   int resident_blocks = 0;  // persistent grid size (SMs x resident CTAs)
 };
 
@@ -2779,6 +2815,39 @@ struct BatchCtx {
 };
 BatchCtx g_batch[64];
 
+// Everything a plan's class pairs are priced from, except the bandwidths:
+// equal for two plans of one graph and mesh under different intra/inter
+// bandwidths (a sweep's ratio axis).
+uint64_t struct_hash_raw(const tp_plan* p) {
+  uint64_t h = hash_words(0x7f4a7c159e3779b9ull ^ (uint64_t)p->env.local, &p->total_pairs, sizeof(p->total_pairs));
+  h = hash_words(h, p->sigs.data(), p->sigs.size() * sizeof(SigDesc));
+  h = hash_words(h, p->side_jobs.data(), p->side_jobs.size() * sizeof(SideJob));
+  h = hash_words(h, p->maps.data(), p->maps.size() * sizeof(int32_t));
+  h = hash_words(h, p->tabs.data(), p->tabs.size() * sizeof(TableDesc));
+  h = hash_words(h, p->overrides.data(), p->overrides.size() * sizeof(double));
+  return h;
+}
+
+uint64_t struct_hash(tp_plan* p) {
+  if (!p->shash_ok) {
+    p->shash = struct_hash_raw(p);
+    p->shash_ok = true;
+  }
+  return p->shash;
+}
+
+template <typename T>
+bool same_vec(const std::vector<T>& a, const std::vector<T>& b) {
+  return a.size() == b.size() && (a.empty() || !std::memcmp(a.data(), b.data(), sizeof(T) * a.size()));
+}
+
+bool same_structure(const tp_plan* a, const tp_plan* b) {
+  return a->env.local == b->env.local && a->n_log2 == b->n_log2 && a->total_pairs == b->total_pairs &&
+         a->pair_form == b->pair_form && same_vec(a->sigs, b->sigs) && same_vec(a->side_jobs, b->side_jobs) &&
+         same_vec(a->maps, b->maps) && same_vec(a->tabs, b->tabs) && same_vec(a->pair_sig, b->pair_sig) &&
+         same_vec(a->overrides, b->overrides);
+}
+
 // err_dev: optional device array [n] that receives every launched plan's
 // error slot (in `live` order via live_out) -- the host batch checks all
 // plans with one copy instead of one synchronising read per plan.
@@ -2826,9 +2895,54 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_batch_kernel<3>, kFusedThreads, 0));
       B.resident_wide = std::max(1, sms * std::max(1, per_sm));
     }
-    // staging: args[m] | unit_off[m+1] | item_off[m+1] | tab_off[m+1]
+    int nwarp = 0;
+    for (int k : live) nwarp += X[k].a.warp_form != 0;
+    // bandwidth groups (thread form only): plans whose pricing inputs are
+    // identical but for intra/inter bandwidth share their class pairs
+    std::vector<int32_t> glist;                       // member lists, leader first (live order)
+    std::vector<std::pair<int, int>> gspan(m, {-1, 0});  // per leader: (offset in glist, size)
+    static const bool no_groups = getenv("TP_BATCH_NO_GROUPS") != nullptr;
+    if (nwarp == 0 && !no_groups) {
+      std::vector<std::vector<int32_t>> groups;             // live indices, the leader first
+      std::unordered_map<uint64_t, std::vector<int>> open;  // structure hash -> group ids
+      for (int k = 0; k < m; ++k) {
+        tp_plan* p = plans[live[k]];
+        if (p->total_pairs == 0 || !X[live[k]].edge_phase) continue;
+        const uint64_t h = struct_hash(p);
+        auto& og = open[h];
+        if (og.empty() || groups[og.back()].size() >= (size_t)tpk::kGroupMax) {
+          og.push_back((int)groups.size());
+          groups.emplace_back();
+        }
+        groups[og.back()].push_back(k);
+      }
+      // verify the members against their leader in parallel; a hash
+      // collision just leaves the plan pricing its own pairs
+      std::vector<std::pair<int, int>> chk;  // (group, position)
+      for (int gi = 0; gi < (int)groups.size(); ++gi)
+        for (int q = 1; q < (int)groups[gi].size(); ++q) chk.push_back({gi, q});
+      std::vector<char> ok(chk.size(), 1);
+      run_pool((int)chk.size(), 0, [&](int c, int) {
+        const auto& gr = groups[chk[c].first];
+        ok[c] = same_structure(plans[live[gr[0]]], plans[live[gr[chk[c].second]]]);
+      });
+      for (size_t c = chk.size(); c-- > 0;)
+        if (!ok[c]) groups[chk[c].first][chk[c].second] = -1;
+      for (auto& gr : groups) gr.erase(std::remove(gr.begin(), gr.end(), -1), gr.end());
+      for (const auto& g : groups) {
+        if (g.size() < 2) continue;
+        gspan[g[0]] = {(int)glist.size(), (int)g.size()};
+        glist.insert(glist.end(), g.begin(), g.end());
+        for (size_t q = 1; q < g.size(); ++q) {
+          ExecPrep& x = X[live[g[q]]];
+          x.a.priced_by_leader = 1;
+          x.units = plans[live[g[q]]]->total_rows;
+        }
+      }
+    }
+    // staging: args[m] | unit_off[m+1] | item_off[m+1] | tab_off[m+1] | group lists
     const size_t args_b = sizeof(FusedArgs) * m, off_b = sizeof(int64_t) * (m + 1);
-    const size_t total = args_b + 3 * off_b;
+    const size_t total = args_b + 3 * off_b + sizeof(int32_t) * (glist.size() + 1);
     if (B.copied) CUDA_TRY(cudaEventSynchronize(B.copied));
     if (B.h_cap < total) {
       if (B.h_stage) cudaFreeHost(B.h_stage);
@@ -2837,21 +2951,28 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
       CUDA_TRY(cudaMallocHost(&B.h_stage, total));
       B.h_cap = total;
     }
+    CUDA_TRY(B.d_args.ensure(total));
     FusedArgs* ha = (FusedArgs*)B.h_stage;
     int64_t* uo = (int64_t*)((char*)B.h_stage + args_b);
     int64_t* io = uo + (m + 1);
     int64_t* to = io + (m + 1);
+    int32_t* hg = (int32_t*)(to + (m + 1));
+    const int32_t* dg = (const int32_t*)((const char*)B.d_args.p + args_b + 3 * off_b);
+    if (!glist.empty()) std::memcpy(hg, glist.data(), sizeof(int32_t) * glist.size());
     uo[0] = io[0] = to[0] = 0;
     for (int k = 0; k < m; ++k) {
       const ExecPrep& x = X[live[k]];
       ha[k] = x.a;
+      if (gspan[k].second >= 2) {
+        ha[k].group = dg + gspan[k].first;
+        ha[k].group_n = gspan[k].second;
+      }
       uo[k + 1] = uo[k] + x.units;
       io[k + 1] = io[k] + x.items;
       to[k + 1] = to[k] + x.a.tables_len;
     }
     if (uo[m] >= (1ll << 30) || io[m] >= (1ll << 30))
       return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many work items in one batch");
-    CUDA_TRY(B.d_args.ensure(total));
     CUDA_TRY(cudaMemcpyAsync(B.d_args.p, B.h_stage, total, cudaMemcpyHostToDevice, s));
     if (!B.copied) CUDA_TRY(cudaEventCreateWithFlags(&B.copied, cudaEventDisableTiming));
     CUDA_TRY(cudaEventRecord(B.copied, s));
@@ -2864,8 +2985,6 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(blocks_needed, B.resident));
     const FusedArgs* da = (const FusedArgs*)B.d_args.p;
     const int64_t* duo = (const int64_t*)((const char*)B.d_args.p + args_b);
-    int nwarp = 0;
-    for (int k : live) nwarp += X[k].a.warp_form != 0;
     static const int wide = getenv("TP_BATCH_WIDE") ? atoi(getenv("TP_BATCH_WIDE")) : 0;  // measured: 4 CTAs/SM with spills beats 2 without
     const int form = nwarp == m ? 1 : (nwarp == 0 ? (wide ? 3 : 2) : 0);
     const dim3 gd((unsigned)std::min<int64_t>(grid, form == 3 ? B.resident_wide : B.resident)), bd(kFusedThreads);
@@ -3116,6 +3235,7 @@ tp_status tp_plan_create_batch(const tp_graph_desc* const* graphs, const tp_topo
   run_pool(n, host_threads, [&](int i, int) {
     tp_plan* p = nullptr;
     const tp_status st = tp_plan_create(graphs[i], topos[i], device, &p);
+    if (p) struct_hash(p);  // cached for the batch's bandwidth groups
     plans_out[i] = p;
     errs[i].take(st);
   });

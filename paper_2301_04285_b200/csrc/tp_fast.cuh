@@ -130,11 +130,39 @@ TP_HD double price_fast(bool a2a, int te, int rexp, int ek, int s, double bytes,
   return scale * v / bw;
 }
 
+// Scenarios that differ only in their bandwidths share a pair's unification,
+// op sequence, volumes and ct: the op list is inferred once and priced for
+// every member environment (members 1..g-1; member 0 is the caller's own env),
+// each member's seconds summed in op order like the reference's.
+constexpr int kGroupMax = 8;
+struct MultiSec {
+  int g;
+  Env env[kGroupMax];
+  FastTabs tab[kGroupMax];
+  double sec[kGroupMax];
+};
+
+#if defined(__CUDACC__)
+#define TP_NOINL __noinline__
+#else
+#define TP_NOINL __attribute__((noinline))
+#endif
+
+// One op priced for members 1..g-1 (out of line: one copy of the code for
+// both call sites keeps the kernels' instruction footprint small).
+TP_HD TP_NOINL void price_members(MultiSec* ms, bool a2a, int pos, int rexp, int e, int s, double bytes,
+                                  int l_log2) {
+  for (int q = 1; q < ms->g; ++q) {
+    double dv = 0;
+    ms->sec[q] += price_fast(a2a, pos, rexp, e, s, bytes, ms->env[q], l_log2, ms->tab[q], &dv, nullptr);
+  }
+}
+
 // Returns the tp_error_kind, or -1 when the pair needs the array form
 // (a device dim held twice by the working map).
 TP_HD int redist_cost_fast(int R, const SideDesc& gf, const SideDesc& gt, const DimT* dt, double bytes,
                            const Env& env, int l_log2, const FastTabs& tab, double& sec_out, double& vol_out,
-                           Trace* tr) {
+                           Trace* tr, MultiSec* ms = nullptr) {
   if (R < 0 || R > kMaxR) return kCapacity;
   // ---- unify: bitmask closure (see tp_core.cuh) ----
   uint32_t D = gf.D | gt.D;
@@ -289,6 +317,7 @@ TP_HD int redist_cost_fast(int R, const SideDesc& gf, const SideDesc& gt, const 
           int64_t ct = 0;
           const double c = price_fast(true, pos, rexp, e, s, bytes, env, l_log2, tab, &vol, tr ? &ct : nullptr);
           sec += c;
+          if (ms) price_members(ms, true, pos, rexp, e, s, bytes, l_log2);
           record(2, k, i, j, 0, ct, c);
           const uint32_t bi = 1u << i, bj = 1u << j;
           pset(W, i, 0);
@@ -316,6 +345,7 @@ TP_HD int redist_cost_fast(int R, const SideDesc& gf, const SideDesc& gt, const 
     int64_t ct = 0;
     const double c = price_fast(false, pos, rexp, e, s, bytes, env, l_log2, tab, &vol, tr ? &ct : nullptr);
     sec += c;
+    if (ms) price_members(ms, false, pos, rexp, e, s, bytes, l_log2);
     record(1, k, i, -1, fb, ct, c);
     const uint32_t bi = 1u << i;
     pset(W, i, 0);
@@ -334,13 +364,27 @@ TP_HD int redist_cost_fast(int R, const SideDesc& gf, const SideDesc& gt, const 
 // that hold a device dim twice (Fl/Tl: the original layouts when known).
 TP_HD int pair_cost_sd(int R, const SideDesc& F, const SideDesc& T, const Lay* Fl, const Lay* Tl, const DimT* dt,
                        double bytes, const Env& env, int l_log2, const FastTabs& tab, double& sec, double& vol,
-                       Trace* tr) {
-  const int st = redist_cost_fast(R, F, T, dt, bytes, env, l_log2, tab, sec, vol, tr);
+                       Trace* tr, MultiSec* ms = nullptr) {
+  if (ms)
+    for (int q = 1; q < ms->g; ++q) ms->sec[q] = 0;
+  const int st = redist_cost_fast(R, F, T, dt, bytes, env, l_log2, tab, sec, vol, tr, ms);
   if (st != -1) return st;
   Lay a, b;
   if (Fl) a = *Fl; else lay_of(F, R, a);
   if (Tl) b = *Tl; else lay_of(T, R, b);
-  return redist_cost(R, a, b, dt, bytes, env, sec, vol, tr);
+  // the array form (rare: a device dim held twice), once per member, one call site
+  for (int q = ms ? ms->g - 1 : 0; q >= 0; --q) {
+    double sc = 0, v = 0;
+    const int e = redist_cost(R, a, b, dt, bytes, q ? ms->env[q] : env, sc, v, q ? nullptr : tr);
+    if (e) return e;
+    if (q) {
+      ms->sec[q] = sc;
+    } else {
+      sec = sc;
+      vol = v;
+    }
+  }
+  return kOk;
 }
 
 TP_HD int pair_cost(int R, const Lay& F, const Lay& T, const DimT* dt, double bytes, const Env& env, int l_log2,

@@ -153,3 +153,20 @@ def test_batch_mixes_forms_errors_and_single_executes():
         for i in (2, 3):
             with pytest.raises(abi.TopoplanError):
                 ds.plans[i].check_errors()
+
+
+def test_batch_entry_edge_cases():
+    """Empty and single-plan batches; a batch of identical scenarios under
+    different bandwidths (one bandwidth group) matches the oracle per member."""
+    import ctypes as C
+    lib = abi.load_engine()
+    assert lib.tp_plan_execute_batch(None, 0, None, None) == abi.TP_OK
+    assert lib.tp_plan_execute_host_batch(None, 0, None, None, 0, None) == abi.TP_OK
+    g, t = M.cfg2()
+    one = engine.build_sweep([(G.flatten(g), t)], device=0)
+    same(one[0], B.oracle_build(G.flatten(g), t), "single")
+    f = G.flatten(g)
+    pairs = [(f, M.ClusterTopology(4, 8, 60e9, 60e9 / r, 80e9)) for r in (1, 2, 3, 5, 7, 10, 20, 50, 100, 150)]
+    res = engine.build_sweep(pairs, device=0, host_threads=4)
+    for i, (ff, tt) in enumerate(pairs):
+        same(res[i], B.oracle_build(ff, tt), f"ratio {i}")
