@@ -201,7 +201,10 @@ struct SideJob {       // the SideDescs of one (edge class, side)
 // pair (latency-bound), so a warp cooperates on each pair; above it the
 // register-resident thread form has ~6x fewer instructions per pair.
 constexpr int64_t kWarpPairLimit = 16384;
-constexpr int kFanPer = 1;  // output positions a fan-out thread has in flight
+#ifndef TP_FAN_PER
+#define TP_FAN_PER 1
+#endif
+constexpr int kFanPer = TP_FAN_PER;  // output positions a fan-out thread has in flight
 
 // ---------------------------------------------------------------------------
 // kernels
