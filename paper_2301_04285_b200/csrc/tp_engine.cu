@@ -406,12 +406,6 @@ __device__ __forceinline__ void wait_at_least(const int* p, int v) {
 // a launch refills the other one.
 constexpr unsigned long long kUnset = 0xfff4000000000badull;
 
-__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
-  double v;
-  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-  return v;
-}
-
 __device__ __forceinline__ double ld_acquire_f64(const double* p) {
   double v;
   asm volatile("ld.acquire.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
@@ -1403,7 +1397,6 @@ struct tp_plan {
 
 namespace {
 
-// FNV-style hash of an interned key (class dedup on the host)
 // hash of a POD byte range, 8 bytes at a time (host class dedup)
 inline uint64_t hash_words(uint64_t h, const void* data, size_t bytes) {
   const unsigned char* b = (const unsigned char*)data;
@@ -1422,14 +1415,6 @@ inline uint64_t hash_words(uint64_t h, const void* data, size_t bytes) {
   }
   return h ^ (bytes << 7);
 }
-
-struct KeyHash {
-  size_t operator()(const std::vector<int64_t>& v) const {
-    uint64_t h = 1469598103934665603ull ^ v.size();
-    for (int64_t x : v) h = (h ^ (uint64_t)x) * 1099511628211ull;
-    return (size_t)(h ^ (h >> 29));
-  }
-};
 
 #ifdef TP_HOST_PROF
 double g_hprof[8];

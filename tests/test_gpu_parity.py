@@ -167,6 +167,20 @@ def test_cfg3_vs_oracle(nodes, ratio, form):
 
 
 @pytest.mark.parametrize("form", FORMS)
+@pytest.mark.parametrize("ratio", [10, 100])
+def test_cfg4_vs_oracle(ratio, form):
+    """cfg4 (GPT-96, hidden 12288, 16x8; the bench workload) in full: every
+    one of the 2,155,580 aux edges and 82,368 aux nodes bit-identical."""
+    g, t = M.cfg4(ratio)
+    f = G.flatten(g)
+    gpu = gpu_build(f, t, row_min=True, pair_form=form)
+    ref = B.oracle_build(f, t, records=False)
+    assert ref.status == 0
+    assert_same(gpu, ref, rowmin=True)
+    assert len(gpu.edge_cost_s) == 2155580 and len(gpu.node_intra_cost_s) == 82368
+
+
+@pytest.mark.parametrize("form", FORMS)
 def test_random_graphs_vs_oracle(form):
     rng = random.Random(1234)
     ok = err = 0

@@ -170,3 +170,22 @@ def test_batch_entry_edge_cases():
     res = engine.build_sweep(pairs, device=0, host_threads=4)
     for i, (ff, tt) in enumerate(pairs):
         same(res[i], B.oracle_build(ff, tt), f"ratio {i}")
+
+
+def test_full_sweep_every_scenario_vs_oracle(sweep1000):
+    """cfg5 in full: all 1,000 scenarios (16,957,929 aux edges) of the batched
+    build, bandwidth groups included, bit-identical to the oracle's standalone
+    build of each scenario (oracle builds on a host thread pool)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    pairs = [(G.flatten(s.graph), s.topo) for s in sweep1000]
+    sw = engine.Sweep(pairs, device=0, host_threads=0)
+    sw.create()
+    sw.allocate(pinned=False)
+    sw.execute()
+    B.oracle()  # load once before the pool
+    with ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 1))) as ex:
+        refs = list(ex.map(lambda p: B.oracle_build(p[0], p[1], records=False), pairs))
+    for i, r in enumerate(refs):
+        same(sw.results[i], r, f"scenario {i}")
+    sw.destroy()
