@@ -240,10 +240,12 @@ def init_dist(local, world):
     import torch
     if world <= 1:
         return None
+    import datetime
     import torch.distributed as dist
     if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
-        os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        os.environ.pop("NCCL_DEBUG", None)  # NCCL's banner goes to stdout: keep it to the one JSON line
+    # a rank that fails must not hold the others at a barrier for NCCL's default 10 minutes
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local), timeout=datetime.timedelta(seconds=180))
     return dist
 
 

@@ -507,6 +507,7 @@ struct FusedArgs {
   const int32_t* group;
   int group_n;
   int priced_by_leader;
+  int64_t perm_mul;  // (experiments) unit -> entry bijection, coprime with total_pairs
   // shared
   const Strat* tables;
   Env env;
@@ -887,7 +888,16 @@ __device__ __forceinline__ void run_unit(const FusedArgs& a, int64_t u, const do
       }
     }
   } else if (kWarpForm) {
+#ifdef TP_PAIR_PERM
+    // spread neighbouring (similarly expensive) entries over SMs: a
+    // multiplicative bijection of the unit order
+    const int64_t k = u - a.total_rows;
+    const int64_t idx = a.total_pairs > 1 ? (int64_t)(((unsigned long long)k * (unsigned long long)a.perm_mul) %
+                                                     (unsigned long long)a.total_pairs)
+                                          : k;
+#else
     const int64_t idx = u - a.total_rows;
+#endif
     pair_warp(a, idx, price);
     const int sig = a.pairs[idx].sig;
     if (lane == 0) {
@@ -2214,12 +2224,15 @@ int pool_size(int n, int host_threads) {
   return std::max(1, std::min(t, n));
 }
 
-// fn(item, worker) over items [0, n), items claimed one at a time
+// fn(item, worker) over items [0, n), items claimed one at a time. The
+// workers make `device` current first (a new host thread starts on device 0:
+// anything they allocate must land on the plans' device).
 template <typename F>
-void run_pool(int n, int workers, F&& fn) {
+void run_pool(int n, int workers, F&& fn, int device = -1) {
   workers = pool_size(n, workers);
   std::atomic<int> next{0};
   auto body = [&](int w) {
+    if (device >= 0 && w > 0) cudaSetDevice(device);
     for (int i = next.fetch_add(1); i < n; i = next.fetch_add(1)) fn(i, w);
   };
   std::vector<std::thread> th;
@@ -2455,6 +2468,7 @@ void upload_stage(UploadPrep& U, char* host, char* dev) {
 // Device buffers the set-up kernels and the launches write (cudaMalloc only
 // when an arena grows), the clean state, the plan's flags.
 tp_status upload_finish(tp_plan* p, UploadPrep& U) {
+  CUDA_TRY(cudaSetDevice(p->device));  // the buffers below belong on the plan's device
   Arena& A = *p->arena;
   CUDA_TRY(A.d_sides.ensure(sizeof(tpk::SideDesc) * (p->side_total + 1)));
   CUDA_TRY(A.d_pairrec.ensure(sizeof(PairRec) * (p->total_pairs + 1)));
@@ -2682,6 +2696,19 @@ tp_status prepare_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   // by size: a warp per pair while the launch has too few pairs to fill the
   // GPU with one thread per pair; a big batch of plans is judged as a whole
   a.warp_form = p->pair_form == 1 || (p->pair_form == 0 && !p->in_big_batch && a.total_pairs <= kWarpPairLimit);
+  {
+    int64_t m = 2654435761ll % std::max<int64_t>(a.total_pairs, 1);
+    auto gcd = [](int64_t x, int64_t y) {
+      while (y) {
+        const int64_t t = x % y;
+        x = y;
+        y = t;
+      }
+      return x;
+    };
+    while (a.total_pairs > 1 && (m < 1 || gcd(m, a.total_pairs) != 1)) ++m;
+    a.perm_mul = m;
+  }
   // phase-1 units: node rows, then class pairs (warp form) or 32-pair chunks;
   // phase-2 items: node ranges, then edge ranges
   const int64_t units = p->total_rows + (a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32);
@@ -3220,13 +3247,16 @@ tp_status tp_plan_create_batch(const tp_graph_desc* const* graphs, const tp_topo
   std::vector<BatchErr> errs(n);
   static const bool prof = getenv("TP_PROFILE_HOST") != nullptr;
   const auto c0 = std::chrono::steady_clock::now();
-  run_pool(n, host_threads, [&](int i, int) {
+  run_pool(
+      n, host_threads,
+      [&](int i, int) {
     tp_plan* p = nullptr;
     const tp_status st = tp_plan_create(graphs[i], topos[i], device, &p);
     if (p) struct_hash(p);  // cached for the batch's bandwidth groups
     plans_out[i] = p;
     errs[i].take(st);
-  });
+      },
+      device);
   if (prof)
     fprintf(stderr, "[tp batch] %d plans created in %.0f us on %d threads\n", n,
             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - c0).count(),
@@ -3353,7 +3383,8 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
   for (int i = 0; i < n; ++i)
     if (borrowed[i]) todo.push_back(i);
   std::vector<UploadPrep> U(todo.size());
-  run_pool((int)todo.size(), host_threads, [&](int j, int) { errs[todo[j]].take(upload_prepare(plans[todo[j]], U[j])); });
+  run_pool((int)todo.size(), host_threads, [&](int j, int) { errs[todo[j]].take(upload_prepare(plans[todo[j]], U[j])); },
+           device);
   for (int i = 0; i < n; ++i)
     if (errs[i].st) {
       give_back();
@@ -3375,11 +3406,14 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
     CUDA_TRY(B.d_pack.ensure(total));
     char* hp = (char*)B.h_pack;
     char* dp = (char*)B.d_pack.p;
-    run_pool(m, host_threads, [&](int j, int) {
-      tp_plan* p = plans[todo[j]];
-      upload_stage(U[j], hp + off[j], dp + off[j]);
-      errs[todo[j]].take(upload_finish(p, U[j]));
-    });
+    run_pool(
+        m, host_threads,
+        [&](int j, int) {
+          tp_plan* p = plans[todo[j]];
+          upload_stage(U[j], hp + off[j], dp + off[j]);
+          errs[todo[j]].take(upload_finish(p, U[j]));
+        },
+        device);
     for (int i = 0; i < n; ++i)
       if (errs[i].st) {
         give_back();

@@ -62,3 +62,27 @@ def test_edge_sharded_build_nccl_gather(cfg):
     assert np.array_equal(c.view(np.uint64), full.edge_cost_s.view(np.uint64))
     assert np.array_equal(v.view(np.uint64), full.edge_volume_bytes.view(np.uint64))
     assert np.array_equal(m.view(np.uint64), full.edge_memory_bytes.view(np.uint64))
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_batches_on_a_second_device():
+    """The batch entry points on device 1 from a process whose current device
+    is 0: every buffer (pooled arenas, the batch pack, the worker threads'
+    allocations) must land on the plans' device."""
+    from oracle import bindings as B
+    from paper_2301_04285_b200 import engine
+    torch.cuda.set_device(0)
+    scen = M.scenario_sweep(60)
+    pairs = [(G.flatten(s.graph), s.topo) for s in scen]
+    res = engine.build_sweep(pairs, device=1, host_threads=4)
+    ds = engine.DeviceSweep(pairs[:30], device=1)
+    ds.run()
+    torch.cuda.synchronize(1)
+    ds.check_errors()
+    for i, (f, t) in enumerate(pairs):
+        ref = B.oracle_build(f, t, records=False)
+        for k in ("node_intra_cost_s", "edge_cost_s", "edge_volume_bytes", "edge_memory_bytes"):
+            assert np.array_equal(getattr(res[i], k).view(np.uint64), getattr(ref, k).view(np.uint64)), (i, k)
+            if i < 30:
+                got = ds.result(i)[k].cpu().numpy()
+                assert np.array_equal(got.view(np.uint64), getattr(ref, k).view(np.uint64)), (i, k)
