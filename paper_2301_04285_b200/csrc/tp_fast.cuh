@@ -143,14 +143,14 @@ struct MultiSec {
 };
 
 #if defined(__CUDACC__)
-#define TP_NOINL __noinline__
+#define TP_HD_NOINL __host__ __device__ __noinline__
 #else
-#define TP_NOINL __attribute__((noinline))
+#define TP_HD_NOINL inline  // host builds (tests/devcheck)
 #endif
 
 // One op priced for members 1..g-1 (out of line: one copy of the code for
 // both call sites keeps the kernels' instruction footprint small).
-TP_HD TP_NOINL void price_members(MultiSec* ms, bool a2a, int pos, int rexp, int e, int s, double bytes,
+TP_HD_NOINL void price_members(MultiSec* ms, bool a2a, int pos, int rexp, int e, int s, double bytes,
                                   int l_log2) {
   for (int q = 1; q < ms->g; ++q) {
     double dv = 0;
