@@ -249,30 +249,12 @@ __device__ int redist_cost_warp(int R, const SideDesc* pf, const SideDesc* pt, c
     }
     ++nops;
   };
-  // Lane k's device-dim descriptor, packed so an op needs ONE shuffle for it:
-  // lower position, log2 extent, to.axis_of(k) + 1 (the to-map's device dims
-  // are distinct and never change) and the log2 in-node repetition below k
-  // (cost_model.hpp:115-119: extents of the dims inner to k that the working
-  // map does not hold; it changes only with the held set PM, i.e. on slices
-  // and gathers, never on AllToAlls).
-  int my_tax = 0;
-  for (int k = 0; k < next; ++k) {
-    const uint32_t b = __ballot_sync(FULL, my_to == k);
-    if (lane == k) my_tax = b ? ffs32(b) + 1 : 0;
-  }
-  uint32_t my_pk = 0;
-  auto refresh = [&]() {  // after PM changed
-    int held = ((PM >> lane) & 1u) ? my_ext : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(FULL, held, o);
-      if (lane >= o) held += v;
-    }
-    held -= ((PM >> lane) & 1u) ? my_ext : 0;  // exclusive: the dims inner to this one
-    my_pk = (uint32_t)(my_pos & 0xff) | ((uint32_t)(my_ext & 0xff) << 8) | ((uint32_t)my_tax << 16) |
-            ((uint32_t)((my_pos - held) & 0xff) << 24);
+  // log2 of the in-node repetition below device dim k (cost_model.hpp:115-119):
+  // extents of the dims inner to k that the working map does not hold
+  auto rexp_below = [&](int k, int te) -> int {
+    const int held = (int)__reduce_add_sync(FULL, (unsigned)((lane < k && ((PM >> lane) & 1u)) ? my_ext : 0));
+    return te - held;
   };
-  refresh();
   // Priced ops. With a trace they are priced on the spot. Otherwise op t is
   // parked on lane t and a batch is priced by all lanes at once -- the fp64
   // chains of up to 32 ops overlap -- then summed in op order, the same
@@ -334,35 +316,28 @@ __device__ int redist_cost_warp(int R, const SideDesc* pf, const SideDesc* pt, c
         PM |= __reduce_or_sync(FULL, me ? (1u << my_to) : 0u);
         s += (int)__reduce_add_sync(FULL, me ? (unsigned)ext_to : 0u);
         if (me) my_w = my_to;
-        refresh();
         progress = true;
       }
       // InferAll2All until none applies (:367-385): a pass takes positions
       // in ascending order, each checked against the state the earlier moves
       // of the pass left. Lane i qualifies when it holds a dim k it must not
       // keep and the position whose to-map is k holds nothing (free_to).
-      // free_to is kept incrementally: a move frees the source position's
-      // target and fills k's.
-      uint32_t free_to = __reduce_or_sync(FULL, (my_to >= 0 && my_w == -1) ? (1u << my_to) : 0u);
       bool a2a = true;
       while (a2a) {
         a2a = false;
         int cursor = -1;
         for (;;) {
+          const uint32_t free_to = __reduce_or_sync(FULL, (my_to >= 0 && my_w == -1) ? (1u << my_to) : 0u);
           const uint32_t ok = __ballot_sync(FULL, lane > cursor && my_w >= 0 && my_w != my_to &&
                                                       ((free_to >> (my_w & 31)) & 1u));
           if (!ok) break;
           const int i = ffs32(ok);
-          const uint32_t wt = __shfl_sync(FULL, (uint32_t)(my_w & 0xff) | ((uint32_t)(my_to & 0xff) << 8), i);
-          const int k = (int)(wt & 0xff);
-          const int to_i = (int)(int8_t)(wt >> 8);
-          const uint32_t pk = __shfl_sync(FULL, my_pk, k);
-          const int te = (int)(pk & 0xff), ek = (int)((pk >> 8) & 0xff), j = (int)((pk >> 16) & 0xff) - 1;
-          const int rexp = (int)(int8_t)(pk >> 24);
-          op(true, te, rexp, ek, k, i, j, 0);
+          const int k = __shfl_sync(FULL, my_w, i);
+          const int j = ffs32(__ballot_sync(FULL, my_to == k));  // to.axis_of(k)
+          const int te = __shfl_sync(FULL, my_pos, k), ek = __shfl_sync(FULL, my_ext, k);
+          op(true, te, rexp_below(k, te), ek, k, i, j, 0);
           if (lane == i) my_w = -1;
           if (lane == j) my_w = k;
-          free_to = (free_to & ~(1u << k)) | (to_i >= 0 ? (1u << to_i) : 0u);
           cursor = i;
           a2a = true;
         }
@@ -381,12 +356,10 @@ __device__ int redist_cost_warp(int R, const SideDesc* pf, const SideDesc* pt, c
     }
     const int i = ffs32(gm);
     const int k = __shfl_sync(FULL, my_w, i);
-    const uint32_t pk = __shfl_sync(FULL, my_pk, k);
-    const int te = (int)(pk & 0xff), ek = (int)((pk >> 8) & 0xff);
-    op(false, te, (int)(int8_t)(pk >> 24), ek, k, i, -1, fb);
+    const int te = __shfl_sync(FULL, my_pos, k), ek = __shfl_sync(FULL, my_ext, k);
+    op(false, te, rexp_below(k, te), ek, k, i, -1, fb);
     if (lane == i) my_w = -1;
     PM = __reduce_or_sync(FULL, my_w >= 0 ? (1u << my_w) : 0u);
-    refresh();
     s -= ek;
     mism = __ballot_sync(FULL, my_w != my_to);
   }
