@@ -264,7 +264,7 @@ def run_sweep(args):
     return 0
 
 
-def measure_sweep(args, rank, world, local, dist, K, W, with_clocks=False):
+def measure_sweep(args, rank, world, local, dist, K, W, with_clocks=False, with_cpu=True):
     """cfg5 through the batch entry points. value: device-resident (plans
     analysed and uploaded, all scenarios rebuilt by one batched persistent
     launch, CUDA events around it); e2e: host graphs in -> tp_plan_create_batch +
@@ -354,7 +354,7 @@ def measure_sweep(args, rank, world, local, dist, K, W, with_clocks=False):
                        "tensors out), wall clock"},
         "gpu_launches": int(launches * K), "clocks": clk,
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and with_cpu and not args.no_cpu_baseline:
         from oracle import bindings as B
         if B.have_reference():
             sample = pairs[::10]
@@ -478,7 +478,7 @@ def run_engine(args):
     sweep = None
     if not args.no_sweep:
         try:
-            sl = measure_sweep(args, rank, world, local, dist, min(K, 10), W)
+            sl = measure_sweep(args, rank, world, local, dist, min(K, 10), W, with_cpu=False)
             if sl is not None:
                 sweep = {k: sl[k] for k in ("value", "unit", "ms_per_step", "scaling")}
                 sweep.update(config=sl["config"], e2e=sl["e2e"], roofline=sl["roofline"],
