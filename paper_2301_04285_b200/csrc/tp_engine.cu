@@ -2949,18 +2949,38 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     int64_t* to = io + (m + 1);
     int32_t* hg = (int32_t*)(to + (m + 1));
     const int32_t* dg = (const int32_t*)((const char*)B.d_args.p + args_b + 3 * off_b);
-    if (!glist.empty()) std::memcpy(hg, glist.data(), sizeof(int32_t) * glist.size());
-    uo[0] = io[0] = to[0] = 0;
-    for (int k = 0; k < m; ++k) {
-      const ExecPrep& x = X[live[k]];
-      ha[k] = x.a;
-      if (gspan[k].second >= 2) {
-        ha[k].group = dg + gspan[k].first;
-        ha[k].group_n = gspan[k].second;
+    // the heaviest plans first (their units are claimed first, so the long
+    // pricing chains do not form the batch's tail): args in `ord` order, the
+    // group lists translated to it
+    std::vector<int> ord(m), pos(m);
+    {
+      std::vector<double> w(m);
+      for (int k = 0; k < m; ++k) {
+        const ExecPrep& x = X[live[k]];
+        w[k] = (double)x.units * (gspan[k].second >= 2 ? 1.0 + 0.5 * (gspan[k].second - 1) : 1.0);
+        ord[k] = k;
       }
-      uo[k + 1] = uo[k] + x.units;
-      io[k + 1] = io[k] + x.items;
-      to[k + 1] = to[k] + x.a.tables_len;
+      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return w[a] > w[b]; });
+      for (int j = 0; j < m; ++j) pos[ord[j]] = j;
+    }
+    for (size_t q = 0; q < glist.size(); ++q) hg[q] = pos[glist[q]];
+    uo[0] = io[0] = to[0] = 0;
+    for (int j = 0; j < m; ++j) {
+      const int k = ord[j];
+      const ExecPrep& x = X[live[k]];
+      ha[j] = x.a;
+      if (gspan[k].second >= 2) {
+        ha[j].group = dg + gspan[k].first;
+        ha[j].group_n = gspan[k].second;
+      }
+      uo[j + 1] = uo[j] + x.units;
+      io[j + 1] = io[j] + x.items;
+      to[j + 1] = to[j] + x.a.tables_len;
+    }
+    {  // callers map the kernel's per-plan outputs (error slots) in args order
+      std::vector<int> l2(m);
+      for (int j = 0; j < m; ++j) l2[j] = live[ord[j]];
+      live.swap(l2);
     }
     if (uo[m] >= (1ll << 30) || io[m] >= (1ll << 30))
       return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many work items in one batch");
