@@ -204,6 +204,12 @@ tp_status tp_plan_execute(tp_plan* plan, const tp_build_opts* opts,
  * (the one-shot call on an existing plan; synchronous). */
 tp_status tp_plan_execute_host(tp_plan* plan, const tp_build_opts* opts,
                                tp_aux_index* index_out, tp_cost_tensors* host_out);
+/* Re-price an analysed plan under other intra/inter bandwidths (a sweep over
+ * the intra/inter ratio, cfg3): nothing of the host analysis depends on them,
+ * so the next execute uploads the new pricing tables and rebuilds. Results
+ * equal a fresh build with ClusterTopology{node_count, local_device_num,
+ * intra_bandwidth, inter_bandwidth, device_memory} (graph.hpp:189-199). */
+tp_status tp_plan_set_bandwidth(tp_plan* plan, double intra_bandwidth, double inter_bandwidth);
 /* Synchronise the plan's stream and turn a kernel-flagged error into a
  * status (and tp_last_error message). */
 tp_status tp_plan_check_errors(tp_plan* plan);

@@ -247,6 +247,8 @@ def load_engine() -> C.CDLL:
     lib.tp_plan_price_assignments.argtypes = [C.c_void_p, P(tp_cost_tensors), _p_i32, C.c_int32, P(C.c_double),
                                               P(C.c_double), P(C.c_double), C.c_void_p]
     lib.tp_plan_price_assignments.restype = C.c_int
+    lib.tp_plan_set_bandwidth.argtypes = [C.c_void_p, C.c_double, C.c_double]
+    lib.tp_plan_set_bandwidth.restype = C.c_int
     lib.tp_last_error.argtypes = []
     lib.tp_last_error.restype = C.c_char_p
     lib.tp_last_error_kind.argtypes = []
@@ -263,7 +265,7 @@ EXPORTED_SYMBOLS = (
     "tp_plan_index", "tp_plan_upload", "tp_plan_execute", "tp_plan_execute_host", "tp_plan_check_errors",
     "tp_plan_last_launches", "tp_plan_set_profile_events", "tp_plan_set_timeline", "tp_plan_timeline", "tp_plan_timeline_detail", "tp_enumerate_strategies", "tp_redistribute_batch",
     "tp_redistribute_batch_form", "tp_plan_set_pair_form", "tp_plan_create_batch", "tp_plan_execute_host_batch",
-    "tp_plan_execute_batch", "tp_plan_price_assignments",
+    "tp_plan_execute_batch", "tp_plan_price_assignments", "tp_plan_set_bandwidth",
     "tp_last_error", "tp_last_error_kind", "tp_abi_version",
 )
 

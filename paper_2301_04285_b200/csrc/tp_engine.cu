@@ -3034,6 +3034,16 @@ tp_status tp_plan_execute_batch(tp_plan* const* plans, int32_t n, tp_cost_tensor
   return execute_batch_impl(plans, n, device_outs, stream, nullptr, nullptr);
 }
 
+tp_status tp_plan_set_bandwidth(tp_plan* p, double intra_bandwidth, double inter_bandwidth) {
+  if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
+  // nothing of the host analysis depends on the bandwidths (classes, layouts,
+  // op sequences, volumes, ct): only the pricing tables and the kernels' Env
+  p->env.intra = intra_bandwidth;
+  p->env.inter = inter_bandwidth;
+  p->uploaded = false;  // the next execute uploads the new pricing tables
+  return TP_OK;
+}
+
 int64_t tp_plan_last_launches(const tp_plan* p) { return p ? p->last_launches : 0; }
 
 tp_status tp_plan_set_pair_form(tp_plan* p, int32_t form) {

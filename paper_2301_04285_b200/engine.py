@@ -176,6 +176,14 @@ class Plan:
     def last_launches(self) -> int:
         return int(self.lib.tp_plan_last_launches(self.handle))
 
+    def set_bandwidth(self, intra_bandwidth: float, inter_bandwidth: float):
+        """Re-price under other intra/inter bandwidths without re-analysing
+        (tp_plan_set_bandwidth); the next execute rebuilds."""
+        _check(self.lib, self.lib.tp_plan_set_bandwidth(self.handle, float(intra_bandwidth), float(inter_bandwidth)))
+        t = self.topo
+        self.topo = ClusterTopology(t.node_count, t.local_device_num, float(intra_bandwidth), float(inter_bandwidth),
+                                    t.device_memory)
+
     def price_assignments(self, tensors: dict, assignments, stream: int = 0):
         """price_assignment (aux_graph.hpp:326-348) of every row of
         `assignments` (a CUDA int32 tensor [k, num_ops]) against this plan's

@@ -301,3 +301,19 @@ def test_timeline_diagnostics():
     plan.check_errors()
     ref = B.oracle_build(f, t)
     np.testing.assert_array_equal(bits(outs["edge_cost_s"].cpu().numpy()), bits(ref.edge_cost_s))
+
+
+@pytest.mark.parametrize("nodes", [2, 8])
+def test_cfg3_ratio_sweep_by_repricing(nodes):
+    """cfg3's sweep of the intra/inter bandwidth ratio (1, 2, 5,
+    10, 20, 50, 100 with intra 60 GB/s) on ONE analysed plan re-priced with
+    tp_plan_set_bandwidth: every ratio bit-identical to a fresh oracle build."""
+    g, _ = M.cfg3(nodes, 10)
+    f = G.flatten(g)
+    plan = engine.Plan(f, M.cfg3(nodes, 10)[1], device=0)
+    for ratio in (10, 1, 2, 5, 20, 50, 100):
+        t = M.cfg3(nodes, ratio)[1]
+        plan.set_bandwidth(t.intra_bandwidth, t.inter_bandwidth)
+        got = plan.execute_host(row_min=True)
+        ref = B.oracle_build(f, t, records=False)
+        assert_same(got, ref, rowmin=True)
