@@ -214,6 +214,32 @@ std::chrono::steady_clock::time_point g_hlast;
   } while (0)
 #endif
 
+// Layout ids of a side's strategies (layout_tables): a pure function of the
+// strategy table (p, log2 N) and the slicing, memoised for the process.
+struct SideMemoKey {
+  uint64_t a, b;
+  bool operator==(const SideMemoKey& o) const { return a == o.a && b == o.b; }
+};
+struct SideMemoHash {
+  size_t operator()(const SideMemoKey& k) const { return (size_t)((k.a * 0x9e3779b97f4a7c15ull) ^ k.b); }
+};
+std::mutex g_side_memo_mu;
+std::unordered_map<SideMemoKey, std::pair<std::vector<int32_t>, std::vector<int32_t>>, SideMemoHash> g_side_memo;
+
+bool side_memo_get(const uint64_t* k, std::vector<int32_t>& uid, std::vector<int32_t>& reps) {
+  std::lock_guard<std::mutex> lk(g_side_memo_mu);
+  auto it = g_side_memo.find(SideMemoKey{k[0], k[1]});
+  if (it == g_side_memo.end()) return false;
+  uid = it->second.first;
+  reps = it->second.second;
+  return true;
+}
+
+void side_memo_put(const uint64_t* k, const std::vector<int32_t>& uid, const std::vector<int32_t>& reps) {
+  std::lock_guard<std::mutex> lk(g_side_memo_mu);
+  if (g_side_memo.size() < 4096) g_side_memo.emplace(SideMemoKey{k[0], k[1]}, std::make_pair(uid, reps));
+}
+
 struct Builder {
   const tp_graph_desc* g;
   const tp_topology_desc* t;
@@ -804,6 +830,12 @@ struct Builder {
         const TableDesc* td = nullptr;
         for (const auto& t : p.tabs)
           if (t.offset == tab) td = &t;
+        // a pure function of (p, log2 N, the slicing): memoised process-wide
+        // (sweeps repeat a handful of sides over many scenarios)
+        uint64_t ck[2] = {(uint64_t)td->p | ((uint64_t)td->n << 8) | ((uint64_t)R << 16), 0};
+        for (int d = 0; d < R; ++d) ck[1] |= (uint64_t)(uint8_t)sa[d] << (8 * d);
+        if (side_memo_get(ck, uid, reps)) goto have_maps;
+        {
         // distinct layout descriptors (POD, zeroed), by hash with a chain per id
         std::unordered_map<uint64_t, int32_t> head;
         std::vector<int32_t> next;
@@ -833,9 +865,12 @@ struct Builder {
           }
           uid[s] = id;
         }
+        }
+        side_memo_put(ck, uid, reps);
       } else {
         for (int32_t s = 0; s < S; ++s) uid[s] = s, reps.push_back(s);
       }
+    have_maps:
       p.maps.insert(p.maps.end(), uid.begin(), uid.end());
       r[1] = (int32_t)p.maps.size();
       r[2] = (int32_t)reps.size();

@@ -1,0 +1,6 @@
+# GPU test suite, smoke, and the default bench line
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -x -q -m gpu -rs > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+echo done
