@@ -134,7 +134,10 @@ TP_HD double price_fast(bool a2a, int te, int rexp, int ek, int s, double bytes,
 // op sequence, volumes and ct: the op list is inferred once and priced for
 // every member environment (members 1..g-1; member 0 is the caller's own env),
 // each member's seconds summed in op order like the reference's.
-constexpr int kGroupMax = 8;
+#ifndef TP_GROUP_MAX
+#define TP_GROUP_MAX 16  // measured on cfg5: 4 / 8 / 16 / 32 / 64 -> 3.05 / 2.55 / 2.26 / 2.62 / 3.53 ms
+#endif
+constexpr int kGroupMax = TP_GROUP_MAX;
 struct MultiSec {
   int g;
   Env env[kGroupMax];
