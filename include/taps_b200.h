@@ -145,6 +145,11 @@ typedef struct tp_cost_tensors {
    * solver's cond_min (solver.hpp:239-253), for both cost modes. */
   double* row_min_cost_s;          /* [num_rows] */
   double* row_min_volume_bytes;    /* [num_rows] */
+  /* Optional per-graph-edge minimum over its rows, the solver's pair_min
+   * (solver.hpp:254-255), both cost modes. Requires the row minima above
+   * (TP_ERR_INVALID_ARGUMENT otherwise). */
+  double* edge_pair_min_cost_s;       /* [num_edges of the slice] */
+  double* edge_pair_min_volume_bytes; /* [num_edges of the slice] */
 } tp_cost_tensors;
 
 typedef struct tp_build_opts {

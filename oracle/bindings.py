@@ -120,6 +120,8 @@ class BuildResult:
     records: Optional[np.ndarray] = None
     row_min_cost_s: Optional[np.ndarray] = None
     row_min_volume_bytes: Optional[np.ndarray] = None
+    edge_pair_min_cost_s: Optional[np.ndarray] = None
+    edge_pair_min_volume_bytes: Optional[np.ndarray] = None
     extra: dict = field(default_factory=dict)
 
 
@@ -141,6 +143,8 @@ def alloc_outputs(num_ops, num_edges, num_nodes, num_aux_edges, num_rows, record
     r.records = np.zeros(max(num_aux_edges, 1) * 40, np.uint8) if records else None
     r.row_min_cost_s = np.zeros(max(num_rows, 1))
     r.row_min_volume_bytes = np.zeros(max(num_rows, 1))
+    r.edge_pair_min_cost_s = np.zeros(max(num_edges, 1))
+    r.edge_pair_min_volume_bytes = np.zeros(max(num_edges, 1))
     return r
 
 
@@ -152,12 +156,13 @@ def index_struct(r: BuildResult) -> abi.tp_aux_index:
 
 
 def cost_struct(r: BuildResult) -> abi.tp_cost_tensors:
-    f = lambda a: abi.ptr(a, C.c_double)
+    f = lambda a: abi.ptr(a, C.c_double) if a is not None else None
     return abi.tp_cost_tensors(f(r.node_intra_cost_s), f(r.node_intra_volume_bytes),
                                f(r.node_memory_bytes), f(r.edge_cost_s), f(r.edge_volume_bytes),
                                f(r.edge_memory_bytes),
                                r.records.ctypes.data_as(C.c_void_p) if r.records is not None else None,
-                               f(r.row_min_cost_s), f(r.row_min_volume_bytes))
+                               f(r.row_min_cost_s), f(r.row_min_volume_bytes),
+                               f(r.edge_pair_min_cost_s), f(r.edge_pair_min_volume_bytes))
 
 
 def sizes(flat, topo):
@@ -180,6 +185,9 @@ def _trim(r: BuildResult, nn, ne, nr, num_ops, num_edges):
         r.records = r.records[: ne * 40]
     r.row_min_cost_s = r.row_min_cost_s[:nr]
     r.row_min_volume_bytes = r.row_min_volume_bytes[:nr]
+    if r.edge_pair_min_cost_s is not None:
+        r.edge_pair_min_cost_s = r.edge_pair_min_cost_s[:num_edges]
+        r.edge_pair_min_volume_bytes = r.edge_pair_min_volume_bytes[:num_edges]
     r.edge_from_op = r.edge_from_op[:num_edges]
     r.edge_to_op = r.edge_to_op[:num_edges]
     r.in_degree = r.in_degree[:num_ops]

@@ -142,6 +142,15 @@ void export_aux(const AuxiliaryGraph& aux, tp_aux_index* index,
       if (out->row_min_volume_bytes) out->row_min_volume_bytes[row] = mv;
     }
   }
+  // pair_min straight from the reference solver's own make_context (solver.hpp:218-287)
+  if (out->edge_pair_min_cost_s || out->edge_pair_min_volume_bytes) {
+    const detail::SearchContext ct = detail::make_context(aux, CostMode::kTopology, 0.0);
+    const detail::SearchContext cv = detail::make_context(aux, CostMode::kVolume, 0.0);
+    for (std::size_t e = 0; e < aux.graph.edges.size(); ++e) {
+      if (out->edge_pair_min_cost_s) out->edge_pair_min_cost_s[e] = ct.pair_min[e];
+      if (out->edge_pair_min_volume_bytes) out->edge_pair_min_volume_bytes[e] = cv.pair_min[e];
+    }
+  }
 }
 
 template <typename F>

@@ -1179,6 +1179,7 @@ static int build_impl(const tp_graph_desc* g, const tp_topology_desc* topo,
     const int64_t Su = node_base[u + 1] - node_base[u];
     const int64_t Sw = node_base[w + 1] - node_base[w];
     if ((ku < 0 || kw < 0) && Su > 0) { kind = TP_E_EDGE_TENSOR_MISSING; goto done; }
+    double pmin_c = 1.0 / 0.0, pmin_v = 1.0 / 0.0; /* pair_min, solver.hpp:254-255 */
     for (int64_t su = 0; su < Su; ++su) {
       const o_layout* from = &layouts[u][su * slots[u].nslots + ku];
       double rmin_c = 1.0 / 0.0, rmin_v = 1.0 / 0.0;
@@ -1224,7 +1225,11 @@ static int build_impl(const tp_graph_desc* g, const tp_topology_desc* topo,
       }
       if (out && out->row_min_cost_s) out->row_min_cost_s[rbase + su] = rmin_c;
       if (out && out->row_min_volume_bytes) out->row_min_volume_bytes[rbase + su] = rmin_v;
+      if (rmin_c < pmin_c) pmin_c = rmin_c;
+      if (rmin_v < pmin_v) pmin_v = rmin_v;
     }
+    if (out && out->edge_pair_min_cost_s) out->edge_pair_min_cost_s[e] = pmin_c;
+    if (out && out->edge_pair_min_volume_bytes) out->edge_pair_min_volume_bytes[e] = pmin_v;
     ebase += Su * Sw;
     rbase += Su;
   }

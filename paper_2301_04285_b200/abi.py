@@ -90,6 +90,8 @@ class tp_cost_tensors(C.Structure):
         ("aux_edge_records", C.c_void_p),
         ("row_min_cost_s", _p_f64),
         ("row_min_volume_bytes", _p_f64),
+        ("edge_pair_min_cost_s", _p_f64),
+        ("edge_pair_min_volume_bytes", _p_f64),
     ]
 
 

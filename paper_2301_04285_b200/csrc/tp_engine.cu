@@ -24,6 +24,8 @@
 //   node fan-out   class rows to every member operator's aux nodes
 // rowmin_kernel (optional, second launch): warp per (edge, su) row, lanes
 // over sw, shuffle min — the solver's cond_min (solver.hpp:239-253).
+// pairmin_kernel (optional, third launch): warp per edge over its row minima —
+// the solver's pair_min (solver.hpp:254-255).
 // The strategy tables (layout.hpp:270-328) are built once per plan by
 // table_kernel at upload and cached per device. Sweeps of many scenarios run
 // as one batched launch (fused_batch_kernel, tp_plan_execute_batch).
@@ -371,6 +373,10 @@ tp_status prepare_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   const bool skip_nodes = opts && opts->skip_nodes;
   static const tp_cost_tensors none{};
   if (!out) out = const_cast<tp_cost_tensors*>(&none);
+  if ((out->edge_pair_min_cost_s || out->edge_pair_min_volume_bytes) &&
+      !(out->row_min_cost_s && out->row_min_volume_bytes && out->edge_pair_min_cost_s &&
+        out->edge_pair_min_volume_bytes))
+    return set_err(TP_ERR_INVALID_ARGUMENT, 0, "pair minima need both row minima and both pair outputs");
   Sched* sched = (Sched*)A.d_sched.p;
   if (!A.sched_clean) {
     CUDA_TRY(cudaMemsetAsync(sched, 0, sizeof(Sched) + sizeof(Line) * (p->sigs.size() + 1), s));
@@ -540,6 +546,14 @@ tp_status finish_execute(tp_plan* p, tp_cost_tensors* out, cudaStream_t s, const
           (const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_maps.p, a.r_tab, a.cls_sv,
           out->row_min_cost_s, out->row_min_volume_bytes);
       ++launches;
+      // K4: pair_min (solver.hpp:254-255), a warp per graph edge over its row minima
+      if (out->edge_pair_min_cost_s) {
+        const int64_t edges = e1 - e0;
+        pairmin_kernel<<<(unsigned)((edges * 32 + th - 1) / th), th, 0, s>>>(
+            (const int64_t*)A.d_rowbase.p, edges, out->row_min_cost_s, out->row_min_volume_bytes,
+            out->edge_pair_min_cost_s, out->edge_pair_min_volume_bytes);
+        ++launches;
+      }
     }
   }
   CUDA_TRY(cudaGetLastError());
@@ -1005,6 +1019,8 @@ tp_status tp_plan_execute_host(tp_plan* p, const tp_build_opts* opts, tp_aux_ind
   d.aux_edge_records = dev(b[6], h.aux_edge_records, ne, 40);
   d.row_min_cost_s = (double*)dev(b[7], h.row_min_cost_s, nr, 8);
   d.row_min_volume_bytes = (double*)dev(b[8], h.row_min_volume_bytes, nr, 8);
+  d.edge_pair_min_cost_s = (double*)dev(b[9], h.edge_pair_min_cost_s, e1 - e0, 8);
+  d.edge_pair_min_volume_bytes = (double*)dev(b[10], h.edge_pair_min_volume_bytes, e1 - e0, 8);
   if (oom) return set_err(TP_ERR_CUDA, 0, "device allocation for the outputs failed");
   tp_build_opts o = opts ? *opts : tp_build_opts{0, -1, 0, -1, nullptr};
   o.stream = nullptr;
@@ -1027,6 +1043,8 @@ tp_status tp_plan_execute_host(tp_plan* p, const tp_build_opts* opts, tp_aux_ind
   ce = ce ? ce : back(h.aux_edge_records, d.aux_edge_records, ne, 40);
   ce = ce ? ce : back(h.row_min_cost_s, d.row_min_cost_s, nr, 8);
   ce = ce ? ce : back(h.row_min_volume_bytes, d.row_min_volume_bytes, nr, 8);
+  ce = ce ? ce : back(h.edge_pair_min_cost_s, d.edge_pair_min_cost_s, e1 - e0, 8);
+  ce = ce ? ce : back(h.edge_pair_min_volume_bytes, d.edge_pair_min_volume_bytes, e1 - e0, 8);
   st = tp_plan_check_errors(p);  // synchronises the stream
   if (ce != cudaSuccess) return set_err(TP_ERR_CUDA, 0, cudaGetErrorString(ce));
   if (st) return st;

@@ -999,6 +999,35 @@ __global__ void rowmin_kernel(const EdgeDesc* __restrict__ edges, const int64_t*
   }
 }
 
+// K4 (optional): pair_min (solver.hpp:254-255), warp per edge over the row
+// minima written by K3. min is exact, so the lane order cannot change a bit;
+// the select keeps std::min's "first wins on ties / NaN" form.
+__global__ void pairmin_kernel(const int64_t* __restrict__ row_base, int64_t nedges,
+                               const double* __restrict__ row_c, const double* __restrict__ row_v,
+                               double* __restrict__ out_c, double* __restrict__ out_v) {
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (e >= nedges) return;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  double mc = inf, mv = inf;
+  for (int64_t r = row_base[e] + lane; r < row_base[e + 1]; r += 32) {
+    const double c = row_c[r], v = row_v[r];
+    mc = c < mc ? c : mc;
+    mv = v < mv ? v : mv;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double oc = __shfl_xor_sync(0xffffffffu, mc, off);
+    const double ov = __shfl_xor_sync(0xffffffffu, mv, off);
+    mc = oc < mc ? oc : mc;
+    mv = ov < mv ? ov : mv;
+  }
+  if (lane == 0) {
+    out_c[e] = mc;
+    out_v[e] = mv;
+  }
+}
+
 // Verification export through the kernels' pair paths: thread form...
 __global__ void query_kernel(const tpk::QueryPOD* __restrict__ q, int n, tp_redist_result* __restrict__ r,
                              const double* __restrict__ tabs) {

@@ -87,7 +87,7 @@ struct Arena {
   DevBuf d_tabs, d_tables, d_classes, d_chks, d_slots, d_occs, d_members, d_sigs, d_edges,
       d_over, d_tables2, d_opnode, d_oprow, d_rowbase, d_sched, d_sidejobs,
       d_sides, d_price, d_pairsigs, d_trace, d_maps, d_rowcls, d_pairrec, d_prof, d_fsegs, d_rfirst;
-  DevBuf out[9];  // one-shot staging of the requested outputs
+  DevBuf out[11];  // one-shot staging of the requested outputs
   DevBuf d_desc;  // the descriptor pack
   void* h_stage = nullptr;  // pinned staging of the pack
   size_t h_stage_cap = 0;

@@ -48,6 +48,8 @@ class CostTensors:
     records: Optional[np.ndarray] = None
     row_min_cost_s: Optional[np.ndarray] = None
     row_min_volume_bytes: Optional[np.ndarray] = None
+    edge_pair_min_cost_s: Optional[np.ndarray] = None  # solver.hpp:254-255 pair_min
+    edge_pair_min_volume_bytes: Optional[np.ndarray] = None
     sizes: dict = field(default_factory=dict)
 
     def strategies_of(self, op: int) -> int:
@@ -219,11 +221,13 @@ class Plan:
             records=alloc(max(ne, 1) * 40, np.uint8) if records else None,
             row_min_cost_s=alloc(max(rows, 1), np.float64) if row_min else None,
             row_min_volume_bytes=alloc(max(rows, 1), np.float64) if row_min else None,
+            edge_pair_min_cost_s=alloc(max(e1 - e0, 1), np.float64) if row_min else None,
+            edge_pair_min_volume_bytes=alloc(max(e1 - e0, 1), np.float64) if row_min else None,
             sizes=dict(self.sizes), **ix)
         out = cost_struct(ct)
         o = abi.tp_build_opts(e0, e1, int(skip_nodes), -1, None)
         _check(self.lib, self.lib.tp_plan_execute_host(self.handle, C.byref(o), None, C.byref(out)))
-        _trim(ct, nn, ne, rows)
+        _trim(ct, nn, ne, rows, e1 - e0)
         return ct
 
 
@@ -238,7 +242,7 @@ def _pinned_empty(n, dtype):
     return torch.empty(n, dtype=tdt, pin_memory=True).numpy()
 
 
-def _trim(ct: CostTensors, nn, ne, rows):
+def _trim(ct: CostTensors, nn, ne, rows, nedges):
     for k in ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes"):
         setattr(ct, k, getattr(ct, k)[:nn])
     for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes"):
@@ -248,6 +252,9 @@ def _trim(ct: CostTensors, nn, ne, rows):
     if ct.row_min_cost_s is not None:
         ct.row_min_cost_s = ct.row_min_cost_s[:rows]
         ct.row_min_volume_bytes = ct.row_min_volume_bytes[:rows]
+    if ct.edge_pair_min_cost_s is not None:
+        ct.edge_pair_min_cost_s = ct.edge_pair_min_cost_s[:nedges]
+        ct.edge_pair_min_volume_bytes = ct.edge_pair_min_volume_bytes[:nedges]
 
 
 def cost_struct(ct) -> abi.tp_cost_tensors:
@@ -256,7 +263,8 @@ def cost_struct(ct) -> abi.tp_cost_tensors:
         f(ct.node_intra_cost_s), f(ct.node_intra_volume_bytes), f(ct.node_memory_bytes),
         f(ct.edge_cost_s), f(ct.edge_volume_bytes), f(ct.edge_memory_bytes),
         ct.records.ctypes.data_as(C.c_void_p) if ct.records is not None else None,
-        f(ct.row_min_cost_s), f(ct.row_min_volume_bytes))
+        f(ct.row_min_cost_s), f(ct.row_min_volume_bytes),
+        f(ct.edge_pair_min_cost_s), f(ct.edge_pair_min_volume_bytes))
 
 
 def device_cost_struct(tensors: dict) -> abi.tp_cost_tensors:
@@ -268,7 +276,8 @@ def device_cost_struct(tensors: dict) -> abi.tp_cost_tensors:
     return abi.tp_cost_tensors(p("node_intra_cost_s"), p("node_intra_volume_bytes"), p("node_memory_bytes"),
                                p("edge_cost_s"), p("edge_volume_bytes"), p("edge_memory_bytes"),
                                C.c_void_p(rec.data_ptr()) if rec is not None else None,
-                               p("row_min_cost_s"), p("row_min_volume_bytes"))
+                               p("row_min_cost_s"), p("row_min_volume_bytes"),
+                               p("edge_pair_min_cost_s"), p("edge_pair_min_volume_bytes"))
 
 
 def build_cost_tensors(graph, topo: ClusterTopology, records=False, row_min=False,

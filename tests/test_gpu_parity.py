@@ -34,7 +34,7 @@ def assert_same(gpu, ref, rowmin=False, records=False):
         bad = np.flatnonzero(bits(a) != bits(b))
         assert bad.size == 0, f"{k}: {bad.size} mismatches, first {bad[:5]} gpu={a[bad[:3]]} ref={b[bad[:3]]}"
     if rowmin:
-        for k in ("row_min_cost_s", "row_min_volume_bytes"):
+        for k in ("row_min_cost_s", "row_min_volume_bytes", "edge_pair_min_cost_s", "edge_pair_min_volume_bytes"):
             assert np.array_equal(bits(getattr(gpu, k)), bits(getattr(ref, k))), k
     if records:
         ra = gpu.records.reshape(-1, 40).copy()
@@ -317,3 +317,35 @@ def test_cfg3_ratio_sweep_by_repricing(nodes):
         got = plan.execute_host(row_min=True)
         ref = B.oracle_build(f, t, records=False)
         assert_same(got, ref, rowmin=True)
+
+
+def test_pair_min_device_and_slices():
+    """pair_min (solver.hpp:254-255) on device tensors and on edge slices, bit-identical to the
+    oracle (itself pinned to the reference's make_context); pair outputs without the row minima
+    are rejected with TP_ERR_INVALID_ARGUMENT before any launch."""
+    import torch
+    from paper_2301_04285_b200 import abi
+    g, t = M.cfg2()
+    f = G.flatten(g)
+    ref = B.oracle_build(f, t, records=False)
+    plan = engine.Plan(f, t, device=0)
+    sz = plan.sizes
+    dev = torch.device("cuda", 0)
+    ne, nr = f.num_edges, int(sz["num_rows"])
+    outs = {k: torch.empty(sz["num_aux_edges"], dtype=torch.float64, device=dev)
+            for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes")}
+    outs["edge_pair_min_cost_s"] = torch.empty(ne, dtype=torch.float64, device=dev)
+    outs["edge_pair_min_volume_bytes"] = torch.empty(ne, dtype=torch.float64, device=dev)
+    with pytest.raises(ValueError):
+        plan.execute(engine.device_cost_struct(outs))
+    outs["row_min_cost_s"] = torch.empty(nr, dtype=torch.float64, device=dev)
+    outs["row_min_volume_bytes"] = torch.empty(nr, dtype=torch.float64, device=dev)
+    plan.execute(engine.device_cost_struct(outs))
+    plan.check_errors()
+    for k in ("row_min_cost_s", "row_min_volume_bytes", "edge_pair_min_cost_s", "edge_pair_min_volume_bytes"):
+        assert np.array_equal(bits(outs[k].cpu().numpy()), bits(getattr(ref, k))), k
+    for e0, e1 in ((0, 1), (3, 9), (ne - 2, ne)):
+        got = plan.execute_host(row_min=True, edge_range=(e0, e1))
+        np.testing.assert_array_equal(bits(got.edge_pair_min_cost_s), bits(ref.edge_pair_min_cost_s[e0:e1]))
+        np.testing.assert_array_equal(bits(got.edge_pair_min_volume_bytes),
+                                      bits(ref.edge_pair_min_volume_bytes[e0:e1]))

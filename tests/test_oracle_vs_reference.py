@@ -12,7 +12,8 @@ pytestmark = pytest.mark.skipif(not B.have_reference(), reason="oracle/_ref not 
 
 FIELDS = ("node_base", "edge_base", "in_degree", "out_degree", "topo_order", "edge_from_op", "edge_to_op",
           "node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes", "edge_cost_s",
-          "edge_volume_bytes", "edge_memory_bytes", "row_min_cost_s", "row_min_volume_bytes")
+          "edge_volume_bytes", "edge_memory_bytes", "row_min_cost_s", "row_min_volume_bytes",
+          "edge_pair_min_cost_s", "edge_pair_min_volume_bytes")
 
 
 def same(o, r):
