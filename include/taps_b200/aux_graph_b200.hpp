@@ -112,10 +112,22 @@ struct PlanGuard {
 
 }  // namespace detail
 
+// Optional side outputs of the build for the solver's search context
+// (solver.hpp:218-287): per-(edge, producer strategy) row minima (cond_min,
+// rows edge-major) and per-edge minima (pair_min), both cost modes, computed
+// on the device; plus find_op of each edge's endpoints. Consumed by
+// make_context_b200 (solver_b200.hpp).
+struct SolverMinima {
+  std::vector<double> row_min_cost_s, row_min_volume_bytes;    // [num_rows]
+  std::vector<double> pair_min_cost_s, pair_min_volume_bytes;  // [num_edges]
+  std::vector<int32_t> edge_from_op, edge_to_op;               // [num_edges]
+};
+
 inline topoplan::AuxiliaryGraph build_auxiliary_graph_b200(const topoplan::ComputationGraph& graph,
                                                            const topoplan::ClusterTopology& topo,
                                                            topoplan::CostMode mode = topoplan::CostMode::kTopology,
-                                                           int device = -1, bool with_layouts = false) {
+                                                           int device = -1, bool with_layouts = false,
+                                                           SolverMinima* minima = nullptr) {
   static_assert(sizeof(topoplan::AuxEdge) == 40, "AuxEdge layout differs from the device records");
   topoplan::AuxiliaryGraph aux;
   aux.graph = graph;
@@ -143,8 +155,26 @@ inline topoplan::AuxiliaryGraph build_auxiliary_graph_b200(const topoplan::Compu
   out.node_intra_volume_bytes = n_vol.data();
   out.node_memory_bytes = n_mem.data();
   out.aux_edge_records = aux.edges.data();
+  if (minima) {
+    minima->row_min_cost_s.assign(sz.num_rows + 1, 0.0);
+    minima->row_min_volume_bytes.assign(sz.num_rows + 1, 0.0);
+    minima->pair_min_cost_s.assign(n_edges + 1, 0.0);
+    minima->pair_min_volume_bytes.assign(n_edges + 1, 0.0);
+    out.row_min_cost_s = minima->row_min_cost_s.data();
+    out.row_min_volume_bytes = minima->row_min_volume_bytes.data();
+    out.edge_pair_min_cost_s = minima->pair_min_cost_s.data();
+    out.edge_pair_min_volume_bytes = minima->pair_min_volume_bytes.data();
+  }
   detail::check(tp_plan_execute_host(plan.p, nullptr, &ix, &out));
 
+  if (minima) {
+    minima->row_min_cost_s.resize(sz.num_rows);
+    minima->row_min_volume_bytes.resize(sz.num_rows);
+    minima->pair_min_cost_s.resize(n_edges);
+    minima->pair_min_volume_bytes.resize(n_edges);
+    minima->edge_from_op.assign(from_op.begin(), from_op.begin() + n_edges);
+    minima->edge_to_op.assign(to_op.begin(), to_op.begin() + n_edges);
+  }
   aux.topo_order.assign(order.begin(), order.begin() + n_ops);
   aux.in_degree_of.assign(in_deg.begin(), in_deg.begin() + n_ops);
   aux.out_degree_of.assign(out_deg.begin(), out_deg.begin() + n_ops);

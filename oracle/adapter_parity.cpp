@@ -20,6 +20,7 @@
 #include "topoplan/solver.hpp"
 #include "test_support.hpp"  // the reference's test oracles, -I$(REF_TESTS) (see Makefile)
 #include "taps_b200/aux_graph_b200.hpp"
+#include "taps_b200/solver_b200.hpp"
 
 using namespace topoplan;
 
@@ -81,6 +82,7 @@ struct SolveCfg {
 void check_case(const std::string& name, const ComputationGraph& graph, const ClusterTopology& topo,
                 SolveCfg sc = {}) {
   AuxiliaryGraph ref, gpu;
+  taps_b200::SolverMinima minima;
   std::string ref_err, gpu_err;
   try {
     ref = build_auxiliary_graph(graph, topo);
@@ -90,7 +92,7 @@ void check_case(const std::string& name, const ComputationGraph& graph, const Cl
     ref_err = "out_of_range";
   }
   try {
-    gpu = taps_b200::build_auxiliary_graph_b200(graph, topo, CostMode::kTopology, -1, true);
+    gpu = taps_b200::build_auxiliary_graph_b200(graph, topo, CostMode::kTopology, -1, true, &minima);
   } catch (const Error& e) {
     gpu_err = "Error";
   } catch (const std::out_of_range& e) {
@@ -109,6 +111,25 @@ void check_case(const std::string& name, const ComputationGraph& graph, const Cl
     const EdgeWeight b = edge_weight(gpu.graph, 0, gpu.nodes[gpu.edges[0].from_node],
                                      gpu.nodes[gpu.edges[0].to_node], topo);
     if (!same_bits(a.cost_s, b.cost_s)) err = "edge_weight via layouts";
+  }
+  // the solver's search context (solver.hpp:218-287) from the device minima
+  for (CostMode mode : {CostMode::kTopology, CostMode::kVolume}) {
+    if (!err.empty()) break;
+    const detail::SearchContext a = detail::make_context(ref, mode, topo.device_memory);
+    const detail::SearchContext b = taps_b200::make_context_b200(gpu, minima, mode, topo.device_memory);
+    auto same_vec = [](const std::vector<double>& x, const std::vector<double>& y) {
+      if (x.size() != y.size()) return false;
+      for (std::size_t i = 0; i < x.size(); ++i)
+        if (!same_bits(x[i], y[i])) return false;
+      return true;
+    };
+    bool ok = a.order == b.order && a.pos_of_op == b.pos_of_op && a.in_edges_of == b.in_edges_of &&
+              a.cond_min.size() == b.cond_min.size() && same_vec(a.pair_min, b.pair_min) &&
+              same_vec(a.source_min, b.source_min) && same_vec(a.suffix_mem_min, b.suffix_mem_min) &&
+              same_vec(a.virtual_min_mem, b.virtual_min_mem) && same_bits(a.root_bound, b.root_bound) &&
+              same_bits(a.memory_bound, b.memory_bound) && a.mode == b.mode;
+    for (std::size_t e = 0; ok && e < a.cond_min.size(); ++e) ok = same_vec(a.cond_min[e], b.cond_min[e]);
+    if (!ok) err = std::string("make_context_b200 differs (") + to_string(mode) + ")";
   }
   std::string extra = std::to_string(gpu.edges.size()) + " aux edges bit-identical";
   if (err.empty() && sc.solve) {

@@ -264,7 +264,7 @@ def cost_struct(ct) -> abi.tp_cost_tensors:
         f(ct.edge_cost_s), f(ct.edge_volume_bytes), f(ct.edge_memory_bytes),
         ct.records.ctypes.data_as(C.c_void_p) if ct.records is not None else None,
         f(ct.row_min_cost_s), f(ct.row_min_volume_bytes),
-        f(ct.edge_pair_min_cost_s), f(ct.edge_pair_min_volume_bytes))
+        f(getattr(ct, "edge_pair_min_cost_s", None)), f(getattr(ct, "edge_pair_min_volume_bytes", None)))
 
 
 def device_cost_struct(tensors: dict) -> abi.tp_cost_tensors:
