@@ -9,6 +9,7 @@
 // the same objective on both, that price_assignment agrees and that
 // export_lp emits the same text. Built by oracle/Makefile into
 // oracle/_ref/adapter_parity; run on a GPU box by tests/test_gpu_adapter.py.
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -131,7 +132,40 @@ void check_case(const std::string& name, const ComputationGraph& graph, const Cl
     for (std::size_t e = 0; ok && e < a.cond_min.size(); ++e) ok = same_vec(a.cond_min[e], b.cond_min[e]);
     if (!ok) err = std::string("make_context_b200 differs (") + to_string(mode) + ")";
   }
+  // formulate_b200 against the reference's formulate (solver.hpp:69-176), field by field
+  double t_ref_ms = 0, t_b200_ms = 0;
+  for (CostMode mode : {CostMode::kTopology, CostMode::kVolume}) {
+    if (!err.empty()) break;
+    const auto t0 = std::chrono::steady_clock::now();
+    const IlpProblem a = formulate(ref, mode, topo.device_memory);
+    const auto t1 = std::chrono::steady_clock::now();
+    const IlpProblem b = taps_b200::formulate_b200(gpu, mode, topo.device_memory);
+    const auto t2 = std::chrono::steady_clock::now();
+    t_ref_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+    t_b200_ms += std::chrono::duration<double, std::milli>(t2 - t1).count();
+    bool ok = a.mode == b.mode && same_bits(a.memory_bound, b.memory_bound) && a.vars.size() == b.vars.size() &&
+              a.objective.size() == b.objective.size() && a.rows.size() == b.rows.size() &&
+              a.x_var_of_node == b.x_var_of_node && a.b_var_of_edge == b.b_var_of_edge;
+    for (std::size_t i = 0; ok && i < a.vars.size(); ++i) {
+      const auto &x = a.vars[i], &y = b.vars[i];
+      ok = x.kind == y.kind && x.name == y.name && x.op_index == y.op_index &&
+           x.strategy_index == y.strategy_index && x.edge_id == y.edge_id && same_bits(a.objective[i], b.objective[i]);
+    }
+    for (std::size_t i = 0; ok && i < a.rows.size(); ++i) {
+      const auto &x = a.rows[i], &y = b.rows[i];
+      ok = x.name == y.name && x.is_equality == y.is_equality && same_bits(x.rhs, y.rhs) &&
+           x.terms.size() == y.terms.size();
+      for (std::size_t k = 0; ok && k < x.terms.size(); ++k)
+        ok = x.terms[k].first == y.terms[k].first && same_bits(x.terms[k].second, y.terms[k].second);
+    }
+    if (!ok) err = std::string("formulate_b200 differs (") + to_string(mode) + ")";
+  }
   std::string extra = std::to_string(gpu.edges.size()) + " aux edges bit-identical";
+  if (gpu.edges.size() >= 100000) {
+    char buf[128];
+    std::snprintf(buf, sizeof(buf), "; formulate x2 modes %.1f ms, formulate_b200 %.1f ms", t_ref_ms, t_b200_ms);
+    extra += buf;
+  }
   if (err.empty() && sc.solve) {
     for (CostMode mode : {CostMode::kTopology, CostMode::kVolume}) {
       SolveOptions opts;
