@@ -700,9 +700,9 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     if (B.resident == 0) {
       int sms = 0, per_sm = 0;
       CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_batch_kernel<0>, kFusedThreads, 0));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_batch_kernel<0>, kFusedThreads, kMsecBytes));
       B.resident = std::max(1, sms * std::max(1, per_sm));
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_batch_kernel<3>, kFusedThreads, 0));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_batch_kernel<3>, kFusedThreads, kMsecBytes));
       B.resident_wide = std::max(1, sms * std::max(1, per_sm));
     }
     int nwarp = 0;
@@ -822,9 +822,9 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     const int64_t* dto = duo + 2 * (m + 1);
     BatchHdr* hd = (BatchHdr*)B.d_hdr.p;
     if (form == 1) fused_batch_kernel<1><<<gd, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
-    else if (form == 2) fused_batch_kernel<2><<<gd, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
-    else if (form == 3) fused_batch_kernel<3><<<gd, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
-    else fused_batch_kernel<0><<<gd, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
+    else if (form == 2) fused_batch_kernel<2><<<gd, bd, kMsecBytes, s>>>(da, m, duo, dio, dto, hd, err_dev);
+    else if (form == 3) fused_batch_kernel<3><<<gd, bd, kMsecBytes, s>>>(da, m, duo, dio, dto, hd, err_dev);
+    else fused_batch_kernel<0><<<gd, bd, kMsecBytes, s>>>(da, m, duo, dio, dto, hd, err_dev);
     if (cudaPeekAtLastError() != cudaSuccess) {
       B.hdr_clean = false;
       for (int k : live) plans[k]->arena->sched_clean = false;

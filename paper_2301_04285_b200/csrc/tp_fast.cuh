@@ -138,11 +138,26 @@ TP_HD double price_fast(bool a2a, int te, int rexp, int ek, int s, double bytes,
 #define TP_GROUP_MAX 16  // measured on cfg5: 4 / 8 / 16 / 32 / 64 -> 3.05 / 2.55 / 2.26 / 2.62 / 3.53 ms
 #endif
 constexpr int kGroupMax = TP_GROUP_MAX;
+// The members of a bandwidth group. Member q's Env and bandwidth table are
+// read in place from its argument block (base + idx[q] * stride) and its
+// seconds accumulate in sec[q * sec_stride] (shared memory on the device):
+// no per-member copies or read-modify-writes in local memory.
+constexpr int kBwEntries = 65;  // bw[] entries before the scale table (== kBwTab, tp_warp.cuh)
+
 struct MultiSec {
   int g;
-  Env env[kGroupMax];
-  FastTabs tab[kGroupMax];
-  double sec[kGroupMax];
+  const char* base;
+  const int32_t* idx;
+  int stride, env_off, bw_off;
+  double* sec;
+  int sec_stride;
+  TP_HD const char* blk(int q) const { return base + (size_t)idx[q] * stride; }
+  TP_HD const Env& env(int q) const { return *reinterpret_cast<const Env*>(blk(q) + env_off); }
+  TP_HD FastTabs tab(int q) const {
+    const double* bw = *reinterpret_cast<const double* const*>(blk(q) + bw_off);
+    return FastTabs{bw, bw + kBwEntries};
+  }
+  TP_HD double& s(int q) { return sec[q * sec_stride]; }
 };
 
 #if defined(__CUDACC__)
@@ -157,7 +172,7 @@ TP_HD_NOINL void price_members(MultiSec* ms, bool a2a, int pos, int rexp, int e,
                                   int l_log2) {
   for (int q = 1; q < ms->g; ++q) {
     double dv = 0;
-    ms->sec[q] += price_fast(a2a, pos, rexp, e, s, bytes, ms->env[q], l_log2, ms->tab[q], &dv, nullptr);
+    ms->s(q) += price_fast(a2a, pos, rexp, e, s, bytes, ms->env(q), l_log2, ms->tab(q), &dv, nullptr);
   }
 }
 
@@ -369,7 +384,7 @@ TP_HD int pair_cost_sd(int R, const SideDesc& F, const SideDesc& T, const Lay* F
                        double bytes, const Env& env, int l_log2, const FastTabs& tab, double& sec, double& vol,
                        Trace* tr, MultiSec* ms = nullptr) {
   if (ms)
-    for (int q = 1; q < ms->g; ++q) ms->sec[q] = 0;
+    for (int q = 1; q < ms->g; ++q) ms->s(q) = 0;
   const int st = redist_cost_fast(R, F, T, dt, bytes, env, l_log2, tab, sec, vol, tr, ms);
   if (st != -1) return st;
   Lay a, b;
@@ -378,10 +393,10 @@ TP_HD int pair_cost_sd(int R, const SideDesc& F, const SideDesc& T, const Lay* F
   // the array form (rare: a device dim held twice), once per member, one call site
   for (int q = ms ? ms->g - 1 : 0; q >= 0; --q) {
     double sc = 0, v = 0;
-    const int e = redist_cost(R, a, b, dt, bytes, q ? ms->env[q] : env, sc, v, q ? nullptr : tr);
+    const int e = redist_cost(R, a, b, dt, bytes, q ? ms->env(q) : env, sc, v, q ? nullptr : tr);
     if (e) return e;
     if (q) {
-      ms->sec[q] = sc;
+      ms->s(q) = sc;
     } else {
       sec = sc;
       vol = v;

@@ -322,6 +322,10 @@ struct FusedArgs {
 };
 
 constexpr int kFusedThreads = 256;
+// bandwidth-group member seconds of the batch kernel's thread-form pricing
+// (pair_thread), one column per thread: dynamic shared memory of fused_batch_kernel
+static_assert(tpk::kBwEntries == tpk::kBwTab, "bandwidth table layout");
+constexpr int kMsecBytes = (int)(tpk::kGroupMax * kFusedThreads * sizeof(double));
 
 // One aux-node row of a node class (aux_graph.hpp:120-167) on one warp:
 // lanes take the slice checks and the tensor occurrences in parallel (their
@@ -420,14 +424,18 @@ __device__ void pair_thread(const FusedArgs& a, int64_t idx, const double* price
   const tpk::SideDesc F = pr.F, T = pr.T;
   const int R = pr.R;
   const int g = (all && a.group_n > 1) ? a.group_n : 1;
+  // member seconds in the batch kernel's dynamic shared memory (kMsecBytes)
+  extern __shared__ double s_msec[];
   tpk::MultiSec ms;
   ms.g = g;
-  for (int q = 1; q < g; ++q) {
-    const FusedArgs& b = all[a.group[q]];
-    ms.env[q] = b.env;
-    ms.tab[q] = tpk::FastTabs{b.bw_tab, b.bw_tab + tpk::kBwTab};
-    ms.sec[q] = 0;
-  }
+  ms.base = reinterpret_cast<const char*>(all);
+  ms.idx = a.group;
+  ms.stride = (int)sizeof(FusedArgs);
+  ms.env_off = (int)offsetof(FusedArgs, env);
+  ms.bw_off = (int)offsetof(FusedArgs, bw_tab);
+  ms.sec = s_msec + threadIdx.x;
+  ms.sec_stride = kFusedThreads;
+  for (int q = 1; q < g; ++q) ms.s(q) = 0;
   double sec = 0, vol = 0;
   if (!tpk::same_side(F, T, R)) {  // aux_graph.hpp:260
     const int st = tpk::pair_cost_sd(R, F, T, nullptr, nullptr, pr.dt, pr.bytes, a.env, a.l_log2,
@@ -438,11 +446,11 @@ __device__ void pair_thread(const FusedArgs& a, int64_t idx, const double* price
       flag_error(a.err, key);
       for (int q = 1; q < g; ++q) flag_error(all[a.group[q]].err, key);
       sec = vol = 0;
-      for (int q = 1; q < g; ++q) ms.sec[q] = 0;
+      for (int q = 1; q < g; ++q) ms.s(q) = 0;
     }
   }
   a.r_tab[idx] = make_double2(sec, vol);
-  for (int q = 1; q < g; ++q) all[a.group[q]].r_tab[idx] = make_double2(ms.sec[q], vol);
+  for (int q = 1; q < g; ++q) all[a.group[q]].r_tab[idx] = make_double2(ms.s(q), vol);
 }
 
 // One class-table entry on one warp (warp form, tp_warp.cuh); lane 0 writes.
