@@ -123,10 +123,11 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """dram bytes per launch of the fused kernel from the committed ncu
-    capture (profiles/ncu_fused_latest.json), or None."""
-    path = os.path.join(REPO, "profiles", "ncu_fused_latest.json")
+def ncu_traffic(name="ncu_fused_latest.json"):
+    """dram bytes per launch of the fused kernel (or, with
+    name="ncu_batch_latest.json", the batch kernel) from the committed ncu
+    capture under profiles/, or None."""
+    path = os.path.join(REPO, "profiles", name)
     try:
         with open(path) as fh:
             j = json.load(fh)
@@ -334,6 +335,9 @@ def measure_sweep(args, rank, world, local, dist, K, W, with_clocks=False, with_
     peak, peak_kind = measured_peak()
     out_bytes = BYTES_PER_EVAL * (int(eoff[-1]) + int(noff[-1]))
     achieved = out_bytes / (dev_ms / K / 1e3) / 1e9
+    traffic, traffic_edges, traffic_note = ncu_traffic("ncu_batch_latest.json")
+    if traffic is not None and traffic_edges and traffic_edges != int(eoff[-1]):
+        traffic = traffic * int(eoff[-1]) / traffic_edges  # the capture covers all 1,000 scenarios on one GPU
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -345,7 +349,8 @@ def measure_sweep(args, rank, world, local, dist, K, W, with_clocks=False, with_
                    "l2": "256 MiB buffer written between timed steps (flush)",
                    "build_ms_e2e": sum(e2e_t) / KE * 1e3},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "fused_batch_kernel (all scenarios of the rank in one persistent launch)",
+                     "traffic": traffic, "traffic_note": traffic_note,
+                     "kernel": "fused_batch_kernel (all scenarios of the rank in one persistent launch)",
                      "bytes_per_launch": out_bytes,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
         "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": h2d,
