@@ -51,3 +51,30 @@ def test_strategy_count_query_needs_no_gpu(engine):
     assert engine.tp_enumerate_strategies(3, 128, C.byref(n), None, None, None, None) == 0
     assert n.value == 129
     assert engine.tp_enumerate_strategies(3, 6, C.byref(n), None, None, None, None) == abi.TP_ERR_TOPOPLAN
+
+
+STRUCTS = ("tp_graph_desc", "tp_topology_desc", "tp_aux_index", "tp_cost_tensors", "tp_build_opts",
+           "tp_plan_sizes_t", "tp_redist_query", "tp_redist_result")
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """Every ctypes mirror in abi.py has the C header's size and field offsets
+    (a field appended to the header but not to abi.py would shift everything
+    the Python side passes across the ABI)."""
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void) {"]
+    for s in STRUCTS:
+        lines.append(f'  printf("{s} sizeof %zu\\n", sizeof({s}));')
+        for f, _ in getattr(abi, s)._fields_:
+            lines.append(f'  printf("{s} {f} %zu\\n", offsetof({s}, {f}));')
+    lines += ["  return 0;", "}"]
+    src, exe = tmp_path / "probe.c", tmp_path / "probe"
+    src.write_text("\n".join(lines) + "\n")
+    import subprocess
+    subprocess.run(["gcc", "-std=c99", "-o", str(exe), str(src)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for s in STRUCTS:
+        cls = getattr(abi, s)
+        assert got[(s, "sizeof")] == C.sizeof(cls), s
+        for f, _ in cls._fields_:
+            assert got[(s, f)] == getattr(cls, f).offset, (s, f)
