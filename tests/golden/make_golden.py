@@ -36,7 +36,9 @@ def build_case(name, g, t, solve=False, threads=8):
                     node_intra_cost_s=hx(r.node_intra_cost_s), node_intra_volume_bytes=hx(r.node_intra_volume_bytes),
                     node_memory_bytes=hx(r.node_memory_bytes), edge_cost_s=hx(r.edge_cost_s),
                     edge_volume_bytes=hx(r.edge_volume_bytes), edge_memory_bytes=hx(r.edge_memory_bytes),
-                    row_min_cost_s=hx(r.row_min_cost_s), row_min_volume_bytes=hx(r.row_min_volume_bytes))
+                    row_min_cost_s=hx(r.row_min_cost_s), row_min_volume_bytes=hx(r.row_min_volume_bytes),
+                    edge_pair_min_cost_s=hx(r.edge_pair_min_cost_s),  # make_context's pair_min
+                    edge_pair_min_volume_bytes=hx(r.edge_pair_min_volume_bytes))
         if solve:
             case["ilp"] = {}
             for mode in ("topology", "volume"):

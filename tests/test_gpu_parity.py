@@ -137,7 +137,7 @@ def test_golden_builds(idx, form):
     assert got.node_base.tolist() == c["node_base"]
     assert got.edge_base.tolist() == c["edge_base"]
     assert got.topo_order.tolist() == c["topo_order"]
-    for k in FIELDS + ("row_min_cost_s", "row_min_volume_bytes"):
+    for k in FIELDS + ("row_min_cost_s", "row_min_volume_bytes", "edge_pair_min_cost_s", "edge_pair_min_volume_bytes"):
         exp = unhex(c[k])
         assert np.array_equal(bits(getattr(got, k)), bits(exp)), (c["name"], k)
 
