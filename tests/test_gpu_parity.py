@@ -349,3 +349,24 @@ def test_pair_min_device_and_slices():
         np.testing.assert_array_equal(bits(got.edge_pair_min_cost_s), bits(ref.edge_pair_min_cost_s[e0:e1]))
         np.testing.assert_array_equal(bits(got.edge_pair_min_volume_bytes),
                                       bits(ref.edge_pair_min_volume_bytes[e0:e1]))
+
+
+def test_cfg4_minima_properties():
+    """Full cfg4 (2,155,580 aux edges): the device row and pair minima equal
+    the minima of the device's own cost blocks (solver.hpp:239-255), both
+    modes — a size-independent check next to the oracle comparisons."""
+    g, t = M.cfg4()
+    ct = gpu_build(g, t, row_min=True)
+    nb, eb = ct.node_base, ct.edge_base
+    r = 0
+    for e in range(len(ct.edge_from_op)):
+        su_n = int(nb[ct.edge_from_op[e] + 1] - nb[ct.edge_from_op[e]])
+        sw_n = int(nb[ct.edge_to_op[e] + 1] - nb[ct.edge_to_op[e]])
+        for src, rows, pair in (("edge_cost_s", "row_min_cost_s", "edge_pair_min_cost_s"),
+                                ("edge_volume_bytes", "row_min_volume_bytes", "edge_pair_min_volume_bytes")):
+            blk = getattr(ct, src)[eb[e]:eb[e] + su_n * sw_n].reshape(su_n, sw_n)
+            rm = blk.min(axis=1)
+            assert np.array_equal(bits(rm), bits(getattr(ct, rows)[r:r + su_n])), (e, rows)
+            assert bits(np.array([rm.min()]))[0] == bits(getattr(ct, pair)[e:e + 1])[0], (e, pair)
+        r += su_n
+    assert r == len(ct.row_min_cost_s)
