@@ -31,7 +31,8 @@
 extern "C" {
 #endif
 
-#define TP_ABI_VERSION 1
+/* 2: tp_cost_tensors gained edge_pair_min_cost_s / edge_pair_min_volume_bytes (appended). */
+#define TP_ABI_VERSION 2
 
 typedef enum tp_status {
   TP_OK = 0,

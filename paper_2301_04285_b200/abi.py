@@ -9,6 +9,9 @@ from __future__ import annotations
 import ctypes as C
 import os
 
+# include/taps_b200.h TP_ABI_VERSION this module's struct mirrors follow
+TP_ABI_VERSION = 2
+
 TP_OK = 0
 TP_ERR_INVALID_ARGUMENT = 1
 TP_ERR_TOPOPLAN = 2
@@ -257,6 +260,8 @@ def load_engine() -> C.CDLL:
     lib.tp_last_error_kind.restype = C.c_int32
     lib.tp_abi_version.argtypes = []
     lib.tp_abi_version.restype = C.c_int32
+    if lib.tp_abi_version() != TP_ABI_VERSION:  # a stale build would read the structs wrong
+        raise EngineMissing(f"{ENGINE_SO} has ABI version {lib.tp_abi_version()}, expected {TP_ABI_VERSION}; rebuild it")
     _engine = lib
     return lib
 

@@ -27,7 +27,7 @@ def test_header_declarations_are_exported(engine):
 
 
 def test_abi_version(engine):
-    assert engine.tp_abi_version() == 1
+    assert engine.tp_abi_version() == abi.TP_ABI_VERSION == 2
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")

@@ -45,7 +45,7 @@ def assert_same(gpu, ref, rowmin=False, records=False):
 
 
 def test_abi_version(engine):
-    assert engine.tp_abi_version() == 1
+    assert engine.tp_abi_version() == abi.TP_ABI_VERSION == 2
 
 
 @pytest.mark.parametrize("p,N", [(1, 1), (2, 8), (3, 4), (3, 8), (2, 128), (3, 128), (4, 64), (5, 32)])
