@@ -259,7 +259,11 @@ tp_status tp_plan_create_batch(const tp_graph_desc* const* graphs,
                                int32_t device, int32_t host_threads,
                                tp_plan** plans_out, int32_t* status_out);
 /* Execute plans[i] into HOST pointers host_outs[i] (like tp_plan_execute_host,
- * whole graphs, nodes included). index_outs may be NULL. Plans with their own
+ * whole graphs, nodes included; every tp_cost_tensors field is honoured).
+ * Plans on one device whose outputs are only the six SoA tensors run as ONE
+ * batched launch (tp_plan_execute_batch) with one D2H per tensor kind; AuxEdge
+ * records or solver minima, or plans on several devices, take one
+ * tp_plan_execute_host per plan on the worker threads. index_outs may be NULL. Plans with their own
  * uploaded arena (tp_plan_upload called) keep it; the others borrow a pooled
  * per-worker arena for the duration of the call. NULL plans are skipped with
  * status TP_ERR_INVALID_ARGUMENT. */

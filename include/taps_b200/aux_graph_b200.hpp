@@ -105,6 +105,14 @@ inline void check(tp_status st) {
   if (st != TP_OK) throw_status(st);
 }
 
+// The structs of include/taps_b200.h this header was compiled with must be
+// the library's (tp_cost_tensors grew in ABI 2): refuse another version.
+inline void check_abi() {
+  if (tp_abi_version() != TP_ABI_VERSION)
+    throw std::runtime_error("taps_b200: libtaps_b200 ABI version " + std::to_string(tp_abi_version()) +
+                             " differs from the header's " + std::to_string(TP_ABI_VERSION));
+}
+
 struct PlanGuard {
   tp_plan* p = nullptr;
   ~PlanGuard() { tp_plan_destroy(p); }
@@ -129,6 +137,7 @@ inline topoplan::AuxiliaryGraph build_auxiliary_graph_b200(const topoplan::Compu
                                                            int device = -1, bool with_layouts = false,
                                                            SolverMinima* minima = nullptr) {
   static_assert(sizeof(topoplan::AuxEdge) == 40, "AuxEdge layout differs from the device records");
+  detail::check_abi();
   topoplan::AuxiliaryGraph aux;
   aux.graph = graph;
   aux.topo = topo;

@@ -182,9 +182,9 @@ void check_case(const std::string& name, const ComputationGraph& graph, const Cl
         err = std::string("export_lp differs (") + to_string(mode) + ")";
         break;
       }
-      char buf[160];
-      std::snprintf(buf, sizeof(buf), "; ILP %s obj %.6g %s", to_string(mode), a.objective,
-                    a.optimal ? "optimal" : "budget");
+      char buf[200];
+      std::snprintf(buf, sizeof(buf), "; ILP %s obj %.17g %s (%lld nodes)", to_string(mode), a.objective,
+                    a.optimal ? "optimal" : "budget", (long long)a.nodes_explored);
       extra += buf;
     }
     std::mt19937 rng(7);
@@ -305,7 +305,7 @@ void check_sweep(int count, int every) {
 }  // namespace
 
 int main(int argc, char** argv) {
-  const bool big = argc > 1 && std::string(argv[1]) == "--big";
+  const bool big = argc > 1 && std::string(argv[1]) == "--big";  // every 10th cfg5 scenario instead of every 40th
   const ClusterTopology t2x4{2, 4, 60e9, 6e9, 32e9};
   {  // cfg1: data/sample_graph.json on 2 x 4
     ComputationGraph g;
@@ -360,11 +360,15 @@ int main(int argc, char** argv) {
       check_case("random planning instance " + std::to_string(i), inst.graph, inst.topo, SolveCfg{i % 4 == 0});
     }
   }
-  {  // cfg3 (24 layers) with a fixed node budget, threads=1 (deterministic truncated search)
-    SolveCfg sc{true, 1, 200000};
-    check_case("cfg3 GPT-24 h2048 2x8", gpt_chain(24, 2048, 8, 512), {2, 8, 60e9, 6e9, 80e9}, sc);
-    check_case("cfg3 GPT-24 h2048 8x8 r100", gpt_chain(24, 2048, 8, 512), {8, 8, 60e9, 0.6e9, 80e9}, SolveCfg{});
-    if (big) check_case("cfg4 GPT-96 h12288 16x8", gpt_chain(96, 12288, 8, 2048), {16, 8, 60e9, 6e9, 80e9}, SolveCfg{});
+  {  // cfg3 (24 layers) on 2/4/8 x 8 and cfg4 (96 layers, 16 x 8) with a fixed node
+     // budget and threads=1: a deterministic truncated search, so the
+     // selections, objectives, `optimal` flags and LP texts must be identical
+    const ComputationGraph gpt24 = gpt_chain(24, 2048, 8, 512);
+    check_case("cfg3 GPT-24 h2048 2x8", gpt24, {2, 8, 60e9, 6e9, 80e9}, SolveCfg{true, 1, 200000});
+    check_case("cfg3 GPT-24 h2048 4x8", gpt24, {4, 8, 60e9, 6e9, 80e9}, SolveCfg{true, 1, 20000});
+    check_case("cfg3 GPT-24 h2048 8x8 r100", gpt24, {8, 8, 60e9, 0.6e9, 80e9}, SolveCfg{true, 1, 20000});
+    check_case("cfg4 GPT-96 h12288 16x8", gpt_chain(96, 12288, 8, 2048), {16, 8, 60e9, 6e9, 80e9},
+               SolveCfg{true, 1, 5000});
   }
   check_sweep(1000, big ? 10 : 40);
   std::printf("[PARITY] %s (%d failures)\n", failures ? "FAILED" : "ALL PASS", failures);

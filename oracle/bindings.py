@@ -89,6 +89,9 @@ def reference() -> C.CDLL:
                                   P(C.c_double), P(C.c_int32), P(C.c_int32), P(C.c_double),
                                   P(C.c_int64)]
         lib.ref_solve.restype = C.c_int
+        lib.ref_price_assignments.argtypes = [P(abi.tp_graph_desc), P(abi.tp_topology_desc), P(C.c_int32),
+                                              C.c_int, P(C.c_double), P(C.c_double), P(C.c_double)]
+        lib.ref_price_assignments.restype = C.c_int
         lib.ref_export_lp.argtypes = [P(abi.tp_graph_desc), P(abi.tp_topology_desc), C.c_int,
                                       C.c_double, C.c_char_p, C.c_int64]
         lib.ref_export_lp.restype = C.c_int64
@@ -293,6 +296,22 @@ def reference_solve(flat, topo, mode_volume=False, memory_bound=None, threads=1,
     return dict(strategy_per_op=per_op[: flat.num_ops].tolist(), objective=obj.value,
                 feasible=bool(feas.value), optimal=bool(opt.value), root_bound=root.value,
                 nodes=nodes.value)
+
+
+def reference_price_assignments(flat, topo, asg):
+    """The reference's price_assignment (aux_graph.hpp:326-348) of every row
+    of asg [k, num_ops] on its own build: (topology cost, volume cost,
+    memory) arrays of length k."""
+    asg = np.ascontiguousarray(asg, dtype=np.int32)
+    k = asg.shape[0]
+    d, t = flat.desc(), topo.desc()
+    c, v, m = (np.zeros(max(k, 1)) for _ in range(3))
+    st = reference().ref_price_assignments(C.byref(d), C.byref(t), abi.ptr(asg, C.c_int32), k,
+                                           abi.ptr(c, C.c_double), abi.ptr(v, C.c_double),
+                                           abi.ptr(m, C.c_double))
+    if st != 0:
+        raise RuntimeError(reference().ref_last_error().decode())
+    return c[:k], v[:k], m[:k]
 
 
 def reference_bench(flat, topo, iters=1, threads=1):

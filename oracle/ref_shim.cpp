@@ -457,6 +457,25 @@ int ref_solve(const tp_graph_desc* g, const tp_topology_desc* t, int mode_volume
   });
 }
 
+// price_assignment (aux_graph.hpp:326-348) of k assignments [k * num_ops]
+// on the reference's own build: the topology-mode cost, the volume-mode cost
+// and the memory sum of each (arrays of length k, any may be NULL).
+int ref_price_assignments(const tp_graph_desc* g, const tp_topology_desc* t, const int32_t* asg, int k,
+                          double* cost_s, double* volume_bytes, double* memory_bytes) {
+  return guarded([&] {
+    const AuxiliaryGraph aux = build_auxiliary_graph(to_graph(g), to_topo(t));
+    const std::size_t nops = aux.graph.operators.size();
+    for (int j = 0; j < k; ++j) {
+      const std::vector<int> a(asg + (std::size_t)j * nops, asg + (std::size_t)(j + 1) * nops);
+      const AssignmentPrice pt = price_assignment(aux, a, CostMode::kTopology);
+      const AssignmentPrice pv = price_assignment(aux, a, CostMode::kVolume);
+      if (cost_s) cost_s[j] = pt.cost;
+      if (volume_bytes) volume_bytes[j] = pv.cost;
+      if (memory_bytes) memory_bytes[j] = pt.memory_bytes;
+    }
+  });
+}
+
 // export_lp (solver.hpp:578) of the reference-built problem; returns the
 // length written (or needed).
 int64_t ref_export_lp(const tp_graph_desc* g, const tp_topology_desc* t, int mode_volume,

@@ -57,6 +57,21 @@ const char* kind_text(int kind) {
       return set_err(TP_ERR_CUDA, 0, std::string(#expr ": ") + cudaGetErrorString(_e));      \
   } while (0)
 
+// Every entry point that may switch the current device restores the caller's
+// on return (a PyTorch caller's current device must not follow the plan's).
+struct DeviceGuard {
+  int dev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+  }
+  ~DeviceGuard() {
+    int now = -1;
+    if (dev >= 0 && cudaGetDevice(&now) == cudaSuccess && now != dev) cudaSetDevice(dev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 // Error keys: (order << 6) | kind; the smallest key is the error the
 // reference would throw first (its iteration order). Node phase orders are
 // 1 + 2*node (+1 for derivation errors), edge phase orders start at 2^46.

@@ -97,6 +97,7 @@ tp_status tp_plan_create(const tp_graph_desc* graph, const tp_topology_desc* top
 }
 
 void tp_plan_destroy(tp_plan* p) {
+  DeviceGuard dg;
   if (!p) return;
   cudaSetDevice(p->device);
   if (p->d_terms) {
@@ -300,6 +301,7 @@ tp_status upload_tables(tp_plan* p, UploadPrep& U, cudaStream_t s) {
 extern "C" {
 
 tp_status tp_plan_upload(tp_plan* p, void* stream) {
+  DeviceGuard dg;
   if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
   tp_status st = ensure_stream(p);
   if (st) return st;
@@ -566,6 +568,7 @@ tp_status finish_execute(tp_plan* p, tp_cost_tensors* out, cudaStream_t s, const
 extern "C" {
 
 tp_status tp_plan_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors* out) {
+  DeviceGuard dg;
   if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
   tp_status st = ensure_stream(p);
   if (st) return st;
@@ -850,6 +853,7 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
 extern "C" {
 
 tp_status tp_plan_execute_batch(tp_plan* const* plans, int32_t n, tp_cost_tensors* device_outs, void* stream) {
+  DeviceGuard dg;
   return execute_batch_impl(plans, n, device_outs, stream, nullptr, nullptr);
 }
 
@@ -885,6 +889,7 @@ tp_status tp_plan_set_timeline(tp_plan* p, int32_t on) {
 }
 
 tp_status tp_plan_timeline(tp_plan* p, int64_t* ns_out) {
+  DeviceGuard dg;
   if (!p || !ns_out) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan or output");
   if (!p->arena || !p->arena->d_sched.p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "plan not executed");
   CUDA_TRY(cudaSetDevice(p->device));
@@ -901,6 +906,7 @@ tp_status tp_plan_timeline(tp_plan* p, int64_t* ns_out) {
 }
 
 tp_status tp_plan_timeline_detail(tp_plan* p, int32_t section, uint32_t* out, int64_t* count) {
+  DeviceGuard dg;
   if (!p || !count || section < 0 || section > 4) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "bad argument");
   if (section == 4) {  // phase-1 exit of every warp of the last launch (ns after kernel start)
     if (!p->timeline || !p->arena || !p->arena->d_prof.p)
@@ -963,6 +969,7 @@ tp_status tp_plan_timeline_detail(tp_plan* p, int32_t section, uint32_t* out, in
 }
 
 tp_status tp_plan_check_errors(tp_plan* p) {
+  DeviceGuard dg;
   if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
   CUDA_TRY(cudaSetDevice(p->device));
   unsigned long long dev = ~0ull;
@@ -983,6 +990,7 @@ tp_status tp_plan_check_errors(tp_plan* p) {
 
 tp_status tp_plan_execute_host(tp_plan* p, const tp_build_opts* opts, tp_aux_index* index_out,
                                tp_cost_tensors* host_out) {
+  DeviceGuard dg;
   if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
   tp_status st = ensure_stream(p);
   if (st) return st;
@@ -1055,6 +1063,7 @@ tp_status tp_plan_execute_host(tp_plan* p, const tp_build_opts* opts, tp_aux_ind
 tp_status tp_build_cost_tensors(const tp_graph_desc* graph, const tp_topology_desc* topo,
                                 const tp_build_opts* opts, tp_aux_index* index_out,
                                 tp_cost_tensors* host_out) {
+  DeviceGuard dg;
   tp_plan* p = nullptr;
   tp_status st = tp_plan_create(graph, topo, opts ? opts->device : -1, &p);
   if (st) return st;
@@ -1159,11 +1168,20 @@ extern "C" {
 // (as engine.Sweep allocates them), and every plan's error read by one copy.
 tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_index* index_outs,
                                      tp_cost_tensors* host_outs, int32_t host_threads, int32_t* status_out) {
+  DeviceGuard dg;
   if (n < 0 || (n > 0 && (!plans || !host_outs))) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null batch arrays");
   if (n == 0) return TP_OK;
   bool one_device = plans[0] != nullptr;
   for (int i = 0; one_device && i < n; ++i) one_device = plans[i] && plans[i]->device == plans[0]->device;
-  if (!one_device || plans[0]->device < 0 || plans[0]->device >= 64)
+  // the batched launch stages the six SoA tensors only: AuxEdge records and
+  // the solver minima go through one tp_plan_execute_host per plan
+  bool extra = false;
+  for (int i = 0; i < n; ++i) {
+    const tp_cost_tensors& h = host_outs[i];
+    extra |= h.aux_edge_records || h.row_min_cost_s || h.row_min_volume_bytes || h.edge_pair_min_cost_s ||
+             h.edge_pair_min_volume_bytes;
+  }
+  if (!one_device || extra || plans[0]->device < 0 || plans[0]->device >= 64)
     return execute_host_each(plans, n, index_outs, host_outs, host_threads, status_out);
   const int device = plans[0]->device;
   CUDA_TRY(cudaSetDevice(device));
@@ -1366,6 +1384,7 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
 
 tp_status tp_plan_price_assignments(tp_plan* p, const tp_cost_tensors* t, const int32_t* assignments, int32_t k,
                                     double* cost_s, double* volume_bytes, double* memory_bytes, void* stream) {
+  DeviceGuard dg;
   if (!p || !t || (k > 0 && !assignments)) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null argument");
   if (k < 0) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "negative assignment count");
   if (p->host_err != ~0ull) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "the plan's build has an error");

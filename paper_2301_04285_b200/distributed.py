@@ -129,10 +129,22 @@ def engine_compute(device: int):
 
     from . import engine as E
 
+    import numpy as np
+
     cache = {}
 
+    def content_key(flat, topo):
+        # by content, not identity: a topology mutated in place (another
+        # bandwidth) or a new FlatGraph at a recycled id() must not reuse a plan
+        if not hasattr(flat, "desc"):
+            from . import graph as G
+            flat = G.flatten(flat)
+        arrays = tuple(v.tobytes() for k, v in sorted(vars(flat).items()) if isinstance(v, np.ndarray))
+        return (arrays, flat.num_ops, flat.num_edges, topo.node_count, topo.local_device_num,
+                topo.intra_bandwidth, topo.inter_bandwidth, topo.device_memory), flat
+
     def compute(flat, topo, rng):
-        key = (id(flat), id(topo))
+        key, flat = content_key(flat, topo)
         if key not in cache:
             cache.clear()
             cache[key] = E.Plan(flat, topo, device=device)

@@ -381,8 +381,11 @@ class Sweep:
         _check(self.lib, self.lib.tp_plan_sizes(self.handles[i], C.byref(s)))
         return {k: getattr(s, k) for k, _ in abi.tp_plan_sizes_t._fields_}
 
-    def allocate(self, pinned: bool = True):
-        """Caller-owned outputs of every scenario (plans must exist)."""
+    def allocate(self, pinned: bool = True, records: bool = False, row_min: bool = False):
+        """Caller-owned outputs of every scenario (plans must exist). With
+        `records` / `row_min` every scenario also gets its AuxEdge records /
+        solver minima (cond_min rows and pair_min, both modes); the engine then
+        builds the scenarios one execute each instead of one batched launch."""
         n = len(self)
         nn = [self.sizes(i)["num_aux_nodes"] if self.handles[i] else 0 for i in range(n)]
         ne = [self.sizes(i)["num_aux_edges"] if self.handles[i] else 0 for i in range(n)]
@@ -406,6 +409,13 @@ class Sweep:
             views = {k: big[k][(node_off if k.startswith("node") else edge_off)[i]:
                                (node_off if k.startswith("node") else edge_off)[i + 1]] for k in _OUT_KEYS}
             ct = CostTensors(sizes=self.sizes(i) if self.handles[i] else {}, **ix, **views)
+            if self.handles[i] and records:
+                ct.records = np.zeros(max(ne[i], 1) * 40, np.uint8)
+            if self.handles[i] and row_min:
+                nr = self.sizes(i)["num_rows"]
+                ct.row_min_cost_s, ct.row_min_volume_bytes = np.zeros(max(nr, 1)), np.zeros(max(nr, 1))
+                ct.edge_pair_min_cost_s = np.zeros(max(f.num_edges, 1))
+                ct.edge_pair_min_volume_bytes = np.zeros(max(f.num_edges, 1))
             self.results.append(ct)
             self._cs[i] = cost_struct(ct) if ne[i] + nn[i] > 0 else abi.tp_cost_tensors()
             self._ix[i] = abi.tp_aux_index(*(abi.ptr(ix[k], C.c_int64 if ix[k].dtype == np.int64 else C.c_int32)

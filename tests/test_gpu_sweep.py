@@ -102,6 +102,31 @@ def test_sweep_mixes_owned_and_borrowed_arenas():
     sw.destroy()
 
 
+def test_host_batch_records_and_minima(sweep1000):
+    """tp_plan_execute_host_batch honours every tp_cost_tensors field: the
+    AuxEdge records and the solver minima (cond_min rows, pair_min) of every
+    scenario equal the oracle's, as tp_plan_execute_host gives them."""
+    scen = sweep1000[:24]
+    pairs = [(G.flatten(s.graph), s.topo) for s in scen]
+    sw = engine.Sweep(pairs, device=0, host_threads=4)
+    sw.create()
+    sw.allocate(pinned=False, records=True, row_min=True)
+    sw.execute()
+    for i, (f, t) in enumerate(pairs):
+        ref = B.oracle_build(f, t)
+        got = sw.results[i]
+        same(got, ref, f"scenario {i}")
+        for k in ("row_min_cost_s", "row_min_volume_bytes", "edge_pair_min_cost_s", "edge_pair_min_volume_bytes"):
+            n = len(getattr(ref, k))
+            assert np.array_equal(bits(getattr(got, k)[:n]), bits(getattr(ref, k))), (i, k)
+        ne = len(ref.edge_cost_s)
+        a, b = got.records[: ne * 40].reshape(-1, 40).copy(), ref.records.reshape(-1, 40).copy()
+        a[:, 12:16] = 0
+        b[:, 12:16] = 0
+        assert np.array_equal(a, b), i
+    sw.destroy()
+
+
 def test_device_sweep_batched_launch_matches_oracle(sweep1000):
     """The device-resident sweep: one persistent launch for all scenarios
     (tp_plan_execute_batch), repeated (the tables alternate parity), matches

@@ -108,3 +108,15 @@ def test_ilp_on_oracle_tensors_matches_reference():
         # the explored-node count depends on how the 4 solver threads interleave
         a.pop("nodes"), b.pop("nodes")
         assert a == b
+
+
+@pytest.mark.gpu
+def test_oracle_pinned_on_gpu_box():
+    """The same pinning, repeated in the GPU run (the box gets the prebuilt
+    oracle/_ref): configs, seeded random graphs and redistributions."""
+    for name in ("cfg1", "cfg2"):
+        test_configs(name)
+    test_cfg3_two_nodes()
+    test_random_graphs(0)
+    test_planning_instances()
+    test_redistributions()
