@@ -8,16 +8,30 @@ topoplan::build_auxiliary_graph, aux_graph.hpp:273-296), plus build ms.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4]
   python bench.py --impl reference ...      # the reference's own CPU build
 
-A step is one complete cost-tensor build of the workload (strategy tables,
-per-node costs, class tables, fan-out of every aux edge). `value` is timed on
-the device with inputs resident in HBM; `e2e` goes through the C-ABI one-shot
-call tp_build_cost_tensors with pinned host buffers (host analysis, H2D,
-kernels, D2H of all tensors) and is wall-clock timed.
+What is timed:
+  value  -- device time of complete rebuilds of an analysed, uploaded plan:
+            ONE launch of fused_kernel per step (node-class rows, class-table
+            pricing of every distinct (producer layout, consumer layout) pair,
+            fan-out of every aux edge and aux node into device memory). Not in
+            it: the host analysis (tp_plan_create), the descriptor H2D and the
+            per-plan set-up kernels (strategy tables, layout descriptors, pair
+            records), which `build_ms_device_full` adds (device-timed) and
+            `e2e` adds together with the host analysis and the D2H.
+  e2e    -- the reference-facing one-shot C-ABI call tp_build_cost_tensors:
+            host graph in, host analysis, H2D, kernels, D2H of every tensor into
+            pinned host memory; wall clock, warm (`e2e_cold_ms`: the first call
+            of the process for the workload, arenas not yet allocated).
+  configs -- the other BASELINE configurations (cfg1, cfg2, cfg3 on 2/4/8 x 8
+            with its seven intra/inter bandwidth ratios), each with device ms,
+            e2e and the reference's single-thread CPU build in the same run.
+  cfg5_sweep -- the 1,000-scenario sweep in one batched launch, with e2e and a
+            single-thread reference sample.
 
-Multi-GPU (torchrun, one process per GPU): weak scaling — every rank builds
+Multi-GPU (torchrun, one process per GPU): weak scaling -- every rank builds
 its own independent scenario (the workload graph under a rank-specific
 bandwidth ratio); no collective on the data path. Max over ranks of the
-device time; NCCL only carries that max.
+device time; NCCL only carries that max. `edge_sharded` (N>1): ONE cfg4 build
+split over the ranks' GPUs by edge ranges, timed the same way.
 """
 from __future__ import annotations
 
@@ -148,6 +162,208 @@ def cpu_baseline(flat, topo, aux_edges, repeats=3):
             "build_ms": best * 1e3,
             "sample": f"{repeats} single-thread builds of the full workload by the reference's "
                       f"build_auxiliary_graph (oracle/_ref, g++ -O2), best of {repeats}"}
+
+
+def host_info(device=0):
+    """CPU model / core counts of the box and the measured host-link
+    bandwidth (pinned, 256 MiB each way, CUDA events): the e2e export is bound
+    by the D2H, not by HBM."""
+    import torch
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    info = {"cpu_model": model, "nproc": os.cpu_count(),
+            "affinity_cores": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None}
+    n = 256 * 1024 * 1024
+    d = torch.empty(n, dtype=torch.uint8, device=torch.device("cuda", device))
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    s = torch.cuda.Stream(device)
+    for direction in ("d2h", "h2d"):
+        best = float("inf")
+        for _ in range(4):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s):
+                a.record(s)
+                (h.copy_(d, non_blocking=True) if direction == "d2h" else d.copy_(h, non_blocking=True))
+                b.record(s)
+            s.synchronize()
+            best = min(best, a.elapsed_time(b))
+        info[f"{direction}_gbs"] = n / (best / 1e3) / 1e9
+    del d, h
+    return info
+
+
+class _H:  # attribute view of host arrays for engine.cost_struct
+    pass
+
+
+def oneshot_outputs(ne, nn, pinned=True):
+    import torch
+    alloc = (lambda n: torch.empty(max(n, 1), dtype=torch.float64, pin_memory=True).numpy()) if pinned else \
+        (lambda n: np.empty(max(n, 1), np.float64))
+    hv = _H()
+    for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes"):
+        setattr(hv, k, alloc(ne))
+    for k in ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes"):
+        setattr(hv, k, alloc(nn))
+    hv.records = hv.row_min_cost_s = hv.row_min_volume_bytes = None
+    return hv
+
+
+def time_oneshot(lib, flat, topo, hs, device, steps):
+    """Wall ms of tp_build_cost_tensors calls (host graph in, pinned out): the
+    first call, then the best and the mean of `steps` warm calls."""
+    from paper_2301_04285_b200 import abi
+    gd, td = flat.desc(), topo.desc()
+    opts = abi.tp_build_opts(0, -1, 0, device, None)
+    ts = []
+    for _ in range(steps + 1):
+        t0 = time.perf_counter()
+        st = lib.tp_build_cost_tensors(C.byref(gd), C.byref(td), C.byref(opts), None, C.byref(hs))
+        ts.append((time.perf_counter() - t0) * 1e3)
+        assert st == 0, lib.tp_last_error()
+    return ts[0], min(ts[1:]), sum(ts[1:]) / steps
+
+
+def device_build_ms(plan, stream, outs_struct, K, W, flush, full=False):
+    """Event-timed device ms per build on `stream`: the fused launch of an
+    uploaded plan, or with full=True upload (descriptor H2D + set-up kernels)
+    plus the launch (tp_plan_set_bandwidth forces the re-upload)."""
+    import torch
+    sp = stream.cuda_stream
+    ts = []
+    with torch.cuda.stream(stream):
+        for i in range(W + K):
+            flush.zero_()
+            if full:
+                plan.set_bandwidth(plan.topo.intra_bandwidth, plan.topo.inter_bandwidth)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            plan.execute(outs_struct, stream=sp)
+            b.record(stream)
+            if i >= W:
+                ts.append((a, b))
+    torch.cuda.synchronize()
+    plan.check_errors()
+    return statistics.median(x.elapsed_time(y) for x, y in ts)
+
+
+def measure_config(name, flat, topo, device, K=20, W=3, cpu_repeats=3, flush=None, lib=None):
+    """One BASELINE configuration: device build ms (kernel; full with
+    uploads), e2e through the one-shot C-ABI (cold and warm) and the
+    reference's single-thread build of the same graph in the same run."""
+    import torch
+    from paper_2301_04285_b200 import engine as E
+    from oracle import bindings as B
+    plan = E.Plan(flat, topo, device=device)
+    ne, nn = plan.sizes["num_aux_edges"], plan.sizes["num_aux_nodes"]
+    dev = torch.device("cuda", device)
+    outs = {k: torch.empty(max(ne, 1), dtype=torch.float64, device=dev)
+            for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes")}
+    outs.update({k: torch.empty(max(nn, 1), dtype=torch.float64, device=dev)
+                 for k in ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes")})
+    cs = E.device_cost_struct(outs)
+    stream = torch.cuda.Stream(device)
+    plan.upload(stream.cuda_stream)
+    kern = device_build_ms(plan, stream, cs, K, W, flush)
+    full = device_build_ms(plan, stream, cs, K, W, flush, full=True)
+    hv = oneshot_outputs(ne, nn)
+    cold, warm, mean = time_oneshot(lib or plan.lib, flat, topo, E.cost_struct(hv), device, max(3, K // 2))
+    out = {"aux_edges": ne, "aux_nodes": nn, "edge_classes": plan.sizes["num_signatures"],
+           "class_pairs": plan.sizes["num_pair_evals"],
+           "build_ms_device": kern, "evals_per_s_device": ne / (kern / 1e3),
+           "build_ms_device_full": full,
+           "e2e": {"build_ms": mean, "build_ms_best": warm, "build_ms_cold": cold,
+                   "evals_per_s": ne / (mean / 1e3), "h2d_bytes": int(plan.sizes["h2d_bytes"]),
+                   "d2h_bytes": BYTES_PER_EVAL * (ne + nn)}}
+    if B.have_reference():
+        best = min(B.reference_bench(flat, topo, iters=1, threads=1)[0] for _ in range(cpu_repeats))
+        out["cpu_baseline"] = {"build_ms": best * 1e3, "evals_per_s": ne / best, "cores": 1, "kind": "reference",
+                               "sample": f"full build, best of {cpu_repeats}"}
+        out["speedup_e2e_vs_cpu"] = best * 1e3 / mean
+    del plan
+    return out
+
+
+def measure_configs(device, K, W, flush, lib):
+    """cfg1, cfg2 and cfg3 (2/4/8 x 8, its seven intra/inter bandwidth ratios)
+    of BASELINE.json, SURVEY §8d."""
+    from paper_2301_04285_b200 import engine as E, graph as G, models as M
+    from oracle import bindings as B
+    res = {}
+    for name in ("cfg1", "cfg2"):
+        g, t = getattr(M, name)()
+        res[name] = measure_config(name, G.flatten(g), t, device, K, W, flush=flush, lib=lib)
+        res[name]["desc"] = workload(name)[2]
+    import torch
+    ratios = (1, 2, 5, 10, 20, 50, 100)
+    flat = G.flatten(M.build_gpt_chain(24, 2048, 8, 512))
+    for nodes in (2, 4, 8):
+        key = f"cfg3_{nodes}x8"
+        r = measure_config(key, flat, M.ClusterTopology(nodes, 8, 60e9, 6e9, 80e9), device, K, W, flush=flush,
+                           lib=lib)
+        r["desc"] = f"GPT-24 hidden 2048 batch 8 seq 512 on {nodes}x8, intra/inter 10"
+        # the ratio sweep: one analysed plan re-priced per ratio (tp_plan_set_bandwidth)
+        plan = E.Plan(flat, M.ClusterTopology(nodes, 8, 60e9, 6e9, 80e9), device=device)
+        ne = plan.sizes["num_aux_edges"]
+        nn = plan.sizes["num_aux_nodes"]
+        stream = torch.cuda.Stream(device)
+        dev = torch.device("cuda", device)
+        outs = {k: torch.empty(max(ne, 1), dtype=torch.float64, device=dev)
+                for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes")}
+        outs.update({k: torch.empty(max(nn, 1), dtype=torch.float64, device=dev)
+                     for k in ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes")})
+        cs = E.device_cost_struct(outs)
+        evs = []
+        with torch.cuda.stream(stream):
+            for rep in range(2):  # the first pass is warm-up
+                for q in ratios:
+                    flush.zero_()
+                    plan.set_bandwidth(60e9, 60e9 / q)
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    plan.execute(cs, stream=stream.cuda_stream)
+                    b.record(stream)
+                    if rep:
+                        evs.append((a, b))
+        torch.cuda.synchronize()
+        plan.check_errors()
+        dev_ms = sum(a.elapsed_time(b) for a, b in evs)
+        # e2e of the sweep: seven re-priced builds into pinned host memory
+        hv = oneshot_outputs(ne, nn)
+        hs = E.cost_struct(hv)
+        from paper_2301_04285_b200 import abi
+        o = abi.tp_build_opts(0, -1, 0, device, None)
+        best_e2e = float("inf")
+        for rep in range(3):
+            t0 = time.perf_counter()
+            for q in ratios:
+                plan.set_bandwidth(60e9, 60e9 / q)
+                st = plan.lib.tp_plan_execute_host(plan.handle, C.byref(o), None, C.byref(hs))
+                assert st == 0, plan.lib.tp_last_error()
+            best_e2e = min(best_e2e, (time.perf_counter() - t0) * 1e3)
+        sweep = {"ratios": list(ratios), "builds": len(ratios), "aux_edges_total": ne * len(ratios),
+                 "build_ms_device_total": dev_ms, "evals_per_s_device": ne * len(ratios) / (dev_ms / 1e3),
+                 "e2e": {"build_ms_total": best_e2e, "evals_per_s": ne * len(ratios) / (best_e2e / 1e3),
+                         "how": "tp_plan_set_bandwidth + tp_plan_execute_host per ratio (pinned host out)"}}
+        if B.have_reference():
+            cpu = 0.0
+            for q in ratios:
+                cpu += B.reference_bench(flat, M.ClusterTopology(nodes, 8, 60e9, 60e9 / q, 80e9), 1, 1)[0]
+            sweep["cpu_baseline"] = {"build_ms_total": cpu * 1e3, "evals_per_s": ne * len(ratios) / cpu,
+                                     "cores": 1, "kind": "reference",
+                                     "sample": "one single-thread build per ratio"}
+            sweep["speedup_e2e_vs_cpu"] = cpu * 1e3 / best_e2e
+        r["ratio_sweep"] = sweep
+        res[key] = r
+        del plan
+    return res
 
 
 def run_reference(args):
@@ -444,8 +660,6 @@ def run_engine(args):
     host.update({k: torch.empty(max(nn, 1), dtype=torch.float64, pin_memory=True).numpy()
                  for k in ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes")})
 
-    class _H:  # attribute view for cost_struct
-        pass
     hv = _H()
     for k, v in host.items():
         setattr(hv, k, v)
@@ -454,8 +668,12 @@ def run_engine(args):
     gd, td = flat.desc(), t.desc()
     opts = E.abi.tp_build_opts(0, -1, 0, local, None)
     KE = max(3, min(K, args.e2e_steps))
-    for _ in range(2):
+    e2e_cold = None
+    for i in range(2):  # the first call of the process: arenas and staging not yet allocated
+        t0 = time.perf_counter()
         st = lib.tp_build_cost_tensors(C.byref(gd), C.byref(td), C.byref(opts), None, C.byref(hs))
+        if i == 0:
+            e2e_cold = (time.perf_counter() - t0) * 1e3
         assert st == 0, lib.tp_last_error()
     if dist:
         dist.barrier()
@@ -478,18 +696,30 @@ def run_engine(args):
             plan.execute(cs, stream=sp)
             stream.synchronize()
     clk = clocks.stop()
+    # the whole device build of the plan: descriptor H2D + set-up kernels + the launch
+    full_ms = device_build_ms(plan, stream, cs, min(K, 10), 2, flush, full=True)
 
     # the cfg5 sweep alongside (BASELINE config 5): all ranks take part
     sweep = None
     if not args.no_sweep:
         try:
-            sl = measure_sweep(args, rank, world, local, dist, min(K, 10), W, with_cpu=False)
+            sl = measure_sweep(args, rank, world, local, dist, min(K, 10), W,
+                               with_cpu=world == 1 and not args.no_cpu_baseline)
             if sl is not None:
                 sweep = {k: sl[k] for k in ("value", "unit", "ms_per_step", "scaling")}
                 sweep.update(config=sl["config"], e2e=sl["e2e"], roofline=sl["roofline"],
-                             gpu_launches=sl["gpu_launches"])
+                             gpu_launches=sl["gpu_launches"], cpu_baseline=sl.get("cpu_baseline"))
         except Exception as ex:  # the headline line must still be printed
             sweep = {"error": f"{type(ex).__name__}: {ex}"}
+
+    # the other BASELINE configurations, one GPU (rank 0 of a 1-GPU run)
+    configs = None
+    if world == 1 and not args.no_configs:
+        try:
+            configs = measure_configs(local, min(K, 20), 3, flush, lib)
+        except Exception as ex:
+            configs = {"error": f"{type(ex).__name__}: {ex}"}
+    hinfo = host_info(local) if rank == 0 else None
 
     if rank != 0:
         if dist:
@@ -511,7 +741,8 @@ def run_engine(args):
                    "edge_classes": sizes["num_signatures"], "class_pairs": sizes["num_pair_evals"],
                    "parallelism": f"scenario-sharded x{world}",
                    "l2": "256 MiB buffer written between timed steps (flush)",
-                   "build_ms_device": total_ms / K, "build_ms_e2e": sum(e2e_t) / KE * 1e3},
+                   "build_ms_device": total_ms / K, "build_ms_device_full": full_ms,
+                   "build_ms_e2e": sum(e2e_t) / KE * 1e3, "e2e_cold_ms": e2e_cold},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note,
                      "kernel": "fused_kernel<true> (node rows + class pairs + fan-out, one launch)",
@@ -523,7 +754,9 @@ def run_engine(args):
                 "how": "tp_build_cost_tensors (host graph in, pinned host tensors out), wall clock"},
         "gpu_launches": int(launches * K),
         "clocks": clk,
+        "host": hinfo,
         "cfg5_sweep": sweep,
+        "configs": configs,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(flat, t, ne)
@@ -545,6 +778,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the cfg5 sweep block of the cfg4 line")
+    ap.add_argument("--no-configs", action="store_true", help="skip the cfg1/cfg2/cfg3 blocks of the cfg4 line")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

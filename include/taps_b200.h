@@ -192,6 +192,20 @@ tp_status tp_build_cost_tensors(const tp_graph_desc* graph,
                                 tp_aux_index* index_out,
                                 tp_cost_tensors* host_out);
 
+/* Single-process multi-GPU form of the one-shot call: the
+ * graph's edges are cut into contiguous ranges balanced by their aux-edge
+ * counts sum |Su| x |Sw|; devices[i] builds range i (devices[0] also the
+ * per-node tensors) and copies its slice [edge_base[e0], edge_base[e1]) of
+ * every requested edge tensor -- SoA, AuxEdge records, row / pair minima --
+ * straight into host_out at that offset (aux_graph.hpp:93-98, 273-296). No
+ * collective: the ranges are independent. Results equal tp_build_cost_tensors
+ * bit for bit; errors are the reference's first (the smallest over devices). */
+tp_status tp_build_cost_tensors_multi(const tp_graph_desc* graph,
+                                      const tp_topology_desc* topo,
+                                      const int32_t* devices, int32_t num_devices,
+                                      tp_aux_index* index_out,
+                                      tp_cost_tensors* host_out);
+
 /* --- split API: analyse once, execute on device-resident buffers --------- */
 
 tp_status tp_plan_create(const tp_graph_desc* graph,
@@ -210,6 +224,10 @@ tp_status tp_plan_execute(tp_plan* plan, const tp_build_opts* opts,
  * (the one-shot call on an existing plan; synchronous). */
 tp_status tp_plan_execute_host(tp_plan* plan, const tp_build_opts* opts,
                                tp_aux_index* index_out, tp_cost_tensors* host_out);
+/* tp_build_cost_tensors_multi on an analysed plan: per-device copies of the
+ * plan (arenas, uploads) are kept on it for repeated executes. */
+tp_status tp_plan_execute_host_multi(tp_plan* plan, const int32_t* devices, int32_t num_devices,
+                                     tp_aux_index* index_out, tp_cost_tensors* host_out);
 /* Re-price an analysed plan under other intra/inter bandwidths (a sweep over
  * the intra/inter ratio, cfg3): nothing of the host analysis depends on them,
  * so the next execute uploads the new pricing tables and rebuilds. Results
@@ -282,6 +300,9 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n,
  * tp_plan_check_errors(plans[i]). */
 tp_status tp_plan_execute_batch(tp_plan* const* plans, int32_t n,
                                 tp_cost_tensors* device_outs, void* stream);
+/* Kernel launches of the last batched execute on `device` (the inference
+ * pass and the build launches of all its plans together). */
+int64_t tp_batch_last_launches(int32_t device);
 
 /* price_assignment (aux_graph.hpp:326-348) of k strategy assignments on the
  * device, both cost modes at once: assignments [k * num_ops] (the strategy
@@ -295,6 +316,15 @@ tp_status tp_plan_price_assignments(tp_plan* plan, const tp_cost_tensors* t,
                                     const int32_t* assignments, int32_t k,
                                     double* cost_s, double* volume_bytes,
                                     double* memory_bytes, void* stream);
+
+/* The reference's ILP of this build as CPLEX LP text, written to `path`:
+ * byte-identical to topoplan::export_lp(topoplan::formulate(aux, mode,
+ * device_memory)) (solver.hpp:69-176, 578-600; mode_volume selects
+ * CostMode::kVolume), produced straight from the plan's index and the six HOST
+ * cost tensors of tp_plan_execute_host (include/taps_b200/lp_export.hpp),
+ * without materialising the problem. *bytes_out (optional) = bytes written. */
+tp_status tp_plan_export_lp(const tp_plan* plan, const tp_cost_tensors* host_tensors, int32_t mode_volume,
+                            double device_memory, const char* path, int64_t* bytes_out);
 
 /* Strategy table of an operator with p axes on N devices, in the reference's
  * enumeration order (layout.hpp:270-328), produced on the device.

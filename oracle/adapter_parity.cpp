@@ -20,7 +20,9 @@
 #include "topoplan/models.hpp"
 #include "topoplan/solver.hpp"
 #include "test_support.hpp"  // the reference's test oracles, -I$(REF_TESTS) (see Makefile)
+#include "topoplan/io.hpp"  // aux_graph_to_json (needs nlohmann/json.hpp, -I in oracle/Makefile)
 #include "taps_b200/aux_graph_b200.hpp"
+#include "taps_b200/export_b200.hpp"
 #include "taps_b200/solver_b200.hpp"
 
 using namespace topoplan;
@@ -80,20 +82,29 @@ struct SolveCfg {
   std::int64_t max_nodes = 200'000'000;
 };
 
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
 void check_case(const std::string& name, const ComputationGraph& graph, const ClusterTopology& topo,
                 SolveCfg sc = {}) {
   AuxiliaryGraph ref, gpu;
   taps_b200::SolverMinima minima;
   std::string ref_err, gpu_err;
+  double t_build_ref = 0, t_build_b200 = 0;
   try {
+    const auto t0 = std::chrono::steady_clock::now();
     ref = build_auxiliary_graph(graph, topo);
+    t_build_ref = ms_since(t0);
   } catch (const Error& e) {
     ref_err = "Error";
   } catch (const std::out_of_range& e) {
     ref_err = "out_of_range";
   }
   try {
+    const auto t0 = std::chrono::steady_clock::now();
     gpu = taps_b200::build_auxiliary_graph_b200(graph, topo, CostMode::kTopology, -1, true, &minima);
+    t_build_b200 = ms_since(t0);
   } catch (const Error& e) {
     gpu_err = "Error";
   } catch (const std::out_of_range& e) {
@@ -160,10 +171,42 @@ void check_case(const std::string& name, const ComputationGraph& graph, const Cl
     }
     if (!ok) err = std::string("formulate_b200 differs (") + to_string(mode) + ")";
   }
+  // the wire formats of the GPU-built graph (export_b200.hpp) against the
+  // reference's on its own graph: export_lp of both modes; the JSON dump
+  // (below ~0.4M aux edges: nlohmann's tree of a cfg4 graph takes many GB)
+  double t_lp_ref = 0, t_lp_b200 = 0, t_js_ref = 0, t_js_b200 = 0;
+  for (CostMode mode : {CostMode::kTopology, CostMode::kVolume}) {
+    if (!err.empty()) break;
+    auto t0 = std::chrono::steady_clock::now();
+    const std::string a = export_lp(formulate(ref, mode, topo.device_memory));
+    t_lp_ref += ms_since(t0);
+    t0 = std::chrono::steady_clock::now();
+    const std::string b = taps_b200::export_lp_b200(gpu, mode, topo.device_memory);
+    t_lp_b200 += ms_since(t0);
+    if (a != b) err = std::string("export_lp_b200 differs (") + to_string(mode) + ")";
+  }
+  if (err.empty() && gpu.edges.size() <= 400000) {
+    auto t0 = std::chrono::steady_clock::now();
+    const std::string a = aux_graph_to_json(ref).dump();
+    t_js_ref = ms_since(t0);
+    t0 = std::chrono::steady_clock::now();
+    const std::string b = taps_b200::aux_graph_to_json_b200(gpu);
+    t_js_b200 = ms_since(t0);
+    if (a != b) err = "aux_graph_to_json_b200 differs";
+  } else if (err.empty()) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const std::string b = taps_b200::aux_graph_to_json_b200(gpu);
+    t_js_b200 = ms_since(t0);
+    std::printf("[PARITY]   %s: aux_graph_to_json_b200 %.1f ms, %.1f MB (reference dump not built at this size)\n",
+                name.c_str(), t_js_b200, b.size() / 1e6);
+  }
   std::string extra = std::to_string(gpu.edges.size()) + " aux edges bit-identical";
   if (gpu.edges.size() >= 100000) {
-    char buf[128];
-    std::snprintf(buf, sizeof(buf), "; formulate x2 modes %.1f ms, formulate_b200 %.1f ms", t_ref_ms, t_b200_ms);
+    char buf[400];
+    std::snprintf(buf, sizeof(buf),
+                  "; build_auxiliary_graph %.1f ms vs build_auxiliary_graph_b200 %.1f ms; formulate x2 modes %.1f ms, "
+                  "formulate_b200 %.1f ms; export_lp x2 %.1f ms vs export_lp_b200 %.1f ms; json %.1f vs %.1f ms",
+                  t_build_ref, t_build_b200, t_ref_ms, t_b200_ms, t_lp_ref, t_lp_b200, t_js_ref, t_js_b200);
     extra += buf;
   }
   if (err.empty() && sc.solve) {

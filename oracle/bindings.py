@@ -314,6 +314,19 @@ def reference_price_assignments(flat, topo, asg):
     return c[:k], v[:k], m[:k]
 
 
+def reference_export_lp(flat, topo, mode_volume=False, memory_bound=None) -> bytes:
+    """export_lp(formulate(...)) (solver.hpp:578-600) of the reference's own
+    build, as bytes."""
+    d, t = flat.desc(), topo.desc()
+    mem = topo.device_memory if memory_bound is None else memory_bound
+    n = reference().ref_export_lp(C.byref(d), C.byref(t), int(mode_volume), mem, None, 0)
+    if n < 0:
+        raise RuntimeError(reference().ref_last_error().decode())
+    buf = C.create_string_buffer(n + 1)
+    reference().ref_export_lp(C.byref(d), C.byref(t), int(mode_volume), mem, buf, n + 1)
+    return buf.raw[:n]
+
+
 def reference_bench(flat, topo, iters=1, threads=1):
     d, t = flat.desc(), topo.desc()
     secs, edges = C.c_double(), C.c_int64()

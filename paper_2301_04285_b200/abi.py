@@ -252,6 +252,16 @@ def load_engine() -> C.CDLL:
     lib.tp_plan_price_assignments.argtypes = [C.c_void_p, P(tp_cost_tensors), _p_i32, C.c_int32, P(C.c_double),
                                               P(C.c_double), P(C.c_double), C.c_void_p]
     lib.tp_plan_price_assignments.restype = C.c_int
+    lib.tp_plan_export_lp.argtypes = [C.c_void_p, P(tp_cost_tensors), C.c_int32, C.c_double, C.c_char_p,
+                                      P(C.c_int64)]
+    lib.tp_plan_export_lp.restype = C.c_int
+    lib.tp_batch_last_launches.argtypes = [C.c_int32]
+    lib.tp_batch_last_launches.restype = C.c_int64
+    lib.tp_build_cost_tensors_multi.argtypes = [P(tp_graph_desc), P(tp_topology_desc), _p_i32, C.c_int32,
+                                                P(tp_aux_index), P(tp_cost_tensors)]
+    lib.tp_build_cost_tensors_multi.restype = C.c_int
+    lib.tp_plan_execute_host_multi.argtypes = [C.c_void_p, _p_i32, C.c_int32, P(tp_aux_index), P(tp_cost_tensors)]
+    lib.tp_plan_execute_host_multi.restype = C.c_int
     lib.tp_plan_set_bandwidth.argtypes = [C.c_void_p, C.c_double, C.c_double]
     lib.tp_plan_set_bandwidth.restype = C.c_int
     lib.tp_last_error.argtypes = []
@@ -273,6 +283,8 @@ EXPORTED_SYMBOLS = (
     "tp_plan_last_launches", "tp_plan_set_profile_events", "tp_plan_set_timeline", "tp_plan_timeline", "tp_plan_timeline_detail", "tp_enumerate_strategies", "tp_redistribute_batch",
     "tp_redistribute_batch_form", "tp_plan_set_pair_form", "tp_plan_create_batch", "tp_plan_execute_host_batch",
     "tp_plan_execute_batch", "tp_plan_price_assignments", "tp_plan_set_bandwidth",
+    "tp_build_cost_tensors_multi", "tp_plan_execute_host_multi", "tp_batch_last_launches",
+    "tp_plan_export_lp",
     "tp_last_error", "tp_last_error_kind", "tp_abi_version",
 )
 

@@ -138,6 +138,12 @@ struct FanSeg {
   int32_t e, Sw, Wn, uid_u, uid_w, ident;
   int32_t st_q, st_r;  // a thread's stride (kFusedThreads ids) in (su, sw)
   int32_t base, need;  // table owner and its entry count (pairs_done target)
+  // batches priced in the fan-out (op lists): the base class's bytes and
+  // whether they come per entry from the overrides; the op lists of the base
+  // class start at opb (filled in shared memory by the kernel)
+  double bytes;
+  int32_t ovr, pad;
+  int64_t opb;
 };
 
 struct EdgeDesc {

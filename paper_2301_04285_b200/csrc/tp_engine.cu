@@ -52,6 +52,7 @@
 #include <thread>
 
 #include "../../include/taps_b200.h"
+#include "../../include/taps_b200/lp_export.hpp"
 #include "tp_core.cuh"
 #include "tp_fast.cuh"
 #include "tp_warp.cuh"
@@ -99,6 +100,7 @@ tp_status tp_plan_create(const tp_graph_desc* graph, const tp_topology_desc* top
 void tp_plan_destroy(tp_plan* p) {
   DeviceGuard dg;
   if (!p) return;
+  for (tp_plan* q : p->shards) tp_plan_destroy(q);
   cudaSetDevice(p->device);
   if (p->d_terms) {
     p->d_terms->release();
@@ -161,10 +163,13 @@ tp_status resident_of(tp_plan* p) {
 
 // Phase 2: the aux nodes and the edge range's aux edges cut into equal
 // ranges, one per resident CTA.
+// A batch sets min_len (batch_range_len): its ranges are cut for the batch
+// as a whole, not per plan -- a small plan is one range, not dozens of
+// 256-id ones whose staging and barriers would cost more than their stores.
 void range_layout(const tp_plan* p, int64_t total_out, int64_t total_nodes, int64_t& range_len, int64_t& exp_items,
-                  int64_t& nfan_items) {
+                  int64_t& nfan_items, int64_t min_len = kFusedThreads * kFanPer) {
   const int64_t nranges = std::max(1, p->resident_blocks - 2);  // the two ceilings below add at most 2
-  range_len = std::max<int64_t>(kFusedThreads * kFanPer, (total_out + total_nodes + nranges - 1) / nranges);
+  range_len = std::max<int64_t>(min_len, (total_out + total_nodes + nranges - 1) / nranges);
   exp_items = (total_out + range_len - 1) / range_len;
   nfan_items = (total_nodes + range_len - 1) / range_len;
 }
@@ -204,8 +209,9 @@ struct UploadPrep {
   std::array<int64_t, 4> def_key{{-1, -1, -1, -1}};
 };
 
-// Host only: the descriptor pieces of the plan (and its default range table).
-tp_status upload_prepare(tp_plan* p, UploadPrep& U) {
+// Host only: the descriptor pieces of the plan (and its default range table;
+// min_len: a batch's range length, batch_range_len).
+tp_status upload_prepare(tp_plan* p, UploadPrep& U, int64_t min_len = kFusedThreads * kFanPer) {
   Arena& A = *p->arena;
   // strategy tables: a pure function of (p, N), cached on the arena
   for (auto& td : p->tabs) U.key.push_back({td.offset, td.count, td.p, td.n});
@@ -240,7 +246,7 @@ tp_status upload_prepare(tp_plan* p, UploadPrep& U) {
     const int64_t total_out =
         (edge_phase && p->edge_base[e1] > p->edge_base[0]) ? p->edge_base[e1] - p->edge_base[0] : 0;
     int64_t rl, ei, ni;
-    range_layout(p, total_out, p->num_aux_nodes, rl, ei, ni);
+    range_layout(p, total_out, p->num_aux_nodes, rl, ei, ni, min_len);
     fill_range_first(p, 0, e1, rl, ei, ni);
     U.def_key = {{0, e1, rl, ni}};
     pk.add(A.d_rfirst, p->range_first);
@@ -364,7 +370,13 @@ struct ExecPrep {
   int64_t units = 0, items = 0;
 };
 
-tp_status prepare_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors* out, cudaStream_t s, ExecPrep& X) {
+// batch_mode: 0 = a plan on its own (or in a batch with class tables
+// published inside one launch); 4 = priced in the fan-out from op lists
+// (units = node rows); 5 = tables priced from op lists in a launch of their
+// own. Modes 4 and 5 never rely on unset-filled tables.
+tp_status prepare_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors* out, cudaStream_t s, ExecPrep& X,
+                          int batch_mode = 0, int64_t min_len = kFusedThreads * kFanPer) {
+  const bool direct = batch_mode == 4;
   Arena& A = *p->arena;
   p->last_stream = s;
   int32_t e0 = opts ? opts->edge_begin : 0;
@@ -385,7 +397,12 @@ tp_status prepare_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
     fill_kernel<<<64, 256, 0, s>>>((double*)A.d_tables2.p, 2 * tables_len(p), kUnset);  // both parities
     CUDA_TRY(cudaGetLastError());
     A.sched_clean = true;
+    A.tables_dirty = false;
     A.parity = 0;
+  } else if (A.tables_dirty && batch_mode == 0) {  // the last launch left the tables un-reset
+    fill_kernel<<<64, 256, 0, s>>>((double*)A.d_tables2.p, 2 * tables_len(p), kUnset);
+    CUDA_TRY(cudaGetLastError());
+    A.tables_dirty = false;
   }
   p->last_parity = -1;
   if (p->timeline || A.timeline_set) {
@@ -411,7 +428,7 @@ tp_status prepare_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   const int64_t total_out = edges_out ? p->edge_base[e1] - out_offset : 0;
   const int64_t total_nodes = nodes_out ? p->num_aux_nodes : 0;
   int64_t range_len, exp_items, nfan_items;
-  range_layout(p, total_out, total_nodes, range_len, exp_items, nfan_items);
+  range_layout(p, total_out, total_nodes, range_len, exp_items, nfan_items, min_len);
   const std::array<int64_t, 4> rkey{{e0, e1, range_len, nfan_items}};
   if (p->range_key != rkey) {  // first edge / operator of every range (cached)
     fill_range_first(p, e0, e1, range_len, exp_items, nfan_items);
@@ -500,7 +517,9 @@ tp_status prepare_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
 
   // phase-1 units: node rows, then class pairs (warp form) or 32-pair chunks;
   // phase-2 items: node ranges, then edge ranges
-  const int64_t units = p->total_rows + (a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32);
+  a.direct = direct;
+  const int64_t units =
+      p->total_rows + (direct ? 0 : (a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32));
   const int64_t total_items = exp_items + nfan_items;
   if (total_items >= (1ll << 30) || units >= (1ll << 30))
     return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many work items");
@@ -608,7 +627,8 @@ namespace {
 struct BatchCtx {
   std::mutex mu;
   std::mutex host_mu;  // the one-shot host batch: output staging below
-  DevBuf d_args, d_hdr, d_err;
+  DevBuf d_args, d_hdr, d_err, d_ops;
+  int64_t last_launches = 0;  // kernel launches of the last batched execute
   DevBuf out[6];
   unsigned long long* h_err = nullptr;
   size_t h_err_cap = 0;
@@ -661,6 +681,75 @@ bool same_structure(const tp_plan* a, const tp_plan* b) {
          same_vec(a->overrides, b->overrides);
 }
 
+// Per edge class of a plan (base classes only): everything its class-table
+// entries' op lists depend on -- both sides' strategy tables (p, log2 N) and
+// slicings, the dims (2-adic valuation, odd part), the table shape and the
+// layout dedup mode -- but not the bytes or bandwidths. Equal keys (any plans)
+// have identical op lists entry by entry. Cached on the plan.
+const std::vector<std::pair<uint64_t, std::vector<int64_t>>>& class_keys(tp_plan* p) {
+  if (p->class_keys.size() == p->sigs.size()) return p->class_keys;
+  p->class_keys.assign(p->sigs.size(), {});
+  auto pn = [&](int32_t tab) -> int64_t {
+    for (const auto& t : p->tabs)
+      if (t.offset == tab) return ((int64_t)t.p << 8) | t.n;
+    return -1;
+  };
+  for (size_t c = 0; c < p->sigs.size(); ++c) {
+    const SigDesc& sd = p->sigs[c];
+    if (sd.base != (int32_t)c) continue;
+    std::vector<int64_t> k{sd.R, pn(sd.tab_u), pn(sd.tab_w), sd.Un, sd.Wn, (int64_t)p->overrides.empty()};
+    for (int d = 0; d < sd.R; ++d) k.insert(k.end(), {sd.sa_u[d], sd.sa_w[d], sd.dt[d].t, sd.dt[d].odd});
+    p->class_keys[c] = {hash_words(0x6a09e667f3bcc909ull, k.data(), k.size() * sizeof(int64_t)), std::move(k)};
+  }
+  return p->class_keys;
+}
+
+// A big batch (thread form) is priced in the fan-out from op lists: every
+// class key of the batch inferred once (infer_kernel), each aux edge priced
+// from its entry's op list with its own plan's bytes and bandwidths -- no
+// class tables and no pair records. Needs every plan's edge tensors written
+// (errors are found where they are written) and no row minima (they read the
+// tables); TP_BATCH_OPLISTS=0 keeps the class tables (and bandwidth groups).
+// Range length of a batch's fan-out: about four ranges per resident CTA over
+// the whole batch (aux edges and nodes of every plan), at least the
+// single-plan minimum.
+int64_t batch_range_len(tp_plan* const* plans, int32_t n) {
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i)
+    if (plans[i]) total += plans[i]->num_aux_edges + plans[i]->num_aux_nodes;
+  int resident = 0;
+  if (n > 0 && plans[0]) {
+    if (plans[0]->resident_blocks == 0) resident_of(plans[0]);
+    resident = plans[0]->resident_blocks;
+  }
+  const int64_t want = total / std::max<int64_t>(1, 4 * (int64_t)std::max(resident, 1));
+  const int64_t unit = kFusedThreads * kFanPer;
+  return std::max<int64_t>(unit, std::min<int64_t>(32768, (want + unit - 1) / unit * unit));
+}
+
+// Returns the batch mode (prepare_execute): 0 = class tables published in
+// one launch; 4 = priced in the fan-out; 5 = tables from op lists, two launches.
+// TP_BATCH_MODE = 0 / 4 / 5 forces one (A/B); the default is 5.
+int batch_mode_of(tp_plan* const* plans, int32_t n, const tp_cost_tensors* outs) {
+  static const int forced = getenv("TP_BATCH_MODE") ? atoi(getenv("TP_BATCH_MODE")) : -1;
+  const int want = forced >= 0 ? forced : 5;
+  int64_t batch_pairs = 0;
+  for (int i = 0; i < n; ++i) batch_pairs += plans[i]->total_pairs;
+  if (want == 0 || batch_pairs <= kWarpPairLimit) return 0;
+  for (int i = 0; i < n; ++i) {
+    const tp_cost_tensors& o = outs[i];
+    if (plans[i]->pair_form == 1) return 0;
+    if (want == 4) {
+      if (o.row_min_cost_s || o.row_min_volume_bytes || o.edge_pair_min_cost_s || o.edge_pair_min_volume_bytes)
+        return 0;
+      if (plans[i]->total_pairs > 0 &&
+          !(o.edge_cost_s || o.edge_volume_bytes || o.edge_memory_bytes || o.aux_edge_records))
+        return 0;
+    }
+  }
+  return want;
+}
+
 // err_dev: optional device array [n] that receives every launched plan's
 // error slot (in `live` order via live_out) -- the host batch checks all
 // plans with one copy instead of one synchronising read per plan.
@@ -685,6 +774,9 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
   int64_t batch_pairs = 0;
   for (int i = 0; i < n; ++i) batch_pairs += plans[i]->total_pairs;
   for (int i = 0; i < n; ++i) plans[i]->in_big_batch = batch_pairs > kWarpPairLimit;
+  const int bmode = batch_mode_of(plans, n, device_outs);
+  const bool use_ops = bmode != 0;
+  const int64_t brange = bmode ? batch_range_len(plans, n) : kFusedThreads * kFanPer;
   for (int i = 0; i < n; ++i) {
     tp_plan* p = plans[i];
     st = ensure_stream(p);
@@ -693,7 +785,7 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
       st = tp_plan_upload(p, s);
       if (st) return st;
     }
-    st = prepare_execute(p, nullptr, &device_outs[i], s, X[i]);
+    st = prepare_execute(p, nullptr, &device_outs[i], s, X[i], bmode, brange);
     p->in_big_batch = false;
     if (st) return st;
     if (!X[i].done && X[i].launch) live.push_back(i);
@@ -715,7 +807,45 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     std::vector<int32_t> glist;                       // member lists, leader first (live order)
     std::vector<std::pair<int, int>> gspan(m, {-1, 0});  // per leader: (offset in glist, size)
     static const bool no_groups = getenv("TP_BATCH_NO_GROUPS") != nullptr;
-    if (nwarp == 0 && !no_groups) {
+    if (use_ops && nwarp != 0) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "internal: op lists with warp-form plans");
+    std::vector<InferJob> ijobs;
+    std::vector<int64_t> ioff{0};
+    std::vector<int64_t> clsops;
+    std::vector<size_t> clsops_at(m, 0);
+    if (use_ops) {
+      std::unordered_map<uint64_t, std::vector<int>> by_hash;  // key hash -> jobs
+      std::vector<const std::vector<int64_t>*> job_key;
+      for (int k = 0; k < m; ++k) {
+        tp_plan* p = plans[live[k]];
+        clsops_at[k] = clsops.size();
+        clsops.resize(clsops.size() + p->sigs.size() + 1, 0);
+        if (p->total_pairs == 0 || !X[live[k]].edge_phase) continue;
+        const auto& keys = class_keys(p);
+        for (size_t c = 0; c < p->sigs.size(); ++c) {
+          const SigDesc& sd = p->sigs[c];
+          if (sd.base != (int32_t)c) continue;
+          auto& cand = by_hash[keys[c].first];
+          int job = -1;
+          for (int j : cand)
+            if (*job_key[j] == keys[c].second) {
+              job = j;
+              break;
+            }
+          if (job < 0) {
+            job = (int)ijobs.size();
+            cand.push_back(job);
+            job_key.push_back(&keys[c].second);
+            Arena& A = *p->arena;
+            ijobs.push_back(InferJob{(const SigDesc*)A.d_sigs.p, (const int32_t*)A.d_pairsigs.p,
+                                     (const int32_t*)A.d_maps.p, (const tpk::SideDesc*)A.d_sides.p, sd.pair_begin,
+                                     ioff.back()});
+            ioff.push_back(ioff.back() + (int64_t)sd.Un * sd.Wn);
+          }
+          clsops[clsops_at[k] + c] = ijobs[job].out;
+        }
+      }
+    }
+    if (nwarp == 0 && !no_groups && !use_ops) {
       std::vector<std::vector<int32_t>> groups;             // live indices, the leader first
       std::unordered_map<uint64_t, std::vector<int>> open;  // structure hash -> group ids
       for (int k = 0; k < m; ++k) {
@@ -753,9 +883,12 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
         }
       }
     }
-    // staging: args[m] | unit_off[m+1] | item_off[m+1] | tab_off[m+1] | group lists
+    // staging: args[m] | unit_off[m+1] | item_off[m+1] | tab_off[m+1] | class op-list offsets |
+    // infer jobs | their prefix sums | group lists
     const size_t args_b = sizeof(FusedArgs) * m, off_b = sizeof(int64_t) * (m + 1);
-    const size_t total = args_b + 3 * off_b + sizeof(int32_t) * (glist.size() + 1);
+    const size_t cls_b = sizeof(int64_t) * clsops.size(), jobs_b = sizeof(InferJob) * ijobs.size(),
+                 ioff_b = sizeof(int64_t) * ioff.size();
+    const size_t total = args_b + 3 * off_b + cls_b + jobs_b + ioff_b + sizeof(int32_t) * (glist.size() + 1);
     if (B.copied) CUDA_TRY(cudaEventSynchronize(B.copied));
     if (B.h_cap < total) {
       if (B.h_stage) cudaFreeHost(B.h_stage);
@@ -769,8 +902,20 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     int64_t* uo = (int64_t*)((char*)B.h_stage + args_b);
     int64_t* io = uo + (m + 1);
     int64_t* to = io + (m + 1);
-    int32_t* hg = (int32_t*)(to + (m + 1));
-    const int32_t* dg = (const int32_t*)((const char*)B.d_args.p + args_b + 3 * off_b);
+    int64_t* hcls = to + (m + 1);
+    InferJob* hjobs = (InferJob*)((char*)hcls + cls_b);
+    int64_t* hioff = (int64_t*)((char*)hjobs + jobs_b);
+    int32_t* hg = (int32_t*)((char*)hioff + ioff_b);
+    const char* dbase = (const char*)B.d_args.p;
+    const int64_t* dcls = (const int64_t*)(dbase + args_b + 3 * off_b);
+    const InferJob* djobs = (const InferJob*)(dbase + args_b + 3 * off_b + cls_b);
+    const int64_t* dioff = (const int64_t*)(dbase + args_b + 3 * off_b + cls_b + jobs_b);
+    const int32_t* dg = (const int32_t*)(dbase + args_b + 3 * off_b + cls_b + jobs_b + ioff_b);
+    if (!clsops.empty()) std::memcpy(hcls, clsops.data(), cls_b);
+    if (!ijobs.empty()) std::memcpy(hjobs, ijobs.data(), jobs_b);
+    std::memcpy(hioff, ioff.data(), ioff_b);
+    const int64_t n_infer = ioff.back();
+    if (use_ops) CUDA_TRY(B.d_ops.ensure(sizeof(uint32_t) * tpk::kOpWords * (size_t)std::max<int64_t>(n_infer, 1)));
     // the heaviest plans first (their units are claimed first, so the long
     // pricing chains do not form the batch's tail): args in `ord` order, the
     // group lists translated to it
@@ -791,6 +936,10 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
       const int k = ord[j];
       const ExecPrep& x = X[live[k]];
       ha[j] = x.a;
+      if (use_ops) {
+        ha[j].oplists = (const uint32_t*)B.d_ops.p;
+        ha[j].cls_ops = dcls + clsops_at[k];
+      }
       if (gspan[k].second >= 2) {
         ha[j].group = dg + gspan[k].first;
         ha[j].group_n = gspan[k].second;
@@ -816,10 +965,15 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     }
     const int64_t blocks_needed = std::max<int64_t>(io[m], (uo[m] + 7) / 8);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(blocks_needed, B.resident));
+    if (use_ops && n_infer > 0) {  // the batch's inference pass, before the build
+      infer_kernel<<<(unsigned)((n_infer + 127) / 128), 128, 0, s>>>(djobs, (int)ijobs.size(), dioff,
+                                                                    (uint32_t*)B.d_ops.p);
+      CUDA_TRY(cudaGetLastError());
+    }
     const FusedArgs* da = (const FusedArgs*)B.d_args.p;
     const int64_t* duo = (const int64_t*)((const char*)B.d_args.p + args_b);
     static const int wide = getenv("TP_BATCH_WIDE") ? atoi(getenv("TP_BATCH_WIDE")) : 0;  // measured: 4 CTAs/SM with spills beats 2 without
-    const int form = nwarp == m ? 1 : (nwarp == 0 ? (wide ? 3 : 2) : 0);
+    const int form = nwarp == m ? 1 : (nwarp == 0 ? (use_ops ? bmode : (wide ? 3 : 2)) : 0);
     const dim3 gd((unsigned)std::min<int64_t>(grid, form == 3 ? B.resident_wide : B.resident)), bd(kFusedThreads);
     const int64_t* dio = duo + (m + 1);
     const int64_t* dto = duo + 2 * (m + 1);
@@ -827,7 +981,15 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     if (form == 1) fused_batch_kernel<1><<<gd, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
     else if (form == 2) fused_batch_kernel<2><<<gd, bd, kMsecBytes, s>>>(da, m, duo, dio, dto, hd, err_dev);
     else if (form == 3) fused_batch_kernel<3><<<gd, bd, kMsecBytes, s>>>(da, m, duo, dio, dto, hd, err_dev);
+    else if (form == 4) fused_batch_kernel<4><<<gd, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
+    else if (form == 5) {  // the tables, then the fan-out (ordered by the launch boundary)
+      const dim3 g1((unsigned)std::max<int64_t>(1, std::min<int64_t>((uo[m] + 15) / 16, B.resident)));
+      const dim3 g2((unsigned)std::max<int64_t>(1, std::min<int64_t>(io[m], B.resident)));
+      fused_batch_kernel<5, 1><<<g1, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
+      fused_batch_kernel<5, 2><<<g2, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
+    }
     else fused_batch_kernel<0><<<gd, bd, kMsecBytes, s>>>(da, m, duo, dio, dto, hd, err_dev);
+    B.last_launches = (use_ops && n_infer > 0 ? 1 : 0) + (form == 5 ? 2 : 1);
     if (cudaPeekAtLastError() != cudaSuccess) {
       B.hdr_clean = false;
       for (int k : live) plans[k]->arena->sched_clean = false;
@@ -835,6 +997,7 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     for (int k : live) {
       after_launch(plans[k]);
       plans[k]->last_grid = grid;
+      if (use_ops) plans[k]->arena->tables_dirty = true;
     }
   }
   for (int i = 0; i < n; ++i) {
@@ -855,6 +1018,10 @@ extern "C" {
 tp_status tp_plan_execute_batch(tp_plan* const* plans, int32_t n, tp_cost_tensors* device_outs, void* stream) {
   DeviceGuard dg;
   return execute_batch_impl(plans, n, device_outs, stream, nullptr, nullptr);
+}
+
+int64_t tp_batch_last_launches(int32_t device) {
+  return device >= 0 && device < 64 ? g_batch[device].last_launches : 0;
 }
 
 tp_status tp_plan_set_bandwidth(tp_plan* p, double intra_bandwidth, double inter_bandwidth) {
@@ -968,9 +1135,12 @@ tp_status tp_plan_timeline_detail(tp_plan* p, int32_t section, uint32_t* out, in
   return TP_OK;
 }
 
-tp_status tp_plan_check_errors(tp_plan* p) {
-  DeviceGuard dg;
-  if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
+}  // extern "C"
+
+namespace {
+// The smallest error key of the plan's last execute (device slot, host
+// analysis); ~0 = none. Synchronises the plan's stream.
+tp_status plan_error_key(tp_plan* p, uint64_t& key) {
   CUDA_TRY(cudaSetDevice(p->device));
   unsigned long long dev = ~0ull;
   if (p->arena && p->arena->d_sched.p && p->last_stream) {
@@ -982,15 +1152,35 @@ tp_status tp_plan_check_errors(tp_plan* p) {
     CUDA_TRY(cudaStreamSynchronize(p->last_stream));
     dev = ~c;  // Sched::err_c holds the complement of the smallest key
   }
-  const uint64_t key = std::min<uint64_t>(dev, p->host_err);
+  key = std::min<uint64_t>(dev, p->host_err);
+  return TP_OK;
+}
+
+tp_status status_of_key(uint64_t key) {
   if (key == ~0ull) return TP_OK;
   const int kind = (int)(key & 63);
   return set_err(status_of_kind(kind), kind, kind_text(kind));
 }
+}  // namespace
 
-tp_status tp_plan_execute_host(tp_plan* p, const tp_build_opts* opts, tp_aux_index* index_out,
-                               tp_cost_tensors* host_out) {
+extern "C" {
+
+tp_status tp_plan_check_errors(tp_plan* p) {
   DeviceGuard dg;
+  if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
+  uint64_t key = ~0ull;
+  tp_status st = plan_error_key(p, key);
+  if (st) return st;
+  return status_of_key(key);
+}
+
+}  // extern "C"
+
+namespace {
+// tp_plan_execute_host; with key_out the smallest error key is returned
+// there instead of as a status (the multi-device build combines its devices').
+tp_status execute_host_impl(tp_plan* p, const tp_build_opts* opts, tp_aux_index* index_out,
+                            tp_cost_tensors* host_out, uint64_t* key_out) {
   if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
   tp_status st = ensure_stream(p);
   if (st) return st;
@@ -1053,11 +1243,21 @@ tp_status tp_plan_execute_host(tp_plan* p, const tp_build_opts* opts, tp_aux_ind
   ce = ce ? ce : back(h.row_min_volume_bytes, d.row_min_volume_bytes, nr, 8);
   ce = ce ? ce : back(h.edge_pair_min_cost_s, d.edge_pair_min_cost_s, e1 - e0, 8);
   ce = ce ? ce : back(h.edge_pair_min_volume_bytes, d.edge_pair_min_volume_bytes, e1 - e0, 8);
-  st = tp_plan_check_errors(p);  // synchronises the stream
+  if (key_out) st = plan_error_key(p, *key_out);  // synchronises the stream
+  else st = tp_plan_check_errors(p);
   if (ce != cudaSuccess) return set_err(TP_ERR_CUDA, 0, cudaGetErrorString(ce));
   if (st) return st;
   if (index_out) tp_plan_index(p, index_out);
   return TP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+tp_status tp_plan_execute_host(tp_plan* p, const tp_build_opts* opts, tp_aux_index* index_out,
+                               tp_cost_tensors* host_out) {
+  DeviceGuard dg;
+  return execute_host_impl(p, opts, index_out, host_out, nullptr);
 }
 
 tp_status tp_build_cost_tensors(const tp_graph_desc* graph, const tp_topology_desc* topo,
@@ -1070,6 +1270,154 @@ tp_status tp_build_cost_tensors(const tp_graph_desc* graph, const tp_topology_de
   p->arena = thread_arena(p->device);  // reused across one-shot calls
   p->owns_arena = p->arena == nullptr;
   st = tp_plan_execute_host(p, opts, index_out, host_out);
+  tp_plan_destroy(p);
+  return st;
+}
+
+}  // extern "C"
+
+namespace {
+// A copy of an analysed plan for another device (the multi-device build):
+// the host analysis is device-independent; arenas, uploads and launch state
+// are not copied.
+tp_plan* clone_for_device(const tp_plan* p, int device) {
+  tp_plan* q = new tp_plan(*p);
+  q->device = device;
+  q->arena = nullptr;
+  q->owns_arena = true;
+  q->d_terms = nullptr;
+  q->uploaded = false;
+  q->range_key = {{-1, -1, -1, -1}};
+  q->last_stream = nullptr;
+  q->prof_start = q->prof_stop = nullptr;
+  q->timeline = false;
+  q->last_parity = -1;
+  q->resident_blocks = 0;
+  q->shards.clear();
+  return q;
+}
+
+// Contiguous graph-edge ranges, one per device, balanced by aux edges
+// (sum |Su| x |Sw|, the edge_base differences).
+std::vector<int32_t> edge_split(const tp_plan* p, int n) {
+  const int32_t E = p->valid_edges;
+  std::vector<int32_t> b(n + 1, 0);
+  b[n] = E;
+  const int64_t a0 = p->edge_base[0], total = p->edge_base[E] - a0;
+  for (int r = 1; r < n; ++r) {
+    const double target = (double)a0 + (double)total * r / n;
+    int32_t e = b[r - 1];
+    while (e < E && (double)p->edge_base[e] + 0.5 * (double)(p->edge_base[e + 1] - p->edge_base[e]) <= target) ++e;
+    b[r] = e;
+  }
+  return b;
+}
+
+// Every device of `devices` builds its edge range of plan p (device 0 of the
+// list also the per-node tensors) and copies its slice straight into the
+// caller's host arrays at the range's offsets. borrow: shards take pooled
+// arenas for the call (the one-shot entry) instead of owning one.
+tp_status execute_host_multi(tp_plan* p, const int32_t* devices, int32_t n, tp_aux_index* index_out,
+                             tp_cost_tensors* host_out, bool borrow) {
+  if (!p || !devices || n < 1 || !host_out) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "bad multi-device arguments");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(TP_ERR_CUDA, 0, "no CUDA device: the engine has no CPU path");
+  for (int i = 0; i < n; ++i) {
+    if (devices[i] < 0 || devices[i] >= ndev || devices[i] >= 64)
+      return set_err(TP_ERR_INVALID_ARGUMENT, 0, "device ordinal out of range");
+    for (int j = 0; j < i; ++j)
+      if (devices[j] == devices[i]) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "device listed twice");
+  }
+  // per-device copies of the analysed plan, cached on it
+  if ((int)p->shards.size() < n) p->shards.resize(n, nullptr);
+  for (int i = 0; i < n; ++i) {
+    tp_plan*& q = p->shards[i];
+    if (q && q->device != devices[i]) {
+      tp_plan_destroy(q);
+      q = nullptr;
+    }
+    if (!q) q = clone_for_device(p, devices[i]);
+    if (q->env.intra != p->env.intra || q->env.inter != p->env.inter) {  // tp_plan_set_bandwidth reaches the shards
+      q->env = p->env;
+      q->uploaded = false;
+    }
+  }
+  const std::vector<int32_t> b = edge_split(p, n);
+  std::vector<tp_status> st(n, TP_OK);
+  std::vector<std::string> msg(n);
+  std::vector<int> kinds(n, 0);
+  std::vector<uint64_t> keys(n, ~0ull);
+  auto work = [&](int i) {
+    tp_plan* q = p->shards[i];
+    cudaSetDevice(q->device);
+    if (borrow && !q->arena) {
+      q->arena = arena_pool_get(q->device);
+      q->owns_arena = false;
+      q->uploaded = false;
+    }
+    const int32_t e0 = b[i], e1 = b[i + 1];
+    const int64_t off = q->edge_base[e0] - q->edge_base[0];
+    const int64_t roff = q->row_base[e0] - q->row_base[0];
+    tp_cost_tensors h = *host_out;
+    if (i) h.node_intra_cost_s = h.node_intra_volume_bytes = h.node_memory_bytes = nullptr;
+    auto sh = [](double* x, int64_t o) { return x ? x + o : nullptr; };
+    h.edge_cost_s = sh(h.edge_cost_s, off);
+    h.edge_volume_bytes = sh(h.edge_volume_bytes, off);
+    h.edge_memory_bytes = sh(h.edge_memory_bytes, off);
+    if (h.aux_edge_records) h.aux_edge_records = (char*)h.aux_edge_records + 40 * off;
+    h.row_min_cost_s = sh(h.row_min_cost_s, roff);
+    h.row_min_volume_bytes = sh(h.row_min_volume_bytes, roff);
+    h.edge_pair_min_cost_s = sh(h.edge_pair_min_cost_s, e0);
+    h.edge_pair_min_volume_bytes = sh(h.edge_pair_min_volume_bytes, e0);
+    const tp_build_opts o{e0, e1, i != 0, q->device, nullptr};
+    st[i] = execute_host_impl(q, &o, nullptr, &h, &keys[i]);
+    if (st[i]) {
+      msg[i] = g_err;
+      kinds[i] = g_err_kind;
+    }
+    if (borrow && !q->owns_arena) {
+      arena_pool_put(q->arena);
+      q->arena = nullptr;
+      q->owns_arena = true;
+      q->uploaded = false;
+      q->range_key = {{-1, -1, -1, -1}};
+    }
+  };
+  std::vector<std::thread> th;
+  for (int i = 1; i < n; ++i) th.emplace_back(work, i);
+  work(0);
+  for (auto& t : th) t.join();
+  for (int i = 0; i < n; ++i)
+    if (st[i]) return set_err(st[i], kinds[i], msg[i]);
+  uint64_t key = ~0ull;
+  for (uint64_t k : keys) key = std::min(key, k);
+  tp_status r = status_of_key(key);
+  if (r) return r;
+  if (index_out) tp_plan_index(p, index_out);
+  g_err[0] = 0;
+  g_err_kind = 0;
+  return TP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+tp_status tp_plan_execute_host_multi(tp_plan* p, const int32_t* devices, int32_t num_devices,
+                                     tp_aux_index* index_out, tp_cost_tensors* host_out) {
+  DeviceGuard dg;
+  return execute_host_multi(p, devices, num_devices, index_out, host_out, false);
+}
+
+tp_status tp_build_cost_tensors_multi(const tp_graph_desc* graph, const tp_topology_desc* topo,
+                                      const int32_t* devices, int32_t num_devices, tp_aux_index* index_out,
+                                      tp_cost_tensors* host_out) {
+  DeviceGuard dg;
+  if (!devices || num_devices < 1) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "empty device list");
+  tp_plan* p = nullptr;
+  tp_status st = tp_plan_create(graph, topo, devices[0], &p);
+  if (st) return st;
+  st = execute_host_multi(p, devices, num_devices, index_out, host_out, true);
   tp_plan_destroy(p);
   return st;
 }
@@ -1229,9 +1577,12 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
   std::vector<int> todo;
   for (int i = 0; i < n; ++i)
     if (borrowed[i]) todo.push_back(i);
+  // as execute_batch_impl will decide (same outputs): with op lists no pair records are read
+  const bool direct = batch_mode_of(plans, n, host_outs) != 0;
   std::vector<UploadPrep> U(todo.size());
-  run_pool((int)todo.size(), host_threads, [&](int j, int) { errs[todo[j]].take(upload_prepare(plans[todo[j]], U[j])); },
-           device);
+  const int64_t brange = direct ? batch_range_len(plans, n) : kFusedThreads * kFanPer;  // as execute_batch_impl
+  run_pool((int)todo.size(), host_threads,
+           [&](int j, int) { errs[todo[j]].take(upload_prepare(plans[todo[j]], U[j], brange)); }, device);
   for (int i = 0; i < n; ++i)
     if (errs[i].st) {
       give_back();
@@ -1290,7 +1641,9 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
     const UpJob* dj = (const UpJob*)(dp + jobs_at);
     const int64_t* dso = (const int64_t*)(dp + jobs_at + sizeof(UpJob) * m);
     if (so[m] > 0) batch_side_kernel<<<(unsigned)((so[m] + 127) / 128), 128, 0, s>>>(dj, m, dso);
-    if (po[m] > 0) batch_pair_rec_kernel<<<(unsigned)((po[m] + 127) / 128), 128, 0, s>>>(dj, m, dso + (m + 1));
+    // a batch priced in the fan-out reads layouts through the descriptors, not pair records
+    if (po[m] > 0 && !direct)
+      batch_pair_rec_kernel<<<(unsigned)((po[m] + 127) / 128), 128, 0, s>>>(dj, m, dso + (m + 1));
     CUDA_TRY(cudaGetLastError());
   }
   const double hb1 = prof ? clk() : 0;
@@ -1445,6 +1798,32 @@ tp_status tp_plan_price_assignments(tp_plan* p, const tp_cost_tensors* t, const 
                                                    t->node_memory_bytes, t->edge_cost_s, t->edge_volume_bytes,
                                                    t->edge_memory_bytes, cost_s, volume_bytes, memory_bytes);
   CUDA_TRY(cudaGetLastError());
+  return TP_OK;
+}
+
+tp_status tp_plan_export_lp(const tp_plan* p, const tp_cost_tensors* h, int32_t mode_volume, double device_memory,
+                            const char* path, int64_t* bytes_out) {
+  if (!p || !h || !path) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null argument");
+  if (p->host_err != ~0ull) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "the plan's build has an error");
+  if (!h->node_intra_cost_s || !h->node_intra_volume_bytes || !h->node_memory_bytes || !h->edge_cost_s ||
+      !h->edge_volume_bytes || !h->edge_memory_bytes)
+    return set_err(TP_ERR_INVALID_ARGUMENT, 0, "all six host cost tensors are needed");
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return set_err(TP_ERR_INVALID_ARGUMENT, 0, std::string("cannot write '") + path + "'");
+  taps_b200::LpInput in{p->num_ops,        p->num_edges,           p->node_base.data(),     p->edge_base.data(),
+                        p->edge_from_op.data(), p->edge_to_op.data(), p->in_deg.data(),      p->out_deg.data(),
+                        h->node_intra_cost_s, h->node_intra_volume_bytes, h->node_memory_bytes, h->edge_cost_s,
+                        h->edge_volume_bytes, h->edge_memory_bytes};
+  int64_t total = 0;
+  bool ok = true;
+  auto sink = [&](const char* d, size_t n) {
+    ok = ok && std::fwrite(d, 1, n, f) == n;
+    total += (int64_t)n;
+  };
+  taps_b200::write_lp(in, mode_volume != 0, device_memory, sink);
+  ok = std::fclose(f) == 0 && ok;
+  if (!ok) return set_err(TP_ERR_INVALID_ARGUMENT, 0, std::string("write to '") + path + "' failed");
+  if (bytes_out) *bytes_out = total;
   return TP_OK;
 }
 

@@ -176,11 +176,45 @@ TP_HD_NOINL void price_members(MultiSec* ms, bool a2a, int pos, int rexp, int e,
   }
 }
 
+// The op list of one pair, recorded instead of priced (kRecord): an op is
+// priced by price_fast from (AllToAll?, lower position, in-node repetition
+// exponent, log2 extent, shard exponent) alone, all of which the inference
+// fixes independently of the tensor bytes and the bandwidths. A sweep infers
+// each distinct (layouts, dims) pair once and prices it per scenario
+// (price_ops): the same additions in the same order as pricing on the fly.
+constexpr int kOpWords = 16;  // header + up to 15 ops (64 B)
+constexpr uint32_t kOpsSame = 1u << 16;  // from == to: no redistribution (aux_graph.hpp:169-171, 260)
+constexpr uint32_t kOpsFull = 1u << 17;  // not representable: price with pair_cost_sd
+struct OpRec {
+  uint32_t w[kOpWords];
+  int n;
+  TP_HD bool push(bool a2a, int pos, int rexp, int e, int s) {
+    if (n >= kOpWords - 1) return false;
+    w[1 + n++] = (uint32_t)a2a | ((uint32_t)pos << 1) | ((uint32_t)rexp << 6) | ((uint32_t)e << 11) |
+                 ((uint32_t)s << 16);
+    return true;
+  }
+};
+
+TP_HD void price_ops(const uint32_t* ops, int n, double bytes, const Env& env, int l_log2, const FastTabs& tab,
+                     double& sec_out, double& vol_out) {
+  double sec = 0, vol = 0;
+  for (int o = 0; o < n; ++o) {
+    const uint32_t w = ops[o];
+    sec += price_fast(w & 1u, (w >> 1) & 31, (w >> 6) & 31, (w >> 11) & 31, (w >> 16) & 31, bytes, env, l_log2,
+                      tab, &vol, nullptr);
+  }
+  sec_out = sec;
+  vol_out = vol;
+}
+
 // Returns the tp_error_kind, or -1 when the pair needs the array form
-// (a device dim held twice by the working map).
+// (a device dim held twice by the working map; with kRecord also when the
+// op list does not fit an OpRec).
+template <bool kRecord = false>
 TP_HD int redist_cost_fast(int R, const SideDesc& gf, const SideDesc& gt, const DimT* dt, double bytes,
                            const Env& env, int l_log2, const FastTabs& tab, double& sec_out, double& vol_out,
-                           Trace* tr, MultiSec* ms = nullptr) {
+                           Trace* tr, MultiSec* ms = nullptr, OpRec* rec = nullptr) {
   if (R < 0 || R > kMaxR) return kCapacity;
   // ---- unify: bitmask closure (see tp_core.cuh) ----
   uint32_t D = gf.D | gt.D;
@@ -332,11 +366,15 @@ TP_HD int redist_cost_fast(int R, const SideDesc& gf, const SideDesc& gt, const 
           if (j < 0 || j == i || ((OCC >> j) & 1u)) continue;
           const int e = p2get(EXT, k), pos = p2get(POS, k);
           const int rexp = pos - popc32(PB & low_bits(pos));
-          int64_t ct = 0;
-          const double c = price_fast(true, pos, rexp, e, s, bytes, env, l_log2, tab, &vol, tr ? &ct : nullptr);
-          sec += c;
-          if (ms) price_members(ms, true, pos, rexp, e, s, bytes, l_log2);
-          record(2, k, i, j, 0, ct, c);
+          if (kRecord) {
+            if (!rec->push(true, pos, rexp, e, s)) return -1;
+          } else {
+            int64_t ct = 0;
+            const double c = price_fast(true, pos, rexp, e, s, bytes, env, l_log2, tab, &vol, tr ? &ct : nullptr);
+            sec += c;
+            if (ms) price_members(ms, true, pos, rexp, e, s, bytes, l_log2);
+            record(2, k, i, j, 0, ct, c);
+          }
           const uint32_t bi = 1u << i, bj = 1u << j;
           pset(W, i, 0);
           pset(W, j, k + 1);
@@ -360,11 +398,15 @@ TP_HD int redist_cost_fast(int R, const SideDesc& gf, const SideDesc& gt, const 
     const int k = pget(W, i) - 1;
     const int e = p2get(EXT, k), pos = p2get(POS, k);
     const int rexp = pos - popc32(PB & low_bits(pos));
-    int64_t ct = 0;
-    const double c = price_fast(false, pos, rexp, e, s, bytes, env, l_log2, tab, &vol, tr ? &ct : nullptr);
-    sec += c;
-    if (ms) price_members(ms, false, pos, rexp, e, s, bytes, l_log2);
-    record(1, k, i, -1, fb, ct, c);
+    if (kRecord) {
+      if (!rec->push(false, pos, rexp, e, s)) return -1;
+    } else {
+      int64_t ct = 0;
+      const double c = price_fast(false, pos, rexp, e, s, bytes, env, l_log2, tab, &vol, tr ? &ct : nullptr);
+      sec += c;
+      if (ms) price_members(ms, false, pos, rexp, e, s, bytes, l_log2);
+      record(1, k, i, -1, fb, ct, c);
+    }
     const uint32_t bi = 1u << i;
     pset(W, i, 0);
     OCC &= ~bi;
@@ -403,6 +445,31 @@ TP_HD int pair_cost_sd(int R, const SideDesc& F, const SideDesc& T, const Lay* F
     }
   }
   return kOk;
+}
+
+// The op list of one class-table entry (the sweep's inference pass): the
+// header word holds the op count, the tp_error_kind << 8 and the flags.
+TP_HD void infer_ops(int R, const SideDesc& F, const SideDesc& T, const DimT* dt, uint32_t* out) {
+  OpRec r;
+  r.n = 0;
+  uint32_t flags = 0;
+  int st = kOk;
+  if (same_side(F, T, R)) {
+    flags = kOpsSame;
+  } else {
+    double sec = 0, vol = 0;
+    st = redist_cost_fast<true>(R, F, T, dt, 0.0, Env{0, 0, 0}, -1, FastTabs{nullptr, nullptr}, sec, vol, nullptr,
+                                nullptr, &r);
+    if (st == -1) {
+      st = kOk;
+      flags = kOpsFull;
+      r.n = 0;
+    } else if (st) {
+      r.n = 0;
+    }
+  }
+  r.w[0] = (uint32_t)r.n | ((uint32_t)st << 8) | flags;
+  for (int o = 0; o < kOpWords; ++o) out[o] = o <= r.n ? r.w[o] : 0u;
 }
 
 TP_HD int pair_cost(int R, const Lay& F, const Lay& T, const DimT* dt, double bytes, const Env& env, int l_log2,

@@ -55,24 +55,30 @@ struct alignas(16) PairRec {
   DimT dt[tpk::kMaxR];
 };
 
-__device__ __forceinline__ void pair_rec_one(const SigDesc* __restrict__ sigs, const int32_t* __restrict__ pair_sig,
-                                             const int32_t* __restrict__ maps, const tpk::SideDesc* __restrict__ sides,
-                                             const double* __restrict__ overrides, int64_t idx,
-                                             PairRec* __restrict__ out) {
+__device__ __forceinline__ void pair_rec_of(const SigDesc* __restrict__ sigs, const int32_t* __restrict__ pair_sig,
+                                            const int32_t* __restrict__ maps, const tpk::SideDesc* __restrict__ sides,
+                                            const double* __restrict__ overrides, int64_t idx, PairRec& r) {
   const int sig = pair_sig[idx];
   const SigDesc& sg = sigs[sig];
   const int32_t t = (int32_t)(idx - sg.pair_begin);
   const int32_t ui = t / sg.Wn, wi = t - ui * sg.Wn;
   const int32_t su = maps[sg.rep_u + ui], sw = maps[sg.rep_w + wi];
-  PairRec r;
   r.F = sides[sg.side_u + su];
   r.T = sides[sg.side_w + sw];
-  r.bytes = sg.has_override ? overrides[idx] : sg.bytes;
+  r.bytes = (sg.has_override && overrides) ? overrides[idx] : sg.bytes;
   r.sig = sig;
   r.local = su * sg.Sw + sw;
   r.R = sg.R;
   r.pad = 0;
   for (int d = 0; d < tpk::kMaxR; ++d) r.dt[d] = sg.dt[d];
+}
+
+__device__ __forceinline__ void pair_rec_one(const SigDesc* __restrict__ sigs, const int32_t* __restrict__ pair_sig,
+                                             const int32_t* __restrict__ maps, const tpk::SideDesc* __restrict__ sides,
+                                             const double* __restrict__ overrides, int64_t idx,
+                                             PairRec* __restrict__ out) {
+  PairRec r;
+  pair_rec_of(sigs, pair_sig, maps, sides, overrides, idx, r);
   out[idx] = r;
 }
 
@@ -307,6 +313,12 @@ struct FusedArgs {
   const int32_t* group;
   int group_n;
   int priced_by_leader;
+  // batches (thread form): the op list of every class-table entry, inferred
+  // once per distinct class key of the batch by infer_kernel; table entry r
+  // of base class c is oplists + (cls_ops[c] + r - pair_begin(c)) * kOpWords
+  const uint32_t* oplists;
+  const int64_t* cls_ops;
+  int direct;  // priced in the fan-out from the op lists: no pair units, no class tables
 
   // shared
   const Strat* tables;
@@ -453,6 +465,34 @@ __device__ void pair_thread(const FusedArgs& a, int64_t idx, const double* price
   for (int q = 1; q < g; ++q) all[a.group[q]].r_tab[idx] = make_double2(ms.s(q), vol);
 }
 
+// The inference pass of a batch: one thread per distinct class-table entry
+// (job q covers entries recs[0, count) of its first plan), writing the op
+// lists the fan-out prices for every plan with that class key.
+struct InferJob {
+  // the first plan with the class key: its descriptors (pair_rec_of)
+  const SigDesc* sigs;
+  const int32_t* pair_sig;
+  const int32_t* maps;
+  const tpk::SideDesc* sides;
+  int64_t first;  // the class's first table entry in that plan
+  int64_t out;    // its first op list (in entries)
+};
+
+__global__ void infer_kernel(const InferJob* __restrict__ jobs, int njobs, const int64_t* __restrict__ off,
+                             uint32_t* __restrict__ oplists) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= off[njobs]) return;
+  const int q = bisect_off(off, njobs, i);
+  const InferJob& jb = jobs[q];
+  PairRec pr;
+  pair_rec_of(jb.sigs, jb.pair_sig, jb.maps, jb.sides, nullptr, jb.first + (i - off[q]), pr);
+  uint32_t w[tpk::kOpWords];
+  tpk::infer_ops(pr.R, pr.F, pr.T, pr.dt, w);
+  uint4* o = reinterpret_cast<uint4*>(oplists + (jobs[q].out + (i - off[q])) * tpk::kOpWords);
+#pragma unroll
+  for (int k = 0; k < tpk::kOpWords / 4; ++k) o[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+}
+
 // One class-table entry on one warp (warp form, tp_warp.cuh); lane 0 writes.
 __device__ void pair_warp(const FusedArgs& a, int64_t idx, const double* price) {
   const int lane = threadIdx.x & 31;
@@ -487,6 +527,82 @@ __device__ void pair_warp(const FusedArgs& a, int64_t idx, const double* price) 
 // consecutive ids, so every warp store is one 256-B segment per array.
 constexpr int kSegs = 32;  // one per lane of warp 0
 
+// An aux edge's redistribution priced in the fan-out (batches with op
+// lists): the entry's op list with the base class's bytes and this plan's
+// bandwidths -- the same expressions and order as its table entry would
+// have. An inference error is flagged at the aux edge's own id: the smallest
+// such id is the entry's first use, where the reference throws.
+__device__ __noinline__ void full_entry(const FusedArgs& a, int64_t r, int64_t o, double& sec, double& vol) {
+  PairRec pr;  // from the descriptors (a batch priced in the fan-out uploads no pair records)
+  pair_rec_of(a.sigs, a.pair_sig, a.maps, a.sides, a.overrides, r, pr);
+  double s2 = 0, v2 = 0;
+  const int st = tpk::pair_cost_sd(pr.R, pr.F, pr.T, nullptr, nullptr, pr.dt, pr.bytes, a.env, a.l_log2,
+                                   tpk::FastTabs{a.bw_tab, a.bw_tab + tpk::kBwTab}, s2, v2, nullptr);
+  if (st) flag_error(a.err, ekey(kEdgePhase + (uint64_t)o * 2 + 1, st));
+  sec = st ? 0.0 : s2;
+  vol = st ? 0.0 : v2;
+}
+
+__device__ __forceinline__ void direct_entry(const FusedArgs& a, const FanSeg& g, int64_t r, int64_t o, double& sec,
+                                             double& vol) {
+  const uint32_t* ol = a.oplists + (g.opb + (r - g.pb)) * tpk::kOpWords;
+  const uint32_t h = ol[0];
+  sec = vol = 0;
+  if (h & tpk::kOpsFull) {
+    full_entry(a, r, o, sec, vol);
+    return;
+  }
+  const int st = (h >> 8) & 0xff;
+  if (st) {
+    flag_error(a.err, ekey(kEdgePhase + (uint64_t)o * 2 + 1, st));
+    return;
+  }
+  if (h & 0xff)
+    tpk::price_ops(ol + 1, h & 0xff, g.ovr ? a.overrides[r] : g.bytes, a.env, a.l_log2,
+                   tpk::FastTabs{a.bw_tab, a.bw_tab + tpk::kBwTab}, sec, vol);
+}
+
+// One class-table entry of a batch plan from its inferred op list: the
+// reference's expressions summed in op order (tp_fast.cuh price_ops) with
+// this plan's bytes and bandwidths; entries the op list cannot represent take
+// the full register form. Errors keep the entry's first aux id (its class's
+// first edge, first strategy pair with these layouts).
+__device__ __noinline__ void pair_entry_full(const FusedArgs& a, int64_t idx, const double* price) {
+  PairRec pr;
+  pair_rec_of(a.sigs, a.pair_sig, a.maps, a.sides, a.overrides, idx, pr);
+  double sec = 0, vol = 0;
+  const int st = tpk::pair_cost_sd(pr.R, pr.F, pr.T, nullptr, nullptr, pr.dt, pr.bytes, a.env, a.l_log2,
+                                   tpk::FastTabs{price, price + tpk::kBwTab}, sec, vol, nullptr);
+  if (st) flag_error(a.err, ekey(kEdgePhase + (uint64_t)(a.sigs[pr.sig].first_aux + pr.local) * 2 + 1, st));
+  a.r_tab[idx] = st ? make_double2(0.0, 0.0) : make_double2(sec, vol);
+}
+
+__device__ __forceinline__ void pair_from_ops(const FusedArgs& a, int64_t idx, const double* price) {
+  const int sig = a.pair_sig[idx];
+  const SigDesc& sg = a.sigs[sig];
+  const uint32_t* ol = a.oplists + (a.cls_ops[sig] + (idx - sg.pair_begin)) * tpk::kOpWords;
+  const uint32_t h = ol[0];
+  if (h & tpk::kOpsFull) {
+    pair_entry_full(a, idx, price);
+    return;
+  }
+  double sec = 0, vol = 0;
+  const int st = (h >> 8) & 0xff;
+  if (st) {
+    PairRec pr;
+    pair_rec_of(a.sigs, a.pair_sig, a.maps, a.sides, a.overrides, idx, pr);
+    flag_error(a.err, ekey(kEdgePhase + (uint64_t)(sg.first_aux + pr.local) * 2 + 1, st));
+  } else if (h & 0xff) {
+    tpk::price_ops(ol + 1, h & 0xff, sg.has_override ? a.overrides[idx] : sg.bytes, a.env, a.l_log2,
+                   tpk::FastTabs{price, price + tpk::kBwTab}, sec, vol);
+  }
+  a.r_tab[idx] = make_double2(sec, vol);
+}
+
+// kDirect: priced here from the op lists (no class tables); kWait = false:
+// the tables and rows come from an earlier launch (no counters, no unset
+// checks).
+template <bool kDirect, bool kWait = true>
 __device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n, int* s_edge) {
   const unsigned long long t0 = a.fan_ns ? gtimer() : 0;
   const int64_t start = a.A0 + (int64_t)item * a.range_len;
@@ -508,11 +624,12 @@ __device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n
       if (in) {
         // relaxed: the entries are unset-checked; an acquire here would also
         // drop the L1 lines the SM's other CTAs are reading
-        wait_relaxed(&a.sched->pairs_done[g.base].v, g.need);
+        if (kDirect) g.opb = a.cls_ops[g.base];
+        else if (kWait) wait_relaxed(&a.sched->pairs_done[g.base].v, g.need);
         seg[lane] = g;
       }
       const int n = __popc(__ballot_sync(0xffffffffu, in));  // a prefix of the lanes
-      if (first) {
+      if (kWait && first) {
         if (lane == 0) wait_at_least(&a.sched->node_done.v, (int)a.total_rows);
         __syncwarp();
       }
@@ -567,7 +684,10 @@ __device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n
         // the range's ids, through L1
         const int64_t row = g.wrow + sw;
         const double2 cv = a.cls_sv[row];
-        const double2 rv = table_load2(a.r_tab + r);
+        double2 rv;
+        if (kDirect) direct_entry(a, g, r, o, rv.x, rv.y);
+        else if (kWait) rv = table_load2(a.r_tab + r);
+        else rv = a.r_tab[r];
         cs[k] = cv.x + rv.x * g.f;  // aux_graph.hpp:290-291
         vs[k] = cv.y + rv.y * g.f;
         ms[k] = a.cls_memdiv[row];                               // :292
@@ -615,13 +735,14 @@ struct NodeSeg {
   int64_t begin, end, row;
 };
 
+template <bool kWait = true>
 __device__ void node_range(const FusedArgs& a, int item, NodeSeg* seg, int* s_n, int* s_op) {
   const int64_t start = (int64_t)item * a.node_range_len;
   const int64_t end = min(start + a.node_range_len, a.num_nodes);
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     *s_op = a.nrange_first[item];  // host-computed
-    wait_at_least(&a.sched->node_done.v, (int)a.total_rows);
+    if (kWait) wait_at_least(&a.sched->node_done.v, (int)a.total_rows);
   }
   int64_t pos = start;
   while (pos < end) {
@@ -669,14 +790,17 @@ __device__ void node_range(const FusedArgs& a, int item, NodeSeg* seg, int* s_n,
 
 // One phase-1 unit u of a plan: a node-class row, or a class pair (warp
 // form) / 32 class pairs (thread form).
-template <bool kWarpForm>
+// kSync = false: the fan-out runs in a later launch (the kernel boundary
+// orders everything), so no counters are published; kOps: thread-form pairs
+// priced from the batch's op lists (pair_from_ops).
+template <bool kWarpForm, bool kSync = true, bool kOps = false>
 __device__ __forceinline__ void run_unit(const FusedArgs& a, int64_t u, const double* price,
                                          const FusedArgs* all = nullptr) {
   const int lane = threadIdx.x & 31;
   const unsigned long long t0 = (a.pair_ns || a.item_ns) ? gtimer() : 0;
   if (u < a.total_rows) {
     node_row(a, u);
-    if (lane == 0) {
+    if (kSync && lane == 0) {
       red_release_add(&a.sched->node_done.v, 1);  // rows: off the critical path, released
       if (a.item_ns) {
         a.item_ns[2 * u] = (unsigned)t0;
@@ -699,7 +823,11 @@ __device__ __forceinline__ void run_unit(const FusedArgs& a, int64_t u, const do
     const bool valid = idx < a.total_pairs;
     const int sig = valid ? sig_of_pair(a, idx) : -1;
     const bool grouped = all && a.group_n > 1;
-    if (valid) pair_thread(a, idx, price, all);
+    if (valid) {
+      if constexpr (kOps) pair_from_ops(a, idx, price);
+      else pair_thread(a, idx, price, all);
+    }
+    if (!kSync) return;
     if (a.pair_ns && valid) {
       a.pair_ns[2 * idx] = (unsigned)t0;
       a.pair_ns[2 * idx + 1] = (unsigned)(gtimer() - t0);
@@ -716,7 +844,7 @@ __device__ __forceinline__ void run_unit(const FusedArgs& a, int64_t u, const do
 }
 
 __device__ __forceinline__ int64_t plan_units(const FusedArgs& a) {
-  if (a.priced_by_leader) return a.total_rows;
+  if (a.priced_by_leader || a.direct) return a.total_rows;
   return a.total_rows + (a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32);
 }
 
@@ -800,7 +928,7 @@ __global__ void __launch_bounds__(kFusedThreads, 4) fused_kernel(FusedArgs a) {
       return;
     }
     if (item < a.i_exp) node_range(a, item, s_seg.n, &s_nseg, &s_edge);
-    else fanout_range(a, item - a.i_exp, s_seg.f, &s_nseg, &s_edge);
+    else fanout_range<false>(a, item - a.i_exp, s_seg.f, &s_nseg, &s_edge);
   }
 }
 
@@ -837,8 +965,13 @@ __device__ __forceinline__ int find_plan(const int64_t* off, int n, int64_t x, i
 
 // pair forms in the batch: 1 = warp only, 2 = thread only, 0 = mixed;
 // 3 = thread only with 2 CTAs per SM (128 registers: the register form's
-// state without spills)
-template <int kForm>
+// state without spills); 4 = thread form priced from the batch's op lists
+// in the fan-out from the batch's op lists (infer_kernel ran first; the
+// units are node rows only)
+// kPhase (form 5, two launches): 1 = the units only (node rows and table
+// entries, nothing published), 2 = the ranges only (reading what launch 1
+// wrote; the kernel boundary orders them); 3 = both in one launch.
+template <int kForm, int kPhase = 3>
 __global__ void __launch_bounds__(kFusedThreads, kForm == 3 ? 2 : 4)
     fused_batch_kernel(const FusedArgs* __restrict__ args, int n, const int64_t* __restrict__ unit_off,
                        const int64_t* __restrict__ item_off, const int64_t* __restrict__ tab_off, BatchHdr* hdr,
@@ -850,23 +983,45 @@ __global__ void __launch_bounds__(kFusedThreads, kForm == 3 ? 2 : 4)
   } s_seg;
   const int lane = threadIdx.x & 31;
   const int64_t units = unit_off[n];
-  if (threadIdx.x == 0) s_unit = blockIdx.x * (kFusedThreads / 32);  // static first units, as fused_kernel
+  // a warp claims kUC consecutive units at a time: one atomic per chunk and a
+  // plan lookup that mostly stays in the previous plan (measured: with one
+  // unit per claim the counter and the lookups were the top stalls of a
+  // 1,000-plan batch). Node rows (form 4's only units) are short; priced
+  // pairs keep one unit per claim for balance.
+  // Form 5's first launch has nothing else to wait for: its warps stride over
+  // the chunks statically (chunk c, c + warps, ...), no counter at all.
+  constexpr int kUC = kForm == 4 ? 8 : (kForm == 5 ? 4 : 1);
+  const int64_t chunks = (units + kUC - 1) / kUC;
+  if (threadIdx.x == 0) s_unit = blockIdx.x * (kFusedThreads / 32);  // static first chunks, as fused_kernel
   __syncthreads();
-  int64_t u = (int64_t)s_unit + (threadIdx.x >> 5);
+  int64_t c = (int64_t)s_unit + (threadIdx.x >> 5);
   int p = -1;
-  while (u < units) {
-    p = find_plan(unit_off, n, u, p);
-    const FusedArgs& a = args[p];
-    if (kForm == 1 || (kForm == 0 && a.warp_form)) run_unit<true>(a, u - unit_off[p], a.bw_tab);
-    else run_unit<false>(a, u - unit_off[p], a.bw_tab, args);
+  if constexpr (kForm == 5 && (kPhase & 1) != 0) {
+    for (; c < chunks; c += (int64_t)gridDim.x * (kFusedThreads / 32)) {
+      const int64_t u1 = min(units, (c + 1) * kUC);
+      for (int64_t u = c * kUC; u < u1; ++u) {
+        p = find_plan(unit_off, n, u, p);
+        run_unit<false, false, true>(args[p], u - unit_off[p], args[p].bw_tab);
+      }
+    }
+  } else if constexpr ((kPhase & 1) != 0) while (c < chunks) {
+    const int64_t u1 = min(units, (c + 1) * kUC);
+    for (int64_t u = c * kUC; u < u1; ++u) {
+      p = find_plan(unit_off, n, u, p);
+      const FusedArgs& a = args[p];
+      if (kForm == 1 || (kForm == 0 && a.warp_form)) run_unit<true>(a, u - unit_off[p], a.bw_tab);
+      else if (kForm == 4) run_unit<true>(a, u - unit_off[p], a.bw_tab);  // node rows only (a.direct)
+      else if (kForm == 5) run_unit<false, false, true>(a, u - unit_off[p], a.bw_tab);
+      else run_unit<false>(a, u - unit_off[p], a.bw_tab, args);
+    }
     int next = 0;
     if (lane == 0) {
       const int64_t base = (int64_t)gridDim.x * (kFusedThreads / 32);
-      next = base + ld_relaxed(&hdr->unit_head.v) >= units ? INT_MAX : (int)(base + atomicAdd(&hdr->unit_head.v, 1));
+      next = base + ld_relaxed(&hdr->unit_head.v) >= chunks ? INT_MAX : (int)(base + atomicAdd(&hdr->unit_head.v, 1));
     }
-    u = __shfl_sync(0xffffffffu, next, 0);
+    c = __shfl_sync(0xffffffffu, next, 0);
   }
-  {  // every plan's other-parity tables start unset: one slice of the concatenation per CTA
+  if (kForm != 4 && kForm != 5) {  // every plan's other-parity tables start unset: one slice of the concatenation per CTA
     const int64_t total = tab_off[n];
     const int64_t per = (total + gridDim.x - 1) / gridDim.x;
     const int64_t b0 = (int64_t)blockIdx.x * per, b1 = min(b0 + per, total);
@@ -878,14 +1033,16 @@ __global__ void __launch_bounds__(kFusedThreads, kForm == 3 ? 2 : 4)
   }
   const int64_t items = item_off[n];
   int ip = -1;
-  for (int64_t item = blockIdx.x;; item += gridDim.x) {
+  if constexpr ((kPhase & 2) != 0) for (int64_t item = blockIdx.x;; item += gridDim.x) {
     __syncthreads();  // s_seg reuse
     if (item >= items) break;
     ip = find_plan(item_off, n, item, ip);
     const FusedArgs& a = args[ip];
     const int li = (int)(item - item_off[ip]);
-    if (li < a.i_exp) node_range(a, li, s_seg.n, &s_nseg, &s_edge);
-    else fanout_range(a, li - a.i_exp, s_seg.f, &s_nseg, &s_edge);
+    if (li < a.i_exp) node_range<kPhase == 3>(a, li, s_seg.n, &s_nseg, &s_edge);
+    else if (kForm == 4) fanout_range<true>(a, li - a.i_exp, s_seg.f, &s_nseg, &s_edge);
+    else if (kForm == 5) fanout_range<false, false>(a, li - a.i_exp, s_seg.f, &s_nseg, &s_edge);
+    else fanout_range<false>(a, li - a.i_exp, s_seg.f, &s_nseg, &s_edge);
   }
   if (threadIdx.x == 0) {
     __threadfence();
@@ -894,7 +1051,7 @@ __global__ void __launch_bounds__(kFusedThreads, kForm == 3 ? 2 : 4)
   __syncthreads();
   if (s_last) {  // every other CTA has finished: reset every plan and the batch queue
     __threadfence();
-    for (int q = threadIdx.x; q < n; q += kFusedThreads) {
+    for (int q = threadIdx.x; (kPhase & 2) && q < n; q += kFusedThreads) {
       if (err_out) err_out[q] = *args[q].err;  // this launch's error slot of every plan
       reset_plan(args[q]);
     }

@@ -93,6 +93,7 @@ struct Arena {
   size_t h_stage_cap = 0;
   cudaEvent_t stage_done = nullptr;  // the last pack copy out of h_stage
   bool sched_clean = false;  // Sched zero (set up, or left so by the last launch)
+  bool tables_dirty = false; // a launch priced in the fan-out left the class tables un-reset
   int64_t tables_L = -1;     // table layout (doubles per parity) the clean state is for
   size_t sched_bytes = 0;
   bool timeline_set = false;
@@ -176,6 +177,8 @@ struct tp_plan {
   uint64_t shash = 0;         // struct_hash, cached (a plan's structure never changes)
   bool shash_ok = false;
   int resident_blocks = 0;  // persistent grid size (SMs x resident CTAs)
+  std::vector<std::pair<uint64_t, std::vector<int64_t>>> class_keys;  // batches: op-list keys (cached)
+  std::vector<tp_plan*> shards;  // per-device copies of a multi-device build (owned)
 };
 
 namespace {
@@ -632,6 +635,8 @@ struct Builder {
       f.st_r = kFusedThreads % sg.Sw;
       f.base = sg.base;
       f.need = bs.Un * bs.Wn;
+      f.bytes = bs.bytes;
+      f.ovr = bs.has_override;
       p.fsegs.push_back(f);
     }
     p.pair_sig.assign(p.total_pairs, 0);

@@ -11,6 +11,7 @@ There is no CPU path: without the CUDA library or a GPU every call raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Optional, Tuple, Union
 
@@ -229,6 +230,60 @@ class Plan:
         _check(self.lib, self.lib.tp_plan_execute_host(self.handle, C.byref(o), None, C.byref(out)))
         _trim(ct, nn, ne, rows, e1 - e0)
         return ct
+
+
+def _multi(self, devices, records=False, row_min=False, pinned=False) -> CostTensors:
+    """tp_plan_execute_host_multi: the graph's edges in contiguous ranges
+    balanced by aux edges, range i built on devices[i] and its slice copied
+    straight into the host arrays at its offset."""
+    ix = self.index()
+    ne, nn = self.sizes["num_aux_edges"], self.sizes["num_aux_nodes"]
+    n_e = self.flat.num_edges
+    rows = _row_counts(ix, 0, n_e)
+    alloc = _pinned_empty if pinned else (lambda n, dt: np.zeros(n, dt))
+    ct = CostTensors(
+        node_intra_cost_s=alloc(max(nn, 1), np.float64), node_intra_volume_bytes=alloc(max(nn, 1), np.float64),
+        node_memory_bytes=alloc(max(nn, 1), np.float64), edge_cost_s=alloc(max(ne, 1), np.float64),
+        edge_volume_bytes=alloc(max(ne, 1), np.float64), edge_memory_bytes=alloc(max(ne, 1), np.float64),
+        records=alloc(max(ne, 1) * 40, np.uint8) if records else None,
+        row_min_cost_s=alloc(max(rows, 1), np.float64) if row_min else None,
+        row_min_volume_bytes=alloc(max(rows, 1), np.float64) if row_min else None,
+        edge_pair_min_cost_s=alloc(max(n_e, 1), np.float64) if row_min else None,
+        edge_pair_min_volume_bytes=alloc(max(n_e, 1), np.float64) if row_min else None,
+        sizes=dict(self.sizes), **ix)
+    out = cost_struct(ct)
+    devs = np.ascontiguousarray(devices, dtype=np.int32)
+    self._multi_keep = (ct, out, devs)
+    _check(self.lib, self.lib.tp_plan_execute_host_multi(self.handle, abi.ptr(devs, C.c_int32), len(devs), None,
+                                                         C.byref(out)))
+    _trim(ct, nn, ne, rows, n_e)
+    return ct
+
+
+Plan.execute_host_multi = _multi
+
+
+def _export_lp(self, ct: CostTensors, path: str, mode: str = "topology", device_memory=None) -> int:
+    """topoplan::export_lp(formulate(aux, mode, device_memory)) of this build
+    (ct = execute_host's result) written to `path` (tp_plan_export_lp);
+    returns the bytes written."""
+    out = cost_struct(ct)
+    n = C.c_int64()
+    mem = self.topo.device_memory if device_memory is None else device_memory
+    _check(self.lib, self.lib.tp_plan_export_lp(self.handle, C.byref(out), int(mode == "volume"), float(mem),
+                                                os.fsencode(path), C.byref(n)))
+    return n.value
+
+
+Plan.export_lp = _export_lp
+
+
+def build_cost_tensors_multi(graph, topo: ClusterTopology, devices, records=False, row_min=False,
+                             pinned=False) -> CostTensors:
+    """The drop-in for build_auxiliary_graph on several GPUs of this process
+    (tp_plan_execute_host_multi): bit-identical to build_cost_tensors."""
+    plan = Plan(graph, topo, int(devices[0]))
+    return plan.execute_host_multi(devices, records=records, row_min=row_min, pinned=pinned)
 
 
 def _row_counts(ix, e0, e1):
@@ -495,8 +550,9 @@ class DeviceSweep:
         return int(self.node_off[-1])
 
     def launches_per_run(self) -> int:
-        """Kernel launches of the last run (the batch launch counts once)."""
-        return 1 if any(p.last_launches() for p in self.plans) else 0
+        """Kernel launches of the last run: the batch's inference pass and
+        build launch(es) (tp_batch_last_launches)."""
+        return int(self.lib.tp_batch_last_launches(self.device)) if self.plans else 0
 
     def run(self):
         """Rebuild every scenario, asynchronously on `self.main`."""
