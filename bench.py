@@ -366,6 +366,76 @@ def measure_configs(device, K, W, flush, lib):
     return res
 
 
+def measure_edge_sharded(flat, topo, devices, K, W):
+    """ONE build split over several GPUs of this process by edge ranges
+    balanced by aux edges: device i builds its range (device 0
+    also the nodes) into its own memory; a step's device time is the max over
+    the devices of their event-timed launch. e2e: tp_build_cost_tensors_multi
+    (host graph in, every device's slice copied straight into one pinned host
+    array), wall clock."""
+    import torch
+    from paper_2301_04285_b200 import distributed as D, engine as E
+    n = len(devices)
+    plans = [E.Plan(flat, topo, device=d) for d in devices]
+    ix = plans[0].index()
+    ranges = D.partition_edges(D.edge_pair_counts(ix["node_base"], ix["edge_from_op"], ix["edge_to_op"]), n)
+    eb = ix["edge_base"]
+    ne, nn = plans[0].sizes["num_aux_edges"], plans[0].sizes["num_aux_nodes"]
+    st, outs, flush = [], [], []
+    for i, d in enumerate(devices):
+        dev = torch.device("cuda", d)
+        with torch.cuda.device(d):
+            s = torch.cuda.Stream(dev)
+            m = int(eb[ranges[i][1]] - eb[ranges[i][0]])
+            o = {k: torch.empty(max(m, 1), dtype=torch.float64, device=dev)
+                 for k in ("edge_cost_s", "edge_volume_bytes", "edge_memory_bytes")}
+            if i == 0:
+                o.update({k: torch.empty(max(nn, 1), dtype=torch.float64, device=dev)
+                          for k in ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes")})
+            plans[i].upload(s.cuda_stream)
+            st.append(s)
+            outs.append(E.device_cost_struct(o))
+            flush.append(torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev))
+    for d in devices:
+        torch.cuda.synchronize(d)
+    per_step = []
+    for step in range(W + K):
+        evs = []
+        for i, d in enumerate(devices):
+            with torch.cuda.device(d), torch.cuda.stream(st[i]):
+                flush[i].zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st[i])
+                plans[i].execute(outs[i], edge_range=ranges[i], skip_nodes=i != 0, stream=st[i].cuda_stream)
+                b.record(st[i])
+                evs.append((a, b))
+        for d in devices:
+            torch.cuda.synchronize(d)
+        if step >= W:
+            per_step.append(max(a.elapsed_time(b) for a, b in evs))
+    for p in plans:
+        p.check_errors()
+    dev_ms = statistics.median(per_step)
+    # e2e: the single-process multi-GPU one-shot call
+    hv = oneshot_outputs(ne, nn)
+    hs = E.cost_struct(hv)
+    lib = plans[0].lib
+    gd, td = flat.desc(), topo.desc()
+    devs = (C.c_int32 * n)(*devices)
+    ts = []
+    for i in range(max(3, K // 2) + 2):
+        t0 = time.perf_counter()
+        rc = lib.tp_build_cost_tensors_multi(C.byref(gd), C.byref(td), devs, n, None, C.byref(hs))
+        ts.append((time.perf_counter() - t0) * 1e3)
+        assert rc == 0, lib.tp_last_error()
+    warm = ts[2:]
+    return {"devices": list(devices), "edge_ranges": [list(r) for r in ranges], "aux_edges": ne,
+            "build_ms_device": dev_ms, "evals_per_s_device": ne / (dev_ms / 1e3),
+            "e2e": {"build_ms": sum(warm) / len(warm), "build_ms_cold": ts[0], "evals_per_s": ne / (sum(warm) / len(warm) / 1e3),
+                    "how": "tp_build_cost_tensors_multi: each device's slice D2H straight into one pinned host array"},
+            "collective": "none (independent edge ranges)"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -720,6 +790,19 @@ def run_engine(args):
         except Exception as ex:
             configs = {"error": f"{type(ex).__name__}: {ex}"}
     hinfo = host_info(local) if rank == 0 else None
+    # ONE cfg4 build sharded over all N GPUs by edge ranges, from rank 0's process
+    sharded = None
+    if world > 1:
+        # the other ranks wait on a CPU (gloo) barrier: an NCCL barrier's kernel
+        # would spin on the very GPUs rank 0 is timing
+        cpu = dist.new_group(backend="gloo")
+        dist.barrier(group=cpu)
+        if rank == 0:
+            try:
+                sharded = measure_edge_sharded(flat, t, list(range(world)), min(K, 10), 3)
+            except Exception as ex:
+                sharded = {"error": f"{type(ex).__name__}: {ex}"}
+        dist.barrier(group=cpu)
 
     if rank != 0:
         if dist:
@@ -757,6 +840,7 @@ def run_engine(args):
         "host": hinfo,
         "cfg5_sweep": sweep,
         "configs": configs,
+        "edge_sharded": sharded,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(flat, t, ne)

@@ -17,8 +17,7 @@
 // GPU) throw std::runtime_error — there is no CPU fallback.
 //
 // AuxNode::layouts (a per-node std::map the solver never reads) is filled
-// only when `with_layouts` is set, using the reference's own
-// derive_tensor_layouts.
+// only when `with_layouts` is set, by tensor_layouts_b200 below.
 #ifndef TAPS_B200_AUX_GRAPH_B200_HPP_
 #define TAPS_B200_AUX_GRAPH_B200_HPP_
 
@@ -120,6 +119,31 @@ struct PlanGuard {
 
 }  // namespace detail
 
+// AuxNode::layouts of a strategy (the value layout.hpp:333-370 gives): one
+// TensorLayout per tensor NAME -- a name declared twice keeps its last spec --
+// over the strategy's device matrix, each tensor dim mapped to the device dim
+// of the last axis slicing it (axes in order, slices in order), -1 when none
+// does. Called only after a successful build, which has already checked every
+// slice's divisibility (the engine's node phase, TP_E_INDIVISIBLE_EXTENT).
+inline std::map<std::string, topoplan::TensorLayout> tensor_layouts_b200(const topoplan::OperatorNode& op,
+                                                                          const topoplan::OperatorStrategy& st) {
+  std::map<std::string, topoplan::TensorLayout> out;
+  auto put = [&](const topoplan::TensorSpec& t) {
+    topoplan::TensorLayout& l = out[t.name];
+    l.spec = t;
+    l.matrix = st.device_matrix;
+    l.map.entries.assign(t.shape.size(), -1);
+  };
+  for (const auto& t : op.inputs) put(t);
+  for (const auto& t : op.outputs) put(t);
+  for (std::size_t a = 0; a < op.axes.size(); ++a)
+    for (const auto& sl : op.axes[a].slices) {
+      auto it = out.find(sl.tensor);
+      if (it != out.end()) it->second.map.entries[sl.dim] = st.device_map[a];
+    }
+  return out;
+}
+
 // Optional side outputs of the build for the solver's search context
 // (solver.hpp:218-287): per-(edge, producer strategy) row minima (cond_min,
 // rows edge-major) and per-edge minima (pair_min), both cost modes, computed
@@ -220,7 +244,7 @@ inline topoplan::AuxiliaryGraph build_auxiliary_graph_b200(const topoplan::Compu
       node.strategy_index = (int)s;
       node.strategy = tab[s];
       node.strategy.op_id = graph.operators[i].id;
-      if (with_layouts) node.layouts = topoplan::derive_tensor_layouts(graph.operators[i], node.strategy);
+      if (with_layouts) node.layouts = tensor_layouts_b200(graph.operators[i], node.strategy);
       node.intra_cost_s = n_sec[id];
       node.intra_volume_bytes = n_vol[id];
       node.memory_bytes = n_mem[id];

@@ -51,6 +51,15 @@ std::string compare(const AuxiliaryGraph& r, const AuxiliaryGraph& g) {
     if (!same_bits(a.intra_cost_s, b.intra_cost_s) || !same_bits(a.intra_volume_bytes, b.intra_volume_bytes) ||
         !same_bits(a.memory_bytes, b.memory_bytes))
       return "node payload " + std::to_string(i);
+    // AuxNode::layouts: the adapter's own tensor_layouts_b200 against derive_tensor_layouts
+    if (a.layouts.size() != b.layouts.size()) return "node layouts " + std::to_string(i);
+    for (auto ia = a.layouts.begin(), ib = b.layouts.begin(); ia != a.layouts.end(); ++ia, ++ib) {
+      const TensorLayout &x = ia->second, &y = ib->second;
+      if (ia->first != ib->first || x.spec.name != y.spec.name || x.spec.shape != y.spec.shape ||
+          x.spec.element_size != y.spec.element_size || x.matrix.dims != y.matrix.dims ||
+          x.map.entries != y.map.entries)
+        return "node layouts " + std::to_string(i);
+    }
   }
   for (std::size_t e = 0; e < r.edges.size(); ++e) {
     const AuxEdge &a = r.edges[e], &b = g.edges[e];

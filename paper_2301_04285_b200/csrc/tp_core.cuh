@@ -458,19 +458,30 @@ TP_HD int unify_bits(int R, const Lay& F, const Lay& T, const DimT* dt, Unified&
   return kOk;
 }
 
-// infer_ct_allgather_dim (cost_model.hpp:108-135) with cnt[k] = number of
-// working-map entries equal to k.
-TP_HD void ct_gather(const uint8_t* ext, const uint8_t* cnt, int g, int64_t L, int64_t& ct,
-                     int64_t& rep, int64_t& gin) {
-  const int64_t pd = (int64_t)1 << ext[g];
-  int te = 0, re = 0;
-  for (int k = 0; k < g; ++k) {
-    te += ext[k];
-    if (cnt[k] == 0) re += ext[k];
+// ct of an AllGather / AllToAll on a device dim of log2 extent ek at lower
+// device position te, with log2 in-node repetition rexp (cost_model.hpp:108-135).
+TP_HD void ct_fast(int te, int rexp, int ek, int64_t L, int l_log2, int64_t& ct, int64_t& rep, int64_t& gin,
+                   int& rep_e, int& gin_e) {
+  if (l_log2 >= 0) {
+    const int l = l_log2;
+    rep_e = rexp < l ? rexp : l;
+    rep = (int64_t)1 << rep_e;
+    if (te >= l) {
+      gin_e = 0;
+      ct = (int64_t)1 << (l - rep_e);
+    } else {
+      const int rem_e = l - te;
+      gin_e = ek < rem_e ? ek : rem_e;
+      ct = rem_e >= ek ? 0 : ((int64_t)1 << (te - rep_e));
+    }
+    gin = (int64_t)1 << gin_e;
+    return;
   }
+  const int64_t pd = (int64_t)1 << ek;
   const int64_t temp = (int64_t)1 << te;
-  rep = (int64_t)1 << re;
+  rep = (int64_t)1 << rexp;
   if (rep > L) rep = L;
+  rep_e = gin_e = -1;
   if (temp >= L) {
     gin = 1;
     ct = L / rep;
@@ -481,35 +492,64 @@ TP_HD void ct_gather(const uint8_t* ext, const uint8_t* cnt, int g, int64_t L, i
   }
 }
 
-// One AllGather (a2a=false) or AllToAll on device dim g with s = log2 of
-// the working map's shard divisor: returns seconds and adds the plan volume
-// (redistribution.hpp:521-553) to *vol.
-TP_HD double price_op(bool a2a, int g, const uint8_t* ext, const uint8_t* cnt, int s,
-                      double bytes, const Env& env, double* vol, int64_t* ct_out) {
-  const double shard = bytes / exp2d(s);
-  const int64_t p = (int64_t)1 << ext[g];
+// Optional per-build tables: inter/ct for small ct and the AllToAll scale
+// k(p-k)/(p-1), computed with the reference's expressions (tp_warp.cuh
+// make_price_tabs). Null pointers: computed directly.
+struct FastTabs {
+  const double* bw;     // [65]
+  const double* scale;  // [17 * 17]
+};
+
+// One AllGather (a2a = false) or AllToAll, the ONE pricing routine of every
+// pair form (register, warp, array, op lists): cost_model.hpp:176-230 with
+// the plan volume of redistribution.hpp:521-553 added to *vol. Branch-free
+// over the op kinds -- lanes of a warp price ops of different kinds without
+// diverging -- and still the reference's expressions:
+//   AllGather        v = (d-1) * shard            sec = v / B_e(ct)
+//   AllToAll, k >= p v = (d-1)/d * shard          sec = v / intra
+//   AllToAll         v = (d-1)/d * shard          sec = (scale * v) / B_e(c)
+// with shard = bytes / 2^s and (d-1)/d = (d-1) * 2^-ek (both exact), and
+// B_e(0) = intra (the table's entry 0), so one division serves all three.
+TP_HD double price_fast(bool a2a, int te, int rexp, int ek, int s, double bytes, const Env& env, int l_log2,
+                        const FastTabs& tab, double* vol, int64_t* ct_out) {
+  const double shard = bytes * exp2d(-s);  // == bytes / 2^s (exact)
+  const int64_t p = (int64_t)1 << ek;
   const double d = (double)p;
   int64_t ct, rep, gin;
-  ct_gather(ext, cnt, g, env.local, ct, rep, gin);
-  if (!a2a) {
-    *vol += (d - 1) * shard;
-    const double v = (double)(p - 1) * shard;
-    if (ct_out) *ct_out = ct;
-    return v / eff_bw(ct, env);
-  }
-  *vol += (d - 1) / d * shard;
-  const double v = (d - 1) / d * shard;
-  const int64_t k = gin;
-  if (k >= p) {
-    if (ct_out) *ct_out = 0;
-    return v / env.intra;
-  }
-  int64_t c = env.local / (k * rep);
+  int rep_e, gin_e;
+  ct_fast(te, rexp, ek, env.local, l_log2, ct, rep, gin, rep_e, gin_e);
+  const double f = a2a ? (d - 1) * exp2d(-ek) : (d - 1);  // both exact
+  const double v = f * shard;
+  *vol += v;
+  const bool a2a_intra = a2a && gin >= p;
+  int64_t c;  // the AllToAll's inter-node count (cost_model.hpp:213-217)
+  if (l_log2 >= 0) c = gin_e + rep_e <= l_log2 ? ((int64_t)1 << (l_log2 - gin_e - rep_e)) : 0;
+  else c = env.local / (gin * rep);
   if (c < 1) c = 1;
-  if (ct_out) *ct_out = c;
-  const double bw = eff_bw(c, env);
-  const double scale = (double)k * (double)(p - k) / (double)(p - 1);
-  return scale * v / bw;
+  const int64_t cc = a2a ? (a2a_intra ? 0 : c) : ct;
+  if (ct_out) *ct_out = cc;
+  const double bw = a2a_intra ? env.intra : ((tab.bw && cc >= 0 && cc < 65) ? tab.bw[cc] : eff_bw(cc, env));
+  double num = v;
+  if (a2a && !a2a_intra) {
+    const double scale = (tab.scale && gin_e >= 0 && ek < 17) ? tab.scale[gin_e * 17 + ek]
+                                                               : (double)gin * (double)(p - gin) / (double)(p - 1);
+    num = scale * v;
+  }
+  return num / bw;
+}
+
+// One AllGather (a2a=false) or AllToAll on device dim g with s = log2 of
+// the working map's shard divisor (array form): its position is the summed
+// extents below g, its in-node repetition those of the dims below g the
+// working map does not hold (cnt == 0; cost_model.hpp:115-119).
+TP_HD double price_op(bool a2a, int g, const uint8_t* ext, const uint8_t* cnt, int s,
+                      double bytes, const Env& env, double* vol, int64_t* ct_out) {
+  int te = 0, re = 0;
+  for (int k = 0; k < g; ++k) {
+    te += ext[k];
+    if (cnt[k] == 0) re += ext[k];
+  }
+  return price_fast(a2a, te, re, ext[g], s, bytes, env, -1, FastTabs{nullptr, nullptr}, vol, ct_out);
 }
 
 // unify + inference (:419-451, all2all on) + pricing (:533-553,

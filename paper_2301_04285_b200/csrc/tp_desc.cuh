@@ -59,9 +59,12 @@ const char* kind_text(int kind) {
 
 // Every entry point that may switch the current device restores the caller's
 // on return (a PyTorch caller's current device must not follow the plan's).
+// It also drops a stale runtime error left by an earlier unrelated call (the
+// launches below check cudaGetLastError, which would report it as theirs).
 struct DeviceGuard {
   int dev = -1;
   DeviceGuard() {
+    (void)cudaGetLastError();
     if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
   }
   ~DeviceGuard() {

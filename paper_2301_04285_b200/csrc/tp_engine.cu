@@ -82,6 +82,7 @@ tp_status tp_plan_create(const tp_graph_desc* graph, const tp_topology_desc* top
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return set_err(TP_ERR_CUDA, 0, "no CUDA device: the engine has no CPU path");
+  if (device >= ndev || device >= 64) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "device ordinal out of range");
   tp_plan* p = new tp_plan();
   if (device < 0) cudaGetDevice(&p->device);
   else p->device = device;
@@ -1829,6 +1830,7 @@ tp_status tp_plan_export_lp(const tp_plan* p, const tp_cost_tensors* h, int32_t 
 
 tp_status tp_enumerate_strategies(int32_t p, int64_t total_devices, int64_t* count, int64_t* degrees,
                                   int32_t* device_map, int64_t* matrix_dims, int32_t* matrix_depth) {
+  DeviceGuard dg;
   if (p < 1) return set_err(TP_ERR_TOPOPLAN, tpk::kNoAxes, "strategy_count: axis count must be >= 1");
   if (total_devices <= 0 || (total_devices & (total_devices - 1)))
     return set_err(TP_ERR_TOPOPLAN, tpk::kNotPow2, "device count is not a power of two");
@@ -1870,6 +1872,7 @@ tp_status tp_redistribute_batch(const tp_redist_query* q, int32_t n, tp_redist_r
 }
 
 tp_status tp_redistribute_batch_form(const tp_redist_query* q, int32_t n, tp_redist_result* r, int32_t form) {
+  DeviceGuard dg;
   if (n <= 0) return TP_OK;
   if (!q || !r) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null argument");
   int ndev = 0;

@@ -56,80 +56,6 @@ TP_HD void p2set(Pack2& p, int i, int v) {
   else p.hi = (p.hi & clr) | val;
 }
 
-// ct of an AllGather / AllToAll on a device dim of log2 extent ek at lower
-// device position te, with log2 in-node repetition rexp (cost_model.hpp:108-135).
-TP_HD void ct_fast(int te, int rexp, int ek, int64_t L, int l_log2, int64_t& ct, int64_t& rep, int64_t& gin,
-                   int& rep_e, int& gin_e) {
-  if (l_log2 >= 0) {
-    const int l = l_log2;
-    rep_e = rexp < l ? rexp : l;
-    rep = (int64_t)1 << rep_e;
-    if (te >= l) {
-      gin_e = 0;
-      ct = (int64_t)1 << (l - rep_e);
-    } else {
-      const int rem_e = l - te;
-      gin_e = ek < rem_e ? ek : rem_e;
-      ct = rem_e >= ek ? 0 : ((int64_t)1 << (te - rep_e));
-    }
-    gin = (int64_t)1 << gin_e;
-    return;
-  }
-  const int64_t pd = (int64_t)1 << ek;
-  const int64_t temp = (int64_t)1 << te;
-  rep = (int64_t)1 << rexp;
-  if (rep > L) rep = L;
-  rep_e = gin_e = -1;
-  if (temp >= L) {
-    gin = 1;
-    ct = L / rep;
-  } else {
-    const int64_t remain = L / temp;
-    gin = pd < remain ? pd : remain;
-    ct = remain >= pd ? 0 : temp / rep;
-  }
-}
-
-// Optional per-build tables: inter/ct for small ct and the AllToAll scale
-// k(p-k)/(p-1), computed with the reference's expressions (tp_warp.cuh
-// make_price_tabs). Null pointers: computed directly.
-struct FastTabs {
-  const double* bw;     // [65]
-  const double* scale;  // [17 * 17]
-};
-
-TP_HD double price_fast(bool a2a, int te, int rexp, int ek, int s, double bytes, const Env& env, int l_log2,
-                        const FastTabs& tab, double* vol, int64_t* ct_out) {
-  const double shard = bytes * exp2d(-s);  // == bytes / 2^s (exact)
-  const int64_t p = (int64_t)1 << ek;
-  const double d = (double)p;
-  int64_t ct, rep, gin;
-  int rep_e, gin_e;
-  ct_fast(te, rexp, ek, env.local, l_log2, ct, rep, gin, rep_e, gin_e);
-  if (!a2a) {
-    const double v = (d - 1) * shard;  // == (double)(p - 1) * shard
-    *vol += v;
-    if (ct_out) *ct_out = ct;
-    return v / ((tab.bw && ct >= 0 && ct < 65) ? tab.bw[ct] : eff_bw(ct, env));
-  }
-  const double v = ((d - 1) * exp2d(-ek)) * shard;  // == (d - 1) / d * shard (exact)
-  *vol += v;
-  const int64_t k = gin;
-  if (k >= p) {
-    if (ct_out) *ct_out = 0;
-    return v / env.intra;
-  }
-  int64_t c;
-  if (l_log2 >= 0) c = gin_e + rep_e <= l_log2 ? ((int64_t)1 << (l_log2 - gin_e - rep_e)) : 0;
-  else c = env.local / (k * rep);
-  if (c < 1) c = 1;
-  if (ct_out) *ct_out = c;
-  const double bw = (tab.bw && c < 65) ? tab.bw[c] : eff_bw(c, env);
-  const double scale = (tab.scale && gin_e >= 0 && ek < 17) ? tab.scale[gin_e * 17 + ek]
-                                                             : (double)k * (double)(p - k) / (double)(p - 1);
-  return scale * v / bw;
-}
-
 // Scenarios that differ only in their bandwidths share a pair's unification,
 // op sequence, volumes and ct: the op list is inferred once and priced for
 // every member environment (members 1..g-1; member 0 is the caller's own env),

@@ -39,80 +39,14 @@ struct WarpEnv {
   PriceTabs tab;  // may hold null pointers: then computed directly
 };
 
-__device__ __forceinline__ double bw_of(int64_t ct, const WarpEnv& we) {
-  if (we.tab.bw && ct >= 0 && ct < kBwTab) return we.tab.bw[ct];
-  return eff_bw(ct, we.env);
-}
-
-__device__ __forceinline__ void ct_gather_warp(int te, int rexp, int ek, const WarpEnv& we, int64_t& ct,
-                                               int& rep_e, int64_t& rep, int64_t& gin, int& gin_e) {
-  if (we.l_log2 >= 0) {
-    const int l = we.l_log2;
-    rep_e = rexp < l ? rexp : l;
-    rep = (int64_t)1 << rep_e;
-    if (te >= l) {
-      gin_e = 0;
-      ct = (int64_t)1 << (l - rep_e);
-    } else {
-      const int rem_e = l - te;
-      gin_e = ek < rem_e ? ek : rem_e;
-      ct = rem_e >= ek ? 0 : ((int64_t)1 << (te - rep_e));
-    }
-    gin = (int64_t)1 << gin_e;
-    return;
-  }
-  const int64_t L = we.env.local;
-  const int64_t pd = (int64_t)1 << ek;
-  const int64_t temp = (int64_t)1 << te;
-  rep = (int64_t)1 << rexp;
-  if (rep > L) rep = L;
-  rep_e = -1;
-  gin_e = -1;
-  if (temp >= L) {
-    gin = 1;
-    ct = L / rep;
-  } else {
-    const int64_t remain = L / temp;
-    gin = pd < remain ? pd : remain;
-    ct = remain >= pd ? 0 : temp / rep;
-  }
-}
-
 // AllGather / AllToAll on a device dim with log2 extent ek at lower device
 // position te; rexp = log2 of the in-node repetition; s = log2 of the
-// working map's shard divisor (cost_model.hpp:176-225, redistribution.hpp:521-553).
-// Divisions by powers of two are exact, so they are multiplications here.
+// working map's shard divisor: the one pricing routine (tp_core.cuh
+// price_fast, branch-free, so the lanes pricing a batch of mixed ops do not
+// diverge).
 __device__ __forceinline__ double price_op_warp(bool a2a, int te, int rexp, int ek, int s, double bytes,
                                                 const WarpEnv& we, double* vol, int64_t* ct_out) {
-  const double shard = bytes * exp2d(-s);  // == bytes / 2^s
-  const int64_t p = (int64_t)1 << ek;
-  const double d = (double)p;
-  int64_t ct, rep, gin;
-  int rep_e, gin_e;
-  ct_gather_warp(te, rexp, ek, we, ct, rep_e, rep, gin, gin_e);
-  if (!a2a) {
-    const double v = (d - 1) * shard;  // == (double)(p - 1) * shard
-    *vol += v;
-    *ct_out = ct;
-    return v / bw_of(ct, we);
-  }
-  const double v = ((d - 1) * exp2d(-ek)) * shard;  // == (d - 1) / d * shard
-  *vol += v;
-  const int64_t k = gin;
-  if (k >= p) {
-    *ct_out = 0;
-    return v / we.env.intra;
-  }
-  int64_t c;
-  if (we.l_log2 >= 0) c = gin_e + rep_e <= we.l_log2 ? ((int64_t)1 << (we.l_log2 - gin_e - rep_e)) : 0;
-  else c = we.env.local / (k * rep);
-  if (c < 1) c = 1;
-  *ct_out = c;
-  const double bw = bw_of(c, we);
-  const double scale = (we.tab.scale && gin_e >= 0 && ek < kScaleDim)
-                           ? we.tab.scale[gin_e * kScaleDim + ek]
-                           : (double)k * (double)(p - k) / (double)(p - 1);
-  return scale * v / bw;
+  return price_fast(a2a, te, rexp, ek, s, bytes, we.env, we.l_log2, FastTabs{we.tab.bw, we.tab.scale}, vol, ct_out);
 }
 
 // All 32 lanes call this with identical arguments. pf/pt point at the two
