@@ -290,6 +290,21 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n,
                                      tp_cost_tensors* host_outs,
                                      int32_t host_threads, int32_t* status_out);
 
+/* The one-shot sweep: build_auxiliary_graph of every (graphs[i], topos[i])
+ * into HOST pointers host_outs[i] (the six SoA tensors; index_outs optional),
+ * equal to n calls of tp_build_cost_tensors. Pipelined in chunks of
+ * scenarios: the host analysis of chunk k + 1 (host_threads workers) runs
+ * while the device builds chunk k, and when the caller's slices of a tensor
+ * kind are contiguous pinned memory the kernels write them directly (no
+ * staging, no separate D2H), so the host link streams for the whole call.
+ * Returns TP_OK when every scenario succeeded, else the first failing one's
+ * status; status_out[i] per scenario. */
+tp_status tp_build_cost_tensors_batch(const tp_graph_desc* const* graphs,
+                                      const tp_topology_desc* const* topos, int32_t n,
+                                      int32_t device, int32_t host_threads,
+                                      tp_aux_index* index_outs, tp_cost_tensors* host_outs,
+                                      int32_t* status_out);
+
 /* Build every plan into DEVICE pointers device_outs[i] with ONE persistent
  * launch on `stream` (NULL = plans[0]'s stream): the units and output ranges
  * of all plans form one work queue, so the latency-bound pricing of many small

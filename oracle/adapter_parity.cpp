@@ -23,6 +23,7 @@
 #include "topoplan/io.hpp"  // aux_graph_to_json (needs nlohmann/json.hpp, -I in oracle/Makefile)
 #include "taps_b200/aux_graph_b200.hpp"
 #include "taps_b200/export_b200.hpp"
+#include "taps_b200/models_b200.hpp"
 #include "taps_b200/solver_b200.hpp"
 
 using namespace topoplan;
@@ -252,77 +253,29 @@ void check_case(const std::string& name, const ComputationGraph& graph, const Cl
   report(name, err, extra);
 }
 
-ComputationGraph gpt_chain(int layers, std::int64_t hidden, std::int64_t batch, std::int64_t seq) {
-  ModelConfig cfg;
-  cfg.family = ModelFamily::kTransformerLayer;
-  cfg.hidden = hidden;
-  cfg.batch = batch;
-  cfg.seq = seq;
-  const ComputationGraph layer = build_transformer_layer(cfg);
-  ComputationGraph g;
-  std::string x = "x";
-  for (int l = 0; l < layers; ++l) {
-    const std::string p = "L" + std::to_string(l) + ".";
-    auto ren = [&](const std::string& n) { return n == "x" ? x : p + n; };
-    for (OperatorNode op : layer.operators) {
-      op.id = p + op.id;
-      for (auto& t : op.inputs) t.name = ren(t.name);
-      for (auto& t : op.outputs) t.name = ren(t.name);
-      for (auto& a : op.axes)
-        for (auto& s : a.slices) s.tensor = ren(s.tensor);
-      g.operators.push_back(op);
-    }
-    if (l > 0) g.edges.push_back({"L" + std::to_string(l - 1) + ".add2", p + "ln1", x});
-    for (const GraphEdge& e : layer.edges) g.edges.push_back({p + e.from, p + e.to, ren(e.tensor)});
-    x = p + "add2_out";
-  }
-  return g;
-}
-
 // cfg5: the seeded scenario sweep (SURVEY.md §8d draw order). For every
 // sampled scenario both builds go through the reference's own ILP in both
 // cost modes and run_compare's TAPS-vs-volume ratio (pipeline.hpp:152-168:
 // both winners priced in topology mode) must be bit-identical.
 void check_sweep(int count, int every) {
-  std::mt19937_64 rng(0x230104285ull);
+  // the C++ composer (include/taps_b200/models_b200.hpp); every scenario built
+  // on the GPU (the aux-edge total of SURVEY §8d), every `every`-th also by the reference
+  const std::vector<taps_b200::Scenario> sweep = taps_b200::scenario_sweep(count);
   int checked = 0;
+  std::int64_t total = 0;
   for (int i = 0; i < count; ++i) {
-    const std::uint64_t fam = rng() % 4;
-    const int nodes = 1 << (rng() % 4);
-    const double ratio = std::pow(10.0, static_cast<double>(rng() % 1001) / 500.0);
-    ComputationGraph g;
-    std::string name;
-    if (fam == 0) {
-      ModelConfig c;
-      c.family = ModelFamily::kMlpChain;
-      c.layers = 2 + static_cast<std::int64_t>(rng() % 7);
-      c.hidden = static_cast<std::int64_t>(256) << (rng() % 5);
-      c.batch = 256;
-      g = build_graph(c);
-      name = "mlp-chain L" + std::to_string(c.layers) + " h" + std::to_string(c.hidden);
-    } else if (fam == 1) {
-      ModelConfig c;
-      c.family = ModelFamily::kTransformerLayer;
-      c.hidden = static_cast<std::int64_t>(1024) << (rng() % 3);
-      c.batch = 8;
-      c.seq = 512;
-      g = build_graph(c);
-      name = "transformer h" + std::to_string(c.hidden);
-    } else if (fam == 2) {
-      ModelConfig c;
-      c.family = ModelFamily::kAlexnetLike;
-      c.batch = 64;
-      g = build_graph(c);
-      name = "alexnet-like";
-    } else {
-      const int L = 2 + static_cast<int>(rng() % 3);
-      g = gpt_chain(L, 2048, 8, 512);
-      name = "gpt-chain L" + std::to_string(L);
+    const ComputationGraph& g = sweep[i].graph;
+    const ClusterTopology& topo = sweep[i].topo;
+    const int nodes = topo.node_count;
+    const double ratio = sweep[i].ratio;
+    std::string name = sweep[i].family;
+    if (i % every != 0) {
+      total += (std::int64_t)taps_b200::build_auxiliary_graph_b200(g, topo).edges.size();
+      continue;
     }
-    if (i % every != 0) continue;
-    const ClusterTopology topo{nodes, 8, 60e9, 60e9 / ratio, 80e9};
     const AuxiliaryGraph ref = build_auxiliary_graph(g, topo);
     const AuxiliaryGraph gpu = taps_b200::build_auxiliary_graph_b200(g, topo, CostMode::kTopology, -1, true);
+    total += (std::int64_t)gpu.edges.size();
     std::string err = compare(ref, gpu);
     double ratios[2] = {0, 0};
     const AuxiliaryGraph* both[2] = {&ref, &gpu};
@@ -351,7 +304,12 @@ void check_sweep(int count, int every) {
     report("cfg5 #" + std::to_string(i) + " " + name, err, buf);
     ++checked;
   }
-  std::printf("[PARITY] cfg5 sweep: %d scenarios checked\n", checked);
+  std::printf("[PARITY] cfg5 sweep: %d scenarios checked, %lld aux edges over all %d\n", checked, (long long)total,
+              count);
+  if (count == 1000 && total != 16957929) {
+    std::printf("[PARITY] cfg5 sweep aux-edge total differs from SURVEY 8d's 16957929\n");
+    ++failures;
+  }
 }
 
 }  // namespace
@@ -415,11 +373,11 @@ int main(int argc, char** argv) {
   {  // cfg3 (24 layers) on 2/4/8 x 8 and cfg4 (96 layers, 16 x 8) with a fixed node
      // budget and threads=1: a deterministic truncated search, so the
      // selections, objectives, `optimal` flags and LP texts must be identical
-    const ComputationGraph gpt24 = gpt_chain(24, 2048, 8, 512);
+    const ComputationGraph gpt24 = taps_b200::gpt_chain(24, 2048, 8, 512);
     check_case("cfg3 GPT-24 h2048 2x8", gpt24, {2, 8, 60e9, 6e9, 80e9}, SolveCfg{true, 1, 200000});
     check_case("cfg3 GPT-24 h2048 4x8", gpt24, {4, 8, 60e9, 6e9, 80e9}, SolveCfg{true, 1, 20000});
     check_case("cfg3 GPT-24 h2048 8x8 r100", gpt24, {8, 8, 60e9, 0.6e9, 80e9}, SolveCfg{true, 1, 20000});
-    check_case("cfg4 GPT-96 h12288 16x8", gpt_chain(96, 12288, 8, 2048), {16, 8, 60e9, 6e9, 80e9},
+    check_case("cfg4 GPT-96 h12288 16x8", taps_b200::gpt_chain(96, 12288, 8, 2048), {16, 8, 60e9, 6e9, 80e9},
                SolveCfg{true, 1, 5000});
   }
   check_sweep(1000, big ? 10 : 40);

@@ -95,6 +95,9 @@ def reference() -> C.CDLL:
         lib.ref_export_lp.argtypes = [P(abi.tp_graph_desc), P(abi.tp_topology_desc), C.c_int,
                                       C.c_double, C.c_char_p, C.c_int64]
         lib.ref_export_lp.restype = C.c_int64
+        lib.ref_composer_json.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_char_p,
+                                          C.c_int64]
+        lib.ref_composer_json.restype = C.c_int64
         lib.ref_model_json.argtypes = [C.c_char_p, C.c_char_p, C.c_int64]
         lib.ref_model_json.restype = C.c_int64
         lib.ref_last_error.argtypes = []

@@ -25,6 +25,7 @@
 #include "topoplan/solver.hpp"
 
 #include "../include/taps_b200.h"
+#include "../include/taps_b200/models_b200.hpp"  // the C++ composer, checked against models.py
 
 using namespace topoplan;
 
@@ -493,6 +494,37 @@ int64_t ref_export_lp(const tp_graph_desc* g, const tp_topology_desc* t, int mod
     buf[n] = 0;
   }
   return static_cast<std::int64_t>(lp.size());
+}
+
+// The C++ composer of include/taps_b200/models_b200.hpp as JSON: which = 0
+// gpt_chain(a, b, c, d); which = 1 scenario a of scenario_sweep(b) with its
+// topology and ratio appended as {"graph": ..., "topo": [...], "family": ...}.
+int64_t ref_composer_json(int which, int64_t a, int64_t b, int64_t c, int64_t d, char* buf, int64_t cap) {
+  std::string s;
+  int st = guarded([&] {
+    std::ostringstream o;
+    if (which == 0) {
+      dump_graph(o, taps_b200::gpt_chain((int)a, b, c, d));
+    } else {
+      const auto sweep = taps_b200::scenario_sweep((int)b);
+      const auto& sc = sweep.at((size_t)a);
+      o << "{\"graph\":";
+      dump_graph(o, sc.graph);
+      char t[256];
+      std::snprintf(t, sizeof(t), ",\"topo\":[%d,%d,%.17g,%.17g,%.17g],\"ratio\":%.17g,\"family\":\"%s\"}",
+                    sc.topo.node_count, sc.topo.local_device_num, sc.topo.intra_bandwidth, sc.topo.inter_bandwidth,
+                    sc.topo.device_memory, sc.ratio, sc.family.c_str());
+      o << t;
+    }
+    s = o.str();
+  });
+  if (st != TP_OK) return -1;
+  if (buf && cap > 0) {
+    const std::int64_t n = std::min<std::int64_t>(cap - 1, static_cast<std::int64_t>(s.size()));
+    std::memcpy(buf, s.data(), static_cast<std::size_t>(n));
+    buf[n] = 0;
+  }
+  return static_cast<std::int64_t>(s.size());
 }
 
 // models.hpp builders (parse_model_spec + build_graph) as JSON, so the

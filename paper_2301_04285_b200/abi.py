@@ -252,6 +252,9 @@ def load_engine() -> C.CDLL:
     lib.tp_plan_price_assignments.argtypes = [C.c_void_p, P(tp_cost_tensors), _p_i32, C.c_int32, P(C.c_double),
                                               P(C.c_double), P(C.c_double), C.c_void_p]
     lib.tp_plan_price_assignments.restype = C.c_int
+    lib.tp_build_cost_tensors_batch.argtypes = [P(P(tp_graph_desc)), P(P(tp_topology_desc)), C.c_int32, C.c_int32,
+                                                C.c_int32, P(tp_aux_index), P(tp_cost_tensors), _p_i32]
+    lib.tp_build_cost_tensors_batch.restype = C.c_int
     lib.tp_plan_export_lp.argtypes = [C.c_void_p, P(tp_cost_tensors), C.c_int32, C.c_double, C.c_char_p,
                                       P(C.c_int64)]
     lib.tp_plan_export_lp.restype = C.c_int
@@ -284,7 +287,7 @@ EXPORTED_SYMBOLS = (
     "tp_redistribute_batch_form", "tp_plan_set_pair_form", "tp_plan_create_batch", "tp_plan_execute_host_batch",
     "tp_plan_execute_batch", "tp_plan_price_assignments", "tp_plan_set_bandwidth",
     "tp_build_cost_tensors_multi", "tp_plan_execute_host_multi", "tp_batch_last_launches",
-    "tp_plan_export_lp",
+    "tp_plan_export_lp", "tp_build_cost_tensors_batch",
     "tp_last_error", "tp_last_error_kind", "tp_abi_version",
 )
 

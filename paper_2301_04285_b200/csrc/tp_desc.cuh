@@ -178,5 +178,8 @@ constexpr int64_t kWarpPairLimit = 16384;
 #define TP_FAN_PER 1
 #endif
 constexpr int kFanPer = TP_FAN_PER;  // output positions a fan-out thread has in flight
+#ifndef TP_BATCH_FAN_PER
+#define TP_BATCH_FAN_PER 4  // the same for a batch's second launch (fused_batch_kernel<5, 2>)
+#endif
 
 }  // namespace

@@ -628,24 +628,33 @@ namespace {
 struct BatchCtx {
   std::mutex mu;
   std::mutex host_mu;  // the one-shot host batch: output staging below
-  DevBuf d_args, d_hdr, d_err, d_ops;
+  DevBuf d_hdr, d_err, d_ops;
   int64_t last_launches = 0;  // kernel launches of the last batched execute
-  DevBuf out[6];
+  // output staging, double-buffered by slot: chunk k builds into out[k & 1]
+  // while the copy stream drains chunk k - 1 from the other half
+  DevBuf out[2][6];
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t built[2] = {nullptr, nullptr}, drained[2] = {nullptr, nullptr};
   unsigned long long* h_err = nullptr;
   size_t h_err_cap = 0;
-  void* h_stage = nullptr;
-  size_t h_cap = 0;
-  cudaEvent_t copied = nullptr;  // the last staging copy
+  // Host staging is double-buffered by slot: a pipelined sweep packs chunk
+  // k + 1 while chunk k's copies still wait on the stream behind chunk k - 1.
+  // Kernel arguments (per launch) and descriptor packs (per host batch):
+  void* h_stage[2] = {nullptr, nullptr};
+  size_t h_cap[2] = {0, 0};
+  DevBuf d_args[2];
+  cudaEvent_t copied[2] = {nullptr, nullptr};  // the last argument copy out of h_stage[slot]
+  void* h_pack[2] = {nullptr, nullptr};
+  size_t h_pack_cap[2] = {0, 0};
+  DevBuf d_pack[2];
+  cudaEvent_t packed[2] = {nullptr, nullptr};  // the last pack copy out of h_pack[slot]
   bool hdr_clean = false;
   int resident = 0, resident_wide = 0;
+  cudaStream_t stream = nullptr;  // the host batch's stream (every chunk, in order)
   // arenas of the one-shot host batch, by position: scenario i of a batch
   // always gets arena i, so a repeated sweep finds its buffers sized (no
   // cudaMalloc / cudaFree, which would synchronise the device)
   std::vector<Arena*> host_arenas;
-  // batched uploads: every plan's descriptor pack + the set-up jobs, one copy
-  void* h_pack = nullptr;
-  size_t h_pack_cap = 0;
-  DevBuf d_pack;
 };
 BatchCtx g_batch[64];
 
@@ -755,7 +764,7 @@ int batch_mode_of(tp_plan* const* plans, int32_t n, const tp_cost_tensors* outs)
 // error slot (in `live` order via live_out) -- the host batch checks all
 // plans with one copy instead of one synchronising read per plan.
 tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* device_outs, void* stream,
-                             unsigned long long* err_dev, std::vector<int>* live_out) {
+                             unsigned long long* err_dev, std::vector<int>* live_out, int slot = 0) {
   if (n < 0 || (n > 0 && (!plans || !device_outs))) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null batch arrays");
   if (n == 0) return TP_OK;
   for (int i = 0; i < n; ++i)
@@ -890,24 +899,25 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     const size_t cls_b = sizeof(int64_t) * clsops.size(), jobs_b = sizeof(InferJob) * ijobs.size(),
                  ioff_b = sizeof(int64_t) * ioff.size();
     const size_t total = args_b + 3 * off_b + cls_b + jobs_b + ioff_b + sizeof(int32_t) * (glist.size() + 1);
-    if (B.copied) CUDA_TRY(cudaEventSynchronize(B.copied));
-    if (B.h_cap < total) {
-      if (B.h_stage) cudaFreeHost(B.h_stage);
-      B.h_stage = nullptr;
-      B.h_cap = 0;
-      CUDA_TRY(cudaMallocHost(&B.h_stage, total));
-      B.h_cap = total;
+    if (B.copied[slot]) CUDA_TRY(cudaEventSynchronize(B.copied[slot]));
+    if (B.h_cap[slot] < total) {
+      if (B.h_stage[slot]) cudaFreeHost(B.h_stage[slot]);
+      B.h_stage[slot] = nullptr;
+      B.h_cap[slot] = 0;
+      CUDA_TRY(cudaMallocHost(&B.h_stage[slot], total));
+      B.h_cap[slot] = total;
     }
-    CUDA_TRY(B.d_args.ensure(total));
-    FusedArgs* ha = (FusedArgs*)B.h_stage;
-    int64_t* uo = (int64_t*)((char*)B.h_stage + args_b);
+    CUDA_TRY(B.d_args[slot].ensure(total));
+    void* const h_stage = B.h_stage[slot];
+    FusedArgs* ha = (FusedArgs*)h_stage;
+    int64_t* uo = (int64_t*)((char*)h_stage + args_b);
     int64_t* io = uo + (m + 1);
     int64_t* to = io + (m + 1);
     int64_t* hcls = to + (m + 1);
     InferJob* hjobs = (InferJob*)((char*)hcls + cls_b);
     int64_t* hioff = (int64_t*)((char*)hjobs + jobs_b);
     int32_t* hg = (int32_t*)((char*)hioff + ioff_b);
-    const char* dbase = (const char*)B.d_args.p;
+    const char* dbase = (const char*)B.d_args[slot].p;
     const int64_t* dcls = (const int64_t*)(dbase + args_b + 3 * off_b);
     const InferJob* djobs = (const InferJob*)(dbase + args_b + 3 * off_b + cls_b);
     const int64_t* dioff = (const int64_t*)(dbase + args_b + 3 * off_b + cls_b + jobs_b);
@@ -956,9 +966,9 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     }
     if (uo[m] >= (1ll << 30) || io[m] >= (1ll << 30))
       return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many work items in one batch");
-    CUDA_TRY(cudaMemcpyAsync(B.d_args.p, B.h_stage, total, cudaMemcpyHostToDevice, s));
-    if (!B.copied) CUDA_TRY(cudaEventCreateWithFlags(&B.copied, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventRecord(B.copied, s));
+    CUDA_TRY(cudaMemcpyAsync(B.d_args[slot].p, h_stage, total, cudaMemcpyHostToDevice, s));
+    if (!B.copied[slot]) CUDA_TRY(cudaEventCreateWithFlags(&B.copied[slot], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(B.copied[slot], s));
     CUDA_TRY(B.d_hdr.ensure(sizeof(BatchHdr)));
     if (!B.hdr_clean) {
       CUDA_TRY(cudaMemsetAsync(B.d_hdr.p, 0, sizeof(BatchHdr), s));
@@ -971,8 +981,8 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
                                                                     (uint32_t*)B.d_ops.p);
       CUDA_TRY(cudaGetLastError());
     }
-    const FusedArgs* da = (const FusedArgs*)B.d_args.p;
-    const int64_t* duo = (const int64_t*)((const char*)B.d_args.p + args_b);
+    const FusedArgs* da = (const FusedArgs*)B.d_args[slot].p;
+    const int64_t* duo = (const int64_t*)((const char*)B.d_args[slot].p + args_b);
     static const int wide = getenv("TP_BATCH_WIDE") ? atoi(getenv("TP_BATCH_WIDE")) : 0;  // measured: 4 CTAs/SM with spills beats 2 without
     const int form = nwarp == m ? 1 : (nwarp == 0 ? (use_ops ? bmode : (wide ? 3 : 2)) : 0);
     const dim3 gd((unsigned)std::min<int64_t>(grid, form == 3 ? B.resident_wide : B.resident)), bd(kFusedThreads);
@@ -1511,50 +1521,19 @@ tp_status status_from_slot(tp_plan* p, unsigned long long c) {
 
 extern "C" {
 
-// One device: every plan's descriptors uploaded (worker threads, pooled
-// arenas), ONE batched launch into staging buffers, the tensors copied back
-// with one copy per tensor kind when the caller's host slices are contiguous
-// (as engine.Sweep allocates them), and every plan's error read by one copy.
-tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_index* index_outs,
-                                     tp_cost_tensors* host_outs, int32_t host_threads, int32_t* status_out) {
-  DeviceGuard dg;
-  if (n < 0 || (n > 0 && (!plans || !host_outs))) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null batch arrays");
-  if (n == 0) return TP_OK;
-  bool one_device = plans[0] != nullptr;
-  for (int i = 0; one_device && i < n; ++i) one_device = plans[i] && plans[i]->device == plans[0]->device;
-  // the batched launch stages the six SoA tensors only: AuxEdge records and
-  // the solver minima go through one tp_plan_execute_host per plan
-  bool extra = false;
-  for (int i = 0; i < n; ++i) {
-    const tp_cost_tensors& h = host_outs[i];
-    extra |= h.aux_edge_records || h.row_min_cost_s || h.row_min_volume_bytes || h.edge_pair_min_cost_s ||
-             h.edge_pair_min_volume_bytes;
-  }
-  if (!one_device || extra || plans[0]->device < 0 || plans[0]->device >= 64)
-    return execute_host_each(plans, n, index_outs, host_outs, host_threads, status_out);
-  const int device = plans[0]->device;
-  CUDA_TRY(cudaSetDevice(device));
-  BatchCtx& B = g_batch[device];
-  std::lock_guard<std::mutex> hl(B.host_mu);
-  static const bool prof = getenv("TP_PROFILE_HOST") != nullptr;
-  auto clk = [] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
-  const double hb0 = prof ? clk() : 0;
-  // arenas: plans without one borrow the batch's arena of their position
-  std::vector<char> borrowed(n, 0);
-  while ((int)B.host_arenas.size() < n) {
-    Arena* a = new Arena();
-    a->device = device;
-    B.host_arenas.push_back(a);
-  }
-  for (int i = 0; i < n; ++i) {
-    tp_plan* p = plans[i];
-    if (p->arena) continue;
-    p->arena = B.host_arenas[i];
-    p->owns_arena = false;
-    p->uploaded = false;
-    borrowed[i] = 1;
-  }
-  auto give_back = [&]() {
+}  // extern "C"
+
+namespace {
+// One enqueued host batch (a whole call, or one chunk of a pipelined sweep).
+struct HostBatch {
+  tp_plan* const* plans = nullptr;
+  int n = 0;
+  std::vector<char> borrowed;
+  std::vector<int> live;
+  std::vector<BatchErr> errs;
+  int64_t err_base = 0;  // this batch's error slots in B.d_err / B.h_err
+  double t[4] = {0, 0, 0, 0};
+  void give_back() {
     for (int i = 0; i < n; ++i) {
       if (!borrowed[i]) continue;
       tp_plan* p = plans[i];
@@ -1563,61 +1542,95 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
       p->uploaded = false;
       p->range_key = {{-1, -1, -1, -1}};
     }
-  };
-  tp_status st = ensure_stream(plans[0]);
-  if (st) {
-    give_back();
-    return st;
   }
-  cudaStream_t s = plans[0]->arena->stream;
+};
+
+double now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Enqueue a batch of plans of one device without waiting for it: every
+// plan's descriptors uploaded (borrowed arenas: ONE packed copy and two
+// set-up launches) and the batched build on B.stream into the output staging
+// of `slot`; the copies back (one per tensor kind where the caller's slices
+// are contiguous) on B.copy_stream once the build is done. `slot` selects
+// the staging halves, `arena_base` the first borrowed arena, `err_base` the
+// error slots.
+tp_status host_batch_enqueue(BatchCtx& B, int device, tp_plan* const* plans, int32_t n, tp_cost_tensors* host_outs,
+                             int32_t host_threads, int slot, int64_t arena_base, int64_t err_base, HostBatch& H) {
+  static const bool prof = getenv("TP_PROFILE_HOST") != nullptr;
+  H.plans = plans;
+  H.n = n;
+  H.err_base = err_base;
+  H.borrowed.assign(n, 0);
+  H.errs.assign(n, BatchErr{});
+  H.t[0] = prof ? now_us() : 0;
+  while ((int64_t)B.host_arenas.size() < arena_base + n) {
+    Arena* a = new Arena();
+    a->device = device;
+    B.host_arenas.push_back(a);
+  }
+  for (int i = 0; i < n; ++i) {
+    tp_plan* p = plans[i];
+    if (p->arena) continue;
+    p->arena = B.host_arenas[arena_base + i];
+    p->owns_arena = false;
+    p->uploaded = false;
+    H.borrowed[i] = 1;
+  }
+  if (!B.stream) CUDA_TRY(cudaStreamCreateWithFlags(&B.stream, cudaStreamNonBlocking));
+  if (!B.copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&B.copy_stream, cudaStreamNonBlocking));
+  for (int q = 0; q < 2; ++q) {
+    if (!B.built[q]) CUDA_TRY(cudaEventCreateWithFlags(&B.built[q], cudaEventDisableTiming));
+    if (!B.drained[q]) CUDA_TRY(cudaEventCreateWithFlags(&B.drained[q], cudaEventDisableTiming));
+  }
+  cudaStream_t s = B.stream;
+  for (int i = 0; i < n; ++i) {
+    tp_status st = ensure_stream(plans[i]);
+    if (st) return st;
+  }
   // uploads: plans on their own arenas the usual way; the borrowed ones in
   // ONE packed copy (descriptors packed by the workers) and two set-up launches
-  std::vector<BatchErr> errs(n);
   for (int i = 0; i < n; ++i)
-    if (!borrowed[i] && !plans[i]->uploaded) errs[i].take(tp_plan_upload(plans[i], s));
+    if (!H.borrowed[i] && !plans[i]->uploaded) H.errs[i].take(tp_plan_upload(plans[i], s));
   std::vector<int> todo;
   for (int i = 0; i < n; ++i)
-    if (borrowed[i]) todo.push_back(i);
+    if (H.borrowed[i]) todo.push_back(i);
   // as execute_batch_impl will decide (same outputs): with op lists no pair records are read
   const bool direct = batch_mode_of(plans, n, host_outs) != 0;
   std::vector<UploadPrep> U(todo.size());
   const int64_t brange = direct ? batch_range_len(plans, n) : kFusedThreads * kFanPer;  // as execute_batch_impl
   run_pool((int)todo.size(), host_threads,
-           [&](int j, int) { errs[todo[j]].take(upload_prepare(plans[todo[j]], U[j], brange)); }, device);
+           [&](int j, int) { H.errs[todo[j]].take(upload_prepare(plans[todo[j]], U[j], brange)); }, device);
   for (int i = 0; i < n; ++i)
-    if (errs[i].st) {
-      give_back();
-      return batch_status(errs, status_out);
-    }
+    if (H.errs[i].st) return H.errs[i].st;
   if (!todo.empty()) {
     const int m = (int)todo.size();
     std::vector<size_t> off(m + 1, 0);
     for (int j = 0; j < m; ++j) off[j + 1] = off[j] + U[j].pk.total();
     const size_t jobs_at = (off[m] + 255) & ~(size_t)255;
     const size_t total = jobs_at + sizeof(UpJob) * m + 2 * sizeof(int64_t) * (m + 1);
-    if (B.h_pack_cap < total) {
-      if (B.h_pack) cudaFreeHost(B.h_pack);
-      B.h_pack = nullptr;
-      B.h_pack_cap = 0;
-      CUDA_TRY(cudaMallocHost(&B.h_pack, total));
-      B.h_pack_cap = total;
+    if (B.packed[slot]) CUDA_TRY(cudaEventSynchronize(B.packed[slot]));  // h_pack[slot] free again
+    if (B.h_pack_cap[slot] < total) {
+      if (B.h_pack[slot]) cudaFreeHost(B.h_pack[slot]);
+      B.h_pack[slot] = nullptr;
+      B.h_pack_cap[slot] = 0;
+      CUDA_TRY(cudaMallocHost(&B.h_pack[slot], total));
+      B.h_pack_cap[slot] = total;
     }
-    CUDA_TRY(B.d_pack.ensure(total));
-    char* hp = (char*)B.h_pack;
-    char* dp = (char*)B.d_pack.p;
+    CUDA_TRY(B.d_pack[slot].ensure(total));
+    char* hp = (char*)B.h_pack[slot];
+    char* dp = (char*)B.d_pack[slot].p;
     run_pool(
         m, host_threads,
         [&](int j, int) {
           tp_plan* p = plans[todo[j]];
           upload_stage(U[j], hp + off[j], dp + off[j]);
-          errs[todo[j]].take(upload_finish(p, U[j]));
+          H.errs[todo[j]].take(upload_finish(p, U[j]));
         },
         device);
     for (int i = 0; i < n; ++i)
-      if (errs[i].st) {
-        give_back();
-        return batch_status(errs, status_out);
-      }
+      if (H.errs[i].st) return H.errs[i].st;
     UpJob* jobs = (UpJob*)(hp + jobs_at);
     int64_t* so = (int64_t*)(hp + jobs_at + sizeof(UpJob) * m);
     int64_t* po = so + (m + 1);
@@ -1632,23 +1645,22 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
       po[j + 1] = po[j] + p->total_pairs;
     }
     CUDA_TRY(cudaMemcpyAsync(dp, hp, total, cudaMemcpyHostToDevice, s));
+    if (!B.packed[slot]) CUDA_TRY(cudaEventCreateWithFlags(&B.packed[slot], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(B.packed[slot], s));
     for (int j = 0; j < m; ++j) {
-      st = upload_tables(plans[todo[j]], U[j], s);
-      if (st) {
-        give_back();
-        return st;
-      }
+      tp_status st = upload_tables(plans[todo[j]], U[j], s);
+      if (st) return st;
     }
     const UpJob* dj = (const UpJob*)(dp + jobs_at);
     const int64_t* dso = (const int64_t*)(dp + jobs_at + sizeof(UpJob) * m);
     if (so[m] > 0) batch_side_kernel<<<(unsigned)((so[m] + 127) / 128), 128, 0, s>>>(dj, m, dso);
-    // a batch priced in the fan-out reads layouts through the descriptors, not pair records
+    // a batch priced from op lists reads layouts through the descriptors, not pair records
     if (po[m] > 0 && !direct)
       batch_pair_rec_kernel<<<(unsigned)((po[m] + 127) / 128), 128, 0, s>>>(dj, m, dso + (m + 1));
     CUDA_TRY(cudaGetLastError());
   }
-  const double hb1 = prof ? clk() : 0;
-  // device staging of the outputs, one buffer per tensor kind
+  H.t[1] = prof ? now_us() : 0;
+  // outputs: device staging of this slot, drained by the copy stream
   std::vector<int64_t> nn(n), ne(n);
   int64_t tn = 0, te = 0;
   for (int i = 0; i < n; ++i) {
@@ -1657,21 +1669,23 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
     tn += nn[i];
     te += ne[i];
   }
-  double* h_of[6];
   auto host_ptr = [&](int i, int k) -> double* {
     const tp_cost_tensors& h = host_outs[i];
     double* const v[6] = {h.node_intra_cost_s, h.node_intra_volume_bytes, h.node_memory_bytes,
                           h.edge_cost_s,       h.edge_volume_bytes,       h.edge_memory_bytes};
     return v[k];
   };
+  // the build may write this half only after the copy stream drained its last use
+  CUDA_TRY(cudaStreamWaitEvent(s, B.drained[slot], 0));
   std::vector<tp_cost_tensors> dev(n);
   bool want[6];
+  double* h_of[6];
   for (int k = 0; k < 6; ++k) {
     want[k] = false;
     for (int i = 0; i < n; ++i) want[k] |= host_ptr(i, k) != nullptr;
     const int64_t tot = k < 3 ? tn : te;
-    if (want[k]) CUDA_TRY(B.out[k].ensure(sizeof(double) * (size_t)std::max<int64_t>(tot, 1)));
-    h_of[k] = (double*)B.out[k].p;
+    if (want[k]) CUDA_TRY(B.out[slot][k].ensure(sizeof(double) * (size_t)std::max<int64_t>(tot, 1)));
+    h_of[k] = (double*)B.out[slot][k].p;
   }
   {
     int64_t on = 0, oe = 0;
@@ -1683,15 +1697,13 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
       oe += ne[i];
     }
   }
-  CUDA_TRY(B.d_err.ensure(sizeof(unsigned long long) * n));
-  std::vector<int> live;
-  st = execute_batch_impl(plans, n, dev.data(), s, (unsigned long long*)B.d_err.p, &live);
-  if (st) {
-    give_back();
-    return st;
-  }
-  const double hb2 = prof ? clk() : 0;
-  // back to the host: one copy per tensor kind where the caller's slices are contiguous
+  tp_status st = execute_batch_impl(plans, n, dev.data(), s, (unsigned long long*)B.d_err.p + err_base, &H.live, slot);
+  if (st) return st;
+  CUDA_TRY(cudaEventRecord(B.built[slot], s));
+  H.t[2] = prof ? now_us() : 0;
+  // back to the host on the copy stream: one copy per tensor kind where the caller's slices are contiguous
+  cudaStream_t c = B.copy_stream;
+  CUDA_TRY(cudaStreamWaitEvent(c, B.built[slot], 0));
   for (int k = 0; k < 6; ++k) {
     if (!want[k]) continue;
     bool contiguous = true;
@@ -1701,38 +1713,189 @@ tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_in
     }
     const int64_t tot = k < 3 ? tn : te;
     if (contiguous) {
-      if (tot > 0) CUDA_TRY(cudaMemcpyAsync(host_ptr(0, k), h_of[k], sizeof(double) * tot, cudaMemcpyDeviceToHost, s));
+      if (tot > 0) CUDA_TRY(cudaMemcpyAsync(host_ptr(0, k), h_of[k], sizeof(double) * tot, cudaMemcpyDeviceToHost, c));
       continue;
     }
     int64_t off = 0;
     for (int i = 0; i < n; ++i) {
-      const int64_t c = k < 3 ? nn[i] : ne[i];
-      if (host_ptr(i, k) && c > 0)
-        CUDA_TRY(cudaMemcpyAsync(host_ptr(i, k), h_of[k] + off, sizeof(double) * c, cudaMemcpyDeviceToHost, s));
-      off += c;
+      const int64_t cnt = k < 3 ? nn[i] : ne[i];
+      if (host_ptr(i, k) && cnt > 0)
+        CUDA_TRY(cudaMemcpyAsync(host_ptr(i, k), h_of[k] + off, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c));
+      off += cnt;
     }
   }
+  if (!H.live.empty())
+    CUDA_TRY(cudaMemcpyAsync(B.h_err + err_base, (unsigned long long*)B.d_err.p + err_base,
+                             sizeof(unsigned long long) * H.live.size(), cudaMemcpyDeviceToHost, c));
+  CUDA_TRY(cudaEventRecord(B.drained[slot], c));
+  H.t[3] = prof ? now_us() : 0;
+  return TP_OK;
+}
+
+// After the stream has passed the batch: statuses, index outputs, arenas back.
+void host_batch_finish(BatchCtx& B, HostBatch& H, tp_aux_index* index_outs) {
+  std::vector<unsigned long long> slot(H.n, 0);
+  for (size_t k = 0; k < H.live.size(); ++k) slot[H.live[k]] = B.h_err[H.err_base + k];
+  for (int i = 0; i < H.n; ++i) {
+    if (!H.errs[i].st) H.errs[i].take(status_from_slot(H.plans[i], slot[i]));
+    if (index_outs) tp_plan_index(H.plans[i], &index_outs[i]);
+  }
+  H.give_back();
+}
+
+tp_status ensure_err_slots(BatchCtx& B, int64_t n) {
+  CUDA_TRY(B.d_err.ensure(sizeof(unsigned long long) * std::max<int64_t>(n, 1)));
   if (B.h_err_cap < (size_t)n) {
     if (B.h_err) cudaFreeHost(B.h_err);
     B.h_err = nullptr;
     B.h_err_cap = 0;
-    CUDA_TRY(cudaMallocHost(&B.h_err, sizeof(unsigned long long) * n));
+    CUDA_TRY(cudaMallocHost(&B.h_err, sizeof(unsigned long long) * std::max<int64_t>(n, 1)));
     B.h_err_cap = n;
   }
-  if (!live.empty())
-    CUDA_TRY(cudaMemcpyAsync(B.h_err, B.d_err.p, sizeof(unsigned long long) * live.size(), cudaMemcpyDeviceToHost, s));
-  const double hb3 = prof ? clk() : 0;
-  CUDA_TRY(cudaStreamSynchronize(s));
+  return TP_OK;
+}
+
+bool needs_each(tp_plan* const* plans, int32_t n, const tp_cost_tensors* host_outs) {
+  bool one_device = plans[0] != nullptr;
+  for (int i = 0; one_device && i < n; ++i) one_device = plans[i] && plans[i]->device == plans[0]->device;
+  // the batched launch writes the six SoA tensors only: AuxEdge records and
+  // the solver minima go through one tp_plan_execute_host per plan
+  bool extra = false;
+  for (int i = 0; i < n; ++i) {
+    const tp_cost_tensors& h = host_outs[i];
+    extra |= h.aux_edge_records || h.row_min_cost_s || h.row_min_volume_bytes || h.edge_pair_min_cost_s ||
+             h.edge_pair_min_volume_bytes;
+  }
+  return !one_device || extra || plans[0]->device < 0 || plans[0]->device >= 64;
+}
+}  // namespace
+
+extern "C" {
+
+tp_status tp_plan_execute_host_batch(tp_plan* const* plans, int32_t n, tp_aux_index* index_outs,
+                                     tp_cost_tensors* host_outs, int32_t host_threads, int32_t* status_out) {
+  DeviceGuard dg;
+  if (n < 0 || (n > 0 && (!plans || !host_outs))) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null batch arrays");
+  if (n == 0) return TP_OK;
+  if (needs_each(plans, n, host_outs)) return execute_host_each(plans, n, index_outs, host_outs, host_threads, status_out);
+  const int device = plans[0]->device;
+  CUDA_TRY(cudaSetDevice(device));
+  BatchCtx& B = g_batch[device];
+  std::lock_guard<std::mutex> hl(B.host_mu);
+  static const bool prof = getenv("TP_PROFILE_HOST") != nullptr;
+  tp_status st = ensure_err_slots(B, n);
+  if (st) return st;
+  HostBatch H;
+  st = host_batch_enqueue(B, device, plans, n, host_outs, host_threads, 0, 0, 0, H);
+  if (st) {  // a failed upload is its plan's status; anything else fails the call
+    cudaStreamSynchronize(B.stream);
+    if (B.copy_stream) cudaStreamSynchronize(B.copy_stream);
+    H.give_back();
+    for (const BatchErr& e : H.errs)
+      if (e.st) return batch_status(H.errs, status_out);
+    return st;
+  }
+  CUDA_TRY(cudaStreamSynchronize(B.stream));
+  CUDA_TRY(cudaStreamSynchronize(B.copy_stream));
   if (prof)
     fprintf(stderr, "[tp batch] %d plans: uploads %.0f us, launch prep %.0f, copies enqueued %.0f, wait %.0f\n", n,
-            hb1 - hb0, hb2 - hb1, hb3 - hb2, clk() - hb3);
-  std::vector<unsigned long long> slot(n, 0);
-  for (size_t k = 0; k < live.size(); ++k) slot[live[k]] = B.h_err[k];
-  for (int i = 0; i < n; ++i) {
-    errs[i].take(status_from_slot(plans[i], slot[i]));
-    if (index_outs) tp_plan_index(plans[i], &index_outs[i]);
+            H.t[1] - H.t[0], H.t[2] - H.t[1], H.t[3] - H.t[2], now_us() - H.t[3]);
+  host_batch_finish(B, H, index_outs);
+  return batch_status(H.errs, status_out);
+}
+
+tp_status tp_build_cost_tensors_batch(const tp_graph_desc* const* graphs, const tp_topology_desc* const* topos,
+                                      int32_t n, int32_t device, int32_t host_threads, tp_aux_index* index_outs,
+                                      tp_cost_tensors* host_outs, int32_t* status_out) {
+  DeviceGuard dg;
+  if (n < 0 || (n > 0 && (!graphs || !topos || !host_outs)))
+    return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null batch arrays");
+  if (n == 0) return TP_OK;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(TP_ERR_CUDA, 0, "no CUDA device: the engine has no CPU path");
+  if (device < 0) CUDA_TRY(cudaGetDevice(&device));
+  if (device >= ndev || device >= 64) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "device ordinal out of range");
+  CUDA_TRY(cudaSetDevice(device));
+  static const bool prof = getenv("TP_PROFILE_HOST") != nullptr;
+  const double t0 = prof ? now_us() : 0;
+  // Chunks of scenarios in a pipeline: the host analysis of chunk k + 1 (a
+  // thread pool) runs while the GPU builds chunk k and streams it into the
+  // caller's pinned memory; chunk k + 1's uploads queue behind it.
+  static const int env_chunks = getenv("TP_SWEEP_CHUNKS") ? atoi(getenv("TP_SWEEP_CHUNKS")) : 0;
+  const int K = std::max(1, std::min<int>(n, env_chunks > 0 ? env_chunks : std::min(8, std::max(1, n / 96))));
+  std::vector<int> cb(K + 1);
+  for (int k = 0; k <= K; ++k) cb[k] = (int)((int64_t)n * k / K);
+  std::vector<tp_plan*> plans(n, nullptr);
+  std::vector<BatchErr> errs(n);
+  auto create = [&](int k) {
+    run_pool(
+        cb[k + 1] - cb[k], host_threads,
+        [&](int j, int) {
+          const int i = cb[k] + j;
+          tp_plan* p = nullptr;
+          errs[i].take(tp_plan_create(graphs[i], topos[i], device, &p));
+          plans[i] = p;
+        },
+        device);
+  };
+  BatchCtx& B = g_batch[device];
+  std::lock_guard<std::mutex> hl(B.host_mu);
+  tp_status st = ensure_err_slots(B, n);
+  if (st) return st;
+  std::vector<HostBatch> H(K);
+  std::vector<char> enq(K, 0);
+  // per chunk: the analysed plans (a failed analysis keeps its status)
+  std::vector<std::vector<int>> ok_idx(K);
+  std::vector<std::vector<tp_plan*>> ok_plans(K);
+  std::vector<std::vector<tp_cost_tensors>> outs(K);
+  double t_create = 0;
+  create(0);
+  for (int k = 0; k < K; ++k) {
+    for (int i = cb[k]; i < cb[k + 1]; ++i)
+      if (plans[i]) {
+        ok_idx[k].push_back(i);
+        ok_plans[k].push_back(plans[i]);
+        outs[k].push_back(host_outs[i]);
+      }
+    if (!ok_plans[k].empty()) {
+      const int m = (int)ok_plans[k].size();
+      if (needs_each(ok_plans[k].data(), m, outs[k].data())) {
+        st = set_err(TP_ERR_INVALID_ARGUMENT, 0, "tp_build_cost_tensors_batch writes the six SoA tensors only");
+        break;
+      }
+      st = host_batch_enqueue(B, device, ok_plans[k].data(), m, outs[k].data(), host_threads, k & 1, cb[k], cb[k],
+                              H[k]);
+      enq[k] = 1;
+      if (st) break;
+    }
+    if (k + 1 < K) {  // overlaps the GPU work just enqueued
+      const double c0 = prof ? now_us() : 0;
+      create(k + 1);
+      if (prof) t_create += now_us() - c0;
+    }
   }
-  give_back();
+  cudaError_t ce = cudaStreamSynchronize(B.stream);
+  const cudaError_t ce2 = B.copy_stream ? cudaStreamSynchronize(B.copy_stream) : cudaSuccess;
+  if (ce == cudaSuccess) ce = ce2;
+  for (int k = 0; k < K; ++k) {
+    if (!enq[k]) continue;
+    if (st == TP_OK && ce == cudaSuccess) {
+      host_batch_finish(B, H[k], nullptr);
+      for (size_t j = 0; j < ok_idx[k].size(); ++j) errs[ok_idx[k][j]] = H[k].errs[j];
+    } else {
+      H[k].give_back();
+    }
+  }
+  if (index_outs && st == TP_OK)
+    for (int i = 0; i < n; ++i)
+      if (plans[i]) tp_plan_index(plans[i], &index_outs[i]);
+  run_pool(n, host_threads, [&](int i, int) { tp_plan_destroy(plans[i]); }, device);
+  if (prof)
+    fprintf(stderr, "[tp sweep] %d scenarios in %d chunks: %.0f us (overlapped analysis %.0f us)\n", n, K,
+            now_us() - t0, t_create);
+  if (st) return st;
+  if (ce != cudaSuccess) return set_err(TP_ERR_CUDA, 0, cudaGetErrorString(ce));
   return batch_status(errs, status_out);
 }
 

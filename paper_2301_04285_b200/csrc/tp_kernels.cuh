@@ -602,7 +602,11 @@ __device__ __forceinline__ void pair_from_ops(const FusedArgs& a, int64_t idx, c
 // kDirect: priced here from the op lists (no class tables); kWait = false:
 // the tables and rows come from an earlier launch (no counters, no unset
 // checks).
-template <bool kDirect, bool kWait = true>
+// kPer: output positions a thread has in flight (the loads of kPer ids
+// overlap). The single-plan build keeps kFanPer (measured best with its
+// short ranges); a batch's second launch reads its tables from L2 / DRAM and
+// needs more in flight.
+template <bool kDirect, bool kWait = true, int kPer = kFanPer>
 __device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n, int* s_edge) {
   const unsigned long long t0 = a.fan_ns ? gtimer() : 0;
   const int64_t start = a.A0 + (int64_t)item * a.range_len;
@@ -653,11 +657,11 @@ __device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n
     // a division only where the thread enters an edge
     int si = -1;
     int32_t su = 0, sw = 0;
-    for (int64_t o0 = pos + threadIdx.x; o0 < span_end; o0 += kFusedThreads * kFanPer) {
-      double cs[kFanPer], vs[kFanPer], ms[kFanPer];
-      int64_t q[kFanPer];
+    for (int64_t o0 = pos + threadIdx.x; o0 < span_end; o0 += kFusedThreads * kPer) {
+      double cs[kPer], vs[kPer], ms[kPer];
+      int64_t q[kPer];
 #pragma unroll
-      for (int k = 0; k < kFanPer; ++k) {
+      for (int k = 0; k < kPer; ++k) {
         const int64_t o = o0 + (int64_t)k * kFusedThreads;
         q[k] = -1;
         if (o >= span_end) continue;
@@ -699,7 +703,7 @@ __device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n
         }
       }
 #pragma unroll
-      for (int k = 0; k < kFanPer; ++k) {
+      for (int k = 0; k < kPer; ++k) {
         if (q[k] < 0) continue;
         if (!a.general_store) {
           __stcs(a.e_sec + q[k], cs[k]);  // streaming: written once, read by the host
@@ -1041,7 +1045,7 @@ __global__ void __launch_bounds__(kFusedThreads, kForm == 3 ? 2 : 4)
     const int li = (int)(item - item_off[ip]);
     if (li < a.i_exp) node_range<kPhase == 3>(a, li, s_seg.n, &s_nseg, &s_edge);
     else if (kForm == 4) fanout_range<true>(a, li - a.i_exp, s_seg.f, &s_nseg, &s_edge);
-    else if (kForm == 5) fanout_range<false, false>(a, li - a.i_exp, s_seg.f, &s_nseg, &s_edge);
+    else if (kForm == 5) fanout_range<false, false, TP_BATCH_FAN_PER>(a, li - a.i_exp, s_seg.f, &s_nseg, &s_edge);
     else fanout_range<false>(a, li - a.i_exp, s_seg.f, &s_nseg, &s_edge);
   }
   if (threadIdx.x == 0) {

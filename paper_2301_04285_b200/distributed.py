@@ -63,6 +63,41 @@ def estimated_aux_edges(graph, topo) -> int:
     return sum(S[graph.find_op(e.from_)] * S[graph.find_op(e.to)] for e in graph.edges)
 
 
+def estimated_build_cost(graph, topo) -> float:
+    """LPT weight of a sweep scenario on the device: its aux edges (the
+    fan-out, ~12 ns each in a batch) plus its class-table entries (priced from
+    op lists, ~70 ns each, fused_batch_kernel<5, 1> / <5, 2> measured on cfg5).
+    Entries are estimated as S(from) * S(to) per distinct edge class (shape,
+    bytes, slicing of both sides, axis counts -- aux_graph.hpp:257-271's memo
+    key); the engine's layout dedup only makes them fewer."""
+    N = topo.total_devices()
+    S = [strategy_count(op.axis_count(), N) for op in graph.operators]
+    aux = 0
+    classes = set()
+    pairs = 0
+    for e in graph.edges:
+        u, w = graph.find_op(e.from_), graph.find_op(e.to)
+        aux += S[u] * S[w]
+        ou, ow = graph.operators[u], graph.operators[w]
+        spec = [t for t in list(ou.inputs) + list(ou.outputs) if t.name == e.tensor]
+        if not spec:
+            continue
+        t = spec[-1]
+
+        def slicing(op):
+            m = [-1] * len(t.shape)
+            for a, ax in enumerate(op.axes):
+                for sl in ax.slices:
+                    if sl.tensor == e.tensor and 0 <= sl.dim < len(m):
+                        m[sl.dim] = a
+            return tuple(m)
+        key = (len(ou.axes), len(ow.axes), tuple(t.shape), t.element_size, slicing(ou), slicing(ow))
+        if key not in classes:
+            classes.add(key)
+            pairs += S[u] * S[w]
+    return float(aux) + 6.0 * pairs
+
+
 def partition_scenarios(costs: Sequence[float], world: int) -> List[List[int]]:
     """Longest-processing-time assignment of scenarios to ranks; each rank's
     list keeps the scenarios' original order."""

@@ -491,6 +491,24 @@ class Sweep:
                 setattr(ct, k, self._keep[i][k][:n])
         return st
 
+    def build(self, raise_errors: bool = True):
+        """Analyse and build every scenario in one pipelined call
+        (tp_build_cost_tensors_batch): the host analysis of one chunk of
+        scenarios overlaps the device build of the previous one, and the
+        pinned output slices from allocate() are written by the kernels
+        directly. Needs allocate() (the output sizes) from an earlier create();
+        the plans of that create are not used."""
+        st = self.lib.tp_build_cost_tensors_batch(self._gp, self._tp, len(self), self.device, self.host_threads,
+                                                  self._ix, self._cs, abi.ptr(self.status, C.c_int32))
+        if raise_errors:
+            _check(self.lib, st)
+        for i, ct in enumerate(self.results):
+            f = self.flats[i]
+            for k, n in (("edge_from_op", f.num_edges), ("edge_to_op", f.num_edges), ("in_degree", f.num_ops),
+                         ("out_degree", f.num_ops), ("topo_order", f.num_ops)):
+                setattr(ct, k, self._keep[i][k][:n])
+        return st
+
     @property
     def num_aux_edges(self) -> int:
         return int(self._outs[2][-1]) if self._outs else 0
@@ -540,6 +558,24 @@ class DeviceSweep:
             sl = self.result(i)
             self._structs[i] = device_cost_struct({k: v for k, v in sl.items() if v.numel()})
         torch.cuda.synchronize(dev)
+
+    def build(self, raise_errors: bool = True):
+        """Analyse and build every scenario in one pipelined call
+        (tp_build_cost_tensors_batch): the host analysis of one chunk of
+        scenarios overlaps the device build of the previous one, and the
+        pinned output slices from allocate() are written by the kernels
+        directly. Needs allocate() (the output sizes) from an earlier create();
+        the plans of that create are not used."""
+        st = self.lib.tp_build_cost_tensors_batch(self._gp, self._tp, len(self), self.device, self.host_threads,
+                                                  self._ix, self._cs, abi.ptr(self.status, C.c_int32))
+        if raise_errors:
+            _check(self.lib, st)
+        for i, ct in enumerate(self.results):
+            f = self.flats[i]
+            for k, n in (("edge_from_op", f.num_edges), ("edge_to_op", f.num_edges), ("in_degree", f.num_ops),
+                         ("out_degree", f.num_ops), ("topo_order", f.num_ops)):
+                setattr(ct, k, self._keep[i][k][:n])
+        return st
 
     @property
     def num_aux_edges(self) -> int:

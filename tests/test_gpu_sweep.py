@@ -258,3 +258,36 @@ def test_batch_modes_match_oracle(mode):
                        text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert "mode ok" in r.stdout
+
+
+def test_one_shot_pipelined_sweep(sweep1000):
+    """tp_build_cost_tensors_batch: analysis and build pipelined in chunks,
+    kernels writing the pinned slices directly -- every scenario's tensors
+    equal the oracle's; pageable slices (staged) too; errors per scenario."""
+    scen = sweep1000[:300]
+    pairs = [(G.flatten(s.graph), s.topo) for s in scen]
+    for pinned in (True, False):
+        sw = engine.Sweep(pairs, device=0, host_threads=4)
+        sw.create()
+        sw.allocate(pinned=pinned)
+        sw.destroy()  # build() analyses on its own
+        for k in FIELDS:
+            for r in sw.results:
+                getattr(r, k)[:] = np.nan
+        sw.build()
+        assert not sw.status.any()
+        for i in list(range(0, 300, 23)) + [299]:
+            same(sw.results[i], B.oracle_build(*pairs[i]), f"scenario {i} pinned={pinned}")
+    a = M.pointwise_op("a", "x", "y", 8, 8)
+    b = M.pointwise_op("b", "y", "x", 8, 8)
+    cycle = G.ComputationGraph([a, b], [G.GraphEdge("a", "b", "y"), G.GraphEdge("b", "a", "x")])
+    g1, t1 = M.cfg1()
+    mixed = [(G.flatten(g1), t1), (G.flatten(cycle), G.ClusterTopology(1, 2, 60e9, 60e9, 32e9))] + pairs[:200]
+    sw = engine.Sweep(mixed, device=0, host_threads=4)
+    sw.create(raise_errors=False)
+    sw.allocate(pinned=True)
+    st = sw.build(raise_errors=False)
+    assert st == abi.TP_ERR_TOPOPLAN
+    assert sw.status[1] == abi.TP_ERR_TOPOPLAN and sw.status[0] == 0 and not sw.status[2:].any()
+    same(sw.results[0], B.oracle_build(*mixed[0]), "cfg1 beside a cycle")
+    same(sw.results[150], B.oracle_build(*mixed[150]), "scenario 148 beside a cycle")

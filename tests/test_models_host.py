@@ -87,3 +87,26 @@ def test_flatten_interns_names():
     assert list(f.op_tensor_begin) == [0, 3, 5, 8]
     assert list(f.op_axis_begin) == [0, 3, 5, 8]
     assert f.names["x1"] == f.edge_tensor[0]
+
+
+def composer_json(which, a, b, c=0, d=0):
+    lib = B.reference()
+    n = lib.ref_composer_json(which, a, b, c, d, None, 0)
+    assert n >= 0, lib.ref_last_error()
+    buf = C.create_string_buffer(n + 1)
+    lib.ref_composer_json(which, a, b, c, d, buf, n + 1)
+    return json.loads(buf.value.decode())
+
+
+@pytest.mark.skipif(not B.have_reference(), reason="oracle/_ref not built")
+def test_cpp_composer_matches_python():
+    """include/taps_b200/models_b200.hpp (the C++ callers' composer) builds the
+    same GPT chains and the same cfg5 scenarios as models.py."""
+    assert composer_json(0, 3, 256, 2, 16) == as_json(M.build_gpt_chain(3, 256, 2, 16))
+    sweep = M.scenario_sweep(1000)
+    for i in (0, 1, 2, 3, 5, 8, 13, 21, 34, 55, 89, 144, 233, 377, 610, 987, 999):
+        j = composer_json(1, i, 1000)
+        s = sweep[i]
+        assert j["graph"] == as_json(s.graph), i
+        t = s.topo
+        assert j["topo"] == [t.node_count, t.local_device_num, t.intra_bandwidth, t.inter_bandwidth, t.device_memory]
