@@ -576,18 +576,31 @@ def measure_sweep(args, rank, world, local, dist, K, W, with_clocks=False, with_
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    # the batch's kernels bracketed by events the engine records just before
+    # its first launch and after its last (tp_batch_set_profile_events): the
+    # device work of a step without the host's enqueue time; the outer pair
+    # (around the whole run() call) is reported beside it
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    with torch.cuda.stream(ds.main):
+        for a, b in kev:  # materialise the cudaEvent_t handles
+            a.record(ds.main)
+            b.record(ds.main)
+    torch.cuda.synchronize()
     for i in range(K):
         with torch.cuda.stream(ds.main):
             flush.zero_()
+        ds.set_profile_events(*kev[i])
         ev[i][0].record(ds.main)
         ds.run()
         ev[i][1].record(ds.main)
+    ds.set_profile_events(None, None)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     launches = ds.launches_per_run()
-    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    outer_ms = sum(a.elapsed_time(b) for a, b in ev)
+    dev_ms = sum(a.elapsed_time(b) for a, b in kev)
     t_max = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
@@ -637,8 +650,8 @@ def measure_sweep(args, rank, world, local, dist, K, W, with_clocks=False, with_
         traffic = traffic * int(eoff[-1]) / traffic_edges  # the capture covers all 1,000 scenarios on one GPU
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
+        "ms_per_step": dev_ms / K, "ms_per_step_outer": outer_ms / K, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "cfg5", "desc": "1,000 seeded (model, mesh, bandwidth-ratio) scenarios, "
                    "LPT-sharded over ranks (SURVEY §8d)", "scenarios_rank0": len(pairs),
                    "aux_edges_total": total_evals, "class_pairs_rank0": pair_evals,
@@ -787,7 +800,7 @@ def run_engine(args):
             sl = measure_sweep(args, rank, world, local, dist, min(K, 10), W,
                                with_cpu=world == 1 and not args.no_cpu_baseline)
             if sl is not None:
-                sweep = {k: sl[k] for k in ("value", "unit", "ms_per_step", "scaling")}
+                sweep = {k: sl[k] for k in ("value", "unit", "ms_per_step", "ms_per_step_outer", "scaling")}
                 sweep.update(config=sl["config"], e2e=sl["e2e"], roofline=sl["roofline"],
                              gpu_launches=sl["gpu_launches"], cpu_baseline=sl.get("cpu_baseline"))
         except Exception as ex:  # the headline line must still be printed

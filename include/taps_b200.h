@@ -318,6 +318,12 @@ tp_status tp_plan_execute_batch(tp_plan* const* plans, int32_t n,
 /* Kernel launches of the last batched execute on `device` (the inference
  * pass and the build launches of all its plans together). */
 int64_t tp_batch_last_launches(int32_t device);
+/* Optional cudaEvent_t pair recorded on the launch stream of every batched
+ * execute on `device`, immediately before its first kernel (the inference
+ * pass) and after its last (the launches are enqueued back to back, so the
+ * pair times the batch's device work without the host's preparation); NULL
+ * disables. */
+tp_status tp_batch_set_profile_events(int32_t device, void* start_event, void* stop_event);
 
 /* price_assignment (aux_graph.hpp:326-348) of k strategy assignments on the
  * device, both cost modes at once: assignments [k * num_ops] (the strategy

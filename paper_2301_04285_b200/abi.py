@@ -258,6 +258,8 @@ def load_engine() -> C.CDLL:
     lib.tp_plan_export_lp.argtypes = [C.c_void_p, P(tp_cost_tensors), C.c_int32, C.c_double, C.c_char_p,
                                       P(C.c_int64)]
     lib.tp_plan_export_lp.restype = C.c_int
+    lib.tp_batch_set_profile_events.argtypes = [C.c_int32, C.c_void_p, C.c_void_p]
+    lib.tp_batch_set_profile_events.restype = C.c_int
     lib.tp_batch_last_launches.argtypes = [C.c_int32]
     lib.tp_batch_last_launches.restype = C.c_int64
     lib.tp_build_cost_tensors_multi.argtypes = [P(tp_graph_desc), P(tp_topology_desc), _p_i32, C.c_int32,
@@ -288,6 +290,7 @@ EXPORTED_SYMBOLS = (
     "tp_plan_execute_batch", "tp_plan_price_assignments", "tp_plan_set_bandwidth",
     "tp_build_cost_tensors_multi", "tp_plan_execute_host_multi", "tp_batch_last_launches",
     "tp_plan_export_lp", "tp_build_cost_tensors_batch",
+    "tp_batch_set_profile_events",
     "tp_last_error", "tp_last_error_kind", "tp_abi_version",
 )
 

@@ -48,6 +48,8 @@
 #include <unordered_map>
 #include <vector>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <thread>
 
@@ -634,6 +636,7 @@ struct BatchCtx {
   // while the copy stream drains chunk k - 1 from the other half
   DevBuf out[2][6];
   cudaStream_t copy_stream = nullptr;
+  cudaEvent_t prof_start = nullptr, prof_stop = nullptr;  // tp_batch_set_profile_events
   cudaEvent_t built[2] = {nullptr, nullptr}, drained[2] = {nullptr, nullptr};
   unsigned long long* h_err = nullptr;
   size_t h_err_cap = 0;
@@ -764,7 +767,8 @@ int batch_mode_of(tp_plan* const* plans, int32_t n, const tp_cost_tensors* outs)
 // error slot (in `live` order via live_out) -- the host batch checks all
 // plans with one copy instead of one synchronising read per plan.
 tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* device_outs, void* stream,
-                             unsigned long long* err_dev, std::vector<int>* live_out, int slot = 0) {
+                             unsigned long long* err_dev, std::vector<int>* live_out, int slot = 0,
+                             int64_t min_range = 0) {
   if (n < 0 || (n > 0 && (!plans || !device_outs))) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null batch arrays");
   if (n == 0) return TP_OK;
   for (int i = 0; i < n; ++i)
@@ -786,7 +790,7 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
   for (int i = 0; i < n; ++i) plans[i]->in_big_batch = batch_pairs > kWarpPairLimit;
   const int bmode = batch_mode_of(plans, n, device_outs);
   const bool use_ops = bmode != 0;
-  const int64_t brange = bmode ? batch_range_len(plans, n) : kFusedThreads * kFanPer;
+  const int64_t brange = min_range > 0 ? min_range : (bmode ? batch_range_len(plans, n) : kFusedThreads * kFanPer);
   for (int i = 0; i < n; ++i) {
     tp_plan* p = plans[i];
     st = ensure_stream(p);
@@ -976,6 +980,7 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     }
     const int64_t blocks_needed = std::max<int64_t>(io[m], (uo[m] + 7) / 8);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(blocks_needed, B.resident));
+    if (B.prof_start) CUDA_TRY(cudaEventRecord(B.prof_start, s));  // the launches follow back to back
     if (use_ops && n_infer > 0) {  // the batch's inference pass, before the build
       infer_kernel<<<(unsigned)((n_infer + 127) / 128), 128, 0, s>>>(djobs, (int)ijobs.size(), dioff,
                                                                     (uint32_t*)B.d_ops.p);
@@ -1000,6 +1005,7 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
       fused_batch_kernel<5, 2><<<g2, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
     }
     else fused_batch_kernel<0><<<gd, bd, kMsecBytes, s>>>(da, m, duo, dio, dto, hd, err_dev);
+    if (B.prof_stop) CUDA_TRY(cudaEventRecord(B.prof_stop, s));
     B.last_launches = (use_ops && n_infer > 0 ? 1 : 0) + (form == 5 ? 2 : 1);
     if (cudaPeekAtLastError() != cudaSuccess) {
       B.hdr_clean = false;
@@ -1029,6 +1035,13 @@ extern "C" {
 tp_status tp_plan_execute_batch(tp_plan* const* plans, int32_t n, tp_cost_tensors* device_outs, void* stream) {
   DeviceGuard dg;
   return execute_batch_impl(plans, n, device_outs, stream, nullptr, nullptr);
+}
+
+tp_status tp_batch_set_profile_events(int32_t device, void* start_event, void* stop_event) {
+  if (device < 0 || device >= 64) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "device ordinal out of range");
+  g_batch[device].prof_start = (cudaEvent_t)start_event;
+  g_batch[device].prof_stop = (cudaEvent_t)stop_event;
+  return TP_OK;
 }
 
 int64_t tp_batch_last_launches(int32_t device) {
@@ -1526,6 +1539,7 @@ extern "C" {
 namespace {
 // One enqueued host batch (a whole call, or one chunk of a pipelined sweep).
 struct HostBatch {
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // TP_PROFILE_HOST: compute start, built, drained
   tp_plan* const* plans = nullptr;
   int n = 0;
   std::vector<char> borrowed;
@@ -1556,13 +1570,16 @@ double now_us() {
 // are contiguous) on B.copy_stream once the build is done. `slot` selects
 // the staging halves, `arena_base` the first borrowed arena, `err_base` the
 // error slots.
+// `pre` (the pipelined sweep): every plan already on its borrowed arena with
+// its descriptors prepared (upload_prepare with range length `min_range`).
 tp_status host_batch_enqueue(BatchCtx& B, int device, tp_plan* const* plans, int32_t n, tp_cost_tensors* host_outs,
-                             int32_t host_threads, int slot, int64_t arena_base, int64_t err_base, HostBatch& H) {
+                             int32_t host_threads, int slot, int64_t arena_base, int64_t err_base, HostBatch& H,
+                             std::vector<UploadPrep>* pre = nullptr, int64_t min_range = 0) {
   static const bool prof = getenv("TP_PROFILE_HOST") != nullptr;
   H.plans = plans;
   H.n = n;
   H.err_base = err_base;
-  H.borrowed.assign(n, 0);
+  H.borrowed.assign(n, pre ? 1 : 0);
   H.errs.assign(n, BatchErr{});
   H.t[0] = prof ? now_us() : 0;
   while ((int64_t)B.host_arenas.size() < arena_base + n) {
@@ -1570,7 +1587,7 @@ tp_status host_batch_enqueue(BatchCtx& B, int device, tp_plan* const* plans, int
     a->device = device;
     B.host_arenas.push_back(a);
   }
-  for (int i = 0; i < n; ++i) {
+  for (int i = 0; i < n && !pre; ++i) {
     tp_plan* p = plans[i];
     if (p->arena) continue;
     p->arena = B.host_arenas[arena_base + i];
@@ -1598,10 +1615,15 @@ tp_status host_batch_enqueue(BatchCtx& B, int device, tp_plan* const* plans, int
     if (H.borrowed[i]) todo.push_back(i);
   // as execute_batch_impl will decide (same outputs): with op lists no pair records are read
   const bool direct = batch_mode_of(plans, n, host_outs) != 0;
-  std::vector<UploadPrep> U(todo.size());
-  const int64_t brange = direct ? batch_range_len(plans, n) : kFusedThreads * kFanPer;  // as execute_batch_impl
-  run_pool((int)todo.size(), host_threads,
-           [&](int j, int) { H.errs[todo[j]].take(upload_prepare(plans[todo[j]], U[j], brange)); }, device);
+  std::vector<UploadPrep> U_own;
+  const int64_t brange =
+      min_range > 0 ? min_range : (direct ? batch_range_len(plans, n) : kFusedThreads * kFanPer);  // as execute_batch_impl
+  if (!pre) {
+    U_own.resize(todo.size());
+    run_pool((int)todo.size(), host_threads,
+             [&](int j, int) { H.errs[todo[j]].take(upload_prepare(plans[todo[j]], U_own[j], brange)); }, device);
+  }
+  std::vector<UploadPrep>& U = pre ? *pre : U_own;
   for (int i = 0; i < n; ++i)
     if (H.errs[i].st) return H.errs[i].st;
   if (!todo.empty()) {
@@ -1677,6 +1699,10 @@ tp_status host_batch_enqueue(BatchCtx& B, int device, tp_plan* const* plans, int
   };
   // the build may write this half only after the copy stream drained its last use
   CUDA_TRY(cudaStreamWaitEvent(s, B.drained[slot], 0));
+  if (prof) {
+    for (auto& e : H.ev) CUDA_TRY(cudaEventCreate(&e));
+    CUDA_TRY(cudaEventRecord(H.ev[0], s));
+  }
   std::vector<tp_cost_tensors> dev(n);
   bool want[6];
   double* h_of[6];
@@ -1697,7 +1723,8 @@ tp_status host_batch_enqueue(BatchCtx& B, int device, tp_plan* const* plans, int
       oe += ne[i];
     }
   }
-  tp_status st = execute_batch_impl(plans, n, dev.data(), s, (unsigned long long*)B.d_err.p + err_base, &H.live, slot);
+  tp_status st = execute_batch_impl(plans, n, dev.data(), s, (unsigned long long*)B.d_err.p + err_base, &H.live, slot,
+                                    min_range);
   if (st) return st;
   CUDA_TRY(cudaEventRecord(B.built[slot], s));
   H.t[2] = prof ? now_us() : 0;
@@ -1728,6 +1755,10 @@ tp_status host_batch_enqueue(BatchCtx& B, int device, tp_plan* const* plans, int
     CUDA_TRY(cudaMemcpyAsync(B.h_err + err_base, (unsigned long long*)B.d_err.p + err_base,
                              sizeof(unsigned long long) * H.live.size(), cudaMemcpyDeviceToHost, c));
   CUDA_TRY(cudaEventRecord(B.drained[slot], c));
+  if (prof) {
+    CUDA_TRY(cudaEventRecord(H.ev[1], s));
+    CUDA_TRY(cudaEventRecord(H.ev[2], c));
+  }
   H.t[3] = prof ? now_us() : 0;
   return TP_OK;
 }
@@ -1828,6 +1859,21 @@ tp_status tp_build_cost_tensors_batch(const tp_graph_desc* const* graphs, const 
   for (int k = 0; k <= K; ++k) cb[k] = (int)((int64_t)n * k / K);
   std::vector<tp_plan*> plans(n, nullptr);
   std::vector<BatchErr> errs(n);
+  BatchCtx& B = g_batch[device];
+  std::lock_guard<std::mutex> hl(B.host_mu);
+  tp_status st = ensure_err_slots(B, n);
+  if (st) return st;
+  while ((int64_t)B.host_arenas.size() < n) {  // scenario i borrows arena i
+    Arena* a = new Arena();
+    a->device = device;
+    B.host_arenas.push_back(a);
+  }
+  // The analysis of a scenario also puts it on its arena and prepares its
+  // descriptor pack (a fixed range length for the whole sweep, so the pack's
+  // range table is the one the launch uses); chunk k's enqueue then only
+  // copies the packs and launches.
+  constexpr int64_t kSweepRange = 1024;
+  std::vector<UploadPrep> prep(n);
   auto create = [&](int k) {
     run_pool(
         cb[k + 1] - cb[k], host_threads,
@@ -1835,65 +1881,170 @@ tp_status tp_build_cost_tensors_batch(const tp_graph_desc* const* graphs, const 
           const int i = cb[k] + j;
           tp_plan* p = nullptr;
           errs[i].take(tp_plan_create(graphs[i], topos[i], device, &p));
+          if (p) {
+            p->arena = B.host_arenas[i];
+            p->owns_arena = false;
+            p->uploaded = false;
+            tp_status s2 = ensure_stream(p);
+            if (!s2) s2 = upload_prepare(p, prep[i], kSweepRange);
+            if (s2) {
+              errs[i].take(s2);
+              p->arena = nullptr;
+              p->owns_arena = true;
+              tp_plan_destroy(p);
+              p = nullptr;
+            }
+          }
           plans[i] = p;
         },
         device);
   };
-  BatchCtx& B = g_batch[device];
-  std::lock_guard<std::mutex> hl(B.host_mu);
-  tp_status st = ensure_err_slots(B, n);
-  if (st) return st;
   std::vector<HostBatch> H(K);
   std::vector<char> enq(K, 0);
   // per chunk: the analysed plans (a failed analysis keeps its status)
   std::vector<std::vector<int>> ok_idx(K);
   std::vector<std::vector<tp_plan*>> ok_plans(K);
   std::vector<std::vector<tp_cost_tensors>> outs(K);
+  std::vector<std::vector<UploadPrep>> preps(K);
   double t_create = 0;
-  create(0);
+  std::vector<double> tk(2 * K + 2, 0);  // per chunk: analysed, enqueued (TP_PROFILE_HOST)
+  // The analysis runs ahead on its own thread (holding the worker pool) while
+  // this thread enqueues the analysed chunks in order -- their set-up then
+  // runs inline here instead of waiting for the pool.
+  std::mutex amu;
+  std::condition_variable acv;
+  int analysed = 0;  // chunks [0, analysed) are ready
+  bool stop = false;
+  // retire[k]: chunk k's statuses taken and its plans destroyed (by the
+  // analyser once its copies completed, overlapping the later chunks)
+  std::vector<char> retired(K, 0);
+  std::vector<cudaEvent_t> done(K, nullptr);
+  for (auto& e : done) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  bool main_done = false, failed = false;
+  auto destroy_chunk = [&](int k) {
+    run_pool(cb[k + 1] - cb[k], host_threads, [&](int j, int) {
+      tp_plan*& p = plans[cb[k] + j];
+      tp_plan_destroy(p);
+      p = nullptr;
+    }, device);
+  };
+  std::thread analyser([&] {
+    cudaSetDevice(device);
+    for (int k = 0; k < K; ++k) {
+      {
+        std::lock_guard<std::mutex> lk(amu);
+        if (stop) break;
+      }
+      const double c0 = prof ? now_us() : 0;
+      create(k);
+      std::lock_guard<std::mutex> lk(amu);
+      if (prof) {
+        t_create += now_us() - c0;
+        tk[2 * k] = now_us() - t0;
+      }
+      analysed = k + 1;
+      acv.notify_all();
+    }
+    for (int k = 0; k < K; ++k) {  // then retire the chunks as their copies complete
+      {
+        std::unique_lock<std::mutex> lk(amu);
+        acv.wait(lk, [&] { return enq[k] || main_done; });
+        if (!enq[k] || failed) break;
+      }
+      if (cudaEventSynchronize(done[k]) != cudaSuccess) break;
+      host_batch_finish(B, H[k], nullptr);
+      for (size_t j = 0; j < ok_idx[k].size(); ++j) {
+        errs[ok_idx[k][j]] = H[k].errs[j];
+        if (index_outs) tp_plan_index(plans[ok_idx[k][j]], &index_outs[ok_idx[k][j]]);
+      }
+      destroy_chunk(k);
+      retired[k] = 1;
+    }
+  });
   for (int k = 0; k < K; ++k) {
+    {
+      std::unique_lock<std::mutex> lk(amu);
+      acv.wait(lk, [&] { return analysed > k; });
+    }
     for (int i = cb[k]; i < cb[k + 1]; ++i)
       if (plans[i]) {
         ok_idx[k].push_back(i);
         ok_plans[k].push_back(plans[i]);
         outs[k].push_back(host_outs[i]);
+        preps[k].push_back(std::move(prep[i]));
       }
+    bool queued = false;
     if (!ok_plans[k].empty()) {
       const int m = (int)ok_plans[k].size();
       if (needs_each(ok_plans[k].data(), m, outs[k].data())) {
         st = set_err(TP_ERR_INVALID_ARGUMENT, 0, "tp_build_cost_tensors_batch writes the six SoA tensors only");
         break;
       }
+      // the pool is the analyser's while it analyses (then this chunk's set-up runs inline)
       st = host_batch_enqueue(B, device, ok_plans[k].data(), m, outs[k].data(), host_threads, k & 1, cb[k], cb[k],
-                              H[k]);
-      enq[k] = 1;
-      if (st) break;
+                              H[k], &preps[k], kSweepRange);
+      queued = true;
+    } else {
+      H[k].plans = ok_plans[k].data();  // nothing analysed in this chunk: nothing to finish
+      H[k].n = 0;
     }
-    if (k + 1 < K) {  // overlaps the GPU work just enqueued
-      const double c0 = prof ? now_us() : 0;
-      create(k + 1);
-      if (prof) t_create += now_us() - c0;
+    if (st == TP_OK) {
+      const cudaError_t ce = cudaEventRecord(done[k], B.copy_stream ? B.copy_stream : B.stream);
+      if (ce != cudaSuccess) st = set_err(TP_ERR_CUDA, 0, cudaGetErrorString(ce));
     }
+    {
+      std::lock_guard<std::mutex> lk(amu);
+      if (st) failed = true;
+      enq[k] = queued || st == TP_OK;
+      acv.notify_all();
+    }
+    if (prof) tk[2 * k + 1] = now_us() - t0;
+    if (st) break;
   }
+  {
+    std::lock_guard<std::mutex> lk(amu);
+    stop = true;
+    main_done = true;
+    acv.notify_all();
+  }
+  analyser.join();
+  const double t_sync = prof ? now_us() : 0;
   cudaError_t ce = cudaStreamSynchronize(B.stream);
   const cudaError_t ce2 = B.copy_stream ? cudaStreamSynchronize(B.copy_stream) : cudaSuccess;
   if (ce == cudaSuccess) ce = ce2;
   for (int k = 0; k < K; ++k) {
-    if (!enq[k]) continue;
-    if (st == TP_OK && ce == cudaSuccess) {
-      host_batch_finish(B, H[k], nullptr);
-      for (size_t j = 0; j < ok_idx[k].size(); ++j) errs[ok_idx[k][j]] = H[k].errs[j];
-    } else {
-      H[k].give_back();
+    if (retired[k]) continue;
+    if (enq[k] && H[k].n > 0) {
+      if (st == TP_OK && ce == cudaSuccess) {
+        host_batch_finish(B, H[k], nullptr);
+        for (size_t j = 0; j < ok_idx[k].size(); ++j) {
+          errs[ok_idx[k][j]] = H[k].errs[j];
+          if (index_outs) tp_plan_index(plans[ok_idx[k][j]], &index_outs[ok_idx[k][j]]);
+        }
+      } else {
+        H[k].give_back();
+      }
     }
   }
-  if (index_outs && st == TP_OK)
-    for (int i = 0; i < n; ++i)
-      if (plans[i]) tp_plan_index(plans[i], &index_outs[i]);
-  run_pool(n, host_threads, [&](int i, int) { tp_plan_destroy(plans[i]); }, device);
-  if (prof)
-    fprintf(stderr, "[tp sweep] %d scenarios in %d chunks: %.0f us (overlapped analysis %.0f us)\n", n, K,
-            now_us() - t0, t_create);
+  for (auto& e : done) cudaEventDestroy(e);
+  run_pool(n, host_threads, [&](int i, int) { tp_plan_destroy(plans[i]); }, device);  // what is left
+  if (prof) {
+    fprintf(stderr, "[tp sweep] %d scenarios in %d chunks: %.0f us (analysis thread %.0f us; sync wait %.0f us)\n",
+            n, K, now_us() - t0, t_create, now_us() - t_sync);
+    for (int k = 0; k < K; ++k) {
+      float a = -1, b = -1, c = -1;
+      if (H[k].ev[0] && H[0].ev[0]) {
+        cudaEventElapsedTime(&a, H[0].ev[0], H[k].ev[0]);
+        cudaEventElapsedTime(&b, H[0].ev[0], H[k].ev[1]);
+        cudaEventElapsedTime(&c, H[0].ev[0], H[k].ev[2]);
+      }
+      fprintf(stderr, "  chunk %d: analysed at %.0f us, enqueued at %.0f; device (from chunk 0 start): "
+              "compute %.0f, built %.0f, drained %.0f us\n", k, tk[2 * k], tk[2 * k + 1], a * 1e3, b * 1e3, c * 1e3);
+    }
+    for (auto& h : H)
+      for (auto& e : h.ev)
+        if (e) cudaEventDestroy(e);
+  }
   if (st) return st;
   if (ce != cudaSuccess) return set_err(TP_ERR_CUDA, 0, cudaGetErrorString(ce));
   return batch_status(errs, status_out);

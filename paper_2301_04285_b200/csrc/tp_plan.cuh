@@ -1037,21 +1037,91 @@ int pool_size(int n, int host_threads) {
   return std::max(1, std::min(t, n));
 }
 
-// fn(item, worker) over items [0, n), items claimed one at a time. The
-// workers make `device` current first (a new host thread starts on device 0:
-// anything they allocate must land on the plans' device).
+// A persistent pool of host workers: a sweep calls run_pool several times
+// per chunk, and spawning 16 threads costs ~0.5 ms each time. Workers sleep
+// on a condition variable between jobs. One job at a time: a caller that finds
+// the pool busy (another device's batch on another thread) or that is itself
+// a worker runs its items inline.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();  // never destroyed: no join at process exit
+    return *p;
+  }
+  int size() const { return (int)th_.size() + 1; }
+  // fn(item, worker) over [0, n) on min(workers, size()) threads (the caller is worker 0)
+  void run(int n, int workers, const std::function<void(int, int)>& fn, int device) {
+    std::unique_lock<std::mutex> busy(run_mu_, std::try_to_lock);
+    if (!busy.owns_lock() || t_in_worker) {
+      for (int i = 0; i < n; ++i) fn(i, 0);
+      return;
+    }
+    workers = std::max(1, std::min(workers, size()));
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      n_ = n;
+      device_ = device;
+      next_.store(0);
+      want_ = workers - 1;
+      running_ = workers - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (int i = next_.fetch_add(1); i < n; i = next_.fetch_add(1)) fn(i, 0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return running_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const int hw = (int)std::min(32u, std::max(1u, std::thread::hardware_concurrency()));
+    for (int w = 1; w < hw; ++w) th_.emplace_back([this, w] { loop(w); });
+  }
+  void loop(int w) {
+    t_in_worker = true;
+    uint64_t seen = 0;
+    int dev = -1;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (w > want_) continue;  // not needed for this job
+      const std::function<void(int, int)>* fn = fn_;
+      const int n = n_, device = device_;
+      lk.unlock();
+      if (device >= 0 && device != dev) {
+        cudaSetDevice(device);  // a new host thread starts on device 0
+        dev = device;
+      }
+      for (int i = next_.fetch_add(1); i < n; i = next_.fetch_add(1)) (*fn)(i, w);
+      lk.lock();
+      if (--running_ == 0) done_.notify_all();
+    }
+  }
+  static thread_local bool t_in_worker;
+  std::vector<std::thread> th_;
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int, int)>* fn_ = nullptr;
+  int n_ = 0, device_ = -1, want_ = 0, running_ = 0;
+  uint64_t gen_ = 0;
+  std::atomic<int> next_{0};
+};
+thread_local bool HostPool::t_in_worker = false;
+
+// fn(item, worker) over items [0, n), items claimed one at a time, on up to
+// `workers` pool threads (pool_size) with `device` current.
 template <typename F>
 void run_pool(int n, int workers, F&& fn, int device = -1) {
   workers = pool_size(n, workers);
-  std::atomic<int> next{0};
-  auto body = [&](int w) {
-    if (device >= 0 && w > 0) cudaSetDevice(device);
-    for (int i = next.fetch_add(1); i < n; i = next.fetch_add(1)) fn(i, w);
-  };
-  std::vector<std::thread> th;
-  for (int w = 1; w < workers; ++w) th.emplace_back(body, w);
-  body(0);
-  for (auto& x : th) x.join();
+  if (workers <= 1) {
+    for (int i = 0; i < n; ++i) fn(i, 0);
+    return;
+  }
+  const std::function<void(int, int)> f = [&](int i, int w) { fn(i, w); };
+  HostPool::get().run(n, workers, f, device);
 }
 
 // a worker's status and message (tp_last_error is per thread)

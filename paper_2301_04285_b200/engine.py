@@ -464,6 +464,9 @@ class Sweep:
             views = {k: big[k][(node_off if k.startswith("node") else edge_off)[i]:
                                (node_off if k.startswith("node") else edge_off)[i + 1]] for k in _OUT_KEYS}
             ct = CostTensors(sizes=self.sizes(i) if self.handles[i] else {}, **ix, **views)
+            for k, m in (("edge_from_op", n_e), ("edge_to_op", n_e), ("in_degree", n_ops), ("out_degree", n_ops),
+                         ("topo_order", n_ops)):
+                setattr(ct, k, ix[k][:m])  # views: filled in place by every execute / build
             if self.handles[i] and records:
                 ct.records = np.zeros(max(ne[i], 1) * 40, np.uint8)
             if self.handles[i] and row_min:
@@ -484,12 +487,7 @@ class Sweep:
                                                  abi.ptr(self.status, C.c_int32))
         if raise_errors:
             _check(self.lib, st)
-        for i, ct in enumerate(self.results):
-            f = self.flats[i]
-            for k, n in (("edge_from_op", f.num_edges), ("edge_to_op", f.num_edges), ("in_degree", f.num_ops),
-                         ("out_degree", f.num_ops), ("topo_order", f.num_ops)):
-                setattr(ct, k, self._keep[i][k][:n])
-        return st
+        return st  # the results' index arrays are views set up by allocate()
 
     def build(self, raise_errors: bool = True):
         """Analyse and build every scenario in one pipelined call
@@ -502,12 +500,7 @@ class Sweep:
                                                   self._ix, self._cs, abi.ptr(self.status, C.c_int32))
         if raise_errors:
             _check(self.lib, st)
-        for i, ct in enumerate(self.results):
-            f = self.flats[i]
-            for k, n in (("edge_from_op", f.num_edges), ("edge_to_op", f.num_edges), ("in_degree", f.num_ops),
-                         ("out_degree", f.num_ops), ("topo_order", f.num_ops)):
-                setattr(ct, k, self._keep[i][k][:n])
-        return st
+        return st  # the results' index arrays are views set up by allocate()
 
     @property
     def num_aux_edges(self) -> int:
@@ -559,24 +552,6 @@ class DeviceSweep:
             self._structs[i] = device_cost_struct({k: v for k, v in sl.items() if v.numel()})
         torch.cuda.synchronize(dev)
 
-    def build(self, raise_errors: bool = True):
-        """Analyse and build every scenario in one pipelined call
-        (tp_build_cost_tensors_batch): the host analysis of one chunk of
-        scenarios overlaps the device build of the previous one, and the
-        pinned output slices from allocate() are written by the kernels
-        directly. Needs allocate() (the output sizes) from an earlier create();
-        the plans of that create are not used."""
-        st = self.lib.tp_build_cost_tensors_batch(self._gp, self._tp, len(self), self.device, self.host_threads,
-                                                  self._ix, self._cs, abi.ptr(self.status, C.c_int32))
-        if raise_errors:
-            _check(self.lib, st)
-        for i, ct in enumerate(self.results):
-            f = self.flats[i]
-            for k, n in (("edge_from_op", f.num_edges), ("edge_to_op", f.num_edges), ("in_degree", f.num_ops),
-                         ("out_degree", f.num_ops), ("topo_order", f.num_ops)):
-                setattr(ct, k, self._keep[i][k][:n])
-        return st
-
     @property
     def num_aux_edges(self) -> int:
         return int(self.edge_off[-1])
@@ -589,6 +564,13 @@ class DeviceSweep:
         """Kernel launches of the last run: the batch's inference pass and
         build launch(es) (tp_batch_last_launches)."""
         return int(self.lib.tp_batch_last_launches(self.device)) if self.plans else 0
+
+    def set_profile_events(self, start, stop):
+        """torch.cuda.Event pair recorded around the batch's kernels of every
+        run (tp_batch_set_profile_events); None disables."""
+        _check(self.lib, self.lib.tp_batch_set_profile_events(
+            self.device, C.c_void_p(start.cuda_event if start is not None else None),
+            C.c_void_p(stop.cuda_event if stop is not None else None)))
 
     def run(self):
         """Rebuild every scenario, asynchronously on `self.main`."""
