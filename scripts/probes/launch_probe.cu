@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 struct Big { char b[400]; };
 __global__ void empty_small() {}
+__global__ void __launch_bounds__(256, 4) empty_ptr(const Big* a) { if (blockIdx.x == 99999) printf("%d", a->b[0]); }
 __global__ void __launch_bounds__(256, 4) empty_big(Big a) { if (a.b[threadIdx.x % 400] == 123 && blockIdx.x == 9999) printf("x"); }
 __global__ void spin_big(Big a, int ns) {
   unsigned long long t0; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -33,6 +34,8 @@ int main() {
     time("empty <<<148,1024>>>", [&] { empty_big<<<148, 1024>>>(big); });
     time("empty <<<296,512>>>", [&] { empty_big<<<296, 512>>>(big); });
     time("empty <<<592,256>>>", [&] { empty_big<<<592, 256>>>(big); });
+    time("empty <<<592,256>>> (8-B param)", [&] { empty_ptr<<<592, 256>>>(nullptr); });
+    time("no kernel (two events)", [&] {});
     time("empty <<<1184,128>>>", [&] { empty_big<<<1184, 128>>>(big); });
     time("empty <<<1,32>>> again", [&] { empty_small<<<1, 32>>>(); });
     time("spin 10us <<<148,1024>>>", [&] { spin_big<<<148, 1024>>>(big, 10000); });
