@@ -521,8 +521,11 @@ tp_status prepare_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   // phase-1 units: node rows, then class pairs (warp form) or 32-pair chunks;
   // phase-2 items: node ranges, then edge ranges
   a.direct = direct;
+  // a two-launch batch (mode 5) publishes nothing: its rows run one per thread
+  a.rows_thread = batch_mode == 5 && !a.warp_form;
+  const int64_t row_units = a.rows_thread ? (p->total_rows + 31) / 32 : p->total_rows;
   const int64_t units =
-      p->total_rows + (direct ? 0 : (a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32));
+      row_units + (direct ? 0 : (a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32));
   const int64_t total_items = exp_items + nfan_items;
   if (total_items >= (1ll << 30) || units >= (1ll << 30))
     return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many work items");

@@ -319,6 +319,7 @@ struct FusedArgs {
   const uint32_t* oplists;
   const int64_t* cls_ops;
   int direct;  // priced in the fan-out from the op lists: no pair units, no class tables
+  int rows_thread;  // node-class rows one per thread, 32 per unit (batches without published counters)
 
   // shared
   const Strat* tables;
@@ -338,6 +339,44 @@ constexpr int kFusedThreads = 256;
 // (pair_thread), one column per thread: dynamic shared memory of fused_batch_kernel
 static_assert(tpk::kBwEntries == tpk::kBwTab, "bandwidth table layout");
 constexpr int kMsecBytes = (int)(tpk::kGroupMax * kFusedThreads * sizeof(double));
+
+// The terms of one tensor occurrence of a node-class row (aux_graph.hpp:120-167):
+// its shard bytes tm (added to the memory if has_m) and, for a tensor the
+// operator's non-slicing axes replicate (group > 1), the AllReduce volume tv
+// and seconds tc (infer_ct_allreduce, cost_model.hpp:75-97; has_v).
+__device__ __forceinline__ void occ_terms(const FusedArgs& a, const ClassDesc& cd, const Strat& st, int q, double& tv,
+                                          double& tc, double& tm, bool& has_v, bool& has_m) {
+  const Occ oc = a.occs[q];
+  const SlotDesc& sd = a.slots[cd.slot_begin + oc.slot];
+  int sdiv = 0;
+  for (int d = 0; d < sd.R; ++d)
+    if (sd.sa[d] >= 0) sdiv += st.deg[sd.sa[d]];
+  const int64_t shard_el = sdiv >= 63 ? 0 : (sd.elements >> sdiv);
+  const double sb = (double)shard_el * sd.es;  // layout.hpp:125-129
+  has_m = oc.in_memory;                        // aux_graph.hpp:151-167
+  tm = sb;
+  tv = tc = 0;
+  has_v = false;
+  int glog = 0;
+  for (int ax = 0; ax < cd.p; ++ax)
+    if ((oc.nonslicing >> ax) & 1) glog += st.deg[ax];
+  if (glog > 0) {  // group > 1
+    const int64_t pd = sdiv > a.n_log2 ? 0 : ((int64_t)1 << (a.n_log2 - sdiv));
+    int64_t remain = a.env.local, dev_in = 1;
+    for (int k = 0; k < st.depth; ++k) {
+      bool contains = false;
+      for (int d = 0; d < sd.R; ++d) contains |= sd.sa[d] >= 0 && st.dmap[sd.sa[d]] == k;
+      const int64_t ek = (int64_t)1 << st.mx[k];
+      if (!contains && remain > 1) dev_in *= remain > ek ? ek : remain;
+      remain >>= st.mx[k];  // remain / ek, ek a power of two, remain >= 0
+    }
+    const int64_t ct = dev_in >= pd ? 0 : (dev_in > 1 ? a.env.local / dev_in : a.env.local);
+    const double n = (double)((int64_t)1 << glog);
+    tv = 2.0 * (n - 1) / n * sb;  // allreduce_volume, cost_model.hpp:39-43
+    tc = tv / tpk::eff_bw(ct, a.env);
+    has_v = true;
+  }
+}
 
 // One aux-node row of a node class (aux_graph.hpp:120-167) on one warp:
 // lanes take the slice checks and the tensor occurrences in parallel (their
@@ -373,37 +412,7 @@ __device__ void node_row(const FusedArgs& a, int64_t row) {
     const int q = q0 + lane;
     double tv = 0, tc = 0, tm = 0;  // this occurrence's terms
     bool has_v = false, has_m = false;
-    if (q < cd.occ_end) {
-      const Occ oc = a.occs[q];
-      const SlotDesc& sd = a.slots[cd.slot_begin + oc.slot];
-      int sdiv = 0;
-      for (int d = 0; d < sd.R; ++d)
-        if (sd.sa[d] >= 0) sdiv += st.deg[sd.sa[d]];
-      const int64_t shard_el = sdiv >= 63 ? 0 : (sd.elements >> sdiv);
-      const double sb = (double)shard_el * sd.es;  // layout.hpp:125-129
-      has_m = oc.in_memory;                        // aux_graph.hpp:151-167
-      tm = sb;
-      int glog = 0;
-      for (int ax = 0; ax < cd.p; ++ax)
-        if ((oc.nonslicing >> ax) & 1) glog += st.deg[ax];
-      if (glog > 0) {  // group > 1
-        // infer_ct_allreduce (cost_model.hpp:75-97)
-        const int64_t pd = sdiv > a.n_log2 ? 0 : ((int64_t)1 << (a.n_log2 - sdiv));
-        int64_t remain = a.env.local, dev_in = 1;
-        for (int k = 0; k < st.depth; ++k) {
-          bool contains = false;
-          for (int d = 0; d < sd.R; ++d) contains |= sd.sa[d] >= 0 && st.dmap[sd.sa[d]] == k;
-          const int64_t ek = (int64_t)1 << st.mx[k];
-          if (!contains && remain > 1) dev_in *= remain > ek ? ek : remain;
-          remain >>= st.mx[k];  // remain / ek, ek a power of two, remain >= 0
-        }
-        const int64_t ct = dev_in >= pd ? 0 : (dev_in > 1 ? a.env.local / dev_in : a.env.local);
-        const double n = (double)((int64_t)1 << glog);
-        tv = 2.0 * (n - 1) / n * sb;  // allreduce_volume, cost_model.hpp:39-43
-        tc = tv / tpk::eff_bw(ct, a.env);
-        has_v = true;
-      }
-    }
+    if (q < cd.occ_end) occ_terms(a, cd, st, q, tv, tc, tm, has_v, has_m);
     const int cnt = min(32, cd.occ_end - q0);
     for (int i = 0; i < cnt; ++i) {  // in occurrence order
       const double v = __shfl_sync(0xffffffffu, tv, i);
@@ -422,6 +431,39 @@ __device__ void node_row(const FusedArgs& a, int64_t row) {
     a.cls_mem[row] = mem;
     a.cls_memdiv[row] = mem / cd.indeg;  // aux_graph.hpp:292
   }
+}
+
+// The same row on one thread (batches: 32 consecutive rows per warp, mostly
+// of one class, so the lanes run the same loops): checks, then occurrences,
+// in order.
+__device__ void node_row_thread(const FusedArgs& a, int64_t row) {
+  const ClassDesc cd = a.classes[a.row_cls[row]];
+  const int64_t s = row - cd.row_base;
+  const Strat& st = a.tables[cd.table + s];
+  for (int c = cd.chk_begin; c < cd.chk_end; ++c) {
+    const SliceChk k = a.chks[c];
+    const int kind = k.slot < 0 ? tpk::kUnknownSliceTensor : (st.deg[k.axis] > k.v ? tpk::kIndivisible : 0);
+    if (kind) {
+      flag_error(a.err, ekey(1 + (uint64_t)(cd.first_node + s) * 2 + 1, kind));
+      a.cls_sv[row] = make_double2(0.0, 0.0);
+      a.cls_mem[row] = a.cls_memdiv[row] = 0;
+      return;
+    }
+  }
+  double sec = 0, vol = 0, mem = 0;
+  for (int q = cd.occ_begin; q < cd.occ_end; ++q) {
+    double tv, tc, tm;
+    bool has_v, has_m;
+    occ_terms(a, cd, st, q, tv, tc, tm, has_v, has_m);
+    if (has_m) mem += tm;
+    if (has_v) {
+      vol += tv;
+      sec += tc;
+    }
+  }
+  a.cls_sv[row] = make_double2(sec, vol);
+  a.cls_mem[row] = mem;
+  a.cls_memdiv[row] = mem / cd.indeg;  // aux_graph.hpp:292
 }
 
 __device__ __forceinline__ int sig_of_pair(const FusedArgs& a, int64_t idx) { return a.pair_sig[idx]; }
@@ -602,11 +644,125 @@ __device__ __forceinline__ void pair_from_ops(const FusedArgs& a, int64_t idx, c
 // kDirect: priced here from the op lists (no class tables); kWait = false:
 // the tables and rows come from an earlier launch (no counters, no unset
 // checks).
+// The fan-out's common case in a batch's second launch (measured: cfg5
+// 0.735 -> 0.697 ms; the single-plan build is not faster with it, 32.9 vs
+// 33.2 us, and keeps one id per thread): the three SoA tensors from class
+// tables, no AuxEdge records. A thread writes two consecutive ids (an even output
+// position and the next), so each tensor gets one 16-B store per pair, and
+// keeps its edge's fields in registers while it stays in the edge; the warp
+// still writes 512 consecutive bytes per tensor and instruction. Pairs start
+// at 16-B aligned output positions (`par`: the tensors' phase); ids of a pair
+// outside [pos, span_end) are skipped (a span starting at an edge boundary may
+// be misaligned: its first pair then starts one id early).
+struct PairIds {  // (edge segment, su, sw) of an id, and the segment's fields
+  int si;
+  int32_t su, sw, Sw, Wn, uid_u, uid_w, ident;
+  int64_t end, pb, wrow;
+  double f;
+};
+
+__device__ __forceinline__ void enter_seg(const FanSeg* seg, int si, int64_t o, PairIds& c) {
+  const FanSeg& g = seg[si];
+  c.si = si;
+  c.Sw = g.Sw;
+  c.Wn = g.Wn;
+  c.uid_u = g.uid_u;
+  c.uid_w = g.uid_w;
+  c.ident = g.ident;
+  c.end = g.end;
+  c.pb = g.pb;
+  c.wrow = g.wrow;
+  c.f = g.f;
+  const int32_t j = (int32_t)(o - g.begin);
+  c.su = j / c.Sw;
+  c.sw = j - c.su * c.Sw;
+}
+
+template <bool kWait>
+__device__ __forceinline__ void pair_vals(const FusedArgs& a, const PairIds& c, double& cs, double& vs, double& ms) {
+  const int64_t r = c.ident ? c.pb + (int64_t)c.su * c.Sw + c.sw
+                            : c.pb + (int64_t)a.maps[c.uid_u + c.su] * c.Wn + a.maps[c.uid_w + c.sw];
+  const int64_t row = c.wrow + c.sw;
+  const double2 cv = a.cls_sv[row];
+  const double2 rv = kWait ? table_load2(a.r_tab + r) : a.r_tab[r];
+  cs = cv.x + rv.x * c.f;  // aux_graph.hpp:290-291
+  vs = cv.y + rv.y * c.f;
+  ms = a.cls_memdiv[row];  // :292
+}
+
+template <bool kWait>
+__device__ __forceinline__ void fanout_pairs(const FusedArgs& a, const FanSeg* seg, int64_t pos, int64_t span_end,
+                                             int par) {
+  constexpr int64_t kStep = 2 * kFusedThreads;
+  const int64_t base = pos - ((pos - a.A0 + par) & 1);  // a 16-B aligned output position
+  PairIds c;
+  c.si = -1;
+  int32_t st_q = 0, st_r = 0;  // (su, sw) stride of kStep ids in this edge
+  for (int64_t o = base + 2 * threadIdx.x; o < span_end; o += kStep) {
+    const int64_t o1 = o + 1;
+    const bool in0 = o >= pos, in1 = o1 < span_end;
+    // the pair's first id: (su, sw) advanced by the stride, or a new edge
+    if (c.si >= 0 && o < c.end) {
+      c.su += st_q;
+      c.sw += st_r;
+      if (c.sw >= c.Sw) {
+        c.sw -= c.Sw;
+        ++c.su;
+      }
+    } else {
+      int si = c.si < 0 ? 0 : c.si;
+      const int64_t oo = o < pos ? pos : o;  // an id before the span: locate from the span start
+      while (oo >= seg[si].end) ++si;
+      enter_seg(seg, si, o < seg[si].begin ? seg[si].begin : o, c);
+      if (o < seg[si].begin) {  // o is the previous edge's last id (skipped): (su, sw) one before
+        if (c.sw == 0) {
+          c.sw = c.Sw - 1;
+          --c.su;
+        } else {
+          --c.sw;
+        }
+      }
+      st_q = (int32_t)(kStep / c.Sw);
+      st_r = (int32_t)(kStep - (int64_t)st_q * c.Sw);
+    }
+    double cs0 = 0, vs0 = 0, ms0 = 0, cs1 = 0, vs1 = 0, ms1 = 0;
+    if (in0) pair_vals<kWait>(a, c, cs0, vs0, ms0);
+    if (in1) {  // the second id: the next (su, sw), or the next edge's (0, 0)
+      if (o1 < c.end) {
+        PairIds d = c;
+        if (++d.sw == d.Sw) {  // (from a skipped first id of the previous edge, (-1, Sw-1) -> (0, 0))
+          d.sw = 0;
+          ++d.su;
+        }
+        pair_vals<kWait>(a, d, cs1, vs1, ms1);
+      } else {
+        PairIds d;
+        enter_seg(seg, c.si + 1, o1, d);
+        pair_vals<kWait>(a, d, cs1, vs1, ms1);
+      }
+    }
+    const int64_t q = o - a.A0;
+    if (in0 && in1) {  // one 16-B streaming store per tensor
+      __stcs(reinterpret_cast<double2*>(a.e_sec + q), make_double2(cs0, cs1));
+      __stcs(reinterpret_cast<double2*>(a.e_vol + q), make_double2(vs0, vs1));
+      __stcs(reinterpret_cast<double2*>(a.e_mem + q), make_double2(ms0, ms1));
+    } else if (in0) {
+      __stcs(a.e_sec + q, cs0);
+      __stcs(a.e_vol + q, vs0);
+      __stcs(a.e_mem + q, ms0);
+    } else if (in1) {
+      __stcs(a.e_sec + q + 1, cs1);
+      __stcs(a.e_vol + q + 1, vs1);
+      __stcs(a.e_mem + q + 1, ms1);
+    }
+  }
+}
+
 // kPer: output positions a thread has in flight (the loads of kPer ids
 // overlap). The single-plan build keeps kFanPer (measured best with its
 // short ranges); a batch's second launch reads its tables from L2 / DRAM and
 // needs more in flight.
-template <bool kDirect, bool kWait = true, int kPer = kFanPer>
+template <bool kDirect, bool kWait = true, int kPer = kFanPer, bool kLean = false>
 __device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n, int* s_edge) {
   const unsigned long long t0 = a.fan_ns ? gtimer() : 0;
   const int64_t start = a.A0 + (int64_t)item * a.range_len;
@@ -615,6 +771,12 @@ __device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n
   if (threadIdx.x == 0) *s_edge = a.range_first[item];  // host-computed
   int64_t pos = start;
   bool first = true;
+  // the common case (the three SoA tensors, no records, tables): pairs of ids
+  // per thread, when the three tensors share their 16-B alignment phase
+  const int par = (int)((reinterpret_cast<uintptr_t>(a.e_sec) >> 3) & 1);
+  const bool lean = kLean && !kDirect && !a.general_store &&
+                    par == (int)((reinterpret_cast<uintptr_t>(a.e_vol) >> 3) & 1) &&
+                    par == (int)((reinterpret_cast<uintptr_t>(a.e_mem) >> 3) & 1);
   while (pos < end) {
     __syncthreads();
     if (threadIdx.x < 32) {  // warp 0 stages the next kSegs edges, lane per edge
@@ -653,6 +815,11 @@ __device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n
     __syncthreads();
     const int n = *s_n;
     const int64_t span_end = min(end, seg[n - 1].end);
+    if (lean) {
+      fanout_pairs<kWait>(a, seg, pos, span_end, par);
+      pos = span_end;
+      continue;
+    }
     // (su, sw) of a thread's ids advance by a fixed stride within an edge;
     // a division only where the thread enters an edge
     int si = -1;
@@ -802,7 +969,13 @@ __device__ __forceinline__ void run_unit(const FusedArgs& a, int64_t u, const do
                                          const FusedArgs* all = nullptr) {
   const int lane = threadIdx.x & 31;
   const unsigned long long t0 = (a.pair_ns || a.item_ns) ? gtimer() : 0;
-  if (u < a.total_rows) {
+  const int64_t row_units = a.rows_thread ? (a.total_rows + 31) / 32 : a.total_rows;
+  if (!kSync && a.rows_thread && u < row_units) {
+    const int64_t row = u * 32 + lane;
+    if (row < a.total_rows) node_row_thread(a, row);
+    return;
+  }
+  if (!a.rows_thread && u < a.total_rows) {
     node_row(a, u);
     if (kSync && lane == 0) {
       red_release_add(&a.sched->node_done.v, 1);  // rows: off the critical path, released
@@ -812,7 +985,7 @@ __device__ __forceinline__ void run_unit(const FusedArgs& a, int64_t u, const do
       }
     }
   } else if (kWarpForm) {
-    const int64_t idx = u - a.total_rows;
+    const int64_t idx = u - row_units;
     pair_warp(a, idx, price);
     const int sig = a.pairs[idx].sig;
     if (lane == 0) {
@@ -823,7 +996,7 @@ __device__ __forceinline__ void run_unit(const FusedArgs& a, int64_t u, const do
       red_relaxed_add(&a.sched->pairs_done[sig].v, 1);  // no fence: see table_load
     }
   } else {
-    const int64_t idx = (u - a.total_rows) * 32 + lane;
+    const int64_t idx = (u - row_units) * 32 + lane;
     const bool valid = idx < a.total_pairs;
     const int sig = valid ? sig_of_pair(a, idx) : -1;
     const bool grouped = all && a.group_n > 1;
@@ -848,8 +1021,9 @@ __device__ __forceinline__ void run_unit(const FusedArgs& a, int64_t u, const do
 }
 
 __device__ __forceinline__ int64_t plan_units(const FusedArgs& a) {
-  if (a.priced_by_leader || a.direct) return a.total_rows;
-  return a.total_rows + (a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32);
+  const int64_t rows = a.rows_thread ? (a.total_rows + 31) / 32 : a.total_rows;
+  if (a.priced_by_leader || a.direct) return rows;
+  return rows + (a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32);
 }
 
 // The plan's per-launch reset, done by the last CTA to leave (one thread).
@@ -1045,7 +1219,7 @@ __global__ void __launch_bounds__(kFusedThreads, kForm == 3 ? 2 : 4)
     const int li = (int)(item - item_off[ip]);
     if (li < a.i_exp) node_range<kPhase == 3>(a, li, s_seg.n, &s_nseg, &s_edge);
     else if (kForm == 4) fanout_range<true>(a, li - a.i_exp, s_seg.f, &s_nseg, &s_edge);
-    else if (kForm == 5) fanout_range<false, false, TP_BATCH_FAN_PER>(a, li - a.i_exp, s_seg.f, &s_nseg, &s_edge);
+    else if (kForm == 5) fanout_range<false, false, TP_BATCH_FAN_PER, true>(a, li - a.i_exp, s_seg.f, &s_nseg, &s_edge);
     else fanout_range<false>(a, li - a.i_exp, s_seg.f, &s_nseg, &s_edge);
   }
   if (threadIdx.x == 0) {
