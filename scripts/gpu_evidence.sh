@@ -1,9 +1,13 @@
-# Full round-2 evidence on one GPU: test suite, default bench (all blocks), reference arm,
+# Round evidence on one GPU: test suite, default bench (all blocks), reference arm,
 # cfg5 chunk variants, launch list + one --set full capture of fused_kernel and the batch kernels.
 mkdir -p gpurun_out
-TAG=${TAG:-r02l}
+TAG=${TAG:-r02}
 timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_${TAG}.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_${TAG}.log
+timeout 1200 ./oracle/_ref/adapter_parity > gpurun_out/adapter_parity_${TAG}.log 2>&1; echo "rc=$?" >> gpurun_out/adapter_parity_${TAG}.log
+./oracle/_ref/export_parity --big > gpurun_out/export_parity_${TAG}.log 2>&1; echo "rc=$?" >> gpurun_out/export_parity_${TAG}.log
+python scripts/fan_probe.py > gpurun_out/fan_${TAG}.log 2>&1
+python scripts/class_probe.py > gpurun_out/class_${TAG}.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_${TAG}.json 2> gpurun_out/bench_ref_${TAG}.err
 timeout 900 python bench.py --impl reference --workload cfg5 --steps 3 > gpurun_out/bench_ref_cfg5_${TAG}.json 2> gpurun_out/bench_ref_cfg5_${TAG}.err
