@@ -1857,7 +1857,9 @@ tp_status tp_build_cost_tensors_batch(const tp_graph_desc* const* graphs, const 
   // thread pool) runs while the GPU builds chunk k and streams it into the
   // caller's pinned memory; chunk k + 1's uploads queue behind it.
   static const int env_chunks = getenv("TP_SWEEP_CHUNKS") ? atoi(getenv("TP_SWEEP_CHUNKS")) : 0;
-  const int K = std::max(1, std::min<int>(n, env_chunks > 0 ? env_chunks : std::min(12, std::max(1, n / 64))));
+  // a few big scenarios (a sweep of one large graph under several bandwidths): one chunk each
+  const int K = std::max(1, std::min<int>(n, env_chunks > 0 ? env_chunks
+                                                            : (n <= 12 ? n : std::min(12, std::max(2, n / 64)))));
   std::vector<int> cb(K + 1);
   for (int k = 0; k <= K; ++k) cb[k] = (int)((int64_t)n * k / K);
   std::vector<tp_plan*> plans(n, nullptr);

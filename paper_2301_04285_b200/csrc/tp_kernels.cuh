@@ -1168,6 +1168,8 @@ __global__ void __launch_bounds__(kFusedThreads, kForm == 3 ? 2 : 4)
   // pairs keep one unit per claim for balance.
   // Form 5's first launch has nothing else to wait for: its warps stride over
   // the chunks statically (chunk c, c + warps, ...), no counter at all.
+  // (measured on cfg5: static chunks of 2 or 4 units are equal; the
+  // counter-claimed chunks of the other forms are far slower here)
   constexpr int kUC = kForm == 4 ? 8 : (kForm == 5 ? 4 : 1);
   const int64_t chunks = (units + kUC - 1) / kUC;
   if (threadIdx.x == 0) s_unit = blockIdx.x * (kFusedThreads / 32);  // static first chunks, as fused_kernel
@@ -1189,7 +1191,6 @@ __global__ void __launch_bounds__(kFusedThreads, kForm == 3 ? 2 : 4)
       const FusedArgs& a = args[p];
       if (kForm == 1 || (kForm == 0 && a.warp_form)) run_unit<true>(a, u - unit_off[p], a.bw_tab);
       else if (kForm == 4) run_unit<true>(a, u - unit_off[p], a.bw_tab);  // node rows only (a.direct)
-      else if (kForm == 5) run_unit<false, false, true>(a, u - unit_off[p], a.bw_tab);
       else run_unit<false>(a, u - unit_off[p], a.bw_tab, args);
     }
     int next = 0;

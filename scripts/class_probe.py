@@ -34,7 +34,9 @@ for c in np.unique(pr[:, 2]):
     e = end[m]
     cl = prof[m]
     print(f"class {c}: {m.sum()} entries, end p50 {np.percentile(e,50):.1f} p90 {np.percentile(e,90):.1f} max {e.max():.1f} us;"
-          f" ops med {np.median(cl[:,3]):.0f} max {cl[:,3].max()}, clocks med {np.median(cl[:,0]+cl[:,1]+cl[:,2]):.0f} max {(cl[:,0]+cl[:,1]+cl[:,2]).max()}")
+          f" ops med {np.median(cl[:,3]):.0f} max {cl[:,3].max()}, clocks med {np.median(cl[:,0]+cl[:,1]+cl[:,2]):.0f} max {(cl[:,0]+cl[:,1]+cl[:,2]).max()}"
+          f" (closure / axes / inference med {np.median(cl[:,0]):.0f} / {np.median(cl[:,1]):.0f} / {np.median(cl[:,2]):.0f};"
+          f" U med {np.median(cl[:,4]):.0f}, depth med {np.median(cl[:,5]):.0f}, rounds med {np.median(cl[:,6]):.0f})")
 print("rows end max", ((it[:, 0] + it[:, 1]) / 1e3).max())
 print("fan ranges: n", len(fo), "ready p50/max", np.percentile((fo[:,0]+fo[:,1])/1e3, 50), ((fo[:,0]+fo[:,1])/1e3).max(),
       "end max", ((fo[:,0]+fo[:,2])/1e3).max())
