@@ -52,6 +52,7 @@
 #include <functional>
 #include <mutex>
 #include <thread>
+#include <malloc.h>
 
 #include "../../include/taps_b200.h"
 #include "../../include/taps_b200/lp_export.hpp"
@@ -67,6 +68,20 @@ using tpk::Strat;
 #include "tp_desc.cuh"
 #include "tp_kernels.cuh"
 #include "tp_plan.cuh"
+
+namespace {
+// TP_MALLOPT=1: keep freed host memory in the heap instead of mapping and
+// unmapping large blocks (an A/B switch for the host analysis of sweeps).
+struct MalloptInit {
+  MalloptInit() {
+    const char* v = getenv("TP_MALLOPT");
+    if (v && atoi(v) > 0) {
+      mallopt(M_MMAP_THRESHOLD, 32 << 20);
+      mallopt(M_TRIM_THRESHOLD, 1 << 30);
+    }
+  }
+} g_mallopt_init;
+}  // namespace
 
 // ---------------------------------------------------------------------------
 // C-ABI
@@ -786,6 +801,8 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
   cudaStream_t s = stream ? (cudaStream_t)stream : plans[0]->arena->stream;
   BatchCtx& B = g_batch[device];
   std::lock_guard<std::mutex> lk(B.mu);
+  static const bool prof = getenv("TP_PROFILE_HOST") != nullptr;
+  double tp0 = prof ? now_us() : 0, tp1 = 0, tp2 = 0;
   std::vector<ExecPrep> X(n);
   std::vector<int> live;
   int64_t batch_pairs = 0;
@@ -808,6 +825,7 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     if (!X[i].done && X[i].launch) live.push_back(i);
   }
   const int m = (int)live.size();
+  if (prof) tp1 = now_us();
   if (m > 0) {
     if (B.resident == 0) {
       int sms = 0, per_sm = 0;
@@ -862,6 +880,7 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
         }
       }
     }
+    if (prof) tp2 = now_us();
     if (nwarp == 0 && !no_groups && !use_ops) {
       std::vector<std::vector<int32_t>> groups;             // live indices, the leader first
       std::unordered_map<uint64_t, std::vector<int>> open;  // structure hash -> group ids
@@ -1010,6 +1029,9 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     else fused_batch_kernel<0><<<gd, bd, kMsecBytes, s>>>(da, m, duo, dio, dto, hd, err_dev);
     if (B.prof_stop) CUDA_TRY(cudaEventRecord(B.prof_stop, s));
     B.last_launches = (use_ops && n_infer > 0 ? 1 : 0) + (form == 5 ? 2 : 1);
+    if (prof && n >= 32)
+      fprintf(stderr, "[tp batch launch] %d plans: prepare %.0f us, class keys %.0f, staging + launches %.0f\n", n,
+              tp1 - tp0, tp2 - tp1, now_us() - tp2);
     if (cudaPeekAtLastError() != cudaSuccess) {
       B.hdr_clean = false;
       for (int k : live) plans[k]->arena->sched_clean = false;
@@ -1550,6 +1572,7 @@ struct HostBatch {
   std::vector<BatchErr> errs;
   int64_t err_base = 0;  // this batch's error slots in B.d_err / B.h_err
   double t[4] = {0, 0, 0, 0};
+  int64_t d2h_bytes = 0;
   void give_back() {
     for (int i = 0; i < n; ++i) {
       if (!borrowed[i]) continue;
@@ -1562,9 +1585,6 @@ struct HostBatch {
   }
 };
 
-double now_us() {
-  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
-}
 
 // Enqueue a batch of plans of one device without waiting for it: every
 // plan's descriptors uploaded (borrowed arenas: ONE packed copy and two
@@ -1700,6 +1720,10 @@ tp_status host_batch_enqueue(BatchCtx& B, int device, tp_plan* const* plans, int
                           h.edge_cost_s,       h.edge_volume_bytes,       h.edge_memory_bytes};
     return v[k];
   };
+  H.d2h_bytes = 0;
+  for (int k = 0; k < 6; ++k)
+    for (int i = 0; i < n; ++i)
+      if (host_ptr(i, k)) H.d2h_bytes += (int64_t)sizeof(double) * (k < 3 ? nn[i] : ne[i]);
   // the build may write this half only after the copy stream drained its last use
   CUDA_TRY(cudaStreamWaitEvent(s, B.drained[slot], 0));
   if (prof) {
@@ -1859,9 +1883,18 @@ tp_status tp_build_cost_tensors_batch(const tp_graph_desc* const* graphs, const 
   static const int env_chunks = getenv("TP_SWEEP_CHUNKS") ? atoi(getenv("TP_SWEEP_CHUNKS")) : 0;
   // a few big scenarios (a sweep of one large graph under several bandwidths): one chunk each
   const int K = std::max(1, std::min<int>(n, env_chunks > 0 ? env_chunks
-                                                            : (n <= 12 ? n : std::min(12, std::max(2, n / 64)))));
-  std::vector<int> cb(K + 1);
-  for (int k = 0; k <= K; ++k) cb[k] = (int)((int64_t)n * k / K);
+                                                            : (n <= 12 ? n : std::min(24, std::max(2, n / 40)))));
+  // the first two chunks a quarter and a half of the others: the device and
+  // the host link start after a short first analysis
+  std::vector<int> cb(K + 1, 0);
+  if (K >= 4) {
+    const double unit = (double)n / (K - 2 + 0.75);
+    cb[1] = std::max(1, (int)(0.25 * unit));
+    cb[2] = std::max(cb[1] + 1, (int)(0.75 * unit));
+    for (int k = 3; k <= K; ++k) cb[k] = cb[2] + (int)((int64_t)(n - cb[2]) * (k - 2) / (K - 2));
+  } else {
+    for (int k = 0; k <= K; ++k) cb[k] = (int)((int64_t)n * k / K);
+  }
   std::vector<tp_plan*> plans(n, nullptr);
   std::vector<BatchErr> errs(n);
   BatchCtx& B = g_batch[device];
@@ -1879,9 +1912,18 @@ tp_status tp_build_cost_tensors_batch(const tp_graph_desc* const* graphs, const 
   // copies the packs and launches.
   constexpr int64_t kSweepRange = 1024;
   std::vector<UploadPrep> prep(n);
+  // Analysis threads: up to 8 (TP_SWEEP_THREADS to override). More finish
+  // the analysis sooner but slow the host link and this thread's enqueues
+  // (measured on cfg5, 16 cores: 15 threads 11.1-11.4 ms, 8 threads 10.0-10.1,
+  // 4 threads 10.4-11.0).
+  static const int env_threads = getenv("TP_SWEEP_THREADS") ? atoi(getenv("TP_SWEEP_THREADS")) : 0;
+  const int analysis_threads =
+      host_threads > 0 ? host_threads
+      : env_threads > 0 ? env_threads
+                        : std::max(2, std::min(8, (int)std::thread::hardware_concurrency() / 2));
   auto create = [&](int k) {
     run_pool(
-        cb[k + 1] - cb[k], host_threads,
+        cb[k + 1] - cb[k], analysis_threads,
         [&](int j, int) {
           const int i = cb[k] + j;
           tp_plan* p = nullptr;
@@ -1892,6 +1934,7 @@ tp_status tp_build_cost_tensors_batch(const tp_graph_desc* const* graphs, const 
             p->uploaded = false;
             tp_status s2 = ensure_stream(p);
             if (!s2) s2 = upload_prepare(p, prep[i], kSweepRange);
+            if (!s2) class_keys(p);  // cached for the batch's inference dedup
             if (s2) {
               errs[i].take(s2);
               p->arena = nullptr;
@@ -1963,6 +2006,7 @@ tp_status tp_build_cost_tensors_batch(const tp_graph_desc* const* graphs, const 
         if (index_outs) tp_plan_index(plans[ok_idx[k][j]], &index_outs[ok_idx[k][j]]);
       }
       destroy_chunk(k);
+      std::vector<UploadPrep>().swap(preps[k]);  // its packs went up with the chunk
       retired[k] = 1;
     }
   });
@@ -2043,8 +2087,10 @@ tp_status tp_build_cost_tensors_batch(const tp_graph_desc* const* graphs, const 
         cudaEventElapsedTime(&b, H[0].ev[0], H[k].ev[1]);
         cudaEventElapsedTime(&c, H[0].ev[0], H[k].ev[2]);
       }
-      fprintf(stderr, "  chunk %d: analysed at %.0f us, enqueued at %.0f; device (from chunk 0 start): "
-              "compute %.0f, built %.0f, drained %.0f us\n", k, tk[2 * k], tk[2 * k + 1], a * 1e3, b * 1e3, c * 1e3);
+      fprintf(stderr, "  chunk %d: analysed at %.0f us, enqueued at %.0f (uploads %.0f, launch prep %.0f, copies %.0f); "
+              "device (from chunk 0 start): compute %.0f, built %.0f, drained %.0f us; %.1f MB\n", k, tk[2 * k],
+              tk[2 * k + 1], H[k].t[1] - H[k].t[0], H[k].t[2] - H[k].t[1], H[k].t[3] - H[k].t[2], a * 1e3, b * 1e3,
+              c * 1e3, H[k].d2h_bytes / 1e6);
     }
     for (auto& h : H)
       for (auto& e : h.ev)

@@ -202,20 +202,6 @@ inline uint64_t hash_words(uint64_t h, const void* data, size_t bytes) {
   return h ^ (bytes << 7);
 }
 
-#ifdef TP_HOST_PROF
-double g_hprof[8];
-std::chrono::steady_clock::time_point g_hlast;
-#define HPROF(k)                                                                                  \
-  do {                                                                                            \
-    auto now_ = std::chrono::steady_clock::now();                                                 \
-    if (k) g_hprof[k] += std::chrono::duration<double, std::micro>(now_ - g_hlast).count();       \
-    g_hlast = now_;                                                                               \
-  } while (0)
-#else
-#define HPROF(k) \
-  do {           \
-  } while (0)
-#endif
 
 // Layout ids of a side's strategies (layout_tables): a pure function of the
 // strategy table (p, log2 N) and the slicing, memoised for the process.
@@ -242,6 +228,161 @@ void side_memo_put(const uint64_t* k, const std::vector<int32_t>& uid, const std
   std::lock_guard<std::mutex> lk(g_side_memo_mu);
   if (g_side_memo.size() < 4096) g_side_memo.emplace(SideMemoKey{k[0], k[1]}, std::make_pair(uid, reps));
 }
+
+double now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// workers for the host analysis of one graph (TP_HOST_WORKERS, default all)
+int host_workers() {
+  static const int w = getenv("TP_HOST_WORKERS") ? atoi(getenv("TP_HOST_WORKERS")) : 0;
+  return w;
+}
+
+int pool_size(int n, int host_threads) {
+  int t = host_threads > 0 ? host_threads : (int)std::min(32u, std::max(1u, std::thread::hardware_concurrency()));
+  return std::max(1, std::min(t, n));
+}
+
+// A persistent pool of host workers: a sweep calls run_pool several times
+// per chunk, and spawning 16 threads costs ~0.5 ms each time. Workers sleep
+// on a condition variable between jobs. One job at a time: a caller that finds
+// the pool busy (another device's batch on another thread) or that is itself
+// a worker runs its items inline.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();  // never destroyed: no join at process exit
+    return *p;
+  }
+  int size() const { return (int)th_.size() + 1; }
+  // fn(item, worker) over [0, n) on min(workers, size()) threads (the caller is worker 0)
+  void run(int n, int workers, const std::function<void(int, int)>& fn, int device) {
+    std::unique_lock<std::mutex> busy(run_mu_, std::try_to_lock);
+    if (!busy.owns_lock() || t_in_worker) {
+      for (int i = 0; i < n; ++i) fn(i, 0);
+      return;
+    }
+    workers = std::max(1, std::min(workers, size()));
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      n_ = n;
+      device_ = device;
+      next_.store(0);
+      want_ = workers - 1;
+      running_ = workers - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (int i = next_.fetch_add(1); i < n; i = next_.fetch_add(1)) fn(i, 0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return running_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const int hw = (int)std::min(32u, std::max(1u, std::thread::hardware_concurrency()));
+    for (int w = 1; w < hw; ++w) th_.emplace_back([this, w] { loop(w); });
+  }
+  void loop(int w) {
+    t_in_worker = true;
+    uint64_t seen = 0;
+    int dev = -1;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (w > want_) continue;  // not needed for this job
+      const std::function<void(int, int)>* fn = fn_;
+      const int n = n_, device = device_;
+      lk.unlock();
+      if (device >= 0 && device != dev) {
+        cudaSetDevice(device);  // a new host thread starts on device 0
+        dev = device;
+      }
+      for (int i = next_.fetch_add(1); i < n; i = next_.fetch_add(1)) (*fn)(i, w);
+      lk.lock();
+      if (--running_ == 0) done_.notify_all();
+    }
+  }
+  static thread_local bool t_in_worker;
+  std::vector<std::thread> th_;
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int, int)>* fn_ = nullptr;
+  int n_ = 0, device_ = -1, want_ = 0, running_ = 0;
+  uint64_t gen_ = 0;
+  std::atomic<int> next_{0};
+};
+thread_local bool HostPool::t_in_worker = false;
+
+// fn(item, worker) over items [0, n), items claimed one at a time, on up to
+// `workers` pool threads (pool_size) with `device` current.
+template <typename F>
+void run_pool(int n, int workers, F&& fn, int device = -1) {
+  workers = pool_size(n, workers);
+  if (workers <= 1) {
+    for (int i = 0; i < n; ++i) fn(i, 0);
+    return;
+  }
+  const std::function<void(int, int)> f = [&](int i, int w) { fn(i, w); };
+  HostPool::get().run(n, workers, f, device);
+}
+
+// a worker's status and message (tp_last_error is per thread)
+struct BatchErr {
+  tp_status st = TP_OK;
+  int kind = 0;
+  std::string msg;
+  void take(tp_status s) {
+    st = s;
+    if (s) {
+      kind = g_err_kind;
+      msg = g_err;
+    }
+  }
+};
+
+tp_status batch_status(const std::vector<BatchErr>& errs, int32_t* status_out) {
+  const BatchErr* first = nullptr;
+  for (size_t i = 0; i < errs.size(); ++i) {
+    if (status_out) status_out[i] = errs[i].st;
+    if (errs[i].st && !first) first = &errs[i];
+  }
+  if (!first) {
+    g_err[0] = 0;
+    g_err_kind = 0;
+    return TP_OK;
+  }
+  return set_err(first->st, first->kind, first->msg);
+}
+
+// 64-bit key hash -> the first id with that hash (open addressing; callers
+// chain equal hashes themselves and compare the keys)
+struct HashIndex {
+  std::vector<uint64_t> key;
+  std::vector<int32_t> val;
+  uint64_t mask = 0;
+  void init(int n) {
+    size_t cap = 16;
+    while (cap < 2 * (size_t)std::max(n, 1)) cap <<= 1;
+    key.assign(cap, 0);
+    val.assign(cap, -1);
+    mask = cap - 1;
+  }
+  // the head for hash h (-1 when new; assign to insert)
+  int32_t& at(uint64_t h) {
+    for (uint64_t i = (h ^ (h >> 31)) & mask;; i = (i + 1) & mask) {
+      if (val[i] < 0) {
+        key[i] = h;
+        return val[i];
+      }
+      if (key[i] == h) return val[i];
+    }
+  }
+};
 
 struct Builder {
   const tp_graph_desc* g;
@@ -293,28 +434,31 @@ struct Builder {
   }
 
   // Per-op slots: the reference keys an operator's layouts by tensor name,
-  // the last occurrence's spec winning (layout.hpp:339-347).
-  // Flat over all operators: op i owns slots [slot_begin[i], slot_begin[i + 1]).
-  std::vector<int32_t> slot_begin, slot_name, slot_spec;
+  // the last occurrence's spec winning (layout.hpp:339-347). Op i's slots sit
+  // at its first tensor index op_tensor_begin[i] (at most one slot per
+  // tensor), slot_cnt[i] of them, so every op fills its own span in parallel.
+  std::vector<int32_t> slot_cnt, slot_name, slot_spec;
   std::vector<std::array<int8_t, tpk::kMaxR>> slot_sa;  // tensor dim -> slicing axis, per slot
   int find_slot(int op, int nm) const {  // local slot index of tensor name nm, or -1
-    const int b = slot_begin[op], e = slot_begin[op + 1];
+    const int b = g->op_tensor_begin[op], e = b + slot_cnt[op];
     for (int i = b; i < e; ++i)
       if (slot_name[i] == nm) return i - b;
     return -1;
   }
-  int spec_of(int op, int k) const { return slot_spec[slot_begin[op] + k]; }
-  const std::array<int8_t, tpk::kMaxR>& sa_of(int op, int k) const { return slot_sa[slot_begin[op] + k]; }
+  int spec_of(int op, int k) const { return slot_spec[g->op_tensor_begin[op] + k]; }
+  const std::array<int8_t, tpk::kMaxR>& sa_of(int op, int k) const { return slot_sa[g->op_tensor_begin[op] + k]; }
   std::map<int, int64_t> table_of_p;
   // node classes by key hash: first class with a hash, then a chain per class
-  std::unordered_map<uint64_t, int32_t> class_head;
+  HashIndex class_head;
   std::vector<int32_t> class_next;
   std::vector<int32_t> class_nslot;
-  // per-operator scratch, reused
-  std::vector<SliceChk> chk;
-  std::vector<SlotDesc> slots;
-  std::vector<Occ> occ;
-  std::vector<int64_t> key;
+  // every op's node-class key parts, where build_op puts them: slice checks
+  // at the op's first slice index, slot descriptors and occurrences at its
+  // first tensor index; with the key's hash
+  std::vector<SliceChk> chk_all;
+  std::vector<SlotDesc> slots_all;
+  std::vector<Occ> occ_all;
+  std::vector<uint64_t> op_hash;
   std::vector<std::vector<int64_t>> class_members;
   // tensors fed by edges, CSR by dense op id (op_key[i] = dense id of op i)
   std::vector<int32_t> fed_begin, fed_list, op_key;
@@ -428,39 +572,73 @@ struct Builder {
     const bool pow2 = p.N > 0 && (p.N & (p.N - 1)) == 0;
     p.n_log2 = pow2 ? log2_floor(p.N) : 0;
     if (pow2 && p.n_log2 > tpk::kMaxD) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "more than 2^16 devices");
-    slot_begin.assign(g->num_ops + 1, 0);
-    slot_name.clear();
-    slot_spec.clear();
-    slot_sa.clear();
-    wrow_of_op.assign(g->num_ops, 0);
-    p.op_row.assign(g->num_ops, 0);
+    const int nops = g->num_ops;
+    wrow_of_op.assign(nops, 0);
+    p.op_row.assign(nops, 0);
+    // In operator order: the aux node ids, the strategy tables, and where the
+    // reference would stop (a non-power-of-two mesh or an op without axes ends
+    // the node phase; a capacity limit fails the call after the ops before it).
     int64_t nodes = 0;
-    p.valid_ops = g->num_ops;
-    for (int i = 0; i < g->num_ops; ++i) {
+    int lim = nops, lim_ek = 0;
+    BatchErr lim_err;
+    for (int i = 0; i < nops; ++i) {
       p.node_base[i] = nodes;
       const int np = g->op_axis_begin[i + 1] - g->op_axis_begin[i];
-      int ek = 0;
-      if (!pow2) ek = tpk::kNotPow2;
-      else if (np < 1) ek = tpk::kNoAxes;
+      const int ek = !pow2 ? tpk::kNotPow2 : (np < 1 ? tpk::kNoAxes : 0);
       if (ek) {
-        p.host_err = ekey(1 + (uint64_t)nodes * 2, ek);
-        p.valid_ops = i;
+        lim = i;
+        lim_ek = ek;
         break;
       }
-      if (np > tpk::kMaxAxes) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "operator with more than 8 axes");
+      if (np > tpk::kMaxAxes) {
+        lim = i;
+        lim_err.take(set_err(TP_ERR_CAPACITY, tpk::kCapacity, "operator with more than 8 axes"));
+        break;
+      }
       const int64_t S = tpk::strategy_count(np, p.n_log2);
-      if (S > (1 << 20)) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "more than 2^20 strategies per operator");
+      if (S > (1 << 20)) {
+        lim = i;
+        lim_err.take(set_err(TP_ERR_CAPACITY, tpk::kCapacity, "more than 2^20 strategies per operator"));
+        break;
+      }
       if (!table_of_p.count(np)) {
         table_of_p[np] = p.table_total;
         p.tabs.push_back(TableDesc{p.table_total, S, np, p.n_log2});
         p.table_total += S;
       }
-      st = build_op(i, np, S, nodes);
-      if (st) return st;
       nodes += S;
     }
-    for (int i = p.valid_ops; i <= g->num_ops; ++i) p.node_base[i] = nodes;
-    for (int i = p.valid_ops; i <= g->num_ops; ++i) slot_begin[i] = (int32_t)slot_name.size();  // unbuilt: no slots
+    for (int i = lim; i <= nops; ++i) p.node_base[i] = nodes;
+    // every op's slots and class key, independently (in parallel for big graphs)
+    {
+      const int nt = num_tensors();
+      const int nslices = nops > 0 && g->op_axis_begin[nops] > 0 ? g->axis_slice_begin[g->op_axis_begin[nops]] : 0;
+      slot_cnt.assign(nops, 0);
+      slot_name.resize(nt);
+      slot_spec.resize(nt);
+      slot_sa.resize(nt);
+      chk_all.resize(nslices);
+      slots_all.resize(nt);
+      occ_all.resize(nt);
+      op_hash.resize(nops);
+      std::vector<BatchErr> op_err(lim);
+      constexpr int kOpsPerItem = 64;
+      const int items = (lim + kOpsPerItem - 1) / kOpsPerItem;
+      run_pool(lim >= 2 * kOpsPerItem ? items : 1, host_workers(), [&](int it, int) {
+        const int i1 = lim >= 2 * kOpsPerItem ? std::min(lim, (it + 1) * kOpsPerItem) : lim;
+        for (int i = lim >= 2 * kOpsPerItem ? it * kOpsPerItem : 0; i < i1; ++i)
+          op_err[i].take(build_op(i, g->op_axis_begin[i + 1] - g->op_axis_begin[i]));
+      });
+      for (int i = 0; i < lim; ++i)  // the first failing op, in order
+        if (op_err[i].st) return set_err(op_err[i].st, op_err[i].kind, op_err[i].msg);
+    }
+    if (lim_err.st) return set_err(lim_err.st, lim_err.kind, lim_err.msg);
+    if (lim_ek) p.host_err = ekey(1 + (uint64_t)nodes * 2, lim_ek);
+    p.valid_ops = lim;
+    // node classes, in operator order (first member first)
+    class_head.init(lim);
+    for (int i = 0; i < lim; ++i) add_to_class(i, g->op_axis_begin[i + 1] - g->op_axis_begin[i],
+                                               p.node_base[i + 1] - p.node_base[i], p.node_base[i]);
     p.num_aux_nodes = nodes;
     for (size_t c = 0; c < p.classes.size(); ++c) {  // class member CSR + fan-out work
       p.classes[c].mem_begin = (int32_t)p.members.size();
@@ -472,62 +650,102 @@ struct Builder {
     // ---------------- edge phase (aux_graph.hpp:273-296) -----------------
     int64_t aux = 0, rows = 0;
     p.valid_edges = 0;
-    std::unordered_map<uint64_t, int32_t> sig_head;  // key hash -> first class; chains below
+    HashIndex sig_head;  // key hash -> first class; chains below
     std::vector<int32_t> sig_next, sig_pu, sig_pw;
     std::vector<int64_t> sig_shape;  // kMaxR extents per class
-    std::vector<std::vector<int32_t>> edges_of_sig;
+    std::vector<int32_t> sig_of_edge;
+    constexpr int kEdgesPerItem = 128;
     if (p.host_err == ~0ull) {
-      p.valid_edges = g->num_edges;
-      for (int e = 0; e < g->num_edges; ++e) {
-        p.edge_base[e] = aux;
-        p.row_base[e] = rows;
+      // every edge's slots, checks and class-key hash, independently (in
+      // parallel for big graphs); then the classes and aux ids in edge order
+      struct EdgePre {
+        int32_t ku, kw, tu, R, pu, pw, tab_u, tab_w;
+        int64_t Su, Sw;
+        double bytes;
+        uint64_t h;
+        int32_t stop;  // 0, or why the reference stops at this edge (1 dangling, 2 tensor missing, 3 shape, 4 capacity)
+      };
+      const int ne = g->num_edges;
+      std::vector<EdgePre> pre(ne);
+      sig_of_edge.resize(ne);
+      auto edge_pre = [&](int e) {
+        EdgePre& x = pre[e];
+        x.stop = 0;
         const int u = p.edge_from_op[e], w = p.edge_to_op[e];
         if (u < 0 || w < 0) {
-          p.host_err = ekey(kEdgePhase + (uint64_t)aux * 2, tpk::kDangling);
-          p.valid_edges = e;
-          break;
+          x.stop = 1;
+          return;
         }
-        const int ku = find_slot(u, g->edge_tensor[e]);
-        const int kw = find_slot(w, g->edge_tensor[e]);
-        if (ku < 0 || kw < 0) {
-          p.host_err = ekey(kEdgePhase + (uint64_t)aux * 2, tpk::kEdgeTensorMissing);
-          p.valid_edges = e;
-          break;
+        x.ku = find_slot(u, g->edge_tensor[e]);
+        x.kw = find_slot(w, g->edge_tensor[e]);
+        if (x.ku < 0 || x.kw < 0) {
+          x.stop = 2;
+          return;
         }
-        const int tu = spec_of(u, ku), tw = spec_of(w, kw);
+        const int tu = spec_of(u, x.ku), tw = spec_of(w, x.kw);
         const int R = rank_of(tu);
         bool same_shape = R == rank_of(tw);
         for (int d = 0; same_shape && d < R; ++d) same_shape = shape_of(tu)[d] == shape_of(tw)[d];
         if (!same_shape) {
-          p.host_err = ekey(kEdgePhase + (uint64_t)aux * 2 + 1, tpk::kShapeMismatch);
-          p.valid_edges = e;
-          break;
+          x.stop = 3;
+          return;
         }
-        const int pu = g->op_axis_begin[u + 1] - g->op_axis_begin[u];
-        const int pw = g->op_axis_begin[w + 1] - g->op_axis_begin[w];
-        const int64_t Su = p.node_base[u + 1] - p.node_base[u];
-        const int64_t Sw = p.node_base[w + 1] - p.node_base[w];
-        if (Su * Sw >= ((int64_t)1 << 31) - 4096)
-          return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "more than 2^31 pairs on one edge");
+        x.tu = tu;
+        x.R = R;
+        x.pu = g->op_axis_begin[u + 1] - g->op_axis_begin[u];
+        x.pw = g->op_axis_begin[w + 1] - g->op_axis_begin[w];
+        x.tab_u = (int32_t)table_of_p.find(x.pu)->second;
+        x.tab_w = (int32_t)table_of_p.find(x.pw)->second;
+        x.Su = p.node_base[u + 1] - p.node_base[u];
+        x.Sw = p.node_base[w + 1] - p.node_base[w];
+        if (x.Su * x.Sw >= ((int64_t)1 << 31) - 4096) {
+          x.stop = 4;
+          return;
+        }
         int64_t elements = 1;
         for (int d = 0; d < R; ++d) elements *= shape_of(tu)[d];
-        const double bytes = (double)elements * g->tensor_element_size[tu];  // graph.hpp:52-54
+        x.bytes = (double)elements * g->tensor_element_size[tu];  // graph.hpp:52-54
         // edge class key (the reference's memo key, aux_graph.hpp:257-271, plus
         // the bytes and axis counts): hashed, compared field by field on a hit
         int64_t bbits;
-        std::memcpy(&bbits, &bytes, 8);
-        const auto& sau = sa_of(u, ku);
-        const auto& saw = sa_of(w, kw);
-        uint64_t h = hash_words(0x51ed27f3c6a8b9d1ull ^ ((uint64_t)pu << 40) ^ ((uint64_t)pw << 20) ^ (uint64_t)R,
+        std::memcpy(&bbits, &x.bytes, 8);
+        uint64_t h = hash_words(0x51ed27f3c6a8b9d1ull ^ ((uint64_t)x.pu << 40) ^ ((uint64_t)x.pw << 20) ^ (uint64_t)R,
                                 &bbits, 8);
         h = hash_words(h, shape_of(tu), sizeof(int64_t) * R);
-        h = hash_words(h, sau.data(), R);
-        h = hash_words(h, saw.data(), R);
+        h = hash_words(h, sa_of(u, x.ku).data(), R);
+        x.h = hash_words(h, sa_of(w, x.kw).data(), R);
+      };
+      if (ne >= 2 * kEdgesPerItem)
+        run_pool((ne + kEdgesPerItem - 1) / kEdgesPerItem, host_workers(), [&](int it, int) {
+          for (int e = it * kEdgesPerItem; e < std::min(ne, (it + 1) * kEdgesPerItem); ++e) edge_pre(e);
+        });
+      else
+        for (int e = 0; e < ne; ++e) edge_pre(e);
+      sig_head.init(ne);
+      p.edges.reserve(ne);
+      p.valid_edges = ne;
+      for (int e = 0; e < ne; ++e) {
+        p.edge_base[e] = aux;
+        p.row_base[e] = rows;
+        const EdgePre& x = pre[e];
+        if (x.stop) {
+          if (x.stop == 4) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "more than 2^31 pairs on one edge");
+          p.host_err = ekey(kEdgePhase + (uint64_t)aux * 2 + (x.stop == 3 ? 1 : 0),
+                            x.stop == 1 ? tpk::kDangling : (x.stop == 2 ? tpk::kEdgeTensorMissing : tpk::kShapeMismatch));
+          p.valid_edges = e;
+          break;
+        }
+        const int u = p.edge_from_op[e], w = p.edge_to_op[e];
+        const int ku = x.ku, kw = x.kw, tu = x.tu, R = x.R, pu = x.pu, pw = x.pw;
+        const int64_t Su = x.Su, Sw = x.Sw;
+        const double bytes = x.bytes;
+        const auto& sau = sa_of(u, ku);
+        const auto& saw = sa_of(w, kw);
+        int32_t& head = sig_head.at(x.h);
         int32_t sig = -1;
-        auto it = sig_head.find(h);
-        for (int32_t c = it == sig_head.end() ? -1 : it->second; c >= 0; c = sig_next[c]) {
+        for (int32_t c = head; c >= 0; c = sig_next[c]) {
           const SigDesc& o = p.sigs[c];
-          if (o.R == R && o.tab_u == (int32_t)table_of_p[pu] && o.tab_w == (int32_t)table_of_p[pw] &&
+          if (o.R == R && o.tab_u == x.tab_u && o.tab_w == x.tab_w &&
               sig_pu[c] == pu && sig_pw[c] == pw && !std::memcmp(&o.bytes, &bytes, 8) &&
               !std::memcmp(sig_shape.data() + (size_t)c * tpk::kMaxR, shape_of(tu), sizeof(int64_t) * R) &&
               !std::memcmp(o.sa_u, sau.data(), R) && !std::memcmp(o.sa_w, saw.data(), R)) {
@@ -537,8 +755,8 @@ struct Builder {
         }
         if (sig < 0) {
           sig = (int32_t)p.sigs.size();
-          sig_next.push_back(it == sig_head.end() ? -1 : it->second);
-          sig_head[h] = sig;
+          sig_next.push_back(head);
+          head = sig;
           sig_pu.push_back(pu);
           sig_pw.push_back(pw);
           sig_shape.resize(sig_shape.size() + tpk::kMaxR, 0);
@@ -550,8 +768,8 @@ struct Builder {
           sd.R = R;
           sd.Su = (int32_t)Su;
           sd.Sw = (int32_t)Sw;
-          sd.tab_u = (int32_t)table_of_p[pu];
-          sd.tab_w = (int32_t)table_of_p[pw];
+          sd.tab_u = x.tab_u;
+          sd.tab_w = x.tab_w;
           for (int side = 0; side < 2; ++side) {
             SideJob j{};
             j.out = p.side_total;
@@ -572,18 +790,9 @@ struct Builder {
             sd.dt[d].odd = (E >> v) > 1;
           }
           p.sigs.push_back(sd);
-          edges_of_sig.emplace_back();
           p.total_pairs += Su * Sw;
         }
-        edges_of_sig[sig].push_back(e);
-        EdgeDesc ed{};
-        ed.aux_base = aux;
-        ed.nb_u = p.node_base[u];
-        ed.nb_w = p.node_base[w];
-        ed.wrow = wrow_of_op[w];
-        ed.sig = sig;
-        ed.e = e;
-        p.edges.push_back(ed);
+        sig_of_edge[e] = sig;
         aux += Su * Sw;
         rows += Su;
       }
@@ -591,14 +800,37 @@ struct Builder {
         p.edge_base[e] = aux;
         p.row_base[e] = rows;
       }
+      // the edge descriptors (independent per edge)
+      const int nv = p.valid_edges;
+      p.edges.resize(nv);
+      auto edge_desc = [&](int e) {
+        EdgeDesc ed{};
+        const int u = p.edge_from_op[e], w = p.edge_to_op[e];
+        ed.aux_base = p.edge_base[e];
+        ed.nb_u = p.node_base[u];
+        ed.nb_w = p.node_base[w];
+        ed.wrow = wrow_of_op[w];
+        ed.sig = sig_of_edge[e];
+        ed.e = e;
+        p.edges[e] = ed;
+      };
+      if (nv >= 2 * kEdgesPerItem)
+        run_pool((nv + kEdgesPerItem - 1) / kEdgesPerItem, host_workers(), [&](int it, int) {
+          for (int e = it * kEdgesPerItem; e < std::min(nv, (it + 1) * kEdgesPerItem); ++e) edge_desc(e);
+        });
+      else
+        for (int e = 0; e < nv; ++e) edge_desc(e);
+      // edges by class, edge order within (counting sort)
+      p.sig_edge_begin.assign(p.sigs.size() + 1, 0);
+      for (int e = 0; e < nv; ++e) ++p.sig_edge_begin[sig_of_edge[e] + 1];
+      for (size_t c = 0; c < p.sigs.size(); ++c) p.sig_edge_begin[c + 1] += p.sig_edge_begin[c];
+      p.sig_edges.resize(nv);
+      std::vector<int32_t> fill(p.sig_edge_begin.begin(), p.sig_edge_begin.end() - 1);
+      for (int e = 0; e < nv; ++e) p.sig_edges[fill[sig_of_edge[e]]++] = e;
     }
     p.num_aux_edges = aux;
     p.num_rows = rows;
-    p.sig_edge_begin.push_back(0);
-    for (auto& v : edges_of_sig) {
-      for (int e : v) p.sig_edges.push_back(e);
-      p.sig_edge_begin.push_back((int32_t)p.sig_edges.size());
-    }
+    if (p.sig_edge_begin.empty()) p.sig_edge_begin.push_back(0);
     for (int i = 0; i < p.valid_ops; ++i)
       if (p.in_deg[i] == 0) p.num_virtual += p.node_base[i + 1] - p.node_base[i];
     for (auto& sd : p.sigs) {
@@ -611,9 +843,8 @@ struct Builder {
     if (st) return st;
     layout_tables(p.overrides.empty());
     double tc6 = prof ? clk() : 0;
-    p.fsegs.clear();
-    p.fsegs.reserve(p.edges.size());
-    for (size_t e = 0; e < p.edges.size(); ++e) {
+    p.fsegs.resize(p.edges.size());
+    auto fan_seg = [&](size_t e) {
       const EdgeDesc& ed = p.edges[e];
       const SigDesc& sg = p.sigs[ed.sig];
       const SigDesc& bs = p.sigs[sg.base];
@@ -637,8 +868,16 @@ struct Builder {
       f.need = bs.Un * bs.Wn;
       f.bytes = bs.bytes;
       f.ovr = bs.has_override;
-      p.fsegs.push_back(f);
-    }
+      p.fsegs[e] = f;
+    };
+    const int nseg = (int)p.edges.size();
+    if (nseg >= 2 * kEdgesPerItem)
+      run_pool((nseg + kEdgesPerItem - 1) / kEdgesPerItem, host_workers(), [&](int it, int) {
+        for (int e = it * kEdgesPerItem; e < std::min(nseg, (it + 1) * kEdgesPerItem); ++e) fan_seg(e);
+      });
+    else
+      for (int e = 0; e < nseg; ++e) fan_seg(e);
+    const double tc7 = prof ? clk() : 0;
     p.pair_sig.assign(p.total_pairs, 0);
     for (size_t c = 0; c < p.sigs.size(); ++c)
       if (p.sigs[c].base == (int32_t)c)
@@ -649,8 +888,9 @@ struct Builder {
       std::fill(p.row_cls.begin() + p.classes[c].row_base, p.row_cls.begin() + p.classes[c].row_base + p.classes[c].S,
                 (int32_t)c);
     if (prof)
-      fprintf(stderr, "[tp host] check %.0f us, graph %.0f, node phase %.0f, edge phase %.0f, memo %.0f, tables %.0f, rest %.0f\n",
-              tc1 - tc0, tc2 - tc1, tc3 - tc2, tc4 - tc3, tc5 - tc4, tc6 - tc5, clk() - tc6);
+      fprintf(stderr, "[tp host] check %.0f us, graph %.0f, node phase %.0f, edge phase %.0f, memo %.0f, tables %.0f, "
+              "fan-out segments %.0f, rest %.0f\n", tc1 - tc0, tc2 - tc1, tc3 - tc2, tc4 - tc3, tc5 - tc4, tc6 - tc5,
+              tc7 - tc6, clk() - tc7);
     p.h2d_bytes = (int64_t)(p.tabs.size() * sizeof(TableDesc) + p.classes.size() * sizeof(ClassDesc) +
                             p.members.size() * sizeof(int64_t) + p.chks.size() * sizeof(SliceChk) +
                             p.slots.size() * sizeof(SlotDesc) + p.occs.size() * sizeof(Occ) +
@@ -661,37 +901,36 @@ struct Builder {
     return st;
   }
 
-  // Slots, slice checks, occurrences of one op; then its node class.
-  tp_status build_op(int i, int np, int64_t S, int64_t nb) {
-    tp_plan& p = *P;
-    HPROF(0);
+  // Slots, slice checks, occurrences of op i and the hash of its node-class
+  // key, each written into the op's own spans (no shared state: ops run in
+  // parallel). The first error in the reference's order is returned.
+  tp_status build_op(int i, int np) {
+    const tp_plan& p = *P;
     const int t0 = g->op_tensor_begin[i], t1 = g->op_tensor_begin[i + 1];
-    const int sb = (int)slot_name.size();
-    slot_begin[i] = sb;
+    int32_t* nm = slot_name.data() + t0;
+    int32_t* sp = slot_spec.data() + t0;
+    int n = 0;
     for (int t = t0; t < t1; ++t) {
       int k = -1;
-      for (int x = sb; x < (int)slot_name.size(); ++x)
-        if (slot_name[x] == g->tensor_name[t]) k = x - sb;
+      for (int x = 0; x < n; ++x)
+        if (nm[x] == g->tensor_name[t]) k = x;
       if (k < 0) {
-        k = (int)slot_name.size() - sb;
-        slot_name.push_back(g->tensor_name[t]);
-        slot_spec.push_back(t);
+        k = n++;
+        nm[k] = g->tensor_name[t];
       }
-      slot_spec[sb + k] = t;
+      sp[k] = t;
       if (rank_of(t) > tpk::kMaxR) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "tensor rank above 8");
       for (int d = 0; d < rank_of(t); ++d)
         if (shape_of(t)[d] < 1) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "tensor extent < 1 is unsupported");
     }
-    HPROF(1);
-    const int nslot = (int)slot_name.size() - sb;
-    slot_begin[i + 1] = sb + nslot;
-    if (nslot > 32000) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many tensors per op");
-    std::array<int8_t, tpk::kMaxR> none;
-    none.fill(-1);
-    slot_sa.resize(sb + nslot, none);
-    std::array<int8_t, tpk::kMaxR>* sa = slot_sa.data() + sb;
-    chk.clear();
+    if (n > 32000) return set_err(TP_ERR_CAPACITY, tpk::kCapacity, "too many tensors per op");
+    slot_cnt[i] = n;
+    std::array<int8_t, tpk::kMaxR>* sa = slot_sa.data() + t0;
+    for (int k = 0; k < n; ++k) sa[k].fill(-1);
     const int a0 = g->op_axis_begin[i];
+    const int s0 = np > 0 ? g->axis_slice_begin[a0] : 0;
+    const int s1 = np > 0 ? g->axis_slice_begin[a0 + np] : 0;
+    SliceChk* chk = chk_all.data() + s0;
     for (int a = 0; a < np; ++a) {
       for (int s = g->axis_slice_begin[a0 + a]; s < g->axis_slice_begin[a0 + a + 1]; ++s) {
         const int k = find_slot(i, g->slice_tensor[s]);
@@ -701,81 +940,92 @@ struct Builder {
         c.v = 0;
         if (k >= 0) {
           const int dim = g->slice_dim[s];
-          const int tk = spec_of(i, k);
+          const int tk = sp[k];
           if (dim < 0 || dim >= rank_of(tk))
             return set_err(TP_ERR_INVALID_ARGUMENT, 0, "slice dimension out of range");
           c.v = (int8_t)v2_capped(shape_of(tk)[dim]);
           sa[k][dim] = (int8_t)a;  // later slices overwrite (layout.hpp:366)
         }
-        chk.push_back(c);
+        chk[s - s0] = c;
       }
     }
-    HPROF(2);
-    slots.clear();
-    for (int k = 0; k < nslot; ++k) {
+    SlotDesc* slots = slots_all.data() + t0;
+    for (int k = 0; k < n; ++k) {
       SlotDesc sd{};
-      const int tk = spec_of(i, k);
+      const int tk = sp[k];
       int64_t el = 1;
       for (int d = 0; d < rank_of(tk); ++d) el *= shape_of(tk)[d];
       sd.elements = el;
       sd.es = g->tensor_element_size[tk];
       sd.R = (int8_t)rank_of(tk);
       for (int d = 0; d < tpk::kMaxR; ++d) sd.sa[d] = sa[k][d];
-      slots.push_back(sd);
+      slots[k] = sd;
     }
-    HPROF(3);
-    occ.clear();
+    Occ* occ = occ_all.data() + t0;
     const int nin = g->op_num_inputs[i];
     const int32_t* fed0 = fed_list.data() + fed_begin[op_key[i]];
     const int32_t* fed1 = fed_list.data() + fed_begin[op_key[i] + 1];
     for (int t = t0; t < t1; ++t) {
       Occ oc{};
-      const int nm = g->tensor_name[t];
-      oc.slot = (int16_t)find_slot(i, nm);
+      const int name = g->tensor_name[t];
+      oc.slot = (int16_t)find_slot(i, name);
       uint8_t mask = 0;
       for (int a = 0; a < np; ++a) {
         bool slices = false;
         for (int s = g->axis_slice_begin[a0 + a]; s < g->axis_slice_begin[a0 + a + 1]; ++s)
-          slices |= g->slice_tensor[s] == nm;
+          slices |= g->slice_tensor[s] == name;
         if (!slices) mask |= (uint8_t)(1u << a);
       }
       oc.nonslicing = mask;
       if (t - t0 < nin) {
         bool fed = false;  // aux_graph.hpp:155-162
-        for (const int32_t* x = fed0; x < fed1; ++x) fed |= *x == nm;
+        for (const int32_t* x = fed0; x < fed1; ++x) fed |= *x == name;
         oc.in_memory = !fed;
       } else {
         oc.in_memory = 1;
       }
-      occ.push_back(oc);
+      occ[t - t0] = oc;
     }
-    HPROF(4);
     // node class key: everything the per-node costs depend on -- the axis
     // count, the in-degree and the slice checks, slots and occurrences (POD,
     // padding zeroed), hashed as words and compared bytewise on a hit
-    uint64_t h = hash_words(0x9e3779b97f4a7c15ull ^ ((uint64_t)np << 32) ^ (uint64_t)(uint32_t)p.in_deg[i], chk.data(),
-                            chk.size() * sizeof(SliceChk));
-    h = hash_words(h ^ chk.size(), slots.data(), slots.size() * sizeof(SlotDesc));
-    h = hash_words(h ^ slots.size(), occ.data(), occ.size() * sizeof(Occ));
-    HPROF(5);
+    const size_t nchk = (size_t)(s1 - s0), nocc = (size_t)(t1 - t0);
+    uint64_t h = hash_words(0x9e3779b97f4a7c15ull ^ ((uint64_t)np << 32) ^ (uint64_t)(uint32_t)p.in_deg[i], chk,
+                            nchk * sizeof(SliceChk));
+    h = hash_words(h ^ nchk, slots, (size_t)n * sizeof(SlotDesc));
+    op_hash[i] = hash_words(h ^ (size_t)n, occ, nocc * sizeof(Occ));
+    return TP_OK;
+  }
+
+  // Op i (aux nodes [nb, nb + S)) joins its node class, a new one if no
+  // earlier op had an equal key.
+  void add_to_class(int i, int np, int64_t S, int64_t nb) {
+    tp_plan& p = *P;
+    const int t0 = g->op_tensor_begin[i];
+    const int s0 = np > 0 ? g->axis_slice_begin[g->op_axis_begin[i]] : 0;
+    const int nchk = np > 0 ? g->axis_slice_begin[g->op_axis_begin[i] + np] - s0 : 0;
+    const int nslot = slot_cnt[i], nocc = g->op_tensor_begin[i + 1] - t0;
+    const SliceChk* chk = chk_all.data() + s0;
+    const SlotDesc* slots = slots_all.data() + t0;
+    const Occ* occ = occ_all.data() + t0;
+    int32_t& head = class_head.at(op_hash[i]);
     int32_t cls = -1;
-    auto it = class_head.find(h);
-    for (int32_t c = it == class_head.end() ? -1 : it->second; c >= 0; c = class_next[c]) {
+    for (int32_t c = head; c >= 0; c = class_next[c]) {
       const ClassDesc& cd = p.classes[c];
-      if (cd.p == np && cd.indeg == (double)p.in_deg[i] && cd.chk_end - cd.chk_begin == (int)chk.size() &&
-          class_nslot[c] == (int)slots.size() && cd.occ_end - cd.occ_begin == (int)occ.size() &&
-          !std::memcmp(p.chks.data() + cd.chk_begin, chk.data(), chk.size() * sizeof(SliceChk)) &&
-          !std::memcmp(p.slots.data() + cd.slot_begin, slots.data(), slots.size() * sizeof(SlotDesc)) &&
-          !std::memcmp(p.occs.data() + cd.occ_begin, occ.data(), occ.size() * sizeof(Occ))) {
+      if (cd.p == np && cd.indeg == (double)p.in_deg[i] && cd.chk_end - cd.chk_begin == nchk &&
+          class_nslot[c] == nslot && cd.occ_end - cd.occ_begin == nocc &&
+          !std::memcmp(p.chks.data() + cd.chk_begin, chk, nchk * sizeof(SliceChk)) &&
+          !std::memcmp(p.slots.data() + cd.slot_begin, slots, nslot * sizeof(SlotDesc)) &&
+          !std::memcmp(p.occs.data() + cd.occ_begin, occ, nocc * sizeof(Occ))) {
         cls = c;
         break;
       }
     }
     if (cls < 0) {
       cls = (int32_t)p.classes.size();
-      class_next.push_back(it == class_head.end() ? -1 : it->second);
-      class_head[h] = cls;
-      class_nslot.push_back((int32_t)slots.size());
+      class_next.push_back(head);
+      head = cls;
+      class_nslot.push_back(nslot);
       ClassDesc cd{};
       cd.row_base = p.total_rows;
       cd.first_node = nb;
@@ -784,22 +1034,20 @@ struct Builder {
       cd.p = np;
       cd.table = (int32_t)table_of_p[np];
       cd.chk_begin = (int32_t)p.chks.size();
-      p.chks.insert(p.chks.end(), chk.begin(), chk.end());
+      p.chks.insert(p.chks.end(), chk, chk + nchk);
       cd.chk_end = (int32_t)p.chks.size();
       cd.slot_begin = (int32_t)p.slots.size();
-      p.slots.insert(p.slots.end(), slots.begin(), slots.end());
+      p.slots.insert(p.slots.end(), slots, slots + nslot);
       cd.occ_begin = (int32_t)p.occs.size();
-      p.occs.insert(p.occs.end(), occ.begin(), occ.end());
+      p.occs.insert(p.occs.end(), occ, occ + nocc);
       cd.occ_end = (int32_t)p.occs.size();
       p.classes.push_back(cd);
       class_members.emplace_back();
       p.total_rows += S;
     }
-    HPROF(6);
     class_members[cls].push_back(nb);
     wrow_of_op[i] = p.classes[cls].row_base;
     p.op_row[i] = p.classes[cls].row_base;
-    return TP_OK;
   }
 
   // Class tables over distinct layouts. A pair's price is a function of the
@@ -1032,124 +1280,5 @@ void arena_pool_put(Arena* a) {
   g_pool[a->device & 63].push_back(a);
 }
 
-int pool_size(int n, int host_threads) {
-  int t = host_threads > 0 ? host_threads : (int)std::min(32u, std::max(1u, std::thread::hardware_concurrency()));
-  return std::max(1, std::min(t, n));
-}
-
-// A persistent pool of host workers: a sweep calls run_pool several times
-// per chunk, and spawning 16 threads costs ~0.5 ms each time. Workers sleep
-// on a condition variable between jobs. One job at a time: a caller that finds
-// the pool busy (another device's batch on another thread) or that is itself
-// a worker runs its items inline.
-class HostPool {
- public:
-  static HostPool& get() {
-    static HostPool* p = new HostPool();  // never destroyed: no join at process exit
-    return *p;
-  }
-  int size() const { return (int)th_.size() + 1; }
-  // fn(item, worker) over [0, n) on min(workers, size()) threads (the caller is worker 0)
-  void run(int n, int workers, const std::function<void(int, int)>& fn, int device) {
-    std::unique_lock<std::mutex> busy(run_mu_, std::try_to_lock);
-    if (!busy.owns_lock() || t_in_worker) {
-      for (int i = 0; i < n; ++i) fn(i, 0);
-      return;
-    }
-    workers = std::max(1, std::min(workers, size()));
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      fn_ = &fn;
-      n_ = n;
-      device_ = device;
-      next_.store(0);
-      want_ = workers - 1;
-      running_ = workers - 1;
-      ++gen_;
-    }
-    cv_.notify_all();
-    for (int i = next_.fetch_add(1); i < n; i = next_.fetch_add(1)) fn(i, 0);
-    std::unique_lock<std::mutex> lk(mu_);
-    done_.wait(lk, [&] { return running_ == 0; });
-    fn_ = nullptr;
-  }
-
- private:
-  HostPool() {
-    const int hw = (int)std::min(32u, std::max(1u, std::thread::hardware_concurrency()));
-    for (int w = 1; w < hw; ++w) th_.emplace_back([this, w] { loop(w); });
-  }
-  void loop(int w) {
-    t_in_worker = true;
-    uint64_t seen = 0;
-    int dev = -1;
-    for (;;) {
-      std::unique_lock<std::mutex> lk(mu_);
-      cv_.wait(lk, [&] { return gen_ != seen; });
-      seen = gen_;
-      if (w > want_) continue;  // not needed for this job
-      const std::function<void(int, int)>* fn = fn_;
-      const int n = n_, device = device_;
-      lk.unlock();
-      if (device >= 0 && device != dev) {
-        cudaSetDevice(device);  // a new host thread starts on device 0
-        dev = device;
-      }
-      for (int i = next_.fetch_add(1); i < n; i = next_.fetch_add(1)) (*fn)(i, w);
-      lk.lock();
-      if (--running_ == 0) done_.notify_all();
-    }
-  }
-  static thread_local bool t_in_worker;
-  std::vector<std::thread> th_;
-  std::mutex run_mu_, mu_;
-  std::condition_variable cv_, done_;
-  const std::function<void(int, int)>* fn_ = nullptr;
-  int n_ = 0, device_ = -1, want_ = 0, running_ = 0;
-  uint64_t gen_ = 0;
-  std::atomic<int> next_{0};
-};
-thread_local bool HostPool::t_in_worker = false;
-
-// fn(item, worker) over items [0, n), items claimed one at a time, on up to
-// `workers` pool threads (pool_size) with `device` current.
-template <typename F>
-void run_pool(int n, int workers, F&& fn, int device = -1) {
-  workers = pool_size(n, workers);
-  if (workers <= 1) {
-    for (int i = 0; i < n; ++i) fn(i, 0);
-    return;
-  }
-  const std::function<void(int, int)> f = [&](int i, int w) { fn(i, w); };
-  HostPool::get().run(n, workers, f, device);
-}
-
-// a worker's status and message (tp_last_error is per thread)
-struct BatchErr {
-  tp_status st = TP_OK;
-  int kind = 0;
-  std::string msg;
-  void take(tp_status s) {
-    st = s;
-    if (s) {
-      kind = g_err_kind;
-      msg = g_err;
-    }
-  }
-};
-
-tp_status batch_status(const std::vector<BatchErr>& errs, int32_t* status_out) {
-  const BatchErr* first = nullptr;
-  for (size_t i = 0; i < errs.size(); ++i) {
-    if (status_out) status_out[i] = errs[i].st;
-    if (errs[i].st && !first) first = &errs[i];
-  }
-  if (!first) {
-    g_err[0] = 0;
-    g_err_kind = 0;
-    return TP_OK;
-  }
-  return set_err(first->st, first->kind, first->msg);
-}
 }  // namespace
 

@@ -1,5 +1,4 @@
 // Host-analysis probe: the engine's Builder on a dumped graph, no GPU needed.
-#define TP_HOST_PROF 1
 #include "../../paper_2301_04285_b200/csrc/tp_engine.cu"
 #include <cstdlib>
 #include <vector>
@@ -37,6 +36,5 @@ int main(int argc, char** argv) {
     delete p;
   }
   printf("best Builder::run %.0f us\n", best);
-  for (int k = 1; k < 8; ++k) printf("  build_op section %d: %.0f us per run\n", k, g_hprof[k] / reps);
   return 0;
 }
