@@ -1228,15 +1228,23 @@ tp_status tp_plan_check_errors(tp_plan* p) {
 namespace {
 // tp_plan_execute_host; with key_out the smallest error key is returned
 // there instead of as a status (the multi-device build combines its devices').
+thread_local char p_exec_detail[256];
+bool prof_host() {
+  static const bool prof = getenv("TP_PROFILE_HOST") != nullptr;
+  return prof;
+}
+
 tp_status execute_host_impl(tp_plan* p, const tp_build_opts* opts, tp_aux_index* index_out,
                             tp_cost_tensors* host_out, uint64_t* key_out) {
   if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
+  const double tx0 = prof_host() ? now_us() : 0;
   tp_status st = ensure_stream(p);
   if (st) return st;
   if (!p->uploaded) {
     st = tp_plan_upload(p, nullptr);
     if (st) return st;
   }
+  const double tx0b = prof_host() ? now_us() : 0;
   int32_t e0 = opts ? opts->edge_begin : 0;
   int32_t e1 = opts ? opts->edge_end : -1;
   if (e1 < 0 || e1 > p->valid_edges) e1 = p->valid_edges;
@@ -1269,10 +1277,12 @@ tp_status execute_host_impl(tp_plan* p, const tp_build_opts* opts, tp_aux_index*
   d.edge_pair_min_cost_s = (double*)dev(b[9], h.edge_pair_min_cost_s, e1 - e0, 8);
   d.edge_pair_min_volume_bytes = (double*)dev(b[10], h.edge_pair_min_volume_bytes, e1 - e0, 8);
   if (oom) return set_err(TP_ERR_CUDA, 0, "device allocation for the outputs failed");
+  const double tx1 = prof_host() ? now_us() : 0;
   tp_build_opts o = opts ? *opts : tp_build_opts{0, -1, 0, -1, nullptr};
   o.stream = nullptr;
   st = tp_plan_execute(p, &o, &d);
   if (st) return st;
+  const double tx2 = prof_host() ? now_us() : 0;
   cudaStream_t s = p->arena->stream;
   auto back = [&](void* hst, void* dv, int64_t n, size_t el) -> cudaError_t {
     if (!hst || !dv || n <= 0) return cudaSuccess;
@@ -1292,8 +1302,12 @@ tp_status execute_host_impl(tp_plan* p, const tp_build_opts* opts, tp_aux_index*
   ce = ce ? ce : back(h.row_min_volume_bytes, d.row_min_volume_bytes, nr, 8);
   ce = ce ? ce : back(h.edge_pair_min_cost_s, d.edge_pair_min_cost_s, e1 - e0, 8);
   ce = ce ? ce : back(h.edge_pair_min_volume_bytes, d.edge_pair_min_volume_bytes, e1 - e0, 8);
+  const double tx3 = prof_host() ? now_us() : 0;
   if (key_out) st = plan_error_key(p, *key_out);  // synchronises the stream
   else st = tp_plan_check_errors(p);
+  if (prof_host())
+    snprintf(p_exec_detail, sizeof(p_exec_detail), "upload %.0f, outputs %.0f, execute enqueue %.0f, copies enqueue %.0f, wait %.0f",
+             tx0b - tx0, tx1 - tx0b, tx2 - tx1, tx3 - tx2, now_us() - tx3);
   if (ce != cudaSuccess) return set_err(TP_ERR_CUDA, 0, cudaGetErrorString(ce));
   if (st) return st;
   if (index_out) tp_plan_index(p, index_out);
@@ -1313,13 +1327,20 @@ tp_status tp_build_cost_tensors(const tp_graph_desc* graph, const tp_topology_de
                                 const tp_build_opts* opts, tp_aux_index* index_out,
                                 tp_cost_tensors* host_out) {
   DeviceGuard dg;
+  static const bool prof = getenv("TP_PROFILE_HOST") != nullptr;
+  const double t0 = prof ? now_us() : 0;
   tp_plan* p = nullptr;
   tp_status st = tp_plan_create(graph, topo, opts ? opts->device : -1, &p);
   if (st) return st;
+  const double t1 = prof ? now_us() : 0;
   p->arena = thread_arena(p->device);  // reused across one-shot calls
   p->owns_arena = p->arena == nullptr;
   st = tp_plan_execute_host(p, opts, index_out, host_out);
+  const double t2 = prof ? now_us() : 0;
   tp_plan_destroy(p);
+  if (prof)
+    fprintf(stderr, "[tp one-shot] create %.0f us, execute_host %.0f us (%s), destroy %.0f us\n", t1 - t0, t2 - t1,
+            p_exec_detail, now_us() - t2);
   return st;
 }
 

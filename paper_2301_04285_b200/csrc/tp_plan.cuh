@@ -233,6 +233,11 @@ double now_us() {
   return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// The host analysis of one graph runs its per-op / per-edge passes on the
+// worker pool from this many ops / edges on (TP_HOST_WORKERS: how many
+// workers, default all).
+// TP_HOST_PAR_MIN overrides the threshold (tests force the parallel passes).
+const int kParallelItems = getenv("TP_HOST_PAR_MIN") ? std::max(1, atoi(getenv("TP_HOST_PAR_MIN"))) : 8192;
 // workers for the host analysis of one graph (TP_HOST_WORKERS, default all)
 int host_workers() {
   static const int w = getenv("TP_HOST_WORKERS") ? atoi(getenv("TP_HOST_WORKERS")) : 0;
@@ -622,11 +627,13 @@ struct Builder {
       occ_all.resize(nt);
       op_hash.resize(nops);
       std::vector<BatchErr> op_err(lim);
-      constexpr int kOpsPerItem = 64;
-      const int items = (lim + kOpsPerItem - 1) / kOpsPerItem;
-      run_pool(lim >= 2 * kOpsPerItem ? items : 1, host_workers(), [&](int it, int) {
-        const int i1 = lim >= 2 * kOpsPerItem ? std::min(lim, (it + 1) * kOpsPerItem) : lim;
-        for (int i = lim >= 2 * kOpsPerItem ? it * kOpsPerItem : 0; i < i1; ++i)
+      // (measured: the pool's dispatch costs more than it saves below a few
+      // thousand ops -- cfg4's 1,152 ops take ~155 us on one thread)
+      const int kOpsPerItem = std::max(1, std::min(256, kParallelItems / 32));
+      const bool par = lim >= kParallelItems && lim > kOpsPerItem;
+      run_pool(par ? (lim + kOpsPerItem - 1) / kOpsPerItem : 1, host_workers(), [&](int it, int) {
+        const int i1 = par ? std::min(lim, (it + 1) * kOpsPerItem) : lim;
+        for (int i = par ? it * kOpsPerItem : 0; i < i1; ++i)
           op_err[i].take(build_op(i, g->op_axis_begin[i + 1] - g->op_axis_begin[i]));
       });
       for (int i = 0; i < lim; ++i)  // the first failing op, in order
@@ -654,7 +661,7 @@ struct Builder {
     std::vector<int32_t> sig_next, sig_pu, sig_pw;
     std::vector<int64_t> sig_shape;  // kMaxR extents per class
     std::vector<int32_t> sig_of_edge;
-    constexpr int kEdgesPerItem = 128;
+    const int kEdgesPerItem = std::max(1, std::min(512, kParallelItems / 16));
     if (p.host_err == ~0ull) {
       // every edge's slots, checks and class-key hash, independently (in
       // parallel for big graphs); then the classes and aux ids in edge order
@@ -715,7 +722,7 @@ struct Builder {
         h = hash_words(h, sa_of(u, x.ku).data(), R);
         x.h = hash_words(h, sa_of(w, x.kw).data(), R);
       };
-      if (ne >= 2 * kEdgesPerItem)
+      if (ne >= kParallelItems)
         run_pool((ne + kEdgesPerItem - 1) / kEdgesPerItem, host_workers(), [&](int it, int) {
           for (int e = it * kEdgesPerItem; e < std::min(ne, (it + 1) * kEdgesPerItem); ++e) edge_pre(e);
         });
@@ -814,7 +821,7 @@ struct Builder {
         ed.e = e;
         p.edges[e] = ed;
       };
-      if (nv >= 2 * kEdgesPerItem)
+      if (nv >= kParallelItems)
         run_pool((nv + kEdgesPerItem - 1) / kEdgesPerItem, host_workers(), [&](int it, int) {
           for (int e = it * kEdgesPerItem; e < std::min(nv, (it + 1) * kEdgesPerItem); ++e) edge_desc(e);
         });
@@ -871,7 +878,7 @@ struct Builder {
       p.fsegs[e] = f;
     };
     const int nseg = (int)p.edges.size();
-    if (nseg >= 2 * kEdgesPerItem)
+    if (nseg >= kParallelItems)
       run_pool((nseg + kEdgesPerItem - 1) / kEdgesPerItem, host_workers(), [&](int it, int) {
         for (int e = it * kEdgesPerItem; e < std::min(nseg, (it + 1) * kEdgesPerItem); ++e) fan_seg(e);
       });

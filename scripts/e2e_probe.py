@@ -12,7 +12,7 @@ gd, td = f.desc(), t.desc()
 def now():
     torch.cuda.synchronize()
     return time.perf_counter()
-for rep in range(4):
+for rep in range(6):
     t0 = now()
     plan = E.Plan(f, t, device=0)
     t1 = now()

@@ -367,3 +367,53 @@ def test_cfg4_minima_properties():
             assert bits(np.array([rm.min()]))[0] == bits(getattr(ct, pair)[e:e + 1])[0], (e, pair)
         r += su_n
     assert r == len(ct.row_min_cost_s)
+
+
+PAR_CHECK = r"""
+import random, sys
+sys.path.insert(0, {repo!r}); sys.path.insert(0, {repo!r} + "/tests")
+import numpy as np
+from oracle import bindings as B
+from paper_2301_04285_b200 import abi, engine, fuzz, graph as G, models as M
+from golden_util import bits
+def same(a, b):
+    for k in ("node_base", "edge_base", "in_degree", "out_degree", "topo_order", "edge_from_op", "edge_to_op"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+    for k in ("node_intra_cost_s", "node_intra_volume_bytes", "node_memory_bytes", "edge_cost_s",
+              "edge_volume_bytes", "edge_memory_bytes"):
+        assert np.array_equal(bits(getattr(a, k)), bits(getattr(b, k))), k
+rng = random.Random(99)
+n_ok = n_err = 0
+for i in range(120):
+    g, t = fuzz.random_graph(rng, odd_extents=(i % 2 == 0), mixed_element_sizes=(i % 5 == 0))
+    f = G.flatten(g)
+    ref = B.oracle_build(f, t)
+    if ref.status != 0:
+        try:
+            engine.build_cost_tensors(f, t)
+            raise SystemExit("expected an error at graph %d" % i)
+        except (abi.TopoplanError, IndexError):
+            n_err += 1
+        continue
+    same(engine.build_cost_tensors(f, t), ref)
+    n_ok += 1
+for g, t in (M.cfg2(), M.cfg3(2, 10)):
+    f = G.flatten(g)
+    same(engine.build_cost_tensors(f, t), B.oracle_build(f, t))
+print("par ok", n_ok, n_err)
+"""
+
+
+def test_parallel_host_analysis_matches_oracle():
+    """The host analysis's per-op / per-edge passes on the worker pool (forced
+    on small graphs, one op or edge per work item) give the oracle's bits and
+    the reference's errors."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TP_HOST_PAR_MIN="1", TP_HOST_WORKERS="8")
+    r = subprocess.run([sys.executable, "-c", PAR_CHECK.format(repo=repo)], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "par ok" in r.stdout
