@@ -1,5 +1,5 @@
 # A/B of prebuilt engine variants (_variants/*.so, git-ignored): parity tests of the in-tree
-# build, then fan_probe.py and the cfg5 bench on each variant twice; VARIANTS picks them.
+# build, then fan_probe.py (FAN=1) and the cfg5 bench (unless NO5=1) on each variant; VARIANTS picks them.
 mkdir -p gpurun_out
 TAG=${TAG:-ab}
 timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_sweep.py tests/test_gpu_multidevice.py -x -q > gpurun_out/pytest_${TAG}.log 2>&1
@@ -10,7 +10,7 @@ for v in ${VARIANTS:-base new base new}; do
   cp _variants/$v.so paper_2301_04285_b200/libtaps_b200.so
   echo "== $v" >> gpurun_out/ab_${TAG}.log
   [ -n "$FAN" ] && python scripts/fan_probe.py 2>&1 | grep "^build " >> gpurun_out/ab_${TAG}.log
-  timeout 600 python bench.py --workload cfg5 --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 3 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('cfg5', d['ms_per_step'], d['config']['build_ms_e2e'])" >> gpurun_out/ab_${TAG}.log
+  [ -z "$NO5" ] && timeout 600 python bench.py --workload cfg5 --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 3 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('cfg5', d['ms_per_step'], d['config']['build_ms_e2e'])" >> gpurun_out/ab_${TAG}.log
 done
 cp /tmp/keep.so paper_2301_04285_b200/libtaps_b200.so
 if [ -n "$NCU5" ]; then
