@@ -1454,10 +1454,7 @@ tp_status execute_host_multi(tp_plan* p, const int32_t* devices, int32_t n, tp_a
       q->range_key = {{-1, -1, -1, -1}};
     }
   };
-  std::vector<std::thread> th;
-  for (int i = 1; i < n; ++i) th.emplace_back(work, i);
-  work(0);
-  for (auto& t : th) t.join();
+  run_pool(n, n, [&](int i, int) { work(i); });  // one pool worker per device (no thread spawns per call)
   for (int i = 0; i < n; ++i)
     if (st[i]) return set_err(st[i], kinds[i], msg[i]);
   uint64_t key = ~0ull;

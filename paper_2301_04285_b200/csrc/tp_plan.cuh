@@ -294,7 +294,6 @@ class HostPool {
   void loop(int w) {
     t_in_worker = true;
     uint64_t seen = 0;
-    int dev = -1;
     for (;;) {
       std::unique_lock<std::mutex> lk(mu_);
       cv_.wait(lk, [&] { return gen_ != seen; });
@@ -303,10 +302,8 @@ class HostPool {
       const std::function<void(int, int)>* fn = fn_;
       const int n = n_, device = device_;
       lk.unlock();
-      if (device >= 0 && device != dev) {
-        cudaSetDevice(device);  // a new host thread starts on device 0
-        dev = device;
-      }
+      // a new host thread starts on device 0, and a job may have switched it
+      if (device >= 0) cudaSetDevice(device);
       for (int i = next_.fetch_add(1); i < n; i = next_.fetch_add(1)) (*fn)(i, w);
       lk.lock();
       if (--running_ == 0) done_.notify_all();

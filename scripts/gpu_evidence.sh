@@ -8,10 +8,12 @@ timeout 1200 ./oracle/_ref/adapter_parity > gpurun_out/adapter_parity_${TAG}.log
 ./oracle/_ref/export_parity --big > gpurun_out/export_parity_${TAG}.log 2>&1; echo "rc=$?" >> gpurun_out/export_parity_${TAG}.log
 python scripts/fan_probe.py > gpurun_out/fan_${TAG}.log 2>&1
 python scripts/class_probe.py > gpurun_out/class_${TAG}.log 2>&1
+TP_PROFILE_HOST=1 timeout 300 python scripts/e2e_probe.py > gpurun_out/e2e_probe_${TAG}.log 2>&1
+TP_PROFILE_HOST=1 timeout 300 python scripts/sweep_probe.py > gpurun_out/sweep_probe_${TAG}.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_${TAG}.json 2> gpurun_out/bench_ref_${TAG}.err
 timeout 900 python bench.py --impl reference --workload cfg5 --steps 3 > gpurun_out/bench_ref_cfg5_${TAG}.json 2> gpurun_out/bench_ref_cfg5_${TAG}.err
-for C in 12 16; do TP_SWEEP_CHUNKS=$C timeout 600 python bench.py --workload cfg5 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 6 > gpurun_out/cfg5_c${C}_${TAG}.json 2>/dev/null; done
+for C in 12 24; do TP_SWEEP_CHUNKS=$C timeout 600 python bench.py --workload cfg5 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 6 > gpurun_out/cfg5_c${C}_${TAG}.json 2>/dev/null; done
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 3 --no-sweep --no-configs"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launches_${TAG}.log 2>&1
