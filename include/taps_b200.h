@@ -224,6 +224,14 @@ tp_status tp_plan_execute(tp_plan* plan, const tp_build_opts* opts,
  * (the one-shot call on an existing plan; synchronous). */
 tp_status tp_plan_execute_host(tp_plan* plan, const tp_build_opts* opts,
                                tp_aux_index* index_out, tp_cost_tensors* host_out);
+/* tp_plan_execute_host on the calling thread's scratch device memory (the
+ * buffers tp_build_cost_tensors reuses across calls) instead of the plan's
+ * own: no device allocation or release when the thread built a graph of the
+ * same sizes before, and the plan keeps no device state afterwards (a plan
+ * that already has its own device memory uses it). For callers that build
+ * once per plan -- the C++ drop-in (include/taps_b200/aux_graph_b200.hpp). */
+tp_status tp_plan_execute_host_scratch(tp_plan* plan, const tp_build_opts* opts,
+                                       tp_aux_index* index_out, tp_cost_tensors* host_out);
 /* tp_build_cost_tensors_multi on an analysed plan: per-device copies of the
  * plan (arenas, uploads) are kept on it for repeated executes. */
 tp_status tp_plan_execute_host_multi(tp_plan* plan, const int32_t* devices, int32_t num_devices,

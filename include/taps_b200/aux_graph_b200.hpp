@@ -21,11 +21,19 @@
 #ifndef TAPS_B200_AUX_GRAPH_B200_HPP_
 #define TAPS_B200_AUX_GRAPH_B200_HPP_
 
+#include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -112,6 +120,56 @@ inline void check_abi() {
                              " differs from the header's " + std::to_string(TP_ABI_VERSION));
 }
 
+// TAPS_B200_PROFILE=1: the phases of build_auxiliary_graph_b200 on stderr.
+struct PhaseClock {
+  bool on = std::getenv("TAPS_B200_PROFILE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  std::string line;
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    char buf[96];
+    std::snprintf(buf, sizeof(buf), "%s%s %.2f ms", line.empty() ? "" : ", ", what,
+                  std::chrono::duration<double, std::milli>(now - t).count());
+    line += buf;
+    t = now;
+  }
+  void report() const {
+    if (on) std::fprintf(stderr, "[taps_b200] build_auxiliary_graph_b200: %s\n", line.c_str());
+  }
+};
+
+// fn(i) for i in [0, n) on up to hardware_concurrency threads (or
+// TAPS_B200_THREADS), at least `per_thread` items each (fewer items: the
+// calling thread alone); the first exception of any item is rethrown here.
+template <typename F>
+inline void parallel_for(int n, int per_thread, F&& fn) {
+  const char* env = std::getenv("TAPS_B200_THREADS");
+  const int hw = env ? std::max(1, std::atoi(env)) : (int)std::max(1u, std::thread::hardware_concurrency());
+  const int T = std::min(hw, std::max(1, n / std::max(1, per_thread)));
+  if (T <= 1) {
+    for (int i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::atomic<int> next{0};
+  std::exception_ptr err;
+  std::mutex mu;
+  auto run = [&] {
+    try {
+      for (int i; (i = next.fetch_add(1)) < n;) fn(i);
+    } catch (...) {
+      std::lock_guard<std::mutex> lk(mu);
+      if (!err) err = std::current_exception();
+      next.store(n);
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t) th.emplace_back(run);
+  run();
+  for (auto& x : th) x.join();
+  if (err) std::rethrow_exception(err);
+}
+
 struct PlanGuard {
   tp_plan* p = nullptr;
   ~PlanGuard() { tp_plan_destroy(p); }
@@ -162,16 +220,20 @@ inline topoplan::AuxiliaryGraph build_auxiliary_graph_b200(const topoplan::Compu
                                                            SolverMinima* minima = nullptr) {
   static_assert(sizeof(topoplan::AuxEdge) == 40, "AuxEdge layout differs from the device records");
   detail::check_abi();
+  detail::PhaseClock clk;
   topoplan::AuxiliaryGraph aux;
   aux.graph = graph;
+  clk.mark("graph copy");
   aux.topo = topo;
   aux.default_mode = mode;
 
   detail::FlatGraph flat(graph);
   const tp_topology_desc td{topo.node_count, topo.local_device_num, topo.intra_bandwidth, topo.inter_bandwidth,
                             topo.device_memory};
+  clk.mark("flatten");
   detail::PlanGuard plan;
   detail::check(tp_plan_create(&flat.desc, &td, device, &plan.p));
+  clk.mark("plan create");
   tp_plan_sizes_t sz{};
   detail::check(tp_plan_sizes(plan.p, &sz));
   const int n_ops = (int)graph.operators.size(), n_edges = (int)graph.edges.size();
@@ -198,7 +260,10 @@ inline topoplan::AuxiliaryGraph build_auxiliary_graph_b200(const topoplan::Compu
     out.edge_pair_min_cost_s = minima->pair_min_cost_s.data();
     out.edge_pair_min_volume_bytes = minima->pair_min_volume_bytes.data();
   }
-  detail::check(tp_plan_execute_host(plan.p, nullptr, &ix, &out));
+  clk.mark("output allocation");
+  // (the thread's reused device memory: a plan built once needs none of its own)
+  detail::check(tp_plan_execute_host_scratch(plan.p, nullptr, &ix, &out));
+  clk.mark("execute + D2H");
 
   if (minima) {
     minima->row_min_cost_s.resize(sz.num_rows);
@@ -234,10 +299,16 @@ inline topoplan::AuxiliaryGraph build_auxiliary_graph_b200(const topoplan::Compu
       v[s].device_matrix.dims.assign(dims.begin() + s * p, dims.begin() + s * p + depth[s]);
     }
   }
+  clk.mark("index + strategy tables");
   aux.nodes.resize(sz.num_aux_nodes);
-  for (int i = 0; i < n_ops; ++i) {
-    const auto& tab = tables[graph.operators[i].axis_count()];
-    for (int64_t s = 0; s < node_base[i + 1] - node_base[i]; ++s) {
+  // every operator's aux nodes independently (strategy copies and, with
+  // layouts, a std::map per node: most of the adapter's host time), on the
+  // host's cores for big graphs
+  detail::parallel_for(n_ops, sz.num_aux_nodes >= 16384 ? 16 : n_ops + 1, [&](int i) {
+    const auto& tab = tables.at(graph.operators[i].axis_count());
+    const int64_t S = node_base[i + 1] - node_base[i];
+    aux.nodes_of_op[i].resize(S);
+    for (int64_t s = 0; s < S; ++s) {
       const int64_t id = node_base[i] + s;
       topoplan::AuxNode& node = aux.nodes[id];
       node.op_index = i;
@@ -248,9 +319,10 @@ inline topoplan::AuxiliaryGraph build_auxiliary_graph_b200(const topoplan::Compu
       node.intra_cost_s = n_sec[id];
       node.intra_volume_bytes = n_vol[id];
       node.memory_bytes = n_mem[id];
-      aux.nodes_of_op[i].push_back((int)id);
+      aux.nodes_of_op[i][s] = (int)id;
     }
-  }
+  });
+  clk.mark(with_layouts ? "nodes + layouts" : "nodes");
   // virtual source edges (aux_graph.hpp:298-312)
   aux.virtual_edge_of_node.assign(aux.nodes.size(), -1);
   for (int i = 0; i < n_ops; ++i) {
@@ -267,6 +339,11 @@ inline topoplan::AuxiliaryGraph build_auxiliary_graph_b200(const topoplan::Compu
       aux.virtual_edges.push_back(ve);
     }
   }
+  clk.mark("virtual edges");
+  tp_plan_destroy(plan.p);
+  plan.p = nullptr;
+  clk.mark("plan destroy");
+  clk.report();
   return aux;
 }
 

@@ -314,7 +314,29 @@ void check_sweep(int count, int every) {
 
 }  // namespace
 
+// --time: the C++ drop-in on cfg4 (with and without AuxNode::layouts), best of 3, and the
+// reference's build once; no parity checks (TAPS_B200_PROFILE=1 adds the adapter's phases).
+int time_cfg4() {
+  const ComputationGraph g = taps_b200::gpt_chain(96, 12288, 8, 2048);
+  const ClusterTopology topo{16, 8, 60e9, 6e9, 80e9};
+  for (int layouts = 0; layouts < 2; ++layouts) {
+    double best = 1e30;
+    for (int r = 0; r < 3; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      const AuxiliaryGraph a = taps_b200::build_auxiliary_graph_b200(g, topo, CostMode::kTopology, -1, layouts != 0);
+      best = std::min(best, ms_since(t0));
+      if (a.edges.size() != 2155580u) return 1;
+    }
+    std::printf("[TIME] cfg4 build_auxiliary_graph_b200 (layouts %d): %.1f ms (best of 3)\n", layouts, best);
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  const AuxiliaryGraph ref = build_auxiliary_graph(g, topo);
+  std::printf("[TIME] cfg4 build_auxiliary_graph (reference, one thread): %.1f ms\n", ms_since(t0));
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "--time") return time_cfg4();
   const bool big = argc > 1 && std::string(argv[1]) == "--big";  // every 10th cfg5 scenario instead of every 40th
   const ClusterTopology t2x4{2, 4, 60e9, 6e9, 32e9};
   {  // cfg1: data/sample_graph.json on 2 x 4

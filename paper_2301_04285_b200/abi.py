@@ -219,6 +219,8 @@ def load_engine() -> C.CDLL:
     lib.tp_plan_execute.restype = C.c_int
     lib.tp_plan_execute_host.argtypes = [C.c_void_p, P(tp_build_opts), P(tp_aux_index), P(tp_cost_tensors)]
     lib.tp_plan_execute_host.restype = C.c_int
+    lib.tp_plan_execute_host_scratch.argtypes = [C.c_void_p, P(tp_build_opts), P(tp_aux_index), P(tp_cost_tensors)]
+    lib.tp_plan_execute_host_scratch.restype = C.c_int
     lib.tp_plan_check_errors.argtypes = [C.c_void_p]
     lib.tp_plan_check_errors.restype = C.c_int
     lib.tp_plan_set_profile_events.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -284,7 +286,7 @@ def load_engine() -> C.CDLL:
 # Every symbol include/taps_b200.h declares (checked by the CPU test suite).
 EXPORTED_SYMBOLS = (
     "tp_build_cost_tensors", "tp_plan_create", "tp_plan_destroy", "tp_plan_sizes",
-    "tp_plan_index", "tp_plan_upload", "tp_plan_execute", "tp_plan_execute_host", "tp_plan_check_errors",
+    "tp_plan_index", "tp_plan_upload", "tp_plan_execute", "tp_plan_execute_host", "tp_plan_execute_host_scratch", "tp_plan_check_errors",
     "tp_plan_last_launches", "tp_plan_set_profile_events", "tp_plan_set_timeline", "tp_plan_timeline", "tp_plan_timeline_detail", "tp_enumerate_strategies", "tp_redistribute_batch",
     "tp_redistribute_batch_form", "tp_plan_set_pair_form", "tp_plan_create_batch", "tp_plan_execute_host_batch",
     "tp_plan_execute_batch", "tp_plan_price_assignments", "tp_plan_set_bandwidth",

@@ -1323,6 +1323,27 @@ tp_status tp_plan_execute_host(tp_plan* p, const tp_build_opts* opts, tp_aux_ind
   return execute_host_impl(p, opts, index_out, host_out, nullptr);
 }
 
+tp_status tp_plan_execute_host_scratch(tp_plan* p, const tp_build_opts* opts, tp_aux_index* index_out,
+                                       tp_cost_tensors* host_out) {
+  DeviceGuard dg;
+  if (!p) return set_err(TP_ERR_INVALID_ARGUMENT, 0, "null plan");
+  if (p->arena) return execute_host_impl(p, opts, index_out, host_out, nullptr);
+  // borrow the thread's one-shot arena for this (synchronous) call: its
+  // descriptors are this plan's only until the call returns
+  p->arena = thread_arena(p->device);
+  if (!p->arena) return execute_host_impl(p, opts, index_out, host_out, nullptr);  // (no such device: owns one)
+  p->owns_arena = false;
+  p->uploaded = false;
+  p->range_key = {{-1, -1, -1, -1}};
+  const tp_status st = execute_host_impl(p, opts, index_out, host_out, nullptr);
+  if (p->arena->stream) cudaStreamSynchronize(p->arena->stream);
+  p->arena = nullptr;
+  p->owns_arena = true;
+  p->uploaded = false;
+  p->range_key = {{-1, -1, -1, -1}};
+  return st;
+}
+
 tp_status tp_build_cost_tensors(const tp_graph_desc* graph, const tp_topology_desc* topo,
                                 const tp_build_opts* opts, tp_aux_index* index_out,
                                 tp_cost_tensors* host_out) {

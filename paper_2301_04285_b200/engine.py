@@ -204,8 +204,10 @@ class Plan:
         return tuple(o[:k] for o in outs)
 
     def execute_host(self, records=False, row_min=False, edge_range=(0, -1), skip_nodes=False,
-                     pinned=False) -> CostTensors:
-        """Synchronous build into HOST buffers (pinned if requested)."""
+                     pinned=False, scratch=False) -> CostTensors:
+        """Synchronous build into HOST buffers (pinned if requested); with
+        `scratch` on the calling thread's reused device memory
+        (tp_plan_execute_host_scratch) when the plan has none of its own."""
         ix = self.index()
         e0, e1 = edge_range
         if e1 < 0:
@@ -227,7 +229,8 @@ class Plan:
             sizes=dict(self.sizes), **ix)
         out = cost_struct(ct)
         o = abi.tp_build_opts(e0, e1, int(skip_nodes), -1, None)
-        _check(self.lib, self.lib.tp_plan_execute_host(self.handle, C.byref(o), None, C.byref(out)))
+        fn = self.lib.tp_plan_execute_host_scratch if scratch else self.lib.tp_plan_execute_host
+        _check(self.lib, fn(self.handle, C.byref(o), None, C.byref(out)))
         _trim(ct, nn, ne, rows, e1 - e0)
         return ct
 
@@ -337,11 +340,42 @@ def device_cost_struct(tensors: dict) -> abi.tp_cost_tensors:
 
 def build_cost_tensors(graph, topo: ClusterTopology, records=False, row_min=False,
                        edge_range=(0, -1), device=-1, pinned=False, pair_form: int = 0) -> CostTensors:
-    """The drop-in for build_auxiliary_graph: host graph in, host tensors out."""
+    """The drop-in for build_auxiliary_graph: host graph in, host tensors out
+    (a plan built once: on the thread's reused device memory)."""
     plan = Plan(graph, topo, device)
     if pair_form:
         plan.set_pair_form(pair_form)
-    return plan.execute_host(records=records, row_min=row_min, edge_range=edge_range, pinned=pinned)
+    return plan.execute_host(records=records, row_min=row_min, edge_range=edge_range, pinned=pinned,
+                             scratch=True)
+
+
+def build_cost_tensors_oneshot(graph, topo: ClusterTopology, device=-1) -> CostTensors:
+    """The same build through the one-shot C-ABI call tp_build_cost_tensors
+    (the reference-facing entry point; the thread's device memory is reused
+    across calls). The output sizes come from a host analysis beforehand."""
+    lib = abi.load_engine()
+    flat = graph if isinstance(graph, FlatGraph) else flatten(graph)
+    plan = Plan(flat, topo, device)
+    nn, ne = plan.sizes["num_aux_nodes"], plan.sizes["num_aux_edges"]
+    del plan
+    n_ops, n_e = flat.num_ops, flat.num_edges
+    ix = dict(node_base=np.zeros(n_ops + 1, np.int64), edge_base=np.zeros(n_e + 1, np.int64),
+              edge_from_op=np.zeros(max(n_e, 1), np.int32), edge_to_op=np.zeros(max(n_e, 1), np.int32),
+              in_degree=np.zeros(max(n_ops, 1), np.int32), out_degree=np.zeros(max(n_ops, 1), np.int32),
+              topo_order=np.zeros(max(n_ops, 1), np.int32))
+    ct = CostTensors(**ix, **{k: np.zeros(max(nn if k.startswith("node") else ne, 1), np.float64)
+                              for k in _OUT_KEYS})
+    xi = abi.tp_aux_index(*(abi.ptr(ix[k], C.c_int64 if ix[k].dtype == np.int64 else C.c_int32)
+                            for k, _ in abi.tp_aux_index._fields_))
+    out = cost_struct(ct)
+    gd, td = flat.desc(), topo.desc()
+    o = abi.tp_build_opts(0, -1, 0, device, None)
+    _check(lib, lib.tp_build_cost_tensors(C.byref(gd), C.byref(td), C.byref(o), C.byref(xi), C.byref(out)))
+    for k, m in (("edge_from_op", n_e), ("edge_to_op", n_e), ("in_degree", n_ops), ("out_degree", n_ops),
+                 ("topo_order", n_ops)):
+        setattr(ct, k, ix[k][:m])
+    _trim(ct, nn, ne, 0, 0)
+    return ct
 
 
 def enumerate_strategies(p: int, total_devices: int):

@@ -417,3 +417,27 @@ def test_parallel_host_analysis_matches_oracle():
                        timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert "par ok" in r.stdout
+
+
+def test_one_shot_and_scratch_calls_match_oracle():
+    """tp_build_cost_tensors (the reference-facing one-shot call) and
+    tp_plan_execute_host_scratch reuse the calling thread's device memory
+    across graphs of different sizes: a sequence of different graphs,
+    alternating those two with a plan's own memory, every build bit-identical
+    to the oracle and every error the reference's."""
+    rng = random.Random(7)
+    cases = [M.cfg2(), M.cfg1(), M.cfg3(2, 10)] + [fuzz.random_graph(rng) for _ in range(60)] + [M.cfg2()]
+    ok = err = 0
+    for i, (g, t) in enumerate(cases):
+        f = G.flatten(g)
+        ref = B.oracle_build(f, t)
+        run = (lambda: engine.build_cost_tensors_oneshot(f, t), lambda: engine.Plan(f, t).execute_host(scratch=True),
+               lambda: engine.build_cost_tensors(f, t))[i % 3]
+        if ref.status != 0:
+            with pytest.raises((abi.TopoplanError, IndexError)):
+                run()
+            err += 1
+            continue
+        assert_same(run(), ref)
+        ok += 1
+    assert ok > 15 and err > 10
