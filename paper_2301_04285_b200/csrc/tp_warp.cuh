@@ -77,12 +77,18 @@ __device__ int redist_cost_warp(int R, const SideDesc* pf, const SideDesc* pt, c
   uint32_t P = 0;  // boundaries of tensor dim `dim` (lanes of both sides agree)
   const int partner = rl ? (side ? lane - R : lane + R) : lane;
   const uint32_t win = low_bits(x) & ~1u;
+  // Each round updates the tensor boundaries from the device ones, then the
+  // device boundaries from the NEW tensor ones (the least fixed point is the
+  // same in any order; this one needs about half the rounds), and folds
+  // "some lane's P changed" into bit 31 of the same reduction (D uses bits
+  // 0..16): a shuffle and a reduction per round, no vote.
   for (;;) {
     const uint32_t tb = x >= 2 ? (mirror((D >> a) & win, x) & win) : 0u;
-    const uint32_t db = x >= 2 ? ((mirror(P & win, x) & win) << a) : 0u;
     const uint32_t nP = P | tb | __shfl_sync(FULL, tb, partner);
-    const uint32_t nD = D | __reduce_or_sync(FULL, db);
-    const bool changed = __any_sync(FULL, nP != P) || nD != D;
+    const uint32_t db = x >= 2 ? ((mirror(nP & win, x) & win) << a) : 0u;
+    const uint32_t red = __reduce_or_sync(FULL, db | (nP != P ? 0x80000000u : 0u));
+    const uint32_t nD = D | (red & 0x7fffffffu);
+    const bool changed = (red >> 31) != 0 || nD != D;
     P = nP;
     D = nD;
     ++rounds;

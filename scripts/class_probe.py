@@ -40,3 +40,11 @@ for c in np.unique(pr[:, 2]):
 print("rows end max", ((it[:, 0] + it[:, 1]) / 1e3).max())
 print("fan ranges: n", len(fo), "ready p50/max", np.percentile((fo[:,0]+fo[:,1])/1e3, 50), ((fo[:,0]+fo[:,1])/1e3).max(),
       "end max", ((fo[:,0]+fo[:,2])/1e3).max())
+# the slowest entries: start, duration and where their SM clocks go
+tot = prof[:, 0] + prof[:, 1] + prof[:, 2]
+print("slowest entries (start us, duration us, clocks closure/axes/inference, ops, U, depth, rounds, class):")
+for i in np.argsort(-end)[:12]:
+    print(f"  start {pr[i,0]/1e3:5.1f} dur {pr[i,1]/1e3:5.1f} clocks {prof[i,0]:6d}/{prof[i,1]:6d}/{prof[i,2]:6d}"
+          f" ops {prof[i,3]} U {prof[i,4]} depth {prof[i,5]} rounds {prof[i,6]} class {pr[i,2]}")
+print("duration vs clocks: ns per clock p50", np.percentile(pr[:, 1] / np.maximum(tot, 1), 50))
+print("entries by start time (us) p0/p50/p100:", np.percentile(pr[:, 0] / 1e3, [0, 50, 100]))
