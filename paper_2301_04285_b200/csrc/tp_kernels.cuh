@@ -820,6 +820,50 @@ __device__ void fanout_range(const FusedArgs& a, int item, FanSeg* seg, int* s_n
       pos = span_end;
       continue;
     }
+    if (!kDirect && kPer == 1 && !a.general_store) {
+      // The three SoA tensors (the single build's common case): edge by edge,
+      // the edge's fields in registers, 32-bit (su, sw) coordinates and table
+      // offsets, one division per edge per thread. Same ids per thread as the
+      // general loop below: id o belongs to thread (o - pos) mod kFusedThreads.
+      for (int i = 0; i < n; ++i) {
+        const FanSeg& gs = seg[i];
+        const int64_t lo = max(pos, gs.begin), hi = min(span_end, gs.end);
+        int64_t d = (pos + (int64_t)threadIdx.x - lo) % kFusedThreads;
+        if (d < 0) d += kFusedThreads;
+        int64_t o = lo + d;
+        if (o >= hi) continue;
+        const int32_t Sw = gs.Sw, Wn = gs.Wn, st_q = gs.st_q, st_r = gs.st_r;
+        const bool ident = gs.ident != 0;
+        const double f = gs.f;
+        const int32_t* mu = a.maps + gs.uid_u;
+        const int32_t* mw = a.maps + gs.uid_w;
+        const double2* tab = a.r_tab + gs.pb;
+        const double2* sv = a.cls_sv + gs.wrow;
+        const double* md = a.cls_memdiv + gs.wrow;
+        const int32_t j = (int32_t)(o - gs.begin);
+        int32_t su = j / Sw, sw = j - su * Sw;
+        double* es = a.e_sec - a.A0;
+        double* ev = a.e_vol - a.A0;
+        double* em = a.e_mem - a.A0;
+        for (; o < hi; o += kFusedThreads) {
+          const int32_t t = ident ? su * Sw + sw : mu[su] * Wn + mw[sw];
+          const double2 cv = sv[sw];
+          const double2 rv = kWait ? table_load2(tab + t) : tab[t];
+          const double m = md[sw];
+          __stcs(es + o, cv.x + rv.x * f);  // aux_graph.hpp:290-291
+          __stcs(ev + o, cv.y + rv.y * f);
+          __stcs(em + o, m);  // :292
+          su += st_q;
+          sw += st_r;
+          if (sw >= Sw) {
+            sw -= Sw;
+            ++su;
+          }
+        }
+      }
+      pos = span_end;
+      continue;
+    }
     // (su, sw) of a thread's ids advance by a fixed stride within an edge;
     // a division only where the thread enters an edge
     int si = -1;
