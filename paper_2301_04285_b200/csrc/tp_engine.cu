@@ -924,7 +924,12 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     const size_t args_b = sizeof(FusedArgs) * m, off_b = sizeof(int64_t) * (m + 1);
     const size_t cls_b = sizeof(int64_t) * clsops.size(), jobs_b = sizeof(InferJob) * ijobs.size(),
                  ioff_b = sizeof(int64_t) * ioff.size();
-    const size_t total = args_b + 3 * off_b + cls_b + jobs_b + ioff_b + sizeof(int32_t) * (glist.size() + 1);
+    // form 5's table launch: the plan of every chunk of kUC5 units (its first unit)
+    int64_t units_all = 0;
+    for (int k = 0; k < m; ++k) units_all += X[live[k]].units;
+    const int64_t nchunks5 = bmode == 5 ? (units_all + kUC5 - 1) / kUC5 : 0;
+    const size_t cp_b = sizeof(int32_t) * (size_t)nchunks5;
+    const size_t total = args_b + 3 * off_b + cls_b + jobs_b + ioff_b + sizeof(int32_t) * (glist.size() + 1) + cp_b;
     if (B.copied[slot]) CUDA_TRY(cudaEventSynchronize(B.copied[slot]));
     if (B.h_cap[slot] < total) {
       if (B.h_stage[slot]) cudaFreeHost(B.h_stage[slot]);
@@ -948,6 +953,9 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     const InferJob* djobs = (const InferJob*)(dbase + args_b + 3 * off_b + cls_b);
     const int64_t* dioff = (const int64_t*)(dbase + args_b + 3 * off_b + cls_b + jobs_b);
     const int32_t* dg = (const int32_t*)(dbase + args_b + 3 * off_b + cls_b + jobs_b + ioff_b);
+    const size_t cp_at = args_b + 3 * off_b + cls_b + jobs_b + ioff_b + sizeof(int32_t) * (glist.size() + 1);
+    int32_t* hcp = (int32_t*)((char*)h_stage + cp_at);
+    const int32_t* dcp = nchunks5 > 0 ? (const int32_t*)(dbase + cp_at) : nullptr;
     if (!clsops.empty()) std::memcpy(hcls, clsops.data(), cls_b);
     if (!ijobs.empty()) std::memcpy(hjobs, ijobs.data(), jobs_b);
     std::memcpy(hioff, ioff.data(), ioff_b);
@@ -985,6 +993,8 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
       io[j + 1] = io[j] + x.items;
       to[j + 1] = to[j] + x.a.tables_len;
     }
+    for (int j = 0; j < m && nchunks5 > 0; ++j)  // chunk c starts in plan j iff kUC5 c in [uo[j], uo[j+1])
+      for (int64_t c = (uo[j] + kUC5 - 1) / kUC5; c < (uo[j + 1] + kUC5 - 1) / kUC5; ++c) hcp[c] = j;
     {  // callers map the kernel's per-plan outputs (error slots) in args order
       std::vector<int> l2(m);
       for (int j = 0; j < m; ++j) l2[j] = live[ord[j]];
@@ -1016,17 +1026,17 @@ tp_status execute_batch_impl(tp_plan* const* plans, int32_t n, tp_cost_tensors* 
     const int64_t* dio = duo + (m + 1);
     const int64_t* dto = duo + 2 * (m + 1);
     BatchHdr* hd = (BatchHdr*)B.d_hdr.p;
-    if (form == 1) fused_batch_kernel<1><<<gd, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
-    else if (form == 2) fused_batch_kernel<2><<<gd, bd, kMsecBytes, s>>>(da, m, duo, dio, dto, hd, err_dev);
-    else if (form == 3) fused_batch_kernel<3><<<gd, bd, kMsecBytes, s>>>(da, m, duo, dio, dto, hd, err_dev);
-    else if (form == 4) fused_batch_kernel<4><<<gd, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
+    if (form == 1) fused_batch_kernel<1><<<gd, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev, nullptr);
+    else if (form == 2) fused_batch_kernel<2><<<gd, bd, kMsecBytes, s>>>(da, m, duo, dio, dto, hd, err_dev, nullptr);
+    else if (form == 3) fused_batch_kernel<3><<<gd, bd, kMsecBytes, s>>>(da, m, duo, dio, dto, hd, err_dev, nullptr);
+    else if (form == 4) fused_batch_kernel<4><<<gd, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev, nullptr);
     else if (form == 5) {  // the tables, then the fan-out (ordered by the launch boundary)
       const dim3 g1((unsigned)std::max<int64_t>(1, std::min<int64_t>((uo[m] + 15) / 16, B.resident)));
       const dim3 g2((unsigned)std::max<int64_t>(1, std::min<int64_t>(io[m], B.resident)));
-      fused_batch_kernel<5, 1><<<g1, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
-      fused_batch_kernel<5, 2><<<g2, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev);
+      fused_batch_kernel<5, 1><<<g1, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev, dcp);
+      fused_batch_kernel<5, 2><<<g2, bd, 0, s>>>(da, m, duo, dio, dto, hd, err_dev, nullptr);
     }
-    else fused_batch_kernel<0><<<gd, bd, kMsecBytes, s>>>(da, m, duo, dio, dto, hd, err_dev);
+    else fused_batch_kernel<0><<<gd, bd, kMsecBytes, s>>>(da, m, duo, dio, dto, hd, err_dev, nullptr);
     if (B.prof_stop) CUDA_TRY(cudaEventRecord(B.prof_stop, s));
     B.last_launches = (use_ops && n_infer > 0 ? 1 : 0) + (form == 5 ? 2 : 1);
     if (prof && n >= 32)

@@ -339,6 +339,7 @@ constexpr int kFusedThreads = 256;
 // (pair_thread), one column per thread: dynamic shared memory of fused_batch_kernel
 static_assert(tpk::kBwEntries == tpk::kBwTab, "bandwidth table layout");
 constexpr int kMsecBytes = (int)(tpk::kGroupMax * kFusedThreads * sizeof(double));
+constexpr int kUC5 = 4;  // units per chunk of form 5's table launch
 
 // The terms of one tensor occurrence of a node-class row (aux_graph.hpp:120-167):
 // its shard bytes tm (added to the memory if has_m) and, for a tensor the
@@ -1197,7 +1198,7 @@ template <int kForm, int kPhase = 3>
 __global__ void __launch_bounds__(kFusedThreads, kForm == 3 ? 2 : 4)
     fused_batch_kernel(const FusedArgs* __restrict__ args, int n, const int64_t* __restrict__ unit_off,
                        const int64_t* __restrict__ item_off, const int64_t* __restrict__ tab_off, BatchHdr* hdr,
-                       unsigned long long* __restrict__ err_out) {
+                       unsigned long long* __restrict__ err_out, const int32_t* __restrict__ chunk_plan) {
   __shared__ int s_unit, s_edge, s_nseg, s_last;
   __shared__ union {
     FanSeg f[kSegs];
@@ -1214,7 +1215,7 @@ __global__ void __launch_bounds__(kFusedThreads, kForm == 3 ? 2 : 4)
   // the chunks statically (chunk c, c + warps, ...), no counter at all.
   // (measured on cfg5: static chunks of 2 or 4 units are equal; the
   // counter-claimed chunks of the other forms are far slower here)
-  constexpr int kUC = kForm == 4 ? 8 : (kForm == 5 ? 4 : 1);
+  constexpr int kUC = kForm == 4 ? 8 : (kForm == 5 ? kUC5 : 1);
   const int64_t chunks = (units + kUC - 1) / kUC;
   if (threadIdx.x == 0) s_unit = blockIdx.x * (kFusedThreads / 32);  // static first chunks, as fused_kernel
   __syncthreads();
@@ -1223,8 +1224,15 @@ __global__ void __launch_bounds__(kFusedThreads, kForm == 3 ? 2 : 4)
   if constexpr (kForm == 5 && (kPhase & 1) != 0) {
     for (; c < chunks; c += (int64_t)gridDim.x * (kFusedThreads / 32)) {
       const int64_t u1 = min(units, (c + 1) * kUC);
+      // the plan of the chunk's first unit from the host's table (a warp's
+      // chunks are a grid of warps apart: a search per chunk otherwise)
+      if (chunk_plan) p = chunk_plan[c];
       for (int64_t u = c * kUC; u < u1; ++u) {
-        p = find_plan(unit_off, n, u, p);
+        if (chunk_plan) {
+          while (unit_off[p + 1] <= u) ++p;  // (a chunk may end in a later plan)
+        } else {
+          p = find_plan(unit_off, n, u, p);
+        }
         run_unit<false, false, true>(args[p], u - unit_off[p], args[p].bw_tab);
       }
     }
