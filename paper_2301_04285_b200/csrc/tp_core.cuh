@@ -535,9 +535,11 @@ TP_HD double price_fast(bool a2a, int te, int rexp, int ek, int s, double bytes,
     *vol += v;
     const bool a2a_intra = a2a && gin_e >= ek;
     const int c_e = l - gin_e - rep_e > 0 ? l - gin_e - rep_e : 0;  // c = max(1, 2^(l - gin_e - rep_e) or 0)
-    const int32_t cc = a2a ? (a2a_intra ? 0 : (1 << c_e)) : (ct_e < 0 ? 0 : (1 << ct_e));
-    if (ct_out) *ct_out = cc;
-    const double bw = a2a_intra ? env.intra : ((tab.bw && cc < 65) ? tab.bw[cc] : eff_bw(cc, env));
+    // the bandwidth's ct: 0 (intra) or 2^e, and eff_bw(2^e) = inter / 2^e = inter * 2^-e exactly
+    const bool intra_bw = a2a ? a2a_intra : ct_e < 0;
+    const int e = a2a ? c_e : ct_e;
+    if (ct_out) *ct_out = intra_bw ? 0 : ((int64_t)1 << e);
+    const double bw = intra_bw ? env.intra : env.inter * exp2d(-e);
     double num = v;
     if (a2a && !a2a_intra) {
       const int64_t p = (int64_t)1 << ek, gin = (int64_t)1 << gin_e;
