@@ -73,6 +73,7 @@ __device__ int redist_cost_warp(int R, const SideDesc* pf, const SideDesc* pt, c
   const int a = rl ? me->a[dim] : 0;
   const int tdim = dt[dim].t;
   if (__any_sync(FULL, rl && x > tdim)) return kFactorization;  // :102-111
+  const long long c_loads = prof ? clock64() : 0;
   uint32_t D = (pf->D | pt->D) & ~1u & low_bits(n);
   uint32_t P = 0;  // boundaries of tensor dim `dim` (lanes of both sides agree)
   const int partner = rl ? (side ? lane - R : lane + R) : lane;
@@ -315,7 +316,7 @@ __device__ int redist_cost_warp(int R, const SideDesc* pf, const SideDesc* pt, c
     prof[4] = (unsigned)U;
     prof[5] = (unsigned)next;
     prof[6] = (unsigned)rounds;
-    prof[7] = 0;
+    prof[7] = (unsigned)(c_loads - c_start);  // of prof[0]: the descriptor reads before the closure
   }
   return kOk;
 }

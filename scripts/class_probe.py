@@ -44,7 +44,7 @@ print("fan ranges: n", len(fo), "ready p50/max", np.percentile((fo[:,0]+fo[:,1])
 tot = prof[:, 0] + prof[:, 1] + prof[:, 2]
 print("slowest entries (start us, duration us, clocks closure/axes/inference, ops, U, depth, rounds, class):")
 for i in np.argsort(-end)[:12]:
-    print(f"  start {pr[i,0]/1e3:5.1f} dur {pr[i,1]/1e3:5.1f} clocks {prof[i,0]:6d}/{prof[i,1]:6d}/{prof[i,2]:6d}"
+    print(f"  start {pr[i,0]/1e3:5.1f} dur {pr[i,1]/1e3:5.1f} clocks {prof[i,0]:6d} (descriptor reads {prof[i,7]:5d})/{prof[i,1]:6d}/{prof[i,2]:6d}"
           f" ops {prof[i,3]} U {prof[i,4]} depth {prof[i,5]} rounds {prof[i,6]} class {pr[i,2]}")
 print("duration vs clocks: ns per clock p50", np.percentile(pr[:, 1] / np.maximum(tot, 1), 50))
 print("entries by start time (us) p0/p50/p100:", np.percentile(pr[:, 0] / 1e3, [0, 50, 100]))
