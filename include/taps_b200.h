@@ -229,7 +229,9 @@ tp_status tp_plan_execute_host(tp_plan* plan, const tp_build_opts* opts,
  * own: no device allocation or release when the thread built a graph of the
  * same sizes before, and the plan keeps no device state afterwards (a plan
  * that already has its own device memory uses it). For callers that build
- * once per plan -- the C++ drop-in (include/taps_b200/aux_graph_b200.hpp). */
+ * once per plan -- the C++ drop-in (include/taps_b200/aux_graph_b200.hpp).
+ * The scratch memory stays allocated for the thread, sized by its largest
+ * build so far. */
 tp_status tp_plan_execute_host_scratch(tp_plan* plan, const tp_build_opts* opts,
                                        tp_aux_index* index_out, tp_cost_tensors* host_out);
 /* tp_build_cost_tensors_multi on an analysed plan: per-device copies of the
