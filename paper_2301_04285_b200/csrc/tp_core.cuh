@@ -179,7 +179,8 @@ TP_HD void unrank_strategy(int p, int n, int64_t s, Strat& out) {
 // strategy s (layout.hpp:333-370 restricted to one tensor).
 TP_HD void side_layout(const Strat& s, const int8_t* sa, int R, Lay& L) {
   L.depth = s.depth;
-  for (int k = 0; k < kMaxD; ++k) L.mx[k] = k < s.depth ? s.mx[k] : 0;
+  for (int k = 0; k < kMaxD; ++k) L.mx[k] = 0;
+  for (int k = 0; k < kMaxAxes && k < s.depth; ++k) L.mx[k] = s.mx[k];  // (a strategy has at most kMaxAxes dims)
   for (int d = 0; d < R; ++d) L.map[d] = sa[d] >= 0 ? s.dmap[sa[d]] : (int8_t)-1;
 }
 
