@@ -538,6 +538,7 @@ tp_status prepare_execute(tp_plan* p, const tp_build_opts* opts, tp_cost_tensors
   a.direct = direct;
   // a two-launch batch (mode 5) publishes nothing: its rows run one per thread
   a.rows_thread = batch_mode == 5 && !a.warp_form;
+  a.timeline = p->timeline ? 1 : 0;
   const int64_t row_units = a.rows_thread ? (p->total_rows + 31) / 32 : p->total_rows;
   const int64_t units =
       row_units + (direct ? 0 : (a.warp_form ? a.total_pairs : (a.total_pairs + 31) / 32));
