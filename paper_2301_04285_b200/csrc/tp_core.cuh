@@ -284,7 +284,15 @@ TP_HD int ffs32(uint32_t v) {  // index of the lowest set bit, v != 0
 // bit j (1 <= j < x) of v  ->  bit x - j
 TP_HD uint32_t mirror(uint32_t v, int x) { return brev32(v) >> (31 - x); }
 
-TP_HD uint32_t low_bits(int x) { return x >= 32 ? 0xffffffffu : ((1u << x) - 1u); }
+TP_HD uint32_t low_bits(int x) {  // x in [0, 32]
+#ifdef __CUDA_ARCH__
+  uint32_t m;
+  asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(m) : "r"(x));  // one instruction (len >= 32: all ones)
+  return m;
+#else
+  return x >= 32 ? 0xffffffffu : ((1u << x) - 1u);
+#endif
+}
 
 struct Unified {
   int next;          // unified depth
