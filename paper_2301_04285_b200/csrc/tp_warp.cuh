@@ -116,26 +116,31 @@ __device__ int redist_cost_warp(int R, const SideDesc* pf, const SideDesc* pt, c
   int U = 0, qi = -1, qj = 0;
   uint32_t Pq = 0;
   int my_w = -1, my_to = -1, my_c = 0;
-  for (int i = 0; i < R; ++i) {
-    uint32_t bnd = __shfl_sync(FULL, P, i);
-    const uint32_t Pi = bnd;
-    const int af = pf->a[i], xf = pf->x[i], at = pt->a[i], xt = pt->x[i];
-    int c = 0, j = 0;
-    for (;;) {  // warp-uniform walk over the dim's parts
-      if (U >= 32) return kCapacity;
-      if (lane == U) {
+  {
+    // lane q finds its axis directly: dim i has popc(P_i) + 1 parts, part j
+    // starts at the j-th boundary of P_i (0 for j = 0)
+    for (int i = 0; i < R; ++i) {
+      const uint32_t Pi = __shfl_sync(FULL, P, i);
+      const int np = popc32(Pi) + 1;
+      if (lane >= U && lane < U + np) {
         qi = i;
-        qj = j;
+        qj = lane - U;
         Pq = Pi;
-        my_c = c;
-        if (c < xf) my_w = popc32(D & low_bits(af + xf - c));
-        if (c < xt) my_to = popc32(D & low_bits(at + xt - c));
       }
-      ++U;
-      ++j;
-      if (!bnd) break;
-      c = ffs32(bnd);
-      bnd &= bnd - 1;
+      U += np;
+    }
+    if (U > 32) return kCapacity;
+    if (qi >= 0) {
+      const int af = pf->a[qi], xf = pf->x[qi], at = pt->a[qi], xt = pt->x[qi];
+      int c = 0;
+      if (qj > 0) {
+        uint32_t b = Pq;
+        for (int t = 1; t < qj; ++t) b &= b - 1;
+        c = ffs32(b);
+      }
+      my_c = c;
+      if (c < xf) my_w = popc32(D & low_bits(af + xf - c));
+      if (c < xt) my_to = popc32(D & low_bits(at + xt - c));
     }
   }
   if (tr) {
