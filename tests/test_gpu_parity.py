@@ -441,3 +441,12 @@ def test_one_shot_and_scratch_calls_match_oracle():
         assert_same(run(), ref)
         ok += 1
     assert ok > 15 and err > 10
+    # a plan with device memory of its own keeps using it; scratch calls between its builds
+    f, t = G.flatten(M.cfg2()[0]), M.cfg2()[1]
+    plan = engine.Plan(f, t)
+    ref = B.oracle_build(f, t)
+    assert_same(plan.execute_host(), ref)
+    assert_same(engine.build_cost_tensors_oneshot(*(G.flatten(M.cfg1()[0]), M.cfg1()[1])),
+                B.oracle_build(G.flatten(M.cfg1()[0]), M.cfg1()[1]))
+    assert_same(plan.execute_host(scratch=True), ref)
+    assert_same(plan.execute_host(), ref)
